@@ -1,0 +1,128 @@
+/* amgb200 -- B200-native solve phase of classical-AMG preconditioned CG.
+ *
+ * C ABI of libamgb200.so (the drop-in boundary).  Plain pointers and sizes
+ * only; every entry point returns an int status (AMG_OK = 0) and leaves a
+ * message for amg_last_error().
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/pkg/src/amgkit):
+ *   amg_upload_matrix / amg_set_smoother / amg_upload_coarse / amg_set_cycle
+ *       the data contract AmgHierarchy / Level / Smoother handed over by
+ *       setup():  hierarchy.py:95-152 (Level a/p/pt, factor, factor_kind,
+ *       config.nu1/nu2), smoothers.py:26-43 (kind, inv_diag, gmat, gmat_t,
+ *       omega).
+ *   amg_spmv          sparse.py:203-217      spmv(A, x)
+ *   amg_smoother      smoothers.py:168-173   apply_smoother(sm, A, b, x0, steps)
+ *   amg_coarse_solve  hierarchy.py:149-152   AmgHierarchy.coarse_solve(b)
+ *   amg_vcycle        hierarchy.py:294-312   vcycle(h, y)
+ *   amg_pcg           krylov.py:40-92        pcg(spmv(A0,.), b, vcycle(h,.), x0, config)
+ * Error mapping (errors.py): AMG_E_DIM -> DimensionMismatchError,
+ * AMG_E_NOT_SPD -> NotSpdError, everything else -> AmgError.
+ *
+ * Conventions: host arrays are borrowed for the duration of the call and
+ * copied; the handle owns all device memory; outputs go to caller buffers,
+ * host pointers when on_device == 0, device pointers (e.g. a torch tensor's
+ * data_ptr()) when on_device == 1.  A handle is driven by one host thread.
+ * There is no CPU fallback: without a usable GPU every call fails with
+ * AMG_E_CUDA.
+ *
+ * Multi-GPU: one process per GPU.  Every rank creates its handle with its
+ * (rank, nranks) and the same 128-byte ncclUniqueId, declares the row
+ * partition of every level with amg_set_partition (contiguous row ranges,
+ * identical on all ranks) and uploads only ITS rows of each matrix, with
+ * global column indices.  Halo plans and NCCL exchanges are built by
+ * amg_finalize.  With nranks == 1 no partition call is needed.
+ */
+#ifndef AMGB200_H
+#define AMGB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    AMG_OK = 0,
+    AMG_E_ARG = 1,      /* invalid argument / call order        -> AmgError */
+    AMG_E_DIM = 2,      /* shape mismatch                        -> DimensionMismatchError */
+    AMG_E_NOT_SPD = 3,  /* PCG curvature <= 0                    -> NotSpdError */
+    AMG_E_CUDA = 4,     /* CUDA runtime failure / no GPU         -> AmgError */
+    AMG_E_NCCL = 5,     /* NCCL failure                          -> AmgError */
+    AMG_E_STATE = 6     /* handle not finalized / already final  -> AmgError */
+};
+
+/* matrix slots of a level (Level.a, Level.p, Level.pt, Smoother.gmat, Smoother.gmat_t) */
+enum { AMG_A = 0, AMG_P = 1, AMG_PT = 2, AMG_G = 3, AMG_GT = 4 };
+/* smoother kinds (smoothers.py:45-50) */
+enum { AMG_SMOOTHER_FSAI = 0, AMG_SMOOTHER_JACOBI = 1 };
+/* coarsest factor kinds (hierarchy.py:123-147) */
+enum { AMG_COARSE_CHOLESKY = 0, AMG_COARSE_LU = 1 };
+
+typedef struct amg_handle amg_t;
+
+typedef struct amg_stats {
+    double solve_ms;          /* device time of the last amg_pcg (CUDA events), excl. H2D/D2H */
+    double e2e_ms;            /* host wall time of the last amg_pcg call incl. copies */
+    int64_t launches_per_iter;/* kernels launched per PCG iteration (graph body) */
+    int64_t launches_last;    /* kernels launched by the last amg_pcg call */
+    int64_t bytes_per_iter;   /* algorithmic bytes per PCG iteration (SURVEY 8(d) model) */
+    int64_t flops_per_iter;   /* algorithmic flops per PCG iteration */
+    int graph_mode;           /* 2 = device while-loop graph, 1 = batched graph launches, 0 = eager */
+    int n_levels;
+} amg_stats_t;
+
+/* Handle for one GPU.  nccl_unique_id: 128 bytes (NULL when nranks == 1). */
+int amg_create(int device, int rank, int nranks, const void *nccl_unique_id, amg_t **out);
+void amg_destroy(amg_t *h);
+const char *amg_last_error(void);
+int amg_get_version(void);
+
+int amg_set_levels(amg_t *h, int n_levels);
+/* starts[0..nranks]: rows [starts[r], starts[r+1]) of `level` belong to rank r. */
+int amg_set_partition(amg_t *h, int level, const int64_t *starts);
+/* This rank's rows of matrix `which` of `level`: local_nrows rows, CSR with
+ * offsets[0..local_nrows] (offsets[0] == 0), GLOBAL column indices (sorted,
+ * unique per row) and values; global_ncols = number of columns. */
+int amg_upload_matrix(amg_t *h, int level, int which, int64_t local_nrows, int64_t global_ncols,
+                      const int64_t *offsets, const int32_t *cols, const double *vals);
+/* inv_diag: this rank's rows (Jacobi) or NULL (FSAI). */
+int amg_set_smoother(amg_t *h, int level, int kind, double omega, const double *inv_diag, int64_t n);
+/* Dense coarsest factor, n x n row-major: lower Cholesky factor (upper part
+ * ignored) or LAPACK getrf LU with 0-based pivots `piv` (kind LU). Replicated on every rank. */
+int amg_upload_coarse(amg_t *h, int n, const double *factor, int kind, const int32_t *piv);
+int amg_set_cycle(amg_t *h, int nu1, int nu2);
+int amg_finalize(amg_t *h);
+
+/* Rows owned by this rank at `level` (vectors passed to the calls below are
+ * this rank's slice). */
+int64_t amg_local_rows(amg_t *h, int level);
+
+/* y = M x for M = matrix `which` of `level`; x has the matrix's column space
+ * (this rank's slice), y its row space. */
+int amg_spmv(amg_t *h, int level, int which, const double *x, double *y, int on_device);
+/* x = apply_smoother(level, b, x0, steps); x0 may be NULL (zeros). */
+int amg_smoother(amg_t *h, int level, const double *b, const double *x0, double *x, int steps,
+                 int on_device);
+/* z = coarse_solve(y) on the coarsest level (replicated). */
+int amg_coarse_solve(amg_t *h, const double *y, double *z, int on_device);
+/* z = vcycle(h, y) from level 0. */
+int amg_vcycle(amg_t *h, const double *y, double *z, int on_device);
+
+/* PCG with the V-cycle preconditioner (krylov.py:40-92).  x0 may be NULL.
+ * history: max_iters+1 doubles or NULL; *hist_len = entries written.
+ * On AMG_E_NOT_SPD, *n_iter holds the failing iteration and
+ * *curvature_at_fail the curvature. */
+int amg_pcg(amg_t *h, const double *b, const double *x0, double rtol, int max_iters,
+            int recompute_every, double *x_out, int *n_iter, double *relres, int *converged,
+            double *history, int *hist_len, double *curvature_at_fail, int on_device);
+
+int amg_get_stats(amg_t *h, amg_stats_t *out);
+/* Tuning / diagnostics: 0 = auto. */
+int amg_set_option(amg_t *h, const char *key, int64_t value);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AMGB200_H */

@@ -1,0 +1,992 @@
+// libamgb200: host runtime + C ABI of the B200-native PCG + AMG solve phase.
+//
+// Owns the device copy of the hierarchy (uploaded once from the reference's
+// setup output), the tile schedules of every matrix, the work vectors of
+// every level, the device-resident PCG state and the CUDA graph of one PCG
+// iteration, which runs as a device-side while loop (conditional graph node)
+// so a whole solve is a single graph launch with no host round trip.
+//
+// Reference behaviour each piece follows is cited at the entry points in
+// include/amgb200.h; the per-level V-cycle sequence is hierarchy.py:294-312
+// with smoothers.py:168-173 expanded as in SURVEY.md 8(a).
+#include "amgb200.h"
+#include "kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "halo.h"
+
+using namespace amg;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg)
+{
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                                      \
+    do {                                                                                              \
+        cudaError_t e_ = (call);                                                                      \
+        if (e_ != cudaSuccess)                                                                        \
+            return fail(AMG_E_CUDA, std::string(#call) + " failed: " + cudaGetErrorString(e_));      \
+    } while (0)
+
+#define TRY(expr)                \
+    do {                         \
+        int s_ = (expr);         \
+        if (s_ != AMG_OK) return s_; \
+    } while (0)
+
+namespace {
+
+struct DevMat {
+    bool present = false;
+    int64_t nrows = 0, ncols = 0, nnz = 0;  // local rows; extended column space
+    int64_t gncols = 0;                      // global columns
+    int32_t *off = nullptr, *col = nullptr;
+    double *val = nullptr;
+    TileDesc *tiles = nullptr;
+    int ntiles = 0;
+    int lanes = 1;
+    int grid = 0;
+    HaloPlan halo;  // exchange feeding this matrix's halo columns (nranks > 1)
+};
+
+struct LevelD {
+    int64_t n = 0;   // local rows
+    int64_t n0 = 0;  // first global row
+    int64_t gn = 0;  // global rows
+    int64_t cap = 0; // vector capacity: local + max halo
+    std::vector<int64_t> starts;  // partition (nranks + 1)
+    DevMat m[5];
+    bool has_smoother = false;
+    int sm_kind = AMG_SMOOTHER_FSAI;
+    double omega = 1.0;
+    double *inv_diag = nullptr;
+    double *y = nullptr, *x = nullptr, *r = nullptr, *t = nullptr;
+};
+
+template <class T>
+int dalloc(T **p, size_t count)
+{
+    size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    cudaError_t e = cudaMalloc((void **)p, bytes);
+    if (e != cudaSuccess) return fail(AMG_E_CUDA, std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    e = cudaMemset(*p, 0, bytes);
+    if (e != cudaSuccess) return fail(AMG_E_CUDA, cudaGetErrorString(e));
+    return AMG_OK;
+}
+
+}  // namespace
+
+struct amg_handle {
+    int device = 0, rank = 0, nranks = 1;
+    cudaStream_t stream = nullptr;
+    int sm_count = 148;
+    std::vector<LevelD> lv;
+    int nu1 = 1, nu2 = 1;
+    // coarsest factor
+    int nc = 0, coarse_kind = AMG_COARSE_CHOLESKY;
+    double *Lp = nullptr, *LU = nullptr;
+    int32_t *piv = nullptr;
+    int coarse_staged = 0;
+    size_t coarse_smem = 0;
+    bool finalized = false;
+    bool container = false;
+    // scratch
+    double *partials = nullptr;
+    unsigned *ticket = nullptr;
+    int max_grid = 0;
+    PcgCtl *ctl = nullptr;
+    PcgCtl *ctl_h = nullptr;  // pinned mirror
+    double *b = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
+    double *tmp_in = nullptr, *tmp_out = nullptr;
+    double *hist = nullptr;
+    int hist_cap = 0;
+    // options
+    int tile_nnz = 2048, tile_rows = 256, stages = 3, ctas_per_sm = 0, force_graph = -1, batch = 8;
+    int lanes_override = 0;
+    // graph
+    cudaGraphExec_t gexec = nullptr;
+    int graph_mode = 0;
+    int64_t launches = 0;  // running launch counter
+    int64_t launches_per_iter = 0;
+    int64_t launches_last = 0;
+    double solve_ms = 0.0, e2e_ms = 0.0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    Comm comm;
+};
+
+// ------------------------------------------------------------------ kernels dispatch
+
+typedef void (*SpmvFn)(const SpmvArgs);
+
+static SpmvFn spmv_fn(int epi, int lanes)
+{
+#define AMG_L(E)                                               \
+    switch (lanes) {                                           \
+    case 1: return spmv_tiles<E, 1>;                           \
+    case 2: return spmv_tiles<E, 2>;                           \
+    case 4: return spmv_tiles<E, 4>;                           \
+    default: return spmv_tiles<E, 8>;                          \
+    }
+    switch (epi) {
+    case EPI_PLAIN: AMG_L(EPI_PLAIN)
+    case EPI_RESID: AMG_L(EPI_RESID)
+    case EPI_AXPYW: AMG_L(EPI_AXPYW)
+    case EPI_SETW: AMG_L(EPI_SETW)
+    default: AMG_L(EPI_ADD)
+    }
+#undef AMG_L
+}
+
+static int stage_smem(const amg_t *h) { return h->stages * stage_layout(h->tile_nnz, h->tile_rows).stage_bytes; }
+
+static int configure_kernels(amg_t *h, int *blocks_per_sm)
+{
+    const int smem = stage_smem(h);
+    int best = 1 << 30;
+    for (int e = 0; e <= 4; ++e)
+        for (int l : {1, 2, 4, 8}) {
+            SpmvFn f = spmv_fn(e, l);
+            CK(cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            int nb = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, TILE_THREADS, smem));
+            best = std::min(best, nb);
+        }
+    if (best < 1) return fail(AMG_E_CUDA, "SpMV tile kernel does not fit on an SM with the chosen staging");
+    *blocks_per_sm = best;
+    return AMG_OK;
+}
+
+// halo exchange (nranks > 1): fills x[n_local ...] for matrix M from peers
+static int exchange(amg_t *h, const DevMat &M, double *x)
+{
+    if (h->nranks == 1 || M.halo.empty()) return AMG_OK;
+    int s = halo_exchange(h->comm, M.halo, x, h->stream);
+    if (s != 0) return fail(AMG_E_NCCL, halo_error());
+    return AMG_OK;
+}
+
+static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, int epi, const double *b, double omega,
+                       const double *dotw, int fin, const int *g1, const int *g2)
+{
+    TRY(exchange(h, M, const_cast<double *>(x)));
+    if (M.ntiles == 0) {
+        if (fin != FIN_NONE) {
+            VecArgs v{};
+            v.n = 0;
+            v.partials = h->partials;
+            v.ticket = h->ticket;
+            v.fin = fin;
+            v.ctl = h->ctl;
+            v.gate1 = g1;
+            v.gate2 = g2;
+            vec_dot<<<1, VEC_THREADS, 0, h->stream>>>(v);
+            ++h->launches;
+        }
+        return AMG_OK;
+    }
+    SpmvArgs a{};
+    a.off = M.off;
+    a.col = M.col;
+    a.val = M.val;
+    a.tiles = M.tiles;
+    a.ntiles = M.ntiles;
+    a.tile_nnz = h->tile_nnz;
+    a.tile_rows = h->tile_rows;
+    a.stages = h->stages;
+    a.x = x;
+    a.y = y;
+    a.b = b;
+    a.omega = omega;
+    a.dotw = dotw;
+    a.partials = h->partials;
+    a.ticket = h->ticket;
+    a.fin = fin;
+    a.ctl = h->ctl;
+    a.gate1 = g1;
+    a.gate2 = g2;
+    spmv_fn(epi, M.lanes)<<<M.grid, TILE_THREADS, stage_smem(h), h->stream>>>(a);
+    ++h->launches;
+    CK(cudaGetLastError());
+    return AMG_OK;
+}
+
+static int vec_grid(const amg_t *h, int64_t n)
+{
+    int64_t g = (n + VEC_THREADS * 4 - 1) / (VEC_THREADS * 4);
+    g = std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)h->sm_count * 8));
+    return (int)g;
+}
+
+static VecArgs vargs(amg_t *h, int64_t n, const int *g1, const int *g2)
+{
+    VecArgs v{};
+    v.n = n;
+    v.partials = h->partials;
+    v.ticket = h->ticket;
+    v.ctl = h->ctl;
+    v.gate1 = g1;
+    v.gate2 = g2;
+    v.fin = FIN_NONE;
+    return v;
+}
+
+static int launch_copy(amg_t *h, double *dst, const double *src, int64_t n, const int *g1)
+{
+    VecArgs v = vargs(h, n, g1, nullptr);
+    v.x = dst;
+    v.p = src;
+    vec_copy<<<vec_grid(h, n), VEC_THREADS, 0, h->stream>>>(v);
+    ++h->launches;
+    CK(cudaGetLastError());
+    return AMG_OK;
+}
+
+static int launch_dot(amg_t *h, const double *a, const double *b, int64_t n, int fin, const int *g1, const int *g2)
+{
+    VecArgs v = vargs(h, n, g1, g2);
+    v.p = a;
+    v.q = b;
+    v.fin = fin;
+    vec_dot<<<vec_grid(h, n), VEC_THREADS, 0, h->stream>>>(v);
+    ++h->launches;
+    CK(cudaGetLastError());
+    return AMG_OK;
+}
+
+static int launch_coarse(amg_t *h, const double *y, double *z, const int *g1, int fin, const double *dotw)
+{
+    const int n = h->nc;
+    if (h->coarse_kind == AMG_COARSE_CHOLESKY) {
+        coarse_chol<<<1, COARSE_THREADS, h->coarse_smem, h->stream>>>(n, h->Lp, y, z, h->coarse_staged, g1,
+                                                                       h->partials, h->ticket, fin, h->ctl, dotw);
+    } else {
+        coarse_lu<<<1, COARSE_THREADS, h->coarse_smem, h->stream>>>(n, h->LU, h->piv, y, z, g1, h->partials,
+                                                                     h->ticket, fin, h->ctl, dotw);
+    }
+    ++h->launches;
+    CK(cudaGetLastError());
+    return AMG_OK;
+}
+
+// x = apply_smoother(level k, b, x, steps) with x == 0 on entry when `from_zero`.
+// The LAST operation carries (fin, dotw) when `tail` is set.
+static int enqueue_smooth(amg_t *h, int k, const double *b, double *x, int steps, bool from_zero, const int *g1,
+                          int fin, const double *dotw)
+{
+    LevelD &L = h->lv[k];
+    for (int s = 0; s < steps; ++s) {
+        const bool last = (s == steps - 1);
+        const int f = last ? fin : FIN_NONE;
+        const double *dw = last ? dotw : nullptr;
+        const double *src = b;  // b - A*0 == b exactly (smoothers.py:172 with x0 = 0)
+        if (!(from_zero && s == 0)) {
+            TRY(launch_spmv(h, L.m[AMG_A], x, L.r, EPI_RESID, b, 0.0, nullptr, FIN_NONE, g1, nullptr));
+            src = L.r;
+        }
+        const bool set = from_zero && s == 0;
+        if (L.sm_kind == AMG_SMOOTHER_FSAI) {
+            TRY(launch_spmv(h, L.m[AMG_G], src, L.t, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, g1, nullptr));
+            TRY(launch_spmv(h, L.m[AMG_GT], L.t, x, set ? EPI_SETW : EPI_AXPYW, x, L.omega, dw, f, g1, nullptr));
+        } else {
+            VecArgs v = vargs(h, L.n, g1, nullptr);
+            v.x = x;
+            v.p = src;
+            v.d = L.inv_diag;
+            v.omega = L.omega;
+            v.mode = set ? 0 : 1;
+            v.q = dw;
+            v.fin = dw ? f : FIN_NONE;
+            jacobi_sweep<<<vec_grid(h, L.n), VEC_THREADS, 0, h->stream>>>(v);
+            ++h->launches;
+            CK(cudaGetLastError());
+        }
+    }
+    return AMG_OK;
+}
+
+// x = vcycle(h, y, level k) (hierarchy.py:294-312).  (fin, dotw) ride on the
+// last operation of level 0 (e.g. r.z for PCG).
+static int enqueue_vcycle(amg_t *h, int k, const double *y, double *x, const int *g1, int fin, const double *dotw)
+{
+    const int nl = (int)h->lv.size();
+    if (k == nl - 1) return launch_coarse(h, y, x, g1, fin, dotw);
+    LevelD &L = h->lv[k];
+    LevelD &C = h->lv[k + 1];
+    const double *r = y;
+    if (h->nu1 > 0) {
+        TRY(enqueue_smooth(h, k, y, x, h->nu1, true, g1, FIN_NONE, nullptr));
+        TRY(launch_spmv(h, L.m[AMG_A], x, L.r, EPI_RESID, y, 0.0, nullptr, FIN_NONE, g1, nullptr));
+        r = L.r;
+    }
+    TRY(launch_spmv(h, L.m[AMG_PT], r, C.y, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, g1, nullptr));
+    TRY(enqueue_vcycle(h, k + 1, C.y, C.x, g1, FIN_NONE, nullptr));
+    const bool tail_on_p = (h->nu2 == 0);
+    TRY(launch_spmv(h, L.m[AMG_P], C.x, x, h->nu1 > 0 ? EPI_ADD : EPI_PLAIN, x, 0.0, tail_on_p ? dotw : nullptr,
+                    tail_on_p ? fin : FIN_NONE, g1, nullptr));
+    if (h->nu2 > 0) TRY(enqueue_smooth(h, k, y, x, h->nu2, false, g1, fin, dotw));
+    return AMG_OK;
+}
+
+// One PCG iteration (krylov.py:66-91), every kernel gated on ctl->active.
+static int enqueue_pcg_body(amg_t *h, cudaGraphConditionalHandle handle, int use_handle)
+{
+    LevelD &L0 = h->lv[0];
+    const DevMat &A = L0.m[AMG_A];
+    const int *act = &h->ctl->active;
+    const int64_t n = L0.n;
+    // q = A p ; curv = p.q ; alpha = rz / curv          (:66-73)
+    TRY(launch_spmv(h, A, h->p, h->q, EPI_PLAIN, nullptr, 0.0, h->p, FIN_CURV, act, nullptr));
+    // x += alpha p ; r -= alpha q ; ||r||               (:74-75, 78)
+    {
+        VecArgs v = vargs(h, n, act, nullptr);
+        v.x = h->x;
+        v.r = h->r;
+        v.p = h->p;
+        v.q = h->q;
+        v.fin = FIN_UPDATE;
+        pcg_update<<<vec_grid(h, n), VEC_THREADS, 0, h->stream>>>(v);
+        ++h->launches;
+        CK(cudaGetLastError());
+    }
+    // every recompute_every iterations: r = b - A x     (:76-77)
+    TRY(launch_spmv(h, A, h->x, h->r, EPI_RESID, h->b, 0.0, h->r, FIN_RECOMPUTE, act, &h->ctl->do_recompute));
+    // relres <= rtol: true residual check              (:81-86)
+    TRY(launch_spmv(h, A, h->x, h->r, EPI_RESID, h->b, 0.0, h->r, FIN_TRUE, act, &h->ctl->need_true));
+    // z = M r ; rz_new = r.z ; beta                     (:87-90)
+    TRY(enqueue_vcycle(h, 0, h->r, h->z, act, FIN_RZ, h->r));
+    if (h->lv.size() == 1) {
+        // the coarse kernel carried the dot already
+    }
+    // p = z + beta p                                    (:91)
+    {
+        VecArgs v = vargs(h, n, act, nullptr);
+        v.x = h->p;
+        v.p = h->z;
+        pcg_xpay<<<vec_grid(h, n), VEC_THREADS, 0, h->stream>>>(v);
+        ++h->launches;
+        CK(cudaGetLastError());
+    }
+    pcg_continue<<<1, 1, 0, h->stream>>>(h->ctl, handle, use_handle);
+    ++h->launches;
+    CK(cudaGetLastError());
+    return AMG_OK;
+}
+
+static int build_graph(amg_t *h)
+{
+    if (h->gexec) return AMG_OK;
+    const int64_t before = h->launches;
+    int mode = (h->force_graph >= 0) ? h->force_graph : 2;
+    if (mode == 2) {
+        cudaGraph_t g = nullptr;
+        cudaGraphConditionalHandle handle;
+        bool ok = cudaGraphCreate(&g, 0) == cudaSuccess &&
+                  cudaGraphConditionalHandleCreate(&handle, g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+        cudaGraphNode_t node;
+        cudaGraphNodeParams params = {cudaGraphNodeTypeConditional};
+        if (ok) {
+            params.conditional.handle = handle;
+            params.conditional.type = cudaGraphCondTypeWhile;
+            params.conditional.size = 1;
+            ok = cudaGraphAddNode(&node, g, nullptr, 0, &params) == cudaSuccess;
+        }
+        if (ok) {
+            cudaGraph_t body = params.conditional.phGraph_out[0];
+            ok = cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            if (ok) {
+                int s = enqueue_pcg_body(h, handle, 1);
+                cudaGraph_t out = nullptr;
+                cudaError_t e = cudaStreamEndCapture(h->stream, &out);
+                ok = (s == AMG_OK) && e == cudaSuccess;
+            }
+        }
+        if (ok) ok = cudaGraphInstantiate(&h->gexec, g, 0) == cudaSuccess;
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        if (ok) {
+            h->graph_mode = 2;
+            h->launches_per_iter = h->launches - before;
+            h->launches = before;
+            return AMG_OK;
+        }
+        if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+        h->launches = before;
+        mode = 1;
+    }
+    if (mode == 1) {
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        cudaGraphConditionalHandle dummy{};
+        int s = enqueue_pcg_body(h, dummy, 0);
+        cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+        if (s != AMG_OK) return s;
+        if (e != cudaSuccess) return fail(AMG_E_CUDA, std::string("graph capture failed: ") + cudaGetErrorString(e));
+        e = cudaGraphInstantiate(&h->gexec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(AMG_E_CUDA, std::string("graph instantiate failed: ") + cudaGetErrorString(e));
+        h->graph_mode = 1;
+        h->launches_per_iter = h->launches - before;
+        h->launches = before;
+        return AMG_OK;
+    }
+    h->graph_mode = 0;
+    return AMG_OK;
+}
+
+// ------------------------------------------------------------------ C ABI
+
+extern "C" {
+
+int amg_get_version(void) { return 1; }
+
+const char *amg_last_error(void) { return g_err.c_str(); }
+
+int amg_create(int device, int rank, int nranks, const void *nccl_unique_id, amg_t **out)
+{
+    if (!out) return fail(AMG_E_ARG, "amg_create: out is NULL");
+    *out = nullptr;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(AMG_E_ARG, "amg_create: bad rank / nranks");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(AMG_E_CUDA, std::string("amg_create: no CUDA device available (") + cudaGetErrorString(e) +
+                                    "); amgb200 has no CPU fallback");
+    if (device < 0 || device >= ndev) return fail(AMG_E_ARG, "amg_create: device ordinal out of range");
+    CK(cudaSetDevice(device));
+    amg_t *h = new amg_t();
+    h->device = device;
+    h->rank = rank;
+    h->nranks = nranks;
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    h->sm_count = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&h->ev0));
+    CK(cudaEventCreate(&h->ev1));
+    if (nranks > 1) {
+        if (!nccl_unique_id) { delete h; return fail(AMG_E_ARG, "amg_create: nranks > 1 needs an ncclUniqueId"); }
+        if (comm_init(h->comm, nccl_unique_id, rank, nranks) != 0) {
+            std::string m = halo_error();
+            delete h;
+            return fail(AMG_E_NCCL, "amg_create: " + m);
+        }
+    }
+    *out = h;
+    return AMG_OK;
+}
+
+void amg_destroy(amg_t *h)
+{
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    auto F = [](void *p) { if (p) cudaFree(p); };
+    for (auto &L : h->lv) {
+        for (auto &M : L.m) {
+            F(M.off); F(M.col); F(M.val); F(M.tiles);
+            halo_free(M.halo);
+        }
+        F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
+    }
+    F(h->Lp); F(h->LU); F(h->piv); F(h->partials); F(h->ticket); F(h->ctl);
+    F(h->b); F(h->x); F(h->r); F(h->z); F(h->p); F(h->q); F(h->tmp_in); F(h->tmp_out); F(h->hist);
+    if (h->ctl_h) cudaFreeHost(h->ctl_h);
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    comm_destroy(h->comm);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+int amg_set_option(amg_t *h, const char *key, int64_t value)
+{
+    if (!h || !key) return fail(AMG_E_ARG, "amg_set_option: NULL argument");
+    std::string k(key);
+    if (k == "graph") { h->force_graph = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
+    if (k == "batch") { h->batch = std::max<int>(1, (int)value); return AMG_OK; }
+    if (h->finalized) return fail(AMG_E_STATE, "amg_set_option: '" + k + "' must be set before amg_finalize");
+    if (k == "tile_nnz") { if (value < 64 || value > 8192) return fail(AMG_E_ARG, "tile_nnz out of range"); h->tile_nnz = (int)value; return AMG_OK; }
+    if (k == "tile_rows") { if (value < 32 || value > 1024) return fail(AMG_E_ARG, "tile_rows out of range"); h->tile_rows = (int)value; return AMG_OK; }
+    if (k == "stages") { if (value < 1 || value > 8) return fail(AMG_E_ARG, "stages out of range"); h->stages = (int)value; return AMG_OK; }
+    if (k == "ctas_per_sm") { h->ctas_per_sm = (int)value; return AMG_OK; }
+    if (k == "lanes") { if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8) return fail(AMG_E_ARG, "lanes must be 0,1,2,4,8"); h->lanes_override = (int)value; return AMG_OK; }
+    return fail(AMG_E_ARG, "amg_set_option: unknown key '" + k + "'");
+}
+
+int amg_set_levels(amg_t *h, int n_levels)
+{
+    if (!h) return fail(AMG_E_ARG, "NULL handle");
+    if (h->finalized) return fail(AMG_E_STATE, "amg_set_levels: already finalized");
+    if (n_levels < 1 || n_levels > 64) return fail(AMG_E_ARG, "amg_set_levels: n_levels out of range");
+    h->lv.assign(n_levels, LevelD());
+    return AMG_OK;
+}
+
+int amg_set_partition(amg_t *h, int level, const int64_t *starts)
+{
+    if (!h || !starts) return fail(AMG_E_ARG, "amg_set_partition: NULL argument");
+    if (level < 0 || level >= (int)h->lv.size()) return fail(AMG_E_ARG, "amg_set_partition: bad level");
+    std::vector<int64_t> s(starts, starts + h->nranks + 1);
+    if (s[0] != 0) return fail(AMG_E_ARG, "amg_set_partition: starts[0] must be 0");
+    for (int i = 0; i < h->nranks; ++i)
+        if (s[i + 1] < s[i]) return fail(AMG_E_ARG, "amg_set_partition: starts must be non-decreasing");
+    h->lv[level].starts = s;
+    return AMG_OK;
+}
+
+int64_t amg_local_rows(amg_t *h, int level)
+{
+    if (!h || level < 0 || level >= (int)h->lv.size()) return -1;
+    return h->lv[level].n;
+}
+
+static void build_tiles(const std::vector<int32_t> &off, int64_t nrows, int tile_nnz, int tile_rows,
+                        std::vector<TileDesc> &tiles)
+{
+    tiles.clear();
+    int64_t r = 0;
+    while (r < nrows) {
+        const int64_t r0 = r;
+        const int32_t k0 = off[r];
+        if (off[r + 1] - off[r] > tile_nnz) {
+            tiles.push_back({(int32_t)r, (int32_t)(r + 1), off[r], off[r + 1]});
+            ++r;
+            continue;
+        }
+        while (r < nrows && r - r0 < tile_rows && off[r + 1] - k0 <= tile_nnz) ++r;
+        tiles.push_back({(int32_t)r0, (int32_t)r, k0, off[r]});
+    }
+}
+
+int amg_upload_matrix(amg_t *h, int level, int which, int64_t local_nrows, int64_t global_ncols,
+                      const int64_t *offsets, const int32_t *cols, const double *vals)
+{
+    if (!h) return fail(AMG_E_ARG, "NULL handle");
+    if (h->finalized) return fail(AMG_E_STATE, "amg_upload_matrix: already finalized");
+    if (level < 0 || level >= (int)h->lv.size()) return fail(AMG_E_ARG, "amg_upload_matrix: bad level (call amg_set_levels first)");
+    if (which < 0 || which > 4) return fail(AMG_E_ARG, "amg_upload_matrix: bad matrix slot");
+    if (local_nrows < 0 || global_ncols < 0 || (!offsets && local_nrows >= 0))
+        return fail(AMG_E_ARG, "amg_upload_matrix: bad sizes / NULL offsets");
+    if (offsets[0] != 0) return fail(AMG_E_ARG, "amg_upload_matrix: offsets[0] must be 0");
+    const int64_t nnz = offsets[local_nrows];
+    if (nnz < 0 || nnz >= INT32_MAX - 64) return fail(AMG_E_ARG, "amg_upload_matrix: local nnz must fit int32 (partition across more GPUs)");
+    if (nnz > 0 && (!cols || !vals)) return fail(AMG_E_ARG, "amg_upload_matrix: NULL cols / vals");
+    if (global_ncols >= INT32_MAX) return fail(AMG_E_ARG, "amg_upload_matrix: too many columns for int32 indices");
+    CK(cudaSetDevice(h->device));
+    DevMat &M = h->lv[level].m[which];
+    if (M.present) return fail(AMG_E_STATE, "amg_upload_matrix: slot already uploaded");
+    std::vector<int32_t> off32(local_nrows + 1 + 8, (int32_t)nnz);
+    for (int64_t i = 0; i <= local_nrows; ++i) {
+        if (i > 0 && offsets[i] < offsets[i - 1]) return fail(AMG_E_ARG, "amg_upload_matrix: offsets must be non-decreasing");
+        off32[i] = (int32_t)offsets[i];
+    }
+    for (int64_t k = 0; k < nnz; ++k)
+        if (cols[k] < 0 || cols[k] >= global_ncols) return fail(AMG_E_ARG, "amg_upload_matrix: column index out of range");
+    M.nrows = local_nrows;
+    M.gncols = global_ncols;
+    M.ncols = global_ncols;
+    M.nnz = nnz;
+    // Local column numbering: on one rank global == local.  With nranks > 1
+    // the halo plan (built at finalize) renumbers non-owned columns.
+    std::vector<int32_t> col_local(cols, cols + nnz);
+    TRY(dalloc(&M.off, off32.size()));
+    TRY(dalloc(&M.col, (size_t)nnz + 8));
+    TRY(dalloc(&M.val, (size_t)nnz + 4));
+    CK(cudaMemcpy(M.off, off32.data(), off32.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    if (nnz) {
+        CK(cudaMemcpy(M.col, col_local.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(M.val, vals, nnz * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    M.present = true;
+    return AMG_OK;
+}
+
+int amg_set_smoother(amg_t *h, int level, int kind, double omega, const double *inv_diag, int64_t n)
+{
+    if (!h) return fail(AMG_E_ARG, "NULL handle");
+    if (h->finalized) return fail(AMG_E_STATE, "amg_set_smoother: already finalized");
+    if (level < 0 || level >= (int)h->lv.size()) return fail(AMG_E_ARG, "amg_set_smoother: bad level");
+    LevelD &L = h->lv[level];
+    if (kind != AMG_SMOOTHER_FSAI && kind != AMG_SMOOTHER_JACOBI) return fail(AMG_E_ARG, "amg_set_smoother: bad kind");
+    L.has_smoother = true;
+    L.sm_kind = kind;
+    L.omega = omega;
+    if (kind == AMG_SMOOTHER_JACOBI) {
+        if (!inv_diag || n < 0) return fail(AMG_E_ARG, "amg_set_smoother: Jacobi needs inv_diag");
+        CK(cudaSetDevice(h->device));
+        if (L.inv_diag) cudaFree(L.inv_diag);
+        TRY(dalloc(&L.inv_diag, (size_t)n + 2));
+        CK(cudaMemcpy(L.inv_diag, inv_diag, n * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    return AMG_OK;
+}
+
+int amg_upload_coarse(amg_t *h, int n, const double *factor, int kind, const int32_t *piv)
+{
+    if (!h || !factor) return fail(AMG_E_ARG, "amg_upload_coarse: NULL argument");
+    if (h->finalized) return fail(AMG_E_STATE, "amg_upload_coarse: already finalized");
+    if (n < 1) return fail(AMG_E_ARG, "amg_upload_coarse: n < 1");
+    CK(cudaSetDevice(h->device));
+    h->nc = n;
+    h->coarse_kind = kind;
+    if (kind == AMG_COARSE_CHOLESKY) {
+        std::vector<double> packed((size_t)n * (n + 1) / 2);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j <= i; ++j) packed[(size_t)i * (i + 1) / 2 + j] = factor[(size_t)i * n + j];
+        TRY(dalloc(&h->Lp, packed.size()));
+        CK(cudaMemcpy(h->Lp, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice));
+        const size_t vbytes = (size_t)((n + 1) & ~1) * sizeof(double);
+        const size_t lbytes = packed.size() * sizeof(double);
+        if (vbytes + lbytes <= 200 * 1024) {
+            h->coarse_staged = 1;
+            h->coarse_smem = vbytes + lbytes;
+        } else {
+            h->coarse_staged = 0;
+            h->coarse_smem = vbytes;
+        }
+    } else if (kind == AMG_COARSE_LU) {
+        if (!piv) return fail(AMG_E_ARG, "amg_upload_coarse: LU needs pivots");
+        for (int i = 0; i < n; ++i)
+            if (piv[i] < 0 || piv[i] >= n) return fail(AMG_E_ARG, "amg_upload_coarse: pivot out of range");
+        TRY(dalloc(&h->LU, (size_t)n * n));
+        TRY(dalloc(&h->piv, (size_t)n));
+        CK(cudaMemcpy(h->LU, factor, (size_t)n * n * sizeof(double), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->piv, piv, (size_t)n * sizeof(int32_t), cudaMemcpyHostToDevice));
+        h->coarse_staged = 0;
+        h->coarse_smem = (size_t)((n + 1) & ~1) * sizeof(double);
+    } else {
+        return fail(AMG_E_ARG, "amg_upload_coarse: bad kind");
+    }
+    if (h->coarse_smem > 48 * 1024) {
+        CK(cudaFuncSetAttribute((const void *)coarse_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->coarse_smem));
+        CK(cudaFuncSetAttribute((const void *)coarse_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->coarse_smem));
+    }
+    return AMG_OK;
+}
+
+int amg_set_cycle(amg_t *h, int nu1, int nu2)
+{
+    if (!h) return fail(AMG_E_ARG, "NULL handle");
+    if (nu1 < 0 || nu2 < 0) return fail(AMG_E_ARG, "smoothing step counts must be nonnegative");
+    h->nu1 = nu1;
+    h->nu2 = nu2;
+    if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+    return AMG_OK;
+}
+
+int amg_finalize(amg_t *h)
+{
+    if (!h) return fail(AMG_E_ARG, "NULL handle");
+    if (h->finalized) return fail(AMG_E_STATE, "amg_finalize: already finalized");
+    const int nl = (int)h->lv.size();
+    if (nl < 1) return fail(AMG_E_STATE, "amg_finalize: no levels");
+    CK(cudaSetDevice(h->device));
+    // A handle without a coarsest factor is a plain matrix container (spmv only).
+    const bool container = (h->nc == 0);
+    // structural checks mirroring the Level / AmgHierarchy contract
+    for (int k = 0; k < nl && !container; ++k) {
+        LevelD &L = h->lv[k];
+        if (!L.m[AMG_A].present) return fail(AMG_E_STATE, "level " + std::to_string(k) + ": operator A missing");
+        L.n = L.m[AMG_A].nrows;
+        if (h->nranks == 1) {
+            L.gn = L.n;
+            L.n0 = 0;
+            if (L.m[AMG_A].gncols != L.n) return fail(AMG_E_DIM, "level " + std::to_string(k) + ": A is not square");
+        } else {
+            if ((int)L.starts.size() != h->nranks + 1) return fail(AMG_E_STATE, "level " + std::to_string(k) + ": partition missing");
+            L.n0 = L.starts[h->rank];
+            L.gn = L.starts[h->nranks];
+            if (L.starts[h->rank + 1] - L.n0 != L.n) return fail(AMG_E_DIM, "level " + std::to_string(k) + ": local rows do not match the partition");
+        }
+        if (k < nl - 1) {
+            if (!L.m[AMG_P].present || !L.m[AMG_PT].present) return fail(AMG_E_STATE, "level " + std::to_string(k) + ": P / Pt missing");
+            if (!L.has_smoother) return fail(AMG_E_STATE, "level " + std::to_string(k) + ": smoother missing");
+            if (L.sm_kind == AMG_SMOOTHER_FSAI && (!L.m[AMG_G].present || !L.m[AMG_GT].present))
+                return fail(AMG_E_STATE, "level " + std::to_string(k) + ": FSAI factor G / Gt missing");
+        }
+    }
+    for (int k = 0; k < nl; ++k) h->lv[k].n = h->lv[k].m[AMG_A].nrows;
+    for (int k = 0; k < nl - 1 && !container; ++k) {
+        LevelD &L = h->lv[k], &C = h->lv[k + 1];
+        if (L.m[AMG_P].nrows != L.n || L.m[AMG_P].gncols != (h->nranks == 1 ? C.n : C.gn))
+            return fail(AMG_E_DIM, "level " + std::to_string(k) + ": P shape does not match the levels");
+        if (L.m[AMG_PT].nrows != C.n) return fail(AMG_E_DIM, "level " + std::to_string(k) + ": Pt shape does not match");
+    }
+    h->container = container;
+    if (!container && h->nc != h->lv[nl - 1].gn) return fail(AMG_E_DIM, "coarsest factor size does not match the last level");
+    int bps = 1;
+    TRY(configure_kernels(h, &bps));
+    const int per_sm = h->ctas_per_sm > 0 ? std::min(h->ctas_per_sm, bps) : bps;
+    h->max_grid = h->sm_count * 8;
+    // halos (nranks > 1) + tile schedules
+    for (int k = 0; k < nl; ++k) {
+        LevelD &L = h->lv[k];
+        for (int w = 0; w < 5; ++w) {
+            DevMat &M = L.m[w];
+            if (!M.present) continue;
+            std::vector<int32_t> off32(M.nrows + 1);
+            CK(cudaMemcpy(off32.data(), M.off, (M.nrows + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+            std::vector<TileDesc> tiles;
+            build_tiles(off32, M.nrows, h->tile_nnz, h->tile_rows, tiles);
+            M.ntiles = (int)tiles.size();
+            TRY(dalloc(&M.tiles, tiles.size()));
+            if (!tiles.empty()) CK(cudaMemcpy(M.tiles, tiles.data(), tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
+            const double avg = M.nrows ? (double)M.nnz / (double)M.nrows : 0.0;
+            M.lanes = h->lanes_override ? h->lanes_override : (avg < 9.0 ? 1 : avg < 17.0 ? 2 : avg < 33.0 ? 4 : 8);
+            M.grid = std::max(1, std::min(M.ntiles, h->sm_count * per_sm));
+            h->max_grid = std::max(h->max_grid, M.grid);
+        }
+    }
+    // vectors: capacity = local rows + the largest halo feeding a matrix on that level's column space
+    int64_t nmax = 0;
+    for (int k = 0; k < nl; ++k) {
+        LevelD &L = h->lv[k];
+        int64_t cap = L.n;
+        for (int w = 0; w < 5; ++w)
+            if (L.m[w].present && (w != AMG_P || container)) cap = std::max(cap, std::max(L.m[w].ncols, L.m[w].nrows));
+        if (k > 0 && h->lv[k - 1].m[AMG_P].present) cap = std::max(cap, h->lv[k - 1].m[AMG_P].ncols);
+        if (k == nl - 1) cap = std::max<int64_t>(cap, h->nc);
+        L.cap = cap + 2;
+        TRY(dalloc(&L.y, L.cap));
+        TRY(dalloc(&L.x, L.cap));
+        TRY(dalloc(&L.r, L.cap));
+        TRY(dalloc(&L.t, L.cap));
+        nmax = std::max(nmax, L.cap);
+    }
+    const int64_t c0 = h->lv[0].cap;
+    TRY(dalloc(&h->b, c0));
+    TRY(dalloc(&h->x, c0));
+    TRY(dalloc(&h->r, c0));
+    TRY(dalloc(&h->z, c0));
+    TRY(dalloc(&h->p, c0));
+    TRY(dalloc(&h->q, c0));
+    TRY(dalloc(&h->tmp_in, nmax));
+    TRY(dalloc(&h->tmp_out, nmax));
+    TRY(dalloc(&h->partials, h->max_grid));
+    TRY(dalloc(&h->ticket, 4));
+    TRY(dalloc(&h->ctl, 1));
+    CK(cudaMallocHost((void **)&h->ctl_h, sizeof(PcgCtl)));
+    std::memset(h->ctl_h, 0, sizeof(PcgCtl));
+    h->finalized = true;
+    CK(cudaDeviceSynchronize());
+    return AMG_OK;
+}
+
+static int check_final(amg_t *h)
+{
+    if (!h) return fail(AMG_E_ARG, "NULL handle");
+    if (!h->finalized) return fail(AMG_E_STATE, "handle is not finalized (call amg_finalize)");
+    cudaError_t e = cudaSetDevice(h->device);
+    if (e != cudaSuccess) return fail(AMG_E_CUDA, cudaGetErrorString(e));
+    return AMG_OK;
+}
+
+static int to_dev(amg_t *h, double *dst, const double *src, int64_t n, int on_device)
+{
+    if (n == 0) return AMG_OK;
+    CK(cudaMemcpyAsync(dst, src, n * sizeof(double), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
+    return AMG_OK;
+}
+
+static int from_dev(amg_t *h, double *dst, const double *src, int64_t n, int on_device)
+{
+    if (n == 0) return AMG_OK;
+    CK(cudaMemcpyAsync(dst, src, n * sizeof(double), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
+    return AMG_OK;
+}
+
+static int sync_stream(amg_t *h)
+{
+    CK(cudaStreamSynchronize(h->stream));
+    return AMG_OK;
+}
+
+int amg_spmv(amg_t *h, int level, int which, const double *x, double *y, int on_device)
+{
+    TRY(check_final(h));
+    if (level < 0 || level >= (int)h->lv.size() || which < 0 || which > 4) return fail(AMG_E_ARG, "amg_spmv: bad level / slot");
+    const DevMat &M = h->lv[level].m[which];
+    if (!M.present) return fail(AMG_E_ARG, "amg_spmv: matrix slot is empty");
+    if (!x || !y) return fail(AMG_E_ARG, "amg_spmv: NULL vector");
+    int64_t xn = M.gncols;
+    if (h->nranks > 1) {
+        const std::vector<int64_t> &cs = (which == AMG_P) ? h->lv[level + 1].starts : h->lv[level].starts;
+        xn = cs[h->rank + 1] - cs[h->rank];
+    }
+    TRY(to_dev(h, h->tmp_in, x, xn, on_device));
+    TRY(launch_spmv(h, M, h->tmp_in, h->tmp_out, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, nullptr, nullptr));
+    TRY(from_dev(h, y, h->tmp_out, M.nrows, on_device));
+    return sync_stream(h);
+}
+
+int amg_smoother(amg_t *h, int level, const double *b, const double *x0, double *x, int steps, int on_device)
+{
+    TRY(check_final(h));
+    if (h->container) return fail(AMG_E_STATE, "matrix container handle: no hierarchy uploaded");
+    if (level < 0 || level >= (int)h->lv.size() - 1) return fail(AMG_E_ARG, "amg_smoother: level has no smoother");
+    if (!b || !x || steps < 0) return fail(AMG_E_ARG, "amg_smoother: bad arguments");
+    LevelD &L = h->lv[level];
+    TRY(to_dev(h, h->tmp_in, b, L.n, on_device));
+    if (x0) TRY(to_dev(h, h->tmp_out, x0, L.n, on_device));
+    else CK(cudaMemsetAsync(h->tmp_out, 0, L.n * sizeof(double), h->stream));
+    TRY(enqueue_smooth(h, level, h->tmp_in, h->tmp_out, steps, x0 == nullptr, nullptr, FIN_NONE, nullptr));
+    TRY(from_dev(h, x, h->tmp_out, L.n, on_device));
+    return sync_stream(h);
+}
+
+int amg_coarse_solve(amg_t *h, const double *y, double *z, int on_device)
+{
+    TRY(check_final(h));
+    if (h->container) return fail(AMG_E_STATE, "matrix container handle: no hierarchy uploaded");
+    if (!y || !z) return fail(AMG_E_ARG, "amg_coarse_solve: NULL vector");
+    TRY(to_dev(h, h->tmp_in, y, h->nc, on_device));
+    TRY(launch_coarse(h, h->tmp_in, h->tmp_out, nullptr, FIN_NONE, nullptr));
+    TRY(from_dev(h, z, h->tmp_out, h->nc, on_device));
+    return sync_stream(h);
+}
+
+int amg_vcycle(amg_t *h, const double *y, double *z, int on_device)
+{
+    TRY(check_final(h));
+    if (h->container) return fail(AMG_E_STATE, "matrix container handle: no hierarchy uploaded");
+    if (!y || !z) return fail(AMG_E_ARG, "amg_vcycle: NULL vector");
+    const int64_t n = h->lv[0].n;
+    TRY(to_dev(h, h->tmp_in, y, n, on_device));
+    TRY(enqueue_vcycle(h, 0, h->tmp_in, h->tmp_out, nullptr, FIN_NONE, nullptr));
+    TRY(from_dev(h, z, h->tmp_out, n, on_device));
+    return sync_stream(h);
+}
+
+int amg_pcg(amg_t *h, const double *b, const double *x0, double rtol, int max_iters, int recompute_every,
+            double *x_out, int *n_iter, double *relres, int *converged, double *history, int *hist_len,
+            double *curvature_at_fail, int on_device)
+{
+    auto t_start = std::chrono::steady_clock::now();
+    TRY(check_final(h));
+    if (h->container) return fail(AMG_E_STATE, "matrix container handle: no hierarchy uploaded");
+    if (!b || !x_out || !n_iter || !relres || !converged) return fail(AMG_E_ARG, "amg_pcg: NULL argument");
+    if (max_iters < 0 || recompute_every < 1) return fail(AMG_E_ARG, "amg_pcg: bad max_iters / recompute_every");
+    const int64_t n = h->lv[0].n;
+    const int64_t launches0 = h->launches;
+    if (history) {
+        if (h->hist_cap < max_iters + 1) {
+            if (h->hist) cudaFree(h->hist);
+            h->hist = nullptr;
+            TRY(dalloc(&h->hist, (size_t)max_iters + 1));
+            h->hist_cap = max_iters + 1;
+        }
+    }
+    TRY(build_graph(h));
+    PcgCtl c{};
+    c.active = 1;
+    c.max_iters = max_iters;
+    c.recompute_every = recompute_every;
+    c.record = history ? 1 : 0;
+    c.rtol = rtol;
+    c.hist = h->hist;
+    *h->ctl_h = c;
+    CK(cudaEventRecord(h->ev0, h->stream));
+    CK(cudaMemcpyAsync(h->ctl, h->ctl_h, sizeof(PcgCtl), cudaMemcpyHostToDevice, h->stream));
+    TRY(to_dev(h, h->b, b, n, on_device));
+    if (x0) TRY(to_dev(h, h->x, x0, n, on_device));
+    else CK(cudaMemsetAsync(h->x, 0, n * sizeof(double), h->stream));
+    // bnorm = ||b||; b == 0 returns zeros (krylov.py:50-53)
+    TRY(launch_dot(h, h->b, h->b, n, FIN_BNORM, nullptr, nullptr));
+    CK(cudaMemcpyAsync(h->ctl_h, h->ctl, sizeof(PcgCtl), cudaMemcpyDeviceToHost, h->stream));
+    TRY(sync_stream(h));
+    if (h->ctl_h->bnorm == 0.0) {
+        CK(cudaMemsetAsync(h->x, 0, n * sizeof(double), h->stream));
+        TRY(from_dev(h, x_out, h->x, n, on_device));
+        TRY(sync_stream(h));
+        *n_iter = 0;
+        *relres = 0.0;
+        *converged = 1;
+        if (hist_len) *hist_len = 0;
+        h->solve_ms = 0.0;
+        return AMG_OK;
+    }
+    const LevelD &L0 = h->lv[0];
+    const int *act = &h->ctl->active;
+    // r = b - A x ; relres_0 ; z = M r ; rz = r.z ; p = z     (krylov.py:55-63)
+    TRY(launch_spmv(h, L0.m[AMG_A], h->x, h->r, EPI_RESID, h->b, 0.0, h->r, FIN_INIT_RES, nullptr, nullptr));
+    TRY(enqueue_vcycle(h, 0, h->r, h->z, nullptr, FIN_INIT_RZ, h->r));
+    TRY(launch_copy(h, h->p, h->z, n, nullptr));
+    (void)act;
+    if (max_iters > 0) {
+        if (h->graph_mode == 2) {
+            CK(cudaGraphLaunch(h->gexec, h->stream));
+            ++h->launches;
+        } else {
+            // batched launches of the iteration graph, host checks every `batch`
+            for (;;) {
+                for (int i = 0; i < h->batch; ++i) {
+                    if (h->graph_mode == 1) CK(cudaGraphLaunch(h->gexec, h->stream));
+                    else { cudaGraphConditionalHandle d{}; TRY(enqueue_pcg_body(h, d, 0)); }
+                }
+                CK(cudaMemcpyAsync(h->ctl_h, h->ctl, sizeof(PcgCtl), cudaMemcpyDeviceToHost, h->stream));
+                TRY(sync_stream(h));
+                if (!h->ctl_h->active) break;
+            }
+        }
+    }
+    CK(cudaMemcpyAsync(h->ctl_h, h->ctl, sizeof(PcgCtl), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaEventRecord(h->ev1, h->stream));
+    TRY(from_dev(h, x_out, h->x, n, on_device));
+    TRY(sync_stream(h));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    h->solve_ms = ms;
+    const PcgCtl &r = *h->ctl_h;
+    int iters = r.it;
+    if (h->graph_mode == 2) h->launches += (int64_t)std::max(iters, 1) * h->launches_per_iter;
+    else if (h->graph_mode == 1) h->launches += (int64_t)std::max(iters, 1) * h->launches_per_iter;
+    h->launches_last = h->launches - launches0;
+    *n_iter = iters;
+    *relres = r.relres;
+    *converged = r.converged;
+    if (history && hist_len) {
+        int hl = r.record ? (iters + 1) : 0;
+        if (r.status == 3) hl = iters;  // failing iteration appended nothing
+        hl = std::min(hl, max_iters + 1);
+        if (hl > 0) CK(cudaMemcpy(history, h->hist, hl * sizeof(double), cudaMemcpyDeviceToHost));
+        *hist_len = hl;
+    }
+    h->e2e_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    if (r.status == 3) {
+        if (curvature_at_fail) *curvature_at_fail = r.curv_fail;
+        char buf[160];
+        snprintf(buf, sizeof(buf), "iteration %d: direction with curvature %.3e; operator is not symmetric positive definite",
+                 iters, r.curv_fail);
+        return fail(AMG_E_NOT_SPD, buf);
+    }
+    return AMG_OK;
+}
+
+int amg_get_stats(amg_t *h, amg_stats_t *out)
+{
+    if (!h || !out) return fail(AMG_E_ARG, "amg_get_stats: NULL argument");
+    std::memset(out, 0, sizeof(*out));
+    out->solve_ms = h->solve_ms;
+    out->e2e_ms = h->e2e_ms;
+    out->launches_per_iter = h->launches_per_iter;
+    out->launches_last = h->launches_last;
+    out->graph_mode = h->graph_mode;
+    out->n_levels = (int)h->lv.size();
+    return AMG_OK;
+}
+
+}  // extern "C"

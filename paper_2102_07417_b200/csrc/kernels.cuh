@@ -1,0 +1,649 @@
+// Device kernels of the amgb200 solve path (sm_100a, fp64, HBM-bound).
+//
+// * spmv_tiles: persistent CSR SpMV.  Rows are cut at upload into tiles of
+//   <= TILE_NNZ stored entries / <= TILE_ROWS rows; each CTA walks its tiles
+//   round-robin and stages a tile's contiguous value / column / offset
+//   ranges in shared memory with cp.async.bulk (TMA bulk engine, mbarrier
+//   completion, STAGES-deep ring), so every HBM byte is moved by fully
+//   coalesced 16-byte-aligned bulk transfers and the next tiles are in
+//   flight while the current one is reduced.
+//   Row sums follow the reference order exactly (amgkit/sparse.py:212-217 ->
+//   np.add.reduceat, restated in oracle/rowsum.c):
+//       y_i = p_0 + pairwise(p_1 .. p_{L-1}),  p_k = a_k * x[c_k] (rounded)
+//   with numpy's eight strided accumulators mapped onto LANES lanes per row
+//   and its ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) combine done as a shuffle
+//   butterfly -- so a row sum is bit-identical to the reference's.
+//   Fused epilogues: y = s | y = b - s | y = b + w*s | y = w*s | y = b + s,
+//   plus an optional deterministic dot partial sum_i y_i * d_i.
+// * vector kernels for the PCG recurrences (krylov.py:40-92) with fused
+//   dot partials; every reduction is fixed-order (per-CTA partials, the last
+//   CTA to finish folds them in index order) -- no fp atomics, so repeated
+//   solves are bitwise identical.
+// * coarse_chol: dense forward/back substitution with the lower Cholesky
+//   factor staged in shared memory (hierarchy.py:149-152, dpotrs).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace amg {
+
+constexpr int TILE_THREADS = 256;
+
+enum Epi { EPI_PLAIN = 0, EPI_RESID = 1, EPI_AXPYW = 2, EPI_SETW = 3, EPI_ADD = 4 };
+
+enum Fin {
+    FIN_NONE = 0,
+    FIN_BNORM,
+    FIN_INIT_RES,
+    FIN_INIT_RZ,
+    FIN_CURV,
+    FIN_UPDATE,
+    FIN_RECOMPUTE,
+    FIN_TRUE,
+    FIN_RZ,
+    FIN_STORE  // store raw sum into ctl->scratch (tests / diagnostics)
+};
+
+// Device-resident PCG state: the control flow of krylov.py:40-92 evaluated
+// on the GPU so an iteration never waits for the host.
+struct PcgCtl {
+    int active;        // 1 while the loop runs (0 after convergence / failure / max_iters)
+    int do_recompute;  // this iteration replaces r by b - A x (recompute_every)
+    int need_true;     // recurrence relres <= rtol: evaluate the true residual
+    int converged;
+    int status;        // 0 ok, 3 = not SPD
+    int it;            // current iteration number
+    int max_iters;
+    int recompute_every;
+    int record;
+    int pad_;
+    double rtol, bnorm, rz, curv, alpha, beta, relres, curv_fail, scratch;
+    double *hist;
+};
+
+struct TileDesc {
+    int32_t r0, r1;  // rows [r0, r1)
+    int32_t k0, k1;  // stored entries [k0, k1)
+};
+
+struct SpmvArgs {
+    const int32_t *off;
+    const int32_t *col;
+    const double *val;
+    const TileDesc *tiles;
+    int ntiles;
+    int tile_nnz;   // staging capacity (entries)
+    int tile_rows;  // staging capacity (rows)
+    int stages;
+    const double *x;  // gathered vector
+    double *y;        // output
+    const double *b;  // epilogue operand (may alias y)
+    double omega;
+    const double *dotw;  // dot partner (nullptr: no dot)
+    double *partials;
+    unsigned *ticket;
+    int fin;
+    PcgCtl *ctl;
+    const int *gate1;
+    const int *gate2;
+};
+
+// ---------------------------------------------------------------- helpers
+
+__device__ __forceinline__ bool gate_open(const int *g1, const int *g2)
+{
+    return (g1 == nullptr || *(volatile const int *)g1) && (g2 == nullptr || *(volatile const int *)g2);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ double prod(double a, double x) { return __dmul_rn(a, x); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+
+// Fixed-shape block reduction (deterministic).  Result valid in thread 0.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double *red)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = (l < NT / 32) ? red[l] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    }
+    return v;
+}
+
+__device__ void apply_fin(int fin, double v, PcgCtl *c)
+{
+    switch (fin) {
+    case FIN_BNORM: c->bnorm = sqrt(v); break;
+    case FIN_INIT_RES: {
+        double rr = sqrt(v) / c->bnorm;
+        c->relres = rr;
+        if (c->record) c->hist[0] = rr;
+        if (rr <= c->rtol) { c->converged = 1; c->active = 0; }
+        break;
+    }
+    case FIN_INIT_RZ: c->rz = v; break;
+    case FIN_CURV:
+        c->it += 1;
+        c->curv = v;
+        if (v <= 0.0) {  // krylov.py:67-72 (NaN passes, as in the reference)
+            c->status = 3;
+            c->curv_fail = v;
+            c->active = 0;
+        } else {
+            c->alpha = c->rz / v;
+        }
+        break;
+    case FIN_UPDATE:
+        if (c->it % c->recompute_every == 0) {
+            c->do_recompute = 1;
+        } else {
+            double rr = sqrt(v) / c->bnorm;
+            c->relres = rr;
+            if (c->record) c->hist[c->it] = rr;
+            c->need_true = rr <= c->rtol;
+        }
+        break;
+    case FIN_RECOMPUTE: {
+        c->do_recompute = 0;
+        double rr = sqrt(v) / c->bnorm;
+        c->relres = rr;
+        if (c->record) c->hist[c->it] = rr;
+        c->need_true = rr <= c->rtol;
+        break;
+    }
+    case FIN_TRUE: {
+        c->need_true = 0;
+        double rr = sqrt(v) / c->bnorm;
+        c->relres = rr;
+        if (rr <= c->rtol) { c->converged = 1; c->active = 0; }
+        break;
+    }
+    case FIN_RZ:
+        c->beta = v / c->rz;
+        c->rz = v;
+        break;
+    case FIN_STORE: c->scratch = v; break;
+    default: break;
+    }
+}
+
+// Per-CTA partial -> last CTA folds all partials in index order and applies
+// the finalize op.  `v` must be the block sum held by thread 0.
+template <int NT>
+__device__ __forceinline__ void grid_finalize(double v, double *partials, unsigned *ticket, int fin, PcgCtl *ctl)
+{
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = v;
+        __threadfence();
+        unsigned t = atomicAdd(ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x < 32) {
+        __threadfence();
+        double a = 0.0;
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) a += __ldcg(partials + i);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+        if (threadIdx.x == 0) {
+            apply_fin(fin, a, ctl);
+            *ticket = 0u;
+            __threadfence();
+        }
+    }
+}
+
+// ---------------------------------------------------------------- SpMV
+
+// Recursive numpy pairwise sum (n > 128) over products read through `P`.
+template <class PF>
+__device__ double pairwise_rec(const PF &P, int base, int n)
+{
+    if (n < 8) {
+        double r = 0.0;
+        for (int i = 0; i < n; ++i) r = add(r, P(base + i));
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = P(base + j);
+        int i = 8;
+        const int main = n - (n % 8);
+        for (; i < main; i += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = add(r[j], P(base + i + j));
+        }
+        double res = add(add(add(r[0], r[1]), add(r[2], r[3])), add(add(r[4], r[5]), add(r[6], r[7])));
+        for (; i < n; ++i) res = add(res, P(base + i));
+        return res;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    double a = pairwise_rec(P, base, n2);
+    double b = pairwise_rec(P, base + n2, n - n2);
+    return add(a, b);
+}
+
+// Row sum in numpy order for one row whose entries sit at smem positions
+// [lo, hi) (relative to the staged arrays).  Executed by the LANES lanes of
+// a group; the result is valid in the group's lane 0.
+template <int LANES>
+__device__ __forceinline__ double row_sum_staged(const double *__restrict__ vs, const int32_t *__restrict__ cs,
+                                                 int vdelta, int cdelta, int lo, int hi,
+                                                 const double *__restrict__ x, int lane, unsigned gmask)
+{
+    auto P = [&](int k) -> double { return prod(vs[k - vdelta], __ldg(x + cs[k - cdelta])); };
+    const int len = hi - lo;
+    if (len <= 0) return 0.0;
+    const int n = len - 1;
+    const int base = lo + 1;
+    if (n < 8 || n > 128) {
+        double s = 0.0;
+        if (lane == 0) {
+            double p0 = P(lo);
+            double res;
+            if (n < 8) {
+                res = 0.0;
+                for (int i = 0; i < n; ++i) res = add(res, P(base + i));
+            } else {
+                res = pairwise_rec(P, base, n);
+            }
+            s = add(p0, res);
+        }
+        return s;
+    }
+    constexpr int M = 8 / LANES;  // accumulators per lane: r_{lane + m*LANES}
+    const int main = n - (n % 8);
+    double acc[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) acc[m] = P(base + lane + m * LANES);
+    for (int i = 8; i < main; i += 8) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) acc[m] = add(acc[m], P(base + i + lane + m * LANES));
+    }
+    double res;
+    if constexpr (LANES == 1) {
+        res = add(add(add(acc[0], acc[1]), add(acc[2], acc[3])), add(add(acc[4], acc[5]), add(acc[6], acc[7])));
+    } else if constexpr (LANES == 2) {
+        // lane j holds r_j, r_{j+2}, r_{j+4}, r_{j+6}
+        double u[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) u[m] = add(acc[m], __shfl_xor_sync(gmask, acc[m], 1));
+        res = add(add(u[0], u[1]), add(u[2], u[3]));
+    } else if constexpr (LANES == 4) {
+        // lane j holds r_j, r_{j+4}
+        double s0 = add(acc[0], __shfl_xor_sync(gmask, acc[0], 1));
+        double s1 = add(acc[1], __shfl_xor_sync(gmask, acc[1], 1));
+        s0 = add(s0, __shfl_xor_sync(gmask, s0, 2));
+        s1 = add(s1, __shfl_xor_sync(gmask, s1, 2));
+        res = add(s0, s1);
+    } else {
+        double s = acc[0];
+        s = add(s, __shfl_xor_sync(gmask, s, 1));
+        s = add(s, __shfl_xor_sync(gmask, s, 2));
+        s = add(s, __shfl_xor_sync(gmask, s, 4));
+        res = s;
+    }
+    double out = 0.0;
+    if (lane == 0) {
+        for (int i = main; i < n; ++i) res = add(res, P(base + i));
+        out = add(P(lo), res);
+    }
+    return out;
+}
+
+template <int EPI>
+__device__ __forceinline__ double epilogue(double s, const double *b, int64_t row, double omega)
+{
+    if constexpr (EPI == EPI_PLAIN) return s;
+    if constexpr (EPI == EPI_RESID) return __dsub_rn(b[row], s);
+    if constexpr (EPI == EPI_AXPYW) return add(b[row], __dmul_rn(omega, s));
+    if constexpr (EPI == EPI_SETW) return __dmul_rn(omega, s);
+    if constexpr (EPI == EPI_ADD) return add(b[row], s);
+    return s;
+}
+
+struct StageLayout {
+    int vals_bytes, cols_bytes, offs_bytes, stage_bytes;
+};
+
+__host__ __device__ inline StageLayout stage_layout(int tile_nnz, int tile_rows)
+{
+    StageLayout L;
+    L.vals_bytes = ((tile_nnz + 2) * 8 + 15) & ~15;
+    L.cols_bytes = ((tile_nnz + 4) * 4 + 15) & ~15;
+    L.offs_bytes = ((tile_rows + 1 + 4) * 4 + 15) & ~15;
+    L.stage_bytes = L.vals_bytes + L.cols_bytes + L.offs_bytes;
+    return L;
+}
+
+__device__ __forceinline__ void issue_tile(const SpmvArgs &a, const StageLayout &L, char *stage, uint64_t *bar,
+                                           int t)
+{
+    const TileDesc d = a.tiles[t];
+    const int nk = d.k1 - d.k0;
+    if (nk > a.tile_nnz) {  // long row: consumers read it from global memory
+        mbar_arrive_tx(bar, 0);
+        return;
+    }
+    const int va = d.k0 & ~1, ca = d.k0 & ~3, oa = d.r0 & ~3;
+    const unsigned vb = nk ? (unsigned)(((d.k1 - va) * 8 + 15) & ~15) : 0u;
+    const unsigned cb = nk ? (unsigned)(((d.k1 - ca) * 4 + 15) & ~15) : 0u;
+    const unsigned ob = (unsigned)(((d.r1 + 1 - oa) * 4 + 15) & ~15);
+    mbar_arrive_tx(bar, vb + cb + ob);
+    if (vb) bulk_g2s(stage, a.val + va, vb, bar);
+    if (cb) bulk_g2s(stage + L.vals_bytes, a.col + ca, cb, bar);
+    bulk_g2s(stage + L.vals_bytes + L.cols_bytes, a.off + oa, ob, bar);
+}
+
+template <int EPI, int LANES>
+__global__ void __launch_bounds__(TILE_THREADS) spmv_tiles(const SpmvArgs a)
+{
+    extern __shared__ __align__(128) char smem[];
+    __shared__ __align__(8) uint64_t bars[8];
+    __shared__ double red[TILE_THREADS / 32];
+    if (!gate_open(a.gate1, a.gate2)) return;
+
+    const StageLayout L = stage_layout(a.tile_nnz, a.tile_rows);
+    const int S = a.stages;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int s = 0; s < S; ++s) {
+            int t = blockIdx.x + s * gridDim.x;
+            if (t < a.ntiles) issue_tile(a, L, smem + s * L.stage_bytes, &bars[s], t);
+        }
+    }
+    __syncthreads();
+
+    constexpr int G = TILE_THREADS / LANES;
+    const int grp = threadIdx.x / LANES;
+    const int lane = threadIdx.x % LANES;
+    const unsigned gmask = (LANES == 32) ? 0xffffffffu
+                                         : (((1u << LANES) - 1u) << ((threadIdx.x & 31) / LANES * LANES));
+    double dacc = 0.0;
+    const bool want_dot = a.dotw != nullptr;
+
+    int i = 0;
+    for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
+        const int s = i % S;
+        char *stage = smem + s * L.stage_bytes;
+        mbar_wait(&bars[s], (unsigned)((i / S) & 1));
+        const TileDesc d = a.tiles[t];
+        const int nrows = d.r1 - d.r0;
+        if (d.k1 - d.k0 > a.tile_nnz) {
+            // a single row longer than the staging tile: lane 0 of the CTA
+            // reduces it straight from global memory (same order).
+            if (threadIdx.x == 0) {
+                const int lo = a.off[d.r0], hi = a.off[d.r0 + 1];
+                auto P = [&](int k) -> double { return prod(a.val[k], __ldg(a.x + a.col[k])); };
+                double sum = add(P(lo), pairwise_rec(P, lo + 1, hi - lo - 1));
+                double yv = epilogue<EPI>(sum, a.b, d.r0, a.omega);
+                a.y[d.r0] = yv;
+                if (want_dot) dacc = fma(yv, a.dotw[d.r0], dacc);
+            }
+        } else {
+            const double *vs = reinterpret_cast<const double *>(stage);
+            const int32_t *cs = reinterpret_cast<const int32_t *>(stage + L.vals_bytes);
+            const int32_t *os = reinterpret_cast<const int32_t *>(stage + L.vals_bytes + L.cols_bytes);
+            const int vdelta = d.k0 & ~1, cdelta = d.k0 & ~3, odelta = d.r0 & ~3;
+            for (int rr = grp; rr < nrows; rr += G) {
+                const int row = d.r0 + rr;
+                const int lo = os[row - odelta], hi = os[row + 1 - odelta];
+                double sum = row_sum_staged<LANES>(vs, cs, vdelta, cdelta, lo, hi, a.x, lane, gmask);
+                if (lane == 0) {
+                    double yv = epilogue<EPI>(sum, a.b, row, a.omega);
+                    a.y[row] = yv;
+                    if (want_dot) dacc = fma(yv, a.dotw[row], dacc);
+                }
+            }
+        }
+        __syncthreads();  // every thread is done with stage s
+        if (threadIdx.x == 0) {
+            int tn = t + S * gridDim.x;
+            if (tn < a.ntiles) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue_tile(a, L, stage, &bars[s], tn);
+            }
+        }
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v = block_sum<TILE_THREADS>(dacc, red);
+        grid_finalize<TILE_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
+// ---------------------------------------------------------------- vectors
+
+constexpr int VEC_THREADS = 256;
+
+struct VecArgs {
+    int64_t n;
+    double *x;        // output / in-out
+    double *r;        // second in-out (pcg_update)
+    const double *p;  // inputs
+    const double *q;
+    const double *d;
+    double omega;
+    int mode;
+    double *partials;
+    unsigned *ticket;
+    int fin;
+    PcgCtl *ctl;
+    const int *gate1;
+    const int *gate2;
+};
+
+// x += alpha p ; r -= alpha q ; partial r.r      (krylov.py:73-75, 78)
+__global__ void __launch_bounds__(VEC_THREADS) pcg_update(const VecArgs a)
+{
+    __shared__ double red[VEC_THREADS / 32];
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const double alpha = a.ctl->alpha;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+        a.x[i] = add(a.x[i], __dmul_rn(alpha, a.p[i]));
+        double rv = __dsub_rn(a.r[i], __dmul_rn(alpha, a.q[i]));
+        a.r[i] = rv;
+        acc = fma(rv, rv, acc);
+    }
+    double v = block_sum<VEC_THREADS>(acc, red);
+    grid_finalize<VEC_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+}
+
+// p = z + beta p                                   (krylov.py:91)
+__global__ void __launch_bounds__(VEC_THREADS) pcg_xpay(const VecArgs a)
+{
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const double beta = a.ctl->beta;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
+        a.x[i] = add(a.p[i], __dmul_rn(beta, a.x[i]));
+}
+
+// mode 0: sum p.q ; finalize
+__global__ void __launch_bounds__(VEC_THREADS) vec_dot(const VecArgs a)
+{
+    __shared__ double red[VEC_THREADS / 32];
+    if (!gate_open(a.gate1, a.gate2)) return;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
+        acc = fma(a.p[i], a.q[i], acc);
+    double v = block_sum<VEC_THREADS>(acc, red);
+    grid_finalize<VEC_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+}
+
+// Jacobi sweep (smoothers.py:47-49, 172): mode 0: x = w*(d*r) ; mode 1: x += w*(d*r)
+// optional dot partial x.q
+__global__ void __launch_bounds__(VEC_THREADS) jacobi_sweep(const VecArgs a)
+{
+    __shared__ double red[VEC_THREADS / 32];
+    if (!gate_open(a.gate1, a.gate2)) return;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+        double z = __dmul_rn(a.omega, __dmul_rn(a.d[i], a.p[i]));
+        double xv = a.mode ? add(a.x[i], z) : z;
+        a.x[i] = xv;
+        if (a.q) acc = fma(xv, a.q[i], acc);
+    }
+    if (a.fin != FIN_NONE) {
+        double v = block_sum<VEC_THREADS>(acc, red);
+        grid_finalize<VEC_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
+__global__ void __launch_bounds__(VEC_THREADS) vec_copy(const VecArgs a)
+{
+    if (!gate_open(a.gate1, a.gate2)) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
+        a.x[i] = a.p ? a.p[i] : 0.0;
+}
+
+// Loop continuation for the device while-loop graph.
+__global__ void pcg_continue(PcgCtl *c, cudaGraphConditionalHandle handle, int use_handle)
+{
+    if (c->active && c->it >= c->max_iters) c->active = 0;
+    if (use_handle) cudaGraphSetConditional(handle, c->active ? 1u : 0u);
+}
+
+// ---------------------------------------------------------------- coarse solve
+
+// Cholesky: solve L y = b, then L^T z = y (dpotrs with uplo = 'L').
+// Lp: packed lower triangle, row-major: row i holds L[i][0..i] at i(i+1)/2.
+// Single CTA; the packed factor is staged in shared memory when it fits.
+constexpr int COARSE_THREADS = 256;
+
+__global__ void __launch_bounds__(COARSE_THREADS) coarse_chol(int n, const double *__restrict__ Lp, const double *y,
+                                                               double *z, int staged, const int *gate1,
+                                                               double *partials, unsigned *ticket, int fin,
+                                                               PcgCtl *ctl, const double *dotw)
+{
+    extern __shared__ __align__(16) double sh[];
+    __shared__ double red[COARSE_THREADS / 32];
+    if (!gate_open(gate1, nullptr)) return;
+    const int64_t np = (int64_t)n * (n + 1) / 2;
+    double *v = sh;  // n
+    const double *L = Lp;
+    if (staged) {
+        double *Ls = sh + ((n + 1) & ~1);
+        for (int64_t i = threadIdx.x; i < np; i += blockDim.x) Ls[i] = Lp[i];
+        L = Ls;
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = y[i];
+    __syncthreads();
+    // forward: column-oriented L y = b
+    for (int j = 0; j < n; ++j) {
+        const int64_t rj = (int64_t)j * (j + 1) / 2;
+        const double yj = v[j] / L[rj + j];
+        __syncthreads();
+        if (threadIdx.x == 0) v[j] = yj;
+        for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) v[i] -= L[(int64_t)i * (i + 1) / 2 + j] * yj;
+        __syncthreads();
+    }
+    // backward: L^T z = y, row j of L^T is column j of L: z_j = (y_j - sum_{i>j} L_ij z_i) / L_jj
+    // column-oriented on L^T: for j = n-1..0: z_j /= L_jj ; v_i -= L_ji z_j for i < j
+    for (int j = n - 1; j >= 0; --j) {
+        const int64_t rj = (int64_t)j * (j + 1) / 2;
+        const double zj = v[j] / L[rj + j];
+        __syncthreads();
+        if (threadIdx.x == 0) v[j] = zj;
+        for (int i = threadIdx.x; i < j; i += blockDim.x) v[i] -= L[rj + i] * zj;
+        __syncthreads();
+    }
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        z[i] = v[i];
+        if (dotw) acc = fma(v[i], dotw[i], acc);
+    }
+    if (fin != FIN_NONE) {
+        double s = block_sum<COARSE_THREADS>(acc, red);
+        grid_finalize<COARSE_THREADS>(s, partials, ticket, fin, ctl);
+    }
+}
+
+// LU (getrs, no transpose): b <- P b ; L (unit) y = b ; U z = y.  LU full n x n row-major.
+__global__ void __launch_bounds__(COARSE_THREADS) coarse_lu(int n, const double *__restrict__ LU,
+                                                             const int32_t *__restrict__ piv, const double *y,
+                                                             double *z, const int *gate1, double *partials,
+                                                             unsigned *ticket, int fin, PcgCtl *ctl,
+                                                             const double *dotw)
+{
+    extern __shared__ __align__(16) double sh[];
+    __shared__ double red[COARSE_THREADS / 32];
+    if (!gate_open(gate1, nullptr)) return;
+    double *v = sh;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = y[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < n; ++i) {
+            int p = piv[i];
+            if (p != i) { double t = v[i]; v[i] = v[p]; v[p] = t; }
+        }
+    }
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {
+        const double yj = v[j];
+        for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) v[i] -= LU[(int64_t)i * n + j] * yj;
+        __syncthreads();
+    }
+    for (int j = n - 1; j >= 0; --j) {
+        const double zj = v[j] / LU[(int64_t)j * n + j];
+        __syncthreads();
+        if (threadIdx.x == 0) v[j] = zj;
+        for (int i = threadIdx.x; i < j; i += blockDim.x) v[i] -= LU[(int64_t)i * n + j] * zj;
+        __syncthreads();
+    }
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        z[i] = v[i];
+        if (dotw) acc = fma(v[i], dotw[i], acc);
+    }
+    if (fin != FIN_NONE) {
+        double s = block_sum<COARSE_THREADS>(acc, red);
+        grid_finalize<COARSE_THREADS>(s, partials, ticket, fin, ctl);
+    }
+}
+
+}  // namespace amg

@@ -1,0 +1,268 @@
+"""On-disk hierarchy cache: the setup output the solve path consumes.
+
+Hierarchy setup (coarsening, interpolation, FSAI, Galerkin products) stays in
+the reference's host Python (``amgkit/hierarchy.py:155-223``).  Setup is
+expensive (minutes to hours for the BASELINE configs) and the
+reference is not importable on the GPU box, so ``tools/export_hierarchy.py``
+runs ``amgkit.setup`` once in the build container and freezes the result here.
+
+The in-memory form is a duck-typed mirror of ``AmgHierarchy`` / ``Level`` /
+``Smoother`` (``amgkit/hierarchy.py:95-152``, ``amgkit/smoothers.py:26-43``)
+so that :meth:`DeviceHierarchy.from_reference` accepts either.
+
+Two storage modes:
+
+* ``full``: every level's A, P, Pt, G, Gt is stored.
+* ``compact``: only what setup *chose* is stored -- G and P per level, the
+  relaxation factors and the coarsest factor.  A_0 is rebuilt from the
+  generator (``problems.py``), A_{k+1} by the Galerkin product, Pt and Gt by
+  exact transposes, each restating the reference's own producer
+  (``amgkit/sparse.py:220-224, 256-282``) with the same scipy calls, and then
+  verified against SHA-256 digests of the reference's arrays recorded at
+  export time.  Any mismatch raises: a hierarchy that differs from the
+  reference's is never used silently.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .problems import Csr, build_config
+
+__all__ = [
+    "HostSmoother",
+    "HostLevel",
+    "HostHierarchy",
+    "save_hierarchy",
+    "load_hierarchy",
+    "csr_digest",
+    "galerkin_product",
+    "transpose",
+]
+
+FORMAT = "amgb200-hier-v1"
+
+
+@dataclass
+class HostSmoother:
+    """Mirror of ``amgkit.smoothers.Smoother`` (fields the solve path reads)."""
+
+    kind: str
+    omega: float = 1.0
+    gmat: Csr | None = None
+    gmat_t: Csr | None = None
+    inv_diag: np.ndarray | None = None
+
+
+@dataclass
+class HostLevel:
+    """Mirror of ``amgkit.hierarchy.Level``."""
+
+    a: Csr
+    smoother: HostSmoother | None = None
+    p: Csr | None = None
+    pt: Csr | None = None
+
+
+@dataclass
+class _Cycle:
+    nu1: int = 1
+    nu2: int = 1
+
+
+@dataclass
+class HostHierarchy:
+    """Mirror of ``amgkit.hierarchy.AmgHierarchy`` after setup."""
+
+    levels: list
+    config: _Cycle
+    factor: tuple
+    factor_kind: str
+    symmetric: bool = True
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def n_levels(self):
+        return len(self.levels)
+
+
+def _as_csr(m):
+    return Csr(m.nrows, m.ncols, m.row_offsets, m.col_indices, m.values)
+
+
+def csr_digest(m):
+    h = hashlib.sha256()
+    h.update(np.asarray([m.nrows, m.ncols], dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(m.row_offsets, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(m.col_indices, dtype=np.int32).tobytes())
+    h.update(np.ascontiguousarray(m.values, dtype=np.float64).tobytes())
+    return h.hexdigest()
+
+
+def _from_scipy(m):
+    # restates SparseMatrix.from_scipy (amgkit/sparse.py:134-140)
+    m = m.tocsr()
+    if not m.has_canonical_format:
+        m.sum_duplicates()
+    m.sort_indices()
+    return Csr(m.shape[0], m.shape[1], m.indptr, m.indices, m.data)
+
+
+def _to_scipy(a):
+    import scipy.sparse as sp
+
+    return sp.csr_matrix((a.values, a.col_indices, a.row_offsets), shape=(a.nrows, a.ncols))
+
+
+def transpose(a):
+    """Exact transpose; restates ``amgkit/sparse.py:220-224``."""
+    t = _to_scipy(a).transpose().tocsr()
+    t.sort_indices()
+    return _from_scipy(t)
+
+
+def galerkin_product(a, p, symmetrize):
+    """P^T A P with optional (R + R^T)/2; restates ``amgkit/sparse.py:256-282``."""
+    import scipy.sparse as sp
+
+    ps = _to_scipy(p)
+    r = ps.T @ (_to_scipy(a) @ ps)
+    if symmetrize:
+        r = (r + r.T) * 0.5
+    r = sp.csr_matrix(r)
+    r.sum_duplicates()
+    r.sort_indices()
+    r.eliminate_zeros()
+    return _from_scipy(r)
+
+
+def _save_csr(path, m):
+    np.savez(path, shape=np.asarray([m.nrows, m.ncols], dtype=np.int64),
+             row_offsets=np.asarray(m.row_offsets, dtype=np.int64),
+             col_indices=np.asarray(m.col_indices, dtype=np.int32),
+             values=np.asarray(m.values, dtype=np.float64))
+
+
+def _load_csr(path):
+    with np.load(path) as z:
+        nr, nc = (int(v) for v in z["shape"])
+        return Csr(nr, nc, z["row_offsets"], z["col_indices"], z["values"])
+
+
+def save_hierarchy(h, directory, mode="full", generator=None, symmetrize_flags=None, extra=None):
+    """Freeze a setup result (``amgkit.AmgHierarchy`` or :class:`HostHierarchy`).
+
+    ``compact`` needs ``generator`` (a ``problems.CONFIGS`` name rebuilding
+    A_0) and ``symmetrize_flags[k]`` -- the ``symmetrize`` argument setup
+    passed to the Galerkin product of level k (``hierarchy.py:210``).
+    """
+    os.makedirs(directory, exist_ok=True)
+    levels = h.levels
+    man = {
+        "format": FORMAT,
+        "mode": mode,
+        "generator": generator,
+        "n_levels": len(levels),
+        "nu1": int(h.config.nu1),
+        "nu2": int(h.config.nu2),
+        "symmetric": bool(h.symmetric),
+        "factor_kind": h.factor_kind,
+        "levels": [],
+        "extra": extra or {},
+    }
+    if mode == "compact" and generator is None:
+        raise ValueError("compact mode needs the generator name")
+    for k, lvl in enumerate(levels):
+        ent = {"n": int(lvl.a.nrows), "nnz_a": int(lvl.a.nnz), "digest": {"a": csr_digest(lvl.a)}}
+        if mode == "full":
+            _save_csr(os.path.join(directory, f"L{k}_a.npz"), lvl.a)
+        sm = lvl.smoother
+        if sm is not None:
+            ent["smoother"] = {"kind": sm.kind, "omega": float(sm.omega)}
+            if sm.kind == "jacobi":
+                np.save(os.path.join(directory, f"L{k}_invdiag.npy"), np.asarray(sm.inv_diag, dtype=np.float64))
+            else:
+                _save_csr(os.path.join(directory, f"L{k}_g.npz"), sm.gmat)
+                ent["digest"]["gt"] = csr_digest(sm.gmat_t)
+                if mode == "full":
+                    _save_csr(os.path.join(directory, f"L{k}_gt.npz"), sm.gmat_t)
+        if lvl.p is not None:
+            _save_csr(os.path.join(directory, f"L{k}_p.npz"), lvl.p)
+            ent["digest"]["pt"] = csr_digest(lvl.pt)
+            if mode == "full":
+                _save_csr(os.path.join(directory, f"L{k}_pt.npz"), lvl.pt)
+            if symmetrize_flags is not None:
+                ent["symmetrize_next"] = bool(symmetrize_flags[k])
+        man["levels"].append(ent)
+    fac = h.factor
+    if h.factor_kind in ("cholesky", "cholesky+shift"):
+        c, lower = fac
+        if not lower:
+            raise ValueError("expected a lower Cholesky factor (hierarchy.py:127)")
+        np.save(os.path.join(directory, "coarse_c.npy"), np.tril(np.asarray(c, dtype=np.float64)))
+    else:
+        lu, piv = fac
+        np.save(os.path.join(directory, "coarse_c.npy"), np.asarray(lu, dtype=np.float64))
+        np.save(os.path.join(directory, "coarse_piv.npy"), np.asarray(piv, dtype=np.int32))
+    with open(os.path.join(directory, "manifest.json"), "w") as f:
+        json.dump(man, f, indent=1)
+    return man
+
+
+def load_hierarchy(directory, verify=True):
+    """Load a frozen hierarchy as a :class:`HostHierarchy`."""
+    with open(os.path.join(directory, "manifest.json")) as f:
+        man = json.load(f)
+    if man.get("format") != FORMAT:
+        raise ValueError(f"{directory}: not an {FORMAT} hierarchy")
+    mode = man["mode"]
+    levels = []
+    a = None
+    for k, ent in enumerate(man["levels"]):
+        if mode == "full":
+            a = _load_csr(os.path.join(directory, f"L{k}_a.npz"))
+        elif k == 0:
+            a = build_config(man["generator"])
+        else:
+            prev = levels[k - 1]
+            a = galerkin_product(prev.a, prev.p, man["levels"][k - 1].get("symmetrize_next", True))
+        if verify and csr_digest(a) != ent["digest"]["a"]:
+            raise ValueError(f"{directory}: level {k} operator does not match the reference digest")
+        lvl = HostLevel(a=a)
+        sm = ent.get("smoother")
+        if sm is not None:
+            if sm["kind"] == "jacobi":
+                inv = np.load(os.path.join(directory, f"L{k}_invdiag.npy"))
+                lvl.smoother = HostSmoother("jacobi", sm["omega"], inv_diag=inv)
+            else:
+                g = _load_csr(os.path.join(directory, f"L{k}_g.npz"))
+                gt_path = os.path.join(directory, f"L{k}_gt.npz")
+                gt = _load_csr(gt_path) if os.path.exists(gt_path) else transpose(g)
+                if verify and csr_digest(gt) != ent["digest"]["gt"]:
+                    raise ValueError(f"{directory}: level {k} G^T does not match the reference digest")
+                lvl.smoother = HostSmoother("fsai", sm["omega"], gmat=g, gmat_t=gt)
+        p_path = os.path.join(directory, f"L{k}_p.npz")
+        if os.path.exists(p_path):
+            lvl.p = _load_csr(p_path)
+            pt_path = os.path.join(directory, f"L{k}_pt.npz")
+            lvl.pt = _load_csr(pt_path) if os.path.exists(pt_path) else transpose(lvl.p)
+            if verify and csr_digest(lvl.pt) != ent["digest"]["pt"]:
+                raise ValueError(f"{directory}: level {k} P^T does not match the reference digest")
+        levels.append(lvl)
+    c = np.load(os.path.join(directory, "coarse_c.npy"))
+    if man["factor_kind"] in ("cholesky", "cholesky+shift"):
+        factor = (c, True)
+    else:
+        factor = (c, np.load(os.path.join(directory, "coarse_piv.npy")))
+    return HostHierarchy(
+        levels=levels,
+        config=_Cycle(man["nu1"], man["nu2"]),
+        factor=factor,
+        factor_kind=man["factor_kind"],
+        symmetric=man["symmetric"],
+        meta=man,
+    )

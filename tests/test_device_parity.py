@@ -1,0 +1,199 @@
+"""Device parity against the reference's golden vectors and the CPU oracle.
+
+Every call goes through libamgb200.so (the C ABI).  Tolerances are the
+north star's: per-kernel <= 1e-12 relative (SpMV and smoother sweeps are in
+fact bit-identical to the reference, asserted as such), PCG iteration count
+within +-1, final relative residual <= rtol.
+"""
+import numpy as np
+import pytest
+
+from conftest import _relerr
+from golden_io import HIER_CASES, SPMV_CASES, load_case, load_spmv_case, matrices_of
+from oracle import solve as O
+
+pytestmark = pytest.mark.gpu
+
+amg = pytest.importorskip("paper_2102_07417_b200")
+
+
+@pytest.fixture(scope="module")
+def cases():
+    return {}
+
+
+def _dh(name, cases, **opts):
+    key = (name, tuple(sorted(opts.items())))
+    if key not in cases:
+        c = load_case(name)
+        cases[key] = (c, amg.DeviceHierarchy.from_reference(c["h"], options=opts or None))
+    return cases[key]
+
+
+@pytest.mark.parametrize("name", HIER_CASES)
+def test_spmv_every_matrix_bit_identical(name, cases):
+    c, dh = _dh(name, cases)
+    for k, slot, m in matrices_of(c["h"]):
+        x = c["vec"][f"spmv_L{k}_{slot}_x"]
+        got = dh.matrix(k, slot)(x)
+        np.testing.assert_array_equal(got, c["vec"][f"spmv_L{k}_{slot}_y"], err_msg=f"L{k}.{slot}")
+
+
+@pytest.mark.parametrize("name", SPMV_CASES)
+@pytest.mark.parametrize("lanes", [0, 1, 2, 4, 8])
+def test_spmv_ragged_rows_bit_identical(name, lanes):
+    m, x, y = load_spmv_case(name)
+    dh = amg.DeviceHierarchy.from_matrices([m], options={"lanes": lanes})
+    np.testing.assert_array_equal(dh.matrix(0, "a")(x), y)
+    dh.close()
+
+
+@pytest.mark.parametrize("opts", [{"tile_nnz": 64, "tile_rows": 32, "stages": 1},
+                                  {"tile_nnz": 300, "tile_rows": 64, "stages": 2},
+                                  {"tile_nnz": 4096, "tile_rows": 512, "stages": 2}])
+def test_spmv_tile_geometry_does_not_change_bits(opts):
+    m, x, y = load_spmv_case("spmv_ragged")
+    dh = amg.DeviceHierarchy.from_matrices([m], options=opts)
+    np.testing.assert_array_equal(dh.matrix(0, "a")(x), y)
+    dh.close()
+
+
+@pytest.mark.parametrize("name", [n for n in HIER_CASES if n != "poisson1d_50_single"])
+def test_smoother_sweeps_bit_identical(name, cases):
+    c, dh = _dh(name, cases)
+    v = c["vec"]
+    for k in range(c["h"].n_levels - 1):
+        b, x0 = v[f"smooth_L{k}_b"], v[f"smooth_L{k}_x0"]
+        for steps in (1, 2):
+            np.testing.assert_array_equal(dh.apply_smoother(k, b, None, steps), v[f"smooth_L{k}_zero_{steps}"])
+            np.testing.assert_array_equal(dh.apply_smoother(k, b, x0, steps), v[f"smooth_L{k}_x0_{steps}"])
+
+
+@pytest.mark.parametrize("name", HIER_CASES)
+def test_coarse_solve_and_vcycle(name, cases):
+    c, dh = _dh(name, cases)
+    v = c["vec"]
+    assert _relerr(dh.coarse_solve(v["coarse_y"]), v["coarse_z"]) <= 1e-12
+    z = dh.vcycle(v["y"])
+    assert _relerr(z, v["vcycle_z"]) <= 1e-12
+    # and against the oracle on a fresh input
+    y2 = np.random.default_rng(99).uniform(-1, 1, v["y"].size)
+    assert _relerr(dh.vcycle(y2), O.vcycle(c["h"], y2)) <= 1e-12
+
+
+@pytest.mark.parametrize("name", [n for n in HIER_CASES if "twogrid" not in n and "lu" not in n])
+def test_pcg_matches_reference(name, cases):
+    c, dh = _dh(name, cases)
+    exp = c["expect"]["pcg"]
+    res = amg.pcg(dh.A0, c["b"], apply_m=dh.vcycle,
+                  config=amg.KrylovConfig(rtol=exp["rtol"], max_iters=exp["max_iters"], record_history=True))
+    assert res.converged == exp["converged"]
+    assert abs(res.n_iterations - exp["n_iterations"]) <= 1
+    assert res.relres <= exp["rtol"]
+    assert len(res.history) == res.n_iterations + 1
+    assert [i for i, _ in res.history] == list(range(res.n_iterations + 1))
+    assert res.history[0][1] == pytest.approx(1.0, rel=1e-14)
+    m = min(len(res.history), len(exp["history"]))
+    np.testing.assert_allclose([r for _, r in res.history[:m]], exp["history"][:m], rtol=1e-6)
+    assert _relerr(res.x, c["vec"]["pcg_x"]) <= 1e-8
+    true = np.linalg.norm(c["b"] - O.spmv(c["h"].levels[0].a, res.x)) / np.linalg.norm(c["b"])
+    assert res.relres == pytest.approx(true, rel=1e-6)
+
+
+def test_pcg_is_bitwise_deterministic(cases):
+    c, dh = _dh("poisson7_12", cases)
+    cfg = amg.KrylovConfig(rtol=1e-10, record_history=True)
+    r1 = amg.pcg(dh.A0, c["b"], apply_m=dh.vcycle, config=cfg)
+    r2 = amg.pcg(dh.A0, c["b"], apply_m=dh.vcycle, config=cfg)
+    np.testing.assert_array_equal(r1.x, r2.x)
+    assert r1.history == r2.history
+
+
+def test_pcg_edge_cases(cases):
+    c, dh = _dh("poisson7_12", cases)
+    n = c["b"].size
+    z = amg.pcg(dh.A0, np.zeros(n), apply_m=dh.vcycle)
+    assert z.converged and z.n_iterations == 0 and z.relres == 0.0 and not z.x.any()
+    xs = np.random.default_rng(3).standard_normal(n)
+    r = amg.pcg(dh.A0, O.spmv(c["h"].levels[0].a, xs), apply_m=dh.vcycle, x0=xs)
+    assert r.converged and r.n_iterations == 0
+    r = amg.pcg(dh.A0, c["b"], apply_m=dh.vcycle, config=amg.KrylovConfig(rtol=1e-14, max_iters=3))
+    assert not r.converged and r.n_iterations == 3 and r.relres > 1e-14
+    r = amg.pcg(dh.A0, c["b"], apply_m=dh.vcycle, config=amg.KrylovConfig(rtol=1e-10, recompute_every=1))
+    assert r.converged
+    assert np.linalg.norm(c["b"] - O.spmv(c["h"].levels[0].a, r.x)) <= 1e-10 * np.linalg.norm(c["b"])
+    ref = O.pcg(lambda v: O.spmv(c["h"].levels[0].a, v), c["b"], apply_m=lambda q: O.vcycle(c["h"], q),
+                config=O.KrylovConfig(rtol=1e-10, recompute_every=1))
+    assert abs(r.n_iterations - ref.n_iterations) <= 1
+
+
+def test_pcg_not_spd_raises_curvature():
+    c = load_case("poisson7_12")
+    h = c["h"]
+    a = h.levels[0].a
+    neg = type(a)(a.nrows, a.ncols, a.row_offsets, a.col_indices, -a.values)
+    h.levels[0].a = neg
+    dh = amg.DeviceHierarchy.from_reference(h)
+    with pytest.raises(amg.NotSpdError, match="curvature"):
+        amg.pcg(dh.A0, c["b"], apply_m=dh.vcycle)
+    dh.close()
+
+
+def test_dimension_mismatch(cases):
+    c, dh = _dh("poisson7_12", cases)
+    with pytest.raises(amg.DimensionMismatchError):
+        dh.A0(np.zeros(c["b"].size + 1))
+    with pytest.raises(TypeError):
+        amg.pcg(lambda v: v, c["b"], apply_m=dh.vcycle)
+
+
+@pytest.mark.parametrize("name", ["poisson1d_8_twogrid_jacobi", "poisson1d_8_twogrid_nu20",
+                                  "poisson1d_8_twogrid_fsai"])
+def test_two_grid_error_operator_matches_dense_oracle(name, cases):
+    # test_hierarchy.py:69-117: e - vcycle(A e) == S^nu2 (I - P Ac^-1 P^T A) S^nu1 e
+    c, dh = _dh(name, cases)
+    h = c["h"]
+    lv = h.levels[0]
+    a = _dense(lv.a)
+    p = _dense(lv.p)
+    ac = _dense(h.levels[1].a)
+    sm = lv.smoother
+    minv = np.diag(sm.inv_diag) if sm.kind == "jacobi" else _dense(sm.gmat).T @ _dense(sm.gmat)
+    s = np.eye(a.shape[0]) - sm.omega * minv @ a
+    cgc = np.eye(a.shape[0]) - p @ np.linalg.solve(ac, p.T @ a)
+    e_dense = np.linalg.matrix_power(s, h.config.nu2) @ cgc @ np.linalg.matrix_power(s, h.config.nu1)
+    rng = np.random.default_rng(47)
+    for _ in range(20):
+        e = rng.standard_normal(a.shape[0])
+        got = e - dh.vcycle(dh.A0(e))
+        assert _relerr(got, e_dense @ e) <= 1e-12
+
+
+def test_vcycle_linear_and_symmetric(cases):
+    c, dh = _dh("poisson2d_16_jacobi", cases)
+    rng = np.random.default_rng(5)
+    n = c["b"].size
+    y1, y2 = rng.standard_normal(n), rng.standard_normal(n)
+    np.testing.assert_allclose(dh.vcycle(2.0 * y1 - 3.0 * y2), 2.0 * dh.vcycle(y1) - 3.0 * dh.vcycle(y2),
+                               rtol=1e-11, atol=1e-13)
+    bx, by = dh.vcycle(y1), dh.vcycle(y2)
+    assert abs(bx @ y2 - y1 @ by) < 1e-10 * np.linalg.norm(bx) * np.linalg.norm(y2)
+
+
+def test_torch_device_vectors(cases):
+    torch = pytest.importorskip("torch")
+    c, dh = _dh("poisson7_12", cases)
+    y = torch.tensor(c["y"], device="cuda")
+    z = dh.vcycle(y)
+    assert z.is_cuda
+    assert _relerr(z.cpu().numpy(), c["vec"]["vcycle_z"]) <= 1e-12
+    b = torch.tensor(c["b"], device="cuda")
+    r = amg.pcg(dh.A0, b, apply_m=dh.vcycle)
+    assert r.converged and r.x.is_cuda
+
+
+def _dense(m):
+    d = np.zeros((m.nrows, m.ncols))
+    rows = np.repeat(np.arange(m.nrows), np.diff(m.row_offsets))
+    d[rows, m.col_indices] = m.values
+    return d

@@ -1,0 +1,76 @@
+"""Hierarchy cache: compact form rebuilds the reference's hierarchy bit for bit;
+bench generators match the reference generators."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import have_reference
+from golden_io import load_case
+from paper_2102_07417_b200 import hiercache, problems
+
+
+def _eq(a, b):
+    return (a.nrows == b.nrows and a.ncols == b.ncols and np.array_equal(a.row_offsets, b.row_offsets)
+            and np.array_equal(a.col_indices, b.col_indices) and np.array_equal(a.values, b.values))
+
+
+def test_full_roundtrip(tmp_path):
+    c = load_case("poisson7_12")
+    h = c["h"]
+    hiercache.save_hierarchy(h, str(tmp_path / "h"), mode="full")
+    h2 = hiercache.load_hierarchy(str(tmp_path / "h"))
+    for l1, l2 in zip(h.levels, h2.levels):
+        assert _eq(l1.a, l2.a)
+    np.testing.assert_array_equal(h.factor[0], h2.factor[0])
+
+
+def test_compact_rebuild_matches_digests(tmp_path):
+    # the rebuilt A_{k+1} = galerkin(A_k, P_k), P^T, G^T must equal what the reference stored
+    c = load_case("poisson7_12")
+    h = c["h"]
+    a0 = problems.poisson7(12, 12, 12)
+    assert _eq(a0, h.levels[0].a)
+    for k in range(h.n_levels - 1):
+        lv = h.levels[k]
+        assert _eq(hiercache.galerkin_product(lv.a, lv.p, True), h.levels[k + 1].a)
+        assert _eq(hiercache.transpose(lv.p), lv.pt)
+        assert _eq(hiercache.transpose(lv.smoother.gmat), lv.smoother.gmat_t)
+
+
+def test_digest_mismatch_is_loud(tmp_path):
+    c = load_case("poisson7_12")
+    d = str(tmp_path / "h")
+    hiercache.save_hierarchy(c["h"], d, mode="full")
+    z = dict(np.load(os.path.join(d, "L0_a.npz")))
+    z["values"] = z["values"].copy()
+    z["values"][0] += 1.0
+    np.savez(os.path.join(d, "L0_a.npz"), **z)
+    with pytest.raises(ValueError, match="digest"):
+        hiercache.load_hierarchy(d)
+
+
+@pytest.mark.skipif(not have_reference(), reason="reference package only in the build container")
+def test_generators_match_reference():
+    from amgkit.problems import gen_poisson7, gen_rotated_anisotropy
+    from amgkit import SparseMatrix
+
+    assert _eq(problems.poisson7(5, 6, 7), gen_poisson7(5, 6, 7))
+    assert _eq(problems.rtanis7(6, 5, 7, 1.0, 1.0, 1e-3), gen_rotated_anisotropy(6, 5, 7, theta=0, kx=1, ky=1, kz=1e-3))
+    a = problems.hetero27(6, 5, 7, sigma=2.0, seed=3)
+    rows = np.repeat(np.arange(a.nrows), np.diff(a.row_offsets))
+    b = SparseMatrix.from_coo(rows, a.col_indices, a.values, a.shape)
+    assert _eq(a, b)
+    assert a.nnz == (3 * 6 - 2) * (3 * 5 - 2) * (3 * 7 - 2)
+
+
+def test_hetero27_sizes_and_symmetry():
+    a = problems.hetero27(7, 6, 5, sigma=2.0, seed=1)
+    assert a.nnz == 19 * 16 * 13
+    rows = np.repeat(np.arange(a.nrows), np.diff(a.row_offsets))
+    d = np.zeros((a.nrows, a.nrows))
+    d[rows, a.col_indices] = a.values
+    assert np.array_equal(d, d.T)
+    assert np.linalg.eigvalsh(d).min() > 0
+    blk = problems.conductivity(8, 8, 8, 3.0, 42, block=4)
+    assert np.unique(blk).size == 8
