@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""PCG + AMG solve-phase benchmark (BASELINE.json metric: solve ms/iter,
+GFLOP/s and HBM-roofline fraction on B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl amgb200|reference]
+
+Workload (``config.workload``): BASELINE configs[1] -- 3-D heterogeneous
+diffusion, 27-point stencil on 128^3 (2,097,152 unknowns, 55,742,968 nnz),
+lognormal sigma=2 conductivity, rhs uniform(-1,1) seed 42, classical AMG +
+FSAI from the reference's setup (frozen in hier_cache/),
+PCG to rtol 1e-8.  A step = one complete PCG solve from x0 = 0 (initial
+residual, every iteration, final true residual) with b already resident in
+HBM; ``value`` = device time of the K solves / total iterations (ms per PCG
+iteration; lower is better).  ``e2e`` = the same through the public API with
+pinned host b / x (H2D + D2H inside the timed region).
+
+``--impl reference``: the reference's solve path on the host CPU (the numpy
+oracle that restates it bit for bit; the reference package itself cannot
+travel to the GPU box), same hierarchy and RHS; a step = one PCG iteration.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+DEFAULT_CONFIG = "c2_hetero27_128"
+METRIC = "PCG+AMG solve ms/iter (GFLOP/s, HBM-roofline fraction alongside)"
+WORKLOADS = {
+    "c1_poisson7_64": "config 1: 3-D Poisson 7-pt 64^3 (262,144 unknowns), FSAI + classical AMG, PCG 1e-8",
+    "c2_hetero27_128": ("config 2: 3-D heterogeneous diffusion 27-pt 128^3 (2,097,152 unknowns, 55.7 M nnz), "
+                        "lognormal sigma=2, FSAI + classical AMG, PCG 1e-8"),
+    "c4_rtanis7_256": "config 4: anisotropic Poisson 7-pt 256^3 eps=1e-3 (16.8 M unknowns), PCG 1e-8",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="amgb200", choices=("amgb200", "reference"))
+    ap.add_argument("--config", default=os.environ.get("AMGB200_BENCH_CONFIG", DEFAULT_CONFIG))
+    ap.add_argument("--cache", default=os.path.join(ROOT, "hier_cache"))
+    ap.add_argument("--cpu-iters", type=int, default=2, help="PCG iterations in the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons through NVML during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, device):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.hd = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.hd, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.hd, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.hd))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def report(self):
+        if self.nv is None or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"], "samples": 0}
+        names = [k for k, v in self.REASONS.items() if self.reasons & v and k != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(config):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(config, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def load(args):
+    from paper_2102_07417_b200 import hiercache, problems
+
+    d = os.path.join(args.cache, args.config)
+    if not os.path.exists(os.path.join(d, "manifest.json")):
+        raise SystemExit(f"bench: hierarchy cache {d} missing (run tools/export_hierarchy.py {args.config})")
+    h = hiercache.load_hierarchy(d, verify=True)
+    b = problems.rhs_uniform(h.levels[0].a.nrows, 42)
+    return h, b
+
+
+def cpu_sample(h, b, iters):
+    """The oracle (reference restatement) on the host: ms per PCG iteration over `iters` iterations."""
+    from oracle import solve as O
+
+    a0 = h.levels[0].a
+    marks = []
+    O.pcg(lambda v: O.spmv(a0, v), b, apply_m=lambda r: O.vcycle(h, r),
+          config=O.KrylovConfig(rtol=1e-8), max_steps=iters, iter_marks=marks)
+    dt = np.diff(marks) * 1e3
+    return [float(x) for x in dt]
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    h, b = load(args)
+    steps, warm = args.steps, args.warmup
+    dts = cpu_sample(h, b, warm + steps)
+    timed = dts[warm:warm + steps]
+    ms = float(np.mean(timed))
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": ms, "unit": "ms/iter", "n_gpus": world, "steps": steps, "warmup": warm,
+        "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator + reference setup hierarchy)",
+        "config": {"workload": WORKLOADS.get(args.config, args.config), "name": args.config,
+                   "step": "one PCG iteration (SpMV A0, V-cycle, 3 dots, 3 axpys) of the reference path"},
+        "cpu_baseline": {"value": ms, "unit": "ms/iter", "cores": 1, "kind": "port",
+                         "sample": f"{steps} PCG iterations after {warm} warm-up iterations, numpy oracle "
+                                   "(bit-identical restatement of amgkit's solve path), single-threaded numpy"},
+        "e2e": {"value": ms, "unit": "ms/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "host_cpu": _cpu_model(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_amgb200(args):
+    import torch
+
+    import paper_2102_07417_b200 as amg
+    from paper_2102_07417_b200.device import model_bytes_flops
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist = None
+    torch.cuda.set_device(local)
+    h, b_host = load(args)
+    n = b_host.size
+    dh = amg.DeviceHierarchy.from_reference(h, device=local)
+    b_dev = torch.tensor(b_host, device=f"cuda:{local}")
+    cfg = amg.KrylovConfig(rtol=1e-8, max_iters=5000)
+    bytes_iter, flops_iter = model_bytes_flops(h)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 0)):
+        res = amg.pcg(dh.A0, b_dev, apply_m=dh.vcycle, config=cfg)
+    barrier()
+    solve_ms, iters, launches = [], [], 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            res = amg.pcg(dh.A0, b_dev, apply_m=dh.vcycle, config=cfg)
+            st = dh.stats()
+            solve_ms.append(st["solve_ms"])
+            iters.append(res.n_iterations)
+            launches += st["launches_last"]
+    barrier()
+    tot_ms = float(sum(solve_ms))
+    tot_it = int(sum(iters))
+    ms_iter = tot_ms / max(tot_it, 1)
+    if dist is not None:
+        t = torch.tensor([ms_iter], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_iter = float(t.item())
+    # parity record of this run
+    from oracle import solve as O  # checker only: true residual of the device answer
+    x = res.x.cpu().numpy()
+    true_rel = float(np.linalg.norm(b_host - O.spmv(h.levels[0].a, x)) / np.linalg.norm(b_host))
+    ref_its = h.meta.get("extra", {}).get("reference_solve", {}).get("n_iterations")
+
+    # e2e: public API with pinned host buffers, copies inside the timed region
+    b_pin = torch.from_numpy(b_host).pin_memory()
+    amg.pcg(dh.A0, b_pin, apply_m=dh.vcycle, config=cfg)
+    barrier()
+    t0 = time.perf_counter()
+    e_it = 0
+    for _ in range(args.steps):
+        r2 = amg.pcg(dh.A0, b_pin, apply_m=dh.vcycle, config=cfg)
+        e_it += r2.n_iterations
+    torch.cuda.synchronize()
+    e2e_ms_iter = (time.perf_counter() - t0) * 1e3 / max(e_it, 1)
+
+    # dominant kernel: SpMV on A0 (tile kernel), timed alone with CUDA events on the library stream
+    a0 = h.levels[0].a
+    k_ms = dh.time_spmv(0, "a", reps=50)
+    k_bytes = 12 * a0.nnz + 4 * (a0.nrows + 1) + 8 * a0.ncols + 8 * a0.nrows
+    peak, peak_src = peaks()
+    achieved = k_bytes / (k_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC,
+        "value": ms_iter,
+        "unit": "ms/iter",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": tot_ms / max(args.steps, 1),
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded generator + reference setup hierarchy)",
+        "config": {
+            "workload": WORKLOADS.get(args.config, args.config),
+            "name": args.config,
+            "parallelism": "1 GPU" if world == 1 else f"replicas x{world} (row-partitioned path: DESIGN.md)",
+            "step": "one PCG solve to rtol 1e-8 from x0=0, b resident in HBM",
+            "l2": "inputs larger than L2 (hierarchy + vectors > 1 GB, per-iteration traffic >> 126 MB)",
+            "levels": [int(l.a.nrows) for l in h.levels],
+        },
+        "iterations": iters[-1] if iters else None,
+        "reference_iterations": ref_its,
+        "final_true_relres": true_rel,
+        "gflops": flops_iter / (ms_iter * 1e-3) / 1e9,
+        "iteration_roofline": {
+            "bytes_per_iter": bytes_iter, "achieved_gbs": bytes_iter / (ms_iter * 1e-3) / 1e9, "peak": peak,
+            "frac": bytes_iter / (ms_iter * 1e-3) / 1e9 / peak,
+        },
+        "roofline": {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": ncu_traffic(args.config), "kernel": "spmv_tiles on A0 (plain epilogue)",
+            "bytes_per_launch": k_bytes, "ms_per_launch": k_ms, "peak_source": peak_src,
+        },
+        "e2e": {"value": e2e_ms_iter, "unit": "ms/iter", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
+        "gpu_launches": int(launches),
+        "graph_mode": dh.stats()["graph_mode"],
+        "clocks": clk.report(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        dts = cpu_sample(h, b_host, args.cpu_iters)
+        line["cpu_baseline"] = {
+            "value": float(np.mean(dts)), "unit": "ms/iter", "cores": 1, "kind": "port",
+            "sample": f"{len(dts)} PCG iterations of the same workload (numpy oracle, bit-identical restatement "
+                      "of the reference path), single-threaded",
+            "host_cpu": _cpu_model(),
+        }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dh.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_amgb200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -118,6 +118,10 @@ int amg_pcg(amg_t *h, const double *b, const double *x0, double rtol, int max_it
             double *history, int *hist_len, double *curvature_at_fail, int on_device);
 
 int amg_get_stats(amg_t *h, amg_stats_t *out);
+/* Diagnostics: launch the SpMV kernel of matrix `which` `reps` times back to
+ * back on the handle's stream between CUDA events (operands resident in
+ * HBM); *ms_per_launch = average device time of one launch. */
+int amg_time_spmv(amg_t *h, int level, int which, int reps, double *ms_per_launch);
 /* Tuning / diagnostics: 0 = auto. */
 int amg_set_option(amg_t *h, const char *key, int64_t value);
 

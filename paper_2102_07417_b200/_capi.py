@@ -24,7 +24,7 @@ EXPORTS = (
     "amg_create", "amg_destroy", "amg_last_error", "amg_get_version", "amg_set_levels",
     "amg_set_partition", "amg_upload_matrix", "amg_set_smoother", "amg_upload_coarse",
     "amg_set_cycle", "amg_finalize", "amg_local_rows", "amg_spmv", "amg_smoother",
-    "amg_coarse_solve", "amg_vcycle", "amg_pcg", "amg_get_stats", "amg_set_option",
+    "amg_coarse_solve", "amg_vcycle", "amg_pcg", "amg_get_stats", "amg_set_option", "amg_time_spmv",
 )
 
 
@@ -80,6 +80,7 @@ def lib():
         "amg_pcg": (I32, [P, P, P, D, I32, I32, P, P, P, P, P, P, P, I32]),
         "amg_get_stats": (I32, [P, ctypes.POINTER(Stats)]),
         "amg_set_option": (I32, [P, ctypes.c_char_p, I64]),
+        "amg_time_spmv": (I32, [P, I32, I32, I32, ctypes.POINTER(D)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -976,6 +976,25 @@ int amg_pcg(amg_t *h, const double *b, const double *x0, double rtol, int max_it
     return AMG_OK;
 }
 
+int amg_time_spmv(amg_t *h, int level, int which, int reps, double *ms_per_launch)
+{
+    TRY(check_final(h));
+    if (level < 0 || level >= (int)h->lv.size() || which < 0 || which > 4 || reps < 1 || !ms_per_launch)
+        return fail(AMG_E_ARG, "amg_time_spmv: bad arguments");
+    const DevMat &M = h->lv[level].m[which];
+    if (!M.present) return fail(AMG_E_ARG, "amg_time_spmv: matrix slot is empty");
+    TRY(launch_spmv(h, M, h->tmp_in, h->tmp_out, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, nullptr, nullptr));
+    CK(cudaEventRecord(h->ev0, h->stream));
+    for (int i = 0; i < reps; ++i)
+        TRY(launch_spmv(h, M, h->tmp_in, h->tmp_out, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, nullptr, nullptr));
+    CK(cudaEventRecord(h->ev1, h->stream));
+    TRY(sync_stream(h));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    *ms_per_launch = ms / reps;
+    return AMG_OK;
+}
+
 int amg_get_stats(amg_t *h, amg_stats_t *out)
 {
     if (!h || !out) return fail(AMG_E_ARG, "amg_get_stats: NULL argument");

@@ -237,34 +237,73 @@ __device__ __forceinline__ void grid_finalize(double v, double *partials, unsign
 
 // ---------------------------------------------------------------- SpMV
 
-// Recursive numpy pairwise sum (n > 128) over products read through `P`.
+// numpy's pairwise sum over products read through `P` (leaf: n <= 128).
 template <class PF>
-__device__ double pairwise_rec(const PF &P, int base, int n)
+__device__ __forceinline__ double pairwise_leaf(const PF &P, int base, int n)
 {
     if (n < 8) {
         double r = 0.0;
         for (int i = 0; i < n; ++i) r = add(r, P(base + i));
         return r;
     }
-    if (n <= 128) {
-        double r[8];
+    double r[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = P(base + j);
-        int i = 8;
-        const int main = n - (n % 8);
-        for (; i < main; i += 8) {
+    for (int j = 0; j < 8; ++j) r[j] = P(base + j);
+    int i = 8;
+    const int main = n - (n % 8);
+    for (; i < main; i += 8) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] = add(r[j], P(base + i + j));
-        }
-        double res = add(add(add(r[0], r[1]), add(r[2], r[3])), add(add(r[4], r[5]), add(r[6], r[7])));
-        for (; i < n; ++i) res = add(res, P(base + i));
-        return res;
+        for (int j = 0; j < 8; ++j) r[j] = add(r[j], P(base + i + j));
     }
+    double res = add(add(add(r[0], r[1]), add(r[2], r[3])), add(add(r[4], r[5]), add(r[6], r[7])));
+    for (; i < n; ++i) res = add(res, P(base + i));
+    return res;
+}
+
+__device__ __forceinline__ int pairwise_split(int n)
+{
     int n2 = n / 2;
-    n2 -= n2 % 8;
-    double a = pairwise_rec(P, base, n2);
-    double b = pairwise_rec(P, base + n2, n - n2);
-    return add(a, b);
+    return n2 - n2 % 8;
+}
+
+// Full pairwise sum with numpy's recursive split (n > 128 -> halves at
+// n/2 - (n/2) % 8), evaluated with an explicit stack (no device recursion).
+template <class PF>
+__device__ __noinline__ double pairwise_sum(const PF &P, int base, int n)
+{
+    if (n <= 128) return pairwise_leaf(P, base, n);
+    int fb[32], fn[32];
+    double fl[32];
+    int fs[32];
+    int sp = 0;
+    int b = base, m = n;
+    double ret;
+    for (;;) {
+        while (m > 128) {  // descend to the left child
+            fb[sp] = b;
+            fn[sp] = m;
+            fs[sp] = 0;
+            ++sp;
+            m = pairwise_split(m);
+        }
+        ret = pairwise_leaf(P, b, m);
+        bool descend = false;
+        while (sp > 0) {
+            const int t = sp - 1;
+            if (fs[t] == 0) {  // left done: evaluate the right child
+                fl[t] = ret;
+                fs[t] = 1;
+                const int n2 = pairwise_split(fn[t]);
+                b = fb[t] + n2;
+                m = fn[t] - n2;
+                descend = true;
+                break;
+            }
+            ret = add(fl[t], ret);
+            --sp;
+        }
+        if (!descend) return ret;
+    }
 }
 
 // Row sum in numpy order for one row whose entries sit at smem positions
@@ -289,7 +328,7 @@ __device__ __forceinline__ double row_sum_staged(const double *__restrict__ vs, 
                 res = 0.0;
                 for (int i = 0; i < n; ++i) res = add(res, P(base + i));
             } else {
-                res = pairwise_rec(P, base, n);
+                res = pairwise_sum(P, base, n);
             }
             s = add(p0, res);
         }
@@ -420,7 +459,7 @@ __global__ void __launch_bounds__(TILE_THREADS) spmv_tiles(const SpmvArgs a)
             if (threadIdx.x == 0) {
                 const int lo = a.off[d.r0], hi = a.off[d.r0 + 1];
                 auto P = [&](int k) -> double { return prod(a.val[k], __ldg(a.x + a.col[k])); };
-                double sum = add(P(lo), pairwise_rec(P, lo + 1, hi - lo - 1));
+                double sum = add(P(lo), pairwise_sum(P, lo + 1, hi - lo - 1));
                 double yv = epilogue<EPI>(sum, a.b, d.r0, a.omega);
                 a.y[d.r0] = yv;
                 if (want_dot) dacc = fma(yv, a.dotw[d.r0], dacc);

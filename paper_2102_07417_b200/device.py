@@ -176,6 +176,12 @@ class DeviceHierarchy:
             if x.shape[0] != n:
                 raise DimensionMismatchError(op, shape, tuple(x.shape))
             return x, 1
+        if hasattr(x, "is_pinned") and x.is_pinned():  # pinned host tensor: async H2D / D2H
+            if x.dtype.itemsize != 8 or not x.is_contiguous() or x.dim() != 1 or not x.is_floating_point():
+                raise AmgError(f"{op}: pinned host vectors must be contiguous 1-D float64 tensors")
+            if x.shape[0] != n:
+                raise DimensionMismatchError(op, shape, tuple(x.shape))
+            return x, 0
         a = _host_f64(x)
         if a.ndim != 1:
             raise AmgError(f"{op}: only 1-D vectors are supported on the device path")
@@ -188,6 +194,10 @@ class DeviceHierarchy:
             import torch
 
             return torch.empty(n, dtype=torch.float64, device=like.device)
+        if hasattr(like, "is_pinned") and like.is_pinned():
+            import torch
+
+            return torch.empty(n, dtype=torch.float64, pin_memory=True)
         return np.empty(n, dtype=np.float64)
 
     def spmv(self, level, slot, x):
@@ -224,6 +234,12 @@ class DeviceHierarchy:
         z = self._vec_out(yin, n)
         C.check(C.lib().amg_vcycle(self._h, C.ptr(yin), C.ptr(z), dev), "vcycle")
         return z
+
+    def time_spmv(self, level, slot, reps=20):
+        """Average device ms of one SpMV launch (CUDA events on the library stream)."""
+        ms = C.D(0.0)
+        C.check(C.lib().amg_time_spmv(self._h, level, C.SLOT[slot], int(reps), ctypes.byref(ms)), "time_spmv")
+        return ms.value
 
     def set_option(self, key, value):
         C.check(C.lib().amg_set_option(self._h, key.encode(), int(value)), f"option {key}")
