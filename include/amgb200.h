@@ -70,6 +70,8 @@ typedef struct amg_stats {
     int64_t flops_per_iter;   /* algorithmic flops per PCG iteration */
     int graph_mode;           /* 2 = device while-loop graph, 1 = batched graph launches, 0 = eager */
     int n_levels;
+    int tail_level;           /* first level run by the cluster tail kernel (0 = none) */
+    int cluster;              /* CTAs in the tail cluster */
 } amg_stats_t;
 
 /* Handle for one GPU.  nccl_unique_id: 128 bytes (NULL when nranks == 1). */

@@ -38,6 +38,8 @@ class Stats(ctypes.Structure):
         ("flops_per_iter", ctypes.c_int64),
         ("graph_mode", ctypes.c_int),
         ("n_levels", ctypes.c_int),
+        ("tail_level", ctypes.c_int),
+        ("cluster", ctypes.c_int),
     ]
 
 

@@ -17,6 +17,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -96,7 +98,7 @@ struct amg_handle {
     int nu1 = 1, nu2 = 1;
     // coarsest factor
     int nc = 0, coarse_kind = AMG_COARSE_CHOLESKY;
-    double *Lp = nullptr, *LU = nullptr;
+    double *Lp = nullptr, *LU = nullptr, *dinv = nullptr;
     int32_t *piv = nullptr;
     int coarse_staged = 0;
     size_t coarse_smem = 0;
@@ -115,6 +117,16 @@ struct amg_handle {
     // options
     int tile_nnz = 2048, tile_rows = 256, stages = 3, ctas_per_sm = 0, force_graph = -1, batch = 8;
     int lanes_override = 0;
+    int pdl = 1;  // programmatic dependent launch between consecutive kernels
+    // cluster tail: levels >= tail_level run inside one cluster kernel
+    int64_t tail_nnz = 400000;
+    int cluster = 16;
+    int tail_level = 0;  // 0 = disabled
+    TailOp *tail_ops = nullptr;
+    int tail_nops = 0;
+    size_t tail_smem = 0;
+    std::vector<TailOp> *collect = nullptr;  // op collection mode (builds the tail)
+    unsigned long long *trace = nullptr;     // AMGB200_TRACE: %globaltimer per tail op
     // graph
     cudaGraphExec_t gexec = nullptr;
     int graph_mode = 0;
@@ -149,16 +161,60 @@ static SpmvFn spmv_fn(int epi, int lanes)
 #undef AMG_L
 }
 
+// Every kernel goes through here: programmatic dependent launch lets a kernel
+// start (stage static matrix tiles) while its predecessor drains.
+template <typename... KArgs, typename... Args>
+static int launch_k(amg_t *h, void (*kern)(KArgs...), int grid, int block, size_t smem, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = h->pdl ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
+    if (e != cudaSuccess) return fail(AMG_E_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e));
+    ++h->launches;
+    return AMG_OK;
+}
+
+// Max-dynamic-smem caps are per-FUNCTION process state: raise them once to
+// the device opt-in maximum so handles with different staging never clash.
+static int raise_smem_caps(int device)
+{
+    static int done_for = -1;
+    if (done_for == device) return AMG_OK;
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    auto cap = [&](const void *f) -> int {
+        cudaFuncAttributes fa;
+        CK(cudaFuncGetAttributes(&fa, f));
+        CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+        return AMG_OK;
+    };
+    for (int e = 0; e <= 4; ++e)
+        for (int l : {1, 2, 4, 8}) TRY(cap((const void *)spmv_fn(e, l)));
+    TRY(cap((const void *)coarse_solve_k));
+    TRY(cap((const void *)tail_vcycle));
+    CK(cudaFuncSetAttribute((const void *)tail_vcycle, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    done_for = device;
+    return AMG_OK;
+}
+
 static int stage_smem(const amg_t *h) { return h->stages * stage_layout(h->tile_nnz, h->tile_rows).stage_bytes; }
 
 static int configure_kernels(amg_t *h, int *blocks_per_sm)
 {
     const int smem = stage_smem(h);
     int best = 1 << 30;
+    TRY(raise_smem_caps(h->device));
     for (int e = 0; e <= 4; ++e)
         for (int l : {1, 2, 4, 8}) {
             SpmvFn f = spmv_fn(e, l);
-            CK(cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             int nb = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, TILE_THREADS, smem));
             best = std::min(best, nb);
@@ -180,6 +236,22 @@ static int exchange(amg_t *h, const DevMat &M, double *x)
 static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, int epi, const double *b, double omega,
                        const double *dotw, int fin, const int *g1, const int *g2)
 {
+    if (h->collect) {
+        if (dotw || fin != FIN_NONE) return fail(AMG_E_STATE, "internal: reduction inside the cluster tail");
+        TailOp o{};
+        o.kind = TAIL_SPMV;
+        o.epi = epi;
+        o.nrows = (int)M.nrows;
+        o.off = M.off;
+        o.col = M.col;
+        o.val = M.val;
+        o.x = x;
+        o.y = y;
+        o.b = b;
+        o.omega = omega;
+        h->collect->push_back(o);
+        return AMG_OK;
+    }
     TRY(exchange(h, M, const_cast<double *>(x)));
     if (M.ntiles == 0) {
         if (fin != FIN_NONE) {
@@ -191,8 +263,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
             v.ctl = h->ctl;
             v.gate1 = g1;
             v.gate2 = g2;
-            vec_dot<<<1, VEC_THREADS, 0, h->stream>>>(v);
-            ++h->launches;
+            TRY(launch_k(h, vec_dot, 1, VEC_THREADS, 0, v));
         }
         return AMG_OK;
     }
@@ -216,9 +287,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     a.ctl = h->ctl;
     a.gate1 = g1;
     a.gate2 = g2;
-    spmv_fn(epi, M.lanes)<<<M.grid, TILE_THREADS, stage_smem(h), h->stream>>>(a);
-    ++h->launches;
-    CK(cudaGetLastError());
+    TRY(launch_k(h, spmv_fn(epi, M.lanes), M.grid, TILE_THREADS, (size_t)stage_smem(h), a));
     return AMG_OK;
 }
 
@@ -247,9 +316,7 @@ static int launch_copy(amg_t *h, double *dst, const double *src, int64_t n, cons
     VecArgs v = vargs(h, n, g1, nullptr);
     v.x = dst;
     v.p = src;
-    vec_copy<<<vec_grid(h, n), VEC_THREADS, 0, h->stream>>>(v);
-    ++h->launches;
-    CK(cudaGetLastError());
+    TRY(launch_k(h, vec_copy, vec_grid(h, n), VEC_THREADS, 0, v));
     return AMG_OK;
 }
 
@@ -259,24 +326,60 @@ static int launch_dot(amg_t *h, const double *a, const double *b, int64_t n, int
     v.p = a;
     v.q = b;
     v.fin = fin;
-    vec_dot<<<vec_grid(h, n), VEC_THREADS, 0, h->stream>>>(v);
-    ++h->launches;
-    CK(cudaGetLastError());
+    TRY(launch_k(h, vec_dot, vec_grid(h, n), VEC_THREADS, 0, v));
     return AMG_OK;
+}
+
+static CoarseArgs coarse_args(const amg_t *h)
+{
+    CoarseArgs c{};
+    c.n = h->nc;
+    c.kind = h->coarse_kind == AMG_COARSE_CHOLESKY ? 0 : 1;
+    c.staged = h->coarse_staged;
+    c.Lp = h->Lp;
+    c.dinv = h->dinv;
+    c.LU = h->LU;
+    c.piv = h->piv;
+    return c;
 }
 
 static int launch_coarse(amg_t *h, const double *y, double *z, const int *g1, int fin, const double *dotw)
 {
-    const int n = h->nc;
-    if (h->coarse_kind == AMG_COARSE_CHOLESKY) {
-        coarse_chol<<<1, COARSE_THREADS, h->coarse_smem, h->stream>>>(n, h->Lp, y, z, h->coarse_staged, g1,
-                                                                       h->partials, h->ticket, fin, h->ctl, dotw);
-    } else {
-        coarse_lu<<<1, COARSE_THREADS, h->coarse_smem, h->stream>>>(n, h->LU, h->piv, y, z, g1, h->partials,
-                                                                     h->ticket, fin, h->ctl, dotw);
+    if (h->collect) {
+        if (dotw || fin != FIN_NONE) return fail(AMG_E_STATE, "internal: reduction inside the cluster tail");
+        TailOp o{};
+        o.kind = TAIL_COARSE;
+        o.nrows = h->nc;
+        o.x = y;
+        o.y = z;
+        h->collect->push_back(o);
+        return AMG_OK;
     }
+    TRY(launch_k(h, coarse_solve_k, 1, COARSE_THREADS, h->coarse_smem, coarse_args(h), y, z, g1, h->partials,
+                 h->ticket, fin, h->ctl, dotw));
+    return AMG_OK;
+}
+
+static int launch_tail(amg_t *h, const int *g1)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)h->cluster);
+    cfg.blockDim = dim3(TAIL_THREADS);
+    cfg.dynamicSmemBytes = h->tail_smem;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)h->cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = h->pdl ? 2 : 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tail_vcycle, (const TailOp *)h->tail_ops, h->tail_nops, coarse_args(h), g1,
+                                       h->trace);
+    if (e != cudaSuccess) return fail(AMG_E_CUDA, std::string("tail launch failed: ") + cudaGetErrorString(e));
     ++h->launches;
-    CK(cudaGetLastError());
     return AMG_OK;
 }
 
@@ -299,6 +402,17 @@ static int enqueue_smooth(amg_t *h, int k, const double *b, double *x, int steps
         if (L.sm_kind == AMG_SMOOTHER_FSAI) {
             TRY(launch_spmv(h, L.m[AMG_G], src, L.t, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, g1, nullptr));
             TRY(launch_spmv(h, L.m[AMG_GT], L.t, x, set ? EPI_SETW : EPI_AXPYW, x, L.omega, dw, f, g1, nullptr));
+        } else if (h->collect) {
+            if (dw) return fail(AMG_E_STATE, "internal: reduction inside the cluster tail");
+            TailOp o{};
+            o.kind = TAIL_JACOBI;
+            o.nrows = (int)L.n;
+            o.mode = set ? 0 : 1;
+            o.x = src;
+            o.y = x;
+            o.d = L.inv_diag;
+            o.omega = L.omega;
+            h->collect->push_back(o);
         } else {
             VecArgs v = vargs(h, L.n, g1, nullptr);
             v.x = x;
@@ -308,9 +422,7 @@ static int enqueue_smooth(amg_t *h, int k, const double *b, double *x, int steps
             v.mode = set ? 0 : 1;
             v.q = dw;
             v.fin = dw ? f : FIN_NONE;
-            jacobi_sweep<<<vec_grid(h, L.n), VEC_THREADS, 0, h->stream>>>(v);
-            ++h->launches;
-            CK(cudaGetLastError());
+            TRY(launch_k(h, jacobi_sweep, vec_grid(h, L.n), VEC_THREADS, 0, v));
         }
     }
     return AMG_OK;
@@ -321,6 +433,7 @@ static int enqueue_smooth(amg_t *h, int k, const double *b, double *x, int steps
 static int enqueue_vcycle(amg_t *h, int k, const double *y, double *x, const int *g1, int fin, const double *dotw)
 {
     const int nl = (int)h->lv.size();
+    if (!h->collect && h->tail_level > 0 && k == h->tail_level) return launch_tail(h, g1);
     if (k == nl - 1) return launch_coarse(h, y, x, g1, fin, dotw);
     LevelD &L = h->lv[k];
     LevelD &C = h->lv[k + 1];
@@ -356,9 +469,7 @@ static int enqueue_pcg_body(amg_t *h, cudaGraphConditionalHandle handle, int use
         v.p = h->p;
         v.q = h->q;
         v.fin = FIN_UPDATE;
-        pcg_update<<<vec_grid(h, n), VEC_THREADS, 0, h->stream>>>(v);
-        ++h->launches;
-        CK(cudaGetLastError());
+        TRY(launch_k(h, pcg_update, vec_grid(h, n), VEC_THREADS, 0, v));
     }
     // every recompute_every iterations: r = b - A x     (:76-77)
     TRY(launch_spmv(h, A, h->x, h->r, EPI_RESID, h->b, 0.0, h->r, FIN_RECOMPUTE, act, &h->ctl->do_recompute));
@@ -374,13 +485,9 @@ static int enqueue_pcg_body(amg_t *h, cudaGraphConditionalHandle handle, int use
         VecArgs v = vargs(h, n, act, nullptr);
         v.x = h->p;
         v.p = h->z;
-        pcg_xpay<<<vec_grid(h, n), VEC_THREADS, 0, h->stream>>>(v);
-        ++h->launches;
-        CK(cudaGetLastError());
+        TRY(launch_k(h, pcg_xpay, vec_grid(h, n), VEC_THREADS, 0, v));
     }
-    pcg_continue<<<1, 1, 0, h->stream>>>(h->ctl, handle, use_handle);
-    ++h->launches;
-    CK(cudaGetLastError());
+    TRY(launch_k(h, pcg_continue, 1, 1, 0, h->ctl, handle, use_handle));
     return AMG_OK;
 }
 
@@ -446,6 +553,57 @@ static int build_graph(amg_t *h)
     return AMG_OK;
 }
 
+// Choose the first level (>= 1) whose operator has at most tail_nnz stored
+// entries (and every deeper level too), collect the ops of the V-cycle from
+// there down, and upload them for the cluster tail kernel.
+static int build_tail(amg_t *h)
+{
+    const int nl = (int)h->lv.size();
+    h->tail_level = 0;
+    if (h->tail_nnz <= 0 || nl < 2 || h->nranks > 1) return AMG_OK;
+    int kt = 0;
+    for (int k = nl - 1; k >= 1; --k) {
+        if (h->lv[k].m[AMG_A].nnz <= h->tail_nnz) kt = k;
+        else break;
+    }
+    if (kt == 0) return AMG_OK;
+    std::vector<TailOp> ops;
+    h->collect = &ops;
+    int st = enqueue_vcycle(h, kt, h->lv[kt].y, h->lv[kt].x, nullptr, FIN_NONE, nullptr);
+    h->collect = nullptr;
+    if (st != AMG_OK) return st;
+    size_t smem = (size_t)((h->nc + 1) & ~1) * sizeof(double);
+    if (h->coarse_kind == AMG_COARSE_CHOLESKY && h->coarse_staged) smem = h->coarse_smem;
+    TRY(raise_smem_caps(h->device));
+    // verify the cluster shape can be resident; fall back to smaller clusters
+    for (;;) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)h->cluster);
+        cfg.blockDim = dim3(TAIL_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)h->cluster;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, (const void *)tail_vcycle, &cfg);
+        if (e == cudaSuccess && nclusters >= 1) break;
+        cudaGetLastError();
+        if (h->cluster <= 1) return fail(AMG_E_CUDA, "cluster tail kernel cannot be made resident");
+        h->cluster /= 2;
+    }
+    TRY(dalloc(&h->tail_ops, ops.size()));
+    CK(cudaMemcpy(h->tail_ops, ops.data(), ops.size() * sizeof(TailOp), cudaMemcpyHostToDevice));
+    h->tail_nops = (int)ops.size();
+    h->tail_smem = std::max<size_t>(smem, 1024);
+    h->tail_level = kt;
+    if (getenv("AMGB200_TRACE")) TRY(dalloc(&h->trace, (size_t)h->tail_nops + 2));
+    return AMG_OK;
+}
+
 // ------------------------------------------------------------------ C ABI
 
 extern "C" {
@@ -501,7 +659,7 @@ void amg_destroy(amg_t *h)
         }
         F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
     }
-    F(h->Lp); F(h->LU); F(h->piv); F(h->partials); F(h->ticket); F(h->ctl);
+    F(h->Lp); F(h->LU); F(h->dinv); F(h->tail_ops); F(h->piv); F(h->partials); F(h->ticket); F(h->ctl);
     F(h->b); F(h->x); F(h->r); F(h->z); F(h->p); F(h->q); F(h->tmp_in); F(h->tmp_out); F(h->hist);
     if (h->ctl_h) cudaFreeHost(h->ctl_h);
     if (h->gexec) cudaGraphExecDestroy(h->gexec);
@@ -518,10 +676,13 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     std::string k(key);
     if (k == "graph") { h->force_graph = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "batch") { h->batch = std::max<int>(1, (int)value); return AMG_OK; }
+    if (k == "pdl") { h->pdl = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (h->finalized) return fail(AMG_E_STATE, "amg_set_option: '" + k + "' must be set before amg_finalize");
     if (k == "tile_nnz") { if (value < 64 || value > 8192) return fail(AMG_E_ARG, "tile_nnz out of range"); h->tile_nnz = (int)value; return AMG_OK; }
     if (k == "tile_rows") { if (value < 32 || value > 1024) return fail(AMG_E_ARG, "tile_rows out of range"); h->tile_rows = (int)value; return AMG_OK; }
     if (k == "stages") { if (value < 1 || value > 8) return fail(AMG_E_ARG, "stages out of range"); h->stages = (int)value; return AMG_OK; }
+    if (k == "tail_nnz") { h->tail_nnz = value; return AMG_OK; }
+    if (k == "cluster") { if (value != 8 && value != 16 && value != 4 && value != 2 && value != 1) return fail(AMG_E_ARG, "cluster must be 1,2,4,8,16"); h->cluster = (int)value; return AMG_OK; }
     if (k == "ctas_per_sm") { h->ctas_per_sm = (int)value; return AMG_OK; }
     if (k == "lanes") { if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8) return fail(AMG_E_ARG, "lanes must be 0,1,2,4,8"); h->lanes_override = (int)value; return AMG_OK; }
     return fail(AMG_E_ARG, "amg_set_option: unknown key '" + k + "'");
@@ -647,8 +808,16 @@ int amg_upload_coarse(amg_t *h, int n, const double *factor, int kind, const int
         std::vector<double> packed((size_t)n * (n + 1) / 2);
         for (int i = 0; i < n; ++i)
             for (int j = 0; j <= i; ++j) packed[(size_t)i * (i + 1) / 2 + j] = factor[(size_t)i * n + j];
+        std::vector<double> dinv(n);
+        for (int i = 0; i < n; ++i) {
+            const double d = factor[(size_t)i * n + i];
+            if (!(d > 0.0)) return fail(AMG_E_ARG, "amg_upload_coarse: Cholesky factor has a non-positive diagonal");
+            dinv[i] = 1.0 / d;
+        }
         TRY(dalloc(&h->Lp, packed.size()));
+        TRY(dalloc(&h->dinv, (size_t)n));
         CK(cudaMemcpy(h->Lp, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->dinv, dinv.data(), n * sizeof(double), cudaMemcpyHostToDevice));
         const size_t vbytes = (size_t)((n + 1) & ~1) * sizeof(double);
         const size_t lbytes = packed.size() * sizeof(double);
         if (vbytes + lbytes <= 200 * 1024) {
@@ -671,10 +840,7 @@ int amg_upload_coarse(amg_t *h, int n, const double *factor, int kind, const int
     } else {
         return fail(AMG_E_ARG, "amg_upload_coarse: bad kind");
     }
-    if (h->coarse_smem > 48 * 1024) {
-        CK(cudaFuncSetAttribute((const void *)coarse_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->coarse_smem));
-        CK(cudaFuncSetAttribute((const void *)coarse_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->coarse_smem));
-    }
+    TRY(raise_smem_caps(h->device));
     return AMG_OK;
 }
 
@@ -781,6 +947,7 @@ int amg_finalize(amg_t *h)
     TRY(dalloc(&h->ctl, 1));
     CK(cudaMallocHost((void **)&h->ctl_h, sizeof(PcgCtl)));
     std::memset(h->ctl_h, 0, sizeof(PcgCtl));
+    if (!container) TRY(build_tail(h));
     h->finalized = true;
     CK(cudaDeviceSynchronize());
     return AMG_OK;
@@ -868,7 +1035,19 @@ int amg_vcycle(amg_t *h, const double *y, double *z, int on_device)
     TRY(to_dev(h, h->tmp_in, y, n, on_device));
     TRY(enqueue_vcycle(h, 0, h->tmp_in, h->tmp_out, nullptr, FIN_NONE, nullptr));
     TRY(from_dev(h, z, h->tmp_out, n, on_device));
-    return sync_stream(h);
+    TRY(sync_stream(h));
+    if (h->trace) {
+        std::vector<unsigned long long> t(h->tail_nops + 1);
+        CK(cudaMemcpy(t.data(), h->trace, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        std::vector<TailOp> ops(h->tail_nops);
+        CK(cudaMemcpy(ops.data(), h->tail_ops, ops.size() * sizeof(TailOp), cudaMemcpyDeviceToHost));
+        fprintf(stderr, "[amgb200 trace] tail from level %d, %d ops, cluster %d:", h->tail_level, h->tail_nops, h->cluster);
+        for (int i = 0; i < h->tail_nops; ++i)
+            fprintf(stderr, " %s%d/%d:%.2fus", ops[i].kind == TAIL_SPMV ? "spmv" : ops[i].kind == TAIL_JACOBI ? "jac" : "coarse",
+                    ops[i].epi, ops[i].nrows, (t[i + 1] - t[i]) * 1e-3);
+        fprintf(stderr, " total %.2fus\n", (t[h->tail_nops] - t[0]) * 1e-3);
+    }
+    return AMG_OK;
 }
 
 int amg_pcg(amg_t *h, const double *b, const double *x0, double rtol, int max_iters, int recompute_every,
@@ -1005,6 +1184,8 @@ int amg_get_stats(amg_t *h, amg_stats_t *out)
     out->launches_last = h->launches_last;
     out->graph_mode = h->graph_mode;
     out->n_levels = (int)h->lv.size();
+    out->tail_level = h->tail_level;
+    out->cluster = h->cluster;
     return AMG_OK;
 }
 

@@ -100,6 +100,12 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p)
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Programmatic dependent launch: a kernel may start (and stage its static
+// matrix tiles) while its predecessor drains; it must call pdl_wait() before
+// touching anything the predecessor writes.  No-ops without the launch attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
 {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -306,15 +312,14 @@ __device__ __noinline__ double pairwise_sum(const PF &P, int base, int n)
     }
 }
 
-// Row sum in numpy order for one row whose entries sit at smem positions
-// [lo, hi) (relative to the staged arrays).  Executed by the LANES lanes of
-// a group; the result is valid in the group's lane 0.
+// Row sum in numpy order for one row whose PRODUCTS p_k sit at smem
+// positions [lo - vdelta, hi - vdelta).  Executed by the LANES lanes of a
+// group; the result is valid in the group's lane 0.
 template <int LANES>
-__device__ __forceinline__ double row_sum_staged(const double *__restrict__ vs, const int32_t *__restrict__ cs,
-                                                 int vdelta, int cdelta, int lo, int hi,
-                                                 const double *__restrict__ x, int lane, unsigned gmask)
+__device__ __forceinline__ double row_sum_staged(const double *__restrict__ ps, int vdelta, int lo, int hi, int lane,
+                                                 unsigned gmask)
 {
-    auto P = [&](int k) -> double { return prod(vs[k - vdelta], __ldg(x + cs[k - cdelta])); };
+    auto P = [&](int k) -> double { return ps[k - vdelta]; };
     const int len = hi - lo;
     if (len <= 0) return 0.0;
     const int n = len - 1;
@@ -322,7 +327,6 @@ __device__ __forceinline__ double row_sum_staged(const double *__restrict__ vs, 
     if (n < 8 || n > 128) {
         double s = 0.0;
         if (lane == 0) {
-            double p0 = P(lo);
             double res;
             if (n < 8) {
                 res = 0.0;
@@ -330,7 +334,7 @@ __device__ __forceinline__ double row_sum_staged(const double *__restrict__ vs, 
             } else {
                 res = pairwise_sum(P, base, n);
             }
-            s = add(p0, res);
+            s = add(P(lo), res);
         }
         return s;
     }
@@ -360,11 +364,11 @@ __device__ __forceinline__ double row_sum_staged(const double *__restrict__ vs, 
         s1 = add(s1, __shfl_xor_sync(gmask, s1, 2));
         res = add(s0, s1);
     } else {
-        double s = acc[0];
-        s = add(s, __shfl_xor_sync(gmask, s, 1));
-        s = add(s, __shfl_xor_sync(gmask, s, 2));
-        s = add(s, __shfl_xor_sync(gmask, s, 4));
-        res = s;
+        double t = acc[0];
+        t = add(t, __shfl_xor_sync(gmask, t, 1));
+        t = add(t, __shfl_xor_sync(gmask, t, 2));
+        t = add(t, __shfl_xor_sync(gmask, t, 4));
+        res = t;
     }
     double out = 0.0;
     if (lane == 0) {
@@ -424,10 +428,11 @@ __global__ void __launch_bounds__(TILE_THREADS) spmv_tiles(const SpmvArgs a)
     extern __shared__ __align__(128) char smem[];
     __shared__ __align__(8) uint64_t bars[8];
     __shared__ double red[TILE_THREADS / 32];
-    if (!gate_open(a.gate1, a.gate2)) return;
 
     const StageLayout L = stage_layout(a.tile_nnz, a.tile_rows);
     const int S = a.stages;
+    // Stage the first S tiles: matrix data is static, so this may run before
+    // the predecessor kernel has finished (programmatic dependent launch).
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -437,6 +442,14 @@ __global__ void __launch_bounds__(TILE_THREADS) spmv_tiles(const SpmvArgs a)
         }
     }
     __syncthreads();
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) {
+        if (threadIdx.x == 0)  // drain the staged copies before the CTA releases its smem
+            for (int s = 0; s < S; ++s)
+                if ((int)blockIdx.x + s * (int)gridDim.x < a.ntiles) mbar_wait(&bars[s], 0u);
+        return;
+    }
 
     constexpr int G = TILE_THREADS / LANES;
     const int grp = threadIdx.x / LANES;
@@ -465,14 +478,26 @@ __global__ void __launch_bounds__(TILE_THREADS) spmv_tiles(const SpmvArgs a)
                 if (want_dot) dacc = fma(yv, a.dotw[d.r0], dacc);
             }
         } else {
-            const double *vs = reinterpret_cast<const double *>(stage);
+            double *vs = reinterpret_cast<double *>(stage);
             const int32_t *cs = reinterpret_cast<const int32_t *>(stage + L.vals_bytes);
             const int32_t *os = reinterpret_cast<const int32_t *>(stage + L.vals_bytes + L.cols_bytes);
             const int vdelta = d.k0 & ~1, cdelta = d.k0 & ~3, odelta = d.r0 & ~3;
+            // phase 1: every product of the tile, flat over the threads so all
+            // x gathers of the tile are in flight together; p_k = a_k * x[c_k]
+            // overwrites a_k in place (rounded product, no FMA contraction).
+            {
+                const int nk = d.k1 - d.k0;
+                double *pv = vs + (d.k0 - vdelta);
+                const int32_t *pc = cs + (d.k0 - cdelta);
+#pragma unroll 4
+                for (int k = threadIdx.x; k < nk; k += TILE_THREADS) pv[k] = prod(pv[k], __ldg(a.x + pc[k]));
+            }
+            __syncthreads();
+            // phase 2: row sums in the reference order from shared memory
             for (int rr = grp; rr < nrows; rr += G) {
                 const int row = d.r0 + rr;
                 const int lo = os[row - odelta], hi = os[row + 1 - odelta];
-                double sum = row_sum_staged<LANES>(vs, cs, vdelta, cdelta, lo, hi, a.x, lane, gmask);
+                double sum = row_sum_staged<LANES>(vs, vdelta, lo, hi, lane, gmask);
                 if (lane == 0) {
                     double yv = epilogue<EPI>(sum, a.b, row, a.omega);
                     a.y[row] = yv;
@@ -520,6 +545,8 @@ struct VecArgs {
 __global__ void __launch_bounds__(VEC_THREADS) pcg_update(const VecArgs a)
 {
     __shared__ double red[VEC_THREADS / 32];
+    pdl_launch();
+    pdl_wait();
     if (!gate_open(a.gate1, a.gate2)) return;
     const double alpha = a.ctl->alpha;
     double acc = 0.0;
@@ -536,6 +563,8 @@ __global__ void __launch_bounds__(VEC_THREADS) pcg_update(const VecArgs a)
 // p = z + beta p                                   (krylov.py:91)
 __global__ void __launch_bounds__(VEC_THREADS) pcg_xpay(const VecArgs a)
 {
+    pdl_launch();
+    pdl_wait();
     if (!gate_open(a.gate1, a.gate2)) return;
     const double beta = a.ctl->beta;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
@@ -546,6 +575,8 @@ __global__ void __launch_bounds__(VEC_THREADS) pcg_xpay(const VecArgs a)
 __global__ void __launch_bounds__(VEC_THREADS) vec_dot(const VecArgs a)
 {
     __shared__ double red[VEC_THREADS / 32];
+    pdl_launch();
+    pdl_wait();
     if (!gate_open(a.gate1, a.gate2)) return;
     double acc = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
@@ -559,6 +590,8 @@ __global__ void __launch_bounds__(VEC_THREADS) vec_dot(const VecArgs a)
 __global__ void __launch_bounds__(VEC_THREADS) jacobi_sweep(const VecArgs a)
 {
     __shared__ double red[VEC_THREADS / 32];
+    pdl_launch();
+    pdl_wait();
     if (!gate_open(a.gate1, a.gate2)) return;
     double acc = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -575,6 +608,8 @@ __global__ void __launch_bounds__(VEC_THREADS) jacobi_sweep(const VecArgs a)
 
 __global__ void __launch_bounds__(VEC_THREADS) vec_copy(const VecArgs a)
 {
+    pdl_launch();
+    pdl_wait();
     if (!gate_open(a.gate1, a.gate2)) return;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
         a.x[i] = a.p ? a.p[i] : 0.0;
@@ -583,6 +618,8 @@ __global__ void __launch_bounds__(VEC_THREADS) vec_copy(const VecArgs a)
 // Loop continuation for the device while-loop graph.
 __global__ void pcg_continue(PcgCtl *c, cudaGraphConditionalHandle handle, int use_handle)
 {
+    pdl_launch();
+    pdl_wait();
     if (c->active && c->it >= c->max_iters) c->active = 0;
     if (use_handle) cudaGraphSetConditional(handle, c->active ? 1u : 0u);
 }
@@ -590,71 +627,85 @@ __global__ void pcg_continue(PcgCtl *c, cudaGraphConditionalHandle handle, int u
 // ---------------------------------------------------------------- coarse solve
 
 // Cholesky: solve L y = b, then L^T z = y (dpotrs with uplo = 'L').
-// Lp: packed lower triangle, row-major: row i holds L[i][0..i] at i(i+1)/2.
-// Single CTA; the packed factor is staged in shared memory when it fits.
+// L: packed lower triangle, row-major: row i holds L[i][0..i] at i(i+1)/2;
+// dinv[i] = 1 / L[i][i] (OpenBLAS' trsm packs inverted diagonals too).
+// One CTA, blocked by 32: warp 0 solves each 32x32 diagonal triangle with
+// shuffles, then all warps apply the block to the remaining rows.  `v` (the
+// right-hand side on entry, the solution on exit) lives in shared memory.
 constexpr int COARSE_THREADS = 256;
 
-__global__ void __launch_bounds__(COARSE_THREADS) coarse_chol(int n, const double *__restrict__ Lp, const double *y,
-                                                               double *z, int staged, const int *gate1,
-                                                               double *partials, unsigned *ticket, int fin,
-                                                               PcgCtl *ctl, const double *dotw)
+__device__ __forceinline__ int64_t tri(int i) { return (int64_t)i * (i + 1) / 2; }
+
+__device__ void chol_solve_cta(int n, const double *__restrict__ L, const double *__restrict__ dinv, double *v)
 {
-    extern __shared__ __align__(16) double sh[];
-    __shared__ double red[COARSE_THREADS / 32];
-    if (!gate_open(gate1, nullptr)) return;
-    const int64_t np = (int64_t)n * (n + 1) / 2;
-    double *v = sh;  // n
-    const double *L = Lp;
-    if (staged) {
-        double *Ls = sh + ((n + 1) & ~1);
-        for (int64_t i = threadIdx.x; i < np; i += blockDim.x) Ls[i] = Lp[i];
-        L = Ls;
-    }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = y[i];
-    __syncthreads();
-    // forward: column-oriented L y = b
-    for (int j = 0; j < n; ++j) {
-        const int64_t rj = (int64_t)j * (j + 1) / 2;
-        const double yj = v[j] / L[rj + j];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int jb = 0; jb < n; jb += 32) {  // forward: L y = b
+        const int nb = min(32, n - jb);
+        if (warp == 0) {
+            double vi = lane < nb ? v[jb + lane] : 0.0;
+            const double di = lane < nb ? dinv[jb + lane] : 0.0;
+            const double *Lr = L + tri(jb + lane) + jb;  // row jb+lane of the diagonal block
+            if (nb == 32) {
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const double vc = __shfl_sync(0xffffffffu, vi * di, c);
+                    if (lane == c) vi = vc;
+                    if (lane > c) vi -= Lr[c] * vc;
+                }
+            } else {
+                for (int c = 0; c < nb; ++c) {
+                    const double vc = __shfl_sync(0xffffffffu, vi * di, c);
+                    if (lane == c) vi = vc;
+                    if (lane > c && lane < nb) vi -= Lr[c] * vc;
+                }
+            }
+            if (lane < nb) v[jb + lane] = vi;
+        }
         __syncthreads();
-        if (threadIdx.x == 0) v[j] = yj;
-        for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) v[i] -= L[(int64_t)i * (i + 1) / 2 + j] * yj;
+        for (int i = jb + nb + threadIdx.x; i < n; i += blockDim.x) {
+            const double *Li = L + tri(i) + jb;
+            double acc = 0.0;
+            for (int c = 0; c < nb; ++c) acc = fma(Li[c], v[jb + c], acc);
+            v[i] -= acc;
+        }
         __syncthreads();
     }
-    // backward: L^T z = y, row j of L^T is column j of L: z_j = (y_j - sum_{i>j} L_ij z_i) / L_jj
-    // column-oriented on L^T: for j = n-1..0: z_j /= L_jj ; v_i -= L_ji z_j for i < j
-    for (int j = n - 1; j >= 0; --j) {
-        const int64_t rj = (int64_t)j * (j + 1) / 2;
-        const double zj = v[j] / L[rj + j];
+    const int nblk = (n + 31) / 32;
+    for (int bi = nblk - 1; bi >= 0; --bi) {  // backward: L^T z = y
+        const int jb = bi * 32;
+        const int nb = min(32, n - jb);
+        if (warp == 0) {
+            double vi = lane < nb ? v[jb + lane] : 0.0;
+            const double di = lane < nb ? dinv[jb + lane] : 0.0;
+            if (nb == 32) {
+#pragma unroll
+                for (int c = 31; c >= 0; --c) {
+                    const double zc = __shfl_sync(0xffffffffu, vi * di, c);
+                    if (lane == c) vi = zc;
+                    if (lane < c) vi -= L[tri(jb + c) + jb + lane] * zc;  // L^T[lane][c] = L[c][lane]
+                }
+            } else {
+                for (int c = nb - 1; c >= 0; --c) {
+                    const double zc = __shfl_sync(0xffffffffu, vi * di, c);
+                    if (lane == c) vi = zc;
+                    if (lane < c) vi -= L[tri(jb + c) + jb + lane] * zc;
+                }
+            }
+            if (lane < nb) v[jb + lane] = vi;
+        }
         __syncthreads();
-        if (threadIdx.x == 0) v[j] = zj;
-        for (int i = threadIdx.x; i < j; i += blockDim.x) v[i] -= L[rj + i] * zj;
+        for (int i = threadIdx.x; i < jb; i += blockDim.x) {
+            double acc = 0.0;
+            for (int c = 0; c < nb; ++c) acc = fma(L[tri(jb + c) + i], v[jb + c], acc);
+            v[i] -= acc;
+        }
         __syncthreads();
-    }
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        z[i] = v[i];
-        if (dotw) acc = fma(v[i], dotw[i], acc);
-    }
-    if (fin != FIN_NONE) {
-        double s = block_sum<COARSE_THREADS>(acc, red);
-        grid_finalize<COARSE_THREADS>(s, partials, ticket, fin, ctl);
     }
 }
 
 // LU (getrs, no transpose): b <- P b ; L (unit) y = b ; U z = y.  LU full n x n row-major.
-__global__ void __launch_bounds__(COARSE_THREADS) coarse_lu(int n, const double *__restrict__ LU,
-                                                             const int32_t *__restrict__ piv, const double *y,
-                                                             double *z, const int *gate1, double *partials,
-                                                             unsigned *ticket, int fin, PcgCtl *ctl,
-                                                             const double *dotw)
+__device__ void lu_solve_cta(int n, const double *__restrict__ LU, const int32_t *__restrict__ piv, double *v)
 {
-    extern __shared__ __align__(16) double sh[];
-    __shared__ double red[COARSE_THREADS / 32];
-    if (!gate_open(gate1, nullptr)) return;
-    double *v = sh;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = y[i];
-    __syncthreads();
     if (threadIdx.x == 0) {
         for (int i = 0; i < n; ++i) {
             int p = piv[i];
@@ -674,6 +725,40 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_lu(int n, const double 
         for (int i = threadIdx.x; i < j; i += blockDim.x) v[i] -= LU[(int64_t)i * n + j] * zj;
         __syncthreads();
     }
+}
+
+struct CoarseArgs {
+    int n;
+    int kind;    // 0 cholesky, 1 lu
+    int staged;  // packed factor copied to shared memory
+    const double *Lp;
+    const double *dinv;
+    const double *LU;
+    const int32_t *piv;
+};
+
+__global__ void __launch_bounds__(COARSE_THREADS) coarse_solve_k(const CoarseArgs c, const double *y, double *z,
+                                                                  const int *gate1, double *partials,
+                                                                  unsigned *ticket, int fin, PcgCtl *ctl,
+                                                                  const double *dotw)
+{
+    extern __shared__ __align__(16) double sh[];
+    __shared__ double red[COARSE_THREADS / 32];
+    const int n = c.n;
+    double *v = sh;
+    const double *L = c.Lp;
+    if (c.kind == 0 && c.staged) {  // the factor is static: stage it before waiting on the producer
+        double *Ls = sh + ((n + 1) & ~1);
+        for (int64_t i = threadIdx.x; i < tri(n); i += blockDim.x) Ls[i] = c.Lp[i];
+        L = Ls;
+    }
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(gate1, nullptr)) return;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = y[i];
+    __syncthreads();
+    if (c.kind == 0) chol_solve_cta(n, L, c.dinv, v);
+    else lu_solve_cta(n, c.LU, c.piv, v);
     double acc = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         z[i] = v[i];
@@ -682,6 +767,134 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_lu(int n, const double 
     if (fin != FIN_NONE) {
         double s = block_sum<COARSE_THREADS>(acc, red);
         grid_finalize<COARSE_THREADS>(s, partials, ticket, fin, ctl);
+    }
+}
+
+// ---------------------------------------------------------------- cluster tail
+
+// The V-cycle below a size threshold runs as ONE kernel on one thread-block
+// cluster: the operations of those levels (same sequence, same epilogues,
+// same reference summation order as the per-op kernels) are executed in
+// order with a cluster barrier between dependent operations, replacing
+// kernel launches (~ microseconds each) by barriers (~0.2 us).
+enum TailKind { TAIL_SPMV = 0, TAIL_JACOBI = 1, TAIL_COARSE = 2 };
+
+struct TailOp {
+    int kind;
+    int epi;
+    int nrows;
+    int mode;  // jacobi: 0 set, 1 accumulate
+    const int32_t *off;
+    const int32_t *col;
+    const double *val;
+    const double *x;
+    double *y;
+    const double *b;
+    const double *d;
+    double omega;
+};
+
+constexpr int TAIL_THREADS = 512;
+
+__device__ __forceinline__ void cluster_barrier()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ unsigned cluster_rank()
+{
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ unsigned cluster_size()
+{
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+
+// Row sum in the reference order with products read from global memory
+// (vectors written inside this kernel are read through L2: __ldcg).
+__device__ __forceinline__ double row_sum_global(const int32_t *__restrict__ off, const int32_t *__restrict__ col,
+                                                 const double *__restrict__ val, const double *x, int row)
+{
+    const int lo = __ldg(off + row), hi = __ldg(off + row + 1);
+    auto P = [&](int k) -> double { return prod(__ldg(val + k), __ldcg(x + __ldg(col + k))); };
+    const int len = hi - lo;
+    if (len <= 0) return 0.0;
+    const int n = len - 1;
+    if (n > 128) return add(P(lo), pairwise_sum(P, lo + 1, n));
+    return add(P(lo), pairwise_leaf(P, lo + 1, n));
+}
+
+template <int EPI>
+__device__ __forceinline__ void tail_spmv(const TailOp &o, int t0, int nt)
+{
+    for (int row = t0; row < o.nrows; row += nt) {
+        const double s = row_sum_global(o.off, o.col, o.val, o.x, row);
+        double yv;
+        if constexpr (EPI == EPI_PLAIN) yv = s;
+        else if constexpr (EPI == EPI_RESID) yv = __dsub_rn(__ldcg(o.b + row), s);
+        else if constexpr (EPI == EPI_AXPYW) yv = add(__ldcg(o.b + row), __dmul_rn(o.omega, s));
+        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(o.omega, s);
+        else yv = add(__ldcg(o.b + row), s);
+        o.y[row] = yv;
+    }
+}
+
+__device__ __forceinline__ unsigned long long globaltimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__restrict__ ops, int nops,
+                                                             const CoarseArgs c, const int *gate1,
+                                                             unsigned long long *trace)
+{
+    extern __shared__ __align__(16) double sh[];
+    const unsigned rank = cluster_rank();
+    const unsigned ncta = cluster_size();
+    const double *L = c.Lp;
+    if (rank == 0 && c.kind == 0 && c.staged) {
+        double *Ls = sh + ((c.n + 1) & ~1);
+        for (int64_t i = threadIdx.x; i < tri(c.n); i += blockDim.x) Ls[i] = c.Lp[i];
+        L = Ls;
+    }
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(gate1, nullptr)) return;  // uniform across the cluster
+    const int t0 = rank * blockDim.x + threadIdx.x;
+    const int nt = ncta * blockDim.x;
+    if (trace && t0 == 0) trace[0] = globaltimer();
+    for (int i = 0; i < nops; ++i) {
+        const TailOp o = ops[i];
+        if (o.kind == TAIL_SPMV) {
+            switch (o.epi) {
+            case EPI_PLAIN: tail_spmv<EPI_PLAIN>(o, t0, nt); break;
+            case EPI_RESID: tail_spmv<EPI_RESID>(o, t0, nt); break;
+            case EPI_AXPYW: tail_spmv<EPI_AXPYW>(o, t0, nt); break;
+            case EPI_SETW: tail_spmv<EPI_SETW>(o, t0, nt); break;
+            default: tail_spmv<EPI_ADD>(o, t0, nt); break;
+            }
+        } else if (o.kind == TAIL_JACOBI) {
+            for (int r = t0; r < o.nrows; r += nt) {
+                const double z = __dmul_rn(o.omega, __dmul_rn(__ldg(o.d + r), __ldcg(o.x + r)));
+                o.y[r] = o.mode ? add(__ldcg(o.y + r), z) : z;
+            }
+        } else if (rank == 0) {  // coarsest solve on CTA 0
+            double *v = sh;
+            for (int r = threadIdx.x; r < c.n; r += blockDim.x) v[r] = __ldcg(o.x + r);
+            __syncthreads();
+            if (c.kind == 0) chol_solve_cta(c.n, L, c.dinv, v);
+            else lu_solve_cta(c.n, c.LU, c.piv, v);
+            for (int r = threadIdx.x; r < c.n; r += blockDim.x) o.y[r] = v[r];
+        }
+        cluster_barrier();
+        if (trace && t0 == 0) trace[i + 1] = globaltimer();
     }
 }
 

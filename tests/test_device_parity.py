@@ -69,9 +69,12 @@ def test_smoother_sweeps_bit_identical(name, cases):
             np.testing.assert_array_equal(dh.apply_smoother(k, b, x0, steps), v[f"smooth_L{k}_x0_{steps}"])
 
 
+@pytest.mark.parametrize("tail", [True, False])
 @pytest.mark.parametrize("name", HIER_CASES)
-def test_coarse_solve_and_vcycle(name, cases):
-    c, dh = _dh(name, cases)
+def test_coarse_solve_and_vcycle(name, tail, cases):
+    c, dh = _dh(name, cases, **({} if tail else {"tail_nnz": 0}))
+    if tail and c["h"].n_levels > 1:
+        assert dh.stats()["tail_level"] >= 1
     v = c["vec"]
     assert _relerr(dh.coarse_solve(v["coarse_y"]), v["coarse_z"]) <= 1e-12
     z = dh.vcycle(v["y"])
@@ -81,9 +84,11 @@ def test_coarse_solve_and_vcycle(name, cases):
     assert _relerr(dh.vcycle(y2), O.vcycle(c["h"], y2)) <= 1e-12
 
 
+@pytest.mark.parametrize("opts", [{}, {"tail_nnz": 0}, {"pdl": 0}, {"graph": 1}])
 @pytest.mark.parametrize("name", [n for n in HIER_CASES if "twogrid" not in n and "lu" not in n])
-def test_pcg_matches_reference(name, cases):
-    c, dh = _dh(name, cases)
+def test_pcg_matches_reference(name, opts, cases):
+    c, dh = _dh(name, cases, **{k: v for k, v in opts.items() if k != "graph"})
+    dh.set_option("graph", opts.get("graph", 2))
     exp = c["expect"]["pcg"]
     res = amg.pcg(dh.A0, c["b"], apply_m=dh.vcycle,
                   config=amg.KrylovConfig(rtol=exp["rtol"], max_iters=exp["max_iters"], record_history=True))
