@@ -119,13 +119,18 @@ struct amg_handle {
     int lanes_override = 0;
     int pdl = 1;  // programmatic dependent launch between consecutive kernels
     // cluster tail: levels >= tail_level run inside one cluster kernel
-    int64_t tail_nnz = 400000;
+    int64_t tail_nnz = 1 << 30;  // level filter on nnz(A_k); the cluster smem budget decides
     int cluster = 16;
     int tail_level = 0;  // 0 = disabled
     TailOp *tail_ops = nullptr;
+    TailMat *tail_mats = nullptr;
+    int tail_nmats = 0;
+    int32_t *tail_splits = nullptr;
+    int tail_prod_off = 0;
     int tail_nops = 0;
     size_t tail_smem = 0;
     std::vector<TailOp> *collect = nullptr;  // op collection mode (builds the tail)
+    std::vector<const DevMat *> *collect_mats = nullptr;
     unsigned long long *trace = nullptr;     // AMGB200_TRACE: %globaltimer per tail op
     // graph
     cudaGraphExec_t gexec = nullptr;
@@ -242,9 +247,9 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         o.kind = TAIL_SPMV;
         o.epi = epi;
         o.nrows = (int)M.nrows;
-        o.off = M.off;
-        o.col = M.col;
-        o.val = M.val;
+        o.mat = -1;
+        h->collect_mats->push_back(&M);
+        o.mode = (int)h->collect_mats->size() - 1;  // provisional: index into collect_mats
         o.x = x;
         o.y = y;
         o.b = b;
@@ -376,8 +381,9 @@ static int launch_tail(amg_t *h, const int *g1)
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = h->pdl ? 2 : 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, tail_vcycle, (const TailOp *)h->tail_ops, h->tail_nops, coarse_args(h), g1,
-                                       h->trace);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tail_vcycle, (const TailOp *)h->tail_ops, h->tail_nops,
+                                       (const TailMat *)h->tail_mats, h->tail_nmats, (const int32_t *)h->tail_splits,
+                                       h->tail_prod_off, coarse_args(h), g1, h->trace);
     if (e != cudaSuccess) return fail(AMG_E_CUDA, std::string("tail launch failed: ") + cudaGetErrorString(e));
     ++h->launches;
     return AMG_OK;
@@ -561,26 +567,96 @@ static int build_tail(amg_t *h)
     const int nl = (int)h->lv.size();
     h->tail_level = 0;
     if (h->tail_nnz <= 0 || nl < 2 || h->nranks > 1) return AMG_OK;
-    int kt = 0;
-    for (int k = nl - 1; k >= 1; --k) {
-        if (h->lv[k].m[AMG_A].nnz <= h->tail_nnz) kt = k;
-        else break;
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+    const size_t coarse_bytes = (h->coarse_kind == AMG_COARSE_CHOLESKY && h->coarse_staged)
+                                    ? h->coarse_smem
+                                    : (size_t)((h->nc + 1) & ~1) * sizeof(double);
+    const int budget = optin - (int)(TAIL_MAX_OPS * sizeof(TailOp) + TAIL_MAX_MATS * 5 * sizeof(int) +
+                                     TAIL_MAX_DINV * sizeof(double)) - 1024;  // static smem + slack
+    // candidate start levels: deepest first; keep the shallowest that fits
+    int best = 0;
+    std::vector<TailOp> best_ops;
+    std::vector<TailMat> best_mats;
+    std::vector<int32_t> best_splits;
+    int best_prod_off = 0, best_smem = 0;
+    for (int kt = nl - 1; kt >= 1; --kt) {
+        if (h->lv[kt].m[AMG_A].nnz > h->tail_nnz) break;
+        std::vector<TailOp> ops;
+        std::vector<const DevMat *> mats_raw;
+        h->collect = &ops;
+        h->collect_mats = &mats_raw;
+        int st = enqueue_vcycle(h, kt, h->lv[kt].y, h->lv[kt].x, nullptr, FIN_NONE, nullptr);
+        h->collect = nullptr;
+        h->collect_mats = nullptr;
+        if (st != AMG_OK) return st;
+        // distinct matrices, balanced row splits, smem regions
+        std::vector<const DevMat *> uniq;
+        std::vector<TailMat> mats;
+        std::vector<int32_t> splits;
+        size_t off_bytes = (coarse_bytes + 15) & ~(size_t)15;
+        int prod_cap = 0;
+        bool fits = true;
+        for (auto &o : ops) {
+            if (o.kind != TAIL_SPMV) continue;
+            const DevMat *M = mats_raw[o.mode];
+            o.mode = 0;
+            int idx = -1;
+            for (size_t u = 0; u < uniq.size(); ++u)
+                if (uniq[u] == M) idx = (int)u;
+            if (idx < 0) {
+                std::vector<int32_t> off(M->nrows + 1);
+                CK(cudaMemcpy(off.data(), M->off, (M->nrows + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+                TailMat T{};
+                T.off = M->off;
+                T.col = M->col;
+                T.val = M->val;
+                T.split = (int)splits.size();
+                const int64_t nnz = off[M->nrows];
+                int r = 0;
+                splits.push_back(0);
+                for (int c = 1; c < h->cluster; ++c) {
+                    const int64_t target = nnz * c / h->cluster;
+                    while (r < M->nrows && off[r] < target) ++r;
+                    splits.push_back(r);
+                }
+                splits.push_back((int32_t)M->nrows);
+                int rc = 0, kc = 0;
+                for (int c = 0; c < h->cluster; ++c) {
+                    rc = std::max(rc, splits[T.split + c + 1] - splits[T.split + c]);
+                    kc = std::max(kc, off[splits[T.split + c + 1]] - off[splits[T.split + c]]);
+                }
+                T.rows_cap = rc;
+                T.nnz_cap = kc;
+                T.smem_off = (int)off_bytes;
+                off_bytes += tail_region_bytes(rc, kc);
+                prod_cap = std::max(prod_cap, kc);
+                idx = (int)uniq.size();
+                uniq.push_back(M);
+                mats.push_back(T);
+            }
+            o.mat = idx;
+        }
+        if ((int)ops.size() > TAIL_MAX_OPS || (int)mats.size() > TAIL_MAX_MATS) break;
+        const size_t prod_off = (off_bytes + 15) & ~(size_t)15;
+        const size_t smem = prod_off + (size_t)prod_cap * 8 + 16;
+        if (smem > (size_t)budget) fits = false;
+        if (!fits) break;
+        best = kt;
+        best_ops = ops;
+        best_mats = mats;
+        best_splits = splits;
+        best_prod_off = (int)prod_off;
+        best_smem = (int)smem;
     }
-    if (kt == 0) return AMG_OK;
-    std::vector<TailOp> ops;
-    h->collect = &ops;
-    int st = enqueue_vcycle(h, kt, h->lv[kt].y, h->lv[kt].x, nullptr, FIN_NONE, nullptr);
-    h->collect = nullptr;
-    if (st != AMG_OK) return st;
-    size_t smem = (size_t)((h->nc + 1) & ~1) * sizeof(double);
-    if (h->coarse_kind == AMG_COARSE_CHOLESKY && h->coarse_staged) smem = h->coarse_smem;
+    if (best == 0) return AMG_OK;
     TRY(raise_smem_caps(h->device));
-    // verify the cluster shape can be resident; fall back to smaller clusters
-    for (;;) {
+    int nclusters = 0;
+    {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)h->cluster);
         cfg.blockDim = dim3(TAIL_THREADS);
-        cfg.dynamicSmemBytes = smem;
+        cfg.dynamicSmemBytes = best_smem;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = (unsigned)h->cluster;
@@ -588,18 +664,21 @@ static int build_tail(amg_t *h)
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        int nclusters = 0;
         cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, (const void *)tail_vcycle, &cfg);
-        if (e == cudaSuccess && nclusters >= 1) break;
-        cudaGetLastError();
-        if (h->cluster <= 1) return fail(AMG_E_CUDA, "cluster tail kernel cannot be made resident");
-        h->cluster /= 2;
+        if (e != cudaSuccess) { cudaGetLastError(); nclusters = 0; }
     }
-    TRY(dalloc(&h->tail_ops, ops.size()));
-    CK(cudaMemcpy(h->tail_ops, ops.data(), ops.size() * sizeof(TailOp), cudaMemcpyHostToDevice));
-    h->tail_nops = (int)ops.size();
-    h->tail_smem = std::max<size_t>(smem, 1024);
-    h->tail_level = kt;
+    if (nclusters < 1) return AMG_OK;  // cluster shape not resident here: per-op kernels are used
+    TRY(dalloc(&h->tail_ops, best_ops.size()));
+    CK(cudaMemcpy(h->tail_ops, best_ops.data(), best_ops.size() * sizeof(TailOp), cudaMemcpyHostToDevice));
+    TRY(dalloc(&h->tail_mats, best_mats.size()));
+    if (!best_mats.empty()) CK(cudaMemcpy(h->tail_mats, best_mats.data(), best_mats.size() * sizeof(TailMat), cudaMemcpyHostToDevice));
+    TRY(dalloc(&h->tail_splits, best_splits.size()));
+    if (!best_splits.empty()) CK(cudaMemcpy(h->tail_splits, best_splits.data(), best_splits.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    h->tail_nops = (int)best_ops.size();
+    h->tail_nmats = (int)best_mats.size();
+    h->tail_smem = best_smem;
+    h->tail_prod_off = best_prod_off;
+    h->tail_level = best;
     if (getenv("AMGB200_TRACE")) TRY(dalloc(&h->trace, (size_t)h->tail_nops + 2));
     return AMG_OK;
 }
@@ -659,7 +738,7 @@ void amg_destroy(amg_t *h)
         }
         F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
     }
-    F(h->Lp); F(h->LU); F(h->dinv); F(h->tail_ops); F(h->piv); F(h->partials); F(h->ticket); F(h->ctl);
+    F(h->Lp); F(h->LU); F(h->dinv); F(h->tail_ops); F(h->tail_mats); F(h->tail_splits); F(h->piv); F(h->partials); F(h->ticket); F(h->ctl);
     F(h->b); F(h->x); F(h->r); F(h->z); F(h->p); F(h->q); F(h->tmp_in); F(h->tmp_out); F(h->hist);
     if (h->ctl_h) cudaFreeHost(h->ctl_h);
     if (h->gexec) cudaGraphExecDestroy(h->gexec);

@@ -664,9 +664,19 @@ __device__ void chol_solve_cta(int n, const double *__restrict__ L, const double
         __syncthreads();
         for (int i = jb + nb + threadIdx.x; i < n; i += blockDim.x) {
             const double *Li = L + tri(i) + jb;
-            double acc = 0.0;
-            for (int c = 0; c < nb; ++c) acc = fma(Li[c], v[jb + c], acc);
-            v[i] -= acc;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            if (nb == 32) {
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {
+                    a0 = fma(Li[c], v[jb + c], a0);
+                    a1 = fma(Li[c + 1], v[jb + c + 1], a1);
+                    a2 = fma(Li[c + 2], v[jb + c + 2], a2);
+                    a3 = fma(Li[c + 3], v[jb + c + 3], a3);
+                }
+            } else {
+                for (int c = 0; c < nb; ++c) a0 = fma(Li[c], v[jb + c], a0);
+            }
+            v[i] -= (a0 + a1) + (a2 + a3);
         }
         __syncthreads();
     }
@@ -695,9 +705,19 @@ __device__ void chol_solve_cta(int n, const double *__restrict__ L, const double
         }
         __syncthreads();
         for (int i = threadIdx.x; i < jb; i += blockDim.x) {
-            double acc = 0.0;
-            for (int c = 0; c < nb; ++c) acc = fma(L[tri(jb + c) + i], v[jb + c], acc);
-            v[i] -= acc;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            if (nb == 32) {
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {
+                    a0 = fma(L[tri(jb + c) + i], v[jb + c], a0);
+                    a1 = fma(L[tri(jb + c + 1) + i], v[jb + c + 1], a1);
+                    a2 = fma(L[tri(jb + c + 2) + i], v[jb + c + 2], a2);
+                    a3 = fma(L[tri(jb + c + 3) + i], v[jb + c + 3], a3);
+                }
+            } else {
+                for (int c = 0; c < nb; ++c) a0 = fma(L[tri(jb + c) + i], v[jb + c], a0);
+            }
+            v[i] -= (a0 + a1) + (a2 + a3);
         }
         __syncthreads();
     }
@@ -776,7 +796,10 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_solve_k(const CoarseArg
 // cluster: the operations of those levels (same sequence, same epilogues,
 // same reference summation order as the per-op kernels) are executed in
 // order with a cluster barrier between dependent operations, replacing
-// kernel launches (~ microseconds each) by barriers (~0.2 us).
+// kernel launches (~ microseconds each) by barriers (~0.2 us).  Every
+// matrix block a CTA owns (rows balanced by stored entries) is staged in its
+// shared memory once at kernel start -- before griddepcontrol.wait, so it
+// overlaps the predecessor -- leaving one x-gather round trip per op.
 enum TailKind { TAIL_SPMV = 0, TAIL_JACOBI = 1, TAIL_COARSE = 2 };
 
 struct TailOp {
@@ -784,9 +807,7 @@ struct TailOp {
     int epi;
     int nrows;
     int mode;  // jacobi: 0 set, 1 accumulate
-    const int32_t *off;
-    const int32_t *col;
-    const double *val;
+    int mat;   // SpMV: index into the staged-matrix table
     const double *x;
     double *y;
     const double *b;
@@ -794,7 +815,28 @@ struct TailOp {
     double omega;
 };
 
+// A distinct matrix of the tail and where each CTA's block of it lives.
+struct TailMat {
+    const int32_t *off;
+    const int32_t *col;
+    const double *val;
+    int split;     // (cluster + 1) row splits in the split table
+    int smem_off;  // byte offset of this matrix's region in every CTA's smem
+    int rows_cap;  // region capacity: rows (offsets: rows_cap + 1 entries)
+    int nnz_cap;   // region capacity: entries
+};
+
+__host__ __device__ inline int tail_region_bytes(int rows_cap, int nnz_cap)
+{
+    const int ob = ((rows_cap + 1) * 4 + 15) & ~15;
+    const int cb = (nnz_cap * 4 + 15) & ~15;
+    return ob + cb + nnz_cap * 8;
+}
+
 constexpr int TAIL_THREADS = 512;
+constexpr int TAIL_MAX_OPS = 96;    // ops per tail (8 per level + coarse): up to 11 levels
+constexpr int TAIL_MAX_MATS = 64;
+constexpr int TAIL_MAX_DINV = 512;
 
 __device__ __forceinline__ void cluster_barrier()
 {
@@ -808,42 +850,6 @@ __device__ __forceinline__ unsigned cluster_rank()
     return r;
 }
 
-__device__ __forceinline__ unsigned cluster_size()
-{
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
-    return r;
-}
-
-// Row sum in the reference order with products read from global memory
-// (vectors written inside this kernel are read through L2: __ldcg).
-__device__ __forceinline__ double row_sum_global(const int32_t *__restrict__ off, const int32_t *__restrict__ col,
-                                                 const double *__restrict__ val, const double *x, int row)
-{
-    const int lo = __ldg(off + row), hi = __ldg(off + row + 1);
-    auto P = [&](int k) -> double { return prod(__ldg(val + k), __ldcg(x + __ldg(col + k))); };
-    const int len = hi - lo;
-    if (len <= 0) return 0.0;
-    const int n = len - 1;
-    if (n > 128) return add(P(lo), pairwise_sum(P, lo + 1, n));
-    return add(P(lo), pairwise_leaf(P, lo + 1, n));
-}
-
-template <int EPI>
-__device__ __forceinline__ void tail_spmv(const TailOp &o, int t0, int nt)
-{
-    for (int row = t0; row < o.nrows; row += nt) {
-        const double s = row_sum_global(o.off, o.col, o.val, o.x, row);
-        double yv;
-        if constexpr (EPI == EPI_PLAIN) yv = s;
-        else if constexpr (EPI == EPI_RESID) yv = __dsub_rn(__ldcg(o.b + row), s);
-        else if constexpr (EPI == EPI_AXPYW) yv = add(__ldcg(o.b + row), __dmul_rn(o.omega, s));
-        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(o.omega, s);
-        else yv = add(__ldcg(o.b + row), s);
-        o.y[row] = yv;
-    }
-}
-
 __device__ __forceinline__ unsigned long long globaltimer()
 {
     unsigned long long t;
@@ -851,34 +857,108 @@ __device__ __forceinline__ unsigned long long globaltimer()
     return t;
 }
 
+template <int EPI>
+__device__ __forceinline__ void tail_spmv(const TailOp &o, int r0, int r1, const int32_t *os, const int32_t *cs,
+                                          const double *vs, double *ps)
+{
+    const int nk = os[r1 - r0];
+    // prefetch the epilogue operand of this thread's first row with the gathers
+    double bpre = 0.0;
+    if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD)
+        if (r0 + (int)threadIdx.x < r1) bpre = __ldcg(o.b + r0 + threadIdx.x);
+#pragma unroll 8
+    for (int k = threadIdx.x; k < nk; k += TAIL_THREADS) ps[k] = prod(vs[k], __ldcg(o.x + cs[k]));
+    __syncthreads();
+    for (int rr = threadIdx.x; rr < r1 - r0; rr += TAIL_THREADS) {
+        const double s = row_sum_staged<1>(ps, 0, os[rr], os[rr + 1], 0, 0u);
+        const int row = r0 + rr;
+        double bv = 0.0;
+        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD)
+            bv = (rr == (int)threadIdx.x) ? bpre : __ldcg(o.b + row);
+        double yv;
+        if constexpr (EPI == EPI_PLAIN) yv = s;
+        else if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, s);
+        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(o.omega, s));
+        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(o.omega, s);
+        else yv = add(bv, s);
+        o.y[row] = yv;
+    }
+}
+
 __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__restrict__ ops, int nops,
+                                                             const TailMat *__restrict__ mats, int nmats,
+                                                             const int32_t *__restrict__ splits, int prod_off,
                                                              const CoarseArgs c, const int *gate1,
                                                              unsigned long long *trace)
 {
     extern __shared__ __align__(16) double sh[];
+    __shared__ TailOp s_ops[TAIL_MAX_OPS];
+    __shared__ int s_split[TAIL_MAX_MATS][2];
+    __shared__ int s_geo[TAIL_MAX_MATS][3];
+    __shared__ double s_dinv[TAIL_MAX_DINV];
+    char *smem = reinterpret_cast<char *>(sh);
+    double *ps = reinterpret_cast<double *>(smem + prod_off);  // product buffer
     const unsigned rank = cluster_rank();
-    const unsigned ncta = cluster_size();
+    // ---- stage static data (before waiting on the predecessor)
     const double *L = c.Lp;
+    const double *dinv = c.dinv;
     if (rank == 0 && c.kind == 0 && c.staged) {
         double *Ls = sh + ((c.n + 1) & ~1);
         for (int64_t i = threadIdx.x; i < tri(c.n); i += blockDim.x) Ls[i] = c.Lp[i];
         L = Ls;
+        if (c.n <= TAIL_MAX_DINV) {
+            for (int i = threadIdx.x; i < c.n; i += blockDim.x) s_dinv[i] = c.dinv[i];
+            dinv = s_dinv;
+        }
     }
+    {
+        const int nw = nops * (int)(sizeof(TailOp) / 4);
+        const int *src = reinterpret_cast<const int *>(ops);
+        int *dst = reinterpret_cast<int *>(s_ops);
+        for (int i = threadIdx.x; i < nw; i += blockDim.x) dst[i] = src[i];
+        for (int m = threadIdx.x; m < nmats; m += blockDim.x) {
+            s_split[m][0] = splits[mats[m].split + rank];
+            s_split[m][1] = splits[mats[m].split + rank + 1];
+            s_geo[m][0] = mats[m].smem_off;
+            s_geo[m][1] = mats[m].rows_cap;
+            s_geo[m][2] = mats[m].nnz_cap;
+        }
+    }
+    for (int m = 0; m < nmats; ++m) {
+        const TailMat M = mats[m];
+        const int r0 = splits[M.split + rank], r1 = splits[M.split + rank + 1];
+        const int k0 = M.off[r0];
+        int32_t *os = reinterpret_cast<int32_t *>(smem + M.smem_off);
+        int32_t *cs = reinterpret_cast<int32_t *>(smem + M.smem_off + (((M.rows_cap + 1) * 4 + 15) & ~15));
+        double *vs = reinterpret_cast<double *>(reinterpret_cast<char *>(cs) + ((M.nnz_cap * 4 + 15) & ~15));
+        for (int r = threadIdx.x; r <= r1 - r0; r += blockDim.x) os[r] = M.off[r0 + r] - k0;
+        const int nk = M.off[r1] - k0;
+        for (int k = threadIdx.x; k < nk; k += blockDim.x) {
+            cs[k] = M.col[k0 + k];
+            vs[k] = M.val[k0 + k];
+        }
+    }
+    __syncthreads();
     pdl_launch();
     pdl_wait();
     if (!gate_open(gate1, nullptr)) return;  // uniform across the cluster
     const int t0 = rank * blockDim.x + threadIdx.x;
-    const int nt = ncta * blockDim.x;
+    const int nt = gridDim.x * blockDim.x;  // grid == one cluster
     if (trace && t0 == 0) trace[0] = globaltimer();
     for (int i = 0; i < nops; ++i) {
-        const TailOp o = ops[i];
+        const TailOp &o = s_ops[i];
         if (o.kind == TAIL_SPMV) {
+            const int r0 = s_split[o.mat][0], r1 = s_split[o.mat][1];
+            const int moff = s_geo[o.mat][0], rcap = s_geo[o.mat][1], kcap = s_geo[o.mat][2];
+            const int32_t *os = reinterpret_cast<const int32_t *>(smem + moff);
+            const int32_t *cs = reinterpret_cast<const int32_t *>(smem + moff + (((rcap + 1) * 4 + 15) & ~15));
+            const double *vs = reinterpret_cast<const double *>(reinterpret_cast<const char *>(cs) + ((kcap * 4 + 15) & ~15));
             switch (o.epi) {
-            case EPI_PLAIN: tail_spmv<EPI_PLAIN>(o, t0, nt); break;
-            case EPI_RESID: tail_spmv<EPI_RESID>(o, t0, nt); break;
-            case EPI_AXPYW: tail_spmv<EPI_AXPYW>(o, t0, nt); break;
-            case EPI_SETW: tail_spmv<EPI_SETW>(o, t0, nt); break;
-            default: tail_spmv<EPI_ADD>(o, t0, nt); break;
+            case EPI_PLAIN: tail_spmv<EPI_PLAIN>(o, r0, r1, os, cs, vs, ps); break;
+            case EPI_RESID: tail_spmv<EPI_RESID>(o, r0, r1, os, cs, vs, ps); break;
+            case EPI_AXPYW: tail_spmv<EPI_AXPYW>(o, r0, r1, os, cs, vs, ps); break;
+            case EPI_SETW: tail_spmv<EPI_SETW>(o, r0, r1, os, cs, vs, ps); break;
+            default: tail_spmv<EPI_ADD>(o, r0, r1, os, cs, vs, ps); break;
             }
         } else if (o.kind == TAIL_JACOBI) {
             for (int r = t0; r < o.nrows; r += nt) {
@@ -889,7 +969,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
             double *v = sh;
             for (int r = threadIdx.x; r < c.n; r += blockDim.x) v[r] = __ldcg(o.x + r);
             __syncthreads();
-            if (c.kind == 0) chol_solve_cta(c.n, L, c.dinv, v);
+            if (c.kind == 0) chol_solve_cta(c.n, L, dinv, v);
             else lu_solve_cta(c.n, c.LU, c.piv, v);
             for (int r = threadIdx.x; r < c.n; r += blockDim.x) o.y[r] = v[r];
         }
