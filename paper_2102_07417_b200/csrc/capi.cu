@@ -115,7 +115,8 @@ struct amg_handle {
     double *hist = nullptr;
     int hist_cap = 0;
     // options
-    int tile_nnz = 2048, tile_rows = 256, stages = 3, ctas_per_sm = 0, force_graph = -1, batch = 8;
+    int tile_nnz = 2048, tile_rows = 256, stages = 2, ctas_per_sm = 0, force_graph = -1, batch = 8;
+    int persistent = 1;  // 1: grid = resident capacity, tiles round-robin; 0: one tile per CTA
     int lanes_override = 0;
     int pdl = 1;  // programmatic dependent launch between consecutive kernels
     // cluster tail: levels >= tail_level run inside one cluster kernel
@@ -762,6 +763,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "stages") { if (value < 1 || value > 8) return fail(AMG_E_ARG, "stages out of range"); h->stages = (int)value; return AMG_OK; }
     if (k == "tail_nnz") { h->tail_nnz = value; return AMG_OK; }
     if (k == "cluster") { if (value != 8 && value != 16 && value != 4 && value != 2 && value != 1) return fail(AMG_E_ARG, "cluster must be 1,2,4,8,16"); h->cluster = (int)value; return AMG_OK; }
+    if (k == "persistent") { h->persistent = value ? 1 : 0; return AMG_OK; }
     if (k == "ctas_per_sm") { h->ctas_per_sm = (int)value; return AMG_OK; }
     if (k == "lanes") { if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8) return fail(AMG_E_ARG, "lanes must be 0,1,2,4,8"); h->lanes_override = (int)value; return AMG_OK; }
     return fail(AMG_E_ARG, "amg_set_option: unknown key '" + k + "'");
@@ -977,6 +979,7 @@ int amg_finalize(amg_t *h)
     TRY(configure_kernels(h, &bps));
     const int per_sm = h->ctas_per_sm > 0 ? std::min(h->ctas_per_sm, bps) : bps;
     h->max_grid = h->sm_count * 8;
+    if (!h->persistent) h->stages = 1;  // one tile per CTA: a single staging buffer
     // halos (nranks > 1) + tile schedules
     for (int k = 0; k < nl; ++k) {
         LevelD &L = h->lv[k];
@@ -992,7 +995,7 @@ int amg_finalize(amg_t *h)
             if (!tiles.empty()) CK(cudaMemcpy(M.tiles, tiles.data(), tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
             const double avg = M.nrows ? (double)M.nnz / (double)M.nrows : 0.0;
             M.lanes = h->lanes_override ? h->lanes_override : (avg < 9.0 ? 1 : avg < 17.0 ? 2 : avg < 33.0 ? 4 : 8);
-            M.grid = std::max(1, std::min(M.ntiles, h->sm_count * per_sm));
+            M.grid = h->persistent ? std::max(1, std::min(M.ntiles, h->sm_count * per_sm)) : std::max(1, M.ntiles);
             h->max_grid = std::max(h->max_grid, M.grid);
         }
     }

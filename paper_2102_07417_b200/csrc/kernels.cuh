@@ -220,6 +220,7 @@ template <int NT>
 __device__ __forceinline__ void grid_finalize(double v, double *partials, unsigned *ticket, int fin, PcgCtl *ctl)
 {
     __shared__ int s_last;
+    __shared__ double s_red[NT / 32];
     if (threadIdx.x == 0) {
         partials[blockIdx.x] = v;
         __threadfence();
@@ -227,12 +228,11 @@ __device__ __forceinline__ void grid_finalize(double v, double *partials, unsign
         s_last = (t == gridDim.x - 1);
     }
     __syncthreads();
-    if (s_last && threadIdx.x < 32) {
+    if (s_last) {  // the whole last CTA folds the partials: fixed assignment + fixed tree
         __threadfence();
         double a = 0.0;
-        for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) a += __ldcg(partials + i);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) a += __ldcg(partials + i);
+        a = block_sum<NT>(a, s_red);
         if (threadIdx.x == 0) {
             apply_fin(fin, a, ctl);
             *ticket = 0u;
@@ -458,6 +458,7 @@ __global__ void __launch_bounds__(TILE_THREADS) spmv_tiles(const SpmvArgs a)
                                          : (((1u << LANES) - 1u) << ((threadIdx.x & 31) / LANES * LANES));
     double dacc = 0.0;
     const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;  // r.r: the partner is the value being written
 
     int i = 0;
     for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
@@ -482,6 +483,12 @@ __global__ void __launch_bounds__(TILE_THREADS) spmv_tiles(const SpmvArgs a)
             const int32_t *cs = reinterpret_cast<const int32_t *>(stage + L.vals_bytes);
             const int32_t *os = reinterpret_cast<const int32_t *>(stage + L.vals_bytes + L.cols_bytes);
             const int vdelta = d.k0 & ~1, cdelta = d.k0 & ~3, odelta = d.r0 & ~3;
+            // epilogue operands of this group's first row, fetched with the gathers
+            double bpre = 0.0, wpre = 0.0;
+            if (lane == 0 && grp < nrows) {
+                if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bpre = a.b[d.r0 + grp];
+                if (want_dot && !self_dot) wpre = a.dotw[d.r0 + grp];
+            }
             // phase 1: every product of the tile, flat over the threads so all
             // x gathers of the tile are in flight together; p_k = a_k * x[c_k]
             // overwrites a_k in place (rounded product, no FMA contraction).
@@ -499,9 +506,18 @@ __global__ void __launch_bounds__(TILE_THREADS) spmv_tiles(const SpmvArgs a)
                 const int lo = os[row - odelta], hi = os[row + 1 - odelta];
                 double sum = row_sum_staged<LANES>(vs, vdelta, lo, hi, lane, gmask);
                 if (lane == 0) {
-                    double yv = epilogue<EPI>(sum, a.b, row, a.omega);
+                    const bool first = (rr == grp);
+                    double yv;
+                    if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) {
+                        const double bv = first ? bpre : a.b[row];
+                        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+                        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+                        else yv = add(bv, sum);
+                    } else {
+                        yv = epilogue<EPI>(sum, a.b, row, a.omega);
+                    }
                     a.y[row] = yv;
-                    if (want_dot) dacc = fma(yv, a.dotw[row], dacc);
+                    if (want_dot) dacc = fma(yv, self_dot ? yv : (first ? wpre : a.dotw[row]), dacc);
                 }
             }
         }
