@@ -26,12 +26,19 @@
  * There is no CPU fallback: without a usable GPU every call fails with
  * AMG_E_CUDA.
  *
- * Multi-GPU: one process per GPU.  Every rank creates its handle with its
- * (rank, nranks) and the same 128-byte ncclUniqueId, declares the row
- * partition of every level with amg_set_partition (contiguous row ranges,
- * identical on all ranks) and uploads only ITS rows of each matrix, with
- * global column indices.  Halo plans and NCCL exchanges are built by
- * amg_finalize.  With nranks == 1 no partition call is needed.
+ * Multi-GPU: one process per GPU.  Rank 0 makes an ncclUniqueId with
+ * amg_nccl_unique_id and shares it (e.g. torch.distributed broadcast); every
+ * rank creates its handle with (rank, nranks, id), declares the contiguous row
+ * partition of every distributed level (amg_set_partition) and the first
+ * REPLICATED level (amg_set_agglomeration; levels from there down are held
+ * whole by every rank, the coarsest always is), then uploads its local
+ * matrices as produced by the host planner (paper_2102_07417_b200/partition.py):
+ * local rows, LOCAL column ids (owned columns first, then halo columns) and
+ * the halo plan of each matrix (amg_set_halo: per-peer receive counts in halo
+ * order, per-peer owned indices to send).  Row entries keep the reference
+ * order, so distributed SpMV rows are bit-identical to single-GPU ones; dots
+ * are per-rank partials all-gathered and summed in rank order.  With
+ * nranks == 1 none of these calls is needed.
  */
 #ifndef AMGB200_H
 #define AMGB200_H
@@ -83,11 +90,23 @@ int amg_get_version(void);
 int amg_set_levels(amg_t *h, int n_levels);
 /* starts[0..nranks]: rows [starts[r], starts[r+1]) of `level` belong to rank r. */
 int amg_set_partition(amg_t *h, int level, const int64_t *starts);
-/* This rank's rows of matrix `which` of `level`: local_nrows rows, CSR with
- * offsets[0..local_nrows] (offsets[0] == 0), GLOBAL column indices (sorted,
- * unique per row) and values; global_ncols = number of columns. */
-int amg_upload_matrix(amg_t *h, int level, int which, int64_t local_nrows, int64_t global_ncols,
+/* Matrix `which` of `level` (this rank's rows when the level is distributed):
+ * local_nrows rows, CSR offsets[0..local_nrows] (offsets[0] == 0), column ids
+ * in [0, ncols) in the reference's stored order, values.  ncols is the
+ * column-space size: global columns on one rank / replicated levels, owned +
+ * halo columns of the local block otherwise. */
+int amg_upload_matrix(amg_t *h, int level, int which, int64_t local_nrows, int64_t ncols,
                       const int64_t *offsets, const int32_t *cols, const double *vals);
+/* Multi-GPU (see top): 128-byte ncclUniqueId for amg_create (rank 0). */
+int amg_nccl_unique_id(void *out);
+/* Halo plan of an uploaded local matrix: columns [n_own, n_own + n_halo) are
+ * received, n_recv peers in order with recv_counts each; n_send peers get
+ * send_counts[i] owned entries listed (concatenated) in send_idx. */
+int amg_set_halo(amg_t *h, int level, int which, int64_t n_own, int64_t n_halo, int n_recv,
+                 const int *recv_peers, const int64_t *recv_counts, int n_send, const int *send_peers,
+                 const int64_t *send_counts, const int32_t *send_idx);
+/* First replicated level (its partition says where each rank's restricted piece goes). */
+int amg_set_agglomeration(amg_t *h, int level);
 /* inv_diag: this rank's rows (Jacobi) or NULL (FSAI). */
 int amg_set_smoother(amg_t *h, int level, int kind, double omega, const double *inv_diag, int64_t n);
 /* Dense coarsest factor, n x n row-major: lower Cholesky factor (upper part

@@ -25,6 +25,7 @@ EXPORTS = (
     "amg_set_partition", "amg_upload_matrix", "amg_set_smoother", "amg_upload_coarse",
     "amg_set_cycle", "amg_finalize", "amg_local_rows", "amg_spmv", "amg_smoother",
     "amg_coarse_solve", "amg_vcycle", "amg_pcg", "amg_get_stats", "amg_set_option", "amg_time_spmv",
+    "amg_nccl_unique_id", "amg_set_halo", "amg_set_agglomeration",
 )
 
 
@@ -83,6 +84,9 @@ def lib():
         "amg_get_stats": (I32, [P, ctypes.POINTER(Stats)]),
         "amg_set_option": (I32, [P, ctypes.c_char_p, I64]),
         "amg_time_spmv": (I32, [P, I32, I32, I32, ctypes.POINTER(D)]),
+        "amg_nccl_unique_id": (I32, [P]),
+        "amg_set_halo": (I32, [P, I32, I32, I64, I64, I32, P, P, I32, P, P, P]),
+        "amg_set_agglomeration": (I32, [P, I32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -53,7 +53,8 @@ namespace {
 struct DevMat {
     bool present = false;
     int64_t nrows = 0, ncols = 0, nnz = 0;  // local rows; extended column space
-    int64_t gncols = 0;                      // global columns
+    int64_t gncols = 0;                      // column-space size passed at upload
+    int64_t n_own = 0;                       // owned columns (== gncols without a halo plan)
     int32_t *off = nullptr, *col = nullptr;
     double *val = nullptr;
     TileDesc *tiles = nullptr;
@@ -142,6 +143,8 @@ struct amg_handle {
     double solve_ms = 0.0, e2e_ms = 0.0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     Comm comm;
+    int agglom_level = -1;     // nranks > 1: first replicated level (-1: none declared)
+    bool dist_dots = false;    // level-0 vectors are distributed: dots need a cross-rank sum
 };
 
 // ------------------------------------------------------------------ kernels dispatch
@@ -213,6 +216,62 @@ static int raise_smem_caps(int device)
 
 static int stage_smem(const amg_t *h) { return h->stages * stage_layout(h->tile_nnz, h->tile_rows).stage_bytes; }
 
+static int exchange(amg_t *h, const DevMat &M, double *x)
+{
+    if (h->nranks == 1 || M.halo.empty()) return AMG_OK;
+    const HaloPlan &P = M.halo;
+    NcclApi &api = nccl();
+    if (P.n_send > 0) {
+        int g = (int)std::min<int64_t>((P.n_send + VEC_THREADS - 1) / VEC_THREADS, (int64_t)h->sm_count * 4);
+        TRY(launch_k(h, halo_pack, std::max(g, 1), VEC_THREADS, 0, (const double *)x, (const int32_t *)P.send_idx,
+                     P.send_buf, P.n_send));
+    }
+    auto chk = [&](ncclResult_t r, const char *w) -> int {
+        if (r != ncclSuccess) return fail(AMG_E_NCCL, std::string(w) + ": " + api.GetErrorString(r));
+        return AMG_OK;
+    };
+    TRY(chk(api.GroupStart(), "ncclGroupStart"));
+    int64_t roff = P.n_own;
+    for (size_t i = 0; i < P.recv_peers.size(); ++i) {
+        TRY(chk(api.Recv(x + roff, (size_t)P.recv_counts[i], ncclDouble, P.recv_peers[i], h->comm.comm, h->stream), "ncclRecv"));
+        roff += P.recv_counts[i];
+    }
+    for (size_t i = 0; i < P.send_peers.size(); ++i)
+        TRY(chk(api.Send(P.send_buf + P.send_displ[i], (size_t)P.send_counts[i], ncclDouble, P.send_peers[i],
+                         h->comm.comm, h->stream), "ncclSend"));
+    TRY(chk(api.GroupEnd(), "ncclGroupEnd"));
+    return AMG_OK;
+}
+
+// Reductions: with distributed level-0 vectors a kernel's finalize stores the
+// rank's partial; the partials are all-gathered and summed in rank order.
+static int kfin(const amg_t *h, int fin) { return (h->dist_dots && fin != FIN_NONE) ? (int)FIN_LOCAL : fin; }
+
+static int post_fin(amg_t *h, int fin, const int *g1)
+{
+    if (!h->dist_dots || fin == FIN_NONE) return AMG_OK;
+    NcclApi &api = nccl();
+    ncclResult_t r = api.AllGather(&h->ctl->part_local, h->ctl->part_all, 1, ncclDouble, h->comm.comm, h->stream);
+    if (r != ncclSuccess) return fail(AMG_E_NCCL, std::string("ncclAllGather: ") + api.GetErrorString(r));
+    TRY(launch_k(h, fin_ranks, 1, 1, 0, h->ctl, fin, h->nranks, g1));
+    return AMG_OK;
+}
+
+// Agglomeration: every rank holds its piece of level k's vector at offset
+// starts[rank]; grouped in-place broadcasts make the full vector everywhere.
+static int allgather_level(amg_t *h, int k, double *y)
+{
+    NcclApi &api = nccl();
+    const std::vector<int64_t> &s = h->lv[k].starts;
+    ncclResult_t r = api.GroupStart();
+    for (int q = 0; q < h->nranks && r == ncclSuccess; ++q)
+        if (s[q + 1] > s[q]) r = api.Broadcast(y + s[q], y + s[q], (size_t)(s[q + 1] - s[q]), ncclDouble, q, h->comm.comm, h->stream);
+    ncclResult_t r2 = api.GroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+        return fail(AMG_E_NCCL, std::string("agglomeration broadcast: ") + api.GetErrorString(r != ncclSuccess ? r : r2));
+    return AMG_OK;
+}
+
 static int configure_kernels(amg_t *h, int *blocks_per_sm)
 {
     const int smem = stage_smem(h);
@@ -230,14 +289,9 @@ static int configure_kernels(amg_t *h, int *blocks_per_sm)
     return AMG_OK;
 }
 
-// halo exchange (nranks > 1): fills x[n_local ...] for matrix M from peers
-static int exchange(amg_t *h, const DevMat &M, double *x)
-{
-    if (h->nranks == 1 || M.halo.empty()) return AMG_OK;
-    int s = halo_exchange(h->comm, M.halo, x, h->stream);
-    if (s != 0) return fail(AMG_E_NCCL, halo_error());
-    return AMG_OK;
-}
+// Halo exchange (nranks > 1): pack the owned entries each peer needs, then
+// one grouped ncclSend/ncclRecv per peer into x[n_own ...] (plan order).
+static int exchange(amg_t *h, const DevMat &M, double *x);
 
 static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, int epi, const double *b, double omega,
                        const double *dotw, int fin, const int *g1, const int *g2)
@@ -259,6 +313,8 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         return AMG_OK;
     }
     TRY(exchange(h, M, const_cast<double *>(x)));
+    const int ufin = fin;
+    fin = kfin(h, fin);
     if (M.ntiles == 0) {
         if (fin != FIN_NONE) {
             VecArgs v{};
@@ -270,6 +326,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
             v.gate1 = g1;
             v.gate2 = g2;
             TRY(launch_k(h, vec_dot, 1, VEC_THREADS, 0, v));
+            TRY(post_fin(h, ufin, g1));
         }
         return AMG_OK;
     }
@@ -294,6 +351,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     a.gate1 = g1;
     a.gate2 = g2;
     TRY(launch_k(h, spmv_fn(epi, M.lanes), M.grid, TILE_THREADS, (size_t)stage_smem(h), a));
+    TRY(post_fin(h, ufin, g1));
     return AMG_OK;
 }
 
@@ -331,8 +389,9 @@ static int launch_dot(amg_t *h, const double *a, const double *b, int64_t n, int
     VecArgs v = vargs(h, n, g1, g2);
     v.p = a;
     v.q = b;
-    v.fin = fin;
+    v.fin = kfin(h, fin);
     TRY(launch_k(h, vec_dot, vec_grid(h, n), VEC_THREADS, 0, v));
+    TRY(post_fin(h, fin, g1));
     return AMG_OK;
 }
 
@@ -428,8 +487,9 @@ static int enqueue_smooth(amg_t *h, int k, const double *b, double *x, int steps
             v.omega = L.omega;
             v.mode = set ? 0 : 1;
             v.q = dw;
-            v.fin = dw ? f : FIN_NONE;
+            v.fin = dw ? kfin(h, f) : FIN_NONE;
             TRY(launch_k(h, jacobi_sweep, vec_grid(h, L.n), VEC_THREADS, 0, v));
+            if (dw) TRY(post_fin(h, f, g1));
         }
     }
     return AMG_OK;
@@ -450,7 +510,10 @@ static int enqueue_vcycle(amg_t *h, int k, const double *y, double *x, const int
         TRY(launch_spmv(h, L.m[AMG_A], x, L.r, EPI_RESID, y, 0.0, nullptr, FIN_NONE, g1, nullptr));
         r = L.r;
     }
-    TRY(launch_spmv(h, L.m[AMG_PT], r, C.y, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, g1, nullptr));
+    const bool agglom = h->nranks > 1 && (k + 1) == h->agglom_level;
+    double *yc = agglom ? C.y + C.starts[h->rank] : C.y;  // this rank's piece of the replicated level
+    TRY(launch_spmv(h, L.m[AMG_PT], r, yc, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, g1, nullptr));
+    if (agglom) TRY(allgather_level(h, k + 1, C.y));
     TRY(enqueue_vcycle(h, k + 1, C.y, C.x, g1, FIN_NONE, nullptr));
     const bool tail_on_p = (h->nu2 == 0);
     TRY(launch_spmv(h, L.m[AMG_P], C.x, x, h->nu1 > 0 ? EPI_ADD : EPI_PLAIN, x, 0.0, tail_on_p ? dotw : nullptr,
@@ -475,8 +538,9 @@ static int enqueue_pcg_body(amg_t *h, cudaGraphConditionalHandle handle, int use
         v.r = h->r;
         v.p = h->p;
         v.q = h->q;
-        v.fin = FIN_UPDATE;
+        v.fin = kfin(h, FIN_UPDATE);
         TRY(launch_k(h, pcg_update, vec_grid(h, n), VEC_THREADS, 0, v));
+        TRY(post_fin(h, FIN_UPDATE, act));
     }
     // every recompute_every iterations: r = b - A x     (:76-77)
     TRY(launch_spmv(h, A, h->x, h->r, EPI_RESID, h->b, 0.0, h->r, FIN_RECOMPUTE, act, &h->ctl->do_recompute));
@@ -769,6 +833,70 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     return fail(AMG_E_ARG, "amg_set_option: unknown key '" + k + "'");
 }
 
+int amg_nccl_unique_id(void *out)
+{
+    if (!out) return fail(AMG_E_ARG, "amg_nccl_unique_id: NULL output");
+    NcclApi &api = nccl();
+    if (!api.loaded) return fail(AMG_E_NCCL, "libnccl.so.2 could not be loaded");
+    ncclUniqueId id;
+    ncclResult_t r = api.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(AMG_E_NCCL, std::string("ncclGetUniqueId: ") + api.GetErrorString(r));
+    memcpy(out, &id, sizeof(id));
+    return AMG_OK;
+}
+
+int amg_set_halo(amg_t *h, int level, int which, int64_t n_own, int64_t n_halo, int n_recv, const int *recv_peers,
+                 const int64_t *recv_counts, int n_send, const int *send_peers, const int64_t *send_counts,
+                 const int32_t *send_idx)
+{
+    if (!h) return fail(AMG_E_ARG, "NULL handle");
+    if (h->finalized) return fail(AMG_E_STATE, "amg_set_halo: already finalized");
+    if (h->nranks == 1) return fail(AMG_E_ARG, "amg_set_halo: single-rank handle has no halos");
+    if (level < 0 || level >= (int)h->lv.size() || which < 0 || which > 4) return fail(AMG_E_ARG, "amg_set_halo: bad level / slot");
+    DevMat &M = h->lv[level].m[which];
+    if (!M.present) return fail(AMG_E_STATE, "amg_set_halo: upload the matrix first");
+    if (n_own < 0 || n_halo < 0 || n_own + n_halo != M.ncols) return fail(AMG_E_DIM, "amg_set_halo: n_own + n_halo must equal the local column count");
+    HaloPlan &P = M.halo;
+    halo_free(P);
+    P = HaloPlan();
+    P.n_own = n_own;
+    P.n_halo = n_halo;
+    M.n_own = n_own;
+    int64_t tot = 0;
+    for (int i = 0; i < n_recv; ++i) {
+        if (recv_peers[i] < 0 || recv_peers[i] >= h->nranks || recv_peers[i] == h->rank) return fail(AMG_E_ARG, "amg_set_halo: bad recv peer");
+        P.recv_peers.push_back(recv_peers[i]);
+        P.recv_counts.push_back(recv_counts[i]);
+        tot += recv_counts[i];
+    }
+    if (tot != n_halo) return fail(AMG_E_DIM, "amg_set_halo: receive counts do not add up to n_halo");
+    int64_t ns = 0;
+    for (int i = 0; i < n_send; ++i) {
+        if (send_peers[i] < 0 || send_peers[i] >= h->nranks || send_peers[i] == h->rank) return fail(AMG_E_ARG, "amg_set_halo: bad send peer");
+        P.send_peers.push_back(send_peers[i]);
+        P.send_counts.push_back(send_counts[i]);
+        P.send_displ.push_back(ns);
+        ns += send_counts[i];
+    }
+    for (int64_t i = 0; i < ns; ++i)
+        if (send_idx[i] < 0 || send_idx[i] >= n_own) return fail(AMG_E_ARG, "amg_set_halo: send index outside the owned range");
+    P.n_send = ns;
+    CK(cudaSetDevice(h->device));
+    TRY(dalloc(&P.send_idx, (size_t)ns + 1));
+    TRY(dalloc(&P.send_buf, (size_t)ns + 1));
+    if (ns) CK(cudaMemcpy(P.send_idx, send_idx, ns * sizeof(int32_t), cudaMemcpyHostToDevice));
+    return AMG_OK;
+}
+
+int amg_set_agglomeration(amg_t *h, int level)
+{
+    if (!h) return fail(AMG_E_ARG, "NULL handle");
+    if (h->finalized) return fail(AMG_E_STATE, "amg_set_agglomeration: already finalized");
+    if (level < 0 || level >= (int)h->lv.size()) return fail(AMG_E_ARG, "amg_set_agglomeration: bad level");
+    h->agglom_level = level;
+    return AMG_OK;
+}
+
 int amg_set_levels(amg_t *h, int n_levels)
 {
     if (!h) return fail(AMG_E_ARG, "NULL handle");
@@ -841,6 +969,7 @@ int amg_upload_matrix(amg_t *h, int level, int which, int64_t local_nrows, int64
     M.nrows = local_nrows;
     M.gncols = global_ncols;
     M.ncols = global_ncols;
+    M.n_own = global_ncols;
     M.nnz = nnz;
     // Local column numbering: on one rank global == local.  With nranks > 1
     // the halo plan (built at finalize) renumbers non-owned columns.
@@ -944,6 +1073,11 @@ int amg_finalize(amg_t *h)
     CK(cudaSetDevice(h->device));
     // A handle without a coarsest factor is a plain matrix container (spmv only).
     const bool container = (h->nc == 0);
+    if (h->nranks > 1 && !container) {
+        if (h->agglom_level < 0 || h->agglom_level > nl - 1)
+            return fail(AMG_E_STATE, "multi-GPU: amg_set_agglomeration must name a level <= the coarsest (replicated) level");
+        h->dist_dots = h->agglom_level > 0;
+    }
     // structural checks mirroring the Level / AmgHierarchy contract
     for (int k = 0; k < nl && !container; ++k) {
         LevelD &L = h->lv[k];
@@ -953,6 +1087,13 @@ int amg_finalize(amg_t *h)
             L.gn = L.n;
             L.n0 = 0;
             if (L.m[AMG_A].gncols != L.n) return fail(AMG_E_DIM, "level " + std::to_string(k) + ": A is not square");
+        } else if (k >= h->agglom_level) {  // replicated level: every rank holds all rows
+            L.gn = L.n;
+            L.n0 = 0;
+            if (L.m[AMG_A].gncols != L.n) return fail(AMG_E_DIM, "level " + std::to_string(k) + ": replicated A is not square");
+            if (k == h->agglom_level && k > 0 &&
+                ((int)L.starts.size() != h->nranks + 1 || L.starts[h->nranks] != L.n))
+                return fail(AMG_E_STATE, "level " + std::to_string(k) + ": agglomeration level needs its partition");
         } else {
             if ((int)L.starts.size() != h->nranks + 1) return fail(AMG_E_STATE, "level " + std::to_string(k) + ": partition missing");
             L.n0 = L.starts[h->rank];
@@ -969,9 +1110,16 @@ int amg_finalize(amg_t *h)
     for (int k = 0; k < nl; ++k) h->lv[k].n = h->lv[k].m[AMG_A].nrows;
     for (int k = 0; k < nl - 1 && !container; ++k) {
         LevelD &L = h->lv[k], &C = h->lv[k + 1];
-        if (L.m[AMG_P].nrows != L.n || L.m[AMG_P].gncols != (h->nranks == 1 ? C.n : C.gn))
-            return fail(AMG_E_DIM, "level " + std::to_string(k) + ": P shape does not match the levels");
-        if (L.m[AMG_PT].nrows != C.n) return fail(AMG_E_DIM, "level " + std::to_string(k) + ": Pt shape does not match");
+        if (h->nranks == 1) {
+            if (L.m[AMG_P].nrows != L.n || L.m[AMG_P].gncols != C.n)
+                return fail(AMG_E_DIM, "level " + std::to_string(k) + ": P shape does not match the levels");
+            if (L.m[AMG_PT].nrows != C.n) return fail(AMG_E_DIM, "level " + std::to_string(k) + ": Pt shape does not match");
+        } else {
+            const int64_t cown = (k + 1 >= h->agglom_level && k < h->agglom_level)
+                                     ? C.starts[h->rank + 1] - C.starts[h->rank] : C.n;
+            if (L.m[AMG_P].nrows != L.n) return fail(AMG_E_DIM, "level " + std::to_string(k) + ": P rows do not match");
+            if (L.m[AMG_PT].nrows != cown) return fail(AMG_E_DIM, "level " + std::to_string(k) + ": Pt rows do not match the coarse partition");
+        }
     }
     h->container = container;
     if (!container && h->nc != h->lv[nl - 1].gn) return fail(AMG_E_DIM, "coarsest factor size does not match the last level");
@@ -1071,11 +1219,7 @@ int amg_spmv(amg_t *h, int level, int which, const double *x, double *y, int on_
     const DevMat &M = h->lv[level].m[which];
     if (!M.present) return fail(AMG_E_ARG, "amg_spmv: matrix slot is empty");
     if (!x || !y) return fail(AMG_E_ARG, "amg_spmv: NULL vector");
-    int64_t xn = M.gncols;
-    if (h->nranks > 1) {
-        const std::vector<int64_t> &cs = (which == AMG_P) ? h->lv[level + 1].starts : h->lv[level].starts;
-        xn = cs[h->rank + 1] - cs[h->rank];
-    }
+    const int64_t xn = M.n_own;  // owned column slice (all columns on one rank / replicated levels)
     TRY(to_dev(h, h->tmp_in, x, xn, on_device));
     TRY(launch_spmv(h, M, h->tmp_in, h->tmp_out, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, nullptr, nullptr));
     TRY(from_dev(h, y, h->tmp_out, M.nrows, on_device));

@@ -41,8 +41,11 @@ enum Fin {
     FIN_RECOMPUTE,
     FIN_TRUE,
     FIN_RZ,
-    FIN_STORE  // store raw sum into ctl->scratch (tests / diagnostics)
+    FIN_STORE,  // store raw sum into ctl->scratch (tests / diagnostics)
+    FIN_LOCAL   // multi-GPU: this rank's partial -> ctl->part_local (all-gathered, then finalized)
 };
+
+constexpr int MAX_RANKS = 64;
 
 // Device-resident PCG state: the control flow of krylov.py:40-92 evaluated
 // on the GPU so an iteration never waits for the host.
@@ -59,6 +62,8 @@ struct PcgCtl {
     int pad_;
     double rtol, bnorm, rz, curv, alpha, beta, relres, curv_fail, scratch;
     double *hist;
+    double part_local;
+    double part_all[MAX_RANKS];
 };
 
 struct TileDesc {
@@ -210,6 +215,7 @@ __device__ void apply_fin(int fin, double v, PcgCtl *c)
         c->rz = v;
         break;
     case FIN_STORE: c->scratch = v; break;
+    case FIN_LOCAL: c->part_local = v; break;
     default: break;
     }
 }
@@ -629,6 +635,27 @@ __global__ void __launch_bounds__(VEC_THREADS) vec_copy(const VecArgs a)
     if (!gate_open(a.gate1, a.gate2)) return;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
         a.x[i] = a.p ? a.p[i] : 0.0;
+}
+
+// Multi-GPU: sum the all-gathered per-rank partials in rank order (the same
+// on every rank, so every rank takes the same control-flow decisions).
+__global__ void fin_ranks(PcgCtl *c, int fin, int nranks, const int *gate1)
+{
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(gate1, nullptr)) return;
+    double v = 0.0;
+    for (int r = 0; r < nranks; ++r) v += c->part_all[r];
+    apply_fin(fin, v, c);
+}
+
+// Halo pack: buf[i] = x[idx[i]] (owned entries a peer needs).
+__global__ void __launch_bounds__(VEC_THREADS) halo_pack(const double *x, const int32_t *idx, double *buf, int64_t n)
+{
+    pdl_launch();
+    pdl_wait();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        buf[i] = x[idx[i]];
 }
 
 // Loop continuation for the device while-loop graph.

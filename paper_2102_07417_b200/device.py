@@ -24,7 +24,14 @@ import numpy as np
 from . import _capi as C
 from .errors import AmgError, DimensionMismatchError
 
-__all__ = ["DeviceHierarchy", "DeviceMatrix", "DeviceVcycle", "model_bytes_flops"]
+__all__ = ["DeviceHierarchy", "DeviceMatrix", "DeviceVcycle", "model_bytes_flops", "nccl_unique_id"]
+
+
+def nccl_unique_id():
+    """128-byte NCCL unique id (rank 0 makes it, every rank passes it to from_plan)."""
+    buf = ctypes.create_string_buffer(128)
+    C.check(C.lib().amg_nccl_unique_id(buf), "amg_nccl_unique_id")
+    return buf.raw
 
 
 def _host_f64(x):
@@ -109,6 +116,80 @@ class DeviceHierarchy:
         C.check(L.amg_finalize(dh._h), "amg_finalize")
         return dh
 
+    @classmethod
+    def from_plan(cls, plan, device=0, nccl_id=None, options=None):
+        """Upload one rank's share of a partitioned hierarchy (``partition.plan_hierarchy``).
+
+        ``nccl_id``: the 128-byte id from :func:`nccl_unique_id` on rank 0,
+        shared with every rank; one process per GPU.
+        """
+        import ctypes as ct
+
+        idbuf = None
+        if plan.nranks > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise AmgError("from_plan: nranks > 1 needs the 128-byte NCCL unique id")
+            idbuf = ct.create_string_buffer(bytes(nccl_id), 128)
+        dh = cls(device=device, rank=plan.rank, nranks=plan.nranks, nccl_id=idbuf, options=options)
+        L = C.lib()
+        nl = len(plan.starts)
+        C.check(L.amg_set_levels(dh._h, nl), "amg_set_levels")
+        dh.n_levels = nl
+        dh.levels = []
+        if plan.nranks > 1:
+            for k in range(nl):
+                s = np.ascontiguousarray(plan.starts[k], dtype=np.int64)
+                C.check(L.amg_set_partition(dh._h, k, C.ptr(s)), "amg_set_partition")
+            C.check(L.amg_set_agglomeration(dh._h, int(min(plan.agglom_level, nl - 1))), "amg_set_agglomeration")
+        for k in range(nl):
+            info = {"n": plan.n_local(k) if plan.nranks > 1 else int(plan.mats[(k, "a")].csr.nrows), "nnz": {}}
+            for slot in ("a", "p", "pt", "g", "gt"):
+                lm = plan.mats.get((k, slot))
+                if lm is None:
+                    continue
+                dh._put(k, slot, lm.csr, info)
+                hp = lm.halo
+                if hp is not None and plan.nranks > 1:
+                    rp = np.asarray(hp.recv_peers, dtype=np.int32)
+                    rc = np.asarray(hp.recv_counts, dtype=np.int64)
+                    sp = np.asarray(hp.send_peers, dtype=np.int32)
+                    sc = np.asarray([i.size for i in hp.send_idx], dtype=np.int64)
+                    si = (np.concatenate(hp.send_idx) if hp.send_idx else np.zeros(0)).astype(np.int32)
+                    C.check(L.amg_set_halo(dh._h, k, C.SLOT[slot], hp.n_own, hp.n_halo, rp.size, C.ptr(rp), C.ptr(rc),
+                                           sp.size, C.ptr(sp), C.ptr(sc), C.ptr(si)), f"halo L{k}.{slot}")
+                    info.setdefault("n_own", {})[slot] = hp.n_own
+            if k in plan.smoothers:
+                kind, omega, inv = plan.smoothers[k]
+                if kind == "jacobi":
+                    inv = _host_f64(inv)
+                    C.check(L.amg_set_smoother(dh._h, k, C.AMG_SMOOTHER_JACOBI, omega, C.ptr(inv), inv.size), "smoother")
+                else:
+                    C.check(L.amg_set_smoother(dh._h, k, C.AMG_SMOOTHER_FSAI, omega, None, 0), "smoother")
+            dh.levels.append(info)
+        dh._upload_coarse(plan.factor_kind, plan.factor)
+        C.check(L.amg_set_cycle(dh._h, plan.nu1, plan.nu2), "amg_set_cycle")
+        dh.nu1, dh.nu2 = plan.nu1, plan.nu2
+        C.check(L.amg_finalize(dh._h), "amg_finalize")
+        dh.A0 = dh.matrix(0, "a")
+        dh.vcycle = DeviceVcycle(dh)
+        return dh
+
+    def _upload_coarse(self, kind, factor):
+        L = C.lib()
+        if kind in ("cholesky", "cholesky+shift"):
+            c, lower = factor
+            if not lower:
+                raise AmgError("expected a lower Cholesky factor (hierarchy.py:127)")
+            c = np.ascontiguousarray(np.tril(c), dtype=np.float64)
+            C.check(L.amg_upload_coarse(self._h, c.shape[0], C.ptr(c), C.AMG_COARSE_CHOLESKY, None), "amg_upload_coarse")
+        else:
+            lu, piv = factor
+            lu = np.ascontiguousarray(lu, dtype=np.float64)
+            piv = np.ascontiguousarray(piv, dtype=np.int32)
+            C.check(L.amg_upload_coarse(self._h, lu.shape[0], C.ptr(lu), C.AMG_COARSE_LU, C.ptr(piv)), "amg_upload_coarse")
+        self.factor_kind = kind
+        self.nc = int(np.asarray(factor[0]).shape[0])
+
     def _upload(self, h):
         L = C.lib()
         levels = h.levels
@@ -135,20 +216,7 @@ class DeviceHierarchy:
                 info["omega"] = float(sm.omega)
                 info["smoother"] = sm.kind
             self.levels.append(info)
-        kind = h.factor_kind
-        if kind in ("cholesky", "cholesky+shift"):
-            c, lower = h.factor
-            if not lower:
-                raise AmgError("expected a lower Cholesky factor (hierarchy.py:127)")
-            c = np.ascontiguousarray(np.tril(c), dtype=np.float64)
-            C.check(L.amg_upload_coarse(self._h, c.shape[0], C.ptr(c), C.AMG_COARSE_CHOLESKY, None), "amg_upload_coarse")
-        else:
-            lu, piv = h.factor
-            lu = np.ascontiguousarray(lu, dtype=np.float64)
-            piv = np.ascontiguousarray(piv, dtype=np.int32)
-            C.check(L.amg_upload_coarse(self._h, lu.shape[0], C.ptr(lu), C.AMG_COARSE_LU, C.ptr(piv)), "amg_upload_coarse")
-        self.factor_kind = kind
-        self.nc = int(levels[-1].a.nrows)
+        self._upload_coarse(h.factor_kind, h.factor)
         C.check(L.amg_set_cycle(self._h, int(h.config.nu1), int(h.config.nu2)), "amg_set_cycle")
         self.nu1, self.nu2 = int(h.config.nu1), int(h.config.nu2)
         C.check(L.amg_finalize(self._h), "amg_finalize")
@@ -203,6 +271,7 @@ class DeviceHierarchy:
     def spmv(self, level, slot, x):
         """``spmv(A, x)`` (``amgkit/sparse.py:203-217``) for an uploaded matrix."""
         nr, nc = self.levels[level]["shape"][slot]
+        nc = self.levels[level].get("n_own", {}).get(slot, nc)
         xin, dev = self._vec_in(x, nc, "spmv", (nr, nc))
         y = self._vec_out(xin, nr)
         C.check(C.lib().amg_spmv(self._h, level, C.SLOT[slot], C.ptr(xin), C.ptr(y), dev), "spmv")
