@@ -118,6 +118,10 @@ struct amg_handle {
     // options
     int tile_nnz = 2048, tile_rows = 256, stages = 2, ctas_per_sm = 0, force_graph = -1, batch = 8;
     int persistent = 1;  // 1: grid = resident capacity, tiles round-robin; 0: one tile per CTA
+    int ws = 0;          // warp-specialized tile kernel (producer warp + consumer warps)
+    int kernel = 2;      // 0: staged tiles (spmv_tiles / spmv_ws), 2: direct register kernel
+    int direct_ctas = 0; // direct kernel CTAs per SM (0 = occupancy)
+    int direct_per_sm = 8;
     int lanes_override = 0;
     int pdl = 1;  // programmatic dependent launch between consecutive kernels
     // cluster tail: levels >= tail_level run inside one cluster kernel
@@ -150,6 +154,46 @@ struct amg_handle {
 // ------------------------------------------------------------------ kernels dispatch
 
 typedef void (*SpmvFn)(const SpmvArgs);
+
+typedef void (*SpmvDirectFn)(const SpmvArgs, int);
+
+static SpmvDirectFn spmv_direct_fn(int epi, int lanes)
+{
+#define AMG_L(E)                                               \
+    switch (lanes) {                                           \
+    case 1: return spmv_direct<E, 1>;                          \
+    case 2: return spmv_direct<E, 2>;                          \
+    case 4: return spmv_direct<E, 4>;                          \
+    default: return spmv_direct<E, 8>;                         \
+    }
+    switch (epi) {
+    case EPI_PLAIN: AMG_L(EPI_PLAIN)
+    case EPI_RESID: AMG_L(EPI_RESID)
+    case EPI_AXPYW: AMG_L(EPI_AXPYW)
+    case EPI_SETW: AMG_L(EPI_SETW)
+    default: AMG_L(EPI_ADD)
+    }
+#undef AMG_L
+}
+
+static SpmvFn spmv_ws_fn(int epi, int lanes)
+{
+#define AMG_L(E)                                               \
+    switch (lanes) {                                           \
+    case 1: return spmv_ws<E, 1>;                              \
+    case 2: return spmv_ws<E, 2>;                              \
+    case 4: return spmv_ws<E, 4>;                              \
+    default: return spmv_ws<E, 8>;                             \
+    }
+    switch (epi) {
+    case EPI_PLAIN: AMG_L(EPI_PLAIN)
+    case EPI_RESID: AMG_L(EPI_RESID)
+    case EPI_AXPYW: AMG_L(EPI_AXPYW)
+    case EPI_SETW: AMG_L(EPI_SETW)
+    default: AMG_L(EPI_ADD)
+    }
+#undef AMG_L
+}
 
 static SpmvFn spmv_fn(int epi, int lanes)
 {
@@ -206,7 +250,10 @@ static int raise_smem_caps(int device)
         return AMG_OK;
     };
     for (int e = 0; e <= 4; ++e)
-        for (int l : {1, 2, 4, 8}) TRY(cap((const void *)spmv_fn(e, l)));
+        for (int l : {1, 2, 4, 8}) {
+            TRY(cap((const void *)spmv_fn(e, l)));
+            TRY(cap((const void *)spmv_ws_fn(e, l)));
+        }
     TRY(cap((const void *)coarse_solve_k));
     TRY(cap((const void *)tail_vcycle));
     CK(cudaFuncSetAttribute((const void *)tail_vcycle, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -279,9 +326,9 @@ static int configure_kernels(amg_t *h, int *blocks_per_sm)
     TRY(raise_smem_caps(h->device));
     for (int e = 0; e <= 4; ++e)
         for (int l : {1, 2, 4, 8}) {
-            SpmvFn f = spmv_fn(e, l);
+            SpmvFn f = h->ws ? spmv_ws_fn(e, l) : spmv_fn(e, l);
             int nb = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, TILE_THREADS, smem));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, h->ws ? WS_THREADS : TILE_THREADS, smem));
             best = std::min(best, nb);
         }
     if (best < 1) return fail(AMG_E_CUDA, "SpMV tile kernel does not fit on an SM with the chosen staging");
@@ -350,7 +397,12 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     a.ctl = h->ctl;
     a.gate1 = g1;
     a.gate2 = g2;
-    TRY(launch_k(h, spmv_fn(epi, M.lanes), M.grid, TILE_THREADS, (size_t)stage_smem(h), a));
+    if (h->kernel == 2) {
+        const int gpr = DIRECT_THREADS / M.lanes;  // row groups per CTA
+        int g = (int)std::min<int64_t>((M.nrows + gpr - 1) / gpr, (int64_t)h->sm_count * h->direct_per_sm);
+        TRY(launch_k(h, spmv_direct_fn(epi, M.lanes), std::max(g, 1), DIRECT_THREADS, 0, a, (int)M.nrows));
+    } else if (h->ws) TRY(launch_k(h, spmv_ws_fn(epi, M.lanes), M.grid, WS_THREADS, (size_t)stage_smem(h), a));
+    else TRY(launch_k(h, spmv_fn(epi, M.lanes), M.grid, TILE_THREADS, (size_t)stage_smem(h), a));
     TRY(post_fin(h, ufin, g1));
     return AMG_OK;
 }
@@ -828,6 +880,9 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "tail_nnz") { h->tail_nnz = value; return AMG_OK; }
     if (k == "cluster") { if (value != 8 && value != 16 && value != 4 && value != 2 && value != 1) return fail(AMG_E_ARG, "cluster must be 1,2,4,8,16"); h->cluster = (int)value; return AMG_OK; }
     if (k == "persistent") { h->persistent = value ? 1 : 0; return AMG_OK; }
+    if (k == "ws") { h->ws = value ? 1 : 0; return AMG_OK; }
+    if (k == "kernel") { h->kernel = (int)value; return AMG_OK; }
+    if (k == "direct_ctas") { h->direct_ctas = (int)value; return AMG_OK; }
     if (k == "ctas_per_sm") { h->ctas_per_sm = (int)value; return AMG_OK; }
     if (k == "lanes") { if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8) return fail(AMG_E_ARG, "lanes must be 0,1,2,4,8"); h->lanes_override = (int)value; return AMG_OK; }
     return fail(AMG_E_ARG, "amg_set_option: unknown key '" + k + "'");
@@ -1126,6 +1181,17 @@ int amg_finalize(amg_t *h)
     int bps = 1;
     TRY(configure_kernels(h, &bps));
     const int per_sm = h->ctas_per_sm > 0 ? std::min(h->ctas_per_sm, bps) : bps;
+    {
+        int best = 1 << 30;
+        for (int e = 0; e <= 4; ++e)
+            for (int l : {1, 2, 4, 8}) {
+                int nb = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_direct_fn(e, l), DIRECT_THREADS, 0));
+                best = std::min(best, nb);
+            }
+        h->direct_per_sm = h->direct_ctas > 0 ? std::min(h->direct_ctas, best) : best;
+        h->max_grid = std::max(h->max_grid, h->sm_count * h->direct_per_sm);
+    }
     h->max_grid = h->sm_count * 8;
     if (!h->persistent) h->stages = 1;  // one tile per CTA: a single staging buffer
     // halos (nranks > 1) + tile schedules
@@ -1142,7 +1208,11 @@ int amg_finalize(amg_t *h)
             TRY(dalloc(&M.tiles, tiles.size()));
             if (!tiles.empty()) CK(cudaMemcpy(M.tiles, tiles.data(), tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
             const double avg = M.nrows ? (double)M.nnz / (double)M.nrows : 0.0;
-            M.lanes = h->lanes_override ? h->lanes_override : (avg < 9.0 ? 1 : avg < 17.0 ? 2 : avg < 33.0 ? 4 : 8);
+            // direct kernel: one lane per row maximises rows in flight (measured on
+            // B200: 27-pt A 3.5 TB/s at 1 lane vs 2.4 at 4); wide rows split over lanes
+            M.lanes = h->lanes_override ? h->lanes_override
+                      : h->kernel == 2   ? (avg < 48.0 ? 1 : avg < 96.0 ? 4 : 8)
+                                         : (avg < 9.0 ? 1 : avg < 17.0 ? 2 : avg < 33.0 ? 4 : 8);
             M.grid = h->persistent ? std::max(1, std::min(M.ntiles, h->sm_count * per_sm)) : std::max(1, M.ntiles);
             h->max_grid = std::max(h->max_grid, M.grid);
         }

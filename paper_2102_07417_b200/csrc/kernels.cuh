@@ -142,6 +142,29 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
         : "memory");
 }
 
+// Bulk copy with an L2 eviction policy (matrix streams are read once:
+// evict_first keeps the gathered vectors resident in L2).
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, unsigned bytes, uint64_t *bar, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ double prod(double a, double x) { return __dmul_rn(a, x); }
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
 
@@ -502,7 +525,7 @@ __global__ void __launch_bounds__(TILE_THREADS) spmv_tiles(const SpmvArgs a)
                 const int nk = d.k1 - d.k0;
                 double *pv = vs + (d.k0 - vdelta);
                 const int32_t *pc = cs + (d.k0 - cdelta);
-#pragma unroll 4
+#pragma unroll 8
                 for (int k = threadIdx.x; k < nk; k += TILE_THREADS) pv[k] = prod(pv[k], __ldg(a.x + pc[k]));
             }
             __syncthreads();
@@ -539,6 +562,335 @@ __global__ void __launch_bounds__(TILE_THREADS) spmv_tiles(const SpmvArgs a)
     if (want_dot || a.fin != FIN_NONE) {
         double v = block_sum<TILE_THREADS>(dacc, red);
         grid_finalize<TILE_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
+// ---------------------------------------------------------------- SpMV, warp-specialized
+
+// Warp-specialized tile SpMV: warp WS_CONSUMERS (the producer) streams tiles
+// into a STAGES-deep smem ring with cp.async.bulk (evict-first L2 policy) and
+// never touches dynamic data, so it runs ahead of griddepcontrol.wait; each
+// consumer warp owns a contiguous slice of every tile's rows: it computes the
+// products of its slice (all x gathers of the slice in flight), then sums its
+// rows in the reference order -- warp-local work, no CTA barriers in the
+// loop; stages are recycled through full/empty mbarriers.
+constexpr int WS_CONSUMERS = 8;
+constexpr int WS_THREADS = 32 * (WS_CONSUMERS + 1);
+
+__device__ __forceinline__ void ws_issue(const SpmvArgs &a, const StageLayout &L, char *stage, uint64_t *bar, int t,
+                                         uint64_t pol)
+{
+    const TileDesc d = a.tiles[t];
+    const int nk = d.k1 - d.k0;
+    if (nk > a.tile_nnz) {
+        mbar_arrive_tx(bar, 0);
+        return;
+    }
+    const int va = d.k0 & ~1, ca = d.k0 & ~3, oa = d.r0 & ~3;
+    const unsigned vb = nk ? (unsigned)(((d.k1 - va) * 8 + 15) & ~15) : 0u;
+    const unsigned cb = nk ? (unsigned)(((d.k1 - ca) * 4 + 15) & ~15) : 0u;
+    const unsigned ob = (unsigned)(((d.r1 + 1 - oa) * 4 + 15) & ~15);
+    mbar_arrive_tx(bar, vb + cb + ob);
+    if (vb) bulk_g2s_hint(stage, a.val + va, vb, bar, pol);
+    if (cb) bulk_g2s_hint(stage + L.vals_bytes, a.col + ca, cb, bar, pol);
+    bulk_g2s_hint(stage + L.vals_bytes + L.cols_bytes, a.off + oa, ob, bar, pol);
+}
+
+template <int EPI, int LANES>
+__global__ void __launch_bounds__(WS_THREADS) spmv_ws(const SpmvArgs a)
+{
+    extern __shared__ __align__(128) char smem[];
+    __shared__ __align__(8) uint64_t full[8];
+    __shared__ __align__(8) uint64_t empty[8];
+    __shared__ double red[WS_THREADS / 32];
+
+    const StageLayout L = stage_layout(a.tile_nnz, a.tile_rows);
+    const int S = a.stages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool producer = (warp == WS_CONSUMERS);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], WS_CONSUMERS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int my_tiles = (a.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const uint64_t pol = policy_evict_first();
+    int issued = 0;
+    if (producer && lane == 0) {  // static data: stage the first S tiles before the dependency wait
+        for (; issued < S && issued < my_tiles; ++issued)
+            ws_issue(a, L, smem + issued * L.stage_bytes, &full[issued], blockIdx.x + issued * gridDim.x, pol);
+    }
+    pdl_launch();
+    pdl_wait();
+    const bool open = gate_open(a.gate1, a.gate2);
+    double dacc = 0.0;
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    if (producer) {
+        if (lane == 0) {
+            if (!open) {  // drain what is in flight before the CTA releases its smem
+                for (int i = 0; i < issued; ++i) mbar_wait(&full[i], 0u);
+            } else {
+                for (int i = issued; i < my_tiles; ++i) {
+                    const int s = i % S;
+                    mbar_wait(&empty[s], (unsigned)(((i / S) - 1) & 1));
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    ws_issue(a, L, smem + s * L.stage_bytes, &full[s], blockIdx.x + i * gridDim.x, pol);
+                }
+            }
+        }
+    } else if (open) {
+        constexpr int G = 32 / LANES;
+        const int grp = lane / LANES;
+        const int gl = lane % LANES;
+        const unsigned gmask = (LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << (grp * LANES));
+        for (int i = 0; i < my_tiles; ++i) {
+            const int t = blockIdx.x + i * gridDim.x;
+            const int s = i % S;
+            char *stage = smem + s * L.stage_bytes;
+            const TileDesc d = a.tiles[t];
+            const int nrows = d.r1 - d.r0;
+            // this warp's row slice of the tile
+            const int w0 = d.r0 + (int)(((long long)nrows * warp) / WS_CONSUMERS);
+            const int w1 = d.r0 + (int)(((long long)nrows * (warp + 1)) / WS_CONSUMERS);
+            double bpre = 0.0, wpre = 0.0;
+            if (gl == 0 && w0 + grp < w1) {
+                if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bpre = a.b[w0 + grp];
+                if (want_dot && !self_dot) wpre = a.dotw[w0 + grp];
+            }
+            mbar_wait(&full[s], (unsigned)((i / S) & 1));
+            if (d.k1 - d.k0 > a.tile_nnz) {
+                if (warp == 0 && lane == 0) {
+                    const int lo = a.off[d.r0], hi = a.off[d.r0 + 1];
+                    auto P = [&](int k) -> double { return prod(a.val[k], __ldg(a.x + a.col[k])); };
+                    double sum = add(P(lo), pairwise_sum(P, lo + 1, hi - lo - 1));
+                    double yv = epilogue<EPI>(sum, a.b, d.r0, a.omega);
+                    a.y[d.r0] = yv;
+                    if (want_dot) dacc = fma(yv, a.dotw[d.r0], dacc);
+                }
+            } else if (w0 < w1) {
+                double *vs = reinterpret_cast<double *>(stage);
+                const int32_t *cs = reinterpret_cast<const int32_t *>(stage + L.vals_bytes);
+                const int32_t *os = reinterpret_cast<const int32_t *>(stage + L.vals_bytes + L.cols_bytes);
+                const int vdelta = d.k0 & ~1, cdelta = d.k0 & ~3, odelta = d.r0 & ~3;
+                const int klo = os[w0 - odelta], khi = os[w1 - odelta];
+                {
+                    double *pv = vs - vdelta;
+                    const int32_t *pc = cs - cdelta;
+#pragma unroll 8
+                    for (int k = klo + lane; k < khi; k += 32) pv[k] = prod(pv[k], __ldg(a.x + pc[k]));
+                }
+                __syncwarp();
+                for (int row = w0 + grp; row < w1; row += G) {
+                    const int lo = os[row - odelta], hi = os[row + 1 - odelta];
+                    double sum = row_sum_staged<LANES>(vs, vdelta, lo, hi, gl, gmask);
+                    if (gl == 0) {
+                        const bool first = (row == w0 + grp);
+                        double yv;
+                        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) {
+                            const double bv = first ? bpre : a.b[row];
+                            if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+                            else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+                            else yv = add(bv, sum);
+                        } else {
+                            yv = epilogue<EPI>(sum, a.b, row, a.omega);
+                        }
+                        a.y[row] = yv;
+                        if (want_dot) dacc = fma(yv, self_dot ? yv : (first ? wpre : a.dotw[row]), dacc);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+    }
+    if ((want_dot || a.fin != FIN_NONE) && open) {
+        double v = block_sum<WS_THREADS>(dacc, red);
+        grid_finalize<WS_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
+// ---------------------------------------------------------------- SpMV, direct
+
+// Register-only CSR SpMV: a group of LANES lanes owns a row; every load of
+// the row (values, columns, then x gathers) is issued before the first add,
+// and the sum is formed in the reference order (numpy's 8 strided
+// accumulators over the lanes, shuffle-butterfly combine, sequential tail,
+// p0 first).  No shared memory and no barriers, so occupancy is limited only
+// by registers -- latency is hidden by many independent row groups.
+// Rows with n = len - 1 > DIRECT_MAXN fall back to lane 0 (pairwise_sum).
+constexpr int DIRECT_THREADS = 256;
+constexpr int DIRECT_MAXN = 128;
+
+template <int EPI, int LANES>
+__global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_direct(const SpmvArgs a, int nrows)
+{
+    __shared__ double red[DIRECT_THREADS / 32];
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    constexpr int M = 8 / LANES;        // accumulators per lane
+    const int lane = threadIdx.x % LANES;
+    const int grp_in_warp = (threadIdx.x & 31) / LANES;
+    const unsigned gmask = (LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << (grp_in_warp * LANES));
+    const int ngroups = gridDim.x * (DIRECT_THREADS / LANES);
+    const int g0 = blockIdx.x * (DIRECT_THREADS / LANES) + threadIdx.x / LANES;
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    const int32_t *__restrict__ off = a.off;
+    const int32_t *__restrict__ col = a.col;
+    const double *__restrict__ val = a.val;
+    const double *__restrict__ x = a.x;
+    double dacc = 0.0;
+    // row offsets of the next row are fetched one iteration ahead
+    int nlo = 0, nhi = 0;
+    if (g0 < nrows) {
+        nlo = __ldg(off + g0);
+        nhi = __ldg(off + g0 + 1);
+    }
+    for (int row = g0; row < nrows; row += ngroups) {
+        const int lo = nlo, hi = nhi;
+        if (row + ngroups < nrows) {
+            nlo = __ldg(off + row + ngroups);
+            nhi = __ldg(off + row + ngroups + 1);
+        }
+        const int n = hi - lo - 1;
+        double bv = 0.0, wv = 0.0;
+        if (lane == 0) {
+            if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
+            if (want_dot && !self_dot) wv = a.dotw[row];
+        }
+        double sum;
+        if (n < 0) {
+            sum = 0.0;
+        } else if (n < 8) {
+            // sequential: p0 + (((0 + p1) + p2) + ...); one lane per entry, gathered by shuffles
+            double pk = 0.0;
+            if (lane <= n) pk = prod(__ldg(val + lo + lane), __ldg(x + __ldg(col + lo + lane)));
+            if constexpr (LANES >= 8) {
+                double res = 0.0;
+#pragma unroll
+                for (int t = 1; t < 8; ++t) {
+                    const double v = __shfl_sync(gmask, pk, t, LANES);
+                    if (t <= n) res = add(res, v);
+                }
+                sum = add(__shfl_sync(gmask, pk, 0, LANES), res);
+            } else {
+                // fewer lanes than entries: each lane holds entries lane, lane+LANES, ...
+                double pe[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) pe[t] = 0.0;
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    if ((t % LANES) == lane && t <= n) pe[t] = prod(__ldg(val + lo + t), __ldg(x + __ldg(col + lo + t)));
+                double res = 0.0;
+#pragma unroll
+                for (int t = 1; t < 8; ++t) {
+                    const double v = (LANES == 1) ? pe[t] : __shfl_sync(gmask, pe[t], t % LANES, LANES);
+                    if (t <= n) res = add(res, v);
+                }
+                const double p0 = (LANES == 1) ? pe[0] : __shfl_sync(gmask, pe[0], 0, LANES);
+                sum = add(p0, res);
+            }
+        } else if (n <= DIRECT_MAXN) {
+            const int base = lo + 1;
+            const int main = n - (n % 8);
+            const int its = main / 8;
+            // tail (n % 8 entries) and p0: spread over the lanes, issued with the main loads
+            const int ntail = n - main;
+            constexpr int TT = (7 + LANES - 1) / LANES;  // tail entries per lane (tail <= 7)
+            double tpa[TT];
+            double p0 = 0.0;
+#pragma unroll
+            for (int j = 0; j < TT; ++j) {
+                const int t = lane + j * LANES;
+                tpa[j] = (t < ntail) ? prod(__ldg(val + base + main + t), __ldg(x + __ldg(col + base + main + t))) : 0.0;
+            }
+            if (lane == 0) p0 = prod(__ldg(val + lo), __ldg(x + __ldg(col + lo)));
+            // main rounds in chunks of R = LANES rounds: 8 loads in flight per lane per chunk
+            constexpr int R = LANES;
+            double acc[M];
+#pragma unroll
+            for (int m = 0; m < M; ++m) acc[m] = 0.0;
+            for (int c0 = 0; c0 < its; c0 += R) {
+                double pv[R][M];
+                int pc[R][M];
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+#pragma unroll
+                    for (int m = 0; m < M; ++m)
+                        if (c0 + r < its) {
+                            const int k = base + (c0 + r) * 8 + lane + m * LANES;
+                            pv[r][m] = __ldg(val + k);
+                            pc[r][m] = __ldg(col + k);
+                        }
+                double xg[R][M];
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+#pragma unroll
+                    for (int m = 0; m < M; ++m)
+                        if (c0 + r < its) xg[r][m] = __ldg(x + pc[r][m]);
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+#pragma unroll
+                    for (int m = 0; m < M; ++m)
+                        if (c0 + r < its) {
+                            const double pr = prod(pv[r][m], xg[r][m]);
+                            acc[m] = (c0 + r == 0) ? pr : add(acc[m], pr);
+                        }
+            }
+            double res;
+            if constexpr (LANES == 1) {
+                res = add(add(add(acc[0], acc[1]), add(acc[2], acc[3])), add(add(acc[4], acc[5]), add(acc[6], acc[7])));
+            } else if constexpr (LANES == 2) {
+                double u[4];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) u[m] = add(acc[m], __shfl_xor_sync(gmask, acc[m], 1));
+                res = add(add(u[0], u[1]), add(u[2], u[3]));
+            } else if constexpr (LANES == 4) {
+                double s0 = add(acc[0], __shfl_xor_sync(gmask, acc[0], 1));
+                double s1 = add(acc[1], __shfl_xor_sync(gmask, acc[1], 1));
+                s0 = add(s0, __shfl_xor_sync(gmask, s0, 2));
+                s1 = add(s1, __shfl_xor_sync(gmask, s1, 2));
+                res = add(s0, s1);
+            } else {
+                double t = acc[0];
+                t = add(t, __shfl_xor_sync(gmask, t, 1));
+                t = add(t, __shfl_xor_sync(gmask, t, 2));
+                t = add(t, __shfl_xor_sync(gmask, t, 4));
+                res = t;
+            }
+            // sequential tail on lane 0 (entries main..n-1 held by lanes t % LANES)
+#pragma unroll
+            for (int t = 0; t < 7; ++t) {
+                const double v = (LANES == 1) ? tpa[t] : __shfl_sync(gmask, tpa[t / LANES], t % LANES, LANES);
+                if (t < ntail) res = add(res, v);
+            }
+            sum = add(p0, res);
+        } else {
+            sum = 0.0;
+            if (lane == 0) {
+                auto P = [&](int k) -> double { return prod(__ldg(val + k), __ldg(x + __ldg(col + k))); };
+                sum = add(P(lo), pairwise_sum(P, lo + 1, n));
+            }
+        }
+        if (lane == 0) {
+            double yv;
+            if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+            else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+            else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+            else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+            else yv = sum;
+            a.y[row] = yv;
+            if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
+        }
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v = block_sum<DIRECT_THREADS>(dacc, red);
+        grid_finalize<DIRECT_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
     }
 }
 
