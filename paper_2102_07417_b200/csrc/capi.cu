@@ -59,6 +59,15 @@ struct DevMat {
     double *val = nullptr;
     TileDesc *tiles = nullptr;
     int ntiles = 0;
+    int32_t *pstart = nullptr;   // padded-aligned layout (spmv_vec), nullptr if unused
+    double *pval = nullptr;
+    int32_t *pcol = nullptr;
+    int pad_grid = 0;
+    TileDesc *wtiles = nullptr;  // warp tiles (<= wt_nnz entries, <= 32 rows)
+    int nwtiles = 0;
+    int wt_nnz = 256;
+    int wt_lanes = 1;
+    int wt_grid = 0;
     int lanes = 1;
     int grid = 0;
     HaloPlan halo;  // exchange feeding this matrix's halo columns (nranks > 1)
@@ -119,7 +128,9 @@ struct amg_handle {
     int tile_nnz = 2048, tile_rows = 256, stages = 2, ctas_per_sm = 0, force_graph = -1, batch = 8;
     int persistent = 1;  // 1: grid = resident capacity, tiles round-robin; 0: one tile per CTA
     int ws = 0;          // warp-specialized tile kernel (producer warp + consumer warps)
-    int kernel = 2;      // 0: staged tiles (spmv_tiles / spmv_ws), 2: direct register kernel
+    int kernel = 2;      // 0: staged CTA tiles (spmv_tiles / spmv_ws), 2: direct register kernel, 3: warp tiles
+    int wt_nnz = 256;    // warp-tile capacity (entries)
+    int pad_min = 8;     // matrices averaging >= pad_min entries/row get the padded-aligned layout (0 = off)
     int direct_ctas = 0; // direct kernel CTAs per SM (0 = occupancy)
     int direct_per_sm = 8;
     int lanes_override = 0;
@@ -154,6 +165,38 @@ struct amg_handle {
 // ------------------------------------------------------------------ kernels dispatch
 
 typedef void (*SpmvFn)(const SpmvArgs);
+
+static SpmvFn spmv_wt_fn(int epi, int lanes)
+{
+#define AMG_L(E)                                               \
+    switch (lanes) {                                           \
+    case 1: return spmv_wt<E, 1>;                              \
+    case 2: return spmv_wt<E, 2>;                              \
+    case 4: return spmv_wt<E, 4>;                              \
+    default: return spmv_wt<E, 8>;                             \
+    }
+    switch (epi) {
+    case EPI_PLAIN: AMG_L(EPI_PLAIN)
+    case EPI_RESID: AMG_L(EPI_RESID)
+    case EPI_AXPYW: AMG_L(EPI_AXPYW)
+    case EPI_SETW: AMG_L(EPI_SETW)
+    default: AMG_L(EPI_ADD)
+    }
+#undef AMG_L
+}
+
+typedef void (*SpmvVecFn)(const SpmvArgs, const PadArgs, int);
+
+static SpmvVecFn spmv_vec_fn(int epi)
+{
+    switch (epi) {
+    case EPI_PLAIN: return spmv_vec<EPI_PLAIN>;
+    case EPI_RESID: return spmv_vec<EPI_RESID>;
+    case EPI_AXPYW: return spmv_vec<EPI_AXPYW>;
+    case EPI_SETW: return spmv_vec<EPI_SETW>;
+    default: return spmv_vec<EPI_ADD>;
+    }
+}
 
 typedef void (*SpmvDirectFn)(const SpmvArgs, int);
 
@@ -253,6 +296,7 @@ static int raise_smem_caps(int device)
         for (int l : {1, 2, 4, 8}) {
             TRY(cap((const void *)spmv_fn(e, l)));
             TRY(cap((const void *)spmv_ws_fn(e, l)));
+            TRY(cap((const void *)spmv_wt_fn(e, l)));
         }
     TRY(cap((const void *)coarse_solve_k));
     TRY(cap((const void *)tail_vcycle));
@@ -397,7 +441,17 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     a.ctl = h->ctl;
     a.gate1 = g1;
     a.gate2 = g2;
-    if (h->kernel == 2) {
+    if (M.pstart) {
+        PadArgs pa{M.pstart, M.pval, M.pcol};
+        TRY(launch_k(h, spmv_vec_fn(epi), M.pad_grid, VEC_SPMV_THREADS, 0, a, pa, (int)M.nrows));
+    } else if (h->kernel == 3 && M.nwtiles > 0) {
+        SpmvArgs w = a;
+        w.tiles = M.wtiles;
+        w.ntiles = M.nwtiles;
+        w.tile_nnz = M.wt_nnz;
+        const size_t smem = (size_t)WT_WARPS * 2 * stage_layout(M.wt_nnz, WT_ROWS).stage_bytes;
+        TRY(launch_k(h, spmv_wt_fn(epi, M.wt_lanes), M.wt_grid, WT_THREADS, smem, w));
+    } else if (h->kernel == 2) {
         const int gpr = DIRECT_THREADS / M.lanes;  // row groups per CTA
         int g = (int)std::min<int64_t>((M.nrows + gpr - 1) / gpr, (int64_t)h->sm_count * h->direct_per_sm);
         TRY(launch_k(h, spmv_direct_fn(epi, M.lanes), std::max(g, 1), DIRECT_THREADS, 0, a, (int)M.nrows));
@@ -850,7 +904,7 @@ void amg_destroy(amg_t *h)
     auto F = [](void *p) { if (p) cudaFree(p); };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.tiles);
+            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol);
             halo_free(M.halo);
         }
         F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
@@ -882,6 +936,8 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "persistent") { h->persistent = value ? 1 : 0; return AMG_OK; }
     if (k == "ws") { h->ws = value ? 1 : 0; return AMG_OK; }
     if (k == "kernel") { h->kernel = (int)value; return AMG_OK; }
+    if (k == "pad_min") { h->pad_min = (int)value; return AMG_OK; }
+    if (k == "wt_nnz") { if (value < 64 || value > 1024) return fail(AMG_E_ARG, "wt_nnz out of range"); h->wt_nnz = (int)value; return AMG_OK; }
     if (k == "direct_ctas") { h->direct_ctas = (int)value; return AMG_OK; }
     if (k == "ctas_per_sm") { h->ctas_per_sm = (int)value; return AMG_OK; }
     if (k == "lanes") { if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8) return fail(AMG_E_ARG, "lanes must be 0,1,2,4,8"); h->lanes_override = (int)value; return AMG_OK; }
@@ -1207,6 +1263,66 @@ int amg_finalize(amg_t *h)
             M.ntiles = (int)tiles.size();
             TRY(dalloc(&M.tiles, tiles.size()));
             if (!tiles.empty()) CK(cudaMemcpy(M.tiles, tiles.data(), tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
+            {   // warp tiles: capacity covers the typical row so long rows stay rare
+                int maxlen = 0;
+                for (int64_t r = 0; r < M.nrows; ++r) maxlen = std::max(maxlen, off32[r + 1] - off32[r]);
+                int cap = h->wt_nnz;
+                while (cap < maxlen && cap < 1024) cap *= 2;
+                M.wt_nnz = cap;
+                std::vector<TileDesc> wt;
+                build_tiles(off32, M.nrows, cap, WT_ROWS, wt);
+                M.nwtiles = (int)wt.size();
+                TRY(dalloc(&M.wtiles, wt.size()));
+                if (!wt.empty()) CK(cudaMemcpy(M.wtiles, wt.data(), wt.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
+                const double rows_per_tile = wt.empty() ? 1.0 : (double)M.nrows / (double)wt.size();
+                M.wt_lanes = h->lanes_override ? h->lanes_override
+                             : rows_per_tile >= 24.0 ? 1 : rows_per_tile >= 12.0 ? 2 : rows_per_tile >= 6.0 ? 4 : 8;
+                const size_t smem = (size_t)WT_WARPS * 2 * stage_layout(cap, WT_ROWS).stage_bytes;
+                int nb = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_wt_fn(EPI_RESID, M.wt_lanes), WT_THREADS, smem));
+                nb = std::max(nb, 1);
+                const int warps_needed = (M.nwtiles + 1) / 2;  // >= 2 tiles per warp keeps the ring busy
+                M.wt_grid = std::max(1, std::min((warps_needed + WT_WARPS - 1) / WT_WARPS, h->sm_count * nb));
+                h->max_grid = std::max(h->max_grid, M.wt_grid);
+            }
+            if (h->pad_min > 0 && M.nrows > 0 && (double)M.nnz / (double)M.nrows >= (double)h->pad_min) {
+                // padded-aligned copy: row starts == 3 (mod 4) so entry 1 is 16-byte aligned
+                std::vector<int32_t> col_h(M.nnz);
+                std::vector<double> val_h(M.nnz);
+                if (M.nnz) {
+                    CK(cudaMemcpy(col_h.data(), M.col, M.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+                    CK(cudaMemcpy(val_h.data(), M.val, M.nnz * sizeof(double), cudaMemcpyDeviceToHost));
+                }
+                std::vector<int32_t> ps(M.nrows + 1);
+                int64_t pos = 3;
+                for (int64_t r = 0; r < M.nrows; ++r) {
+                    ps[r] = (int32_t)pos;
+                    const int64_t len = off32[r + 1] - off32[r];
+                    pos += len;
+                    pos += (3 - (pos % 4) + 4) % 4;  // next start == 3 (mod 4)
+                    if (pos >= INT32_MAX - 64) return fail(AMG_E_ARG, "padded layout exceeds int32 indexing");
+                }
+                ps[M.nrows] = (int32_t)pos;
+                const int64_t tot = pos + 16;  // vector over-read slack
+                std::vector<int32_t> pc(tot, 0);
+                std::vector<double> pv(tot, 0.0);
+                for (int64_t r = 0; r < M.nrows; ++r)
+                    for (int32_t k = off32[r]; k < off32[r + 1]; ++k) {
+                        pc[ps[r] + (k - off32[r])] = col_h[k];
+                        pv[ps[r] + (k - off32[r])] = val_h[k];
+                    }
+                TRY(dalloc(&M.pstart, ps.size()));
+                TRY(dalloc(&M.pcol, pc.size()));
+                TRY(dalloc(&M.pval, pv.size()));
+                CK(cudaMemcpy(M.pstart, ps.data(), ps.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                CK(cudaMemcpy(M.pcol, pc.data(), pc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                CK(cudaMemcpy(M.pval, pv.data(), pv.size() * sizeof(double), cudaMemcpyHostToDevice));
+                int nb = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_vec_fn(EPI_RESID), VEC_SPMV_THREADS, 0));
+                M.pad_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
+                                                                        (int64_t)h->sm_count * std::max(nb, 1)));
+                h->max_grid = std::max(h->max_grid, M.pad_grid);
+            }
             const double avg = M.nrows ? (double)M.nnz / (double)M.nrows : 0.0;
             // direct kernel: one lane per row maximises rows in flight (measured on
             // B200: 27-pt A 3.5 TB/s at 1 lane vs 2.4 at 4); wide rows split over lanes

@@ -723,6 +723,12 @@ __global__ void __launch_bounds__(WS_THREADS) spmv_ws(const SpmvArgs a)
 // by registers -- latency is hidden by many independent row groups.
 // Rows with n = len - 1 > DIRECT_MAXN fall back to lane 0 (pairwise_sum).
 constexpr int DIRECT_THREADS = 256;
+
+// matrix loads go through L1: with one lane per row a warp's 32 rows are
+// contiguous, and L1 merges the per-lane strided loads (evict-first measured
+// slower on B200: 255 vs 204 us for the 27-pt A0)
+__device__ __forceinline__ double ldm(const double *p) { return __ldg(p); }
+__device__ __forceinline__ int ldm(const int32_t *p) { return __ldg(p); }
 constexpr int DIRECT_MAXN = 128;
 
 template <int EPI, int LANES>
@@ -769,7 +775,7 @@ __global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_direct(const SpmvArgs 
         } else if (n < 8) {
             // sequential: p0 + (((0 + p1) + p2) + ...); one lane per entry, gathered by shuffles
             double pk = 0.0;
-            if (lane <= n) pk = prod(__ldg(val + lo + lane), __ldg(x + __ldg(col + lo + lane)));
+            if (lane <= n) pk = prod(ldm(val + lo + lane), __ldg(x + ldm(col + lo + lane)));
             if constexpr (LANES >= 8) {
                 double res = 0.0;
 #pragma unroll
@@ -785,7 +791,7 @@ __global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_direct(const SpmvArgs 
                 for (int t = 0; t < 8; ++t) pe[t] = 0.0;
 #pragma unroll
                 for (int t = 0; t < 8; ++t)
-                    if ((t % LANES) == lane && t <= n) pe[t] = prod(__ldg(val + lo + t), __ldg(x + __ldg(col + lo + t)));
+                    if ((t % LANES) == lane && t <= n) pe[t] = prod(ldm(val + lo + t), __ldg(x + ldm(col + lo + t)));
                 double res = 0.0;
 #pragma unroll
                 for (int t = 1; t < 8; ++t) {
@@ -807,9 +813,9 @@ __global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_direct(const SpmvArgs 
 #pragma unroll
             for (int j = 0; j < TT; ++j) {
                 const int t = lane + j * LANES;
-                tpa[j] = (t < ntail) ? prod(__ldg(val + base + main + t), __ldg(x + __ldg(col + base + main + t))) : 0.0;
+                tpa[j] = (t < ntail) ? prod(ldm(val + base + main + t), __ldg(x + ldm(col + base + main + t))) : 0.0;
             }
-            if (lane == 0) p0 = prod(__ldg(val + lo), __ldg(x + __ldg(col + lo)));
+            if (lane == 0) p0 = prod(ldm(val + lo), __ldg(x + ldm(col + lo)));
             // main rounds in chunks of R = LANES rounds: 8 loads in flight per lane per chunk
             constexpr int R = LANES;
             double acc[M];
@@ -824,8 +830,8 @@ __global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_direct(const SpmvArgs 
                     for (int m = 0; m < M; ++m)
                         if (c0 + r < its) {
                             const int k = base + (c0 + r) * 8 + lane + m * LANES;
-                            pv[r][m] = __ldg(val + k);
-                            pc[r][m] = __ldg(col + k);
+                            pv[r][m] = ldm(val + k);
+                            pc[r][m] = ldm(col + k);
                         }
                 double xg[R][M];
 #pragma unroll
@@ -873,7 +879,7 @@ __global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_direct(const SpmvArgs 
         } else {
             sum = 0.0;
             if (lane == 0) {
-                auto P = [&](int k) -> double { return prod(__ldg(val + k), __ldg(x + __ldg(col + k))); };
+                auto P = [&](int k) -> double { return prod(ldm(val + k), __ldg(x + ldm(col + k))); };
                 sum = add(P(lo), pairwise_sum(P, lo + 1, n));
             }
         }
@@ -891,6 +897,256 @@ __global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_direct(const SpmvArgs 
     if (want_dot || a.fin != FIN_NONE) {
         double v = block_sum<DIRECT_THREADS>(dacc, red);
         grid_finalize<DIRECT_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
+// ---------------------------------------------------------------- SpMV, warp tiles
+
+// Warp-tile SpMV: rows are cut into small tiles (<= wt_nnz entries, <= 32
+// rows); every warp streams its own tiles into a private 2-slot smem ring
+// with cp.async.bulk issued by its lane 0 (per-warp mbarriers), so the matrix
+// never passes through L1 and a warp never waits on another warp.  Per tile:
+// all products of the tile are formed flat over the 32 lanes (every x gather
+// of the tile in flight at once), then rows are summed in the reference
+// order by LANES-wide groups.  The first two tiles of each warp are static
+// data and are staged before griddepcontrol.wait.
+constexpr int WT_WARPS = 8;
+constexpr int WT_THREADS = 32 * WT_WARPS;
+constexpr int WT_ROWS = 32;
+
+template <int EPI, int LANES>
+__global__ void __launch_bounds__(WT_THREADS, 4) spmv_wt(const SpmvArgs a)
+{
+    extern __shared__ __align__(128) char smem[];
+    __shared__ __align__(8) uint64_t full[WT_WARPS][2];
+    __shared__ TileDesc sdesc[WT_WARPS][2];  // descriptor of the tile in each slot (written at issue)
+    __shared__ double red[WT_THREADS / 32];
+    const StageLayout L = stage_layout(a.tile_nnz, WT_ROWS);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    char *wbuf = smem + (size_t)warp * 2 * L.stage_bytes;
+    const int wg = blockIdx.x * WT_WARPS + warp;
+    const int nw = gridDim.x * WT_WARPS;
+    const int my_tiles = (a.ntiles > wg) ? (a.ntiles - wg + nw - 1) / nw : 0;
+    const uint64_t pol = policy_evict_first();
+    if (lane == 0) {
+        mbar_init(&full[warp][0], 1);
+        mbar_init(&full[warp][1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int i = 0; i < 2 && i < my_tiles; ++i) {
+            sdesc[warp][i] = a.tiles[wg + i * nw];
+            ws_issue(a, L, wbuf + i * L.stage_bytes, &full[warp][i], wg + i * nw, pol);
+        }
+    }
+    __syncwarp();
+    pdl_launch();
+    pdl_wait();
+    const bool open = gate_open(a.gate1, a.gate2);
+    if (!open) {
+        if (lane == 0)
+            for (int i = 0; i < 2 && i < my_tiles; ++i) mbar_wait(&full[warp][i], 0u);
+        return;  // uniform over the grid: no reduction follows
+    }
+    constexpr int G = 32 / LANES;
+    const int grp = lane / LANES;
+    const int gl = lane % LANES;
+    const unsigned gmask = (LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << (grp * LANES));
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    double dacc = 0.0;
+    for (int i = 0; i < my_tiles; ++i) {
+        const int s = i & 1;
+        char *stage = wbuf + s * L.stage_bytes;
+        const TileDesc d = sdesc[warp][s];
+        const int nrows = d.r1 - d.r0;
+        // epilogue operands of this group's first row, in flight with the tile
+        double bpre = 0.0, wpre = 0.0;
+        if (gl == 0 && grp < nrows) {
+            if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bpre = a.b[d.r0 + grp];
+            if (want_dot && !self_dot) wpre = a.dotw[d.r0 + grp];
+        }
+        mbar_wait(&full[warp][s], (unsigned)((i >> 1) & 1));
+        if (d.k1 - d.k0 > a.tile_nnz) {  // one row longer than the tile capacity: straight from global
+            double sum = 0.0;
+            if (lane == 0) {
+                const int lo = a.off[d.r0], hi = a.off[d.r0 + 1];
+                auto P = [&](int k) -> double { return prod(a.val[k], __ldg(a.x + a.col[k])); };
+                sum = add(P(lo), pairwise_sum(P, lo + 1, hi - lo - 1));
+                double yv = epilogue<EPI>(sum, a.b, d.r0, a.omega);
+                a.y[d.r0] = yv;
+                if (want_dot) dacc = fma(yv, a.dotw[d.r0], dacc);
+            }
+        } else {
+            double *vs = reinterpret_cast<double *>(stage);
+            const int32_t *cs = reinterpret_cast<const int32_t *>(stage + L.vals_bytes);
+            const int32_t *os = reinterpret_cast<const int32_t *>(stage + L.vals_bytes + L.cols_bytes);
+            const int vdelta = d.k0 & ~1, cdelta = d.k0 & ~3, odelta = d.r0 & ~3;
+            {
+                const int nk = d.k1 - d.k0;
+                double *pv = vs + (d.k0 - vdelta);
+                const int32_t *pc = cs + (d.k0 - cdelta);
+#pragma unroll 8
+                for (int k = lane; k < nk; k += 32) pv[k] = prod(pv[k], __ldg(a.x + pc[k]));
+            }
+            __syncwarp();
+            for (int rr = grp; rr < nrows; rr += G) {
+                const int row = d.r0 + rr;
+                const int lo = os[row - odelta], hi = os[row + 1 - odelta];
+                double sum = row_sum_staged<LANES>(vs, vdelta, lo, hi, gl, gmask);
+                if (gl == 0) {
+                    const bool first = (rr == grp);
+                    double yv;
+                    if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) {
+                        const double bv = first ? bpre : a.b[row];
+                        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+                        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+                        else yv = add(bv, sum);
+                    } else {
+                        yv = epilogue<EPI>(sum, a.b, row, a.omega);
+                    }
+                    a.y[row] = yv;
+                    if (want_dot) dacc = fma(yv, self_dot ? yv : (first ? wpre : a.dotw[row]), dacc);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0 && i + 2 < my_tiles) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            sdesc[warp][s] = a.tiles[wg + (i + 2) * nw];
+            ws_issue(a, L, stage, &full[warp][s], wg + (i + 2) * nw, pol);
+        }
+        __syncwarp();
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v = block_sum<WT_THREADS>(dacc, red);
+        grid_finalize<WT_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
+// ---------------------------------------------------------------- SpMV, padded-aligned rows
+
+// Padded-aligned CSR (device-only layout for rows averaging >= ~12 entries):
+// row i's entries start at pstart[i] with pstart[i] % 4 == 3, so entry 1 --
+// the start of numpy's 8-wide rounds -- is 16-byte aligned for both the
+// values (double2) and the columns (int4).  One lane per row; a round of 8
+// entries is 4 double2 + 2 int4 loads (L1 sector lookups per entry drop ~3x
+// versus scalar loads), gathers and sums exactly as the reference orders them.
+constexpr int VEC_SPMV_THREADS = 256;
+
+struct PadArgs {
+    const int32_t *pstart;  // nrows + 1 padded row starts (== 3 mod 4)
+    const double *pval;     // padded values (16-byte aligned base)
+    const int32_t *pcol;    // padded columns
+};
+
+template <int EPI>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_vec(const SpmvArgs a, const PadArgs pa, int nrows)
+{
+    __shared__ double red[VEC_SPMV_THREADS / 32];
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const int nthreads = gridDim.x * VEC_SPMV_THREADS;
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    const double *__restrict__ x = a.x;
+    double dacc = 0.0;
+    int row = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x;
+    int nlo = 0, nhi = 0, nps = 0;
+    if (row < nrows) {
+        nlo = __ldg(a.off + row);
+        nhi = __ldg(a.off + row + 1);
+        nps = __ldg(pa.pstart + row);
+    }
+    for (; row < nrows; row += nthreads) {
+        const int len = nhi - nlo;
+        const int ps = nps;
+        if (row + nthreads < nrows) {
+            nlo = __ldg(a.off + row + nthreads);
+            nhi = __ldg(a.off + row + nthreads + 1);
+            nps = __ldg(pa.pstart + row + nthreads);
+        }
+        double bv = 0.0, wv = 0.0;
+        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
+        if (want_dot && !self_dot) wv = a.dotw[row];
+        const int n = len - 1;
+        double sum = 0.0;
+        if (n >= 0 && n <= 128) {
+            const double p0 = prod(__ldg(pa.pval + ps), __ldg(x + __ldg(pa.pcol + ps)));
+            const int b1 = ps + 1;  // 16-byte aligned
+            const double2 *v2 = reinterpret_cast<const double2 *>(pa.pval + b1);
+            const int4 *c4 = reinterpret_cast<const int4 *>(pa.pcol + b1);
+            auto round8 = [&](int r, double p[8]) {
+                const int4 ca = __ldg(c4 + 2 * r), cb = __ldg(c4 + 2 * r + 1);
+                const double2 va = __ldg(v2 + 4 * r), vb = __ldg(v2 + 4 * r + 1), vc = __ldg(v2 + 4 * r + 2),
+                              vd = __ldg(v2 + 4 * r + 3);
+                p[0] = prod(va.x, __ldg(x + ca.x));
+                p[1] = prod(va.y, __ldg(x + ca.y));
+                p[2] = prod(vb.x, __ldg(x + ca.z));
+                p[3] = prod(vb.y, __ldg(x + ca.w));
+                p[4] = prod(vc.x, __ldg(x + cb.x));
+                p[5] = prod(vc.y, __ldg(x + cb.y));
+                p[6] = prod(vd.x, __ldg(x + cb.z));
+                p[7] = prod(vd.y, __ldg(x + cb.w));
+            };
+            // masked round (entries beyond `cnt` belong to padding / the next row: not used)
+            auto round8m = [&](int r, int cnt, double p[8]) {
+                const int4 ca = __ldg(c4 + 2 * r);
+                const int4 cb = cnt > 4 ? __ldg(c4 + 2 * r + 1) : make_int4(0, 0, 0, 0);
+                const double2 va = __ldg(v2 + 4 * r);
+                const double2 vb = cnt > 2 ? __ldg(v2 + 4 * r + 1) : make_double2(0.0, 0.0);
+                const double2 vc = cnt > 4 ? __ldg(v2 + 4 * r + 2) : make_double2(0.0, 0.0);
+                const double2 vd = cnt > 6 ? __ldg(v2 + 4 * r + 3) : make_double2(0.0, 0.0);
+                const int cc[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+                const double vv[8] = {va.x, va.y, vb.x, vb.y, vc.x, vc.y, vd.x, vd.y};
+#pragma unroll
+                for (int t = 0; t < 8; ++t) p[t] = (t < cnt) ? prod(vv[t], __ldg(x + cc[t])) : 0.0;
+            };
+            double res;
+            // the first round is shared by short (n < 8) and long rows, so a warp
+            // with mixed row lengths diverges only in the (cheap) arithmetic
+            double acc[8];
+            round8m(0, n < 8 ? n : 8, acc);
+            if (n < 8) {
+                res = 0.0;
+#pragma unroll
+                for (int t = 0; t < 7; ++t)
+                    if (t < n) res = add(res, acc[t]);
+            } else {
+                const int main = n - (n % 8);
+                const int its = main / 8;
+                for (int r = 1; r < its; ++r) {
+                    double p[8];
+                    round8(r, p);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[j] = add(acc[j], p[j]);
+                }
+                res = add(add(add(acc[0], acc[1]), add(acc[2], acc[3])), add(add(acc[4], acc[5]), add(acc[6], acc[7])));
+                const int ntail = n - main;
+                if (ntail > 0) {
+                    double p[8];
+                    round8m(its, ntail, p);
+#pragma unroll
+                    for (int t = 0; t < 7; ++t)
+                        if (t < ntail) res = add(res, p[t]);
+                }
+            }
+            sum = add(p0, res);
+        } else if (n > 128) {
+            auto P = [&](int k) -> double { return prod(__ldg(pa.pval + ps + k), __ldg(x + __ldg(pa.pcol + ps + k))); };
+            sum = add(P(0), pairwise_sum(P, 1, n));
+        }
+        double yv;
+        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+        else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+        else yv = sum;
+        a.y[row] = yv;
+        if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
+        grid_finalize<VEC_SPMV_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
     }
 }
 
