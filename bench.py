@@ -300,7 +300,7 @@ def run_amgb200(args):
         },
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": ncu_traffic(args.config), "kernel": "spmv_tiles on A0 (plain epilogue)",
+            "traffic": ncu_traffic(args.config), "kernel": "spmv_vec on A0 (plain epilogue, padded-aligned layout)",
             "bytes_per_launch": k_bytes, "ms_per_launch": k_ms, "peak_source": peak_src,
         },
         "e2e": {"value": e2e_ms_iter, "unit": "ms/iter", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
