@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--cache", default=os.path.join(ROOT, "hier_cache"))
     ap.add_argument("--cpu-iters", type=int, default=2, help="PCG iterations in the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of the row partition")
+    ap.add_argument("--agglom-rows", type=int, default=50000, help="levels with <= this many rows are replicated")
+    ap.add_argument("--partitioned", action="store_true", help="use the partition-plan upload even at N=1")
+    ap.add_argument("--watchdog", type=float, default=900.0, help="abort (exit 3) if the GPU phase exceeds this")
     return ap.parse_args()
 
 
@@ -215,8 +219,34 @@ def run_amgb200(args):
     torch.cuda.set_device(local)
     h, b_host = load(args)
     n = b_host.size
-    dh = amg.DeviceHierarchy.from_reference(h, device=local)
-    b_dev = torch.tensor(b_host, device=f"cuda:{local}")
+
+    def _watchdog():
+        time.sleep(args.watchdog)
+        print(json.dumps({"error": f"bench watchdog: GPU phase exceeded {args.watchdog} s (rank {rank})"}), flush=True)
+        os._exit(3)
+
+    threading.Thread(target=_watchdog, daemon=True).start()
+    partitioned = (world > 1 and not args.replicas) or args.partitioned
+    if partitioned:
+        from paper_2102_07417_b200.partition import plan_hierarchy
+
+        plan = plan_hierarchy(h, world, rank, agglom_rows=args.agglom_rows)
+        uid = None
+        if world > 1:
+            t = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local}")
+            if rank == 0:
+                t.copy_(torch.tensor(list(amg.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(t, 0)
+            uid = bytes(t.cpu().tolist())
+        dh = amg.DeviceHierarchy.from_plan(plan, device=local, nccl_id=uid)
+        s0 = plan.starts[0]
+        lo, hi = (int(s0[rank]), int(s0[rank + 1])) if world > 1 else (0, n)
+    else:
+        plan = None
+        dh = amg.DeviceHierarchy.from_reference(h, device=local)
+        lo, hi = 0, n
+    b_local = np.ascontiguousarray(b_host[lo:hi])
+    b_dev = torch.tensor(b_local, device=f"cuda:{local}")
     cfg = amg.KrylovConfig(rtol=1e-8, max_iters=5000)
     bytes_iter, flops_iter = model_bytes_flops(h)
 
@@ -248,11 +278,19 @@ def run_amgb200(args):
     # parity record of this run
     from oracle import solve as O  # checker only: true residual of the device answer
     x = res.x.cpu().numpy()
+    if world > 1 and partitioned:
+        m = int(max(np.diff(plan.starts[0])))
+        tx = torch.zeros(m, dtype=torch.float64, device=f"cuda:{local}")
+        tx[: x.size] = torch.from_numpy(x)
+        outs = [torch.zeros(m, dtype=torch.float64, device=f"cuda:{local}") for _ in range(world)]
+        dist.all_gather(outs, tx)
+        s0 = plan.starts[0]
+        x = np.concatenate([outs[q].cpu().numpy()[: s0[q + 1] - s0[q]] for q in range(world)])
     true_rel = float(np.linalg.norm(b_host - O.spmv(h.levels[0].a, x)) / np.linalg.norm(b_host))
     ref_its = h.meta.get("extra", {}).get("reference_solve", {}).get("n_iterations")
 
     # e2e: public API with pinned host buffers, copies inside the timed region
-    b_pin = torch.from_numpy(b_host).pin_memory()
+    b_pin = torch.from_numpy(b_local).pin_memory()
     amg.pcg(dh.A0, b_pin, apply_m=dh.vcycle, config=cfg)
     barrier()
     t0 = time.perf_counter()
@@ -264,7 +302,7 @@ def run_amgb200(args):
     e2e_ms_iter = (time.perf_counter() - t0) * 1e3 / max(e_it, 1)
 
     # dominant kernel: SpMV on A0 (tile kernel), timed alone with CUDA events on the library stream
-    a0 = h.levels[0].a
+    a0 = plan.mats[(0, "a")].csr if plan is not None else h.levels[0].a
     k_ms = dh.time_spmv(0, "a", reps=50)
     k_bytes = 12 * a0.nnz + 4 * (a0.nrows + 1) + 8 * a0.ncols + 8 * a0.nrows
     peak, peak_src = peaks()
@@ -278,14 +316,16 @@ def run_amgb200(args):
         "warmup": args.warmup,
         "ms_per_step": tot_ms / max(args.steps, 1),
         "higher_is_better": False,
-        "scaling": "weak",
+        "scaling": "strong" if (world > 1 and partitioned) else "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded generator + reference setup hierarchy)",
         "config": {
             "workload": WORKLOADS.get(args.config, args.config),
             "name": args.config,
-            "parallelism": "1 GPU" if world == 1 else f"replicas x{world} (row-partitioned path: DESIGN.md)",
+            "parallelism": ("1 GPU" if world == 1 else
+                            (f"row partition x{world} (NCCL halos, agglomeration below {args.agglom_rows} rows)"
+                             if partitioned else f"replicas x{world}")),
             "step": "one PCG solve to rtol 1e-8 from x0=0, b resident in HBM",
             "l2": "inputs larger than L2 (hierarchy + vectors > 1 GB, per-iteration traffic >> 126 MB)",
             "levels": [int(l.a.nrows) for l in h.levels],
@@ -303,7 +343,8 @@ def run_amgb200(args):
             "traffic": ncu_traffic(args.config), "kernel": "spmv_vec on A0 (plain epilogue, padded-aligned layout)",
             "bytes_per_launch": k_bytes, "ms_per_launch": k_ms, "peak_source": peak_src,
         },
-        "e2e": {"value": e2e_ms_iter, "unit": "ms/iter", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
+        "e2e": {"value": e2e_ms_iter, "unit": "ms/iter", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                "note": "whole job: every rank copies its slice of b in and of x out"},
         "gpu_launches": int(launches),
         "graph_mode": dh.stats()["graph_mode"],
         "clocks": clk.report(),

@@ -131,6 +131,7 @@ struct amg_handle {
     int kernel = 2;      // 0: staged CTA tiles (spmv_tiles / spmv_ws), 2: direct register kernel, 3: warp tiles
     int wt_nnz = 256;    // warp-tile capacity (entries)
     int pad_min = 8;     // matrices averaging >= pad_min entries/row get the padded-aligned layout (0 = off)
+    int small_rows_per_sm = 512;  // below sm_count * this many rows a matrix counts as small
     int direct_ctas = 0; // direct kernel CTAs per SM (0 = occupancy)
     int direct_per_sm = 8;
     int lanes_override = 0;
@@ -717,10 +718,17 @@ static int build_graph(amg_t *h)
         int s = enqueue_pcg_body(h, dummy, 0);
         cudaError_t e = cudaStreamEndCapture(h->stream, &g);
         if (s != AMG_OK) return s;
-        if (e != cudaSuccess) return fail(AMG_E_CUDA, std::string("graph capture failed: ") + cudaGetErrorString(e));
-        e = cudaGraphInstantiate(&h->gexec, g, 0);
-        cudaGraphDestroy(g);
-        if (e != cudaSuccess) return fail(AMG_E_CUDA, std::string("graph instantiate failed: ") + cudaGetErrorString(e));
+        if (e == cudaSuccess) {
+            e = cudaGraphInstantiate(&h->gexec, g, 0);
+            cudaGraphDestroy(g);
+        }
+        if (e != cudaSuccess) {  // e.g. a collective that cannot be captured here: launch eagerly
+            cudaGetLastError();
+            if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+            h->launches = before;
+            h->graph_mode = 0;
+            return AMG_OK;
+        }
         h->graph_mode = 1;
         h->launches_per_iter = h->launches - before;
         h->launches = before;
@@ -937,6 +945,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "ws") { h->ws = value ? 1 : 0; return AMG_OK; }
     if (k == "kernel") { h->kernel = (int)value; return AMG_OK; }
     if (k == "pad_min") { h->pad_min = (int)value; return AMG_OK; }
+    if (k == "small_rows_per_sm") { h->small_rows_per_sm = (int)value; return AMG_OK; }
     if (k == "wt_nnz") { if (value < 64 || value > 1024) return fail(AMG_E_ARG, "wt_nnz out of range"); h->wt_nnz = (int)value; return AMG_OK; }
     if (k == "direct_ctas") { h->direct_ctas = (int)value; return AMG_OK; }
     if (k == "ctas_per_sm") { h->ctas_per_sm = (int)value; return AMG_OK; }
@@ -1285,7 +1294,8 @@ int amg_finalize(amg_t *h)
                 M.wt_grid = std::max(1, std::min((warps_needed + WT_WARPS - 1) / WT_WARPS, h->sm_count * nb));
                 h->max_grid = std::max(h->max_grid, M.wt_grid);
             }
-            if (h->pad_min > 0 && M.nrows > 0 && (double)M.nnz / (double)M.nrows >= (double)h->pad_min) {
+            if (h->pad_min > 0 && M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm && !h->lanes_override &&
+                (double)M.nnz / (double)M.nrows >= (double)h->pad_min) {
                 // padded-aligned copy: row starts == 3 (mod 4) so entry 1 is 16-byte aligned
                 std::vector<int32_t> col_h(M.nnz);
                 std::vector<double> val_h(M.nnz);
@@ -1326,8 +1336,12 @@ int amg_finalize(amg_t *h)
             const double avg = M.nrows ? (double)M.nnz / (double)M.nrows : 0.0;
             // direct kernel: one lane per row maximises rows in flight (measured on
             // B200: 27-pt A 3.5 TB/s at 1 lane vs 2.4 at 4); wide rows split over lanes
+            // small matrices (fewer rows than ~2 CTAs/SM of one-lane rows) spread each row over
+            // more lanes: the dependent load chain per lane shrinks and more SMs take part
+            const bool small = M.nrows < (int64_t)h->sm_count * h->small_rows_per_sm;
             M.lanes = h->lanes_override ? h->lanes_override
-                      : h->kernel == 2   ? (avg < 48.0 ? 1 : avg < 96.0 ? 4 : 8)
+                      : h->kernel == 2   ? (small ? (avg >= 16.0 ? 8 : avg >= 6.0 ? 4 : 2)
+                                                  : (avg < 48.0 ? 1 : avg < 96.0 ? 4 : 8))
                                          : (avg < 9.0 ? 1 : avg < 17.0 ? 2 : avg < 33.0 ? 4 : 8);
             M.grid = h->persistent ? std::max(1, std::min(M.ntiles, h->sm_count * per_sm)) : std::max(1, M.ntiles);
             h->max_grid = std::max(h->max_grid, M.grid);

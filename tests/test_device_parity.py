@@ -202,3 +202,18 @@ def _dense(m):
     rows = np.repeat(np.arange(m.nrows), np.diff(m.row_offsets))
     d[rows, m.col_indices] = m.values
     return d
+
+
+def test_plan_upload_single_rank_matches_reference_upload(cases):
+    # the multi-GPU upload path (partition plan, local matrices) at nranks = 1
+    from paper_2102_07417_b200.partition import plan_hierarchy
+
+    c, dh = _dh("poisson7_12", cases)
+    plan = plan_hierarchy(c["h"], 1, 0)
+    dp = amg.DeviceHierarchy.from_plan(plan)
+    cfg = amg.KrylovConfig(rtol=1e-10, record_history=True)
+    r1 = amg.pcg(dh.A0, c["b"], apply_m=dh.vcycle, config=cfg)
+    r2 = amg.pcg(dp.A0, c["b"], apply_m=dp.vcycle, config=cfg)
+    np.testing.assert_array_equal(r1.x, r2.x)
+    np.testing.assert_array_equal(dp.vcycle(c["y"]), dh.vcycle(c["y"]))
+    dp.close()
