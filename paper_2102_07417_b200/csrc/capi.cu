@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <unordered_map>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -59,6 +60,10 @@ struct DevMat {
     double *val = nullptr;
     TileDesc *tiles = nullptr;
     int ntiles = 0;
+    uint8_t *pid = nullptr;      // stencil-pattern layout (spmv_pat): pattern id per row
+    int32_t *prel = nullptr;     // concatenated relative offsets
+    int32_t *pbeg = nullptr;     // pattern starts into prel
+    int npat = 0, nrel = 0;
     int32_t *pstart = nullptr;   // padded-aligned layout (spmv_vec), nullptr if unused
     double *pval = nullptr;
     int32_t *pcol = nullptr;
@@ -132,6 +137,7 @@ struct amg_handle {
     int wt_nnz = 256;    // warp-tile capacity (entries)
     int pad_min = 8;     // matrices averaging >= pad_min entries/row get the padded-aligned layout (0 = off)
     int small_rows_per_sm = 512;  // below sm_count * this many rows a matrix counts as small
+    int patterns = 1;             // stencil-pattern layout for square operators with few row patterns
     int direct_ctas = 0; // direct kernel CTAs per SM (0 = occupancy)
     int direct_per_sm = 8;
     int lanes_override = 0;
@@ -184,6 +190,19 @@ static SpmvFn spmv_wt_fn(int epi, int lanes)
     default: AMG_L(EPI_ADD)
     }
 #undef AMG_L
+}
+
+typedef void (*SpmvPatFn)(const SpmvArgs, const PatArgs, int);
+
+static SpmvPatFn spmv_pat_fn(int epi)
+{
+    switch (epi) {
+    case EPI_PLAIN: return spmv_pat<EPI_PLAIN>;
+    case EPI_RESID: return spmv_pat<EPI_RESID>;
+    case EPI_AXPYW: return spmv_pat<EPI_AXPYW>;
+    case EPI_SETW: return spmv_pat<EPI_SETW>;
+    default: return spmv_pat<EPI_ADD>;
+    }
 }
 
 typedef void (*SpmvVecFn)(const SpmvArgs, const PadArgs, int);
@@ -442,7 +461,10 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     a.ctl = h->ctl;
     a.gate1 = g1;
     a.gate2 = g2;
-    if (M.pstart) {
+    if (M.pid) {
+        PatArgs pa{M.pstart, M.pval, M.pid, M.prel, M.pbeg, M.npat, M.nrel};
+        TRY(launch_k(h, spmv_pat_fn(epi), M.pad_grid, VEC_SPMV_THREADS, 0, a, pa, (int)M.nrows));
+    } else if (M.pstart) {
         PadArgs pa{M.pstart, M.pval, M.pcol};
         TRY(launch_k(h, spmv_vec_fn(epi), M.pad_grid, VEC_SPMV_THREADS, 0, a, pa, (int)M.nrows));
     } else if (h->kernel == 3 && M.nwtiles > 0) {
@@ -912,7 +934,7 @@ void amg_destroy(amg_t *h)
     auto F = [](void *p) { if (p) cudaFree(p); };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol);
+            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg);
             halo_free(M.halo);
         }
         F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
@@ -946,6 +968,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "kernel") { h->kernel = (int)value; return AMG_OK; }
     if (k == "pad_min") { h->pad_min = (int)value; return AMG_OK; }
     if (k == "small_rows_per_sm") { h->small_rows_per_sm = (int)value; return AMG_OK; }
+    if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
     if (k == "wt_nnz") { if (value < 64 || value > 1024) return fail(AMG_E_ARG, "wt_nnz out of range"); h->wt_nnz = (int)value; return AMG_OK; }
     if (k == "direct_ctas") { h->direct_ctas = (int)value; return AMG_OK; }
     if (k == "ctas_per_sm") { h->ctas_per_sm = (int)value; return AMG_OK; }
@@ -1327,6 +1350,45 @@ int amg_finalize(amg_t *h)
                 CK(cudaMemcpy(M.pstart, ps.data(), ps.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
                 CK(cudaMemcpy(M.pcol, pc.data(), pc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
                 CK(cudaMemcpy(M.pval, pv.data(), pv.size() * sizeof(double), cudaMemcpyHostToDevice));
+                // stencil patterns: every row's (col - row) tuple from a small dictionary
+                if (h->patterns && h->nranks == 1 && M.ncols == M.nrows) {
+                    std::unordered_map<std::string, int> dict;
+                    std::vector<int32_t> rel, beg{0};
+                    std::vector<uint8_t> ids(M.nrows);
+                    bool ok = true;
+                    std::string key;
+                    for (int64_t r = 0; r < M.nrows && ok; ++r) {
+                        const int32_t lo = off32[r], hi = off32[r + 1];
+                        key.assign(reinterpret_cast<const char *>(&col_h[0]) + 0, 0);
+                        key.resize((size_t)(hi - lo) * 4);
+                        for (int32_t k = lo; k < hi; ++k) {
+                            const int32_t d = col_h[k] - (int32_t)r;
+                            memcpy(&key[(size_t)(k - lo) * 4], &d, 4);
+                        }
+                        auto it = dict.find(key);
+                        int id;
+                        if (it == dict.end()) {
+                            id = (int)dict.size();
+                            if (id >= PAT_MAX || (int)rel.size() + (hi - lo) > PAT_MAX_REL || hi - lo > 129) { ok = false; break; }
+                            dict.emplace(key, id);
+                            for (int32_t k = lo; k < hi; ++k) rel.push_back(col_h[k] - (int32_t)r);
+                            beg.push_back((int32_t)rel.size());
+                        } else {
+                            id = it->second;
+                        }
+                        ids[r] = (uint8_t)id;
+                    }
+                    if (ok && !dict.empty()) {
+                        M.npat = (int)dict.size();
+                        M.nrel = (int)rel.size();
+                        TRY(dalloc(&M.pid, ids.size() + 16));
+                        TRY(dalloc(&M.prel, rel.size()));
+                        TRY(dalloc(&M.pbeg, beg.size()));
+                        CK(cudaMemcpy(M.pid, ids.data(), ids.size(), cudaMemcpyHostToDevice));
+                        CK(cudaMemcpy(M.prel, rel.data(), rel.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                        CK(cudaMemcpy(M.pbeg, beg.data(), beg.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                    }
+                }
                 int nb = 0;
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_vec_fn(EPI_RESID), VEC_SPMV_THREADS, 0));
                 M.pad_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,

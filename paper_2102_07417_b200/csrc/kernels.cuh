@@ -1150,6 +1150,140 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_vec(const SpmvArgs a
     }
 }
 
+// ---------------------------------------------------------------- SpMV, stencil patterns
+
+// Stencil-pattern CSR (device-only layout for square operators whose rows
+// use at most 255 distinct relative column patterns, e.g. the 27-point
+// fine-grid operators of the BASELINE configs): row i stores a 1-byte
+// pattern id and its values in the padded-aligned layout; its columns are
+// i + rel[pattern][k] with the pattern table in shared memory (staged before
+// griddepcontrol.wait).  The 4-byte column stream disappears and the x
+// gathers no longer wait on a global column load.  Same products, same
+// reference summation order as spmv_vec.
+constexpr int PAT_MAX = 255;
+constexpr int PAT_MAX_REL = 8192;  // total relative offsets over all patterns
+
+struct PatArgs {
+    const int32_t *pstart;  // padded row starts (== 3 mod 4)
+    const double *pval;
+    const uint8_t *pid;     // pattern id per row
+    const int32_t *rel;     // concatenated relative offsets (col - row)
+    const int32_t *pbeg;    // npat + 1 starts into rel
+    int npat;
+    int nrel;
+};
+
+template <int EPI>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_pat(const SpmvArgs a, const PatArgs pa, int nrows)
+{
+    __shared__ double red[VEC_SPMV_THREADS / 32];
+    __shared__ int32_t s_rel[PAT_MAX_REL];
+    __shared__ int32_t s_beg[PAT_MAX + 1];
+    for (int i = threadIdx.x; i < pa.nrel; i += blockDim.x) s_rel[i] = pa.rel[i];
+    for (int i = threadIdx.x; i <= pa.npat; i += blockDim.x) s_beg[i] = pa.pbeg[i];
+    __syncthreads();
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const int nthreads = gridDim.x * VEC_SPMV_THREADS;
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    const double *__restrict__ x = a.x;
+    double dacc = 0.0;
+    int row = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x;
+    int nps = 0, npid = 0;
+    if (row < nrows) {
+        nps = __ldg(pa.pstart + row);
+        npid = __ldg(pa.pid + row);
+    }
+    for (; row < nrows; row += nthreads) {
+        const int ps = nps, pid = npid;
+        if (row + nthreads < nrows) {
+            nps = __ldg(pa.pstart + row + nthreads);
+            npid = __ldg(pa.pid + row + nthreads);
+        }
+        double bv = 0.0, wv = 0.0;
+        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
+        if (want_dot && !self_dot) wv = a.dotw[row];
+        const int rb = s_beg[pid];
+        const int len = s_beg[pid + 1] - rb;
+        const int32_t *rl = s_rel + rb;
+        const int n = len - 1;
+        double sum = 0.0;
+        if (n >= 0 && n <= 128) {
+            const double p0 = prod(__ldg(pa.pval + ps), __ldg(x + row + rl[0]));
+            const double2 *v2 = reinterpret_cast<const double2 *>(pa.pval + ps + 1);
+            const int32_t *r1 = rl + 1;
+            auto round8 = [&](int r, double p[8]) {
+                const double2 va = __ldg(v2 + 4 * r), vb = __ldg(v2 + 4 * r + 1), vc = __ldg(v2 + 4 * r + 2),
+                              vd = __ldg(v2 + 4 * r + 3);
+                const int k = 8 * r;
+                p[0] = prod(va.x, __ldg(x + row + r1[k]));
+                p[1] = prod(va.y, __ldg(x + row + r1[k + 1]));
+                p[2] = prod(vb.x, __ldg(x + row + r1[k + 2]));
+                p[3] = prod(vb.y, __ldg(x + row + r1[k + 3]));
+                p[4] = prod(vc.x, __ldg(x + row + r1[k + 4]));
+                p[5] = prod(vc.y, __ldg(x + row + r1[k + 5]));
+                p[6] = prod(vd.x, __ldg(x + row + r1[k + 6]));
+                p[7] = prod(vd.y, __ldg(x + row + r1[k + 7]));
+            };
+            auto round8m = [&](int r, int cnt, double p[8]) {
+                const double2 va = __ldg(v2 + 4 * r);
+                const double2 vb = cnt > 2 ? __ldg(v2 + 4 * r + 1) : make_double2(0.0, 0.0);
+                const double2 vc = cnt > 4 ? __ldg(v2 + 4 * r + 2) : make_double2(0.0, 0.0);
+                const double2 vd = cnt > 6 ? __ldg(v2 + 4 * r + 3) : make_double2(0.0, 0.0);
+                const double vv[8] = {va.x, va.y, vb.x, vb.y, vc.x, vc.y, vd.x, vd.y};
+                const int k = 8 * r;
+#pragma unroll
+                for (int t = 0; t < 8; ++t) p[t] = (t < cnt) ? prod(vv[t], __ldg(x + row + r1[k + t])) : 0.0;
+            };
+            double res;
+            double acc[8];
+            round8m(0, n < 8 ? n : 8, acc);
+            if (n < 8) {
+                res = 0.0;
+#pragma unroll
+                for (int t = 0; t < 7; ++t)
+                    if (t < n) res = add(res, acc[t]);
+            } else {
+                const int main = n - (n % 8);
+                const int its = main / 8;
+                for (int r = 1; r < its; ++r) {
+                    double p[8];
+                    round8(r, p);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[j] = add(acc[j], p[j]);
+                }
+                res = add(add(add(acc[0], acc[1]), add(acc[2], acc[3])), add(add(acc[4], acc[5]), add(acc[6], acc[7])));
+                const int ntail = n - main;
+                if (ntail > 0) {
+                    double p[8];
+                    round8m(its, ntail, p);
+#pragma unroll
+                    for (int t = 0; t < 7; ++t)
+                        if (t < ntail) res = add(res, p[t]);
+                }
+            }
+            sum = add(p0, res);
+        } else if (n > 128) {
+            auto P = [&](int k) -> double { return prod(__ldg(pa.pval + ps + k), __ldg(x + row + rl[k])); };
+            sum = add(P(0), pairwise_sum(P, 1, n));
+        }
+        double yv;
+        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+        else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+        else yv = sum;
+        a.y[row] = yv;
+        if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
+        grid_finalize<VEC_SPMV_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
 // ---------------------------------------------------------------- vectors
 
 constexpr int VEC_THREADS = 256;
