@@ -60,6 +60,11 @@ struct DevMat {
     double *val = nullptr;
     TileDesc *tiles = nullptr;
     int ntiles = 0;
+    int32_t *sbeg = nullptr;     // SELL-32 layout (spmv_sell), nullptr if unused
+    double *sval = nullptr;
+    int32_t *scol = nullptr;
+    uint8_t *slen = nullptr;
+    int sell_grid = 0;
     uint8_t *pid = nullptr;      // stencil-pattern layout (spmv_pat): pattern id per row
     int32_t *prel = nullptr;     // concatenated relative offsets
     int32_t *pbeg = nullptr;     // pattern starts into prel
@@ -138,6 +143,8 @@ struct amg_handle {
     int pad_min = 8;     // matrices averaging >= pad_min entries/row get the padded-aligned layout (0 = off)
     int small_rows_per_sm = 512;  // below sm_count * this many rows a matrix counts as small
     int patterns = 1;             // stencil-pattern layout for square operators with few row patterns
+    int sell = 1;                 // SELL-32 slices where padding <= sell_pad %
+    int sell_pad = 10;
     int direct_ctas = 0; // direct kernel CTAs per SM (0 = occupancy)
     int direct_per_sm = 8;
     int lanes_override = 0;
@@ -190,6 +197,21 @@ static SpmvFn spmv_wt_fn(int epi, int lanes)
     default: AMG_L(EPI_ADD)
     }
 #undef AMG_L
+}
+
+typedef void (*SpmvSellFn)(const SpmvArgs, const SellArgs, int);
+
+static SpmvSellFn spmv_sell_fn(int epi, bool pat)
+{
+#define AMG_S(E) return pat ? spmv_sell<E, true> : spmv_sell<E, false>;
+    switch (epi) {
+    case EPI_PLAIN: AMG_S(EPI_PLAIN)
+    case EPI_RESID: AMG_S(EPI_RESID)
+    case EPI_AXPYW: AMG_S(EPI_AXPYW)
+    case EPI_SETW: AMG_S(EPI_SETW)
+    default: AMG_S(EPI_ADD)
+    }
+#undef AMG_S
 }
 
 typedef void (*SpmvPatFn)(const SpmvArgs, const PatArgs, int);
@@ -461,7 +483,10 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     a.ctl = h->ctl;
     a.gate1 = g1;
     a.gate2 = g2;
-    if (M.pid) {
+    if (M.sbeg) {
+        SellArgs sa{M.sbeg, M.sval, M.scol, M.slen, M.pid, M.prel, M.pbeg, M.npat, M.nrel};
+        TRY(launch_k(h, spmv_sell_fn(epi, M.scol == nullptr), M.sell_grid, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
+    } else if (M.pid) {
         PatArgs pa{M.pstart, M.pval, M.pid, M.prel, M.pbeg, M.npat, M.nrel};
         TRY(launch_k(h, spmv_pat_fn(epi), M.pad_grid, VEC_SPMV_THREADS, 0, a, pa, (int)M.nrows));
     } else if (M.pstart) {
@@ -934,7 +959,7 @@ void amg_destroy(amg_t *h)
     auto F = [](void *p) { if (p) cudaFree(p); };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg);
+            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen);
             halo_free(M.halo);
         }
         F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
@@ -969,6 +994,8 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "pad_min") { h->pad_min = (int)value; return AMG_OK; }
     if (k == "small_rows_per_sm") { h->small_rows_per_sm = (int)value; return AMG_OK; }
     if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
+    if (k == "sell") { h->sell = value ? 1 : 0; return AMG_OK; }
+    if (k == "sell_pad") { h->sell_pad = (int)value; return AMG_OK; }
     if (k == "wt_nnz") { if (value < 64 || value > 1024) return fail(AMG_E_ARG, "wt_nnz out of range"); h->wt_nnz = (int)value; return AMG_OK; }
     if (k == "direct_ctas") { h->direct_ctas = (int)value; return AMG_OK; }
     if (k == "ctas_per_sm") { h->ctas_per_sm = (int)value; return AMG_OK; }
@@ -1387,6 +1414,50 @@ int amg_finalize(amg_t *h)
                         CK(cudaMemcpy(M.pid, ids.data(), ids.size(), cudaMemcpyHostToDevice));
                         CK(cudaMemcpy(M.prel, rel.data(), rel.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
                         CK(cudaMemcpy(M.pbeg, beg.data(), beg.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                    }
+                }
+                // SELL-32: coalesced slices where the padding stays small
+                if (h->sell) {
+                    const int64_t ns = (M.nrows + 31) / 32;
+                    std::vector<int32_t> sb(ns + 1);
+                    int64_t tot = 0, maxlen = 0;
+                    for (int64_t sl = 0; sl < ns; ++sl) {
+                        int w = 0;
+                        for (int64_t r = sl * 32; r < std::min<int64_t>(M.nrows, sl * 32 + 32); ++r)
+                            w = std::max(w, off32[r + 1] - off32[r]);
+                        sb[sl] = (int32_t)tot;
+                        tot += (int64_t)w * 32;
+                        maxlen = std::max<int64_t>(maxlen, w);
+                    }
+                    sb[ns] = (int32_t)tot;
+                    if (maxlen <= 129 && tot <= (int64_t)(M.nnz * (1.0 + h->sell_pad / 100.0)) && tot < INT32_MAX - 64) {
+                        std::vector<double> sv(tot + 32, 0.0);
+                        const bool pat = M.pid != nullptr;
+                        std::vector<int32_t> sc(pat ? 0 : tot + 32, 0);
+                        std::vector<uint8_t> ln(M.nrows + 16, 0);
+                        for (int64_t r = 0; r < M.nrows; ++r) {
+                            const int64_t sl = r / 32, l = r % 32;
+                            ln[r] = (uint8_t)(off32[r + 1] - off32[r]);
+                            for (int32_t k = off32[r]; k < off32[r + 1]; ++k) {
+                                const int64_t dst = sb[sl] + (int64_t)(k - off32[r]) * 32 + l;
+                                sv[dst] = val_h[k];
+                                if (!pat) sc[dst] = col_h[k];
+                            }
+                        }
+                        TRY(dalloc(&M.sbeg, sb.size()));
+                        TRY(dalloc(&M.sval, sv.size()));
+                        TRY(dalloc(&M.slen, ln.size()));
+                        CK(cudaMemcpy(M.sbeg, sb.data(), sb.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                        CK(cudaMemcpy(M.sval, sv.data(), sv.size() * sizeof(double), cudaMemcpyHostToDevice));
+                        CK(cudaMemcpy(M.slen, ln.data(), ln.size(), cudaMemcpyHostToDevice));
+                        if (!pat) {
+                            TRY(dalloc(&M.scol, sc.size()));
+                            CK(cudaMemcpy(M.scol, sc.data(), sc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                        }
+                        int nbs = 0;
+                        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbs, (const void *)spmv_sell_fn(EPI_RESID, pat), VEC_SPMV_THREADS, 0));
+                        M.sell_grid = (int)std::max<int64_t>(1, std::min<int64_t>((ns + 7) / 8, (int64_t)h->sm_count * std::max(nbs, 1)));
+                        h->max_grid = std::max(h->max_grid, M.sell_grid);
                     }
                 }
                 int nb = 0;

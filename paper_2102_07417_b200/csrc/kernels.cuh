@@ -1284,6 +1284,121 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_pat(const SpmvArgs a
     }
 }
 
+// ---------------------------------------------------------------- SpMV, SELL-32 slices
+
+// SELL-32 (sliced ELLPACK, slice = 32 consecutive rows = one warp): entry k
+// of the slice's rows is stored contiguously (sval[sbeg + 32 k + lane]), so
+// every value / column load of a warp is one fully coalesced 256 / 128-byte
+// access.  Lane = row, each lane sums its own row in the reference order
+// (p0 + numpy pairwise over 8 strided accumulators), so results are
+// bit-identical.  Columns come from the stencil-pattern table (PAT) or from
+// the SELL column array.  Used where slices are uniform (padding <= ~10%).
+struct SellArgs {
+    const int32_t *sbeg;    // per slice: start (entries) of the slice block
+    const double *sval;
+    const int32_t *scol;    // nullptr with PAT
+    const uint8_t *len;     // row lengths (<= 129)
+    const uint8_t *pid;     // PAT: pattern id per row
+    const int32_t *rel;
+    const int32_t *pbeg;
+    int npat, nrel;
+};
+
+template <int EPI, bool PAT>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_sell(const SpmvArgs a, const SellArgs sa, int nrows)
+{
+    __shared__ double red[VEC_SPMV_THREADS / 32];
+    __shared__ int32_t s_rel[PAT ? PAT_MAX_REL : 1];
+    __shared__ int32_t s_beg[PAT ? PAT_MAX + 1 : 1];
+    if constexpr (PAT) {
+        for (int i = threadIdx.x; i < sa.nrel; i += blockDim.x) s_rel[i] = sa.rel[i];
+        for (int i = threadIdx.x; i <= sa.npat; i += blockDim.x) s_beg[i] = sa.pbeg[i];
+        __syncthreads();
+    }
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const int lane = threadIdx.x & 31;
+    const int nslices = (nrows + 31) >> 5;
+    const int wstride = gridDim.x * (VEC_SPMV_THREADS / 32);
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    const double *__restrict__ x = a.x;
+    double dacc = 0.0;
+    for (int sl = blockIdx.x * (VEC_SPMV_THREADS / 32) + (threadIdx.x >> 5); sl < nslices; sl += wstride) {
+        const int row = sl * 32 + lane;
+        const bool live = row < nrows;
+        const int sb = __ldg(sa.sbeg + sl);
+        int len = 0, rb = 0;
+        if (live) {
+            len = __ldg(sa.len + row);
+            if constexpr (PAT) rb = s_beg[__ldg(sa.pid + row)];
+        }
+        double bv = 0.0, wv = 0.0;
+        if (live) {
+            if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
+            if (want_dot && !self_dot) wv = a.dotw[row];
+        }
+        const double *vb = sa.sval + sb + lane;
+        const int32_t *cb = PAT ? nullptr : sa.scol + sb + lane;
+        auto P = [&](int k) -> double {
+            const int c = PAT ? row + s_rel[rb + k] : __ldg(cb + 32 * k);
+            return prod(__ldg(vb + 32 * k), __ldg(x + c));
+        };
+        const int n = len - 1;
+        double sum = 0.0;
+        if (n >= 0 && n <= 128) {
+            double acc[8];
+            // first round shared by short and long rows (masked)
+            const int c0 = n < 8 ? n : 8;
+            const double p0 = P(0);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) acc[t] = (t < c0) ? P(1 + t) : 0.0;
+            double res;
+            if (n < 8) {
+                res = 0.0;
+#pragma unroll
+                for (int t = 0; t < 7; ++t)
+                    if (t < n) res = add(res, acc[t]);
+            } else {
+                const int main = n - (n % 8);
+                for (int i = 8; i < main; i += 8) {
+                    double p[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) p[t] = P(1 + i + t);
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) acc[t] = add(acc[t], p[t]);
+                }
+                res = add(add(add(acc[0], acc[1]), add(acc[2], acc[3])), add(add(acc[4], acc[5]), add(acc[6], acc[7])));
+                const int ntail = n - main;
+                double p[7];
+#pragma unroll
+                for (int t = 0; t < 7; ++t) p[t] = (t < ntail) ? P(1 + main + t) : 0.0;
+#pragma unroll
+                for (int t = 0; t < 7; ++t)
+                    if (t < ntail) res = add(res, p[t]);
+            }
+            sum = add(p0, res);
+        } else if (n > 128) {
+            sum = add(P(0), pairwise_sum(P, 1, n));
+        }
+        if (live) {
+            double yv;
+            if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+            else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+            else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+            else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+            else yv = sum;
+            a.y[row] = yv;
+            if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
+        }
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
+        grid_finalize<VEC_SPMV_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
 // ---------------------------------------------------------------- vectors
 
 constexpr int VEC_THREADS = 256;
