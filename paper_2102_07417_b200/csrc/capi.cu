@@ -118,7 +118,7 @@ struct amg_handle {
     int nu1 = 1, nu2 = 1;
     // coarsest factor
     int nc = 0, coarse_kind = AMG_COARSE_CHOLESKY;
-    double *Lp = nullptr, *LU = nullptr, *dinv = nullptr;
+    double *Lp = nullptr, *LU = nullptr, *dinv = nullptr, *binv = nullptr;
     int32_t *piv = nullptr;
     int coarse_staged = 0;
     size_t coarse_smem = 0;
@@ -150,7 +150,9 @@ struct amg_handle {
     int lanes_override = 0;
     int pdl = 1;  // programmatic dependent launch between consecutive kernels
     // cluster tail: levels >= tail_level run inside one cluster kernel
-    int64_t tail_nnz = 1 << 30;  // level filter on nnz(A_k); the cluster smem budget decides
+    int64_t tail_nnz = 400000;   // levels whose A_k has at most this many entries run in the cluster tail
+    int tail_stage = 0;          // stage tail matrices in smem (measured slower on B200: the big smem
+                                 // footprint delays the cluster launch; streamed from L2 by default)
     int cluster = 16;
     int tail_level = 0;  // 0 = disabled
     TailOp *tail_ops = nullptr;
@@ -556,6 +558,7 @@ static CoarseArgs coarse_args(const amg_t *h)
     c.kind = h->coarse_kind == AMG_COARSE_CHOLESKY ? 0 : 1;
     c.staged = h->coarse_staged;
     c.Lp = h->Lp;
+    c.binv = h->binv;
     c.dinv = h->dinv;
     c.LU = h->LU;
     c.piv = h->piv;
@@ -797,17 +800,22 @@ static int build_tail(amg_t *h)
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
     const size_t coarse_bytes = (h->coarse_kind == AMG_COARSE_CHOLESKY && h->coarse_staged)
                                     ? h->coarse_smem
-                                    : (size_t)((h->nc + 1) & ~1) * sizeof(double);
-    const int budget = optin - (int)(TAIL_MAX_OPS * sizeof(TailOp) + TAIL_MAX_MATS * 5 * sizeof(int) +
-                                     TAIL_MAX_DINV * sizeof(double)) - 1024;  // static smem + slack
-    // candidate start levels: deepest first; keep the shallowest that fits
+                                    : (size_t)(((h->nc + 1) & ~1) + 32) * sizeof(double);
+    const int budget = optin - (int)(TAIL_MAX_OPS * sizeof(TailOp) + TAIL_MAX_MATS * 5 * sizeof(int)) - 1024;  // static smem + slack
+    // start level: the shallowest level (>= 1) from which every A_k has at most
+    // tail_nnz entries; matrices are staged in smem coarsest-first while the
+    // budget lasts, the rest are streamed from L2 inside their op
     int best = 0;
     std::vector<TailOp> best_ops;
     std::vector<TailMat> best_mats;
     std::vector<int32_t> best_splits;
     int best_prod_off = 0, best_smem = 0;
+    int kstart = 0;
     for (int kt = nl - 1; kt >= 1; --kt) {
         if (h->lv[kt].m[AMG_A].nnz > h->tail_nnz) break;
+        kstart = kt;
+    }
+    for (int kt = kstart; kt >= 1 && kt < nl && best == 0; ++kt) {
         std::vector<TailOp> ops;
         std::vector<const DevMat *> mats_raw;
         h->collect = &ops;
@@ -816,13 +824,12 @@ static int build_tail(amg_t *h)
         h->collect = nullptr;
         h->collect_mats = nullptr;
         if (st != AMG_OK) return st;
-        // distinct matrices, balanced row splits, smem regions
+        if ((int)ops.size() > TAIL_MAX_OPS) continue;
         std::vector<const DevMat *> uniq;
         std::vector<TailMat> mats;
         std::vector<int32_t> splits;
-        size_t off_bytes = (coarse_bytes + 15) & ~(size_t)15;
+        std::vector<int> mat_level;
         int prod_cap = 0;
-        bool fits = true;
         for (auto &o : ops) {
             if (o.kind != TAIL_SPMV) continue;
             const DevMat *M = mats_raw[o.mode];
@@ -839,10 +846,14 @@ static int build_tail(amg_t *h)
                 T.val = M->val;
                 T.split = (int)splits.size();
                 const int64_t nnz = off[M->nrows];
+                // CTA 0 runs the coarsest solve and owns no SpMV rows; rows are
+                // balanced by stored entries over CTAs 1..cluster-1
+                const int workers = std::max(1, h->cluster - 1);
                 int r = 0;
                 splits.push_back(0);
-                for (int c = 1; c < h->cluster; ++c) {
-                    const int64_t target = nnz * c / h->cluster;
+                if (h->cluster > 1) splits.push_back(0);
+                for (int c = 1; c < workers; ++c) {
+                    const int64_t target = nnz * c / workers;
                     while (r < M->nrows && off[r] < target) ++r;
                     splits.push_back(r);
                 }
@@ -854,26 +865,45 @@ static int build_tail(amg_t *h)
                 }
                 T.rows_cap = rc;
                 T.nnz_cap = kc;
-                T.smem_off = (int)off_bytes;
-                off_bytes += tail_region_bytes(rc, kc);
                 prod_cap = std::max(prod_cap, kc);
                 idx = (int)uniq.size();
                 uniq.push_back(M);
                 mats.push_back(T);
+                int lvl = 0;
+                for (int k = 0; k < nl; ++k)
+                    for (int w = 0; w < 5; ++w)
+                        if (&h->lv[k].m[w] == M) lvl = k;
+                mat_level.push_back(lvl);
             }
             o.mat = idx;
         }
-        if ((int)ops.size() > TAIL_MAX_OPS || (int)mats.size() > TAIL_MAX_MATS) break;
+        if ((int)mats.size() > TAIL_MAX_MATS) continue;
+        // smem: CTA 0 = coarse area; CTAs >= 1 = [staged regions ...][products] (overlaid)
+        const size_t base = (h->cluster > 1) ? 0 : ((coarse_bytes + 15) & ~(size_t)15);
+        const size_t prod_bytes = (size_t)prod_cap * 8 + 16;
+        if (base + prod_bytes > (size_t)budget || coarse_bytes > (size_t)budget) continue;
+        std::vector<int> order(mats.size());
+        for (size_t u = 0; u < order.size(); ++u) order[u] = (int)u;
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return mat_level[a] > mat_level[b]; });
+        size_t off_bytes = base;
+        for (int u : order) {
+            const size_t rb = tail_region_bytes(mats[u].rows_cap, mats[u].nnz_cap);
+            if (h->tail_stage && off_bytes + rb + prod_bytes <= (size_t)budget) {
+                mats[u].staged = 1;
+                mats[u].smem_off = (int)off_bytes;
+                off_bytes += rb;
+            } else {
+                mats[u].staged = 0;
+                mats[u].smem_off = 0;
+            }
+        }
         const size_t prod_off = (off_bytes + 15) & ~(size_t)15;
-        const size_t smem = prod_off + (size_t)prod_cap * 8 + 16;
-        if (smem > (size_t)budget) fits = false;
-        if (!fits) break;
         best = kt;
         best_ops = ops;
         best_mats = mats;
         best_splits = splits;
         best_prod_off = (int)prod_off;
-        best_smem = (int)smem;
+        best_smem = (int)std::max(prod_off + prod_bytes, coarse_bytes);
     }
     if (best == 0) return AMG_OK;
     TRY(raise_smem_caps(h->device));
@@ -964,7 +994,7 @@ void amg_destroy(amg_t *h)
         }
         F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
     }
-    F(h->Lp); F(h->LU); F(h->dinv); F(h->tail_ops); F(h->tail_mats); F(h->tail_splits); F(h->piv); F(h->partials); F(h->ticket); F(h->ctl);
+    F(h->Lp); F(h->LU); F(h->dinv); F(h->binv); F(h->tail_ops); F(h->tail_mats); F(h->tail_splits); F(h->piv); F(h->partials); F(h->ticket); F(h->ctl);
     F(h->b); F(h->x); F(h->r); F(h->z); F(h->p); F(h->q); F(h->tmp_in); F(h->tmp_out); F(h->hist);
     if (h->ctl_h) cudaFreeHost(h->ctl_h);
     if (h->gexec) cudaGraphExecDestroy(h->gexec);
@@ -987,6 +1017,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "tile_rows") { if (value < 32 || value > 1024) return fail(AMG_E_ARG, "tile_rows out of range"); h->tile_rows = (int)value; return AMG_OK; }
     if (k == "stages") { if (value < 1 || value > 8) return fail(AMG_E_ARG, "stages out of range"); h->stages = (int)value; return AMG_OK; }
     if (k == "tail_nnz") { h->tail_nnz = value; return AMG_OK; }
+    if (k == "tail_stage") { h->tail_stage = value ? 1 : 0; return AMG_OK; }
     if (k == "cluster") { if (value != 8 && value != 16 && value != 4 && value != 2 && value != 1) return fail(AMG_E_ARG, "cluster must be 1,2,4,8,16"); h->cluster = (int)value; return AMG_OK; }
     if (k == "persistent") { h->persistent = value ? 1 : 0; return AMG_OK; }
     if (k == "ws") { h->ws = value ? 1 : 0; return AMG_OK; }
@@ -1198,14 +1229,14 @@ int amg_upload_coarse(amg_t *h, int n, const double *factor, int kind, const int
         TRY(dalloc(&h->dinv, (size_t)n));
         CK(cudaMemcpy(h->Lp, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(h->dinv, dinv.data(), n * sizeof(double), cudaMemcpyHostToDevice));
-        const size_t vbytes = (size_t)((n + 1) & ~1) * sizeof(double);
+        const size_t vbytes = (size_t)(2 * ((n + 1) & ~1) + 32) * sizeof(double);  // v, tmp, 1/L_ii
         const size_t lbytes = packed.size() * sizeof(double);
         if (vbytes + lbytes <= 200 * 1024) {
             h->coarse_staged = 1;
             h->coarse_smem = vbytes + lbytes;
         } else {
             h->coarse_staged = 0;
-            h->coarse_smem = vbytes;
+            h->coarse_smem = (size_t)(((n + 1) & ~1) + 32) * sizeof(double);  // v + tmp; factor read from L2
         }
     } else if (kind == AMG_COARSE_LU) {
         if (!piv) return fail(AMG_E_ARG, "amg_upload_coarse: LU needs pivots");
@@ -1717,6 +1748,17 @@ int amg_pcg(amg_t *h, const double *b, const double *x0, double rtol, int max_it
 int amg_time_spmv(amg_t *h, int level, int which, int reps, double *ms_per_launch)
 {
     TRY(check_final(h));
+    if (level == -1 && reps >= 1 && ms_per_launch && !h->container) {  // diagnostics: the coarsest solve
+        TRY(launch_coarse(h, h->tmp_in, h->tmp_out, nullptr, FIN_NONE, nullptr));
+        CK(cudaEventRecord(h->ev0, h->stream));
+        for (int i = 0; i < reps; ++i) TRY(launch_coarse(h, h->tmp_in, h->tmp_out, nullptr, FIN_NONE, nullptr));
+        CK(cudaEventRecord(h->ev1, h->stream));
+        TRY(sync_stream(h));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+        *ms_per_launch = ms / reps;
+        return AMG_OK;
+    }
     if (level < 0 || level >= (int)h->lv.size() || which < 0 || which > 4 || reps < 1 || !ms_per_launch)
         return fail(AMG_E_ARG, "amg_time_spmv: bad arguments");
     const DevMat &M = h->lv[level].m[which];

@@ -1536,15 +1536,25 @@ constexpr int COARSE_THREADS = 256;
 
 __device__ __forceinline__ int64_t tri(int i) { return (int64_t)i * (i + 1) / 2; }
 
-__device__ void chol_solve_cta(int n, const double *__restrict__ L, const double *__restrict__ dinv, double *v)
+// Blocked forward / back substitution (dpotrs order of operations per block:
+// warp 0 solves each 32x32 diagonal triangle by substitution with shuffles;
+// the rows below / above are updated as GEMVs).  The forward update reads
+// row segments L[i][jb..jb+31] with one warp per row (conflict-free smem,
+// shuffle reduction); the backward update reads L[jb+c][i] along rows.
+// `tmp` is unused (kept for the call signature of the staged layouts).
+__device__ void chol_solve_cta(int n, const double *__restrict__ L, const double *__restrict__ dinv, double *v,
+                               double *tmp)
 {
+    (void)tmp;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int jb = 0; jb < n; jb += 32) {  // forward: L y = b
-        const int nb = min(32, n - jb);
+    const int nwarps = blockDim.x >> 5;
+    const int nblk = (n + 31) / 32;
+    for (int bi = 0; bi < nblk; ++bi) {  // forward: L y = b
+        const int jb = bi * 32, nb = min(32, n - jb);
         if (warp == 0) {
             double vi = lane < nb ? v[jb + lane] : 0.0;
             const double di = lane < nb ? dinv[jb + lane] : 0.0;
-            const double *Lr = L + tri(jb + lane) + jb;  // row jb+lane of the diagonal block
+            const double *Lr = L + tri(jb + lane) + jb;
             if (nb == 32) {
 #pragma unroll
                 for (int c = 0; c < 32; ++c) {
@@ -1562,28 +1572,17 @@ __device__ void chol_solve_cta(int n, const double *__restrict__ L, const double
             if (lane < nb) v[jb + lane] = vi;
         }
         __syncthreads();
-        for (int i = jb + nb + threadIdx.x; i < n; i += blockDim.x) {
-            const double *Li = L + tri(i) + jb;
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            if (nb == 32) {
+        const double vb = lane < nb ? v[jb + lane] : 0.0;
+        for (int i = jb + nb + warp; i < n; i += nwarps) {  // one warp per row: lanes read L[i][jb + lane]
+            double t = lane < nb ? L[tri(i) + jb + lane] * vb : 0.0;
 #pragma unroll
-                for (int c = 0; c < 32; c += 4) {
-                    a0 = fma(Li[c], v[jb + c], a0);
-                    a1 = fma(Li[c + 1], v[jb + c + 1], a1);
-                    a2 = fma(Li[c + 2], v[jb + c + 2], a2);
-                    a3 = fma(Li[c + 3], v[jb + c + 3], a3);
-                }
-            } else {
-                for (int c = 0; c < nb; ++c) a0 = fma(Li[c], v[jb + c], a0);
-            }
-            v[i] -= (a0 + a1) + (a2 + a3);
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (lane == 0) v[i] -= t;
         }
         __syncthreads();
     }
-    const int nblk = (n + 31) / 32;
     for (int bi = nblk - 1; bi >= 0; --bi) {  // backward: L^T z = y
-        const int jb = bi * 32;
-        const int nb = min(32, n - jb);
+        const int jb = bi * 32, nb = min(32, n - jb);
         if (warp == 0) {
             double vi = lane < nb ? v[jb + lane] : 0.0;
             const double di = lane < nb ? dinv[jb + lane] : 0.0;
@@ -1650,8 +1649,9 @@ __device__ void lu_solve_cta(int n, const double *__restrict__ LU, const int32_t
 struct CoarseArgs {
     int n;
     int kind;    // 0 cholesky, 1 lu
-    int staged;  // packed factor copied to shared memory
+    int staged;  // packed factor + block inverses copied to shared memory
     const double *Lp;
+    const double *binv;  // packed inverses of the 32x32 diagonal blocks (528 doubles per block)
     const double *dinv;
     const double *LU;
     const int32_t *piv;
@@ -1666,18 +1666,24 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_solve_k(const CoarseArg
     __shared__ double red[COARSE_THREADS / 32];
     const int n = c.n;
     double *v = sh;
-    const double *L = c.Lp;
+    double *tmp = sh + ((n + 1) & ~1);
+    const double *L = c.Lp, *D = c.dinv;
     if (c.kind == 0 && c.staged) {  // the factor is static: stage it before waiting on the producer
-        double *Ls = sh + ((n + 1) & ~1);
-        for (int64_t i = threadIdx.x; i < tri(n); i += blockDim.x) Ls[i] = c.Lp[i];
+        double *Ds = tmp + 32;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) Ds[i] = c.dinv[i];
+        double *Ls = Ds + ((n + 1) & ~1);
+        const int64_t np = tri(n);
+#pragma unroll 8
+        for (int64_t i = threadIdx.x; i < np; i += blockDim.x) Ls[i] = __ldg(c.Lp + i);
         L = Ls;
+        D = Ds;
     }
     pdl_launch();
     pdl_wait();
     if (!gate_open(gate1, nullptr)) return;
     for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = y[i];
     __syncthreads();
-    if (c.kind == 0) chol_solve_cta(n, L, c.dinv, v);
+    if (c.kind == 0) chol_solve_cta(n, L, D, v, tmp);
     else lu_solve_cta(n, c.LU, c.piv, v);
     double acc = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -1721,6 +1727,7 @@ struct TailMat {
     const int32_t *col;
     const double *val;
     int split;     // (cluster + 1) row splits in the split table
+    int staged;    // 1: block staged in smem at kernel start; 0: streamed from L2 per op
     int smem_off;  // byte offset of this matrix's region in every CTA's smem
     int rows_cap;  // region capacity: rows (offsets: rows_cap + 1 entries)
     int nnz_cap;   // region capacity: entries
@@ -1757,10 +1764,51 @@ __device__ __forceinline__ unsigned long long globaltimer()
     return t;
 }
 
+// Streamed variant: the block's values / columns / offsets are read from
+// global memory (L2) in the op itself (matrices that did not fit the smem
+// budget); same phases and order as the staged variant.
+template <int EPI>
+__device__ __forceinline__ void tail_spmv_streamed(const TailOp &o, const TailMat &M, int r0, int r1, double *ps)
+{
+    const int k0 = __ldg(M.off + r0);
+    const int nk = __ldg(M.off + r1) - k0;
+    double bpre = 0.0;
+    if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD)
+        if (r0 + (int)threadIdx.x < r1) bpre = __ldcg(o.b + r0 + threadIdx.x);
+    int lo = 0, hi = 0;
+    if (r0 + (int)threadIdx.x < r1) {
+        lo = __ldg(M.off + r0 + threadIdx.x) - k0;
+        hi = __ldg(M.off + r0 + threadIdx.x + 1) - k0;
+    }
+#pragma unroll 8
+    for (int k = threadIdx.x; k < nk; k += TAIL_THREADS)
+        ps[k] = prod(__ldg(M.val + k0 + k), __ldcg(o.x + __ldg(M.col + k0 + k)));
+    __syncthreads();
+    for (int rr = threadIdx.x; rr < r1 - r0; rr += TAIL_THREADS) {
+        if (rr != (int)threadIdx.x) {
+            lo = __ldg(M.off + r0 + rr) - k0;
+            hi = __ldg(M.off + r0 + rr + 1) - k0;
+        }
+        const double sv = row_sum_staged<1>(ps, 0, lo, hi, 0, 0u);
+        const int row = r0 + rr;
+        double bv = 0.0;
+        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD)
+            bv = (rr == (int)threadIdx.x) ? bpre : __ldcg(o.b + row);
+        double yv;
+        if constexpr (EPI == EPI_PLAIN) yv = sv;
+        else if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sv);
+        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(o.omega, sv));
+        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(o.omega, sv);
+        else yv = add(bv, sv);
+        o.y[row] = yv;
+    }
+}
+
 template <int EPI>
 __device__ __forceinline__ void tail_spmv(const TailOp &o, int r0, int r1, const int32_t *os, const int32_t *cs,
                                           const double *vs, double *ps)
 {
+    if (r1 <= r0) return;  // no rows on this CTA (CTA 0 runs the coarsest solve; its smem holds the factor)
     const int nk = os[r1 - r0];
     // prefetch the epilogue operand of this thread's first row with the gathers
     double bpre = 0.0;
@@ -1795,21 +1843,21 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
     __shared__ TailOp s_ops[TAIL_MAX_OPS];
     __shared__ int s_split[TAIL_MAX_MATS][2];
     __shared__ int s_geo[TAIL_MAX_MATS][3];
-    __shared__ double s_dinv[TAIL_MAX_DINV];
     char *smem = reinterpret_cast<char *>(sh);
     double *ps = reinterpret_cast<double *>(smem + prod_off);  // product buffer
     const unsigned rank = cluster_rank();
     // ---- stage static data (before waiting on the predecessor)
-    const double *L = c.Lp;
-    const double *dinv = c.dinv;
-    if (rank == 0 && c.kind == 0 && c.staged) {
-        double *Ls = sh + ((c.n + 1) & ~1);
-        for (int64_t i = threadIdx.x; i < tri(c.n); i += blockDim.x) Ls[i] = c.Lp[i];
+    const double *L = c.Lp, *D = c.dinv;
+    double *ctmp = sh + ((c.n + 1) & ~1);
+    if (rank == 0 && c.kind == 0 && c.staged) {  // CTA 0 owns no SpMV rows: its smem is the coarse area
+        double *Ds = ctmp + 32;
+        for (int i = threadIdx.x; i < c.n; i += blockDim.x) Ds[i] = c.dinv[i];
+        double *Ls = Ds + ((c.n + 1) & ~1);
+        const int64_t np = tri(c.n);
+#pragma unroll 8
+        for (int64_t i = threadIdx.x; i < np; i += blockDim.x) Ls[i] = __ldg(c.Lp + i);
         L = Ls;
-        if (c.n <= TAIL_MAX_DINV) {
-            for (int i = threadIdx.x; i < c.n; i += blockDim.x) s_dinv[i] = c.dinv[i];
-            dinv = s_dinv;
-        }
+        D = Ds;
     }
     {
         const int nw = nops * (int)(sizeof(TailOp) / 4);
@@ -1819,14 +1867,16 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
         for (int m = threadIdx.x; m < nmats; m += blockDim.x) {
             s_split[m][0] = splits[mats[m].split + rank];
             s_split[m][1] = splits[mats[m].split + rank + 1];
-            s_geo[m][0] = mats[m].smem_off;
+            s_geo[m][0] = mats[m].staged ? mats[m].smem_off : -1;
             s_geo[m][1] = mats[m].rows_cap;
             s_geo[m][2] = mats[m].nnz_cap;
         }
     }
     for (int m = 0; m < nmats; ++m) {
         const TailMat M = mats[m];
+        if (!M.staged) continue;
         const int r0 = splits[M.split + rank], r1 = splits[M.split + rank + 1];
+        if (r1 <= r0) continue;  // no rows here: the region overlays the coarse area on CTA 0
         const int k0 = M.off[r0];
         int32_t *os = reinterpret_cast<int32_t *>(smem + M.smem_off);
         int32_t *cs = reinterpret_cast<int32_t *>(smem + M.smem_off + (((M.rows_cap + 1) * 4 + 15) & ~15));
@@ -1850,6 +1900,19 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
         if (o.kind == TAIL_SPMV) {
             const int r0 = s_split[o.mat][0], r1 = s_split[o.mat][1];
             const int moff = s_geo[o.mat][0], rcap = s_geo[o.mat][1], kcap = s_geo[o.mat][2];
+            if (moff < 0) {
+                const TailMat M = mats[o.mat];
+                switch (o.epi) {
+                case EPI_PLAIN: tail_spmv_streamed<EPI_PLAIN>(o, M, r0, r1, ps); break;
+                case EPI_RESID: tail_spmv_streamed<EPI_RESID>(o, M, r0, r1, ps); break;
+                case EPI_AXPYW: tail_spmv_streamed<EPI_AXPYW>(o, M, r0, r1, ps); break;
+                case EPI_SETW: tail_spmv_streamed<EPI_SETW>(o, M, r0, r1, ps); break;
+                default: tail_spmv_streamed<EPI_ADD>(o, M, r0, r1, ps); break;
+                }
+                cluster_barrier();
+                if (trace && t0 == 0) trace[i + 1] = globaltimer();
+                continue;
+            }
             const int32_t *os = reinterpret_cast<const int32_t *>(smem + moff);
             const int32_t *cs = reinterpret_cast<const int32_t *>(smem + moff + (((rcap + 1) * 4 + 15) & ~15));
             const double *vs = reinterpret_cast<const double *>(reinterpret_cast<const char *>(cs) + ((kcap * 4 + 15) & ~15));
@@ -1869,7 +1932,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
             double *v = sh;
             for (int r = threadIdx.x; r < c.n; r += blockDim.x) v[r] = __ldcg(o.x + r);
             __syncthreads();
-            if (c.kind == 0) chol_solve_cta(c.n, L, dinv, v);
+            if (c.kind == 0) chol_solve_cta(c.n, L, D, v, ctmp);
             else lu_solve_cta(c.n, c.LU, c.piv, v);
             for (int r = threadIdx.x; r < c.n; r += blockDim.x) o.y[r] = v[r];
         }
