@@ -558,7 +558,7 @@ static CoarseArgs coarse_args(const amg_t *h)
     c.kind = h->coarse_kind == AMG_COARSE_CHOLESKY ? 0 : 1;
     c.staged = h->coarse_staged;
     c.Lp = h->Lp;
-    c.binv = h->binv;
+    c.mn = h->binv;
     c.dinv = h->dinv;
     c.LU = h->LU;
     c.piv = h->piv;
@@ -798,8 +798,9 @@ static int build_tail(amg_t *h)
     if (h->tail_nnz <= 0 || nl < 2 || h->nranks > 1) return AMG_OK;
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+    // CTA 0 of the tail stages v, tmp, 1/L_ii and the packed factor (not the pre-scaled blocks)
     const size_t coarse_bytes = (h->coarse_kind == AMG_COARSE_CHOLESKY && h->coarse_staged)
-                                    ? h->coarse_smem
+                                    ? (size_t)(2 * ((h->nc + 1) & ~1) + 32 + (int64_t)h->nc * (h->nc + 1) / 2) * sizeof(double)
                                     : (size_t)(((h->nc + 1) & ~1) + 32) * sizeof(double);
     const int budget = optin - (int)(TAIL_MAX_OPS * sizeof(TailOp) + TAIL_MAX_MATS * 5 * sizeof(int)) - 1024;  // static smem + slack
     // start level: the shallowest level (>= 1) from which every A_k has at most
@@ -1225,11 +1226,25 @@ int amg_upload_coarse(amg_t *h, int n, const double *factor, int kind, const int
             if (!(d > 0.0)) return fail(AMG_E_ARG, "amg_upload_coarse: Cholesky factor has a non-positive diagonal");
             dinv[i] = 1.0 / d;
         }
+        // pre-scaled diagonal blocks: Ms[r][c] = L[r][c] / L[c][c], Ns[r][c] = L[r][c] / L[r][r] (r > c)
+        const int nblk = (n + 31) / 32;
+        std::vector<double> mn((size_t)nblk * 1056, 0.0);
+        for (int b = 0; b < nblk; ++b) {
+            const int jb = b * 32, nb = std::min(32, n - jb);
+            for (int r = 0; r < nb; ++r)
+                for (int c2 = 0; c2 < r; ++c2) {
+                    const double l = factor[(size_t)(jb + r) * n + (jb + c2)];
+                    mn[(size_t)b * 1056 + r * (r + 1) / 2 + c2] = l * dinv[jb + c2];
+                    mn[(size_t)b * 1056 + 528 + r * (r + 1) / 2 + c2] = l * dinv[jb + r];
+                }
+        }
+        TRY(dalloc(&h->binv, mn.size()));
+        CK(cudaMemcpy(h->binv, mn.data(), mn.size() * sizeof(double), cudaMemcpyHostToDevice));
         TRY(dalloc(&h->Lp, packed.size()));
         TRY(dalloc(&h->dinv, (size_t)n));
         CK(cudaMemcpy(h->Lp, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(h->dinv, dinv.data(), n * sizeof(double), cudaMemcpyHostToDevice));
-        const size_t vbytes = (size_t)(2 * ((n + 1) & ~1) + 32) * sizeof(double);  // v, tmp, 1/L_ii
+        const size_t vbytes = (size_t)(2 * ((n + 1) & ~1) + 32 + mn.size()) * sizeof(double);  // v, tmp, 1/L_ii, M/N
         const size_t lbytes = packed.size() * sizeof(double);
         if (vbytes + lbytes <= 200 * 1024) {
             h->coarse_staged = 1;

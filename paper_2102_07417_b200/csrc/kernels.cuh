@@ -1536,40 +1536,48 @@ constexpr int COARSE_THREADS = 256;
 
 __device__ __forceinline__ int64_t tri(int i) { return (int64_t)i * (i + 1) / 2; }
 
-// Blocked forward / back substitution (dpotrs order of operations per block:
-// warp 0 solves each 32x32 diagonal triangle by substitution with shuffles;
-// the rows below / above are updated as GEMVs).  The forward update reads
-// row segments L[i][jb..jb+31] with one warp per row (conflict-free smem,
-// shuffle reduction); the backward update reads L[jb+c][i] along rows.
-// `tmp` is unused (kept for the call signature of the staged layouts).
-__device__ void chol_solve_cta(int n, const double *__restrict__ L, const double *__restrict__ dinv, double *v,
-                               double *tmp)
+// Blocked forward / back substitution with the lower Cholesky factor.
+// Diagonal 32x32 blocks are solved by warp 0 with the pre-scaled blocks
+// Ms[r][c] = L[r][c] / L[c][c] (forward) and Ns[c][r] = L[c][r] / L[c][c]
+// (backward, L^T), packed lower triangles computed at upload: one step of the
+// substitution chain is then shuffle -> FMA, and the division by the
+// diagonal is applied to the whole block at the end.  Rows below / above the
+// block are updated as GEMVs (forward: one warp per row, conflict-free row
+// segments; backward: along rows of L).
+__device__ void chol_solve_cta(int n, const double *__restrict__ L, const double *__restrict__ dinv,
+                               const double *__restrict__ MN, double *v)
 {
-    (void)tmp;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
     const int nblk = (n + 31) / 32;
     for (int bi = 0; bi < nblk; ++bi) {  // forward: L y = b
         const int jb = bi * 32, nb = min(32, n - jb);
-        if (warp == 0) {
+        if (warp == 0 && MN == nullptr) {  // unscaled chain: vc = v_c / L_cc, then vi -= L_ic vc
             double vi = lane < nb ? v[jb + lane] : 0.0;
             const double di = lane < nb ? dinv[jb + lane] : 0.0;
             const double *Lr = L + tri(jb + lane) + jb;
-            if (nb == 32) {
-#pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const double vc = __shfl_sync(0xffffffffu, vi * di, c);
-                    if (lane == c) vi = vc;
-                    if (lane > c) vi -= Lr[c] * vc;
-                }
-            } else {
-                for (int c = 0; c < nb; ++c) {
-                    const double vc = __shfl_sync(0xffffffffu, vi * di, c);
-                    if (lane == c) vi = vc;
-                    if (lane > c && lane < nb) vi -= Lr[c] * vc;
-                }
+            for (int c = 0; c < nb; ++c) {
+                const double vc = __shfl_sync(0xffffffffu, vi * di, c);
+                if (lane == c) vi = vc;
+                if (lane > c && lane < nb) vi -= Lr[c] * vc;
             }
             if (lane < nb) v[jb + lane] = vi;
+        } else if (warp == 0) {
+            const double *Mr = MN + (size_t)bi * 1056 + lane * (lane + 1) / 2;  // row `lane` of Ms
+            double vi = lane < nb ? v[jb + lane] : 0.0;
+            if (nb == 32) {
+#pragma unroll
+                for (int c = 0; c < 31; ++c) {
+                    const double vc = __shfl_sync(0xffffffffu, vi, c);
+                    if (lane > c) vi = fma(-Mr[c], vc, vi);
+                }
+            } else {
+                for (int c = 0; c + 1 < nb; ++c) {
+                    const double vc = __shfl_sync(0xffffffffu, vi, c);
+                    if (lane > c && lane < nb) vi = fma(-Mr[c], vc, vi);
+                }
+            }
+            if (lane < nb) v[jb + lane] = vi * dinv[jb + lane];
         }
         __syncthreads();
         const double vb = lane < nb ? v[jb + lane] : 0.0;
@@ -1583,24 +1591,31 @@ __device__ void chol_solve_cta(int n, const double *__restrict__ L, const double
     }
     for (int bi = nblk - 1; bi >= 0; --bi) {  // backward: L^T z = y
         const int jb = bi * 32, nb = min(32, n - jb);
-        if (warp == 0) {
+        if (warp == 0 && MN == nullptr) {
             double vi = lane < nb ? v[jb + lane] : 0.0;
             const double di = lane < nb ? dinv[jb + lane] : 0.0;
-            if (nb == 32) {
-#pragma unroll
-                for (int c = 31; c >= 0; --c) {
-                    const double zc = __shfl_sync(0xffffffffu, vi * di, c);
-                    if (lane == c) vi = zc;
-                    if (lane < c) vi -= L[tri(jb + c) + jb + lane] * zc;  // L^T[lane][c] = L[c][lane]
-                }
-            } else {
-                for (int c = nb - 1; c >= 0; --c) {
-                    const double zc = __shfl_sync(0xffffffffu, vi * di, c);
-                    if (lane == c) vi = zc;
-                    if (lane < c) vi -= L[tri(jb + c) + jb + lane] * zc;
-                }
+            for (int c = nb - 1; c >= 0; --c) {
+                const double zc = __shfl_sync(0xffffffffu, vi * di, c);
+                if (lane == c) vi = zc;
+                if (lane < c) vi -= L[tri(jb + c) + jb + lane] * zc;  // L^T[lane][c] = L[c][lane]
             }
             if (lane < nb) v[jb + lane] = vi;
+        } else if (warp == 0) {
+            const double *N = MN + (size_t)bi * 1056 + 528;
+            double vi = lane < nb ? v[jb + lane] : 0.0;
+            if (nb == 32) {
+#pragma unroll
+                for (int c = 31; c > 0; --c) {
+                    const double vc = __shfl_sync(0xffffffffu, vi, c);
+                    if (lane < c) vi = fma(-N[c * (c + 1) / 2 + lane], vc, vi);
+                }
+            } else {
+                for (int c = nb - 1; c > 0; --c) {
+                    const double vc = __shfl_sync(0xffffffffu, vi, c);
+                    if (lane < c) vi = fma(-N[c * (c + 1) / 2 + lane], vc, vi);
+                }
+            }
+            if (lane < nb) v[jb + lane] = vi * dinv[jb + lane];
         }
         __syncthreads();
         for (int i = threadIdx.x; i < jb; i += blockDim.x) {
@@ -1651,7 +1666,7 @@ struct CoarseArgs {
     int kind;    // 0 cholesky, 1 lu
     int staged;  // packed factor + block inverses copied to shared memory
     const double *Lp;
-    const double *binv;  // packed inverses of the 32x32 diagonal blocks (528 doubles per block)
+    const double *mn;    // per diagonal block: Ms then Ns (2 x 528 doubles, packed lower)
     const double *dinv;
     const double *LU;
     const int32_t *piv;
@@ -1667,23 +1682,27 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_solve_k(const CoarseArg
     const int n = c.n;
     double *v = sh;
     double *tmp = sh + ((n + 1) & ~1);
-    const double *L = c.Lp, *D = c.dinv;
+    const double *L = c.Lp, *D = c.dinv, *MN = c.mn;
     if (c.kind == 0 && c.staged) {  // the factor is static: stage it before waiting on the producer
         double *Ds = tmp + 32;
         for (int i = threadIdx.x; i < n; i += blockDim.x) Ds[i] = c.dinv[i];
-        double *Ls = Ds + ((n + 1) & ~1);
+        double *MNs = Ds + ((n + 1) & ~1);
+        const int nmn = ((n + 31) / 32) * 1056;
+        for (int i = threadIdx.x; i < nmn; i += blockDim.x) MNs[i] = __ldg(c.mn + i);
+        double *Ls = MNs + nmn;
         const int64_t np = tri(n);
 #pragma unroll 8
         for (int64_t i = threadIdx.x; i < np; i += blockDim.x) Ls[i] = __ldg(c.Lp + i);
         L = Ls;
         D = Ds;
+        MN = MNs;
     }
     pdl_launch();
     pdl_wait();
     if (!gate_open(gate1, nullptr)) return;
     for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = y[i];
     __syncthreads();
-    if (c.kind == 0) chol_solve_cta(n, L, D, v, tmp);
+    if (c.kind == 0) chol_solve_cta(n, L, D, MN, v);
     else lu_solve_cta(n, c.LU, c.piv, v);
     double acc = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -1847,11 +1866,13 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
     double *ps = reinterpret_cast<double *>(smem + prod_off);  // product buffer
     const unsigned rank = cluster_rank();
     // ---- stage static data (before waiting on the predecessor)
-    const double *L = c.Lp, *D = c.dinv;
+    const double *L = c.Lp, *D = c.dinv, *MN = c.mn;
     double *ctmp = sh + ((c.n + 1) & ~1);
     if (rank == 0 && c.kind == 0 && c.staged) {  // CTA 0 owns no SpMV rows: its smem is the coarse area
         double *Ds = ctmp + 32;
         for (int i = threadIdx.x; i < c.n; i += blockDim.x) Ds[i] = c.dinv[i];
+        // the pre-scaled diagonal blocks stay in L2 here (their loads hoist off the chain);
+        // a smaller footprint lets the cluster launch early
         double *Ls = Ds + ((c.n + 1) & ~1);
         const int64_t np = tri(c.n);
 #pragma unroll 8
@@ -1932,7 +1953,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
             double *v = sh;
             for (int r = threadIdx.x; r < c.n; r += blockDim.x) v[r] = __ldcg(o.x + r);
             __syncthreads();
-            if (c.kind == 0) chol_solve_cta(c.n, L, D, v, ctmp);
+            if (c.kind == 0) chol_solve_cta(c.n, L, D, c.staged ? nullptr : MN, v);
             else lu_solve_cta(c.n, c.LU, c.piv, v);
             for (int r = threadIdx.x; r < c.n; r += blockDim.x) o.y[r] = v[r];
         }
