@@ -149,7 +149,7 @@ def load(args):
     if not os.path.exists(os.path.join(d, "manifest.json")):
         raise SystemExit(f"bench: hierarchy cache {d} missing (run tools/export_hierarchy.py {args.config})")
     h = hiercache.load_hierarchy(d, verify=True)
-    b = problems.rhs_uniform(h.levels[0].a.nrows, 42)
+    b = problems.build_rhs(args.config, h.levels[0].a.nrows)
     return h, b
 
 

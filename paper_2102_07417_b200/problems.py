@@ -17,6 +17,15 @@ same storage ``SparseMatrix.from_coo`` produces (``amgkit/sparse.py:149-156``).
   per cell from ``default_rng(seed)`` (or per ``block``^3 cell block);
   an eliminated Dirichlet neighbour adds w * k_i to the diagonal, following
   ``gen_heterogeneous``'s convention (``problems.py:223-231``).
+* config 3 -- ``elasticity3d``: trilinear Q1 hexahedra on the unit cube
+  (element size h = 1/n), 3 dofs per node, node-major xyz dof order, the
+  x = 0 face clamped (its dofs eliminated) -- restating
+  ``gen_elasticity3d`` / ``hex_element_stiffness``
+  (``amgkit/problems.py:91-199``) with a per-element Young's modulus
+  E_e = exp(sigma * N(0,1)) from ``default_rng(seed)`` (sigma = 1) and
+  nu = 0.3; K_e = E_e * h * K_unit (3-D elasticity scales linearly in h).
+  RHS: body load (0, 0, -1) per node times the nodal volume h^3, times
+  (1 + 0.01 N(0,1)) per dof from ``default_rng(seed + 1)``.
 * config 4 -- ``rtanis7``: ``gen_rotated_anisotropy(nx, ny, nz, theta=0,
   kx=1, ky=1, kz=eps)`` (``problems.py:62-88``); with theta = 0 the cross
   terms vanish exactly and are eliminated, leaving a 7-point stencil with
@@ -28,7 +37,8 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["Csr", "poisson7", "rtanis7", "hetero27", "rhs_uniform", "build_config", "CONFIGS"]
+__all__ = ["Csr", "poisson7", "rtanis7", "hetero27", "elasticity3d", "hex_stiffness", "rhs_uniform", "rhs_body_load",
+           "build_config", "build_rhs", "CONFIGS"]
 
 
 class Csr:
@@ -161,6 +171,96 @@ def hetero27(nx, ny, nz, sigma=2.0, seed=42, block=1):
     return _assemble(nx, ny, nz, _offsets27(), coupling, lambda d, idx: d)
 
 
+def hex_stiffness(e, nu, hx=1.0, hy=1.0, hz=1.0):
+    """Q1 hexahedron stiffness (8 nodes x 3 dofs, 2x2x2 Gauss); restates
+    ``hex_element_stiffness`` (``amgkit/problems.py:91-139``): node order x
+    fastest, dof order node-major xyz."""
+    lam = e * nu / ((1.0 + nu) * (1.0 - 2.0 * nu))
+    mu = e / (2.0 * (1.0 + nu))
+    d = np.zeros((6, 6))
+    d[:3, :3] = lam
+    d[np.arange(3), np.arange(3)] += 2.0 * mu
+    d[3:, 3:] = np.eye(3) * mu
+    corners = np.array([[sx, sy, sz] for sz in (-1, 1) for sy in (-1, 1) for sx in (-1, 1)], dtype=float)
+    g = np.array([-1.0, 1.0]) / np.sqrt(3.0)
+    half = np.array([hx, hy, hz]) / 2.0
+    detj = float(np.prod(half))
+    ke = np.zeros((24, 24))
+    for gx in g:
+        for gy in g:
+            for gz in g:
+                xi = (gx, gy, gz)
+                dn = np.empty((8, 3))
+                for a in range(8):
+                    sx, sy, sz = corners[a]
+                    dn[a, 0] = sx * (1 + sy * xi[1]) * (1 + sz * xi[2]) / 8.0
+                    dn[a, 1] = sy * (1 + sx * xi[0]) * (1 + sz * xi[2]) / 8.0
+                    dn[a, 2] = sz * (1 + sx * xi[0]) * (1 + sy * xi[1]) / 8.0
+                dn = dn / half
+                bm = np.zeros((6, 24))
+                for a in range(8):
+                    bx, by, bz = dn[a]
+                    c = 3 * a
+                    bm[0, c], bm[1, c + 1], bm[2, c + 2] = bx, by, bz
+                    bm[3, c], bm[3, c + 1] = by, bx
+                    bm[4, c + 1], bm[4, c + 2] = bz, by
+                    bm[5, c], bm[5, c + 2] = bz, bx
+                ke += bm.T @ d @ bm * detj
+    return ke
+
+
+def elasticity3d(nx, ny, nz, sigma=1.0, nu=0.3, seed=42):
+    """Config-3 operator and node coordinates (see module doc)."""
+    import scipy.sparse as sp
+
+    h = 1.0 / nx
+    mx, my, mz = nx + 1, ny + 1, nz + 1
+    node = lambda i, j, k: i + mx * (j + my * k)
+    ke = hex_stiffness(1.0, nu, h, h, h)
+    young = np.exp(sigma * np.random.default_rng(seed).standard_normal(nx * ny * nz))
+    ei, ej, ek = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+    # element e = ei + nx * (ej + ny * ek) (x fastest, like the nodes)
+    ei, ej, ek = ei.transpose(2, 1, 0).ravel(), ej.transpose(2, 1, 0).ravel(), ek.transpose(2, 1, 0).ravel()
+    corners = np.stack([node(ei + dx, ej + dy, ek + dz) for dz in (0, 1) for dy in (0, 1) for dx in (0, 1)], axis=1)
+    dofs = (3 * corners[:, :, None] + np.arange(3)).reshape(-1, 24)
+    n_nodes = mx * my * mz
+    keep_node = np.ones(n_nodes, dtype=bool)
+    keep_node[np.arange(n_nodes) % mx == 0] = False  # clamp x = 0
+    keep_dof = np.repeat(keep_node, 3)
+    new_dof = np.full(3 * n_nodes, -1, dtype=np.int64)
+    new_dof[keep_dof] = np.arange(int(keep_dof.sum()))
+    nd = int(keep_dof.sum())
+    rows_l, cols_l, vals_l = [], [], []
+    chunk = 1 << 16
+    for e0 in range(0, dofs.shape[0], chunk):
+        dd = dofs[e0:e0 + chunk]
+        r = np.repeat(dd, 24, axis=1).ravel()
+        c = np.tile(dd, (1, 24)).ravel()
+        v = (young[e0:e0 + chunk, None] * ke.ravel()[None, :]).ravel()
+        ok = keep_dof[r] & keep_dof[c]
+        rows_l.append(new_dof[r[ok]])
+        cols_l.append(new_dof[c[ok]])
+        vals_l.append(v[ok])
+    m = sp.coo_matrix((np.concatenate(vals_l), (np.concatenate(rows_l), np.concatenate(cols_l))), shape=(nd, nd)).tocsr()
+    m.sum_duplicates()
+    m.sort_indices()
+    m.eliminate_zeros()
+    ii, jj, kk = np.meshgrid(np.arange(mx), np.arange(my), np.arange(mz), indexing="ij")
+    coords = np.empty((n_nodes, 3))
+    flat = node(ii, jj, kk).ravel()
+    coords[flat, 0] = ii.ravel() * h
+    coords[flat, 1] = jj.ravel() * h
+    coords[flat, 2] = kk.ravel() * h
+    return Csr(nd, nd, m.indptr, m.indices, m.data), coords[keep_node]
+
+
+def rhs_body_load(n_dofs, h, seed=42):
+    """Config-3 RHS: (0, 0, -1) h^3 per node times (1 + 0.01 N(0,1)) per dof."""
+    f = np.zeros(n_dofs)
+    f[2::3] = -(h ** 3)
+    return f * (1.0 + 0.01 * np.random.default_rng(seed + 1).standard_normal(n_dofs))
+
+
 def rhs_uniform(n, seed=42):
     """``default_rng(seed).uniform(-1, 1, n)`` (BASELINE RHS for configs 1, 2, 4, 5)."""
     return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
@@ -171,16 +271,31 @@ def rhs_uniform(n, seed=42):
 CONFIGS = {
     "c1_poisson7_64": (poisson7, (64, 64, 64), {}, {"smoother": "fsai"}),
     "c2_hetero27_128": (hetero27, (128, 128, 128), {"sigma": 2.0, "seed": 42}, {"smoother": "fsai"}),
+    "c3_elasticity_64": (elasticity3d, (64, 64, 64), {"sigma": 1.0, "nu": 0.3, "seed": 42},
+                         {"smoother": "fsai", "interp": "bamg", "testspace": "rigid_body", "n_test_vectors": 6}),
     "c4_rtanis7_256": (rtanis7, (256, 256, 256), {"kx": 1.0, "ky": 1.0, "kz": 1e-3}, {"smoother": "fsai"}),
     "c5_hetero27_512": (hetero27, (512, 512, 256), {"sigma": 3.0, "seed": 42, "block": 4}, {"smoother": "fsai"}),
     # reduced-size stand-ins used by tests and smoke runs
     "t_poisson7_16": (poisson7, (16, 16, 16), {}, {"smoother": "fsai"}),
     "t_hetero27_24": (hetero27, (24, 24, 24), {"sigma": 2.0, "seed": 42}, {"smoother": "fsai"}),
     "t_rtanis7_32": (rtanis7, (32, 32, 32), {"kx": 1.0, "ky": 1.0, "kz": 1e-3}, {"smoother": "fsai"}),
+    "t_elasticity_12": (elasticity3d, (12, 12, 12), {"sigma": 1.0, "nu": 0.3, "seed": 42},
+                        {"smoother": "fsai", "interp": "bamg", "testspace": "rigid_body", "n_test_vectors": 6}),
 }
 
 
-def build_config(name):
-    """Level-0 operator of a named config."""
+def build_config(name, with_coords=False):
+    """Level-0 operator of a named config (and node coordinates for elasticity)."""
     fn, args, kwargs, _ = CONFIGS[name]
-    return fn(*args, **kwargs)
+    out = fn(*args, **kwargs)
+    if isinstance(out, tuple):
+        return out if with_coords else out[0]
+    return (out, None) if with_coords else out
+
+
+def build_rhs(name, n):
+    """Right-hand side of a named config (seed 42)."""
+    fn, args, kwargs, _ = CONFIGS[name]
+    if fn is elasticity3d:
+        return rhs_body_load(n, 1.0 / args[0], kwargs.get("seed", 42))
+    return rhs_uniform(n, 42)

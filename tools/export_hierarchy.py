@@ -43,16 +43,19 @@ def main():
     args = ap.parse_args()
 
     fn, gargs, gkw, recipe = problems.CONFIGS[args.config]
-    a0 = problems.build_config(args.config)
+    a0, coords = problems.build_config(args.config, with_coords=True)
     A = SparseMatrix(a0.nrows, a0.ncols, a0.row_offsets, a0.col_indices, a0.values, check=True)
+    cfg = dict(recipe)
+    if coords is not None:
+        cfg["coords"] = coords
     t0 = time.perf_counter()
-    h = setup(A, AmgConfig(**recipe))
+    h = setup(A, AmgConfig(**cfg))
     t_setup = time.perf_counter() - t0
     flags = []
     for lvl in h.levels[:-1]:
         flags.append(bool(is_symmetric(lvl.a)) if h.symmetric else False)
     extra = {
-        "recipe": recipe,
+        "recipe": {k: v for k, v in recipe.items()},
         "setup_seconds": t_setup,
         "peak_rss_mb": resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1024.0,
         "amgkit_version": amgkit.__version__,
@@ -62,7 +65,7 @@ def main():
         "nnz": [int(l.a.nnz) for l in h.levels],
     }
     if args.solve:
-        b = problems.rhs_uniform(A.nrows, 42)
+        b = problems.build_rhs(args.config, A.nrows)
         t1 = time.perf_counter()
         res = pcg(lambda v: spmv(A, v), b, apply_m=lambda r: vcycle(h, r),
                   config=KrylovConfig(rtol=1e-8, record_history=True))
