@@ -16,6 +16,7 @@
  *   amg_coarse_solve  hierarchy.py:149-152   AmgHierarchy.coarse_solve(b)
  *   amg_vcycle        hierarchy.py:294-312   vcycle(h, y)
  *   amg_pcg           krylov.py:40-92        pcg(spmv(A0,.), b, vcycle(h,.), x0, config)
+ *   amg_bicgstab      krylov.py:95-193       bicgstab(spmv(A0,.), b, vcycle(h,.), x0, config)
  * Error mapping (errors.py): AMG_E_DIM -> DimensionMismatchError,
  * AMG_E_NOT_SPD -> NotSpdError, everything else -> AmgError.
  *
@@ -56,7 +57,8 @@ enum {
     AMG_E_NOT_SPD = 3,  /* PCG curvature <= 0                    -> NotSpdError */
     AMG_E_CUDA = 4,     /* CUDA runtime failure / no GPU         -> AmgError */
     AMG_E_NCCL = 5,     /* NCCL failure                          -> AmgError */
-    AMG_E_STATE = 6     /* handle not finalized / already final  -> AmgError */
+    AMG_E_STATE = 6,    /* handle not finalized / already final  -> AmgError */
+    AMG_E_BREAKDOWN = 7 /* BiCGstab breakdown                    -> BreakdownError */
 };
 
 /* matrix slots of a level (Level.a, Level.p, Level.pt, Smoother.gmat, Smoother.gmat_t) */
@@ -137,6 +139,13 @@ int amg_vcycle(amg_t *h, const double *y, double *z, int on_device);
 int amg_pcg(amg_t *h, const double *b, const double *x0, double rtol, int max_iters,
             int recompute_every, double *x_out, int *n_iter, double *relres, int *converged,
             double *history, int *hist_len, double *curvature_at_fail, int on_device);
+
+/* Preconditioned BiCGstab (krylov.py:95-193): one restart on a vanishing
+ * shadow product, true-residual checks; AMG_E_BREAKDOWN on a breakdown the
+ * reference raises BreakdownError for (outputs hold the state at that point). */
+int amg_bicgstab(amg_t *h, const double *b, const double *x0, double rtol, int max_iters,
+                 int recompute_every, double *x_out, int *n_iter, double *relres, int *converged,
+                 int *restarts, double *history, int *hist_len, int on_device);
 
 int amg_get_stats(amg_t *h, amg_stats_t *out);
 /* Diagnostics: launch the SpMV kernel of matrix `which` `reps` times back to

@@ -17,6 +17,8 @@ from .solve import (  # noqa: F401
     KrylovConfig,
     KrylovResult,
     NotSpdError,
+    BreakdownError,
+    bicgstab,
     DimensionMismatchError,
     apply_smoother,
     coarse_solve,

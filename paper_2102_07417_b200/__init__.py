@@ -15,9 +15,9 @@ Reference names mirrored: ``pcg``, ``KrylovConfig``, ``KrylovResult``,
 ``vcycle``, ``spmv``, ``apply_smoother``, ``AmgError``,
 ``DimensionMismatchError``, ``NotSpdError``.
 """
-from .errors import AmgError, DimensionMismatchError, NotSpdError  # noqa: F401
+from .errors import AmgError, BreakdownError, DimensionMismatchError, NotSpdError  # noqa: F401
 from .device import DeviceHierarchy, DeviceMatrix, DeviceVcycle, model_bytes_flops  # noqa: F401
-from .krylov import KrylovConfig, KrylovResult, pcg  # noqa: F401
+from .krylov import KrylovConfig, KrylovResult, bicgstab, pcg  # noqa: F401
 from .ops import apply_smoother, coarse_solve, spmv, vcycle  # noqa: F401
 
 __version__ = "0.1.0"

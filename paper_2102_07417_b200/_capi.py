@@ -9,11 +9,11 @@ from __future__ import annotations
 import ctypes
 import os
 
-from .errors import AmgError, DimensionMismatchError, NotSpdError
+from .errors import AmgError, BreakdownError, DimensionMismatchError, NotSpdError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libamgb200.so")
 
-AMG_OK, AMG_E_ARG, AMG_E_DIM, AMG_E_NOT_SPD, AMG_E_CUDA, AMG_E_NCCL, AMG_E_STATE = range(7)
+AMG_OK, AMG_E_ARG, AMG_E_DIM, AMG_E_NOT_SPD, AMG_E_CUDA, AMG_E_NCCL, AMG_E_STATE, AMG_E_BREAKDOWN = range(8)
 AMG_A, AMG_P, AMG_PT, AMG_G, AMG_GT = range(5)
 SLOT = {"a": AMG_A, "p": AMG_P, "pt": AMG_PT, "g": AMG_G, "gt": AMG_GT}
 AMG_SMOOTHER_FSAI, AMG_SMOOTHER_JACOBI = 0, 1
@@ -25,7 +25,7 @@ EXPORTS = (
     "amg_set_partition", "amg_upload_matrix", "amg_set_smoother", "amg_upload_coarse",
     "amg_set_cycle", "amg_finalize", "amg_local_rows", "amg_spmv", "amg_smoother",
     "amg_coarse_solve", "amg_vcycle", "amg_pcg", "amg_get_stats", "amg_set_option", "amg_time_spmv",
-    "amg_nccl_unique_id", "amg_set_halo", "amg_set_agglomeration",
+    "amg_nccl_unique_id", "amg_set_halo", "amg_set_agglomeration", "amg_bicgstab",
 )
 
 
@@ -87,6 +87,7 @@ def lib():
         "amg_nccl_unique_id": (I32, [P]),
         "amg_set_halo": (I32, [P, I32, I32, I64, I64, I32, P, P, I32, P, P, P]),
         "amg_set_agglomeration": (I32, [P, I32]),
+        "amg_bicgstab": (I32, [P, P, P, D, I32, I32, P, P, P, P, P, P, P, I32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -105,6 +106,8 @@ def check(status, what=""):
         msg = f"{what}: {msg}"
     if status == AMG_E_NOT_SPD:
         raise NotSpdError(msg)
+    if status == AMG_E_BREAKDOWN:
+        raise BreakdownError(msg)
     if status == AMG_E_DIM:
         err = DimensionMismatchError(what or "amgb200", "?", "?")
         err.args = (msg,)

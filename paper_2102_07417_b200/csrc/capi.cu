@@ -132,6 +132,7 @@ struct amg_handle {
     PcgCtl *ctl_h = nullptr;  // pinned mirror
     double *b = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
     double *tmp_in = nullptr, *tmp_out = nullptr;
+    double *bicg[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // rs, v, phat, s, shat, t
     double *hist = nullptr;
     int hist_cap = 0;
     // options
@@ -997,6 +998,7 @@ void amg_destroy(amg_t *h)
     }
     F(h->Lp); F(h->LU); F(h->dinv); F(h->binv); F(h->tail_ops); F(h->tail_mats); F(h->tail_splits); F(h->piv); F(h->partials); F(h->ticket); F(h->ctl);
     F(h->b); F(h->x); F(h->r); F(h->z); F(h->p); F(h->q); F(h->tmp_in); F(h->tmp_out); F(h->hist);
+    for (auto *bp : h->bicg) F(bp);
     if (h->ctl_h) cudaFreeHost(h->ctl_h);
     if (h->gexec) cudaGraphExecDestroy(h->gexec);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -1788,6 +1790,172 @@ int amg_time_spmv(amg_t *h, int level, int which, int reps, double *ms_per_launc
     CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
     *ms_per_launch = ms / reps;
     return AMG_OK;
+}
+
+// ------------------------------------------------------------------ BiCGstab
+
+static int dev_dot(amg_t *h, const double *a, const double *b, int64_t n, double *out)
+{
+    TRY(launch_dot(h, a, b, n, FIN_STORE, nullptr, nullptr));
+    CK(cudaMemcpyAsync(&h->ctl_h->scratch, &h->ctl->scratch, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    TRY(sync_stream(h));
+    *out = h->ctl_h->scratch;
+    return AMG_OK;
+}
+
+static int bicg_op(amg_t *h, int mode, double *x, const double *p, const double *q, double alpha, double beta,
+                   double omega)
+{
+    BicgArgs a{};
+    a.n = h->lv[0].n;
+    a.x = x;
+    a.p = p;
+    a.q = q;
+    a.alpha = alpha;
+    a.beta = beta;
+    a.omega = omega;
+    a.mode = mode;
+    TRY(launch_k(h, bicg_update, vec_grid(h, a.n), VEC_THREADS, 0, a));
+    return AMG_OK;
+}
+
+int amg_bicgstab(amg_t *h, const double *b, const double *x0, double rtol, int max_iters, int recompute_every,
+                 double *x_out, int *n_iter, double *relres_out, int *converged, int *restarts_out,
+                 double *history, int *hist_len, int on_device)
+{
+    auto t_start = std::chrono::steady_clock::now();
+    TRY(check_final(h));
+    if (h->container) return fail(AMG_E_STATE, "matrix container handle: no hierarchy uploaded");
+    if (!b || !x_out || !n_iter || !relres_out || !converged) return fail(AMG_E_ARG, "amg_bicgstab: NULL argument");
+    if (max_iters < 0 || recompute_every < 1) return fail(AMG_E_ARG, "amg_bicgstab: bad max_iters / recompute_every");
+    const int64_t n = h->lv[0].n;
+    const int64_t cap = h->lv[0].cap;
+    for (auto *&bp : h->bicg)
+        if (!bp) TRY(dalloc(&bp, cap));
+    double *r = h->r, *x = h->x, *bb = h->b, *p = h->p;
+    double *rs = h->bicg[0], *v = h->bicg[1], *phat = h->bicg[2], *sv = h->bicg[3], *shat = h->bicg[4],
+           *t = h->bicg[5];
+    const DevMat &A = h->lv[0].m[AMG_A];
+    std::vector<double> hist;
+    int hl = 0, restarts = 0;
+    auto finish = [&](int its, double rr, int conv) -> int {
+        TRY(from_dev(h, x_out, x, n, on_device));
+        TRY(sync_stream(h));
+        *n_iter = its;
+        *relres_out = rr;
+        *converged = conv;
+        if (restarts_out) *restarts_out = restarts;
+        if (history && hist_len) {
+            hl = (int)std::min<size_t>(hist.size(), (size_t)max_iters + 1);
+            for (int i = 0; i < hl; ++i) history[i] = hist[i];
+            *hist_len = hl;
+        }
+        h->e2e_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+        return AMG_OK;
+    };
+    auto resid = [&]() -> int {  // r = b - A x
+        return launch_spmv(h, A, x, r, EPI_RESID, bb, 0.0, nullptr, FIN_NONE, nullptr, nullptr);
+    };
+    auto norm = [&](const double *a, double *out) -> int {
+        double d = 0.0;
+        TRY(dev_dot(h, a, a, n, &d));
+        *out = std::sqrt(d);
+        return AMG_OK;
+    };
+    TRY(to_dev(h, bb, b, n, on_device));
+    if (x0) TRY(to_dev(h, x, x0, n, on_device));
+    else CK(cudaMemsetAsync(x, 0, n * sizeof(double), h->stream));
+    double bnorm = 0.0;
+    TRY(norm(bb, &bnorm));
+    if (bnorm == 0.0) {  // krylov.py:106-109
+        CK(cudaMemsetAsync(x, 0, n * sizeof(double), h->stream));
+        return finish(0, 0.0, 1);
+    }
+    TRY(resid());
+    CK(cudaMemcpyAsync(rs, r, n * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    double rho = 1.0, alpha = 1.0, omega = 1.0;
+    CK(cudaMemsetAsync(v, 0, n * sizeof(double), h->stream));
+    CK(cudaMemsetAsync(p, 0, n * sizeof(double), h->stream));
+    double nr = 0.0;
+    TRY(norm(r, &nr));
+    double relres = nr / bnorm;
+    if (history) hist.push_back(relres);
+    if (relres <= rtol) return finish(0, relres, 1);
+    const double eps = 2.220446049250313e-16;
+    const double eps_break = eps * eps;
+    for (int it = 1; it <= max_iters; ++it) {
+        double rho_new = 0.0;
+        TRY(dev_dot(h, rs, r, n, &rho_new));
+        if (std::fabs(rho_new) < eps_break * bnorm * bnorm) {  // krylov.py:125-143
+            if (restarts >= 1) {
+                TRY(finish(it, relres, 0));
+                char buf[128];
+                snprintf(buf, sizeof(buf), "iteration %d: shadow product vanished twice (rho=%.3e)", it, rho_new);
+                return fail(AMG_E_BREAKDOWN, buf);
+            }
+            ++restarts;
+            TRY(resid());
+            TRY(norm(r, &nr));
+            relres = nr / bnorm;
+            if (relres <= rtol) return finish(it - 1, relres, 1);
+            CK(cudaMemcpyAsync(rs, r, n * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+            rho = alpha = omega = 1.0;
+            CK(cudaMemsetAsync(v, 0, n * sizeof(double), h->stream));
+            CK(cudaMemsetAsync(p, 0, n * sizeof(double), h->stream));
+            TRY(dev_dot(h, rs, r, n, &rho_new));
+        }
+        const double beta = (rho_new / rho) * (alpha / omega);
+        rho = rho_new;
+        TRY(bicg_op(h, 0, p, r, v, 0.0, beta, omega));                         // p = r + beta (p - omega v)
+        TRY(enqueue_vcycle(h, 0, p, phat, nullptr, FIN_NONE, nullptr));        // phat = M p
+        TRY(launch_spmv(h, A, phat, v, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, nullptr, nullptr));
+        double denom = 0.0;
+        TRY(dev_dot(h, rs, v, n, &denom));
+        if (denom == 0.0) {
+            TRY(finish(it, relres, 0));
+            return fail(AMG_E_BREAKDOWN, "iteration " + std::to_string(it) + ": stagnated (shadow direction orthogonal)");
+        }
+        alpha = rho / denom;
+        TRY(bicg_op(h, 1, sv, r, v, alpha, 0.0, 0.0));                         // s = r - alpha v
+        double ns = 0.0;
+        TRY(norm(sv, &ns));
+        if (ns / bnorm <= rtol) {                                                // krylov.py:154-165
+            TRY(bicg_op(h, 4, x, phat, nullptr, alpha, 0.0, 0.0));
+            TRY(resid());
+            TRY(norm(r, &nr));
+            relres = nr / bnorm;
+            if (history) hist.push_back(relres);
+            if (relres <= rtol) return finish(it, relres, 1);
+            continue;
+        }
+        TRY(enqueue_vcycle(h, 0, sv, shat, nullptr, FIN_NONE, nullptr));      // shat = M s
+        TRY(launch_spmv(h, A, shat, t, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, nullptr, nullptr));
+        double tt = 0.0, ts = 0.0;
+        TRY(dev_dot(h, t, t, n, &tt));
+        if (tt == 0.0) {
+            TRY(finish(it, relres, 0));
+            return fail(AMG_E_BREAKDOWN, "iteration " + std::to_string(it) + ": t vanished");
+        }
+        TRY(dev_dot(h, t, sv, n, &ts));
+        omega = ts / tt;
+        TRY(bicg_op(h, 2, x, phat, shat, alpha, 0.0, omega));                  // x += alpha phat + omega shat
+        TRY(bicg_op(h, 3, r, sv, t, 0.0, 0.0, omega));                         // r = s - omega t
+        if (it % recompute_every == 0) TRY(resid());
+        TRY(norm(r, &nr));
+        relres = nr / bnorm;
+        if (history) hist.push_back(relres);
+        if (relres <= rtol) {
+            TRY(resid());
+            TRY(norm(r, &nr));
+            relres = nr / bnorm;
+            if (relres <= rtol) return finish(it, relres, 1);
+        }
+        if (omega == 0.0) {
+            TRY(finish(it, relres, 0));
+            return fail(AMG_E_BREAKDOWN, "iteration " + std::to_string(it) + ": omega vanished");
+        }
+    }
+    return finish(max_iters, relres, 0);
 }
 
 int amg_get_stats(amg_t *h, amg_stats_t *out)

@@ -1515,6 +1515,36 @@ __global__ void __launch_bounds__(VEC_THREADS) halo_pack(const double *x, const 
         buf[i] = x[idx[i]];
 }
 
+// BiCGstab vector updates (krylov.py:146-172), numpy's operation order:
+// mode 0: p = r + beta * (p - omega * v)      x=p, p=r, q=v
+// mode 1: s = r - alpha * v                   x=s, p=r, q=v
+// mode 2: x = x + (alpha * phat + omega * shat)  x=x, p=phat, q=shat
+// mode 3: r = s - omega * t                   x=r, p=s, q=t
+// mode 4: x = x + alpha * phat                x=x, p=phat
+struct BicgArgs {
+    int64_t n;
+    double *x;
+    const double *p;
+    const double *q;
+    double alpha, beta, omega;
+    int mode;
+};
+
+__global__ void __launch_bounds__(VEC_THREADS) bicg_update(const BicgArgs a)
+{
+    pdl_launch();
+    pdl_wait();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+        switch (a.mode) {
+        case 0: a.x[i] = add(a.p[i], __dmul_rn(a.beta, __dsub_rn(a.x[i], __dmul_rn(a.omega, a.q[i])))); break;
+        case 1: a.x[i] = __dsub_rn(a.p[i], __dmul_rn(a.alpha, a.q[i])); break;
+        case 2: a.x[i] = add(a.x[i], add(__dmul_rn(a.alpha, a.p[i]), __dmul_rn(a.omega, a.q[i]))); break;
+        case 3: a.x[i] = __dsub_rn(a.p[i], __dmul_rn(a.omega, a.q[i])); break;
+        default: a.x[i] = add(a.x[i], __dmul_rn(a.alpha, a.p[i])); break;
+        }
+    }
+}
+
 // Loop continuation for the device while-loop graph.
 __global__ void pcg_continue(PcgCtl *c, cudaGraphConditionalHandle handle, int use_handle)
 {

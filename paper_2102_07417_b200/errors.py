@@ -14,8 +14,9 @@ try:  # optional: make `except amgkit.X` catch ours
     _RefAmg = (_ref.AmgError,)
     _RefDim = (_ref.DimensionMismatchError,)
     _RefSpd = (_ref.NotSpdError,)
+    _RefBrk = (_ref.BreakdownError,)
 except Exception:  # pragma: no cover - reference absent (GPU box)
-    _RefAmg = _RefDim = _RefSpd = ()
+    _RefAmg = _RefDim = _RefSpd = _RefBrk = ()
 
 
 class AmgError(*(_RefAmg or (Exception,))):
@@ -34,3 +35,7 @@ class DimensionMismatchError(AmgError, *_RefDim):
 
 class NotSpdError(AmgError, *_RefSpd):
     """Non-positive PCG curvature (``amgkit/errors.py:26-27``, ``krylov.py:67-72``)."""
+
+
+class BreakdownError(AmgError, *_RefBrk):
+    """BiCGstab breakdown (``amgkit/errors.py:30-31``, ``krylov.py:128-189``)."""

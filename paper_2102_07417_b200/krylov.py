@@ -18,7 +18,7 @@ import numpy as np
 from . import _capi as C
 from .device import DeviceMatrix, DeviceVcycle
 
-__all__ = ["KrylovConfig", "KrylovResult", "pcg"]
+__all__ = ["KrylovConfig", "KrylovResult", "pcg", "bicgstab"]
 
 
 @dataclass
@@ -89,3 +89,41 @@ def pcg(apply_a, b, apply_m=None, x0=None, config=None):
         restarts=0,
         solve_ms=float(s["solve_ms"]),
     )
+
+
+def bicgstab(apply_a, b, apply_m=None, x0=None, config=None):
+    """Preconditioned BiCGstab on the device (control flow of ``amgkit/krylov.py:95-193``).
+
+    Used by the reference for operator-filtered (nonsymmetric) hierarchies
+    (``amgkit/cli.py:242-251``).  Raises :class:`BreakdownError` where the
+    reference does.
+    """
+    import ctypes
+
+    if not isinstance(apply_a, DeviceMatrix) or apply_a.level != 0 or apply_a.slot != "a":
+        raise TypeError("bicgstab: apply_a must be DeviceHierarchy.A0 (no CPU fallback)")
+    if not isinstance(apply_m, DeviceVcycle) or apply_m.dh is not apply_a.dh:
+        raise TypeError("bicgstab: apply_m must be the DeviceVcycle of the same DeviceHierarchy")
+    cfg = config or KrylovConfig()
+    dh = apply_a.dh
+    n = dh.levels[0]["n"]
+    bin_, dev = dh._vec_in(b, n, "bicgstab", (n, n))
+    x0in = None
+    if x0 is not None:
+        x0in, _ = dh._vec_in(x0, n, "bicgstab", (n, n))
+    x = dh._vec_out(bin_, n)
+    n_iter, conv, rst, hist_len = C.I32(0), C.I32(0), C.I32(0), C.I32(0)
+    relres = C.D(0.0)
+    hist = np.empty(cfg.max_iters + 1, dtype=np.float64) if cfg.record_history else None
+    st = C.lib().amg_bicgstab(
+        dh._h, C.ptr(bin_), C.ptr(x0in), float(cfg.rtol), int(cfg.max_iters), int(cfg.recompute_every),
+        C.ptr(x), ctypes.byref(n_iter), ctypes.byref(relres), ctypes.byref(conv), ctypes.byref(rst),
+        C.ptr(hist), ctypes.byref(hist_len), dev,
+    )
+    C.check(st)
+    history = []
+    if hist is not None:
+        # the reference numbers history entries by iteration (restarts / s-exits keep the count)
+        history = [(i, float(hist[i])) for i in range(hist_len.value)]
+    return KrylovResult(x=x, converged=bool(conv.value), n_iterations=int(n_iter.value), relres=float(relres.value),
+                        history=history, restarts=int(rst.value))

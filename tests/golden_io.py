@@ -13,6 +13,7 @@ from paper_2102_07417_b200.problems import Csr
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 HIER_CASES = [
+    "poisson7_12_bicg",
     "poisson7_12",
     "hetero27_10",
     "rtanis7_12",
@@ -25,6 +26,16 @@ HIER_CASES = [
     "poisson2d_12_lu",
 ]
 SPMV_CASES = ["spmv_ragged", "spmv_longrow", "spmv_random_spd"]
+
+
+def cases_with(key):
+    """Hierarchy cases whose reference record includes `key` ("pcg" / "bicgstab")."""
+    out = []
+    for n in HIER_CASES:
+        with open(os.path.join(GOLDEN, n, "expect.json")) as f:
+            if key in json.load(f):
+                out.append(n)
+    return out
 
 
 def load_case(name):

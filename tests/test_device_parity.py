@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 from conftest import _relerr
-from golden_io import HIER_CASES, SPMV_CASES, load_case, load_spmv_case, matrices_of
+from golden_io import HIER_CASES, SPMV_CASES, cases_with, load_case, load_spmv_case, matrices_of
 from oracle import solve as O
 
 pytestmark = pytest.mark.gpu
@@ -85,7 +85,7 @@ def test_coarse_solve_and_vcycle(name, tail, cases):
 
 
 @pytest.mark.parametrize("opts", [{}, {"tail_nnz": 0}, {"pdl": 0}, {"graph": 1}])
-@pytest.mark.parametrize("name", [n for n in HIER_CASES if "twogrid" not in n and "lu" not in n])
+@pytest.mark.parametrize("name", cases_with("pcg"))
 def test_pcg_matches_reference(name, opts, cases):
     c, dh = _dh(name, cases, **{k: v for k, v in opts.items() if k != "graph"})
     dh.set_option("graph", opts.get("graph", 2))
@@ -217,3 +217,32 @@ def test_plan_upload_single_rank_matches_reference_upload(cases):
     np.testing.assert_array_equal(r1.x, r2.x)
     np.testing.assert_array_equal(dp.vcycle(c["y"]), dh.vcycle(c["y"]))
     dp.close()
+
+
+@pytest.mark.parametrize("name", ["poisson2d_12_lu", "poisson7_12_bicg"])
+def test_bicgstab_matches_reference(name, cases):
+    # krylov.py:95-193 on the device: the operator-filtered (nonsymmetric, LU-coarsest) hierarchy
+    c, dh = _dh(name, cases)
+    exp = c["expect"]["bicgstab"]
+    res = amg.bicgstab(dh.A0, c["b"], apply_m=dh.vcycle,
+                       config=amg.KrylovConfig(rtol=exp["rtol"], max_iters=exp["max_iters"], record_history=True))
+    assert res.converged == exp["converged"]
+    assert res.relres <= exp["rtol"]
+    true = np.linalg.norm(c["b"] - O.spmv(c["h"].levels[0].a, res.x)) / np.linalg.norm(c["b"])
+    assert res.relres == pytest.approx(true, rel=1e-6)
+    if name == "poisson2d_12_lu":
+        # operator-filtered nonsymmetric hierarchy: BiCGstab is chaotic here -- the
+        # oracle itself with b perturbed by one ulp takes 23 instead of 22 iterations
+        # and drifts from history entry 10 (tools/bicg_check.py); the V-cycle itself is
+        # bit-identical (test_coarse_solve_and_vcycle), so check the early trajectory
+        # and an iteration count within the perturbation spread
+        np.testing.assert_allclose([r for _, r in res.history[:6]], exp["history"][:6], rtol=1e-6)
+        assert abs(res.n_iterations - exp["n_iterations"]) <= max(3, exp["n_iterations"] // 4)
+    else:
+        assert abs(res.n_iterations - exp["n_iterations"]) <= 1
+        assert res.restarts == exp["restarts"]
+        m = min(len(res.history), len(exp["history"]))
+        np.testing.assert_allclose([r for _, r in res.history[:m]], exp["history"][:m], rtol=1e-5, atol=1e-13)
+        assert _relerr(res.x, c["vec"]["bicgstab_x"]) <= 1e-7
+    z = amg.bicgstab(dh.A0, np.zeros_like(c["b"]), apply_m=dh.vcycle)
+    assert z.converged and z.n_iterations == 0 and not z.x.any()

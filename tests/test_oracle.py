@@ -10,7 +10,7 @@ import os
 import numpy as np
 import pytest
 
-from golden_io import HIER_CASES, SPMV_CASES, load_case, load_spmv_case, matrices_of
+from golden_io import HIER_CASES, SPMV_CASES, cases_with, load_case, load_spmv_case, matrices_of
 from oracle import solve as O
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -34,7 +34,7 @@ def test_oracle_kernels_match_reference_bitwise(name):
     np.testing.assert_array_equal(O.vcycle(h, vec["y"]), vec["vcycle_z"])
 
 
-@pytest.mark.parametrize("name", [n for n in HIER_CASES if "twogrid" not in n and "lu" not in n])
+@pytest.mark.parametrize("name", cases_with("pcg"))
 def test_oracle_pcg_matches_reference(name):
     c = load_case(name)
     h, vec, exp = c["h"], c["vec"], c["expect"]["pcg"]
@@ -95,3 +95,15 @@ def test_oracle_pcg_edge_cases():
         O.pcg(lambda v: -A(v), c["b"], apply_m=M)
     r = O.pcg(A, c["b"], apply_m=M, config=O.KrylovConfig(rtol=1e-14, max_iters=3))
     assert not r.converged and r.n_iterations == 3
+
+
+@pytest.mark.parametrize("name", ["poisson2d_12_lu", "poisson7_12_bicg"])
+def test_oracle_bicgstab_matches_reference(name):
+    c = load_case(name)
+    h, vec, exp = c["h"], c["vec"], c["expect"]["bicgstab"]
+    a0 = h.levels[0].a
+    res = O.bicgstab(lambda v: O.spmv(a0, v), vec["b"], apply_m=lambda r: O.vcycle(h, r),
+                     config=O.KrylovConfig(rtol=exp["rtol"], max_iters=exp["max_iters"], record_history=True))
+    assert res.n_iterations == exp["n_iterations"] and res.converged == exp["converged"]
+    assert res.restarts == exp["restarts"]
+    np.testing.assert_allclose(res.x, vec["bicgstab_x"], rtol=0, atol=1e-13 * np.abs(vec["bicgstab_x"]).max())

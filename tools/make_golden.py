@@ -27,7 +27,7 @@ import numpy as np  # noqa: E402
 import scipy.sparse as sp  # noqa: E402
 
 from amgkit import (  # noqa: E402
-    AmgConfig, KrylovConfig, SparseMatrix, apply_smoother, pcg, setup, spmv, vcycle,
+    AmgConfig, KrylovConfig, SparseMatrix, apply_smoother, bicgstab, pcg, setup, spmv, vcycle,
 )
 from amgkit.problems import gen_elasticity3d, gen_poisson7  # noqa: E402
 from conftest import poisson1d, poisson2d, random_spd  # noqa: E402  (reference fixtures)
@@ -41,7 +41,7 @@ def _sm(m):
     return SparseMatrix(m.nrows, m.ncols, m.row_offsets, m.col_indices, m.values, check=True)
 
 
-def hierarchy_case(name, A, cfg, seed=7, rtol=1e-8, max_iters=500, solve=True):
+def hierarchy_case(name, A, cfg, seed=7, rtol=1e-8, max_iters=500, solve=True, bicg=False):
     d = os.path.join(OUT, name)
     if os.path.exists(d):
         shutil.rmtree(d)
@@ -84,6 +84,13 @@ def hierarchy_case(name, A, cfg, seed=7, rtol=1e-8, max_iters=500, solve=True):
         exp["pcg"] = {"rtol": rtol, "max_iters": max_iters, "converged": bool(res.converged),
                       "n_iterations": int(res.n_iterations), "relres": float(res.relres),
                       "history": [float(r) for _, r in res.history]}
+    if bicg:
+        res = bicgstab(lambda v: spmv(A, v), b, apply_m=lambda r: vcycle(h, r),
+                       config=KrylovConfig(rtol=rtol, max_iters=max_iters, record_history=True))
+        vec["bicgstab_x"] = res.x
+        exp["bicgstab"] = {"rtol": rtol, "max_iters": max_iters, "converged": bool(res.converged),
+                           "n_iterations": int(res.n_iterations), "relres": float(res.relres),
+                           "restarts": int(res.restarts), "history": [float(r) for _, r in res.history]}
     np.savez(os.path.join(d, "vectors.npz"), **vec)
     with open(os.path.join(d, "expect.json"), "w") as f:
         json.dump(exp, f, indent=1)
@@ -140,7 +147,8 @@ def main():
                                                       n_test_vectors=6, coords=coords, max_coarse=50))
     # nonsymmetric coarse operators -> LU coarsest factor (hierarchy.py:143-147)
     hierarchy_case("poisson2d_12_lu", poisson2d(12),
-                   AmgConfig(max_coarse=30, filter_target="operator", filter_rho=0.6), solve=False)
+                   AmgConfig(max_coarse=30, filter_target="operator", filter_rho=0.6), solve=False, bicg=True)
+    hierarchy_case("poisson7_12_bicg", gen_poisson7(12, 12, 12), AmgConfig(smoother="fsai"), solve=False, bicg=True)
     # row-sum order: ragged rows incl. empty and > 128 entries (recursive pairwise)
     rng = np.random.default_rng(5)
     lengths = np.concatenate([np.arange(0, 140), [0, 0, 200, 257, 300, 400, 129, 130, 136, 137],
