@@ -246,3 +246,23 @@ def test_bicgstab_matches_reference(name, cases):
         assert _relerr(res.x, c["vec"]["bicgstab_x"]) <= 1e-7
     z = amg.bicgstab(dh.A0, np.zeros_like(c["b"]), apply_m=dh.vcycle)
     assert z.converged and z.n_iterations == 0 and not z.x.any()
+
+
+def test_run_solve_report_and_cli(tmp_path):
+    # device-backed run_solve (cli.py:237-295) on a frozen reference hierarchy
+    from paper_2102_07417_b200.solve import main, run_solve
+
+    c = load_case("poisson7_12")
+    res, rep, _ = run_solve(c["h"].levels[0].a, c["b"], {"solver.rtol": 1e-8}, hierarchy=c["h"])
+    assert rep.converged and abs(rep.n_iterations - c["expect"]["pcg"]["n_iterations"]) <= 1
+    assert len(rep.history) == rep.n_iterations + 1
+    with pytest.raises(amg.AmgError, match="operator filtering"):
+        run_solve(c["h"].levels[0].a, c["b"], {"interp.filter_target": "operator", "interp.filter_rho": 0.5},
+                  hierarchy=c["h"])
+    from paper_2102_07417_b200 import hiercache
+
+    d = str(tmp_path / "h")
+    hiercache.save_hierarchy(c["h"], d, mode="full")
+    assert main(["solve", "--cache", d, "--format", "json", "--history", str(tmp_path / "hist.csv")]) == 0
+    assert main(["solve", "--cache", d, "--max-iters", "2"]) == 2
+    assert main(["solve", "--cache", str(tmp_path / "missing")]) == 1

@@ -74,3 +74,23 @@ def test_hetero27_sizes_and_symmetry():
     assert np.linalg.eigvalsh(d).min() > 0
     blk = problems.conductivity(8, 8, 8, 3.0, 42, block=4)
     assert np.unique(blk).size == 8
+
+
+def test_report_emit_matches_reference_schema():
+    from paper_2102_07417_b200.solve import SolveReport, level_table, report_emit, complexities
+
+    c = load_case("poisson7_12")
+    h = c["h"]
+    rep = SolveReport("pcg", True, 10, 1e-8, 3e-9, 1.2, 1.3, h.n_levels, level_table(h), 0.1, 0.2, 0.3,
+                      h.levels[0].a.nrows, h.levels[0].a.nnz, [(0, 1.0)])
+    doc = __import__("json").loads(report_emit(rep, "json"))
+    assert doc["schema_version"] == 1 and doc["n_iterations"] == 10 and len(doc["levels"]) == h.n_levels
+    assert report_emit(rep, "csv").startswith("level,n,nnz,avg_nnz_per_row,coarsening_ratio")
+    if have_reference():
+        from amgkit.cli import report_emit as ref_emit
+        from amgkit.hierarchy import SolveReport as RefReport, level_table as ref_table
+
+        assert level_table(h) == ref_table(h)
+        ref = RefReport(**rep.__dict__)
+        for fmt in ("json", "csv", "text"):
+            assert report_emit(rep, fmt) == ref_emit(ref, fmt)
