@@ -340,7 +340,7 @@ def run_amgb200(args):
         },
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": ncu_traffic(args.config), "kernel": "spmv_vec on A0 (plain epilogue, padded-aligned layout)",
+            "traffic": ncu_traffic(args.config), "kernel": "A0 SpMV, plain epilogue (auto layout; config 2: SELL-32 + stencil patterns)",
             "bytes_per_launch": k_bytes, "ms_per_launch": k_ms, "peak_source": peak_src,
         },
         "e2e": {"value": e2e_ms_iter, "unit": "ms/iter", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
