@@ -151,7 +151,7 @@ struct amg_handle {
     int lanes_override = 0;
     int pdl = 1;  // programmatic dependent launch between consecutive kernels
     // cluster tail: levels >= tail_level run inside one cluster kernel
-    int64_t tail_nnz = 400000;   // levels whose A_k has at most this many entries run in the cluster tail
+    int64_t tail_nnz = 100000;   // levels whose A_k has at most this many entries run in the cluster tail
     int tail_stage = 0;          // stage tail matrices in smem (measured slower on B200: the big smem
                                  // footprint delays the cluster launch; streamed from L2 by default)
     int cluster = 16;

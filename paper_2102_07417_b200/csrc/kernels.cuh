@@ -1305,7 +1305,7 @@ struct SellArgs {
 };
 
 template <int EPI, bool PAT>
-__global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_sell(const SpmvArgs a, const SellArgs sa, int nrows)
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, PAT ? 5 : 4) spmv_sell(const SpmvArgs a, const SellArgs sa, int nrows)
 {
     __shared__ double red[VEC_SPMV_THREADS / 32];
     __shared__ int32_t s_rel[PAT ? PAT_MAX_REL : 1];
