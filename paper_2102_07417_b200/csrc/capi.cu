@@ -145,6 +145,9 @@ struct amg_handle {
     int small_rows_per_sm = 512;  // below sm_count * this many rows a matrix counts as small
     int patterns = 1;             // stencil-pattern layout for square operators with few row patterns
     int sell = 1;                 // SELL-32 slices where padding <= sell_pad %
+    int gated_grid = 1;           // CTAs per SM for the rarely active gated residual SpMVs (0 = full grid)
+    int grid_per_sm = 0;          // cap on SpMV CTAs per SM (0 = occupancy)
+    int vec_per_sm = 0;           // cap on vector-kernel CTAs per SM (0 = 8)
     int sell_pad = 10;
     int direct_ctas = 0; // direct kernel CTAs per SM (0 = occupancy)
     int direct_per_sm = 8;
@@ -430,7 +433,7 @@ static int configure_kernels(amg_t *h, int *blocks_per_sm)
 static int exchange(amg_t *h, const DevMat &M, double *x);
 
 static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, int epi, const double *b, double omega,
-                       const double *dotw, int fin, const int *g1, const int *g2)
+                       const double *dotw, int fin, const int *g1, const int *g2, int grid_cap = 0)
 {
     if (h->collect) {
         if (dotw || fin != FIN_NONE) return fail(AMG_E_STATE, "internal: reduction inside the cluster tail");
@@ -449,6 +452,10 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         return AMG_OK;
     }
     TRY(exchange(h, M, const_cast<double *>(x)));
+    if (h->grid_per_sm > 0) {  // global cap on CTAs per SM (tuning)
+        const int c = h->grid_per_sm * h->sm_count;
+        grid_cap = grid_cap ? std::min(grid_cap, c) : c;
+    }
     const int ufin = fin;
     fin = kfin(h, fin);
     if (M.ntiles == 0) {
@@ -488,13 +495,16 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     a.gate2 = g2;
     if (M.sbeg) {
         SellArgs sa{M.sbeg, M.sval, M.scol, M.slen, M.pid, M.prel, M.pbeg, M.npat, M.nrel};
-        TRY(launch_k(h, spmv_sell_fn(epi, M.scol == nullptr), M.sell_grid, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
+        TRY(launch_k(h, spmv_sell_fn(epi, M.scol == nullptr), grid_cap ? std::min(grid_cap, M.sell_grid) : M.sell_grid,
+                     VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
     } else if (M.pid) {
         PatArgs pa{M.pstart, M.pval, M.pid, M.prel, M.pbeg, M.npat, M.nrel};
-        TRY(launch_k(h, spmv_pat_fn(epi), M.pad_grid, VEC_SPMV_THREADS, 0, a, pa, (int)M.nrows));
+        TRY(launch_k(h, spmv_pat_fn(epi), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
+                     pa, (int)M.nrows));
     } else if (M.pstart) {
         PadArgs pa{M.pstart, M.pval, M.pcol};
-        TRY(launch_k(h, spmv_vec_fn(epi), M.pad_grid, VEC_SPMV_THREADS, 0, a, pa, (int)M.nrows));
+        TRY(launch_k(h, spmv_vec_fn(epi), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
+                     pa, (int)M.nrows));
     } else if (h->kernel == 3 && M.nwtiles > 0) {
         SpmvArgs w = a;
         w.tiles = M.wtiles;
@@ -505,6 +515,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     } else if (h->kernel == 2) {
         const int gpr = DIRECT_THREADS / M.lanes;  // row groups per CTA
         int g = (int)std::min<int64_t>((M.nrows + gpr - 1) / gpr, (int64_t)h->sm_count * h->direct_per_sm);
+        if (grid_cap) g = std::min(g, grid_cap);
         TRY(launch_k(h, spmv_direct_fn(epi, M.lanes), std::max(g, 1), DIRECT_THREADS, 0, a, (int)M.nrows));
     } else if (h->ws) TRY(launch_k(h, spmv_ws_fn(epi, M.lanes), M.grid, WS_THREADS, (size_t)stage_smem(h), a));
     else TRY(launch_k(h, spmv_fn(epi, M.lanes), M.grid, TILE_THREADS, (size_t)stage_smem(h), a));
@@ -515,7 +526,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
 static int vec_grid(const amg_t *h, int64_t n)
 {
     int64_t g = (n + VEC_THREADS * 4 - 1) / (VEC_THREADS * 4);
-    g = std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)h->sm_count * 8));
+    g = std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)h->sm_count * (h->vec_per_sm > 0 ? h->vec_per_sm : 8)));
     return (int)g;
 }
 
@@ -701,9 +712,11 @@ static int enqueue_pcg_body(amg_t *h, cudaGraphConditionalHandle handle, int use
         TRY(post_fin(h, FIN_UPDATE, act));
     }
     // every recompute_every iterations: r = b - A x     (:76-77)
-    TRY(launch_spmv(h, A, h->x, h->r, EPI_RESID, h->b, 0.0, h->r, FIN_RECOMPUTE, act, &h->ctl->do_recompute));
+    // (rarely active: launched one CTA per SM so the usual no-op costs little)
+    const int gcap = h->gated_grid > 0 ? h->gated_grid * h->sm_count : 0;
+    TRY(launch_spmv(h, A, h->x, h->r, EPI_RESID, h->b, 0.0, h->r, FIN_RECOMPUTE, act, &h->ctl->do_recompute, gcap));
     // relres <= rtol: true residual check              (:81-86)
-    TRY(launch_spmv(h, A, h->x, h->r, EPI_RESID, h->b, 0.0, h->r, FIN_TRUE, act, &h->ctl->need_true));
+    TRY(launch_spmv(h, A, h->x, h->r, EPI_RESID, h->b, 0.0, h->r, FIN_TRUE, act, &h->ctl->need_true, gcap));
     // z = M r ; rz_new = r.z ; beta                     (:87-90)
     TRY(enqueue_vcycle(h, 0, h->r, h->z, act, FIN_RZ, h->r));
     if (h->lv.size() == 1) {
@@ -1029,6 +1042,9 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "small_rows_per_sm") { h->small_rows_per_sm = (int)value; return AMG_OK; }
     if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
     if (k == "sell") { h->sell = value ? 1 : 0; return AMG_OK; }
+    if (k == "grid_per_sm") { h->grid_per_sm = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
+    if (k == "vec_per_sm") { h->vec_per_sm = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
+    if (k == "gated_grid") { h->gated_grid = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "sell_pad") { h->sell_pad = (int)value; return AMG_OK; }
     if (k == "wt_nnz") { if (value < 64 || value > 1024) return fail(AMG_E_ARG, "wt_nnz out of range"); h->wt_nnz = (int)value; return AMG_OK; }
     if (k == "direct_ctas") { h->direct_ctas = (int)value; return AMG_OK; }
