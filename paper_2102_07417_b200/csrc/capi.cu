@@ -64,6 +64,7 @@ struct DevMat {
     double *sval = nullptr;
     int32_t *scol = nullptr;
     uint8_t *slen = nullptr;
+    int32_t *sperm = nullptr;    // SELL-sigma permutation (slice position -> row)
     int sell_grid = 0;
     uint8_t *pid = nullptr;      // stencil-pattern layout (spmv_pat): pattern id per row
     int32_t *prel = nullptr;     // concatenated relative offsets
@@ -142,13 +143,14 @@ struct amg_handle {
     int kernel = 2;      // 0: staged CTA tiles (spmv_tiles / spmv_ws), 2: direct register kernel, 3: warp tiles
     int wt_nnz = 256;    // warp-tile capacity (entries)
     int pad_min = 8;     // matrices averaging >= pad_min entries/row get the padded-aligned layout (0 = off)
-    int small_rows_per_sm = 512;  // below sm_count * this many rows a matrix counts as small
+    int small_rows_per_sm = 128;  // below sm_count * this many rows a matrix counts as small
     int patterns = 1;             // stencil-pattern layout for square operators with few row patterns
     int sell = 1;                 // SELL-32 slices where padding <= sell_pad %
     int gated_grid = 1;           // CTAs per SM for the rarely active gated residual SpMVs (0 = full grid)
     int grid_per_sm = 0;          // cap on SpMV CTAs per SM (0 = occupancy)
     int vec_per_sm = 0;           // cap on vector-kernel CTAs per SM (0 = 8)
     int sell_pad = 10;
+    int sell_sigma = 0;           // SELL-sigma sort window (rows); <= 32 disables (measured slower on config 2)
     int direct_ctas = 0; // direct kernel CTAs per SM (0 = occupancy)
     int direct_per_sm = 8;
     int lanes_override = 0;
@@ -494,7 +496,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     a.gate1 = g1;
     a.gate2 = g2;
     if (M.sbeg) {
-        SellArgs sa{M.sbeg, M.sval, M.scol, M.slen, M.pid, M.prel, M.pbeg, M.npat, M.nrel};
+        SellArgs sa{M.sbeg, M.sval, M.scol, M.slen, M.pid, M.prel, M.pbeg, M.npat, M.nrel, M.sperm};
         TRY(launch_k(h, spmv_sell_fn(epi, M.scol == nullptr), grid_cap ? std::min(grid_cap, M.sell_grid) : M.sell_grid,
                      VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
     } else if (M.pid) {
@@ -1004,7 +1006,7 @@ void amg_destroy(amg_t *h)
     auto F = [](void *p) { if (p) cudaFree(p); };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen);
+            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm);
             halo_free(M.halo);
         }
         F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
@@ -1046,6 +1048,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "vec_per_sm") { h->vec_per_sm = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "gated_grid") { h->gated_grid = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "sell_pad") { h->sell_pad = (int)value; return AMG_OK; }
+    if (k == "sell_sigma") { h->sell_sigma = (int)value; return AMG_OK; }
     if (k == "wt_nnz") { if (value < 64 || value > 1024) return fail(AMG_E_ARG, "wt_nnz out of range"); h->wt_nnz = (int)value; return AMG_OK; }
     if (k == "direct_ctas") { h->direct_ctas = (int)value; return AMG_OK; }
     if (k == "ctas_per_sm") { h->ctas_per_sm = (int)value; return AMG_OK; }
@@ -1484,29 +1487,55 @@ int amg_finalize(amg_t *h)
                 if (h->sell) {
                     const int64_t ns = (M.nrows + 31) / 32;
                     std::vector<int32_t> sb(ns + 1);
-                    int64_t tot = 0, maxlen = 0;
-                    for (int64_t sl = 0; sl < ns; ++sl) {
-                        int w = 0;
-                        for (int64_t r = sl * 32; r < std::min<int64_t>(M.nrows, sl * 32 + 32); ++r)
-                            w = std::max(w, off32[r + 1] - off32[r]);
-                        sb[sl] = (int32_t)tot;
-                        tot += (int64_t)w * 32;
-                        maxlen = std::max<int64_t>(maxlen, w);
+                    // slice order: natural, or (SELL-sigma) rows sorted by length inside windows of
+                    // sigma rows when the natural slices pad too much; the pattern layout keeps order
+                    std::vector<int32_t> order(M.nrows);
+                    for (int64_t r = 0; r < M.nrows; ++r) order[r] = (int32_t)r;
+                    auto slice_total = [&](int64_t *maxlen) {
+                        int64_t tot = 0;
+                        *maxlen = 0;
+                        for (int64_t sl = 0; sl < ns; ++sl) {
+                            int w = 0;
+                            for (int64_t p = sl * 32; p < std::min<int64_t>(M.nrows, sl * 32 + 32); ++p)
+                                w = std::max(w, off32[order[p] + 1] - off32[order[p]]);
+                            sb[sl] = (int32_t)tot;
+                            tot += (int64_t)w * 32;
+                            *maxlen = std::max<int64_t>(*maxlen, w);
+                        }
+                        sb[ns] = (int32_t)tot;
+                        return tot;
+                    };
+                    int64_t maxlen = 0;
+                    int64_t tot = slice_total(&maxlen);
+                    bool sorted = false;
+                    if (tot > (int64_t)(M.nnz * (1.0 + h->sell_pad / 100.0)) && M.pid == nullptr && h->sell_sigma > 32) {
+                        for (int64_t w0 = 0; w0 < M.nrows; w0 += h->sell_sigma) {
+                            const int64_t w1 = std::min<int64_t>(M.nrows, w0 + h->sell_sigma);
+                            std::stable_sort(order.begin() + w0, order.begin() + w1, [&](int32_t a, int32_t b) {
+                                return off32[a + 1] - off32[a] > off32[b + 1] - off32[b];
+                            });
+                        }
+                        tot = slice_total(&maxlen);
+                        sorted = true;
                     }
-                    sb[ns] = (int32_t)tot;
                     if (maxlen <= 129 && tot <= (int64_t)(M.nnz * (1.0 + h->sell_pad / 100.0)) && tot < INT32_MAX - 64) {
                         std::vector<double> sv(tot + 32, 0.0);
                         const bool pat = M.pid != nullptr;
                         std::vector<int32_t> sc(pat ? 0 : tot + 32, 0);
                         std::vector<uint8_t> ln(M.nrows + 16, 0);
-                        for (int64_t r = 0; r < M.nrows; ++r) {
-                            const int64_t sl = r / 32, l = r % 32;
-                            ln[r] = (uint8_t)(off32[r + 1] - off32[r]);
+                        for (int64_t q = 0; q < M.nrows; ++q) {  // q = slice position, r = row
+                            const int64_t r = order[q];
+                            const int64_t sl = q / 32, l = q % 32;
+                            ln[q] = (uint8_t)(off32[r + 1] - off32[r]);
                             for (int32_t k = off32[r]; k < off32[r + 1]; ++k) {
                                 const int64_t dst = sb[sl] + (int64_t)(k - off32[r]) * 32 + l;
                                 sv[dst] = val_h[k];
                                 if (!pat) sc[dst] = col_h[k];
                             }
+                        }
+                        if (sorted) {
+                            TRY(dalloc(&M.sperm, (size_t)M.nrows));
+                            CK(cudaMemcpy(M.sperm, order.data(), (size_t)M.nrows * sizeof(int32_t), cudaMemcpyHostToDevice));
                         }
                         TRY(dalloc(&M.sbeg, sb.size()));
                         TRY(dalloc(&M.sval, sv.size()));

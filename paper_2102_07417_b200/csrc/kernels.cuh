@@ -1302,6 +1302,7 @@ struct SellArgs {
     const int32_t *rel;
     const int32_t *pbeg;
     int npat, nrel;
+    const int32_t *perm;    // SELL-sigma: original row of each slice position (nullptr: identity)
 };
 
 template <int EPI, bool PAT>
@@ -1326,12 +1327,13 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, PAT ? 5 : 4) spmv_sell(const
     const double *__restrict__ x = a.x;
     double dacc = 0.0;
     for (int sl = blockIdx.x * (VEC_SPMV_THREADS / 32) + (threadIdx.x >> 5); sl < nslices; sl += wstride) {
-        const int row = sl * 32 + lane;
-        const bool live = row < nrows;
+        const int pos = sl * 32 + lane;  // slice position (== row unless rows are sigma-sorted)
+        const bool live = pos < nrows;
         const int sb = __ldg(sa.sbeg + sl);
-        int len = 0, rb = 0;
+        int len = 0, rb = 0, row = pos;
         if (live) {
-            len = __ldg(sa.len + row);
+            len = __ldg(sa.len + pos);
+            if (sa.perm) row = __ldg(sa.perm + pos);
             if constexpr (PAT) rb = s_beg[__ldg(sa.pid + row)];
         }
         double bv = 0.0, wv = 0.0;

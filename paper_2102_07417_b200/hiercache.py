@@ -141,7 +141,7 @@ def galerkin_product(a, p, symmetrize):
 
 
 def _save_csr(path, m):
-    np.savez(path, shape=np.asarray([m.nrows, m.ncols], dtype=np.int64),
+    np.savez_compressed(path, shape=np.asarray([m.nrows, m.ncols], dtype=np.int64),
              row_offsets=np.asarray(m.row_offsets, dtype=np.int64),
              col_indices=np.asarray(m.col_indices, dtype=np.int32),
              values=np.asarray(m.values, dtype=np.float64))

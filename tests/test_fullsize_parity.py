@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CACHE = os.path.join(ROOT, "hier_cache")
-CONFIGS = ["c1_poisson7_64", "c2_hetero27_128", "c4_rtanis7_256"]
+CONFIGS = ["c1_poisson7_64", "c2_hetero27_128", "c3_elasticity_64", "c4_rtanis7_256"]
 
 
 def _load(name):
@@ -77,7 +77,7 @@ def test_fullsize_pcg_matches_reference_solve(full):
 
     name, h, dh = full
     ref = h.meta.get("extra", {}).get("reference_solve")
-    b = problems.rhs_uniform(h.levels[0].a.nrows, 42)
+    b = problems.build_rhs(name, h.levels[0].a.nrows)
     res = amg.pcg(dh.A0, b, apply_m=dh.vcycle, config=amg.KrylovConfig(rtol=1e-8, record_history=True))
     assert res.converged and res.relres <= 1e-8
     true = np.linalg.norm(b - O.spmv(h.levels[0].a, res.x)) / np.linalg.norm(b)
