@@ -1411,8 +1411,10 @@ int amg_finalize(amg_t *h)
                 M.wt_grid = std::max(1, std::min((warps_needed + WT_WARPS - 1) / WT_WARPS, h->sm_count * nb));
                 h->max_grid = std::max(h->max_grid, M.wt_grid);
             }
+            // (rows averaging > 128 entries stay on the direct kernel: its lane groups share each
+            // row's pairwise leaves, where the padded kernels give a row to one thread)
             if (h->pad_min > 0 && M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm && !h->lanes_override &&
-                (double)M.nnz / (double)M.nrows >= (double)h->pad_min) {
+                (double)M.nnz / (double)M.nrows >= (double)h->pad_min && (double)M.nnz / (double)M.nrows <= 128.0) {
                 // padded-aligned copy: row starts == 3 (mod 4) so entry 1 is 16-byte aligned
                 std::vector<int32_t> col_h(M.nnz);
                 std::vector<double> val_h(M.nnz);

@@ -721,7 +721,8 @@ __global__ void __launch_bounds__(WS_THREADS) spmv_ws(const SpmvArgs a)
 // accumulators over the lanes, shuffle-butterfly combine, sequential tail,
 // p0 first).  No shared memory and no barriers, so occupancy is limited only
 // by registers -- latency is hidden by many independent row groups.
-// Rows with n = len - 1 > DIRECT_MAXN fall back to lane 0 (pairwise_sum).
+// Rows with n = len - 1 > DIRECT_MAXN follow numpy's recursive split, every
+// leaf summed by the whole lane group (direct_tree).
 constexpr int DIRECT_THREADS = 256;
 
 // matrix loads go through L1: with one lane per row a warp's 32 rows are
@@ -731,6 +732,128 @@ __device__ __forceinline__ double ldm(const double *p) { return __ldg(p); }
 __device__ __forceinline__ int ldm(const int32_t *p) { return __ldg(p); }
 constexpr int DIRECT_MAXN = 128;
 
+// One pairwise leaf (8 <= n <= 128 products starting at `base`) in numpy's
+// order -- 8 strided accumulators spread over the LANES lanes of a group,
+// butterfly combine, sequential tail -- with every load of the leaf issued
+// before the first add.  The result is valid (and identical) in all lanes.
+template <int LANES>
+__device__ __forceinline__ double direct_leaf(const double *__restrict__ val, const int32_t *__restrict__ col,
+                                              const double *__restrict__ x, int base, int n, int lane, unsigned gmask)
+{
+    constexpr int M = 8 / LANES;  // accumulators per lane: r_{lane + m*LANES}
+    const int main = n - (n % 8);
+    const int its = main / 8;
+    // tail (n % 8 entries): spread over the lanes, issued with the main loads
+    const int ntail = n - main;
+    constexpr int TT = (7 + LANES - 1) / LANES;  // tail entries per lane (tail <= 7)
+    double tpa[TT];
+#pragma unroll
+    for (int j = 0; j < TT; ++j) {
+        const int t = lane + j * LANES;
+        tpa[j] = (t < ntail) ? prod(ldm(val + base + main + t), __ldg(x + ldm(col + base + main + t))) : 0.0;
+    }
+    // main rounds in chunks of R = LANES rounds: 8 loads in flight per lane per chunk
+    constexpr int R = LANES;
+    double acc[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) acc[m] = 0.0;
+    for (int c0 = 0; c0 < its; c0 += R) {
+        double pv[R][M];
+        int pc[R][M];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int m = 0; m < M; ++m)
+                if (c0 + r < its) {
+                    const int k = base + (c0 + r) * 8 + lane + m * LANES;
+                    pv[r][m] = ldm(val + k);
+                    pc[r][m] = ldm(col + k);
+                }
+        double xg[R][M];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int m = 0; m < M; ++m)
+                if (c0 + r < its) xg[r][m] = __ldg(x + pc[r][m]);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int m = 0; m < M; ++m)
+                if (c0 + r < its) {
+                    const double pr = prod(pv[r][m], xg[r][m]);
+                    acc[m] = (c0 + r == 0) ? pr : add(acc[m], pr);
+                }
+    }
+    double res;
+    if constexpr (LANES == 1) {
+        res = add(add(add(acc[0], acc[1]), add(acc[2], acc[3])), add(add(acc[4], acc[5]), add(acc[6], acc[7])));
+    } else if constexpr (LANES == 2) {
+        double u[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) u[m] = add(acc[m], __shfl_xor_sync(gmask, acc[m], 1));
+        res = add(add(u[0], u[1]), add(u[2], u[3]));
+    } else if constexpr (LANES == 4) {
+        double s0 = add(acc[0], __shfl_xor_sync(gmask, acc[0], 1));
+        double s1 = add(acc[1], __shfl_xor_sync(gmask, acc[1], 1));
+        s0 = add(s0, __shfl_xor_sync(gmask, s0, 2));
+        s1 = add(s1, __shfl_xor_sync(gmask, s1, 2));
+        res = add(s0, s1);
+    } else {
+        double t = acc[0];
+        t = add(t, __shfl_xor_sync(gmask, t, 1));
+        t = add(t, __shfl_xor_sync(gmask, t, 2));
+        t = add(t, __shfl_xor_sync(gmask, t, 4));
+        res = t;
+    }
+    // sequential tail (entries main..n-1 held by lanes t % LANES), broadcast to every lane
+#pragma unroll
+    for (int t = 0; t < 7; ++t) {
+        const double v = (LANES == 1) ? tpa[t] : __shfl_sync(gmask, tpa[t / LANES], t % LANES, LANES);
+        if (t < ntail) res = add(res, v);
+    }
+    return res;
+}
+
+// numpy's pairwise sum for n > 128 (split at n/2 - (n/2) % 8, leaves of
+// 64..128 products) with the explicit-stack walk of pairwise_sum; the walk is
+// uniform over the lane group and every leaf is a direct_leaf of all lanes.
+template <int LANES>
+__device__ __noinline__ double direct_tree(const double *__restrict__ val, const int32_t *__restrict__ col,
+                                           const double *__restrict__ x, int base, int n, int lane, unsigned gmask)
+{
+    int fb[26], fn[26], fs[26];
+    double fl[26];
+    int sp = 0;
+    int b = base, m = n;
+    double ret;
+    for (;;) {
+        while (m > 128) {  // descend to the left child
+            fb[sp] = b;
+            fn[sp] = m;
+            fs[sp] = 0;
+            ++sp;
+            m = pairwise_split(m);
+        }
+        ret = direct_leaf<LANES>(val, col, x, b, m, lane, gmask);
+        bool descend = false;
+        while (sp > 0) {
+            const int t = sp - 1;
+            if (fs[t] == 0) {  // left done: evaluate the right child
+                fl[t] = ret;
+                fs[t] = 1;
+                const int n2 = pairwise_split(fn[t]);
+                b = fb[t] + n2;
+                m = fn[t] - n2;
+                descend = true;
+                break;
+            }
+            ret = add(fl[t], ret);
+            --sp;
+        }
+        if (!descend) return ret;
+    }
+}
+
 template <int EPI, int LANES>
 __global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_direct(const SpmvArgs a, int nrows)
 {
@@ -738,7 +861,6 @@ __global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_direct(const SpmvArgs 
     pdl_launch();
     pdl_wait();
     if (!gate_open(a.gate1, a.gate2)) return;
-    constexpr int M = 8 / LANES;        // accumulators per lane
     const int lane = threadIdx.x % LANES;
     const int grp_in_warp = (threadIdx.x & 31) / LANES;
     const unsigned gmask = (LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << (grp_in_warp * LANES));
@@ -801,87 +923,13 @@ __global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_direct(const SpmvArgs 
                 const double p0 = (LANES == 1) ? pe[0] : __shfl_sync(gmask, pe[0], 0, LANES);
                 sum = add(p0, res);
             }
-        } else if (n <= DIRECT_MAXN) {
-            const int base = lo + 1;
-            const int main = n - (n % 8);
-            const int its = main / 8;
-            // tail (n % 8 entries) and p0: spread over the lanes, issued with the main loads
-            const int ntail = n - main;
-            constexpr int TT = (7 + LANES - 1) / LANES;  // tail entries per lane (tail <= 7)
-            double tpa[TT];
-            double p0 = 0.0;
-#pragma unroll
-            for (int j = 0; j < TT; ++j) {
-                const int t = lane + j * LANES;
-                tpa[j] = (t < ntail) ? prod(ldm(val + base + main + t), __ldg(x + ldm(col + base + main + t))) : 0.0;
-            }
-            if (lane == 0) p0 = prod(ldm(val + lo), __ldg(x + ldm(col + lo)));
-            // main rounds in chunks of R = LANES rounds: 8 loads in flight per lane per chunk
-            constexpr int R = LANES;
-            double acc[M];
-#pragma unroll
-            for (int m = 0; m < M; ++m) acc[m] = 0.0;
-            for (int c0 = 0; c0 < its; c0 += R) {
-                double pv[R][M];
-                int pc[R][M];
-#pragma unroll
-                for (int r = 0; r < R; ++r)
-#pragma unroll
-                    for (int m = 0; m < M; ++m)
-                        if (c0 + r < its) {
-                            const int k = base + (c0 + r) * 8 + lane + m * LANES;
-                            pv[r][m] = ldm(val + k);
-                            pc[r][m] = ldm(col + k);
-                        }
-                double xg[R][M];
-#pragma unroll
-                for (int r = 0; r < R; ++r)
-#pragma unroll
-                    for (int m = 0; m < M; ++m)
-                        if (c0 + r < its) xg[r][m] = __ldg(x + pc[r][m]);
-#pragma unroll
-                for (int r = 0; r < R; ++r)
-#pragma unroll
-                    for (int m = 0; m < M; ++m)
-                        if (c0 + r < its) {
-                            const double pr = prod(pv[r][m], xg[r][m]);
-                            acc[m] = (c0 + r == 0) ? pr : add(acc[m], pr);
-                        }
-            }
-            double res;
-            if constexpr (LANES == 1) {
-                res = add(add(add(acc[0], acc[1]), add(acc[2], acc[3])), add(add(acc[4], acc[5]), add(acc[6], acc[7])));
-            } else if constexpr (LANES == 2) {
-                double u[4];
-#pragma unroll
-                for (int m = 0; m < 4; ++m) u[m] = add(acc[m], __shfl_xor_sync(gmask, acc[m], 1));
-                res = add(add(u[0], u[1]), add(u[2], u[3]));
-            } else if constexpr (LANES == 4) {
-                double s0 = add(acc[0], __shfl_xor_sync(gmask, acc[0], 1));
-                double s1 = add(acc[1], __shfl_xor_sync(gmask, acc[1], 1));
-                s0 = add(s0, __shfl_xor_sync(gmask, s0, 2));
-                s1 = add(s1, __shfl_xor_sync(gmask, s1, 2));
-                res = add(s0, s1);
-            } else {
-                double t = acc[0];
-                t = add(t, __shfl_xor_sync(gmask, t, 1));
-                t = add(t, __shfl_xor_sync(gmask, t, 2));
-                t = add(t, __shfl_xor_sync(gmask, t, 4));
-                res = t;
-            }
-            // sequential tail on lane 0 (entries main..n-1 held by lanes t % LANES)
-#pragma unroll
-            for (int t = 0; t < 7; ++t) {
-                const double v = (LANES == 1) ? tpa[t] : __shfl_sync(gmask, tpa[t / LANES], t % LANES, LANES);
-                if (t < ntail) res = add(res, v);
-            }
-            sum = add(p0, res);
         } else {
-            sum = 0.0;
-            if (lane == 0) {
-                auto P = [&](int k) -> double { return prod(ldm(val + k), __ldg(x + ldm(col + k))); };
-                sum = add(P(lo), pairwise_sum(P, lo + 1, n));
-            }
+            // p0 issued with the first leaf's loads; n > DIRECT_MAXN walks numpy's
+            // recursive split with every leaf summed by the whole lane group
+            const double p0 = (lane == 0) ? prod(ldm(val + lo), __ldg(x + ldm(col + lo))) : 0.0;
+            const double res = (n <= DIRECT_MAXN) ? direct_leaf<LANES>(val, col, x, lo + 1, n, lane, gmask)
+                                                  : direct_tree<LANES>(val, col, x, lo + 1, n, lane, gmask);
+            sum = add(p0, res);
         }
         if (lane == 0) {
             double yv;

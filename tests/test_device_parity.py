@@ -48,6 +48,26 @@ def test_spmv_ragged_rows_bit_identical(name, lanes):
     dh.close()
 
 
+@pytest.mark.parametrize("nrows,mean", [(700, 300), (20000, 200)])
+@pytest.mark.parametrize("lanes", [0, 1, 8])
+def test_spmv_long_rows_bit_identical(nrows, mean, lanes):
+    # rows of 0..~3*mean entries: numpy's recursive pairwise split (n > 128) on
+    # both the small-matrix and the large-matrix dispatch paths
+    from paper_2102_07417_b200.problems import Csr
+
+    rng = np.random.default_rng(nrows)
+    lens = rng.integers(0, 3 * mean, nrows)
+    lens[:5] = [0, 1, 129, 130, 2049]
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ncols = max(nrows, 4096)
+    cols = np.concatenate([np.sort(rng.choice(ncols, l, replace=False)) for l in lens]).astype(np.int32)
+    m = Csr(nrows, ncols, off, cols, rng.uniform(-1, 1, off[-1]))
+    x = rng.uniform(-1, 1, ncols)
+    dh = amg.DeviceHierarchy.from_matrices([m], options={"lanes": lanes})
+    np.testing.assert_array_equal(dh.matrix(0, "a")(x), O.spmv(m, x))
+    dh.close()
+
+
 @pytest.mark.parametrize("opts", [{"tile_nnz": 64, "tile_rows": 32, "stages": 1},
                                   {"tile_nnz": 300, "tile_rows": 64, "stages": 2},
                                   {"tile_nnz": 4096, "tile_rows": 512, "stages": 2}])

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--graph", type=int, default=0)
     ap.add_argument("--solves", type=int, default=1)
     ap.add_argument("--spmv-only", action="store_true")
+    ap.add_argument("--levels", action="store_true", help="time every level's SpMVs and the coarse solve")
     ap.add_argument("--opt", action="append", default=[])
     args = ap.parse_args()
     import numpy as np
@@ -38,7 +39,17 @@ def main():
         for slot in ("a", "g", "gt", "p", "pt"):
             print(slot, dh.time_spmv(0, slot, reps=5))
         return
-    b = problems.rhs_uniform(h.levels[0].a.nrows, 42)
+    if args.levels:
+        for k, lv in enumerate(h.levels):
+            slots = ("a", "g", "gt", "p", "pt") if lv.p is not None else ("a",)
+            def t(k, s):
+                try:
+                    return f"{1e3 * dh.time_spmv(k, s, reps=20):.1f}us"
+                except Exception as exc:  # levels folded into the tail kernel
+                    return f"n/a({type(exc).__name__})"
+            print(f"L{k} n={lv.a.nrows} nnz={lv.a.nnz} " + " ".join(f"{s}={t(k, s)}" for s in slots))
+        print(f"coarse {t(-1, 'a')}")
+    b = problems.build_rhs(args.config, h.levels[0].a.nrows)
     for _ in range(args.solves):
         t = time.perf_counter()
         r = amg.pcg(dh.A0, b, apply_m=dh.vcycle, config=amg.KrylovConfig(rtol=1e-8))
