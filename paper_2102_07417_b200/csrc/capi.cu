@@ -81,6 +81,10 @@ struct DevMat {
     int wt_grid = 0;
     int lanes = 1;
     int grid = 0;
+    int2 *leaf = nullptr;        // long-row leaves (spmv_leaves + spmv_leafsum), nullptr if unused
+    int32_t *row_leaf = nullptr;
+    double *lsum = nullptr;
+    int nleaves = 0, leaf_grid = 0, leafsum_grid = 0;
     HaloPlan halo;  // exchange feeding this matrix's halo columns (nranks > 1)
 };
 
@@ -143,6 +147,7 @@ struct amg_handle {
     int kernel = 2;      // 0: staged CTA tiles (spmv_tiles / spmv_ws), 2: direct register kernel, 3: warp tiles
     int wt_nnz = 256;    // warp-tile capacity (entries)
     int pad_min = 8;     // matrices averaging >= pad_min entries/row get the padded-aligned layout (0 = off)
+    int long_avg = 128;           // rows averaging more entries run leaf by leaf (spmv_leaves); 0 = off
     int small_rows_per_sm = 128;  // below sm_count * this many rows a matrix counts as small
     int patterns = 1;             // stencil-pattern layout for square operators with few row patterns
     int sell = 1;                 // SELL-32 slices where padding <= sell_pad %
@@ -267,6 +272,19 @@ static SpmvDirectFn spmv_direct_fn(int epi, int lanes)
     default: AMG_L(EPI_ADD)
     }
 #undef AMG_L
+}
+
+typedef void (*SpmvLeafsumFn)(const SpmvArgs, const LeafArgs, int);
+
+static SpmvLeafsumFn spmv_leafsum_fn(int epi)
+{
+    switch (epi) {
+    case EPI_PLAIN: return spmv_leafsum<EPI_PLAIN>;
+    case EPI_RESID: return spmv_leafsum<EPI_RESID>;
+    case EPI_AXPYW: return spmv_leafsum<EPI_AXPYW>;
+    case EPI_SETW: return spmv_leafsum<EPI_SETW>;
+    default: return spmv_leafsum<EPI_ADD>;
+    }
 }
 
 static SpmvFn spmv_ws_fn(int epi, int lanes)
@@ -503,6 +521,14 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         PatArgs pa{M.pstart, M.pval, M.pid, M.prel, M.pbeg, M.npat, M.nrel};
         TRY(launch_k(h, spmv_pat_fn(epi), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
                      pa, (int)M.nrows));
+    } else if (M.leaf) {
+        LeafArgs la{M.leaf, M.nleaves, M.lsum, M.row_leaf};
+        SpmvArgs a1 = a;  // leaf pass: no reduction
+        a1.dotw = nullptr;
+        a1.fin = FIN_NONE;
+        TRY(launch_k(h, spmv_leaves, grid_cap ? std::min(grid_cap, M.leaf_grid) : M.leaf_grid, DIRECT_THREADS, 0, a1, la));
+        TRY(launch_k(h, spmv_leafsum_fn(epi), grid_cap ? std::min(grid_cap, M.leafsum_grid) : M.leafsum_grid,
+                     DIRECT_THREADS, 0, a, la, (int)M.nrows));
     } else if (M.pstart) {
         PadArgs pa{M.pstart, M.pval, M.pcol};
         TRY(launch_k(h, spmv_vec_fn(epi), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
@@ -519,8 +545,8 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         int g = (int)std::min<int64_t>((M.nrows + gpr - 1) / gpr, (int64_t)h->sm_count * h->direct_per_sm);
         if (grid_cap) g = std::min(g, grid_cap);
         TRY(launch_k(h, spmv_direct_fn(epi, M.lanes), std::max(g, 1), DIRECT_THREADS, 0, a, (int)M.nrows));
-    } else if (h->ws) TRY(launch_k(h, spmv_ws_fn(epi, M.lanes), M.grid, WS_THREADS, (size_t)stage_smem(h), a));
-    else TRY(launch_k(h, spmv_fn(epi, M.lanes), M.grid, TILE_THREADS, (size_t)stage_smem(h), a));
+    } else if (h->ws) TRY(launch_k(h, spmv_ws_fn(epi, std::min(M.lanes, 8)), M.grid, WS_THREADS, (size_t)stage_smem(h), a));
+    else TRY(launch_k(h, spmv_fn(epi, std::min(M.lanes, 8)), M.grid, TILE_THREADS, (size_t)stage_smem(h), a));
     TRY(post_fin(h, ufin, g1));
     return AMG_OK;
 }
@@ -1006,7 +1032,7 @@ void amg_destroy(amg_t *h)
     auto F = [](void *p) { if (p) cudaFree(p); };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm);
+            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum);
             halo_free(M.halo);
         }
         F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
@@ -1041,6 +1067,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "ws") { h->ws = value ? 1 : 0; return AMG_OK; }
     if (k == "kernel") { h->kernel = (int)value; return AMG_OK; }
     if (k == "pad_min") { h->pad_min = (int)value; return AMG_OK; }
+    if (k == "long_avg") { h->long_avg = (int)value; return AMG_OK; }
     if (k == "small_rows_per_sm") { h->small_rows_per_sm = (int)value; return AMG_OK; }
     if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
     if (k == "sell") { h->sell = value ? 1 : 0; return AMG_OK; }
@@ -1401,7 +1428,7 @@ int amg_finalize(amg_t *h)
                 TRY(dalloc(&M.wtiles, wt.size()));
                 if (!wt.empty()) CK(cudaMemcpy(M.wtiles, wt.data(), wt.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
                 const double rows_per_tile = wt.empty() ? 1.0 : (double)M.nrows / (double)wt.size();
-                M.wt_lanes = h->lanes_override ? h->lanes_override
+                M.wt_lanes = h->lanes_override ? std::min(h->lanes_override, 8)
                              : rows_per_tile >= 24.0 ? 1 : rows_per_tile >= 12.0 ? 2 : rows_per_tile >= 6.0 ? 4 : 8;
                 const size_t smem = (size_t)WT_WARPS * 2 * stage_layout(cap, WT_ROWS).stage_bytes;
                 int nb = 0;
@@ -1411,10 +1438,48 @@ int amg_finalize(amg_t *h)
                 M.wt_grid = std::max(1, std::min((warps_needed + WT_WARPS - 1) / WT_WARPS, h->sm_count * nb));
                 h->max_grid = std::max(h->max_grid, M.wt_grid);
             }
-            // (rows averaging > 128 entries stay on the direct kernel: its lane groups share each
-            // row's pairwise leaves, where the padded kernels give a row to one thread)
-            if (h->pad_min > 0 && M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm && !h->lanes_override &&
-                (double)M.nnz / (double)M.nrows >= (double)h->pad_min && (double)M.nnz / (double)M.nrows <= 128.0) {
+            // rows averaging > long_avg entries: leaf list for spmv_leaves / spmv_leafsum
+            const bool longrows = h->long_avg > 0 && !h->lanes_override && M.nrows > 0 &&
+                                  (double)M.nnz / (double)M.nrows > (double)h->long_avg;
+            if (longrows) {
+                std::vector<int2> lv;
+                std::vector<int32_t> rl(M.nrows + 1);
+                int sb[32], sm[32];
+                for (int64_t r = 0; r < M.nrows; ++r) {
+                    rl[r] = (int32_t)lv.size();
+                    const int n = off32[r + 1] - off32[r] - 1;
+                    if (n < 8) continue;
+                    int sp = 1;
+                    sb[0] = off32[r] + 1;
+                    sm[0] = n;
+                    while (sp > 0) {  // in-order leaves: pre-order walk, pending right children stacked
+                        --sp;
+                        int b = sb[sp], m = sm[sp];
+                        while (m > 128) {
+                            const int n2 = m / 2 - (m / 2) % 8;
+                            sb[sp] = b + n2;
+                            sm[sp] = m - n2;
+                            ++sp;
+                            m = n2;
+                        }
+                        lv.push_back(make_int2(b, m));
+                    }
+                }
+                rl[M.nrows] = (int32_t)lv.size();
+                M.nleaves = (int)lv.size();
+                TRY(dalloc(&M.leaf, lv.size() + 1));
+                TRY(dalloc(&M.row_leaf, rl.size()));
+                TRY(dalloc(&M.lsum, lv.size() + 1));
+                if (!lv.empty()) CK(cudaMemcpy(M.leaf, lv.data(), lv.size() * sizeof(int2), cudaMemcpyHostToDevice));
+                CK(cudaMemcpy(M.row_leaf, rl.data(), rl.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                M.leaf_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nleaves + 31) / 32,
+                                                                         (int64_t)h->sm_count * h->direct_per_sm));
+                M.leafsum_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + DIRECT_THREADS - 1) / DIRECT_THREADS,
+                                                                            (int64_t)h->sm_count * 4));
+                h->max_grid = std::max(h->max_grid, std::max(M.leaf_grid, M.leafsum_grid));
+            }
+            if (!longrows && h->pad_min > 0 && M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm && !h->lanes_override &&
+                (double)M.nnz / (double)M.nrows >= (double)h->pad_min) {
                 // padded-aligned copy: row starts == 3 (mod 4) so entry 1 is 16-byte aligned
                 std::vector<int32_t> col_h(M.nnz);
                 std::vector<double> val_h(M.nnz);

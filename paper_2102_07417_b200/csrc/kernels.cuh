@@ -948,6 +948,113 @@ __global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_direct(const SpmvArgs 
     }
 }
 
+// ---------------------------------------------------------------- SpMV, long rows
+
+// Rows of several pairwise leaves (n > 128: coarse Galerkin operators of
+// elasticity / aggressive coarsening).  The leaves only depend on the row
+// lengths, so they are listed once at upload (numpy's split at
+// n/2 - (n/2) % 8, leaves of 64..128 products) and every SpMV runs in two
+// launches: spmv_leaves sums every leaf of the matrix side by side (8 lanes
+// per leaf, direct_leaf), spmv_leafsum forms each row as p0 + the leaf sums
+// folded in the tree's order, with the epilogue and the fused dot.  Rows with
+// 8 <= n <= 128 are a single leaf; rows with n < 8 are summed in spmv_leafsum.
+struct LeafArgs {
+    const int2 *leaf;         // (first product index, products) per leaf, rows in order
+    int nleaves;
+    double *lsum;             // leaf sums
+    const int32_t *row_leaf;  // first leaf of each row (nrows + 1)
+};
+
+// numpy's pairwise tree over a row's leaf sums (n = products after p0).
+__device__ __forceinline__ double leaf_tree_combine(const double *sl, int n)
+{
+    int fn[26], fs[26];
+    double fl[26];
+    int sp = 0, m = n, j = 0;
+    double ret;
+    for (;;) {
+        while (m > 128) {
+            fn[sp] = m;
+            fs[sp] = 0;
+            ++sp;
+            m = pairwise_split(m);
+        }
+        ret = sl[j++];
+        bool descend = false;
+        while (sp > 0) {
+            const int t = sp - 1;
+            if (fs[t] == 0) {
+                fl[t] = ret;
+                fs[t] = 1;
+                m = fn[t] - pairwise_split(fn[t]);
+                descend = true;
+                break;
+            }
+            ret = add(fl[t], ret);
+            --sp;
+        }
+        if (!descend) return ret;
+    }
+}
+
+__global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_leaves(const SpmvArgs a, const LeafArgs la)
+{
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const int lane = threadIdx.x % 8;
+    const unsigned tmask = 0xffu << ((threadIdx.x & 31) & ~7);
+    const int teams = gridDim.x * (DIRECT_THREADS / 8);
+    for (int v = blockIdx.x * (DIRECT_THREADS / 8) + threadIdx.x / 8; v < la.nleaves; v += teams) {
+        const int2 d = __ldg(la.leaf + v);
+        const double s = direct_leaf<8>(a.val, a.col, a.x, d.x, d.y, lane, tmask);
+        if (lane == 0) la.lsum[v] = s;
+    }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(DIRECT_THREADS) spmv_leafsum(const SpmvArgs a, const LeafArgs la, int nrows)
+{
+    __shared__ double red[DIRECT_THREADS / 32];
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    double dacc = 0.0;
+    for (int row = blockIdx.x * DIRECT_THREADS + threadIdx.x; row < nrows; row += gridDim.x * DIRECT_THREADS) {
+        const int lo = __ldg(a.off + row), hi = __ldg(a.off + row + 1);
+        const int n = hi - lo - 1;
+        double bv = 0.0, wv = 0.0;
+        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
+        if (want_dot && !self_dot) wv = a.dotw[row];
+        double sum = 0.0;
+        if (n >= 0) {
+            const double p0 = prod(ldm(a.val + lo), __ldg(a.x + ldm(a.col + lo)));
+            double res = 0.0;
+            if (n < 8) {
+                for (int t = 1; t <= n; ++t) res = add(res, prod(ldm(a.val + lo + t), __ldg(a.x + ldm(a.col + lo + t))));
+            } else {
+                const double *ls = la.lsum + __ldg(la.row_leaf + row);
+                res = (n <= 128) ? ls[0] : leaf_tree_combine(ls, n);
+            }
+            sum = add(p0, res);
+        }
+        double yv;
+        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+        else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+        else yv = sum;
+        a.y[row] = yv;
+        if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v = block_sum<DIRECT_THREADS>(dacc, red);
+        grid_finalize<DIRECT_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
 // ---------------------------------------------------------------- SpMV, warp tiles
 
 // Warp-tile SpMV: rows are cut into small tiles (<= wt_nnz entries, <= 32

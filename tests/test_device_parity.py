@@ -51,8 +51,8 @@ def test_spmv_ragged_rows_bit_identical(name, lanes):
 @pytest.mark.parametrize("nrows,mean", [(700, 300), (20000, 200)])
 @pytest.mark.parametrize("lanes", [0, 1, 8])
 def test_spmv_long_rows_bit_identical(nrows, mean, lanes):
-    # rows of 0..~3*mean entries: numpy's recursive pairwise split (n > 128) on
-    # both the small-matrix and the large-matrix dispatch paths
+    # rows of 0..~3*mean entries: numpy's recursive pairwise split (n > 128);
+    # lanes=0 takes the leaf-list kernels, the overrides the direct kernel's tree walk
     from paper_2102_07417_b200.problems import Csr
 
     rng = np.random.default_rng(nrows)
