@@ -81,6 +81,8 @@ struct DevMat {
     int wt_grid = 0;
     int lanes = 1;
     int grid = 0;
+    int32_t *sq_cta = nullptr;   // SELL streamed by bulk copies (spmv_sellq), nullptr if unused
+    int sq_grid = 0, sq_stage = 0, sq_stages = 0, sq_smem = 0;
     int2 *leaf = nullptr;        // long-row leaves (spmv_leaves + spmv_leafsum), nullptr if unused
     int32_t *row_leaf = nullptr;
     double *lsum = nullptr;
@@ -147,6 +149,8 @@ struct amg_handle {
     int kernel = 2;      // 0: staged CTA tiles (spmv_tiles / spmv_ws), 2: direct register kernel, 3: warp tiles
     int wt_nnz = 256;    // warp-tile capacity (entries)
     int pad_min = 8;     // matrices averaging >= pad_min entries/row get the padded-aligned layout (0 = off)
+    int sellq = 0;                // (measured slower than spmv_sell on B200: the ring leaves L1 too small for x)
+    int sell_pf = 0;              // spmv_sell: L2 bulk prefetch distance in grid strides (0 = off)                // SELL matrices with rows <= 33 entries streamed by bulk copies (spmv_sellq)
     int long_avg = 128;           // rows averaging more entries run leaf by leaf (spmv_leaves); 0 = off
     int small_rows_per_sm = 128;  // below sm_count * this many rows a matrix counts as small
     int patterns = 1;             // stencil-pattern layout for square operators with few row patterns
@@ -161,7 +165,7 @@ struct amg_handle {
     int lanes_override = 0;
     int pdl = 1;  // programmatic dependent launch between consecutive kernels
     // cluster tail: levels >= tail_level run inside one cluster kernel
-    int64_t tail_nnz = 100000;   // levels whose A_k has at most this many entries run in the cluster tail
+    int64_t tail_nnz = 300000;   // levels whose A_k has at most this many entries run in the cluster tail
     int tail_stage = 0;          // stage tail matrices in smem (measured slower on B200: the big smem
                                  // footprint delays the cluster launch; streamed from L2 by default)
     int cluster = 16;
@@ -217,6 +221,21 @@ typedef void (*SpmvSellFn)(const SpmvArgs, const SellArgs, int);
 static SpmvSellFn spmv_sell_fn(int epi, bool pat)
 {
 #define AMG_S(E) return pat ? spmv_sell<E, true> : spmv_sell<E, false>;
+    switch (epi) {
+    case EPI_PLAIN: AMG_S(EPI_PLAIN)
+    case EPI_RESID: AMG_S(EPI_RESID)
+    case EPI_AXPYW: AMG_S(EPI_AXPYW)
+    case EPI_SETW: AMG_S(EPI_SETW)
+    default: AMG_S(EPI_ADD)
+    }
+#undef AMG_S
+}
+
+typedef void (*SpmvSellqFn)(const SpmvArgs, const SellArgs, const SellqArgs, int);
+
+static SpmvSellqFn spmv_sellq_fn(int epi, bool pat)
+{
+#define AMG_S(E) return pat ? spmv_sellq<E, true> : spmv_sellq<E, false>;
     switch (epi) {
     case EPI_PLAIN: AMG_S(EPI_PLAIN)
     case EPI_RESID: AMG_S(EPI_RESID)
@@ -366,6 +385,10 @@ static int raise_smem_caps(int device)
             TRY(cap((const void *)spmv_ws_fn(e, l)));
             TRY(cap((const void *)spmv_wt_fn(e, l)));
         }
+    for (int e = 0; e <= 4; ++e) {
+        TRY(cap((const void *)spmv_sellq_fn(e, true)));
+        TRY(cap((const void *)spmv_sellq_fn(e, false)));
+    }
     TRY(cap((const void *)coarse_solve_k));
     TRY(cap((const void *)tail_vcycle));
     CK(cudaFuncSetAttribute((const void *)tail_vcycle, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -513,7 +536,13 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     a.ctl = h->ctl;
     a.gate1 = g1;
     a.gate2 = g2;
-    if (M.sbeg) {
+    if (M.sbeg && M.sq_cta && h->sellq) {
+        SellArgs sa{M.sbeg, M.sval, M.scol, M.slen, M.pid, M.prel, M.pbeg, M.npat, M.nrel, M.sperm};
+        SellqArgs q{M.sq_cta, M.sq_stage, M.sq_stages};
+        // grid fixed by the upload-time CTA ranges (one CTA per SM, never above a gated grid cap)
+        TRY(launch_k(h, spmv_sellq_fn(epi, M.scol == nullptr), M.sq_grid, SQ_THREADS, (size_t)M.sq_smem, a, sa, q,
+                     (int)M.nrows));
+    } else if (M.sbeg) {
         SellArgs sa{M.sbeg, M.sval, M.scol, M.slen, M.pid, M.prel, M.pbeg, M.npat, M.nrel, M.sperm};
         TRY(launch_k(h, spmv_sell_fn(epi, M.scol == nullptr), grid_cap ? std::min(grid_cap, M.sell_grid) : M.sell_grid,
                      VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
@@ -1032,7 +1061,7 @@ void amg_destroy(amg_t *h)
     auto F = [](void *p) { if (p) cudaFree(p); };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum);
+            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta);
             halo_free(M.halo);
         }
         F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
@@ -1067,6 +1096,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "ws") { h->ws = value ? 1 : 0; return AMG_OK; }
     if (k == "kernel") { h->kernel = (int)value; return AMG_OK; }
     if (k == "pad_min") { h->pad_min = (int)value; return AMG_OK; }
+    if (k == "sellq") { h->sellq = (int)value; return AMG_OK; }
     if (k == "long_avg") { h->long_avg = (int)value; return AMG_OK; }
     if (k == "small_rows_per_sm") { h->small_rows_per_sm = (int)value; return AMG_OK; }
     if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
@@ -1613,6 +1643,37 @@ int amg_finalize(amg_t *h)
                         if (!pat) {
                             TRY(dalloc(&M.scol, sc.size()));
                             CK(cudaMemcpy(M.scol, sc.data(), sc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                        }
+                        if (h->sellq && maxlen <= SQ_MAXLEN && !sorted) {
+                            // bulk-copy streamed variant: chunk c = slices [8c, 8c + 8); ring stages sized for
+                            // the largest chunk, as many as fit (2..4); chunk ranges per CTA balanced by entries
+                            const int bpe = pat ? 8 : 12;
+                            const int rel_bytes = pat ? (((M.nrel + 3) & ~3) + M.npat + 1) * 4 : 0;
+                            cudaFuncAttributes fa;
+                            CK(cudaFuncGetAttributes(&fa, (const void *)spmv_sellq_fn(EPI_RESID, pat)));
+                            int optin = 0;
+                            CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+                            const int avail = optin - (int)fa.sharedSizeBytes - rel_bytes - 256;
+                            const int64_t nch = (ns + SQ_WARPS - 1) / SQ_WARPS;
+                            int64_t se = 0;
+                            for (int64_t c = 0; c < nch; ++c)
+                                se = std::max<int64_t>(se, sb[std::min<int64_t>(ns, (c + 1) * SQ_WARPS)] - sb[c * SQ_WARPS]);
+                            const int S = (int)std::min<int64_t>(SQ_MAXSTAGES, avail / std::max<int64_t>(1, se * bpe));
+                            if (S >= 2 && nch > 0) {
+                                const int G = (int)std::max<int64_t>(1, std::min<int64_t>(h->sm_count, nch));
+                                std::vector<int32_t> ct(G + 1, (int32_t)nch);
+                                ct[0] = 0;
+                                int b = 1;
+                                for (int64_t c = 0; c < nch && b < G; ++c)  // CTA b starts past b/G of the entries
+                                    while (b < G && (int64_t)sb[std::min<int64_t>(ns, (c + 1) * SQ_WARPS)] * G >= (int64_t)tot * b)
+                                        ct[b++] = (int32_t)(c + 1);
+                                TRY(dalloc(&M.sq_cta, ct.size()));
+                                CK(cudaMemcpy(M.sq_cta, ct.data(), ct.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                                M.sq_grid = G;
+                                M.sq_stage = (int)se;
+                                M.sq_stages = S;
+                                M.sq_smem = S * (int)se * bpe + rel_bytes;
+                            }
                         }
                         int nbs = 0;
                         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbs, (const void *)spmv_sell_fn(EPI_RESID, pat), VEC_SPMV_THREADS, 0));

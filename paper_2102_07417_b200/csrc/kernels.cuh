@@ -1556,6 +1556,205 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, PAT ? 5 : 4) spmv_sell(const
     }
 }
 
+// ---------------------------------------------------------------- SpMV, SELL-32 streamed by the bulk-copy engine
+
+// The SELL-32 layout's value (and column) arrays are one contiguous stream, so
+// a persistent CTA (one per SM) can move its share with cp.async.bulk instead
+// of per-lane loads: a producer thread copies chunks of SQ_WARPS consecutive
+// slices (chunk c = slices [c*SQ_WARPS, (c+1)*SQ_WARPS)) into a q.stages-deep
+// shared-memory ring (full / empty mbarriers); consumer warp w sums the rows
+// of slice c*SQ_WARPS + w from shared memory in exactly the spmv_sell order.
+// The matrix stream needs no registers in flight, so each lane issues every x
+// gather of its row (<= SQ_MAXLEN entries) at once; the per-slice metadata
+// (slice offsets, row lengths, pattern ids, b) is fetched one chunk ahead.
+// Chunks are static data: the first stages are copied before
+// griddepcontrol.wait, overlapping the previous kernel.  CTA b owns chunks
+// [q.cta[b], q.cta[b+1]) (entries balanced at upload).
+constexpr int SQ_WARPS = 8;
+constexpr int SQ_THREADS = (SQ_WARPS + 1) * 32;  // + one producer warp
+constexpr int SQ_MAXSTAGES = 4;
+constexpr int SQ_MAXLEN = 33;                     // rows of <= 33 entries: p0 + 4 full rounds
+
+struct SellqArgs {
+    const int32_t *cta;       // CTA b = chunks [cta[b], cta[b+1])
+    int stage_entries;        // ring stage capacity (entries) >= the largest chunk
+    int stages;               // ring depth (<= SQ_MAXSTAGES)
+};
+
+template <int EPI, bool PAT>
+__global__ void __launch_bounds__(SQ_THREADS, 1) spmv_sellq(const SpmvArgs a, const SellArgs sa, const SellqArgs q,
+                                                             int nrows)
+{
+    extern __shared__ __align__(128) unsigned char sq_smem[];
+    __shared__ double red[SQ_THREADS / 32];
+    __shared__ __align__(8) uint64_t full[SQ_MAXSTAGES], empty[SQ_MAXSTAGES];
+    // dynamic smem: [stages: values (8 B/entry) | columns (4 B/entry, !PAT)] [pattern table]
+    constexpr int bpe = PAT ? 8 : 12;
+    const int S = q.stages;
+    auto stage = [&](int st) { return sq_smem + (size_t)st * q.stage_entries * bpe; };
+    int32_t *s_rel = reinterpret_cast<int32_t *>(sq_smem + (size_t)S * q.stage_entries * bpe);
+    int32_t *s_beg = s_rel + (PAT ? ((sa.nrel + 3) & ~3) : 0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c0 = __ldg(q.cta + blockIdx.x), c1 = __ldg(q.cta + blockIdx.x + 1);
+    const int nch = c1 - c0;
+    const int nslices = (nrows + 31) >> 5;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < S; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], SQ_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if constexpr (PAT) {
+        for (int i = threadIdx.x; i < sa.nrel; i += SQ_THREADS) s_rel[i] = sa.rel[i];
+        for (int i = threadIdx.x; i <= sa.npat; i += SQ_THREADS) s_beg[i] = sa.pbeg[i];
+    }
+    __syncthreads();
+    const bool producer = warp == SQ_WARPS && lane == 0;
+    auto chunk_range = [&](int c, int &e0, int &nb) {
+        const int f = c * SQ_WARPS, e = min(f + SQ_WARPS, nslices);
+        e0 = __ldg(sa.sbeg + f);
+        nb = __ldg(sa.sbeg + e) - e0;
+    };
+    auto issue = [&](int i, int e0, int nb) {  // chunk c0 + i -> stage i % S
+        const int st = i % S;
+        unsigned char *sp = stage(st);
+        mbar_arrive_tx(&full[st], (unsigned)nb * (unsigned)bpe);
+        bulk_g2s(sp, sa.sval + e0, (unsigned)nb * 8u, &full[st]);
+        if constexpr (!PAT) bulk_g2s(sp + (size_t)nb * 8, sa.scol + e0, (unsigned)nb * 4u, &full[st]);
+    };
+    const int pre = nch < S ? nch : S;
+    if (producer)  // the matrix is static: stage ahead of the dependency wait
+        for (int i = 0; i < pre; ++i) {
+            int e0, nb;
+            chunk_range(c0 + i, e0, nb);
+            issue(i, e0, nb);
+        }
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) {
+        if (producer)
+            for (int i = 0; i < pre; ++i) mbar_wait(&full[i], 0u);  // no copy may outlive the CTA
+        return;
+    }
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    const double *__restrict__ x = a.x;
+    double dacc = 0.0;
+    if (warp == SQ_WARPS) {
+        if (producer && nch > S) {
+            int e0, nb;
+            chunk_range(c0 + S, e0, nb);
+            for (int i = S; i < nch; ++i) {
+                int ne0 = 0, nnb = 0;
+                if (i + 1 < nch) chunk_range(c0 + i + 1, ne0, nnb);  // next descriptor in flight
+                mbar_wait(&empty[i % S], (unsigned)(((i / S) - 1) & 1));
+                issue(i, e0, nb);
+                e0 = ne0;
+                nb = nnb;
+            }
+        }
+    } else {
+        // per-slice metadata of chunk i, fetched one chunk ahead
+        int m_eoff = 0, m_nent = 0, m_len = 0, m_rb = 0;
+        double m_bv = 0.0, m_wv = 0.0;
+        auto meta = [&](int c, int &eoff, int &nent, int &len, int &pidv, double &bv, double &wv) {
+            const int f = c * SQ_WARPS, e = min(f + SQ_WARPS, nslices);
+            const int sl = f + warp;
+            const int pos = sl * 32 + lane;
+            const int fb = __ldg(sa.sbeg + f);
+            nent = __ldg(sa.sbeg + e) - fb;
+            eoff = (sl < e) ? __ldg(sa.sbeg + sl) - fb : 0;
+            len = 0;
+            pidv = 0;
+            bv = 0.0;
+            wv = 0.0;
+            if (sl < e && pos < nrows) {
+                len = __ldg(sa.len + pos);
+                if constexpr (PAT) pidv = __ldg(sa.pid + pos);
+                if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[pos];
+                if (want_dot && !self_dot) wv = a.dotw[pos];
+            }
+        };
+        if (nch > 0) meta(c0, m_eoff, m_nent, m_len, m_rb, m_bv, m_wv);
+        for (int i = 0; i < nch; ++i) {
+            const int st = i % S;
+            const int sl = (c0 + i) * SQ_WARPS + warp;
+            const int pos = sl * 32 + lane;
+            const int eoff = m_eoff, nent = m_nent, len = m_len;
+            const double bv = m_bv, wv = m_wv;
+            const int rb = PAT ? s_beg[m_rb] : 0;
+            if (i + 1 < nch) meta(c0 + i + 1, m_eoff, m_nent, m_len, m_rb, m_bv, m_wv);
+            mbar_wait(&full[st], (unsigned)((i / S) & 1));
+            if (sl < nslices) {
+                const bool live = pos < nrows;
+                const int row = pos;
+                const double *vb = reinterpret_cast<const double *>(stage(st)) + eoff + lane;
+                const int32_t *cb = PAT ? nullptr
+                                        : reinterpret_cast<const int32_t *>(stage(st) + (size_t)nent * 8) + eoff + lane;
+                // every gather of the row in flight at once
+                double pk[SQ_MAXLEN];
+#pragma unroll
+                for (int k = 0; k < SQ_MAXLEN; ++k) {
+                    if (k < len) {
+                        const int c = PAT ? row + s_rel[rb + k] : cb[32 * k];
+                        pk[k] = __ldg(x + c);
+                    } else {
+                        pk[k] = 0.0;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < SQ_MAXLEN; ++k)
+                    if (k < len) pk[k] = prod(vb[32 * k], pk[k]);
+                const int n = len - 1;
+                double sum = 0.0;
+                if (n >= 0) {
+                    double res;
+                    if (n < 8) {
+                        res = 0.0;
+#pragma unroll
+                        for (int t = 1; t < 8; ++t)
+                            if (t <= n) res = add(res, pk[t]);
+                    } else {
+                        const int main = n - (n % 8);
+                        double acc[8];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) acc[t] = pk[1 + t];
+#pragma unroll
+                        for (int i8 = 8; i8 < 32; i8 += 8)
+                            if (i8 < main) {
+#pragma unroll
+                                for (int t = 0; t < 8; ++t) acc[t] = add(acc[t], pk[1 + i8 + t]);
+                            }
+                        res = add(add(add(acc[0], acc[1]), add(acc[2], acc[3])),
+                                  add(add(acc[4], acc[5]), add(acc[6], acc[7])));
+#pragma unroll
+                        for (int k = 9; k < SQ_MAXLEN; ++k)  // tail: entries main+1 .. n
+                            if (k > main && k <= n) res = add(res, pk[k]);
+                    }
+                    sum = add(pk[0], res);
+                }
+                if (live) {
+                    double yv;
+                    if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+                    else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+                    else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+                    else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+                    else yv = sum;
+                    a.y[row] = yv;
+                    if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+        }
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v = block_sum<SQ_THREADS>(dacc, red);
+        grid_finalize<SQ_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
 // ---------------------------------------------------------------- vectors
 
 constexpr int VEC_THREADS = 256;

@@ -68,6 +68,29 @@ def test_spmv_long_rows_bit_identical(nrows, mean, lanes):
     dh.close()
 
 
+@pytest.mark.parametrize("sellq", [0, 1])
+@pytest.mark.parametrize("kind", ["stencil", "uniform", "uniform_wide"])
+def test_spmv_sell_layouts_bit_identical(kind, sellq):
+    # SELL-32 (stencil-pattern columns or stored columns), per-lane loads or
+    # bulk-copy streamed (spmv_sellq), on matrices large enough for the layout
+    from paper_2102_07417_b200.problems import Csr, poisson7
+
+    rng = np.random.default_rng(3)
+    if kind == "stencil":
+        m = poisson7(40, 40, 24)
+    else:
+        n = 40000
+        lo, hi = (20, 23) if kind == "uniform" else (30, 34)
+        lens = rng.integers(lo, hi, n)
+        off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        cols = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+        m = Csr(n, n, off, cols, rng.uniform(-1, 1, off[-1]))
+    x = rng.uniform(-1, 1, m.ncols)
+    dh = amg.DeviceHierarchy.from_matrices([m], options={"sellq": sellq})
+    np.testing.assert_array_equal(dh.matrix(0, "a")(x), O.spmv(m, x))
+    dh.close()
+
+
 @pytest.mark.parametrize("opts", [{"tile_nnz": 64, "tile_rows": 32, "stages": 1},
                                   {"tile_nnz": 300, "tile_rows": 64, "stages": 2},
                                   {"tile_nnz": 4096, "tile_rows": 512, "stages": 2}])
