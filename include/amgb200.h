@@ -152,6 +152,19 @@ int amg_get_stats(amg_t *h, amg_stats_t *out);
  * back on the handle's stream between CUDA events (operands resident in
  * HBM); *ms_per_launch = average device time of one launch. */
 int amg_time_spmv(amg_t *h, int level, int which, int reps, double *ms_per_launch);
+/* Diagnostics: the device layout the SpMV of matrix `which` of `level` runs on
+ * (chosen at amg_finalize; every layout gives bit-identical rows). */
+enum {
+    AMG_LAYOUT_CSR = 0,       /* CSR, register / tile kernels */
+    AMG_LAYOUT_PADDED = 1,    /* padded-aligned CSR (vector loads) */
+    AMG_LAYOUT_PATTERN = 2,   /* padded values + stencil-pattern columns */
+    AMG_LAYOUT_SELL = 3,      /* SELL-32 slices, stored columns */
+    AMG_LAYOUT_SELL_PAT = 4,  /* SELL-32 slices, stencil-pattern columns */
+    AMG_LAYOUT_SYMD = 5,      /* symmetric stencil: upper diagonals + pattern ids */
+    AMG_LAYOUT_LEAVES = 6,    /* long rows, leaf list */
+    AMG_LAYOUT_EMPTY = 7
+};
+int amg_matrix_layout(amg_t *h, int level, int which, int *layout);
 /* Tuning / diagnostics: 0 = auto. */
 int amg_set_option(amg_t *h, const char *key, int64_t value);
 

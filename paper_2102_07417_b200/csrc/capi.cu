@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <memory>
+#include <mutex>
 #include <unordered_map>
 #include <chrono>
 #include <cmath>
@@ -70,6 +72,9 @@ struct DevMat {
     int32_t *prel = nullptr;     // concatenated relative offsets
     int32_t *pbeg = nullptr;     // pattern starts into prel
     int npat = 0, nrel = 0;
+    double *uval = nullptr;      // symmetric stencil layout (spmv_symd), nullptr if unused
+    int sym_slot = -1;           // its __constant__ pattern-table slot
+    int nudiag = 0, sym_grid = 0, sym_fl = 0, symf_grid = 0;  // sym_fl: fixed-slot kernel width (0: none)
     int32_t *pstart = nullptr;   // padded-aligned layout (spmv_vec), nullptr if unused
     double *pval = nullptr;
     int32_t *pcol = nullptr;
@@ -117,6 +122,30 @@ int dalloc(T **p, size_t count)
 
 }  // namespace
 
+// __constant__ pattern-table slots (kernels.cuh c_symd_*), per device, process-wide:
+// handles on one device share the module's constant bank.
+static std::mutex g_symd_mu;
+static std::unordered_map<int, unsigned> g_symd_used;  // device -> slot bitmask
+
+static int symd_slot_take(int device)
+{
+    std::lock_guard<std::mutex> g(g_symd_mu);
+    unsigned &m = g_symd_used[device];
+    for (int i = 0; i < SYMD_SLOTS; ++i)
+        if (!(m & (1u << i))) {
+            m |= 1u << i;
+            return i;
+        }
+    return -1;
+}
+
+static void symd_slot_give(int device, int slot)
+{
+    if (slot < 0) return;
+    std::lock_guard<std::mutex> g(g_symd_mu);
+    g_symd_used[device] &= ~(1u << slot);
+}
+
 struct amg_handle {
     int device = 0, rank = 0, nranks = 1;
     cudaStream_t stream = nullptr;
@@ -154,6 +183,11 @@ struct amg_handle {
     int long_avg = 128;           // rows averaging more entries run leaf by leaf (spmv_leaves); 0 = off
     int small_rows_per_sm = 128;  // below sm_count * this many rows a matrix counts as small
     int patterns = 1;             // stencil-pattern layout for square operators with few row patterns
+    int symd_minb = 4;            // fixed-slot 32-wide kernel: min CTAs/SM (register budget) 3, 4 or 5
+    int symd_chunked = 0;         // symmetric kernels: contiguous row chunk per CTA (measured slower than grid-stride)
+    int symd_fixed = 1;           // fixed-slot symmetric kernel: 1 rows <= 8 entries (7-point), 2 also <= 32 (27-point:
+                                  // measured slower than the round-by-round kernel on config 2), 0 off
+    int symm = 1;                 // symmetric stencil layout (upper diagonals) for bitwise-symmetric pattern operators
     int sell = 1;                 // SELL-32 slices where padding <= sell_pad %
     int gated_grid = 1;           // CTAs per SM for the rarely active gated residual SpMVs (0 = full grid)
     int grid_per_sm = 0;          // cap on SpMV CTAs per SM (0 = occupancy)
@@ -229,6 +263,35 @@ static SpmvSellFn spmv_sell_fn(int epi, bool pat)
     default: AMG_S(EPI_ADD)
     }
 #undef AMG_S
+}
+
+typedef void (*SpmvSymFn)(const SpmvArgs, const SymArgs, int);
+
+static SpmvSymFn spmv_symd_fn(int epi)
+{
+    switch (epi) {
+    case EPI_PLAIN: return spmv_symd<EPI_PLAIN>;
+    case EPI_RESID: return spmv_symd<EPI_RESID>;
+    case EPI_AXPYW: return spmv_symd<EPI_AXPYW>;
+    case EPI_SETW: return spmv_symd<EPI_SETW>;
+    default: return spmv_symd<EPI_ADD>;
+    }
+}
+
+static SpmvSymFn spmv_symd_fixed_fn(int epi, int fl, int minb = 0)
+{
+#define AMG_F(E)                                                                          \
+    return fl <= 8 ? spmv_symd_fixed<E, 8, 6>                                               \
+                   : (minb == 3 ? spmv_symd_fixed<E, 32, 3>                                \
+                                : minb == 5 ? spmv_symd_fixed<E, 32, 5> : spmv_symd_fixed<E, 32, 4>);
+    switch (epi) {
+    case EPI_PLAIN: AMG_F(EPI_PLAIN)
+    case EPI_RESID: AMG_F(EPI_RESID)
+    case EPI_AXPYW: AMG_F(EPI_AXPYW)
+    case EPI_SETW: AMG_F(EPI_SETW)
+    default: AMG_F(EPI_ADD)
+    }
+#undef AMG_F
 }
 
 typedef void (*SpmvSellqFn)(const SpmvArgs, const SellArgs, const SellqArgs, int);
@@ -536,7 +599,25 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     a.ctl = h->ctl;
     a.gate1 = g1;
     a.gate2 = g2;
-    if (M.sbeg && M.sq_cta && h->sellq) {
+    if (M.uval && h->symm) {
+        const bool fx = M.sym_fl && (h->symd_fixed >= 2 || (h->symd_fixed == 1 && M.sym_fl <= 8));
+        int g = fx ? M.symf_grid : M.sym_grid;
+        if (grid_cap) g = std::min(g, grid_cap);
+        // contiguous row chunks per CTA (multiples of 256 rows) when the grid covers the matrix in >= 2 steps
+        int chunk = 0;
+        if (h->symd_chunked) {
+            const int64_t c = ((M.nrows + g - 1) / g + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS * VEC_SPMV_THREADS;
+            if (c >= 2 * VEC_SPMV_THREADS) {
+                chunk = (int)c;
+                g = (int)((M.nrows + c - 1) / c);
+            }
+        }
+        SymArgs sa{M.uval, M.pid, M.sym_slot, chunk};
+        if (fx)
+            TRY(launch_k(h, spmv_symd_fixed_fn(epi, M.sym_fl, h->symd_minb), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
+        else
+            TRY(launch_k(h, spmv_symd_fn(epi), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
+    } else if (M.sbeg && M.sq_cta && h->sellq) {
         SellArgs sa{M.sbeg, M.sval, M.scol, M.slen, M.pid, M.prel, M.pbeg, M.npat, M.nrel, M.sperm};
         SellqArgs q{M.sq_cta, M.sq_stage, M.sq_stages};
         // grid fixed by the upload-time CTA ranges (one CTA per SM, never above a gated grid cap)
@@ -546,7 +627,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         SellArgs sa{M.sbeg, M.sval, M.scol, M.slen, M.pid, M.prel, M.pbeg, M.npat, M.nrel, M.sperm};
         TRY(launch_k(h, spmv_sell_fn(epi, M.scol == nullptr), grid_cap ? std::min(grid_cap, M.sell_grid) : M.sell_grid,
                      VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
-    } else if (M.pid) {
+    } else if (M.pid && M.pstart) {
         PatArgs pa{M.pstart, M.pval, M.pid, M.prel, M.pbeg, M.npat, M.nrel};
         TRY(launch_k(h, spmv_pat_fn(epi), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
                      pa, (int)M.nrows));
@@ -1061,7 +1142,9 @@ void amg_destroy(amg_t *h)
     auto F = [](void *p) { if (p) cudaFree(p); };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta);
+            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta); F(M.uval);
+            symd_slot_give(h->device, M.sym_slot);
+            M.sym_slot = -1;
             halo_free(M.halo);
         }
         F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
@@ -1100,6 +1183,10 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "long_avg") { h->long_avg = (int)value; return AMG_OK; }
     if (k == "small_rows_per_sm") { h->small_rows_per_sm = (int)value; return AMG_OK; }
     if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
+    if (k == "symm") { h->symm = value ? 1 : 0; return AMG_OK; }
+    if (k == "symd_fixed") { h->symd_fixed = (int)value; return AMG_OK; }
+    if (k == "symd_chunked") { h->symd_chunked = value ? 1 : 0; return AMG_OK; }
+    if (k == "symd_minb") { h->symd_minb = (int)value; return AMG_OK; }
     if (k == "sell") { h->sell = value ? 1 : 0; return AMG_OK; }
     if (k == "grid_per_sm") { h->grid_per_sm = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "vec_per_sm") { h->vec_per_sm = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
@@ -1358,6 +1445,113 @@ int amg_set_cycle(amg_t *h, int nu1, int nu2)
     return AMG_OK;
 }
 
+// Stencil patterns: every row's (col - row) tuple from a dictionary of at most
+// PAT_MAX patterns (PAT_MAX_REL offsets in total, rows <= 129 entries).
+static bool pattern_dict(const DevMat &M, const std::vector<int32_t> &off32, const std::vector<int32_t> &col_h,
+                         std::vector<uint8_t> &ids, std::vector<int32_t> &rel, std::vector<int32_t> &beg)
+{
+    std::unordered_map<std::string, int> dict;
+    ids.assign(M.nrows, 0);
+    rel.clear();
+    beg.assign(1, 0);
+    std::string key;
+    for (int64_t r = 0; r < M.nrows; ++r) {
+        const int32_t lo = off32[r], hi = off32[r + 1];
+        key.resize((size_t)(hi - lo) * 4);
+        for (int32_t k = lo; k < hi; ++k) {
+            const int32_t d = col_h[k] - (int32_t)r;
+            memcpy(&key[(size_t)(k - lo) * 4], &d, 4);
+        }
+        auto it = dict.find(key);
+        int id;
+        if (it == dict.end()) {
+            id = (int)dict.size();
+            if (id >= PAT_MAX || (int)rel.size() + (hi - lo) > PAT_MAX_REL || hi - lo > 129) return false;
+            dict.emplace(key, id);
+            for (int32_t k = lo; k < hi; ++k) rel.push_back(col_h[k] - (int32_t)r);
+            beg.push_back((int32_t)rel.size());
+        } else {
+            id = it->second;
+        }
+        ids[r] = (uint8_t)id;
+    }
+    return !dict.empty();
+}
+
+// Symmetric stencil layout (spmv_symd): taken when the operator is square, its
+// pattern dictionary exists, its relative offsets are closed under negation,
+// every below-diagonal entry equals its mirror BIT FOR BIT, and storing the
+// nu >= 0 diagonals densely costs at most 3/4 of the full value stream.
+static int build_symd(amg_t *h, DevMat &M, const std::vector<int32_t> &off32, const std::vector<int32_t> &col_h,
+                      const std::vector<double> &val_h, const std::vector<uint8_t> &ids,
+                      const std::vector<int32_t> &rel, const std::vector<int32_t> &beg)
+{
+    std::vector<int32_t> dist(rel.begin(), rel.end());
+    std::sort(dist.begin(), dist.end());
+    dist.erase(std::unique(dist.begin(), dist.end()), dist.end());
+    std::vector<int32_t> up;  // stored diagonals d >= 0, ascending
+    for (int32_t d : dist) {
+        if (!std::binary_search(dist.begin(), dist.end(), -d)) return AMG_OK;  // not structurally symmetric
+        if (d >= 0) up.push_back(d);
+    }
+    if (rel.size() > (size_t)SYMD_ENT_MAX || beg.size() > (size_t)SYMD_BEG_MAX) return AMG_OK;  // constant table
+    const int64_t n = M.nrows;
+    const int nu = (int)up.size();
+    if (nu == 0 || (double)nu * (double)n > 0.75 * (double)M.nnz) return AMG_OK;
+    const int64_t npad = ((n + 31) / 32) * 32;
+    if ((int64_t)nu * npad + npad >= INT32_MAX - 64) return AMG_OK;
+    auto jof = [&](int32_t d) { return (int)(std::lower_bound(up.begin(), up.end(), d) - up.begin()); };
+    std::vector<double> uv((size_t)nu * npad, 0.0);
+    std::vector<uint8_t> have((size_t)nu * npad, 0);
+    for (int64_t r = 0; r < n; ++r)  // upper entries (and the diagonal) first
+        for (int32_t k = off32[r]; k < off32[r + 1]; ++k) {
+            const int32_t d = col_h[k] - (int32_t)r;
+            if (d < 0) continue;
+            const size_t q = (size_t)jof(d) * npad + r;
+            uv[q] = val_h[k];
+            have[q] = 1;
+        }
+    for (int64_t r = 0; r < n; ++r)  // every lower entry must be its mirror, bitwise
+        for (int32_t k = off32[r]; k < off32[r + 1]; ++k) {
+            const int32_t d = col_h[k] - (int32_t)r;
+            if (d >= 0) continue;
+            const size_t q = (size_t)jof(-d) * npad + (r + d);
+            if (!have[q] || memcmp(&uv[q], &val_h[k], sizeof(double)) != 0) return AMG_OK;
+        }
+    const int slot = symd_slot_take(h->device);
+    if (slot < 0) return AMG_OK;  // every table slot of this device in use: keep the other layouts
+    std::vector<int2> ent(SYMD_ENT_MAX, make_int2(0, 0));
+    std::vector<int32_t> bg(SYMD_BEG_MAX, 0);
+    for (size_t i = 0; i < rel.size(); ++i) {
+        const int32_t d = rel[i];
+        ent[i] = d >= 0 ? make_int2(d, (int)((int64_t)jof(d) * npad)) : make_int2(d, (int)((int64_t)jof(-d) * npad + d));
+    }
+    for (size_t i = 0; i < beg.size(); ++i) bg[i] = slot * SYMD_ENT_MAX + beg[i];
+    CK(cudaMemcpyToSymbol(c_symd_ent, ent.data(), ent.size() * sizeof(int2), (size_t)slot * SYMD_ENT_MAX * sizeof(int2)));
+    CK(cudaMemcpyToSymbol(c_symd_beg, bg.data(), bg.size() * sizeof(int32_t), (size_t)slot * SYMD_BEG_MAX * sizeof(int32_t)));
+    M.sym_slot = slot;
+    TRY(dalloc(&M.uval, uv.size()));
+    CK(cudaMemcpy(M.uval, uv.data(), uv.size() * sizeof(double), cudaMemcpyHostToDevice));
+    M.nudiag = nu;
+    int nb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_symd_fn(EPI_RESID), VEC_SPMV_THREADS, 0));
+    M.sym_grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
+                                                             (int64_t)h->sm_count * std::max(nb, 1)));
+    h->max_grid = std::max(h->max_grid, M.sym_grid);
+    int maxlen = 0;
+    for (size_t i = 0; i + 1 < beg.size(); ++i) maxlen = std::max(maxlen, beg[i + 1] - beg[i]);
+    M.sym_fl = maxlen <= 8 ? 8 : maxlen <= 32 ? 32 : 0;
+    if (M.sym_fl) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_symd_fixed_fn(EPI_RESID, M.sym_fl, h->symd_minb),
+                                                         VEC_SPMV_THREADS, 0));
+        M.symf_grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
+                                                                  (int64_t)h->sm_count * std::max(nb, 1)));
+        h->max_grid = std::max(h->max_grid, M.symf_grid);
+    }
+    (void)ids;
+    return AMG_OK;
+}
+
 int amg_finalize(amg_t *h)
 {
     if (!h) return fail(AMG_E_ARG, "NULL handle");
@@ -1543,34 +1737,10 @@ int amg_finalize(amg_t *h)
                 CK(cudaMemcpy(M.pval, pv.data(), pv.size() * sizeof(double), cudaMemcpyHostToDevice));
                 // stencil patterns: every row's (col - row) tuple from a small dictionary
                 if (h->patterns && h->nranks == 1 && M.ncols == M.nrows) {
-                    std::unordered_map<std::string, int> dict;
-                    std::vector<int32_t> rel, beg{0};
-                    std::vector<uint8_t> ids(M.nrows);
-                    bool ok = true;
-                    std::string key;
-                    for (int64_t r = 0; r < M.nrows && ok; ++r) {
-                        const int32_t lo = off32[r], hi = off32[r + 1];
-                        key.assign(reinterpret_cast<const char *>(&col_h[0]) + 0, 0);
-                        key.resize((size_t)(hi - lo) * 4);
-                        for (int32_t k = lo; k < hi; ++k) {
-                            const int32_t d = col_h[k] - (int32_t)r;
-                            memcpy(&key[(size_t)(k - lo) * 4], &d, 4);
-                        }
-                        auto it = dict.find(key);
-                        int id;
-                        if (it == dict.end()) {
-                            id = (int)dict.size();
-                            if (id >= PAT_MAX || (int)rel.size() + (hi - lo) > PAT_MAX_REL || hi - lo > 129) { ok = false; break; }
-                            dict.emplace(key, id);
-                            for (int32_t k = lo; k < hi; ++k) rel.push_back(col_h[k] - (int32_t)r);
-                            beg.push_back((int32_t)rel.size());
-                        } else {
-                            id = it->second;
-                        }
-                        ids[r] = (uint8_t)id;
-                    }
-                    if (ok && !dict.empty()) {
-                        M.npat = (int)dict.size();
+                    std::vector<int32_t> rel, beg;
+                    std::vector<uint8_t> ids;
+                    if (pattern_dict(M, off32, col_h, ids, rel, beg)) {
+                        M.npat = (int)beg.size() - 1;
                         M.nrel = (int)rel.size();
                         TRY(dalloc(&M.pid, ids.size() + 16));
                         TRY(dalloc(&M.prel, rel.size()));
@@ -1578,6 +1748,7 @@ int amg_finalize(amg_t *h)
                         CK(cudaMemcpy(M.pid, ids.data(), ids.size(), cudaMemcpyHostToDevice));
                         CK(cudaMemcpy(M.prel, rel.data(), rel.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
                         CK(cudaMemcpy(M.pbeg, beg.data(), beg.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                        if (h->symm) TRY(build_symd(h, M, off32, col_h, val_h, ids, rel, beg));
                     }
                 }
                 // SELL-32: coalesced slices where the padding stays small
@@ -1686,6 +1857,29 @@ int amg_finalize(amg_t *h)
                 M.pad_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
                                                                         (int64_t)h->sm_count * std::max(nb, 1)));
                 h->max_grid = std::max(h->max_grid, M.pad_grid);
+            } else if (!longrows && h->symm && h->patterns && h->nranks == 1 && M.ncols == M.nrows && !h->lanes_override &&
+                       M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm) {
+                // short-row stencil operators (7-point): the symmetric layout alone, pattern ids kept only with it
+                std::vector<int32_t> col_h(M.nnz);
+                std::vector<double> val_h(M.nnz);
+                if (M.nnz) {
+                    CK(cudaMemcpy(col_h.data(), M.col, M.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+                    CK(cudaMemcpy(val_h.data(), M.val, M.nnz * sizeof(double), cudaMemcpyDeviceToHost));
+                }
+                std::vector<int32_t> rel, beg;
+                std::vector<uint8_t> ids;
+                if (pattern_dict(M, off32, col_h, ids, rel, beg)) {
+                    M.npat = (int)beg.size() - 1;
+                    M.nrel = (int)rel.size();
+                    TRY(dalloc(&M.pid, ids.size() + 16));
+                    CK(cudaMemcpy(M.pid, ids.data(), ids.size(), cudaMemcpyHostToDevice));
+                    TRY(build_symd(h, M, off32, col_h, val_h, ids, rel, beg));
+                    if (!M.uval) {
+                        cudaFree(M.pid);
+                        M.pid = nullptr;
+                        M.npat = M.nrel = 0;
+                    }
+                }
             }
             const double avg = M.nrows ? (double)M.nnz / (double)M.nrows : 0.0;
             // direct kernel: one lane per row maximises rows in flight (measured on
@@ -2129,6 +2323,25 @@ int amg_bicgstab(amg_t *h, const double *b, const double *x0, double rtol, int m
         }
     }
     return finish(max_iters, relres, 0);
+}
+
+int amg_matrix_layout(amg_t *h, int level, int which, int *layout)
+{
+    if (!h || !layout) return fail(AMG_E_ARG, "amg_matrix_layout: NULL argument");
+    if (!h->finalized) return fail(AMG_E_STATE, "amg_matrix_layout: handle not finalized");
+    if (level < 0 || level >= (int)h->lv.size() || which < 0 || which > 4)
+        return fail(AMG_E_ARG, "amg_matrix_layout: level/which out of range");
+    const DevMat &M = h->lv[level].m[which];
+    if (!M.present) return fail(AMG_E_ARG, "amg_matrix_layout: matrix not uploaded");
+    // same precedence as launch_spmv
+    *layout = M.ntiles == 0           ? AMG_LAYOUT_EMPTY
+              : (M.uval && h->symm)   ? AMG_LAYOUT_SYMD
+              : M.sbeg                ? (M.scol ? AMG_LAYOUT_SELL : AMG_LAYOUT_SELL_PAT)
+              : (M.pid && M.pstart)   ? AMG_LAYOUT_PATTERN
+              : M.leaf                ? AMG_LAYOUT_LEAVES
+              : M.pstart              ? AMG_LAYOUT_PADDED
+                                      : AMG_LAYOUT_CSR;
+    return AMG_OK;
 }
 
 int amg_get_stats(amg_t *h, amg_stats_t *out)

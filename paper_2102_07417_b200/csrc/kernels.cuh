@@ -1556,6 +1556,211 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, PAT ? 5 : 4) spmv_sell(const
     }
 }
 
+// ---------------------------------------------------------------- SpMV, symmetric stencil diagonals
+
+// Symmetric stencil layout (device-only, chosen at upload for square operators
+// that are BITWISE symmetric, a_ij == a_ji, and whose rows use few relative
+// column patterns -- the fine-grid operators of configs 1, 2 and 4): only the
+// diagonals d >= 0 are stored, as nu arrays of npad doubles,
+//     uval[j * npad + i] = a(i, i + d_j),
+// and an entry of row i below the diagonal (d < 0) is read from its mirror,
+//     a(i, i + d) = a(i + d, i) = uval[j(-d) * npad + i + d].
+// Lane = row, consecutive rows per warp, so both reads are coalesced; the
+// mirror read touches a line read by the sweep |d| rows earlier (an L2 hit),
+// so HBM sees ~half of the value stream of a full copy.  Per pattern entry k
+// the smem table holds {rel, voff}: column = row + rel, value = uval[row +
+// voff].  Entries are visited in the row's stored (ascending column) order and
+// summed in the reference order (p0 + numpy pairwise), so every row sum is
+// bit-identical to amgkit/sparse.py:212-217.
+// Pattern tables live in __constant__ memory: warp-uniform reads are
+// constant-cache broadcasts (LDC) and stay off the LSU pipe, which the value
+// and x streams saturate.  SYMD_SLOTS tables per device, handed out per matrix
+// at upload (capi.cu symd_slot_*).
+constexpr int SYMD_SLOTS = 8;
+constexpr int SYMD_ENT_MAX = 512;        // pattern entries per table
+constexpr int SYMD_BEG_MAX = PAT_MAX + 1;
+__constant__ int2 c_symd_ent[SYMD_SLOTS * SYMD_ENT_MAX];      // {rel, voff}
+__constant__ int32_t c_symd_beg[SYMD_SLOTS * SYMD_BEG_MAX];   // absolute starts into c_symd_ent
+
+struct SymArgs {
+    const double *uval;
+    const uint8_t *pid;  // pattern id per row
+    int slot;
+    int chunk;  // > 0: CTA b sweeps rows [b*chunk, (b+1)*chunk) in 256-row steps (x and mirror lines
+                // reused from L1 by the next step); 0: grid-stride over 256-row blocks
+};
+
+// reference row sum of P(0..len-1): p0 + numpy pairwise(p1..), as spmv_sell
+template <bool LONG, class PF>
+__device__ __forceinline__ double ref_row_sum(const PF &P, int len)
+{
+    const int n = len - 1;
+    double sum = 0.0;
+    if (n >= 0 && n <= 128) {
+        double acc[8];
+        const int c0 = n < 8 ? n : 8;
+        const double p0 = P(0);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc[t] = (t < c0) ? P(1 + t) : 0.0;
+        double res;
+        if (n < 8) {
+            res = 0.0;
+#pragma unroll
+            for (int t = 0; t < 7; ++t)
+                if (t < n) res = add(res, acc[t]);
+        } else {
+            const int main = n - (n % 8);
+            for (int i = 8; i < main; i += 8) {
+                double p[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) p[t] = P(1 + i + t);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) acc[t] = add(acc[t], p[t]);
+            }
+            res = add(add(add(acc[0], acc[1]), add(acc[2], acc[3])), add(add(acc[4], acc[5]), add(acc[6], acc[7])));
+            const int ntail = n - main;
+            double p[7];
+#pragma unroll
+            for (int t = 0; t < 7; ++t) p[t] = (t < ntail) ? P(1 + main + t) : 0.0;
+#pragma unroll
+            for (int t = 0; t < 7; ++t)
+                if (t < ntail) res = add(res, p[t]);
+        }
+        sum = add(p0, res);
+    } else if (LONG && n > 128) {
+        sum = add(P(0), pairwise_sum(P, 1, n));
+    }
+    return sum;
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, 5) spmv_symd(const SpmvArgs a, const SymArgs sa, int nrows)
+{
+    __shared__ double red[VEC_SPMV_THREADS / 32];
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const int nthreads = gridDim.x * VEC_SPMV_THREADS;
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    const double *__restrict__ x = a.x;
+    const double *__restrict__ uv = sa.uval;
+    const int bbase = sa.slot * SYMD_BEG_MAX;
+    double dacc = 0.0;
+    const int r0 = sa.chunk ? blockIdx.x * sa.chunk : blockIdx.x * VEC_SPMV_THREADS;
+    const int rend = sa.chunk ? min(nrows, r0 + sa.chunk) : nrows;
+    const int step = sa.chunk ? VEC_SPMV_THREADS : nthreads;
+    for (int row = r0 + threadIdx.x; row < rend; row += step) {
+        const int pid = __ldg(sa.pid + row);
+        double bv = 0.0, wv = 0.0;
+        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
+        if (want_dot && !self_dot) wv = a.dotw[row];
+        const int rb = c_symd_beg[bbase + pid];
+        const int len = c_symd_beg[bbase + pid + 1] - rb;
+        auto P = [&](int k) -> double {
+            const int2 q = c_symd_ent[rb + k];
+            return prod(__ldg(uv + (row + q.y)), __ldg(x + (row + q.x)));
+        };
+        const double sum = ref_row_sum<false>(P, len);  // pattern rows have <= 129 entries
+        double yv;
+        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+        else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+        else yv = sum;
+        a.y[row] = yv;
+        if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
+        grid_finalize<VEC_SPMV_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
+// Fixed-slot variant for matrices whose rows have at most FL entries (the
+// stencil operators: FL = 8 covers 7-point, FL = 32 the 27-point rows).  Every
+// lane walks the same FL statically unrolled slots, slot k live iff k < len:
+// all loads of a row are independent and issued together (no round-by-round
+// dependency), and rows of different lengths in one warp (boundary rows) do
+// not diverge -- the reference summation order for the lane's own len is
+// realised with predicated adds:
+//   n = len - 1 < 8 : res = p1 + p2 + ... (sequential), y = p0 + res
+//   n >= 8          : acc_t = p_{1+t} + p_{9+t} + ... over the main part
+//                     (main = n - n % 8), ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)),
+//                     then the n % 8 tail sequentially, y = p0 + res
+// exactly as ref_row_sum / numpy's pairwise_sum (n <= 128 here).
+template <int EPI, int FL, int MINB>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, MINB) spmv_symd_fixed(const SpmvArgs a, const SymArgs sa,
+                                                                                     int nrows)
+{
+    __shared__ double red[VEC_SPMV_THREADS / 32];
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const int nthreads = gridDim.x * VEC_SPMV_THREADS;
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    const double *__restrict__ x = a.x;
+    const double *__restrict__ uv = sa.uval;
+    const int bbase = sa.slot * SYMD_BEG_MAX;
+    double dacc = 0.0;
+    const int r0 = sa.chunk ? blockIdx.x * sa.chunk : blockIdx.x * VEC_SPMV_THREADS;
+    const int rend = sa.chunk ? min(nrows, r0 + sa.chunk) : nrows;
+    const int step = sa.chunk ? VEC_SPMV_THREADS : nthreads;
+    int row = r0 + threadIdx.x;
+    int npid = row < rend ? __ldg(sa.pid + row) : 0;
+    for (; row < rend; row += step) {
+        const int pid = npid;
+        if (row + step < rend) npid = __ldg(sa.pid + row + step);
+        double bv = 0.0, wv = 0.0;
+        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
+        if (want_dot && !self_dot) wv = a.dotw[row];
+        const int rb = c_symd_beg[bbase + pid];
+        const int len = c_symd_beg[bbase + pid + 1] - rb;
+        double p[FL];
+#pragma unroll
+        for (int k = 0; k < FL; ++k) {
+            p[k] = 0.0;
+            if (k < len) {
+                const int2 q = c_symd_ent[rb + k];
+                p[k] = prod(__ldg(uv + (row + q.y)), __ldg(x + (row + q.x)));
+            }
+        }
+        const int n = len - 1;
+        double res = 0.0;
+        if (n < 8) {
+#pragma unroll
+            for (int k = 1; k < (FL < 8 ? FL : 8); ++k)
+                if (k <= n) res = add(res, p[k]);
+        } else {
+            const int main = n - (n % 8);
+            double acc[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) acc[t] = (1 + t < FL) ? p[1 + t] : 0.0;
+#pragma unroll
+            for (int k = 9; k < FL; ++k)
+                if (k <= main) acc[(k - 1) % 8] = add(acc[(k - 1) % 8], p[k]);
+            res = add(add(add(acc[0], acc[1]), add(acc[2], acc[3])), add(add(acc[4], acc[5]), add(acc[6], acc[7])));
+#pragma unroll
+            for (int k = 9; k < FL; ++k)
+                if (k > main && k <= n) res = add(res, p[k]);
+        }
+        const double sum = len > 0 ? add(p[0], res) : 0.0;
+        double yv;
+        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+        else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+        else yv = sum;
+        a.y[row] = yv;
+        if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
+        grid_finalize<VEC_SPMV_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
 // ---------------------------------------------------------------- SpMV, SELL-32 streamed by the bulk-copy engine
 
 // The SELL-32 layout's value (and column) arrays are one contiguous stream, so

@@ -313,6 +313,15 @@ class DeviceHierarchy:
     def set_option(self, key, value):
         C.check(C.lib().amg_set_option(self._h, key.encode(), int(value)), f"option {key}")
 
+    LAYOUTS = ("csr", "padded", "pattern", "sell", "sell_pattern", "symd", "leaves", "empty")
+    _SLOTS = {"a": 0, "p": 1, "pt": 2, "g": 3, "gt": 4}
+
+    def layout(self, level, slot):
+        """Name of the device layout matrix `slot` of `level` runs on (diagnostics)."""
+        v = ctypes.c_int32(0)
+        C.check(C.lib().amg_matrix_layout(self._h, int(level), self._SLOTS[slot], ctypes.byref(v)), "amg_matrix_layout")
+        return self.LAYOUTS[v.value]
+
     def stats(self):
         s = C.Stats()
         C.check(C.lib().amg_get_stats(self._h, ctypes.byref(s)), "amg_get_stats")

@@ -91,6 +91,48 @@ def test_spmv_sell_layouts_bit_identical(kind, sellq):
     dh.close()
 
 
+def _stencil(kind):
+    from paper_2102_07417_b200 import problems as Pb
+
+    if kind == "poisson7":
+        return Pb.poisson7(40, 40, 24)
+    if kind == "hetero27":
+        return Pb.hetero27(32, 32, 24, sigma=2.0, seed=5)
+    return Pb.rtanis7(36, 36, 20, kx=1.0, ky=1.0, kz=1e-3)
+
+
+@pytest.mark.parametrize("kind", ["poisson7", "hetero27", "rtanis7"])
+def test_spmv_symmetric_diagonals_bit_identical(kind):
+    # bitwise-symmetric stencil operators run on the upper-diagonal layout
+    # (mirror reads for d < 0); rows must equal the reference's bit for bit
+    m = _stencil(kind)
+    x = np.random.default_rng(11).uniform(-1, 1, m.ncols)
+    want = O.spmv(m, x)
+    variants = [{"symm": 0}] + [{"symm": 1, "symd_fixed": f, "symd_chunked": c} for f in (0, 1, 2) for c in (0, 1)]
+    for opts in variants:
+        dh = amg.DeviceHierarchy.from_matrices([m], options=opts)
+        assert (dh.layout(0, "a") == "symd") == bool(opts["symm"])
+        np.testing.assert_array_equal(dh.matrix(0, "a")(x), want, err_msg=str(opts))
+        dh.close()
+
+
+def test_spmv_symmetric_layout_rejects_one_ulp_asymmetry():
+    from paper_2102_07417_b200.problems import Csr
+
+    m = _stencil("hetero27")
+    v = m.values.copy()
+    r = m.nrows // 2
+    k = m.row_offsets[r]  # first (lowest-column) entry of row r: below the diagonal
+    assert m.col_indices[k] < r
+    v[k] = np.nextafter(v[k], np.inf)
+    m2 = Csr(m.nrows, m.ncols, m.row_offsets, m.col_indices, v)
+    x = np.random.default_rng(12).uniform(-1, 1, m.ncols)
+    dh = amg.DeviceHierarchy.from_matrices([m2])
+    assert dh.layout(0, "a") != "symd"
+    np.testing.assert_array_equal(dh.matrix(0, "a")(x), O.spmv(m2, x))
+    dh.close()
+
+
 @pytest.mark.parametrize("opts", [{"tile_nnz": 64, "tile_rows": 32, "stages": 1},
                                   {"tile_nnz": 300, "tile_rows": 64, "stages": 2},
                                   {"tile_nnz": 4096, "tile_rows": 512, "stages": 2}])
