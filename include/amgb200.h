@@ -81,6 +81,7 @@ typedef struct amg_stats {
     int n_levels;
     int tail_level;           /* first level run by the cluster tail kernel (0 = none) */
     int cluster;              /* CTAs in the tail cluster */
+    int fused_levels;         /* bit k: level k's FSAI steps run as one G/G^T kernel */
 } amg_stats_t;
 
 /* Handle for one GPU.  nccl_unique_id: 128 bytes (NULL when nranks == 1). */
@@ -162,7 +163,8 @@ enum {
     AMG_LAYOUT_SELL_PAT = 4,  /* SELL-32 slices, stencil-pattern columns */
     AMG_LAYOUT_SYMD = 5,      /* symmetric stencil: upper diagonals + pattern ids */
     AMG_LAYOUT_LEAVES = 6,    /* long rows, leaf list */
-    AMG_LAYOUT_EMPTY = 7
+    AMG_LAYOUT_EMPTY = 7,
+    AMG_LAYOUT_SELL_UNIFORM = 8 /* SELL-32, every slice the same width (short rows) */
 };
 int amg_matrix_layout(amg_t *h, int level, int which, int *layout);
 /* Tuning / diagnostics: 0 = auto. */

@@ -74,6 +74,10 @@ struct DevMat {
     int npat = 0, nrel = 0;
     double *uval = nullptr;      // symmetric stencil layout (spmv_symd), nullptr if unused
     int sym_slot = -1;           // its __constant__ pattern-table slot
+    double *uval_s = nullptr;    // uniform-width SELL-32 (spmv_sellu), nullptr if unused
+    int32_t *ucol_s = nullptr;
+    uint8_t *ulen_s = nullptr;
+    int uW = 0, u_grid = 0;
     int nudiag = 0, sym_grid = 0, sym_fl = 0, symf_grid = 0;  // sym_fl: fixed-slot kernel width (0: none)
     int32_t *pstart = nullptr;   // padded-aligned layout (spmv_vec), nullptr if unused
     double *pval = nullptr;
@@ -107,6 +111,17 @@ struct LevelD {
     double omega = 1.0;
     double *inv_diag = nullptr;
     double *y = nullptr, *x = nullptr, *r = nullptr, *t = nullptr;
+    struct Fused {  // FSAI step with G and G^T in one kernel (fsai_fused), nullptrs if unused
+        bool on = false;
+        double *gval = nullptr;
+        int32_t *gcol = nullptr;
+        uint8_t *glen = nullptr;
+        int32_t *tstart = nullptr, *tq = nullptr;
+        unsigned *bcnt = nullptr;
+        unsigned *ctr = nullptr;
+        double *upart = nullptr;
+        int W = 0, nunits = 0, nblk = 0, lag = 0, reach = 0, grid = 0;
+    } fz;
 };
 
 template <class T>
@@ -184,6 +199,11 @@ struct amg_handle {
     int small_rows_per_sm = 128;  // below sm_count * this many rows a matrix counts as small
     int patterns = 1;             // stencil-pattern layout for square operators with few row patterns
     int symd_minb = 4;            // fixed-slot 32-wide kernel: min CTAs/SM (register budget) 3, 4 or 5
+    int sellu = 1;                // uniform-width SELL-32 for rows of <= 16 entries padding <= 10% (e.g. FSAI G)
+    int fused = 0;                // FSAI steps of large levels as one G/G^T kernel (fsai_fused): bit-identical but
+                                  // measured slower on config 2 (294 vs 144 us per level-0 step: the kernels are latency-
+                                  // bound, fusing serialises G's and G^T's dependent loads per warp)
+    int fused_lag_extra = 0;      // extra ticket lag (0 = one grid)
     int symd_chunked = 0;         // symmetric kernels: contiguous row chunk per CTA (measured slower than grid-stride)
     int symd_fixed = 1;           // fixed-slot symmetric kernel: 1 rows <= 8 entries (7-point), 2 also <= 32 (27-point:
                                   // measured slower than the round-by-round kernel on config 2), 0 off
@@ -292,6 +312,21 @@ static SpmvSymFn spmv_symd_fixed_fn(int epi, int fl, int minb = 0)
     default: AMG_F(EPI_ADD)
     }
 #undef AMG_F
+}
+
+typedef void (*SpmvSellUFn)(const SpmvArgs, const SellUArgs, int);
+
+static SpmvSellUFn spmv_sellu_fn(int epi, int W)
+{
+#define AMG_U(E) return W <= 4 ? spmv_sellu<E, 4> : W <= 9 ? spmv_sellu<E, 9> : spmv_sellu<E, 16>;
+    switch (epi) {
+    case EPI_PLAIN: AMG_U(EPI_PLAIN)
+    case EPI_RESID: AMG_U(EPI_RESID)
+    case EPI_AXPYW: AMG_U(EPI_AXPYW)
+    case EPI_SETW: AMG_U(EPI_SETW)
+    default: AMG_U(EPI_ADD)
+    }
+#undef AMG_U
 }
 
 typedef void (*SpmvSellqFn)(const SpmvArgs, const SellArgs, const SellqArgs, int);
@@ -617,6 +652,10 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
             TRY(launch_k(h, spmv_symd_fixed_fn(epi, M.sym_fl, h->symd_minb), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
         else
             TRY(launch_k(h, spmv_symd_fn(epi), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
+    } else if (M.uval_s && h->sellu) {
+        SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW};
+        TRY(launch_k(h, spmv_sellu_fn(epi, M.uW), grid_cap ? std::min(grid_cap, M.u_grid) : M.u_grid, VEC_SPMV_THREADS, 0,
+                     a, ua, (int)M.nrows));
     } else if (M.sbeg && M.sq_cta && h->sellq) {
         SellArgs sa{M.sbeg, M.sval, M.scol, M.slen, M.pid, M.prel, M.pbeg, M.npat, M.nrel, M.sperm};
         SellqArgs q{M.sq_cta, M.sq_stage, M.sq_stages};
@@ -772,7 +811,34 @@ static int enqueue_smooth(amg_t *h, int k, const double *b, double *x, int steps
             src = L.r;
         }
         const bool set = from_zero && s == 0;
-        if (L.sm_kind == AMG_SMOOTHER_FSAI) {
+        if (L.sm_kind == AMG_SMOOTHER_FSAI && L.fz.on && h->fused && !h->collect) {
+            FusedArgs fa{};
+            fa.gval = L.fz.gval;
+            fa.gcol = L.fz.gcol;
+            fa.glen = L.fz.glen;
+            fa.tstart = L.fz.tstart;
+            fa.tq = L.fz.tq;
+            fa.y = src;
+            fa.t = L.t;
+            fa.x = x;
+            fa.omega = L.omega;
+            fa.nrows = (int)L.n;
+            fa.W = L.fz.W;
+            fa.nunits = L.fz.nunits;
+            fa.nblk = L.fz.nblk;
+            fa.lag = L.fz.lag;
+            fa.reach = L.fz.reach;
+            fa.bcnt = L.fz.bcnt;
+            fa.ctr = L.fz.ctr;
+            fa.upart = L.fz.upart;
+            fa.dotw = dw;
+            fa.fin = kfin(h, f);
+            fa.ctl = h->ctl;
+            fa.gate1 = g1;
+            fa.gate2 = nullptr;
+            TRY(launch_k(h, set ? fsai_fused<EPI_SETW> : fsai_fused<EPI_AXPYW>, L.fz.grid, FUSED_THREADS, 0, fa));
+            TRY(post_fin(h, f, g1));
+        } else if (L.sm_kind == AMG_SMOOTHER_FSAI) {
             TRY(launch_spmv(h, L.m[AMG_G], src, L.t, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, g1, nullptr));
             TRY(launch_spmv(h, L.m[AMG_GT], L.t, x, set ? EPI_SETW : EPI_AXPYW, x, L.omega, dw, f, g1, nullptr));
         } else if (h->collect) {
@@ -1142,12 +1208,13 @@ void amg_destroy(amg_t *h)
     auto F = [](void *p) { if (p) cudaFree(p); };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta); F(M.uval);
+            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s);
             symd_slot_give(h->device, M.sym_slot);
             M.sym_slot = -1;
             halo_free(M.halo);
         }
         F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
+        F(L.fz.gval); F(L.fz.gcol); F(L.fz.glen); F(L.fz.tstart); F(L.fz.tq); F(L.fz.bcnt); F(L.fz.ctr); F(L.fz.upart);
     }
     F(h->Lp); F(h->LU); F(h->dinv); F(h->binv); F(h->tail_ops); F(h->tail_mats); F(h->tail_splits); F(h->piv); F(h->partials); F(h->ticket); F(h->ctl);
     F(h->b); F(h->x); F(h->r); F(h->z); F(h->p); F(h->q); F(h->tmp_in); F(h->tmp_out); F(h->hist);
@@ -1184,6 +1251,9 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "small_rows_per_sm") { h->small_rows_per_sm = (int)value; return AMG_OK; }
     if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
     if (k == "symm") { h->symm = value ? 1 : 0; return AMG_OK; }
+    if (k == "sellu") { h->sellu = value ? 1 : 0; return AMG_OK; }
+    if (k == "fused") { h->fused = value ? 1 : 0; return AMG_OK; }
+    if (k == "fused_lag_extra") { h->fused_lag_extra = (int)value; return AMG_OK; }
     if (k == "symd_fixed") { h->symd_fixed = (int)value; return AMG_OK; }
     if (k == "symd_chunked") { h->symd_chunked = value ? 1 : 0; return AMG_OK; }
     if (k == "symd_minb") { h->symd_minb = (int)value; return AMG_OK; }
@@ -1552,6 +1622,95 @@ static int build_symd(amg_t *h, DevMat &M, const std::vector<int32_t> &off32, co
     return AMG_OK;
 }
 
+// FSAI step kernel data (fsai_fused) for the large levels of a single-GPU
+// hierarchy: G as uniform-width SELL-32 (padding <= 10%), G^T as positions
+// into it.  Taken only if the uploaded G^T is exactly the transpose of G
+// (same entries, same order, bitwise values); otherwise the two-kernel path stays.
+static int build_fused(amg_t *h)
+{
+    if (h->nranks != 1) return AMG_OK;
+    const int nl = (int)h->lv.size();
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)fsai_fused<EPI_AXPYW>, FUSED_THREADS, 0));
+    if (occ < 1) return AMG_OK;
+    for (int k = 0; k < nl - 1; ++k) {
+        LevelD &L = h->lv[k];
+        if (L.sm_kind != AMG_SMOOTHER_FSAI || L.n < (int64_t)h->sm_count * h->small_rows_per_sm) continue;
+        const DevMat &G = L.m[AMG_G], &GT = L.m[AMG_GT];
+        if (!G.present || !GT.present || G.nrows != L.n || G.ncols != L.n || GT.nrows != L.n || GT.nnz != G.nnz) continue;
+        const int64_t n = L.n, nnz = G.nnz;
+        std::vector<int32_t> go(n + 1), gc(nnz), to(n + 1), tc(nnz);
+        std::vector<double> gv(nnz), tv(nnz);
+        CK(cudaMemcpy(go.data(), G.off, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(to.data(), GT.off, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        if (nnz) {
+            CK(cudaMemcpy(gc.data(), G.col, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(gv.data(), G.val, nnz * sizeof(double), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(tc.data(), GT.col, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(tv.data(), GT.val, nnz * sizeof(double), cudaMemcpyDeviceToHost));
+        }
+        int W = 0;
+        for (int64_t r = 0; r < n; ++r) W = std::max(W, go[r + 1] - go[r]);
+        const int64_t ns = (n + 31) / 32;
+        if (W == 0 || W > 129 || (double)ns * 32 * W > 1.10 * (double)nnz || ns * 32 * W >= INT32_MAX - 64) continue;
+        for (int64_t r = 0; r < n; ++r)
+            if (to[r + 1] - to[r] > 129) W = -1;
+        if (W < 0) continue;
+        std::vector<double> sv((size_t)ns * 32 * W, 0.0);
+        std::vector<int32_t> sc((size_t)ns * 32 * W, 0);
+        std::vector<uint8_t> ln(n + 16, 0);
+        std::vector<int32_t> cnt(n + 1, 0);
+        for (int64_t r = 0; r < n; ++r) {
+            ln[r] = (uint8_t)(go[r + 1] - go[r]);
+            for (int32_t e = go[r]; e < go[r + 1]; ++e) {
+                const int64_t q = (r >> 5) * 32 * W + 32 * (int64_t)(e - go[r]) + (r & 31);
+                sv[q] = gv[e];
+                sc[q] = gc[e];
+                ++cnt[gc[e] + 1];
+            }
+            for (int32_t e = go[r + 1] - go[r]; e < W; ++e) sc[(r >> 5) * 32 * W + 32 * e + (r & 31)] = (int32_t)r;
+        }
+        for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+        bool ok = true;
+        for (int64_t i = 0; i < n && ok; ++i) ok = (cnt[i + 1] - cnt[i]) == (to[i + 1] - to[i]) && to[i] == cnt[i];
+        if (!ok) continue;
+        std::vector<int32_t> tq(nnz > 0 ? nnz : 1), fill(cnt.begin(), cnt.end() - 1);
+        int64_t reach = 0;
+        for (int64_t r = 0; r < n; ++r)  // rows of G in ascending order: G^T rows fill in ascending column order
+            for (int32_t e = go[r]; e < go[r + 1]; ++e) {
+                const int32_t i = gc[e];
+                const int64_t q = (r >> 5) * 32 * W + 32 * (int64_t)(e - go[r]) + (r & 31);
+                const int32_t m = fill[i]++;
+                if (tc[m] != (int32_t)r || memcmp(&tv[m], &gv[e], sizeof(double)) != 0) ok = false;
+                tq[m] = (int32_t)q;
+                reach = std::max<int64_t>(reach, r - i);
+            }
+        if (!ok) continue;
+        auto &F = L.fz;
+        F.W = W;
+        F.nunits = (int)((n + 31) / 32);
+        F.nblk = (F.nunits + 7) / 8;
+        F.reach = (int)reach;
+        F.grid = std::max(1, std::min((F.nunits + 7) / 8, occ * h->sm_count));  // one resident wave
+        F.lag = (int)((reach + 63) / 32) + 8 + (h->fused_lag_extra > 0 ? h->fused_lag_extra : F.grid * (FUSED_THREADS / 32));
+        TRY(dalloc(&F.gval, sv.size()));
+        TRY(dalloc(&F.gcol, sc.size()));
+        TRY(dalloc(&F.glen, ln.size()));
+        TRY(dalloc(&F.tstart, (size_t)n + 1));
+        TRY(dalloc(&F.tq, tq.size()));
+        TRY(dalloc(&F.bcnt, (size_t)F.nblk));
+        TRY(dalloc(&F.ctr, 4));
+        TRY(dalloc(&F.upart, (size_t)F.nunits));
+        CK(cudaMemcpy(F.gval, sv.data(), sv.size() * sizeof(double), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(F.gcol, sc.data(), sc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(F.glen, ln.data(), ln.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(F.tstart, cnt.data(), ((size_t)n + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(F.tq, tq.data(), tq.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        F.on = true;
+    }
+    return AMG_OK;
+}
+
 int amg_finalize(amg_t *h)
 {
     if (!h) return fail(AMG_E_ARG, "NULL handle");
@@ -1881,6 +2040,51 @@ int amg_finalize(amg_t *h)
                     }
                 }
             }
+            if (!M.uval && !longrows && !h->lanes_override && M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm) {
+                // uniform-width SELL-32: rows of <= 16 entries, every slice as wide as the widest row
+                int W = 0;
+                for (int64_t r = 0; r < M.nrows; ++r) W = std::max(W, off32[r + 1] - off32[r]);
+                const int64_t ns = (M.nrows + 31) / 32;
+                if (W >= 1 && W <= 16 && (double)ns * 32 * W <= 1.10 * (double)M.nnz && ns * 32 * W < INT32_MAX - 64) {
+                    std::vector<int32_t> col_h(M.nnz);
+                    std::vector<double> val_h(M.nnz);
+                    if (M.nnz) {
+                        CK(cudaMemcpy(col_h.data(), M.col, M.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+                        CK(cudaMemcpy(val_h.data(), M.val, M.nnz * sizeof(double), cudaMemcpyDeviceToHost));
+                    }
+                    const size_t tot = (size_t)ns * 32 * W;
+                    std::vector<double> sv(tot, 0.0);
+                    std::vector<int32_t> sc(tot, 0);
+                    std::vector<uint8_t> ln(M.nrows + 16, 0);
+                    for (int64_t r = 0; r < M.nrows; ++r) {
+                        const int32_t len = off32[r + 1] - off32[r];
+                        ln[r] = (uint8_t)len;
+                        const int64_t b0 = (r >> 5) * 32 * W + (r & 31);
+                        for (int32_t k = 0; k < W; ++k) {
+                            const int64_t q = b0 + 32 * (int64_t)k;
+                            if (k < len) {
+                                sv[q] = val_h[off32[r] + k];
+                                sc[q] = col_h[off32[r] + k];
+                            } else {
+                                sc[q] = (int32_t)std::min<int64_t>(r, M.ncols - 1);  // padding: any valid column
+                            }
+                        }
+                    }
+                    TRY(dalloc(&M.uval_s, tot));
+                    TRY(dalloc(&M.ucol_s, tot));
+                    TRY(dalloc(&M.ulen_s, ln.size()));
+                    CK(cudaMemcpy(M.uval_s, sv.data(), tot * sizeof(double), cudaMemcpyHostToDevice));
+                    CK(cudaMemcpy(M.ucol_s, sc.data(), tot * sizeof(int32_t), cudaMemcpyHostToDevice));
+                    CK(cudaMemcpy(M.ulen_s, ln.data(), ln.size(), cudaMemcpyHostToDevice));
+                    M.uW = W;
+                    int nbu = 0;
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbu, (const void *)spmv_sellu_fn(EPI_RESID, W),
+                                                                     VEC_SPMV_THREADS, 0));
+                    M.u_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
+                                                                          (int64_t)h->sm_count * std::max(nbu, 1)));
+                    h->max_grid = std::max(h->max_grid, M.u_grid);
+                }
+            }
             const double avg = M.nrows ? (double)M.nnz / (double)M.nrows : 0.0;
             // direct kernel: one lane per row maximises rows in flight (measured on
             // B200: 27-pt A 3.5 TB/s at 1 lane vs 2.4 at 4); wide rows split over lanes
@@ -1925,6 +2129,7 @@ int amg_finalize(amg_t *h)
     TRY(dalloc(&h->ctl, 1));
     CK(cudaMallocHost((void **)&h->ctl_h, sizeof(PcgCtl)));
     std::memset(h->ctl_h, 0, sizeof(PcgCtl));
+    if (!container && h->fused) TRY(build_fused(h));
     if (!container) TRY(build_tail(h));
     h->finalized = true;
     CK(cudaDeviceSynchronize());
@@ -2143,6 +2348,18 @@ int amg_time_spmv(amg_t *h, int level, int which, int reps, double *ms_per_launc
         *ms_per_launch = ms / reps;
         return AMG_OK;
     }
+    if (which == 5 && level >= 0 && level + 1 < (int)h->lv.size() && reps >= 1 && ms_per_launch && !h->container) {
+        // diagnostics: one smoother step from zero (x = w M^-1 b) at `level`
+        TRY(enqueue_smooth(h, level, h->tmp_in, h->tmp_out, 1, true, nullptr, FIN_NONE, nullptr));
+        CK(cudaEventRecord(h->ev0, h->stream));
+        for (int i = 0; i < reps; ++i) TRY(enqueue_smooth(h, level, h->tmp_in, h->tmp_out, 1, true, nullptr, FIN_NONE, nullptr));
+        CK(cudaEventRecord(h->ev1, h->stream));
+        TRY(sync_stream(h));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+        *ms_per_launch = ms / reps;
+        return AMG_OK;
+    }
     if (level < 0 || level >= (int)h->lv.size() || which < 0 || which > 4 || reps < 1 || !ms_per_launch)
         return fail(AMG_E_ARG, "amg_time_spmv: bad arguments");
     const DevMat &M = h->lv[level].m[which];
@@ -2336,6 +2553,7 @@ int amg_matrix_layout(amg_t *h, int level, int which, int *layout)
     // same precedence as launch_spmv
     *layout = M.ntiles == 0           ? AMG_LAYOUT_EMPTY
               : (M.uval && h->symm)   ? AMG_LAYOUT_SYMD
+              : (M.uval_s && h->sellu) ? AMG_LAYOUT_SELL_UNIFORM
               : M.sbeg                ? (M.scol ? AMG_LAYOUT_SELL : AMG_LAYOUT_SELL_PAT)
               : (M.pid && M.pstart)   ? AMG_LAYOUT_PATTERN
               : M.leaf                ? AMG_LAYOUT_LEAVES
@@ -2356,6 +2574,8 @@ int amg_get_stats(amg_t *h, amg_stats_t *out)
     out->n_levels = (int)h->lv.size();
     out->tail_level = h->tail_level;
     out->cluster = h->cluster;
+    for (size_t k = 0; k < h->lv.size() && k < 31; ++k)
+        if (h->lv[k].fz.on && h->fused) out->fused_levels |= 1 << k;
     return AMG_OK;
 }
 

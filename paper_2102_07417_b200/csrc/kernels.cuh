@@ -1689,6 +1689,39 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, 5) spmv_symd(const SpmvArgs 
 //                     (main = n - n % 8), ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)),
 //                     then the n % 8 tail sequentially, y = p0 + res
 // exactly as ref_row_sum / numpy's pairwise_sum (n <= 128 here).
+// Reference row sum (p0 + numpy pairwise) of the first len of FL products
+// held in registers, realised with predicated adds (no divergence between
+// rows of different lengths):
+//   n = len - 1 < 8 : res = p1 + p2 + ... (sequential), y = p0 + res
+//   n >= 8          : acc_t = p_{1+t} + p_{9+t} + ... over the main part
+//                     (main = n - n % 8), ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)),
+//                     then the n % 8 tail sequentially, y = p0 + res
+// exactly as ref_row_sum / numpy's pairwise_sum (len <= FL <= 129).
+template <int FL>
+__device__ __forceinline__ double ref_sum_fixed(const double (&p)[FL], int len)
+{
+    const int n = len - 1;
+    double res = 0.0;
+    if (n < 8) {
+#pragma unroll
+        for (int k = 1; k < (FL < 8 ? FL : 8); ++k)
+            if (k <= n) res = add(res, p[k]);
+    } else {
+        const int main = n - (n % 8);
+        double acc[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc[t] = (1 + t < FL) ? p[1 + t] : 0.0;
+#pragma unroll
+        for (int k = 9; k < FL; ++k)
+            if (k <= main) acc[(k - 1) % 8] = add(acc[(k - 1) % 8], p[k]);
+        res = add(add(add(acc[0], acc[1]), add(acc[2], acc[3])), add(add(acc[4], acc[5]), add(acc[6], acc[7])));
+#pragma unroll
+        for (int k = 9; k < FL; ++k)
+            if (k > main && k <= n) res = add(res, p[k]);
+    }
+    return len > 0 ? add(p[0], res) : 0.0;
+}
+
 template <int EPI, int FL, int MINB>
 __global__ void __launch_bounds__(VEC_SPMV_THREADS, MINB) spmv_symd_fixed(const SpmvArgs a, const SymArgs sa,
                                                                                      int nrows)
@@ -1726,26 +1759,7 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, MINB) spmv_symd_fixed(const 
                 p[k] = prod(__ldg(uv + (row + q.y)), __ldg(x + (row + q.x)));
             }
         }
-        const int n = len - 1;
-        double res = 0.0;
-        if (n < 8) {
-#pragma unroll
-            for (int k = 1; k < (FL < 8 ? FL : 8); ++k)
-                if (k <= n) res = add(res, p[k]);
-        } else {
-            const int main = n - (n % 8);
-            double acc[8];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) acc[t] = (1 + t < FL) ? p[1 + t] : 0.0;
-#pragma unroll
-            for (int k = 9; k < FL; ++k)
-                if (k <= main) acc[(k - 1) % 8] = add(acc[(k - 1) % 8], p[k]);
-            res = add(add(add(acc[0], acc[1]), add(acc[2], acc[3])), add(add(acc[4], acc[5]), add(acc[6], acc[7])));
-#pragma unroll
-            for (int k = 9; k < FL; ++k)
-                if (k > main && k <= n) res = add(res, p[k]);
-        }
-        const double sum = len > 0 ? add(p[0], res) : 0.0;
+        const double sum = ref_sum_fixed<FL>(p, len);
         double yv;
         if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
         else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
@@ -1758,6 +1772,222 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, MINB) spmv_symd_fixed(const 
     if (want_dot || a.fin != FIN_NONE) {
         double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
         grid_finalize<VEC_SPMV_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
+// ---------------------------------------------------------------- SpMV, uniform-width SELL-32
+
+// Every 32-row slice padded to the same width W (taken where that costs
+// <= 10%: the FSAI factors G, 9 entries on every row): entry k of row i sits
+// at (i/32)*32W + 32k + i%32, so a lane's addresses follow from its row alone.
+// All W value / column loads are issued at once (padding slots hold value 0
+// and column = row, and are never summed), the x gathers in the next step --
+// two dependent memory steps per row instead of slice offset -> length ->
+// values -> gathers.  Sum over the lane's own len in the reference order.
+struct SellUArgs {
+    const double *val;
+    const int32_t *col;
+    const uint8_t *len;
+    int W;
+};
+
+// Software-pipelined: the next row's columns and length are loaded one
+// iteration ahead, so a row's W value loads and its x gathers leave together
+// (one dependent memory step per row instead of length -> values/columns ->
+// gathers).
+template <int EPI, int FL>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, FL <= 4 ? 6 : FL <= 9 ? 4 : 3) spmv_sellu(const SpmvArgs a,
+                                                                                           const SellUArgs u, int nrows)
+{
+    __shared__ double red[VEC_SPMV_THREADS / 32];
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const int nthreads = gridDim.x * VEC_SPMV_THREADS;
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    const double *__restrict__ x = a.x;
+    const int W32 = 32 * u.W;
+    double dacc = 0.0;
+    int row = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x;
+    int c[FL];
+    int len = 0;
+    auto fetch = [&](int r) {
+        const int base = (r >> 5) * W32 + (r & 31);
+        len = __ldg(u.len + r);
+#pragma unroll
+        for (int k = 0; k < FL; ++k) c[k] = (k < u.W) ? __ldg(u.col + base + 32 * k) : r;
+    };
+    if (row < nrows) fetch(row);
+    for (; row < nrows; row += nthreads) {
+        const int base = (row >> 5) * W32 + (row & 31);
+        double p[FL];
+#pragma unroll
+        for (int k = 0; k < FL; ++k) p[k] = (k < u.W) ? prod(__ldg(u.val + base + 32 * k), __ldg(x + c[k])) : 0.0;
+        const int clen = len;
+        if (row + nthreads < nrows) fetch(row + nthreads);
+        double bv = 0.0, wv = 0.0;
+        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
+        if (want_dot && !self_dot) wv = a.dotw[row];
+        const double sum = ref_sum_fixed<FL>(p, clen);
+        double yv;
+        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+        else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+        else yv = sum;
+        a.y[row] = yv;
+        if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v2 = block_sum<VEC_SPMV_THREADS>(dacc, red);
+        grid_finalize<VEC_SPMV_THREADS>(v2, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
+// ---------------------------------------------------------------- FSAI smoother step, G and G^T fused
+
+// x = w * G^T (G y)  (EPI_SETW)  or  x = x + w * G^T (G y)  (EPI_AXPYW)
+// (amgkit/smoothers.py:45-50, 170-172) in ONE persistent kernel.  Work unit =
+// 32 rows = one warp, no CTA barriers: warp w of the grid takes tickets
+// w, w + NW, w + 2 NW, ...  Ticket u: phase A computes t = G y for unit u (G
+// in uniform-width SELL-32, lane = row) and counts the unit into its 256-row
+// block's completion counter (release); phase B computes the G^T rows of
+// unit u - lag once every block holding a G row they read (up to `reach`
+// rows ahead) is complete (acquire; a per-warp watermark skips blocks
+// already seen complete).  G^T is not stored as values: entry m of G^T row i
+// is the position q of G(j, i) in G's SELL array -> value gval[q], column
+// j = (q / (32 W)) * 32 + q % 32, both read from L2 where phase A left them,
+// as it left t.  HBM traffic per step: G once (12 B/entry) + 4 B/entry of
+// G^T positions + the y / x vectors (vs. G and G^T as two 12 B/entry
+// matrices plus t written and re-read).  Row sums are the reference's
+// (p0 + numpy pairwise; G^T rows in ascending column order), so x is
+// bit-identical to the two-kernel sequence.  Progress: a ticket only waits
+// on smaller tickets; the grid is at most one resident wave (occupancy), so
+// every ticket's warp is running.  Dot partials are per unit (fixed),
+// folded in unit order by the last CTA: deterministic.
+struct FusedArgs {
+    const double *gval;     // G, SELL-32 uniform width W: entry k of row j at (j/32)*32W + 32k + j%32
+    const int32_t *gcol;
+    const uint8_t *glen;    // G row lengths (<= W)
+    const int32_t *tstart;  // G^T rows: CSR starts into tq
+    const int32_t *tq;      // positions of the G^T entries in gval
+    const double *y;
+    double *t;
+    double *x;
+    double omega;
+    int nrows, W, nunits, nblk, lag, reach;
+    unsigned *bcnt;         // per 256-row block: completed units, cumulative over launches
+    unsigned *ctr;          // [1] CTAs done, [2] generation
+    double *upart;          // per-unit dot partials
+    const double *dotw;
+    int fin;
+    PcgCtl *ctl;
+    const int *gate1;
+    const int *gate2;
+};
+
+constexpr int FUSED_THREADS = 256;
+
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned *p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void red_release_gpu_add(unsigned *p, unsigned v)
+{
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(FUSED_THREADS, 4) fsai_fused(const FusedArgs a)
+{
+    __shared__ int s_last;
+    __shared__ double red[FUSED_THREADS / 32];
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const unsigned gen = *(volatile unsigned *)(a.ctr + 2) + 1u;
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.x;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int nw = gridDim.x * (FUSED_THREADS / 32);
+    const int W32 = 32 * a.W;
+    const int total = a.nunits + a.lag;
+    int ready = -1;  // blocks [0, ready] seen complete by this warp
+    for (int u = blockIdx.x * (FUSED_THREADS / 32) + (tid >> 5); u < total; u += nw) {
+        if (u < a.nunits) {  // phase A: t = G y, rows of unit u
+            const int row = u * 32 + lane;
+            if (row < a.nrows) {
+                const int len = __ldg(a.glen + row);
+                const int sb = u * W32 + lane;
+                const double *__restrict__ y = a.y;
+                auto P = [&](int k) -> double {
+                    return prod(__ldg(a.gval + sb + 32 * k), __ldg(y + __ldg(a.gcol + sb + 32 * k)));
+                };
+                a.t[row] = ref_row_sum<false>(P, len);
+            }
+            __syncwarp();
+            if (lane == 0) red_release_gpu_add(a.bcnt + (u >> 3), 1u);
+        }
+        const int ub = u - a.lag;
+        if (ub >= 0) {  // phase B: x = EPI(w * G^T t), rows of unit ub
+            const int need = min(a.nblk - 1, (ub * 32 + 31 + a.reach) >> 8);
+            while (ready < need) {
+                const int b = ready + 1 + lane;
+                if (b <= need) {
+                    const unsigned full = (b == a.nblk - 1) ? (unsigned)(a.nunits - 8 * b) : 8u;
+                    while (ld_acquire_gpu_u32(a.bcnt + b) < full * gen) __nanosleep(32);
+                }
+                __syncwarp();
+                ready = min(need, ready + 32);
+            }
+            const int row = ub * 32 + lane;
+            double dv = 0.0;
+            if (row < a.nrows) {
+                const int ts = __ldg(a.tstart + row);
+                const int len = __ldg(a.tstart + row + 1) - ts;
+                const double *tt = a.t;
+                auto P = [&](int m) -> double {
+                    const int q = __ldg(a.tq + ts + m);
+                    const int j = (q / W32) * 32 + (q & 31);
+                    return prod(__ldg(a.gval + q), __ldcg(tt + j));
+                };
+                const double sum = ref_row_sum<false>(P, len);
+                double yv;
+                if constexpr (EPI == EPI_AXPYW) yv = add(a.x[row], __dmul_rn(a.omega, sum));
+                else yv = __dmul_rn(a.omega, sum);
+                a.x[row] = yv;
+                if (want_dot) dv = yv * (self_dot ? yv : a.dotw[row]);
+            }
+            if (want_dot || a.fin != FIN_NONE) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) dv += __shfl_xor_sync(0xffffffffu, dv, o);
+                if (lane == 0) a.upart[ub] = dv;
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        s_last = atomicAdd(a.ctr + 1, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        if (want_dot || a.fin != FIN_NONE) {
+            double acc = 0.0;
+            for (int i = tid; i < a.nunits; i += FUSED_THREADS) acc += __ldcg(a.upart + i);
+            acc = block_sum<FUSED_THREADS>(acc, red);
+            if (tid == 0) apply_fin(a.fin, acc, a.ctl);
+        }
+        if (tid == 0) {
+            a.ctr[1] = 0u;
+            a.ctr[2] = gen;
+            __threadfence();
+        }
     }
 }
 

@@ -307,13 +307,14 @@ class DeviceHierarchy:
     def time_spmv(self, level, slot, reps=20):
         """Average device ms of one SpMV launch (CUDA events on the library stream)."""
         ms = C.D(0.0)
-        C.check(C.lib().amg_time_spmv(self._h, level, C.SLOT[slot], int(reps), ctypes.byref(ms)), "time_spmv")
+        which = 5 if slot == "smooth" else C.SLOT[slot]  # "smooth": one smoother step from zero
+        C.check(C.lib().amg_time_spmv(self._h, level, which, int(reps), ctypes.byref(ms)), "time_spmv")
         return ms.value
 
     def set_option(self, key, value):
         C.check(C.lib().amg_set_option(self._h, key.encode(), int(value)), f"option {key}")
 
-    LAYOUTS = ("csr", "padded", "pattern", "sell", "sell_pattern", "symd", "leaves", "empty")
+    LAYOUTS = ("csr", "padded", "pattern", "sell", "sell_pattern", "symd", "leaves", "empty", "sell_uniform")
     _SLOTS = {"a": 0, "p": 1, "pt": 2, "g": 3, "gt": 4}
 
     def layout(self, level, slot):

@@ -116,6 +116,28 @@ def test_spmv_symmetric_diagonals_bit_identical(kind):
         dh.close()
 
 
+@pytest.mark.parametrize("width", [3, 9, 16])
+def test_spmv_uniform_sell_bit_identical(width):
+    # rows of <= 16 entries with every 32-row slice padded to the widest row
+    # (FSAI factors): all slots loaded at once, summed over each row's own length
+    from paper_2102_07417_b200.problems import Csr
+
+    rng = np.random.default_rng(width)
+    n = 40000
+    lens = np.where(rng.random(n) < 0.97, width, rng.integers(0, width + 1, n))
+    lens[:3] = [0, 1, width]
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    m = Csr(n, n, off, cols, rng.uniform(-1, 1, off[-1]))
+    x = rng.uniform(-1, 1, n)
+    want = O.spmv(m, x)
+    for sellu in (1, 0):
+        dh = amg.DeviceHierarchy.from_matrices([m], options={"sellu": sellu, "symm": 0})
+        assert (dh.layout(0, "a") == "sell_uniform") == bool(sellu)
+        np.testing.assert_array_equal(dh.matrix(0, "a")(x), want)
+        dh.close()
+
+
 def test_spmv_symmetric_layout_rejects_one_ulp_asymmetry():
     from paper_2102_07417_b200.problems import Csr
 
