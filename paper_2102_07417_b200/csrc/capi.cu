@@ -75,6 +75,10 @@ struct DevMat {
     double *uval = nullptr;      // symmetric stencil layout (spmv_symd), nullptr if unused
     int sym_slot = -1;           // its __constant__ pattern-table slot
     double *uval_s = nullptr;    // uniform-width SELL-32 (spmv_sellu), nullptr if unused
+    double *sv_s = nullptr;      // sorted SELL-32 (spmv_sells), nullptr if unused
+    int32_t *sc_s = nullptr, *sb_s = nullptr, *sp_s = nullptr;
+    uint8_t *sw_s = nullptr, *sl_s = nullptr;
+    int s_grid = 0;
     int32_t *ucol_s = nullptr;
     uint8_t *ulen_s = nullptr;
     int uW = 0, u_grid = 0;
@@ -199,6 +203,12 @@ struct amg_handle {
     int small_rows_per_sm = 128;  // below sm_count * this many rows a matrix counts as small
     int patterns = 1;             // stencil-pattern layout for square operators with few row patterns
     int symd_minb = 4;            // fixed-slot 32-wide kernel: min CTAs/SM (register budget) 3, 4 or 5
+    int sells = 1;                // sorted SELL-32 (sigma window below) where natural slices pad > 10%
+    int sells_sigma = 1024;
+    double sells_min_avg = 4.0;   // ... for matrices averaging at least this many entries per row
+    int64_t sells_max_rows = 1 << 20;  // ... and at most this many rows (sorting costs fine-grid rows their gather
+                                       // locality: config-2 G^T_0 85 -> 134 us; coarse A_1 18 -> 13 us)
+    int vec_pipe = 0;             // padded-CSR kernel with the first round's columns fetched one row ahead
     int sellu = 1;                // uniform-width SELL-32 for rows of <= 16 entries padding <= 10% (e.g. FSAI G)
     int fused = 0;                // FSAI steps of large levels as one G/G^T kernel (fsai_fused): bit-identical but
                                   // measured slower on config 2 (294 vs 144 us per level-0 step: the kernels are latency-
@@ -329,6 +339,19 @@ static SpmvSellUFn spmv_sellu_fn(int epi, int W)
 #undef AMG_U
 }
 
+typedef void (*SpmvSellSFn)(const SpmvArgs, const SellSArgs, int);
+
+static SpmvSellSFn spmv_sells_fn(int epi)
+{
+    switch (epi) {
+    case EPI_PLAIN: return spmv_sells<EPI_PLAIN>;
+    case EPI_RESID: return spmv_sells<EPI_RESID>;
+    case EPI_AXPYW: return spmv_sells<EPI_AXPYW>;
+    case EPI_SETW: return spmv_sells<EPI_SETW>;
+    default: return spmv_sells<EPI_ADD>;
+    }
+}
+
 typedef void (*SpmvSellqFn)(const SpmvArgs, const SellArgs, const SellqArgs, int);
 
 static SpmvSellqFn spmv_sellq_fn(int epi, bool pat)
@@ -359,15 +382,17 @@ static SpmvPatFn spmv_pat_fn(int epi)
 
 typedef void (*SpmvVecFn)(const SpmvArgs, const PadArgs, int);
 
-static SpmvVecFn spmv_vec_fn(int epi)
+static SpmvVecFn spmv_vec_fn(int epi, bool pipe = false)
 {
+#define AMG_V(E) return pipe ? spmv_vec<E, true> : spmv_vec<E, false>;
     switch (epi) {
-    case EPI_PLAIN: return spmv_vec<EPI_PLAIN>;
-    case EPI_RESID: return spmv_vec<EPI_RESID>;
-    case EPI_AXPYW: return spmv_vec<EPI_AXPYW>;
-    case EPI_SETW: return spmv_vec<EPI_SETW>;
-    default: return spmv_vec<EPI_ADD>;
+    case EPI_PLAIN: AMG_V(EPI_PLAIN)
+    case EPI_RESID: AMG_V(EPI_RESID)
+    case EPI_AXPYW: AMG_V(EPI_AXPYW)
+    case EPI_SETW: AMG_V(EPI_SETW)
+    default: AMG_V(EPI_ADD)
     }
+#undef AMG_V
 }
 
 typedef void (*SpmvDirectFn)(const SpmvArgs, int);
@@ -652,6 +677,10 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
             TRY(launch_k(h, spmv_symd_fixed_fn(epi, M.sym_fl, h->symd_minb), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
         else
             TRY(launch_k(h, spmv_symd_fn(epi), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
+    } else if (M.sv_s && h->sells) {
+        SellSArgs qa{M.sv_s, M.sc_s, M.sb_s, M.sw_s, M.sp_s, M.sl_s};
+        TRY(launch_k(h, spmv_sells_fn(epi), grid_cap ? std::min(grid_cap, M.s_grid) : M.s_grid, VEC_SPMV_THREADS, 0, a,
+                     qa, (int)M.nrows));
     } else if (M.uval_s && h->sellu) {
         SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW};
         TRY(launch_k(h, spmv_sellu_fn(epi, M.uW), grid_cap ? std::min(grid_cap, M.u_grid) : M.u_grid, VEC_SPMV_THREADS, 0,
@@ -680,7 +709,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
                      DIRECT_THREADS, 0, a, la, (int)M.nrows));
     } else if (M.pstart) {
         PadArgs pa{M.pstart, M.pval, M.pcol};
-        TRY(launch_k(h, spmv_vec_fn(epi), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
+        TRY(launch_k(h, spmv_vec_fn(epi, h->vec_pipe), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
                      pa, (int)M.nrows));
     } else if (h->kernel == 3 && M.nwtiles > 0) {
         SpmvArgs w = a;
@@ -1208,7 +1237,7 @@ void amg_destroy(amg_t *h)
     auto F = [](void *p) { if (p) cudaFree(p); };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s);
+            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s);
             symd_slot_give(h->device, M.sym_slot);
             M.sym_slot = -1;
             halo_free(M.halo);
@@ -1251,6 +1280,11 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "small_rows_per_sm") { h->small_rows_per_sm = (int)value; return AMG_OK; }
     if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
     if (k == "symm") { h->symm = value ? 1 : 0; return AMG_OK; }
+    if (k == "sells") { h->sells = (int)value; return AMG_OK; }
+    if (k == "sells_max_rows") { h->sells_max_rows = value; return AMG_OK; }
+    if (k == "sells_sigma") { h->sells_sigma = (int)value; return AMG_OK; }
+    if (k == "sells_min_avg10") { h->sells_min_avg = value / 10.0; return AMG_OK; }
+    if (k == "vec_pipe") { h->vec_pipe = value ? 1 : 0; return AMG_OK; }
     if (k == "sellu") { h->sellu = value ? 1 : 0; return AMG_OK; }
     if (k == "fused") { h->fused = value ? 1 : 0; return AMG_OK; }
     if (k == "fused_lag_extra") { h->fused_lag_extra = (int)value; return AMG_OK; }
@@ -2012,7 +2046,7 @@ int amg_finalize(amg_t *h)
                     }
                 }
                 int nb = 0;
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_vec_fn(EPI_RESID), VEC_SPMV_THREADS, 0));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_vec_fn(EPI_RESID, h->vec_pipe), VEC_SPMV_THREADS, 0));
                 M.pad_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
                                                                         (int64_t)h->sm_count * std::max(nb, 1)));
                 h->max_grid = std::max(h->max_grid, M.pad_grid);
@@ -2083,6 +2117,84 @@ int amg_finalize(amg_t *h)
                     M.u_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
                                                                           (int64_t)h->sm_count * std::max(nbu, 1)));
                     h->max_grid = std::max(h->max_grid, M.u_grid);
+                }
+            }
+            if (!M.uval && !M.uval_s && h->sells && !longrows && !h->lanes_override && h->sells_sigma >= 32 &&
+                M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm && M.nrows <= h->sells_max_rows &&
+                (double)M.nnz >= h->sells_min_avg * (double)M.nrows) {
+                // sorted SELL-32: taken where natural slices pad > 10% and sorted ones <= 10%
+                const int64_t ns = (M.nrows + 31) / 32;
+                int64_t nat = 0, maxlen = 0;
+                for (int64_t sl = 0; sl < ns; ++sl) {
+                    int w = 0;
+                    for (int64_t r = sl * 32; r < std::min<int64_t>(M.nrows, sl * 32 + 32); ++r) w = std::max(w, off32[r + 1] - off32[r]);
+                    nat += 32 * (int64_t)w;
+                    maxlen = std::max<int64_t>(maxlen, w);
+                }
+                std::vector<int32_t> order(M.nrows);
+                for (int64_t r = 0; r < M.nrows; ++r) order[r] = (int32_t)r;
+                for (int64_t w0 = 0; w0 < M.nrows; w0 += h->sells_sigma) {
+                    const int64_t w1 = std::min<int64_t>(M.nrows, w0 + h->sells_sigma);
+                    std::stable_sort(order.begin() + w0, order.begin() + w1, [&](int32_t x1, int32_t x2) {
+                        return off32[x1 + 1] - off32[x1] > off32[x2 + 1] - off32[x2];
+                    });
+                }
+                std::vector<int32_t> sb(ns + 1);
+                std::vector<uint8_t> sw(ns + 1, 0);
+                int64_t tot = 0;
+                for (int64_t sl = 0; sl < ns; ++sl) {
+                    int w = 0;
+                    for (int64_t p = sl * 32; p < std::min<int64_t>(M.nrows, sl * 32 + 32); ++p)
+                        w = std::max(w, off32[order[p] + 1] - off32[order[p]]);
+                    sb[sl] = (int32_t)tot;
+                    sw[sl] = (uint8_t)w;
+                    tot += 32 * (int64_t)w;
+                }
+                sb[ns] = (int32_t)tot;
+                if (maxlen <= 129 && nat > (int64_t)(1.10 * (double)M.nnz) && tot <= (int64_t)(1.10 * (double)M.nnz) &&
+                    tot < INT32_MAX - 64) {
+                    std::vector<int32_t> col_h(M.nnz);
+                    std::vector<double> val_h(M.nnz);
+                    if (M.nnz) {
+                        CK(cudaMemcpy(col_h.data(), M.col, M.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+                        CK(cudaMemcpy(val_h.data(), M.val, M.nnz * sizeof(double), cudaMemcpyDeviceToHost));
+                    }
+                    std::vector<double> sv(tot + 32, 0.0);
+                    std::vector<int32_t> sc(tot + 32, 0);
+                    std::vector<uint8_t> ln(ns * 32 + 16, 0);
+                    std::vector<int32_t> pm(ns * 32 + 16, 0);
+                    for (int64_t p = 0; p < M.nrows; ++p) {
+                        const int64_t r = order[p], sl = p / 32, l = p % 32;
+                        const int32_t len = off32[r + 1] - off32[r];
+                        ln[p] = (uint8_t)len;
+                        pm[p] = (int32_t)r;
+                        for (int32_t k = 0; k < sw[sl]; ++k) {
+                            const int64_t q = sb[sl] + 32 * (int64_t)k + l;
+                            if (k < len) {
+                                sv[q] = val_h[off32[r] + k];
+                                sc[q] = col_h[off32[r] + k];
+                            } else {
+                                sc[q] = (int32_t)std::min<int64_t>(r, M.ncols - 1);
+                            }
+                        }
+                    }
+                    TRY(dalloc(&M.sv_s, sv.size()));
+                    TRY(dalloc(&M.sc_s, sc.size()));
+                    TRY(dalloc(&M.sb_s, sb.size()));
+                    TRY(dalloc(&M.sw_s, sw.size()));
+                    TRY(dalloc(&M.sp_s, pm.size()));
+                    TRY(dalloc(&M.sl_s, ln.size()));
+                    CK(cudaMemcpy(M.sv_s, sv.data(), sv.size() * sizeof(double), cudaMemcpyHostToDevice));
+                    CK(cudaMemcpy(M.sc_s, sc.data(), sc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                    CK(cudaMemcpy(M.sb_s, sb.data(), sb.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                    CK(cudaMemcpy(M.sw_s, sw.data(), sw.size(), cudaMemcpyHostToDevice));
+                    CK(cudaMemcpy(M.sp_s, pm.data(), pm.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                    CK(cudaMemcpy(M.sl_s, ln.data(), ln.size(), cudaMemcpyHostToDevice));
+                    int nbs = 0;
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbs, (const void *)spmv_sells_fn(EPI_RESID),
+                                                                     VEC_SPMV_THREADS, 0));
+                    M.s_grid = (int)std::max<int64_t>(1, std::min<int64_t>((ns + 7) / 8, (int64_t)h->sm_count * std::max(nbs, 1)));
+                    h->max_grid = std::max(h->max_grid, M.s_grid);
                 }
             }
             const double avg = M.nrows ? (double)M.nnz / (double)M.nrows : 0.0;
@@ -2553,6 +2665,7 @@ int amg_matrix_layout(amg_t *h, int level, int which, int *layout)
     // same precedence as launch_spmv
     *layout = M.ntiles == 0           ? AMG_LAYOUT_EMPTY
               : (M.uval && h->symm)   ? AMG_LAYOUT_SYMD
+              : (M.sv_s && h->sells)   ? AMG_LAYOUT_SELL_SORTED
               : (M.uval_s && h->sellu) ? AMG_LAYOUT_SELL_UNIFORM
               : M.sbeg                ? (M.scol ? AMG_LAYOUT_SELL : AMG_LAYOUT_SELL_PAT)
               : (M.pid && M.pstart)   ? AMG_LAYOUT_PATTERN

@@ -1193,8 +1193,12 @@ struct PadArgs {
     const int32_t *pcol;    // padded columns
 };
 
-template <int EPI>
-__global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_vec(const SpmvArgs a, const PadArgs pa, int nrows)
+// PIPE: software pipeline -- row offsets two rows ahead and the first
+// round's columns (entry 0 and the aligned 8 after it) one row ahead, so a
+// row's first-round value loads and x gathers leave together (fewer CTAs:
+// the prefetched columns cost registers).
+template <int EPI, bool PIPE>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, PIPE ? 3 : 4) spmv_vec(const SpmvArgs a, const PadArgs pa, int nrows)
 {
     __shared__ double red[VEC_SPMV_THREADS / 32];
     pdl_launch();
@@ -1207,15 +1211,44 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_vec(const SpmvArgs a
     double dacc = 0.0;
     int row = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x;
     int nlo = 0, nhi = 0, nps = 0;
+    int len2 = 0, ps2 = 0, nc0 = 0;
+    int4 nca = make_int4(0, 0, 0, 0), ncb = make_int4(0, 0, 0, 0);
+    auto fetch_cols = [&](int ps, int len) {
+        if (len > 0) nc0 = __ldg(pa.pcol + ps);
+        const int4 *c4 = reinterpret_cast<const int4 *>(pa.pcol + ps + 1);
+        nca = len > 1 ? __ldg(c4) : make_int4(0, 0, 0, 0);
+        ncb = len > 5 ? __ldg(c4 + 1) : make_int4(0, 0, 0, 0);
+    };
     if (row < nrows) {
         nlo = __ldg(a.off + row);
         nhi = __ldg(a.off + row + 1);
         nps = __ldg(pa.pstart + row);
     }
+    if constexpr (PIPE) {
+        if (row + nthreads < nrows) {
+            len2 = __ldg(a.off + row + nthreads + 1) - __ldg(a.off + row + nthreads);
+            ps2 = __ldg(pa.pstart + row + nthreads);
+        }
+        if (row < nrows) fetch_cols(nps, nhi - nlo);
+    }
     for (; row < nrows; row += nthreads) {
         const int len = nhi - nlo;
         const int ps = nps;
-        if (row + nthreads < nrows) {
+        int c0 = 0;
+        int4 fca = make_int4(0, 0, 0, 0), fcb = make_int4(0, 0, 0, 0);
+        if constexpr (PIPE) {
+            c0 = nc0;
+            fca = nca;
+            fcb = ncb;
+            nlo = 0;
+            nhi = len2;
+            nps = ps2;
+            if (row + nthreads < nrows) fetch_cols(nps, nhi);
+            if (row + 2 * nthreads < nrows) {
+                len2 = __ldg(a.off + row + 2 * nthreads + 1) - __ldg(a.off + row + 2 * nthreads);
+                ps2 = __ldg(pa.pstart + row + 2 * nthreads);
+            }
+        } else if (row + nthreads < nrows) {
             nlo = __ldg(a.off + row + nthreads);
             nhi = __ldg(a.off + row + nthreads + 1);
             nps = __ldg(pa.pstart + row + nthreads);
@@ -1226,7 +1259,7 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_vec(const SpmvArgs a
         const int n = len - 1;
         double sum = 0.0;
         if (n >= 0 && n <= 128) {
-            const double p0 = prod(__ldg(pa.pval + ps), __ldg(x + __ldg(pa.pcol + ps)));
+            const double p0 = prod(__ldg(pa.pval + ps), __ldg(x + (PIPE ? c0 : __ldg(pa.pcol + ps))));
             const int b1 = ps + 1;  // 16-byte aligned
             const double2 *v2 = reinterpret_cast<const double2 *>(pa.pval + b1);
             const int4 *c4 = reinterpret_cast<const int4 *>(pa.pcol + b1);
@@ -1245,8 +1278,8 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_vec(const SpmvArgs a
             };
             // masked round (entries beyond `cnt` belong to padding / the next row: not used)
             auto round8m = [&](int r, int cnt, double p[8]) {
-                const int4 ca = __ldg(c4 + 2 * r);
-                const int4 cb = cnt > 4 ? __ldg(c4 + 2 * r + 1) : make_int4(0, 0, 0, 0);
+                const int4 ca = (PIPE && r == 0) ? fca : __ldg(c4 + 2 * r);
+                const int4 cb = (PIPE && r == 0) ? fcb : (cnt > 4 ? __ldg(c4 + 2 * r + 1) : make_int4(0, 0, 0, 0));
                 const double2 va = __ldg(v2 + 4 * r);
                 const double2 vb = cnt > 2 ? __ldg(v2 + 4 * r + 1) : make_double2(0.0, 0.0);
                 const double2 vc = cnt > 4 ? __ldg(v2 + 4 * r + 2) : make_double2(0.0, 0.0);
@@ -1842,6 +1875,84 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, FL <= 4 ? 6 : FL <= 9 ? 4 : 
     if (want_dot || a.fin != FIN_NONE) {
         double v2 = block_sum<VEC_SPMV_THREADS>(dacc, red);
         grid_finalize<VEC_SPMV_THREADS>(v2, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
+// ---------------------------------------------------------------- SpMV, sorted SELL-32 (SELL-C-sigma)
+
+// Rows sorted by length (descending) inside windows of sigma rows, then cut
+// into 32-row slices padded to their widest row: slice s holds W_s entries
+// per lane, entry k of slot l at sbeg[s] + 32k + l, original row perm[32s+l].
+// Slices of width <= 16 (most slices of the FSAI transposes) issue every
+// value / column load at once, predicated on the warp-uniform W_s rather
+// than on each row's length, then sum each row over its own length in the
+// reference order; wider slices take the round-by-round path.  The slice
+// metadata (offset, width) and the slot's row / length are fetched one slice
+// ahead.
+struct SellSArgs {
+    const double *val;
+    const int32_t *col;
+    const int32_t *sbeg;   // per slice start
+    const uint8_t *swid;   // per slice width
+    const int32_t *perm;   // slot -> row
+    const uint8_t *slen;   // per slot row length
+};
+
+template <int EPI>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_sells(const SpmvArgs a, const SellSArgs q, int nrows)
+{
+    __shared__ double red[VEC_SPMV_THREADS / 32];
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const int lane = threadIdx.x & 31;
+    const int nslices = (nrows + 31) >> 5;
+    const int wstride = gridDim.x * (VEC_SPMV_THREADS / 32);
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    const double *__restrict__ x = a.x;
+    double dacc = 0.0;
+    int sl = blockIdx.x * (VEC_SPMV_THREADS / 32) + (threadIdx.x >> 5);
+    int nsb = 0, nw = 0, nrow = -1, nlen = 0;
+    auto meta = [&](int s) {
+        nsb = __ldg(q.sbeg + s);
+        nw = __ldg(q.swid + s);
+        const int pos = s * 32 + lane;
+        nrow = pos < nrows ? __ldg(q.perm + pos) : -1;
+        nlen = pos < nrows ? __ldg(q.slen + pos) : 0;
+    };
+    if (sl < nslices) meta(sl);
+    for (; sl < nslices; sl += wstride) {
+        const int sb = nsb, W = nw, row = nrow, len = nlen;
+        if (sl + wstride < nslices) meta(sl + wstride);
+        const double *vb = q.val + sb + lane;
+        const int32_t *cb = q.col + sb + lane;
+        double sum;
+        if (W <= 16) {
+            double p[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) p[k] = (k < W) ? prod(__ldg(vb + 32 * k), __ldg(x + __ldg(cb + 32 * k))) : 0.0;
+            sum = ref_sum_fixed<16>(p, len);
+        } else {
+            auto P = [&](int k) -> double { return prod(__ldg(vb + 32 * k), __ldg(x + __ldg(cb + 32 * k))); };
+            sum = ref_row_sum<false>(P, len);
+        }
+        if (row >= 0) {
+            double bv = 0.0;
+            if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
+            double yv;
+            if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+            else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+            else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+            else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+            else yv = sum;
+            a.y[row] = yv;
+            if (want_dot) dacc = fma(yv, self_dot ? yv : a.dotw[row], dacc);
+        }
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
+        grid_finalize<VEC_SPMV_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
     }
 }
 

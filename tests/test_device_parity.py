@@ -138,6 +138,28 @@ def test_spmv_uniform_sell_bit_identical(width):
         dh.close()
 
 
+@pytest.mark.parametrize("maxlen", [12, 46, 129])
+def test_spmv_sorted_sell_bit_identical(maxlen):
+    # ragged rows (FSAI-transpose-like length spread) on SELL-32 slices sorted
+    # by length inside windows; narrow slices take the all-slots-at-once path
+    from paper_2102_07417_b200.problems import Csr
+
+    rng = np.random.default_rng(maxlen)
+    n = 50000
+    lens = np.minimum(rng.geometric(1.0 / 9.0, n), maxlen)
+    lens[:4] = [0, 1, maxlen, 17]
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    m = Csr(n, n, off, cols, rng.uniform(-1, 1, off[-1]))
+    x = rng.uniform(-1, 1, n)
+    want = O.spmv(m, x)
+    for sells in (1, 0):
+        dh = amg.DeviceHierarchy.from_matrices([m], options={"sells": sells, "symm": 0, "sells_sigma": 16384})
+        assert (dh.layout(0, "a") == "sell_sorted") == bool(sells)
+        np.testing.assert_array_equal(dh.matrix(0, "a")(x), want)
+        dh.close()
+
+
 def test_spmv_symmetric_layout_rejects_one_ulp_asymmetry():
     from paper_2102_07417_b200.problems import Csr
 
