@@ -82,7 +82,7 @@ struct DevMat {
     int32_t *ucol_s = nullptr;
     uint8_t *ulen_s = nullptr;
     int uW = 0, u_grid = 0;
-    int nudiag = 0, sym_grid = 0, sym_fl = 0, symf_grid = 0;  // sym_fl: fixed-slot kernel width (0: none)
+    int nudiag = 0, sym_grid = 0, sym_fl = 0, symf_grid = 0, sym_blocked = 0;  // sym_fl: fixed-slot kernel width (0: none)
     int32_t *pstart = nullptr;   // padded-aligned layout (spmv_vec), nullptr if unused
     double *pval = nullptr;
     int32_t *pcol = nullptr;
@@ -202,6 +202,8 @@ struct amg_handle {
     int long_avg = 128;           // rows averaging more entries run leaf by leaf (spmv_leaves); 0 = off
     int small_rows_per_sm = 128;  // below sm_count * this many rows a matrix counts as small
     int patterns = 1;             // stencil-pattern layout for square operators with few row patterns
+    int symd_blocked = 1;         // symmetric layout stored slice-blocked (32 rows x nu diagonals contiguous)
+    int symd_gminb = 5;           // round-by-round symmetric kernel: min CTAs/SM 5, 6 or 8
     int symd_minb = 4;            // fixed-slot 32-wide kernel: min CTAs/SM (register budget) 3, 4 or 5
     int sells = 1;                // sorted SELL-32 (sigma window below) where natural slices pad > 10%
     int sells_sigma = 1024;
@@ -297,23 +299,28 @@ static SpmvSellFn spmv_sell_fn(int epi, bool pat)
 
 typedef void (*SpmvSymFn)(const SpmvArgs, const SymArgs, int);
 
-static SpmvSymFn spmv_symd_fn(int epi)
+static SpmvSymFn spmv_symd_fn(int epi, int minb = 5, bool blk = false)
 {
+#define AMG_Y(E)                                                                                     \
+    return blk ? spmv_symd<E, 5, true>                                                                \
+               : (minb >= 8 ? spmv_symd<E, 8, false> : minb == 6 ? spmv_symd<E, 6, false> : spmv_symd<E, 5, false>);
     switch (epi) {
-    case EPI_PLAIN: return spmv_symd<EPI_PLAIN>;
-    case EPI_RESID: return spmv_symd<EPI_RESID>;
-    case EPI_AXPYW: return spmv_symd<EPI_AXPYW>;
-    case EPI_SETW: return spmv_symd<EPI_SETW>;
-    default: return spmv_symd<EPI_ADD>;
+    case EPI_PLAIN: AMG_Y(EPI_PLAIN)
+    case EPI_RESID: AMG_Y(EPI_RESID)
+    case EPI_AXPYW: AMG_Y(EPI_AXPYW)
+    case EPI_SETW: AMG_Y(EPI_SETW)
+    default: AMG_Y(EPI_ADD)
     }
+#undef AMG_Y
 }
 
-static SpmvSymFn spmv_symd_fixed_fn(int epi, int fl, int minb = 0)
+static SpmvSymFn spmv_symd_fixed_fn(int epi, int fl, int minb = 0, bool blk = false)
 {
-#define AMG_F(E)                                                                          \
-    return fl <= 8 ? spmv_symd_fixed<E, 8, 6>                                               \
-                   : (minb == 3 ? spmv_symd_fixed<E, 32, 3>                                \
-                                : minb == 5 ? spmv_symd_fixed<E, 32, 5> : spmv_symd_fixed<E, 32, 4>);
+#define AMG_F(E)                                                                                     \
+    return fl <= 8 ? (blk ? spmv_symd_fixed<E, 8, 6, true> : spmv_symd_fixed<E, 8, 6, false>)          \
+                   : blk ? spmv_symd_fixed<E, 32, 4, true>                                            \
+                   : (minb == 3 ? spmv_symd_fixed<E, 32, 3, false>                                    \
+                                : minb == 5 ? spmv_symd_fixed<E, 32, 5, false> : spmv_symd_fixed<E, 32, 4, false>);
     switch (epi) {
     case EPI_PLAIN: AMG_F(EPI_PLAIN)
     case EPI_RESID: AMG_F(EPI_RESID)
@@ -672,11 +679,11 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
                 g = (int)((M.nrows + c - 1) / c);
             }
         }
-        SymArgs sa{M.uval, M.pid, M.sym_slot, chunk};
+        SymArgs sa{M.uval, M.pid, M.sym_slot, chunk, M.sym_blocked ? 32 * M.nudiag : 0};
         if (fx)
-            TRY(launch_k(h, spmv_symd_fixed_fn(epi, M.sym_fl, h->symd_minb), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
+            TRY(launch_k(h, spmv_symd_fixed_fn(epi, M.sym_fl, h->symd_minb, M.sym_blocked), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
         else
-            TRY(launch_k(h, spmv_symd_fn(epi), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
+            TRY(launch_k(h, spmv_symd_fn(epi, h->symd_gminb, M.sym_blocked), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
     } else if (M.sv_s && h->sells) {
         SellSArgs qa{M.sv_s, M.sc_s, M.sb_s, M.sw_s, M.sp_s, M.sl_s};
         TRY(launch_k(h, spmv_sells_fn(epi), grid_cap ? std::min(grid_cap, M.s_grid) : M.s_grid, VEC_SPMV_THREADS, 0, a,
@@ -1290,6 +1297,8 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "fused_lag_extra") { h->fused_lag_extra = (int)value; return AMG_OK; }
     if (k == "symd_fixed") { h->symd_fixed = (int)value; return AMG_OK; }
     if (k == "symd_chunked") { h->symd_chunked = value ? 1 : 0; return AMG_OK; }
+    if (k == "symd_blocked") { h->symd_blocked = value ? 1 : 0; return AMG_OK; }
+    if (k == "symd_gminb") { h->symd_gminb = (int)value; return AMG_OK; }
     if (k == "symd_minb") { h->symd_minb = (int)value; return AMG_OK; }
     if (k == "sell") { h->sell = value ? 1 : 0; return AMG_OK; }
     if (k == "grid_per_sm") { h->grid_per_sm = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
@@ -1605,13 +1614,21 @@ static int build_symd(amg_t *h, DevMat &M, const std::vector<int32_t> &off32, co
     const int64_t npad = ((n + 31) / 32) * 32;
     if ((int64_t)nu * npad + npad >= INT32_MAX - 64) return AMG_OK;
     auto jof = [&](int32_t d) { return (int)(std::lower_bound(up.begin(), up.end(), d) - up.begin()); };
+    int maxlen = 0;
+    for (size_t i = 0; i + 1 < beg.size(); ++i) maxlen = std::max(maxlen, beg[i + 1] - beg[i]);
+    // slice-blocked storage for the round-by-round kernel (27-point: 88 -> 81 us on config 2); the
+    // fixed-slot 7-point kernel keeps one array per diagonal (config 4: 159 vs 171 us)
+    const bool blk = h->symd_blocked && nu <= 63 && !(maxlen <= 8 && h->symd_fixed >= 1);
+    auto sidx = [&](int64_t r, int j) -> size_t {  // storage index of a(r, r + up[j])
+        return blk ? (size_t)((r >> 5) * 32 * nu + 32 * j + (r & 31)) : (size_t)j * npad + r;
+    };
     std::vector<double> uv((size_t)nu * npad, 0.0);
     std::vector<uint8_t> have((size_t)nu * npad, 0);
     for (int64_t r = 0; r < n; ++r)  // upper entries (and the diagonal) first
         for (int32_t k = off32[r]; k < off32[r + 1]; ++k) {
             const int32_t d = col_h[k] - (int32_t)r;
             if (d < 0) continue;
-            const size_t q = (size_t)jof(d) * npad + r;
+            const size_t q = sidx(r, jof(d));
             uv[q] = val_h[k];
             have[q] = 1;
         }
@@ -1619,7 +1636,7 @@ static int build_symd(amg_t *h, DevMat &M, const std::vector<int32_t> &off32, co
         for (int32_t k = off32[r]; k < off32[r + 1]; ++k) {
             const int32_t d = col_h[k] - (int32_t)r;
             if (d >= 0) continue;
-            const size_t q = (size_t)jof(-d) * npad + (r + d);
+            const size_t q = sidx(r + d, jof(-d));
             if (!have[q] || memcmp(&uv[q], &val_h[k], sizeof(double)) != 0) return AMG_OK;
         }
     const int slot = symd_slot_take(h->device);
@@ -1628,22 +1645,22 @@ static int build_symd(amg_t *h, DevMat &M, const std::vector<int32_t> &off32, co
     std::vector<int32_t> bg(SYMD_BEG_MAX, 0);
     for (size_t i = 0; i < rel.size(); ++i) {
         const int32_t d = rel[i];
-        ent[i] = d >= 0 ? make_int2(d, (int)((int64_t)jof(d) * npad)) : make_int2(d, (int)((int64_t)jof(-d) * npad + d));
+        if (blk) ent[i] = d >= 0 ? make_int2(d, jof(d)) : make_int2(d, (int)(((int64_t)d << 6) | jof(-d)));
+        else ent[i] = d >= 0 ? make_int2(d, (int)((int64_t)jof(d) * npad)) : make_int2(d, (int)((int64_t)jof(-d) * npad + d));
     }
     for (size_t i = 0; i < beg.size(); ++i) bg[i] = slot * SYMD_ENT_MAX + beg[i];
     CK(cudaMemcpyToSymbol(c_symd_ent, ent.data(), ent.size() * sizeof(int2), (size_t)slot * SYMD_ENT_MAX * sizeof(int2)));
     CK(cudaMemcpyToSymbol(c_symd_beg, bg.data(), bg.size() * sizeof(int32_t), (size_t)slot * SYMD_BEG_MAX * sizeof(int32_t)));
     M.sym_slot = slot;
+    M.sym_blocked = blk ? 1 : 0;
     TRY(dalloc(&M.uval, uv.size()));
     CK(cudaMemcpy(M.uval, uv.data(), uv.size() * sizeof(double), cudaMemcpyHostToDevice));
     M.nudiag = nu;
     int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_symd_fn(EPI_RESID), VEC_SPMV_THREADS, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_symd_fn(EPI_RESID, h->symd_gminb, blk), VEC_SPMV_THREADS, 0));
     M.sym_grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
                                                              (int64_t)h->sm_count * std::max(nb, 1)));
     h->max_grid = std::max(h->max_grid, M.sym_grid);
-    int maxlen = 0;
-    for (size_t i = 0; i + 1 < beg.size(); ++i) maxlen = std::max(maxlen, beg[i + 1] - beg[i]);
     M.sym_fl = maxlen <= 8 ? 8 : maxlen <= 32 ? 32 : 0;
     if (M.sym_fl) {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_symd_fixed_fn(EPI_RESID, M.sym_fl, h->symd_minb),

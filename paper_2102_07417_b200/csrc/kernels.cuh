@@ -1621,7 +1621,19 @@ struct SymArgs {
     int slot;
     int chunk;  // > 0: CTA b sweeps rows [b*chunk, (b+1)*chunk) in 256-row steps (x and mirror lines
                 // reused from L1 by the next step); 0: grid-stride over 256-row blocks
+    int w32;    // blocked storage (> 0): the nu diagonals of each 32-row slice contiguous,
+                // uval[(i/32)*w32 + 32 j + i%32] with w32 = 32 nu; table entry y = (dsrc << 6) | j
 };
+
+// value index of a pattern entry {rel, y}: diagonal-major (w32 == 0: y = voff)
+// or slice-blocked (y = (row offset of the stored copy) << 6 | diagonal)
+template <bool BLK>
+__device__ __forceinline__ int symd_vidx(int row, int y, int w32)
+{
+    if constexpr (!BLK) return row + y;
+    const int r2 = row + (y >> 6);
+    return (r2 >> 5) * w32 + ((y & 63) << 5) + (r2 & 31);
+}
 
 // reference row sum of P(0..len-1): p0 + numpy pairwise(p1..), as spmv_sell
 template <bool LONG, class PF>
@@ -1666,8 +1678,8 @@ __device__ __forceinline__ double ref_row_sum(const PF &P, int len)
     return sum;
 }
 
-template <int EPI>
-__global__ void __launch_bounds__(VEC_SPMV_THREADS, 5) spmv_symd(const SpmvArgs a, const SymArgs sa, int nrows)
+template <int EPI, int MINB, bool BLK>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, MINB) spmv_symd(const SpmvArgs a, const SymArgs sa, int nrows)
 {
     __shared__ double red[VEC_SPMV_THREADS / 32];
     pdl_launch();
@@ -1692,7 +1704,7 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, 5) spmv_symd(const SpmvArgs 
         const int len = c_symd_beg[bbase + pid + 1] - rb;
         auto P = [&](int k) -> double {
             const int2 q = c_symd_ent[rb + k];
-            return prod(__ldg(uv + (row + q.y)), __ldg(x + (row + q.x)));
+            return prod(__ldg(uv + symd_vidx<BLK>(row, q.y, sa.w32)), __ldg(x + (row + q.x)));
         };
         const double sum = ref_row_sum<false>(P, len);  // pattern rows have <= 129 entries
         double yv;
@@ -1755,7 +1767,7 @@ __device__ __forceinline__ double ref_sum_fixed(const double (&p)[FL], int len)
     return len > 0 ? add(p[0], res) : 0.0;
 }
 
-template <int EPI, int FL, int MINB>
+template <int EPI, int FL, int MINB, bool BLK>
 __global__ void __launch_bounds__(VEC_SPMV_THREADS, MINB) spmv_symd_fixed(const SpmvArgs a, const SymArgs sa,
                                                                                      int nrows)
 {
@@ -1789,7 +1801,7 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, MINB) spmv_symd_fixed(const 
             p[k] = 0.0;
             if (k < len) {
                 const int2 q = c_symd_ent[rb + k];
-                p[k] = prod(__ldg(uv + (row + q.y)), __ldg(x + (row + q.x)));
+                p[k] = prod(__ldg(uv + symd_vidx<BLK>(row, q.y, sa.w32)), __ldg(x + (row + q.x)));
             }
         }
         const double sum = ref_sum_fixed<FL>(p, len);
