@@ -206,7 +206,9 @@ struct amg_handle {
     int symd_gminb = 5;           // round-by-round symmetric kernel: min CTAs/SM 5, 6 or 8
     int symd_minb = 4;            // fixed-slot 32-wide kernel: min CTAs/SM (register budget) 3, 4 or 5
     int sells = 1;                // sorted SELL-32 (sigma window below) where natural slices pad > 10%
-    int sells_sigma = 1024;
+    int sells_sigma = 128;
+    int sells_plen = 1;           // sorted SELL: predicate slot loads on the row length (padding moves no bytes)
+    int sells_max_pad = 60;       // % padding allowed for the sorted layout (padding slots are skipped with sells_plen)
     double sells_min_avg = 4.0;   // ... for matrices averaging at least this many entries per row
     int64_t sells_max_rows = 1 << 20;  // ... and at most this many rows (sorting costs fine-grid rows their gather
                                        // locality: config-2 G^T_0 85 -> 134 us; coarse A_1 18 -> 13 us)
@@ -235,6 +237,7 @@ struct amg_handle {
     int tail_stage = 0;          // stage tail matrices in smem (measured slower on B200: the big smem
                                  // footprint delays the cluster launch; streamed from L2 by default)
     int cluster = 16;
+    int tail_prefetch = 1;        // tail kernel prefetches its streamed matrices into L2 before griddepcontrol.wait
     int tail_level = 0;  // 0 = disabled
     TailOp *tail_ops = nullptr;
     TailMat *tail_mats = nullptr;
@@ -348,15 +351,17 @@ static SpmvSellUFn spmv_sellu_fn(int epi, int W)
 
 typedef void (*SpmvSellSFn)(const SpmvArgs, const SellSArgs, int);
 
-static SpmvSellSFn spmv_sells_fn(int epi)
+static SpmvSellSFn spmv_sells_fn(int epi, bool plen = false)
 {
+#define AMG_S2(E) return plen ? spmv_sells<E, true> : spmv_sells<E, false>;
     switch (epi) {
-    case EPI_PLAIN: return spmv_sells<EPI_PLAIN>;
-    case EPI_RESID: return spmv_sells<EPI_RESID>;
-    case EPI_AXPYW: return spmv_sells<EPI_AXPYW>;
-    case EPI_SETW: return spmv_sells<EPI_SETW>;
-    default: return spmv_sells<EPI_ADD>;
+    case EPI_PLAIN: AMG_S2(EPI_PLAIN)
+    case EPI_RESID: AMG_S2(EPI_RESID)
+    case EPI_AXPYW: AMG_S2(EPI_AXPYW)
+    case EPI_SETW: AMG_S2(EPI_SETW)
+    default: AMG_S2(EPI_ADD)
     }
+#undef AMG_S2
 }
 
 typedef void (*SpmvSellqFn)(const SpmvArgs, const SellArgs, const SellqArgs, int);
@@ -686,7 +691,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
             TRY(launch_k(h, spmv_symd_fn(epi, h->symd_gminb, M.sym_blocked), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
     } else if (M.sv_s && h->sells) {
         SellSArgs qa{M.sv_s, M.sc_s, M.sb_s, M.sw_s, M.sp_s, M.sl_s};
-        TRY(launch_k(h, spmv_sells_fn(epi), grid_cap ? std::min(grid_cap, M.s_grid) : M.s_grid, VEC_SPMV_THREADS, 0, a,
+        TRY(launch_k(h, spmv_sells_fn(epi, h->sells_plen), grid_cap ? std::min(grid_cap, M.s_grid) : M.s_grid, VEC_SPMV_THREADS, 0, a,
                      qa, (int)M.nrows));
     } else if (M.uval_s && h->sellu) {
         SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW};
@@ -787,6 +792,7 @@ static CoarseArgs coarse_args(const amg_t *h)
     c.dinv = h->dinv;
     c.LU = h->LU;
     c.piv = h->piv;
+    c.prefetch = h->tail_prefetch;
     return c;
 }
 
@@ -1289,6 +1295,8 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "symm") { h->symm = value ? 1 : 0; return AMG_OK; }
     if (k == "sells") { h->sells = (int)value; return AMG_OK; }
     if (k == "sells_max_rows") { h->sells_max_rows = value; return AMG_OK; }
+    if (k == "sells_plen") { h->sells_plen = value ? 1 : 0; return AMG_OK; }
+    if (k == "sells_max_pad") { h->sells_max_pad = (int)value; return AMG_OK; }
     if (k == "sells_sigma") { h->sells_sigma = (int)value; return AMG_OK; }
     if (k == "sells_min_avg10") { h->sells_min_avg = value / 10.0; return AMG_OK; }
     if (k == "vec_pipe") { h->vec_pipe = value ? 1 : 0; return AMG_OK; }
@@ -1297,6 +1305,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "fused_lag_extra") { h->fused_lag_extra = (int)value; return AMG_OK; }
     if (k == "symd_fixed") { h->symd_fixed = (int)value; return AMG_OK; }
     if (k == "symd_chunked") { h->symd_chunked = value ? 1 : 0; return AMG_OK; }
+    if (k == "tail_prefetch") { h->tail_prefetch = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "symd_blocked") { h->symd_blocked = value ? 1 : 0; return AMG_OK; }
     if (k == "symd_gminb") { h->symd_gminb = (int)value; return AMG_OK; }
     if (k == "symd_minb") { h->symd_minb = (int)value; return AMG_OK; }
@@ -2168,7 +2177,8 @@ int amg_finalize(amg_t *h)
                     tot += 32 * (int64_t)w;
                 }
                 sb[ns] = (int32_t)tot;
-                if (maxlen <= 129 && nat > (int64_t)(1.10 * (double)M.nnz) && tot <= (int64_t)(1.10 * (double)M.nnz) &&
+                if (maxlen <= 129 && nat > (int64_t)(1.10 * (double)M.nnz) &&
+                    tot <= (int64_t)((1.0 + h->sells_max_pad / 100.0) * (double)M.nnz) &&
                     tot < INT32_MAX - 64) {
                     std::vector<int32_t> col_h(M.nnz);
                     std::vector<double> val_h(M.nnz);
@@ -2208,7 +2218,7 @@ int amg_finalize(amg_t *h)
                     CK(cudaMemcpy(M.sp_s, pm.data(), pm.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
                     CK(cudaMemcpy(M.sl_s, ln.data(), ln.size(), cudaMemcpyHostToDevice));
                     int nbs = 0;
-                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbs, (const void *)spmv_sells_fn(EPI_RESID),
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbs, (const void *)spmv_sells_fn(EPI_RESID, h->sells_plen),
                                                                      VEC_SPMV_THREADS, 0));
                     M.s_grid = (int)std::max<int64_t>(1, std::min<int64_t>((ns + 7) / 8, (int64_t)h->sm_count * std::max(nbs, 1)));
                     h->max_grid = std::max(h->max_grid, M.s_grid);

@@ -1910,7 +1910,7 @@ struct SellSArgs {
     const uint8_t *slen;   // per slot row length
 };
 
-template <int EPI>
+template <int EPI, bool PLEN>
 __global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_sells(const SpmvArgs a, const SellSArgs q, int nrows)
 {
     __shared__ double red[VEC_SPMV_THREADS / 32];
@@ -1943,7 +1943,8 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_sells(const SpmvArgs
         if (W <= 16) {
             double p[16];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) p[k] = (k < W) ? prod(__ldg(vb + 32 * k), __ldg(x + __ldg(cb + 32 * k))) : 0.0;
+            for (int k = 0; k < 16; ++k)  // PLEN: padding slots are not loaded (no bytes for padding)
+                p[k] = (k < (PLEN ? len : W)) ? prod(__ldg(vb + 32 * k), __ldg(x + __ldg(cb + 32 * k))) : 0.0;
             sum = ref_sum_fixed<16>(p, len);
         } else {
             auto P = [&](int k) -> double { return prod(__ldg(vb + 32 * k), __ldg(x + __ldg(cb + 32 * k))); };
@@ -2614,6 +2615,7 @@ struct CoarseArgs {
     const double *dinv;
     const double *LU;
     const int32_t *piv;
+    int prefetch;  // tail kernel: L2-prefetch the streamed matrices before waiting on the predecessor
 };
 
 __global__ void __launch_bounds__(COARSE_THREADS) coarse_solve_k(const CoarseArgs c, const double *y, double *z,
@@ -2851,6 +2853,26 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
         for (int k = threadIdx.x; k < nk; k += blockDim.x) {
             cs[k] = M.col[k0 + k];
             vs[k] = M.val[k0 + k];
+        }
+    }
+    if (c.prefetch) {
+        // pull this CTA's share of the streamed matrices into L2 while the predecessor
+        // drains: the level-0 sweeps evicted them, and 16 SMs alone fetch them from HBM slowly
+        for (int m = 0; m < nmats; ++m) {
+            const TailMat M = mats[m];
+            if (M.staged) continue;
+            const int r0 = splits[M.split + rank], r1 = splits[M.split + rank + 1];
+            if (r1 <= r0) continue;
+            const int k0 = M.off[r0], k1 = M.off[r1];
+            const char *pv = reinterpret_cast<const char *>(M.val + k0);
+            const char *pc = reinterpret_cast<const char *>(M.col + k0);
+            const char *po = reinterpret_cast<const char *>(M.off + r0);
+            for (int i = threadIdx.x * 128; i < (k1 - k0) * 8; i += blockDim.x * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pv + i));
+            for (int i = threadIdx.x * 128; i < (k1 - k0) * 4; i += blockDim.x * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pc + i));
+            for (int i = threadIdx.x * 128; i < (r1 - r0 + 1) * 4; i += blockDim.x * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(po + i));
         }
     }
     __syncthreads();
