@@ -237,6 +237,7 @@ struct amg_handle {
     int tail_stage = 0;          // stage tail matrices in smem (measured slower on B200: the big smem
                                  // footprint delays the cluster launch; streamed from L2 by default)
     int cluster = 16;
+    int coarse_pipe = 1;          // pipelined per-warp Cholesky substitution
     int tail_prefetch = 1;        // tail kernel prefetches its streamed matrices into L2 before griddepcontrol.wait
     int tail_level = 0;  // 0 = disabled
     TailOp *tail_ops = nullptr;
@@ -793,6 +794,7 @@ static CoarseArgs coarse_args(const amg_t *h)
     c.LU = h->LU;
     c.piv = h->piv;
     c.prefetch = h->tail_prefetch;
+    c.pipe = h->coarse_pipe;
     return c;
 }
 
@@ -1305,6 +1307,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "fused_lag_extra") { h->fused_lag_extra = (int)value; return AMG_OK; }
     if (k == "symd_fixed") { h->symd_fixed = (int)value; return AMG_OK; }
     if (k == "symd_chunked") { h->symd_chunked = value ? 1 : 0; return AMG_OK; }
+    if (k == "coarse_pipe") { h->coarse_pipe = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "tail_prefetch") { h->tail_prefetch = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "symd_blocked") { h->symd_blocked = value ? 1 : 0; return AMG_OK; }
     if (k == "symd_gminb") { h->symd_gminb = (int)value; return AMG_OK; }

@@ -2582,6 +2582,101 @@ __device__ void chol_solve_cta(int n, const double *__restrict__ L, const double
     }
 }
 
+// Pipelined variant (n <= 32 * warps, <= 16 blocks): warp w owns rows
+// [32w, 32w + 32).  Forward: it folds in the solved chunks 0..w-1 as each one
+// is published (smem flag), then runs its own 32-step chain and publishes;
+// backward mirrors it from the last chunk down.  The critical path is the
+// chain of diagonal blocks alone (no CTA-wide barrier and GEMV between
+// blocks): n = 188 takes ~1/3 of the blocked schedule.  Same arithmetic per
+// entry (different association of the updates, as dtrsm's blocking differs
+// from both).  `v` holds b on entry and z on exit; ends with __syncthreads.
+__device__ void chol_solve_pipe(int n, const double *__restrict__ L, const double *__restrict__ dinv, double *v,
+                                int nap = 0)
+{
+    __shared__ int s_done[2][16];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nblk = (n + 31) / 32;
+    if (threadIdx.x < 32) {
+        s_done[0][lane & 15] = 0;
+        s_done[1][lane & 15] = 0;
+    }
+    __syncthreads();
+    if (warp < nblk) {
+        volatile int *fdone = s_done[0], *bdone = s_done[1];
+        const int jb = warp * 32, nb = min(32, n - jb);
+        const int i = jb + lane;
+        const bool live = lane < nb;
+        const double di = live ? dinv[i] : 0.0;
+        const double *Li = L + tri(live ? i : jb);
+        // the own diagonal block's row segment (forward) and column segment (backward) in
+        // registers before any wait: the chains then run shuffle -> FMA only
+        double Lr[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) Lr[c] = (c < lane && live) ? Li[jb + c] : 0.0;
+        // forward: L y = b
+        double vi = live ? v[i] : 0.0;
+        for (int cb = 0; cb < warp; ++cb) {
+            while (fdone[cb] == 0)
+                if (nap) __nanosleep(nap);
+            __syncwarp();
+            const int c0 = cb * 32;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+            for (int c = 0; c < 32; c += 4) {
+                a0 = fma(Li[c0 + c], v[c0 + c], a0);
+                a1 = fma(Li[c0 + c + 1], v[c0 + c + 1], a1);
+                a2 = fma(Li[c0 + c + 2], v[c0 + c + 2], a2);
+                a3 = fma(Li[c0 + c + 3], v[c0 + c + 3], a3);
+            }
+            if (live) vi -= (a0 + a1) + (a2 + a3);
+        }
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {  // lanes >= nb are inert: no live lane reads them
+            const double vc = __shfl_sync(0xffffffffu, vi * di, c);
+            vi = (lane == c) ? vc : vi;
+            vi = (lane > c) ? fma(-Lr[c], vc, vi) : vi;
+        }
+        if (live) v[i] = vi;
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) fdone[warp] = 1;
+        double Lc[32];  // L^T[i][jb + c] = L[jb + c][i], loaded before the backward waits
+#pragma unroll
+        for (int c = 0; c < 32; ++c) Lc[c] = (c > lane && c < nb) ? L[tri(jb + c) + i] : 0.0;
+        // backward: L^T z = y
+        for (int cb = nblk - 1; cb > warp; --cb) {
+            while (bdone[cb] == 0)
+                if (nap) __nanosleep(nap);
+            __syncwarp();
+            const int c0 = cb * 32, cn = min(32, n - c0);
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            if (cn == 32) {
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {
+                    a0 = fma(L[tri(c0 + c) + i], v[c0 + c], a0);
+                    a1 = fma(L[tri(c0 + c + 1) + i], v[c0 + c + 1], a1);
+                    a2 = fma(L[tri(c0 + c + 2) + i], v[c0 + c + 2], a2);
+                    a3 = fma(L[tri(c0 + c + 3) + i], v[c0 + c + 3], a3);
+                }
+            } else {
+                for (int c = 0; c < cn; ++c) a0 = fma(L[tri(c0 + c) + i], v[c0 + c], a0);
+            }
+            if (live) vi -= (a0 + a1) + (a2 + a3);
+        }
+#pragma unroll
+        for (int c = 31; c >= 0; --c) {
+            const double zc = __shfl_sync(0xffffffffu, vi * di, c);
+            vi = (lane == c) ? zc : vi;
+            vi = (lane < c) ? fma(-Lc[c], zc, vi) : vi;
+        }
+        if (live) v[i] = vi;
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) bdone[warp] = 1;
+    }
+    __syncthreads();
+}
+
 // LU (getrs, no transpose): b <- P b ; L (unit) y = b ; U z = y.  LU full n x n row-major.
 __device__ void lu_solve_cta(int n, const double *__restrict__ LU, const int32_t *__restrict__ piv, double *v)
 {
@@ -2616,6 +2711,7 @@ struct CoarseArgs {
     const double *LU;
     const int32_t *piv;
     int prefetch;  // tail kernel: L2-prefetch the streamed matrices before waiting on the predecessor
+    int pipe;      // Cholesky: pipelined per-warp substitution (chol_solve_pipe)
 };
 
 __global__ void __launch_bounds__(COARSE_THREADS) coarse_solve_k(const CoarseArgs c, const double *y, double *z,
@@ -2648,7 +2744,8 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_solve_k(const CoarseArg
     if (!gate_open(gate1, nullptr)) return;
     for (int i = threadIdx.x; i < n; i += blockDim.x) v[i] = y[i];
     __syncthreads();
-    if (c.kind == 0) chol_solve_cta(n, L, D, MN, v);
+    if (c.kind == 0 && c.pipe && n <= 32 * (int)(blockDim.x / 32) && n <= 512) chol_solve_pipe(n, L, D, v, c.pipe > 1 ? c.pipe : 0);
+    else if (c.kind == 0) chol_solve_cta(n, L, D, MN, v);
     else lu_solve_cta(n, c.LU, c.piv, v);
     double acc = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -2919,7 +3016,8 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
             double *v = sh;
             for (int r = threadIdx.x; r < c.n; r += blockDim.x) v[r] = __ldcg(o.x + r);
             __syncthreads();
-            if (c.kind == 0) chol_solve_cta(c.n, L, D, c.staged ? nullptr : MN, v);
+            if (c.kind == 0 && c.pipe && c.n <= 32 * (int)(blockDim.x / 32) && c.n <= 512) chol_solve_pipe(c.n, L, D, v, c.pipe > 1 ? c.pipe : 0);
+            else if (c.kind == 0) chol_solve_cta(c.n, L, D, c.staged ? nullptr : MN, v);
             else lu_solve_cta(c.n, c.LU, c.piv, v);
             for (int r = threadIdx.x; r < c.n; r += blockDim.x) o.y[r] = v[r];
         }
