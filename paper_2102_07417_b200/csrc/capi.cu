@@ -124,6 +124,8 @@ struct LevelD {
         unsigned *bcnt = nullptr;
         unsigned *ctr = nullptr;
         double *upart = nullptr;
+        uint16_t *gt16 = nullptr;  // warp-specialised kernel (fsai_ws): G^T as (k << 8 | offset id)
+        int slot = -1, ws_grid = 0;
         int W = 0, nunits = 0, nblk = 0, lag = 0, reach = 0, grid = 0;
     } fz;
 };
@@ -217,6 +219,7 @@ struct amg_handle {
     int fused = 0;                // FSAI steps of large levels as one G/G^T kernel (fsai_fused): bit-identical but
                                   // measured slower on config 2 (294 vs 144 us per level-0 step: the kernels are latency-
                                   // bound, fusing serialises G's and G^T's dependent loads per warp)
+    int fused_wa = 4;             // fsai_ws: G warps per CTA of 8 (the rest compute G^T)
     int fused_lag_extra = 0;      // extra ticket lag (0 = one grid)
     int symd_chunked = 0;         // symmetric kernels: contiguous row chunk per CTA (measured slower than grid-stride)
     int symd_fixed = 1;           // fixed-slot symmetric kernel: 1 rows <= 8 entries (7-point), 2 also <= 32 (27-point:
@@ -363,6 +366,14 @@ static SpmvSellSFn spmv_sells_fn(int epi, bool plen = false)
     default: AMG_S2(EPI_ADD)
     }
 #undef AMG_S2
+}
+
+typedef void (*FusedWsFn)(const FusedWsArgs);
+
+static FusedWsFn fsai_ws_fn(bool set, int wa)
+{
+    if (set) return wa <= 2 ? fsai_ws<EPI_SETW, 2> : wa <= 3 ? fsai_ws<EPI_SETW, 3> : wa <= 4 ? fsai_ws<EPI_SETW, 4> : fsai_ws<EPI_SETW, 5>;
+    return wa <= 2 ? fsai_ws<EPI_AXPYW, 2> : wa <= 3 ? fsai_ws<EPI_AXPYW, 3> : wa <= 4 ? fsai_ws<EPI_AXPYW, 4> : fsai_ws<EPI_AXPYW, 5>;
 }
 
 typedef void (*SpmvSellqFn)(const SpmvArgs, const SellArgs, const SellqArgs, int);
@@ -880,7 +891,34 @@ static int enqueue_smooth(amg_t *h, int k, const double *b, double *x, int steps
             fa.ctl = h->ctl;
             fa.gate1 = g1;
             fa.gate2 = nullptr;
-            TRY(launch_k(h, set ? fsai_fused<EPI_SETW> : fsai_fused<EPI_AXPYW>, L.fz.grid, FUSED_THREADS, 0, fa));
+            if (h->fused >= 2 && L.fz.gt16) {
+                FusedWsArgs wa{};
+                wa.gval = L.fz.gval;
+                wa.gcol = L.fz.gcol;
+                wa.glen = L.fz.glen;
+                wa.tstart = L.fz.tstart;
+                wa.gt16 = L.fz.gt16;
+                wa.y = src;
+                wa.t = L.t;
+                wa.x = x;
+                wa.omega = L.omega;
+                wa.nrows = (int)L.n;
+                wa.W = L.fz.W;
+                wa.nunits = L.fz.nunits;
+                wa.nblk = L.fz.nblk;
+                wa.reach = L.fz.reach;
+                wa.slot = L.fz.slot;
+                wa.bcnt = L.fz.bcnt;
+                wa.ctr = L.fz.ctr;
+                wa.upart = L.fz.upart;
+                wa.dotw = dw;
+                wa.fin = kfin(h, f);
+                wa.ctl = h->ctl;
+                wa.gate1 = g1;
+                TRY(launch_k(h, fsai_ws_fn(set, h->fused_wa), L.fz.ws_grid, FUSED_THREADS, 0, wa));
+            } else {
+                TRY(launch_k(h, set ? fsai_fused<EPI_SETW> : fsai_fused<EPI_AXPYW>, L.fz.grid, FUSED_THREADS, 0, fa));
+            }
             TRY(post_fin(h, f, g1));
         } else if (L.sm_kind == AMG_SMOOTHER_FSAI) {
             TRY(launch_spmv(h, L.m[AMG_G], src, L.t, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, g1, nullptr));
@@ -1258,7 +1296,9 @@ void amg_destroy(amg_t *h)
             halo_free(M.halo);
         }
         F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
-        F(L.fz.gval); F(L.fz.gcol); F(L.fz.glen); F(L.fz.tstart); F(L.fz.tq); F(L.fz.bcnt); F(L.fz.ctr); F(L.fz.upart);
+        F(L.fz.gval); F(L.fz.gcol); F(L.fz.glen); F(L.fz.tstart); F(L.fz.tq); F(L.fz.bcnt); F(L.fz.ctr); F(L.fz.upart); F(L.fz.gt16);
+        symd_slot_give(h->device, L.fz.slot);
+        L.fz.slot = -1;
     }
     F(h->Lp); F(h->LU); F(h->dinv); F(h->binv); F(h->tail_ops); F(h->tail_mats); F(h->tail_splits); F(h->piv); F(h->partials); F(h->ticket); F(h->ctl);
     F(h->b); F(h->x); F(h->r); F(h->z); F(h->p); F(h->q); F(h->tmp_in); F(h->tmp_out); F(h->hist);
@@ -1303,7 +1343,8 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "sells_min_avg10") { h->sells_min_avg = value / 10.0; return AMG_OK; }
     if (k == "vec_pipe") { h->vec_pipe = value ? 1 : 0; return AMG_OK; }
     if (k == "sellu") { h->sellu = value ? 1 : 0; return AMG_OK; }
-    if (k == "fused") { h->fused = value ? 1 : 0; return AMG_OK; }
+    if (k == "fused") { h->fused = (int)value; return AMG_OK; }
+    if (k == "fused_wa") { h->fused_wa = (int)value; return AMG_OK; }
     if (k == "fused_lag_extra") { h->fused_lag_extra = (int)value; return AMG_OK; }
     if (k == "symd_fixed") { h->symd_fixed = (int)value; return AMG_OK; }
     if (k == "symd_chunked") { h->symd_chunked = value ? 1 : 0; return AMG_OK; }
@@ -1749,6 +1790,27 @@ static int build_fused(amg_t *h)
                 reach = std::max<int64_t>(reach, r - i);
             }
         if (!ok) continue;
+        // 2-byte G^T entries for fsai_ws: G offset ids (<= 256 distinct) and positions k < 256
+        std::vector<uint16_t> g16;
+        std::vector<int32_t> rels;
+        if (h->fused >= 2 && W <= 16) {
+            std::vector<int32_t> all(nnz);
+            for (int64_t r = 0; r < n; ++r)
+                for (int32_t e = go[r]; e < go[r + 1]; ++e) all[e] = r - gc[e];  // j - i >= 0
+            rels = all;
+            std::sort(rels.begin(), rels.end());
+            rels.erase(std::unique(rels.begin(), rels.end()), rels.end());
+            if (rels.size() <= 256) {
+                g16.resize(nnz > 0 ? nnz : 1);
+                std::vector<int32_t> fill2(cnt.begin(), cnt.end() - 1);
+                for (int64_t r = 0; r < n; ++r)
+                    for (int32_t e = go[r]; e < go[r + 1]; ++e) {
+                        const int32_t i = gc[e];
+                        const int id = (int)(std::lower_bound(rels.begin(), rels.end(), (int32_t)(r - i)) - rels.begin());
+                        g16[fill2[i]++] = (uint16_t)(((e - go[r]) << 8) | id);
+                    }
+            }
+        }
         auto &F = L.fz;
         F.W = W;
         F.nunits = (int)((n + 31) / 32);
@@ -1769,6 +1831,21 @@ static int build_fused(amg_t *h)
         CK(cudaMemcpy(F.glen, ln.data(), ln.size(), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(F.tstart, cnt.data(), ((size_t)n + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(F.tq, tq.data(), tq.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        if (!g16.empty()) {
+            const int slot = symd_slot_take(h->device);
+            if (slot >= 0) {
+                std::vector<int32_t> tab(256, 0);
+                for (size_t q = 0; q < rels.size(); ++q) tab[q] = -rels[q];  // j = i - c_gt_rel[id]
+                CK(cudaMemcpyToSymbol(c_gt_rel, tab.data(), 256 * sizeof(int32_t), (size_t)slot * 256 * sizeof(int32_t)));
+                TRY(dalloc(&F.gt16, g16.size()));
+                CK(cudaMemcpy(F.gt16, g16.data(), g16.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+                F.slot = slot;
+                int occw = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occw, (const void *)fsai_ws_fn(false, h->fused_wa),
+                                                                 FUSED_THREADS, 0));
+                F.ws_grid = std::max(1, std::min((F.nunits + 7) / 8, std::max(occw, 1) * h->sm_count));  // one resident wave
+            }
+        }
         F.on = true;
     }
     return AMG_OK;

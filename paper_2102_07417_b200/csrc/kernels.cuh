@@ -2115,6 +2115,146 @@ __global__ void __launch_bounds__(FUSED_THREADS, 4) fsai_fused(const FusedArgs a
     }
 }
 
+// ---------------------------------------------------------------- FSAI step, warp-specialised G / G^T
+
+// The same step as fsai_fused with the two halves on DIFFERENT warps, so
+// their dependent load chains overlap instead of adding up: in every CTA,
+// warps [0, WA) stream t = G y over 32-row units (uniform SELL-32 G, next
+// row's columns fetched one unit ahead) and count each unit into its 256-row
+// block's completion counter (release); warps [WA, 8) compute the G^T rows of
+// their units once every block holding a G row they read is complete
+// (acquire).  G^T is stored as 2 bytes per entry: the G offset id (column
+// j = i - rel[id], rel in __constant__) and the position k of G(j, i) in G
+// row j, so its value gval[(j/32)*32W + 32k + j%32] and t_j come from L2,
+// where the G warps left them.  HBM per step: G (12 B/entry) + 2 B/entry +
+// y, x.  Reference order throughout (bit-identical to G then G^T).  Only the
+// G^T warps wait, only on G warps, which never wait; the grid is one
+// resident wave, so every unit's producer is running.  Dot partials per unit.
+__constant__ int32_t c_gt_rel[SYMD_SLOTS][256];
+
+struct FusedWsArgs {
+    const double *gval;
+    const int32_t *gcol;
+    const uint8_t *glen;
+    const int32_t *tstart;   // G^T rows: CSR starts into gt16
+    const uint16_t *gt16;    // (k << 8) | offset id
+    const double *y;
+    double *t;
+    double *x;
+    double omega;
+    int nrows, W, nunits, nblk, reach, slot;
+    unsigned *bcnt;
+    unsigned *ctr;           // [1] CTAs done, [2] generation
+    double *upart;
+    const double *dotw;
+    int fin;
+    PcgCtl *ctl;
+    const int *gate1;
+    const int *gate2;
+};
+
+template <int EPI, int WA>
+__global__ void __launch_bounds__(FUSED_THREADS, 4) fsai_ws(const FusedWsArgs a)
+{
+    __shared__ int s_last;
+    __shared__ double red[FUSED_THREADS / 32];
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const unsigned gen = *(volatile unsigned *)(a.ctr + 2) + 1u;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int W32 = 32 * a.W;
+    if (warp < WA) {  // ---- G warps: t = G y
+        const int na = gridDim.x * WA;
+        int u = blockIdx.x * WA + warp;
+        constexpr int FL = 16;
+        int c[FL];
+        int len = 0;
+        auto fetch = [&](int uu) {
+            const int r = uu * 32 + lane;
+            const int base = uu * W32 + lane;
+            len = r < a.nrows ? __ldg(a.glen + r) : 0;
+#pragma unroll
+            for (int k = 0; k < FL; ++k) c[k] = (k < a.W) ? __ldg(a.gcol + base + 32 * k) : 0;
+        };
+        if (u < a.nunits) fetch(u);
+        for (; u < a.nunits; u += na) {
+            const int row = u * 32 + lane;
+            const int base = u * W32 + lane;
+            double p[FL];
+#pragma unroll
+            for (int k = 0; k < FL; ++k) p[k] = (k < a.W) ? prod(__ldg(a.gval + base + 32 * k), __ldg(a.y + c[k])) : 0.0;
+            const int clen = len;
+            if (u + na < a.nunits) fetch(u + na);
+            if (row < a.nrows) a.t[row] = ref_sum_fixed<FL>(p, clen);
+            __syncwarp();
+            if (lane == 0) red_release_gpu_add(a.bcnt + (u >> 3), 1u);
+        }
+    } else {  // ---- G^T warps: x = EPI(w * G^T t)
+        const int nb = gridDim.x * (8 - WA);
+        const bool want_dot = a.dotw != nullptr;
+        const bool self_dot = a.dotw == a.x;
+        const int slot = a.slot;
+        int ready = -1;
+        for (int u = blockIdx.x * (8 - WA) + (warp - WA); u < a.nunits; u += nb) {
+            const int need = min(a.nblk - 1, (u * 32 + 31 + a.reach) >> 8);
+            while (ready < need) {
+                const int b = ready + 1 + lane;
+                if (b <= need) {
+                    const unsigned full = (b == a.nblk - 1) ? (unsigned)(a.nunits - 8 * b) : 8u;
+                    while (ld_acquire_gpu_u32(a.bcnt + b) < full * gen) __nanosleep(32);
+                }
+                __syncwarp();
+                ready = min(need, ready + 32);
+            }
+            const int row = u * 32 + lane;
+            double dv = 0.0;
+            if (row < a.nrows) {
+                const int ts = __ldg(a.tstart + row);
+                const int len = __ldg(a.tstart + row + 1) - ts;
+                const double *tt = a.t;
+                auto P = [&](int m) -> double {
+                    const unsigned e = __ldg(a.gt16 + ts + m);
+                    const int j = row - c_gt_rel[slot][e & 255u];
+                    const int q = (j >> 5) * W32 + 32 * (int)(e >> 8) + (j & 31);
+                    return prod(__ldg(a.gval + q), __ldcg(tt + j));
+                };
+                const double sum = ref_row_sum<false>(P, len);
+                double yv;
+                if constexpr (EPI == EPI_AXPYW) yv = add(a.x[row], __dmul_rn(a.omega, sum));
+                else yv = __dmul_rn(a.omega, sum);
+                a.x[row] = yv;
+                if (want_dot) dv = yv * (self_dot ? yv : a.dotw[row]);
+            }
+            if (want_dot || a.fin != FIN_NONE) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) dv += __shfl_xor_sync(0xffffffffu, dv, o);
+                if (lane == 0) a.upart[u] = dv;
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        s_last = atomicAdd(a.ctr + 1, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        if (a.dotw != nullptr || a.fin != FIN_NONE) {
+            double acc = 0.0;
+            for (int i = tid; i < a.nunits; i += FUSED_THREADS) acc += __ldcg(a.upart + i);
+            acc = block_sum<FUSED_THREADS>(acc, red);
+            if (tid == 0) apply_fin(a.fin, acc, a.ctl);
+        }
+        if (tid == 0) {
+            a.ctr[1] = 0u;
+            a.ctr[2] = gen;
+            __threadfence();
+        }
+    }
+}
+
 // ---------------------------------------------------------------- SpMV, SELL-32 streamed by the bulk-copy engine
 
 // The SELL-32 layout's value (and column) arrays are one contiguous stream, so

@@ -91,7 +91,8 @@ def test_fullsize_pcg_matches_reference_solve(full):
     np.testing.assert_array_equal(res.x, res2.x)
 
 
-def test_fullsize_fused_fsai_steps_bit_identical(full):
+@pytest.mark.parametrize("mode", [1, 2])
+def test_fullsize_fused_fsai_steps_bit_identical(full, mode):
     # the one-kernel G/G^T step (fsai_fused) on the large levels: smoother
     # sweeps bit-identical to the oracle, V-cycle bit-identical to the
     # two-kernel path
@@ -101,7 +102,7 @@ def test_fullsize_fused_fsai_steps_bit_identical(full):
     name, h, dh0 = full
     if h.levels[0].smoother is None or h.levels[0].smoother.kind != "fsai":
         pytest.skip("no FSAI smoother")
-    dh = amg.DeviceHierarchy.from_reference(h, options={"fused": 1})
+    dh = amg.DeviceHierarchy.from_reference(h, options={"fused": mode})
     fused = dh.stats()["fused_levels"]
     assert fused & 1, "level 0 should run the fused FSAI step"
     rng = np.random.default_rng(23)
