@@ -214,6 +214,39 @@ def test_coarse_solve_and_vcycle(name, tail, cases):
     assert _relerr(dh.vcycle(y2), O.vcycle(c["h"], y2)) <= 1e-12
 
 
+@pytest.mark.parametrize("opts", [{"coarse_pipe": 0}, {"coarse_pipe": 1}, {"coarse_pipe": 0, "tail_nnz": 0},
+                                  {"coarse_pipe": 1, "tail_nnz": 0}, {"tail_prefetch": 0}])
+@pytest.mark.parametrize("name", [n for n in HIER_CASES if n != "poisson1d_50_single"])
+def test_coarse_solve_variants(name, opts, cases):
+    # blocked and pipelined substitution, standalone and inside the cluster tail
+    c, dh = _dh(name, cases, **opts)
+    v = c["vec"]
+    assert _relerr(dh.coarse_solve(v["coarse_y"]), v["coarse_z"]) <= 1e-12
+    assert _relerr(dh.vcycle(v["y"]), v["vcycle_z"]) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [31, 33, 96, 200, 250])
+@pytest.mark.parametrize("pipe", [0, 1])
+def test_coarse_cholesky_sizes(n, pipe):
+    # dense SPD coarsest level of n rows (1..8 diagonal blocks of 32, partial last block):
+    # device dpotrs restatement vs scipy.linalg.cho_solve, the reference call (hierarchy.py:149-152)
+    import scipy.linalg as sla
+    from paper_2102_07417_b200.hiercache import HostHierarchy, HostLevel, _Cycle
+    from paper_2102_07417_b200.problems import Csr
+
+    rng = np.random.default_rng(n)
+    b = rng.standard_normal((n, n))
+    a = b @ b.T + n * np.eye(n)
+    rows, cols = np.nonzero(np.ones((n, n)))
+    m = Csr(n, n, np.arange(0, n * n + 1, n), cols.astype(np.int32), a[rows, cols])
+    fac = sla.cho_factor(a, lower=True)
+    h = HostHierarchy(levels=[HostLevel(a=m)], config=_Cycle(), factor=fac, factor_kind="cholesky")
+    dh = amg.DeviceHierarchy.from_reference(h, options={"coarse_pipe": pipe})
+    y = rng.uniform(-1, 1, n)
+    assert _relerr(dh.coarse_solve(y), sla.cho_solve(fac, y)) <= 1e-12
+    dh.close()
+
+
 @pytest.mark.parametrize("opts", [{}, {"tail_nnz": 0}, {"pdl": 0}, {"graph": 1}])
 @pytest.mark.parametrize("name", cases_with("pcg"))
 def test_pcg_matches_reference(name, opts, cases):
