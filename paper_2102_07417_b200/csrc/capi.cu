@@ -209,6 +209,8 @@ struct amg_handle {
     int symd_minb = 4;            // fixed-slot 32-wide kernel: min CTAs/SM (register budget) 3, 4 or 5
     int sells = 1;                // sorted SELL-32 (sigma window below) where natural slices pad > 10%
     int sells_sigma = 128;
+    int sells_buckets = 0;        // > 0: matrices above sells_max_rows get rows partitioned by round count into
+                                  // 1 + sells_buckets classes (order kept inside a class)
     int sells_plen = 1;           // sorted SELL: predicate slot loads on the row length (padding moves no bytes)
     int sells_max_pad = 60;       // % padding allowed for the sorted layout (padding slots are skipped with sells_plen)
     double sells_min_avg = 4.0;   // ... for matrices averaging at least this many entries per row
@@ -1337,6 +1339,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "symm") { h->symm = value ? 1 : 0; return AMG_OK; }
     if (k == "sells") { h->sells = (int)value; return AMG_OK; }
     if (k == "sells_max_rows") { h->sells_max_rows = value; return AMG_OK; }
+    if (k == "sells_buckets") { h->sells_buckets = (int)value; return AMG_OK; }
     if (k == "sells_plen") { h->sells_plen = value ? 1 : 0; return AMG_OK; }
     if (k == "sells_max_pad") { h->sells_max_pad = (int)value; return AMG_OK; }
     if (k == "sells_sigma") { h->sells_sigma = (int)value; return AMG_OK; }
@@ -2226,7 +2229,8 @@ int amg_finalize(amg_t *h)
                 }
             }
             if (!M.uval && !M.uval_s && h->sells && !longrows && !h->lanes_override && h->sells_sigma >= 32 &&
-                M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm && M.nrows <= h->sells_max_rows &&
+                M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm &&
+                (M.nrows <= h->sells_max_rows || h->sells_buckets) &&
                 (double)M.nnz >= h->sells_min_avg * (double)M.nrows) {
                 // sorted SELL-32: taken where natural slices pad > 10% and sorted ones <= 10%
                 const int64_t ns = (M.nrows + 31) / 32;
@@ -2239,7 +2243,19 @@ int amg_finalize(amg_t *h)
                 }
                 std::vector<int32_t> order(M.nrows);
                 for (int64_t r = 0; r < M.nrows; ++r) order[r] = (int32_t)r;
-                for (int64_t w0 = 0; w0 < M.nrows; w0 += h->sells_sigma) {
+                const bool bucket = M.nrows > h->sells_max_rows;
+                if (bucket) {
+                    // fine-level rows: stable partition by the number of 8-entry rounds the row needs
+                    // (1 | 2 | 3 | more), rows keep their order inside a bucket, so lanes stay on
+                    // neighbouring rows (the x gathers keep their locality) while a warp's rows need
+                    // about the same number of rounds
+                    auto bk = [&](int32_t r) {
+                        const int n1 = off32[r + 1] - off32[r] - 1;
+                        return n1 < 8 ? 0 : std::min(1 + (n1 - 8) / 8, h->sells_buckets);
+                    };
+                    std::stable_sort(order.begin(), order.end(), [&](int32_t x1, int32_t x2) { return bk(x1) < bk(x2); });
+                }
+                for (int64_t w0 = 0; w0 < M.nrows && !bucket; w0 += h->sells_sigma) {
                     const int64_t w1 = std::min<int64_t>(M.nrows, w0 + h->sells_sigma);
                     std::stable_sort(order.begin() + w0, order.begin() + w1, [&](int32_t x1, int32_t x2) {
                         return off32[x1 + 1] - off32[x1] > off32[x2 + 1] - off32[x2];

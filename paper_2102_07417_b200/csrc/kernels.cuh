@@ -2730,7 +2730,7 @@ __device__ void chol_solve_cta(int n, const double *__restrict__ L, const double
 // blocks): n = 188 takes ~1/3 of the blocked schedule.  Same arithmetic per
 // entry (different association of the updates, as dtrsm's blocking differs
 // from both).  `v` holds b on entry and z on exit; ends with __syncthreads.
-__device__ void chol_solve_pipe(int n, const double *__restrict__ L, const double *__restrict__ dinv, double *v,
+__device__ __noinline__ void chol_solve_pipe(int n, const double *__restrict__ L, const double *__restrict__ dinv, double *v,
                                 int nap = 0)
 {
     __shared__ int s_done[2][16];
