@@ -73,7 +73,8 @@ struct DevMat {
     int32_t *pbeg = nullptr;     // pattern starts into prel
     int npat = 0, nrel = 0;
     double *uval = nullptr;      // symmetric stencil layout (spmv_symd), nullptr if unused
-    int sym_slot = -1;           // its __constant__ pattern-table slot
+    int sym_slot = -1;           // its __constant__ pattern-start slot
+    int sym_tab = -1, sym_ntab = 0, sym_classes = 1, sym_npad = 0;  // entry range in c_symd_tab; row classes
     double *uval_s = nullptr;    // uniform-width SELL-32 (spmv_sellu), nullptr if unused
     double *sv_s = nullptr;      // sorted SELL-32 (spmv_sells), nullptr if unused
     int32_t *sc_s = nullptr, *sb_s = nullptr, *sp_s = nullptr;
@@ -160,6 +161,35 @@ static int symd_slot_take(int device)
     return -1;
 }
 
+static std::unordered_map<int, std::vector<std::pair<int, int>>> g_symd_tab;  // device -> used [start, len)
+
+static int symd_tab_take(int device, int len)
+{
+    std::lock_guard<std::mutex> g(g_symd_mu);
+    auto &u = g_symd_tab[device];
+    std::sort(u.begin(), u.end());
+    int at = 0;
+    for (auto &r : u) {
+        if (r.first - at >= len) break;
+        at = std::max(at, r.first + r.second);
+    }
+    if (at + len > SYMD_TAB) return -1;
+    u.emplace_back(at, len);
+    return at;
+}
+
+static void symd_tab_give(int device, int start, int len)
+{
+    if (start < 0) return;
+    std::lock_guard<std::mutex> g(g_symd_mu);
+    auto &u = g_symd_tab[device];
+    for (size_t i = 0; i < u.size(); ++i)
+        if (u[i].first == start && u[i].second == len) {
+            u.erase(u.begin() + i);
+            return;
+        }
+}
+
 static void symd_slot_give(int device, int slot)
 {
     if (slot < 0) return;
@@ -204,6 +234,7 @@ struct amg_handle {
     int long_avg = 128;           // rows averaging more entries run leaf by leaf (spmv_leaves); 0 = off
     int small_rows_per_sm = 128;  // below sm_count * this many rows a matrix counts as small
     int patterns = 1;             // stencil-pattern layout for square operators with few row patterns
+    int symd_classes = 3;         // symmetric layout: try row classes r % K, K = 1..symd_classes
     int symd_blocked = 1;         // symmetric layout stored slice-blocked (32 rows x nu diagonals contiguous)
     int symd_gminb = 5;           // round-by-round symmetric kernel: min CTAs/SM 5, 6 or 8
     int symd_minb = 4;            // fixed-slot 32-wide kernel: min CTAs/SM (register budget) 3, 4 or 5
@@ -698,7 +729,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
                 g = (int)((M.nrows + c - 1) / c);
             }
         }
-        SymArgs sa{M.uval, M.pid, M.sym_slot, chunk, M.sym_blocked ? 32 * M.nudiag : 0};
+        SymArgs sa{M.uval, M.pid, M.sym_slot, chunk, M.sym_blocked ? 32 * M.nudiag : 0, M.sym_npad};
         if (fx)
             TRY(launch_k(h, spmv_symd_fixed_fn(epi, M.sym_fl, h->symd_minb, M.sym_blocked), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
         else
@@ -1295,6 +1326,8 @@ void amg_destroy(amg_t *h)
             F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s);
             symd_slot_give(h->device, M.sym_slot);
             M.sym_slot = -1;
+            symd_tab_give(h->device, M.sym_tab, M.sym_ntab);
+            M.sym_tab = -1;
             halo_free(M.halo);
         }
         F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
@@ -1353,6 +1386,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "symd_chunked") { h->symd_chunked = value ? 1 : 0; return AMG_OK; }
     if (k == "coarse_pipe") { h->coarse_pipe = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "tail_prefetch") { h->tail_prefetch = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
+    if (k == "symd_classes") { h->symd_classes = (int)value; return AMG_OK; }
     if (k == "symd_blocked") { h->symd_blocked = value ? 1 : 0; return AMG_OK; }
     if (k == "symd_gminb") { h->symd_gminb = (int)value; return AMG_OK; }
     if (k == "symd_minb") { h->symd_minb = (int)value; return AMG_OK; }
@@ -1655,27 +1689,58 @@ static int build_symd(amg_t *h, DevMat &M, const std::vector<int32_t> &off32, co
                       const std::vector<double> &val_h, const std::vector<uint8_t> &ids,
                       const std::vector<int32_t> &rel, const std::vector<int32_t> &beg)
 {
-    std::vector<int32_t> dist(rel.begin(), rel.end());
-    std::sort(dist.begin(), dist.end());
-    dist.erase(std::unique(dist.begin(), dist.end()), dist.end());
-    std::vector<int32_t> up;  // stored diagonals d >= 0, ascending
-    for (int32_t d : dist) {
-        if (!std::binary_search(dist.begin(), dist.end(), -d)) return AMG_OK;  // not structurally symmetric
-        if (d >= 0) up.push_back(d);
-    }
-    if (rel.size() > (size_t)SYMD_ENT_MAX || beg.size() > (size_t)SYMD_BEG_MAX) return AMG_OK;  // constant table
     const int64_t n = M.nrows;
-    const int nu = (int)up.size();
-    if (nu == 0 || (double)nu * (double)n > 0.75 * (double)M.nnz) return AMG_OK;
+    const int npat = (int)beg.size() - 1;
+    if (npat < 1 || rel.size() > (size_t)SYMD_TAB || beg.size() > (size_t)SYMD_BEG_MAX) return AMG_OK;
     const int64_t npad = ((n + 31) / 32) * 32;
-    if ((int64_t)nu * npad + npad >= INT32_MAX - 64) return AMG_OK;
-    auto jof = [&](int32_t d) { return (int)(std::lower_bound(up.begin(), up.end(), d) - up.begin()); };
     int maxlen = 0;
-    for (size_t i = 0; i + 1 < beg.size(); ++i) maxlen = std::max(maxlen, beg[i + 1] - beg[i]);
+    for (int p = 0; p < npat; ++p) maxlen = std::max(maxlen, beg[p + 1] - beg[p]);
+    // Row classes: rows r with r % K == c share their set of stored diagonals D_c (d >= 0).
+    // K = 1 for scalar stencils; K = 3 for node-major 3-dof systems (elasticity), whose
+    // classes each use 41 of the 68 non-negative offsets.  A pattern must belong to one class.
+    int K = 0;
+    std::vector<std::vector<int32_t>> up;
+    std::vector<int> pcls;
+    for (int k : {1, 2, 3, 4}) {
+        if (k > h->symd_classes) break;
+        std::vector<int> cl(npat, -1);
+        bool ok = true;
+        for (int64_t r = 0; r < n && ok; ++r) {
+            const int c = (int)(r % k), p = ids[r];
+            if (cl[p] < 0) cl[p] = c;
+            else if (cl[p] != c) ok = false;
+        }
+        if (!ok) continue;
+        std::vector<std::vector<int32_t>> u(k);
+        for (int p = 0; p < npat; ++p)
+            if (cl[p] >= 0)
+                for (int e = beg[p]; e < beg[p + 1]; ++e)
+                    if (rel[e] >= 0) u[cl[p]].push_back(rel[e]);
+        size_t nu = 0;
+        for (auto &v : u) {
+            std::sort(v.begin(), v.end());
+            v.erase(std::unique(v.begin(), v.end()), v.end());
+            nu = std::max(nu, v.size());
+        }
+        if (nu == 0 || nu > 63 || (double)nu * (double)n > 0.75 * (double)M.nnz) continue;
+        K = k;
+        up = u;
+        pcls = cl;
+        break;
+    }
+    if (K == 0) return AMG_OK;
+    int nu = 0;
+    for (auto &v : up) nu = std::max(nu, (int)v.size());
+    if ((int64_t)nu * npad + npad >= INT32_MAX - 64) return AMG_OK;
+    auto jof = [&](int64_t r, int32_t d) -> int {  // stored diagonal index of a(r, r + d), d >= 0; -1 if none
+        const auto &v = up[r % K];
+        auto it = std::lower_bound(v.begin(), v.end(), d);
+        return (it == v.end() || *it != d) ? -1 : (int)(it - v.begin());
+    };
     // slice-blocked storage for the round-by-round kernel (27-point: 88 -> 81 us on config 2); the
     // fixed-slot 7-point kernel keeps one array per diagonal (config 4: 159 vs 171 us)
-    const bool blk = h->symd_blocked && nu <= 63 && !(maxlen <= 8 && h->symd_fixed >= 1);
-    auto sidx = [&](int64_t r, int j) -> size_t {  // storage index of a(r, r + up[j])
+    const bool blk = h->symd_blocked && !(maxlen <= 8 && h->symd_fixed >= 1 && K == 1);
+    auto sidx = [&](int64_t r, int j) -> size_t {  // storage index of stored diagonal j of row r
         return blk ? (size_t)((r >> 5) * 32 * nu + 32 * j + (r & 31)) : (size_t)j * npad + r;
     };
     std::vector<double> uv((size_t)nu * npad, 0.0);
@@ -1684,7 +1749,7 @@ static int build_symd(amg_t *h, DevMat &M, const std::vector<int32_t> &off32, co
         for (int32_t k = off32[r]; k < off32[r + 1]; ++k) {
             const int32_t d = col_h[k] - (int32_t)r;
             if (d < 0) continue;
-            const size_t q = sidx(r, jof(d));
+            const size_t q = sidx(r, jof(r, d));
             uv[q] = val_h[k];
             have[q] = 1;
         }
@@ -1692,23 +1757,43 @@ static int build_symd(amg_t *h, DevMat &M, const std::vector<int32_t> &off32, co
         for (int32_t k = off32[r]; k < off32[r + 1]; ++k) {
             const int32_t d = col_h[k] - (int32_t)r;
             if (d >= 0) continue;
-            const size_t q = sidx(r + d, jof(-d));
+            const int j = jof(r + d, -d);
+            if (j < 0) return AMG_OK;
+            const size_t q = sidx(r + d, j);
             if (!have[q] || memcmp(&uv[q], &val_h[k], sizeof(double)) != 0) return AMG_OK;
         }
+    // pattern entries; a pattern's rows are all of class pcls[p], so the mirror row's class is known
+    std::vector<int2> ent(rel.size());
+    for (int p = 0; p < npat; ++p) {
+        const int c = pcls[p] < 0 ? 0 : pcls[p];
+        for (int e = beg[p]; e < beg[p + 1]; ++e) {
+            const int32_t d = rel[e];
+            if (std::abs((int64_t)d) >= (1 << 24)) return AMG_OK;
+            const int64_t src = d >= 0 ? c : (((c + d) % K) + K) % K;  // class of the row holding the copy
+            const int j = jof(src, d >= 0 ? d : -d);
+            if (j < 0) return AMG_OK;
+            const int64_t ds = d >= 0 ? 0 : d;  // row offset of the stored copy
+            ent[e] = make_int2(d, blk ? (int)((ds << 6) | j) : (int)((int64_t)j * npad + ds));
+        }
+    }
     const int slot = symd_slot_take(h->device);
     if (slot < 0) return AMG_OK;  // every table slot of this device in use: keep the other layouts
-    std::vector<int2> ent(SYMD_ENT_MAX, make_int2(0, 0));
-    std::vector<int32_t> bg(SYMD_BEG_MAX, 0);
-    for (size_t i = 0; i < rel.size(); ++i) {
-        const int32_t d = rel[i];
-        if (blk) ent[i] = d >= 0 ? make_int2(d, jof(d)) : make_int2(d, (int)(((int64_t)d << 6) | jof(-d)));
-        else ent[i] = d >= 0 ? make_int2(d, (int)((int64_t)jof(d) * npad)) : make_int2(d, (int)((int64_t)jof(-d) * npad + d));
+    const int tbase = symd_tab_take(h->device, (int)ent.size());
+    if (tbase < 0) {
+        symd_slot_give(h->device, slot);
+        return AMG_OK;
     }
-    for (size_t i = 0; i < beg.size(); ++i) bg[i] = slot * SYMD_ENT_MAX + beg[i];
-    CK(cudaMemcpyToSymbol(c_symd_ent, ent.data(), ent.size() * sizeof(int2), (size_t)slot * SYMD_ENT_MAX * sizeof(int2)));
+    std::vector<int32_t> bg(SYMD_BEG_MAX, 0);
+    for (size_t i = 0; i < beg.size(); ++i) bg[i] = tbase + beg[i];
+    if (!ent.empty())
+        CK(cudaMemcpyToSymbol(c_symd_tab, ent.data(), ent.size() * sizeof(int2), (size_t)tbase * sizeof(int2)));
     CK(cudaMemcpyToSymbol(c_symd_beg, bg.data(), bg.size() * sizeof(int32_t), (size_t)slot * SYMD_BEG_MAX * sizeof(int32_t)));
     M.sym_slot = slot;
+    M.sym_tab = tbase;
+    M.sym_ntab = (int)ent.size();
     M.sym_blocked = blk ? 1 : 0;
+    M.sym_classes = K;
+    M.sym_npad = (int)npad;
     TRY(dalloc(&M.uval, uv.size()));
     CK(cudaMemcpy(M.uval, uv.data(), uv.size() * sizeof(double), cudaMemcpyHostToDevice));
     M.nudiag = nu;
@@ -1725,7 +1810,6 @@ static int build_symd(amg_t *h, DevMat &M, const std::vector<int32_t> &off32, co
                                                                   (int64_t)h->sm_count * std::max(nb, 1)));
         h->max_grid = std::max(h->max_grid, M.symf_grid);
     }
-    (void)ids;
     return AMG_OK;
 }
 

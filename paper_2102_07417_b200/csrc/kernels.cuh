@@ -1610,10 +1610,13 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, PAT ? 5 : 4) spmv_sell(const
 // and x streams saturate.  SYMD_SLOTS tables per device, handed out per matrix
 // at upload (capi.cu symd_slot_*).
 constexpr int SYMD_SLOTS = 8;
-constexpr int SYMD_ENT_MAX = 512;        // pattern entries per table
+constexpr int SYMD_TAB = 4096;           // pattern entries over all tables of a device (32 KB)
 constexpr int SYMD_BEG_MAX = PAT_MAX + 1;
-__constant__ int2 c_symd_ent[SYMD_SLOTS * SYMD_ENT_MAX];      // {rel, voff}
-__constant__ int32_t c_symd_beg[SYMD_SLOTS * SYMD_BEG_MAX];   // absolute starts into c_symd_ent
+// entry {rel, y}: column = row + rel; value = stored diagonal j of row r2 = row + (below ? rel : 0)
+// (its mirror when below the diagonal): y = j * npad + (r2 - row) diagonal-major, or
+// y = ((r2 - row) << 6) | j slice-blocked
+__constant__ int2 c_symd_tab[SYMD_TAB];
+__constant__ int32_t c_symd_beg[SYMD_SLOTS * SYMD_BEG_MAX];   // absolute starts into c_symd_tab
 
 struct SymArgs {
     const double *uval;
@@ -1621,12 +1624,12 @@ struct SymArgs {
     int slot;
     int chunk;  // > 0: CTA b sweeps rows [b*chunk, (b+1)*chunk) in 256-row steps (x and mirror lines
                 // reused from L1 by the next step); 0: grid-stride over 256-row blocks
-    int w32;    // blocked storage (> 0): the nu diagonals of each 32-row slice contiguous,
-                // uval[(i/32)*w32 + 32 j + i%32] with w32 = 32 nu; table entry y = (dsrc << 6) | j
+    int w32;    // slice-blocked storage (BLK): the nu diagonals of each 32-row slice contiguous,
+                // uval[(i/32)*w32 + 32 j + i%32], w32 = 32 nu
+    int npad;   // diagonal-major storage (!BLK): uval[j * npad + i]
 };
 
-// value index of a pattern entry {rel, y}: diagonal-major (w32 == 0: y = voff)
-// or slice-blocked (y = (row offset of the stored copy) << 6 | diagonal)
+// value index of pattern entry {rel, y} for `row`
 template <bool BLK>
 __device__ __forceinline__ int symd_vidx(int row, int y, int w32)
 {
@@ -1703,7 +1706,7 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, MINB) spmv_symd(const SpmvAr
         const int rb = c_symd_beg[bbase + pid];
         const int len = c_symd_beg[bbase + pid + 1] - rb;
         auto P = [&](int k) -> double {
-            const int2 q = c_symd_ent[rb + k];
+            const int2 q = c_symd_tab[rb + k];
             return prod(__ldg(uv + symd_vidx<BLK>(row, q.y, sa.w32)), __ldg(x + (row + q.x)));
         };
         const double sum = ref_row_sum<false>(P, len);  // pattern rows have <= 129 entries
@@ -1800,7 +1803,7 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, MINB) spmv_symd_fixed(const 
         for (int k = 0; k < FL; ++k) {
             p[k] = 0.0;
             if (k < len) {
-                const int2 q = c_symd_ent[rb + k];
+                const int2 q = c_symd_tab[rb + k];
                 p[k] = prod(__ldg(uv + symd_vidx<BLK>(row, q.y, sa.w32)), __ldg(x + (row + q.x)));
             }
         }

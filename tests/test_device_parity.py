@@ -94,6 +94,17 @@ def test_spmv_sell_layouts_bit_identical(kind, sellq):
 def _stencil(kind):
     from paper_2102_07417_b200 import problems as Pb
 
+    if kind == "elast_sym":
+        # node-major 3-dof elasticity operator made bitwise symmetric ((A + A^T) / 2 is exactly
+        # symmetric): 135 scalar offsets, 68 of them >= 0 -- stored per row class r % 3 (41 each)
+        import scipy.sparse as sp
+
+        m = Pb.elasticity3d(20, 20, 20, sigma=1.0, nu=0.3, seed=42)
+        m = m[0] if isinstance(m, tuple) else m
+        a = sp.csr_matrix((m.values, m.col_indices, m.row_offsets), shape=(m.nrows, m.ncols))
+        s2 = ((a + a.T) * 0.5).tocsr()
+        s2.sort_indices()
+        return Pb.Csr(s2.shape[0], s2.shape[1], s2.indptr, s2.indices, s2.data)
     if kind == "poisson7":
         return Pb.poisson7(40, 40, 24)
     if kind == "hetero27":
@@ -101,7 +112,7 @@ def _stencil(kind):
     return Pb.rtanis7(36, 36, 20, kx=1.0, ky=1.0, kz=1e-3)
 
 
-@pytest.mark.parametrize("kind", ["poisson7", "hetero27", "rtanis7"])
+@pytest.mark.parametrize("kind", ["poisson7", "hetero27", "rtanis7", "elast_sym"])
 def test_spmv_symmetric_diagonals_bit_identical(kind):
     # bitwise-symmetric stencil operators run on the upper-diagonal layout
     # (mirror reads for d < 0); rows must equal the reference's bit for bit
