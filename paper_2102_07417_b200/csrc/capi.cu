@@ -200,6 +200,11 @@ static void symd_slot_give(int device, int slot)
 struct amg_handle {
     int device = 0, rank = 0, nranks = 1;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;           // side stream: L2 prefetch of the tail levels
+    cudaEvent_t pf_fork = nullptr, pf_join = nullptr;
+    PrefetchRange *pf_ranges = nullptr;    // device copy of the tail matrices' ranges
+    int pf_n = 0;
+    bool pf_pending = false;
     int sm_count = 148;
     std::vector<LevelD> lv;
     int nu1 = 1, nu2 = 1;
@@ -274,6 +279,7 @@ struct amg_handle {
                                  // footprint delays the cluster launch; streamed from L2 by default)
     int cluster = 16;
     int coarse_pipe = 1;          // pipelined per-warp Cholesky substitution
+    int side_prefetch = 1;        // side-stream L2 prefetch of the tail matrices during the level above it
     int tail_prefetch = 1;        // tail kernel prefetches its streamed matrices into L2 before griddepcontrol.wait
     int tail_level = 0;  // 0 = disabled
     TailOp *tail_ops = nullptr;
@@ -861,6 +867,11 @@ static int launch_coarse(amg_t *h, const double *y, double *z, const int *g1, in
 
 static int launch_tail(amg_t *h, const int *g1)
 {
+    if (h->pf_pending) {  // the side-stream prefetch joins before the tail
+        CK(cudaEventRecord(h->pf_join, h->side));
+        CK(cudaStreamWaitEvent(h->stream, h->pf_join, 0));
+        h->pf_pending = false;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)h->cluster);
     cfg.blockDim = dim3(TAIL_THREADS);
@@ -992,6 +1003,14 @@ static int enqueue_vcycle(amg_t *h, int k, const double *y, double *x, const int
     if (k == nl - 1) return launch_coarse(h, y, x, g1, fin, dotw);
     LevelD &L = h->lv[k];
     LevelD &C = h->lv[k + 1];
+    if (!h->collect && h->side_prefetch && h->pf_n > 0 && h->tail_level > 0 && k == h->tail_level - 1) {
+        CK(cudaEventRecord(h->pf_fork, h->stream));
+        CK(cudaStreamWaitEvent(h->side, h->pf_fork, 0));
+        l2_prefetch<<<2 * h->sm_count, 256, 0, h->side>>>(h->pf_ranges, h->pf_n);
+        CK(cudaGetLastError());
+        ++h->launches;
+        h->pf_pending = true;
+    }
     const double *r = y;
     if (h->nu1 > 0) {
         TRY(enqueue_smooth(h, k, y, x, h->nu1, true, g1, FIN_NONE, nullptr));
@@ -1270,6 +1289,21 @@ static int build_tail(amg_t *h)
     h->tail_prod_off = best_prod_off;
     h->tail_level = best;
     if (getenv("AMGB200_TRACE")) TRY(dalloc(&h->trace, (size_t)h->tail_nops + 2));
+    {   // L2 prefetch ranges for the side stream: every CSR array of the tail levels + the coarse factor
+        std::vector<PrefetchRange> pr;
+        for (int k = best; k < nl; ++k)
+            for (int w = 0; w < 5; ++w) {
+                const DevMat &M = h->lv[k].m[w];
+                if (!M.present || M.nnz == 0) continue;
+                pr.push_back({reinterpret_cast<const char *>(M.off), (long long)(M.nrows + 1) * 4});
+                pr.push_back({reinterpret_cast<const char *>(M.col), (long long)M.nnz * 4});
+                pr.push_back({reinterpret_cast<const char *>(M.val), (long long)M.nnz * 8});
+            }
+        if (h->Lp) pr.push_back({reinterpret_cast<const char *>(h->Lp), (long long)h->nc * (h->nc + 1) / 2 * 8});
+        TRY(dalloc(&h->pf_ranges, pr.size()));
+        if (!pr.empty()) CK(cudaMemcpy(h->pf_ranges, pr.data(), pr.size() * sizeof(PrefetchRange), cudaMemcpyHostToDevice));
+        h->pf_n = (int)pr.size();
+    }
     return AMG_OK;
 }
 
@@ -1301,6 +1335,9 @@ int amg_create(int device, int rank, int nranks, const void *nccl_unique_id, amg
     CK(cudaGetDeviceProperties(&prop, device));
     h->sm_count = prop.multiProcessorCount;
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->pf_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->pf_join, cudaEventDisableTiming));
     CK(cudaEventCreate(&h->ev0));
     CK(cudaEventCreate(&h->ev1));
     if (nranks > 1) {
@@ -1335,6 +1372,10 @@ void amg_destroy(amg_t *h)
         symd_slot_give(h->device, L.fz.slot);
         L.fz.slot = -1;
     }
+    F(h->pf_ranges);
+    if (h->side) cudaStreamDestroy(h->side);
+    if (h->pf_fork) cudaEventDestroy(h->pf_fork);
+    if (h->pf_join) cudaEventDestroy(h->pf_join);
     F(h->Lp); F(h->LU); F(h->dinv); F(h->binv); F(h->tail_ops); F(h->tail_mats); F(h->tail_splits); F(h->piv); F(h->partials); F(h->ticket); F(h->ctl);
     F(h->b); F(h->x); F(h->r); F(h->z); F(h->p); F(h->q); F(h->tmp_in); F(h->tmp_out); F(h->hist);
     for (auto *bp : h->bicg) F(bp);
@@ -1385,6 +1426,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "symd_fixed") { h->symd_fixed = (int)value; return AMG_OK; }
     if (k == "symd_chunked") { h->symd_chunked = value ? 1 : 0; return AMG_OK; }
     if (k == "coarse_pipe") { h->coarse_pipe = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
+    if (k == "side_prefetch") { h->side_prefetch = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "tail_prefetch") { h->tail_prefetch = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "symd_classes") { h->symd_classes = (int)value; return AMG_OK; }
     if (k == "symd_blocked") { h->symd_blocked = value ? 1 : 0; return AMG_OK; }

@@ -1972,6 +1972,27 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_sells(const SpmvArgs
     }
 }
 
+// ---------------------------------------------------------------- L2 prefetch of the coarse levels
+
+// Launched on a side stream while the level above the cluster tail runs: pulls
+// the tail's matrices (evicted by the fine-level sweeps) into L2, so the tail
+// -- 16 SMs, latency-bound -- finds them there.  ranges: (ptr, bytes) pairs.
+struct PrefetchRange {
+    const char *p;
+    long long bytes;
+};
+
+__global__ void __launch_bounds__(256) l2_prefetch(const PrefetchRange *__restrict__ r, int nr)
+{
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long nt = (long long)gridDim.x * blockDim.x;
+    for (int k = 0; k < nr; ++k) {
+        const PrefetchRange q = r[k];
+        for (long long off = t * 128; off < q.bytes; off += nt * 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(q.p + off));
+    }
+}
+
 // ---------------------------------------------------------------- FSAI smoother step, G and G^T fused
 
 // x = w * G^T (G y)  (EPI_SETW)  or  x = x + w * G^T (G y)  (EPI_AXPYW)
