@@ -82,7 +82,7 @@ struct DevMat {
     int s_grid = 0;
     int32_t *ucol_s = nullptr;
     uint8_t *ulen_s = nullptr;
-    int uW = 0, u_grid = 0;
+    int uW = 0, u_grid = 0, u_plen = 0;  // u_plen: padding slots skipped (short ragged rows)
     int nudiag = 0, sym_grid = 0, sym_fl = 0, symf_grid = 0, sym_blocked = 0;  // sym_fl: fixed-slot kernel width (0: none)
     int32_t *pstart = nullptr;   // padded-aligned layout (spmv_vec), nullptr if unused
     double *pval = nullptr;
@@ -253,6 +253,7 @@ struct amg_handle {
     int64_t sells_max_rows = 1 << 20;  // ... and at most this many rows (sorting costs fine-grid rows their gather
                                        // locality: config-2 G^T_0 85 -> 134 us; coarse A_1 18 -> 13 us)
     int vec_pipe = 0;             // padded-CSR kernel with the first round's columns fetched one row ahead
+    int sellu_short = 1;          // ... and for rows of <= 8 entries at any padding, padding slots skipped
     int sellu = 1;                // uniform-width SELL-32 for rows of <= 16 entries padding <= 10% (e.g. FSAI G)
     int fused = 0;                // FSAI steps of large levels as one G/G^T kernel (fsai_fused): bit-identical but
                                   // measured slower on config 2 (294 vs 144 us per level-0 step: the kernels are latency-
@@ -379,9 +380,11 @@ static SpmvSymFn spmv_symd_fixed_fn(int epi, int fl, int minb = 0, bool blk = fa
 
 typedef void (*SpmvSellUFn)(const SpmvArgs, const SellUArgs, int);
 
-static SpmvSellUFn spmv_sellu_fn(int epi, int W)
+static SpmvSellUFn spmv_sellu_fn(int epi, int W, bool plen = false)
 {
-#define AMG_U(E) return W <= 4 ? spmv_sellu<E, 4> : W <= 9 ? spmv_sellu<E, 9> : spmv_sellu<E, 16>;
+#define AMG_U(E)                                                                                        \
+    return plen ? (W <= 4 ? spmv_sellu<E, 4, true> : spmv_sellu<E, 8, true>)                             \
+                : (W <= 4 ? spmv_sellu<E, 4, false> : W <= 9 ? spmv_sellu<E, 9, false> : spmv_sellu<E, 16, false>);
     switch (epi) {
     case EPI_PLAIN: AMG_U(EPI_PLAIN)
     case EPI_RESID: AMG_U(EPI_RESID)
@@ -746,7 +749,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
                      qa, (int)M.nrows));
     } else if (M.uval_s && h->sellu) {
         SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW};
-        TRY(launch_k(h, spmv_sellu_fn(epi, M.uW), grid_cap ? std::min(grid_cap, M.u_grid) : M.u_grid, VEC_SPMV_THREADS, 0,
+        TRY(launch_k(h, spmv_sellu_fn(epi, M.uW, M.u_plen), grid_cap ? std::min(grid_cap, M.u_grid) : M.u_grid, VEC_SPMV_THREADS, 0,
                      a, ua, (int)M.nrows));
     } else if (M.sbeg && M.sq_cta && h->sellq) {
         SellArgs sa{M.sbeg, M.sval, M.scol, M.slen, M.pid, M.prel, M.pbeg, M.npat, M.nrel, M.sperm};
@@ -1419,6 +1422,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "sells_sigma") { h->sells_sigma = (int)value; return AMG_OK; }
     if (k == "sells_min_avg10") { h->sells_min_avg = value / 10.0; return AMG_OK; }
     if (k == "vec_pipe") { h->vec_pipe = value ? 1 : 0; return AMG_OK; }
+    if (k == "sellu_short") { h->sellu_short = value ? 1 : 0; return AMG_OK; }
     if (k == "sellu") { h->sellu = value ? 1 : 0; return AMG_OK; }
     if (k == "fused") { h->fused = (int)value; return AMG_OK; }
     if (k == "fused_wa") { h->fused_wa = (int)value; return AMG_OK; }
@@ -2314,7 +2318,8 @@ int amg_finalize(amg_t *h)
                 int W = 0;
                 for (int64_t r = 0; r < M.nrows; ++r) W = std::max(W, off32[r + 1] - off32[r]);
                 const int64_t ns = (M.nrows + 31) / 32;
-                if (W >= 1 && W <= 16 && (double)ns * 32 * W <= 1.10 * (double)M.nnz && ns * 32 * W < INT32_MAX - 64) {
+                const bool plen = h->sellu_short && W <= 8 && (double)ns * 32 * W > 1.10 * (double)M.nnz;
+                if (W >= 1 && W <= 16 && ((double)ns * 32 * W <= 1.10 * (double)M.nnz || plen) && ns * 32 * W < INT32_MAX - 64) {
                     std::vector<int32_t> col_h(M.nnz);
                     std::vector<double> val_h(M.nnz);
                     if (M.nnz) {
@@ -2346,8 +2351,9 @@ int amg_finalize(amg_t *h)
                     CK(cudaMemcpy(M.ucol_s, sc.data(), tot * sizeof(int32_t), cudaMemcpyHostToDevice));
                     CK(cudaMemcpy(M.ulen_s, ln.data(), ln.size(), cudaMemcpyHostToDevice));
                     M.uW = W;
+                    M.u_plen = plen ? 1 : 0;
                     int nbu = 0;
-                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbu, (const void *)spmv_sellu_fn(EPI_RESID, W),
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbu, (const void *)spmv_sellu_fn(EPI_RESID, W, plen),
                                                                      VEC_SPMV_THREADS, 0));
                     M.u_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
                                                                           (int64_t)h->sm_count * std::max(nbu, 1)));

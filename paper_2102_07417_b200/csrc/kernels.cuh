@@ -1843,7 +1843,9 @@ struct SellUArgs {
 // iteration ahead, so a row's W value loads and its x gathers leave together
 // (one dependent memory step per row instead of length -> values/columns ->
 // gathers).
-template <int EPI, int FL>
+// PLEN: slots at or beyond the row's length are not loaded (no bytes for padding): short ragged
+// rows (interpolation P, 1..8 entries) pad their slices freely.
+template <int EPI, int FL, bool PLEN>
 __global__ void __launch_bounds__(VEC_SPMV_THREADS, FL <= 4 ? 6 : FL <= 9 ? 4 : 3) spmv_sellu(const SpmvArgs a,
                                                                                            const SellUArgs u, int nrows)
 {
@@ -1864,14 +1866,15 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, FL <= 4 ? 6 : FL <= 9 ? 4 : 
         const int base = (r >> 5) * W32 + (r & 31);
         len = __ldg(u.len + r);
 #pragma unroll
-        for (int k = 0; k < FL; ++k) c[k] = (k < u.W) ? __ldg(u.col + base + 32 * k) : r;
+        for (int k = 0; k < FL; ++k) c[k] = (k < (PLEN ? len : u.W)) ? __ldg(u.col + base + 32 * k) : r;
     };
     if (row < nrows) fetch(row);
     for (; row < nrows; row += nthreads) {
         const int base = (row >> 5) * W32 + (row & 31);
         double p[FL];
 #pragma unroll
-        for (int k = 0; k < FL; ++k) p[k] = (k < u.W) ? prod(__ldg(u.val + base + 32 * k), __ldg(x + c[k])) : 0.0;
+        for (int k = 0; k < FL; ++k)
+            p[k] = (k < (PLEN ? len : u.W)) ? prod(__ldg(u.val + base + 32 * k), __ldg(x + c[k])) : 0.0;
         const int clen = len;
         if (row + nthreads < nrows) fetch(row + nthreads);
         double bv = 0.0, wv = 0.0;

@@ -128,15 +128,21 @@ def test_spmv_symmetric_diagonals_bit_identical(kind):
         dh.close()
 
 
-@pytest.mark.parametrize("width", [3, 9, 16])
+@pytest.mark.parametrize("width", [3, 9, 16, -4, -8])
 def test_spmv_uniform_sell_bit_identical(width):
     # rows of <= 16 entries with every 32-row slice padded to the widest row
-    # (FSAI factors): all slots loaded at once, summed over each row's own length
+    # (FSAI factors): all slots loaded at once, summed over each row's own length.
+    # width < 0: ragged short rows (0..|width| entries, interpolation-like) whose
+    # padding slots are skipped
     from paper_2102_07417_b200.problems import Csr
 
-    rng = np.random.default_rng(width)
+    rng = np.random.default_rng(abs(width))
     n = 40000
-    lens = np.where(rng.random(n) < 0.97, width, rng.integers(0, width + 1, n))
+    if width < 0:
+        width = -width
+        lens = rng.integers(0, width + 1, n)
+    else:
+        lens = np.where(rng.random(n) < 0.97, width, rng.integers(0, width + 1, n))
     lens[:3] = [0, 1, width]
     off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
     cols = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
