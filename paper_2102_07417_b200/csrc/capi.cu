@@ -76,6 +76,10 @@ struct DevMat {
     int sym_slot = -1;           // its __constant__ pattern-start slot
     int sym_tab = -1, sym_ntab = 0, sym_classes = 1, sym_npad = 0;  // entry range in c_symd_tab; row classes
     double *uval_s = nullptr;    // uniform-width SELL-32 (spmv_sellu), nullptr if unused
+    double *spv = nullptr;       // short/long split (spmv_split_short + spmv_split_long), nullptr if unused
+    int32_t *spc = nullptr, *splong = nullptr;
+    uint8_t *splen = nullptr;
+    int sp_nlong = 0, sp_grid = 0, sp_lgrid = 0;
     double *sv_s = nullptr;      // sorted SELL-32 (spmv_sells), nullptr if unused
     int32_t *sc_s = nullptr, *sb_s = nullptr, *sp_s = nullptr;
     uint8_t *sw_s = nullptr, *sl_s = nullptr;
@@ -243,6 +247,8 @@ struct amg_handle {
     int symd_blocked = 1;         // symmetric layout stored slice-blocked (32 rows x nu diagonals contiguous)
     int symd_gminb = 5;           // round-by-round symmetric kernel: min CTAs/SM 5, 6 or 8
     int symd_minb = 4;            // fixed-slot 32-wide kernel: min CTAs/SM (register budget) 3, 4 or 5
+    int split = 0;                // fine-level ragged matrices: short rows (<= 16) as SELL-32 + long-row list
+                                  // (measured slower on config-2 G^T_0: 121 vs 85 us)
     int sells = 1;                // sorted SELL-32 (sigma window below) where natural slices pad > 10%
     int sells_sigma = 128;
     int sells_buckets = 0;        // > 0: matrices above sells_max_rows get rows partitioned by round count into
@@ -416,6 +422,31 @@ static FusedWsFn fsai_ws_fn(bool set, int wa)
 {
     if (set) return wa <= 2 ? fsai_ws<EPI_SETW, 2> : wa <= 3 ? fsai_ws<EPI_SETW, 3> : wa <= 4 ? fsai_ws<EPI_SETW, 4> : fsai_ws<EPI_SETW, 5>;
     return wa <= 2 ? fsai_ws<EPI_AXPYW, 2> : wa <= 3 ? fsai_ws<EPI_AXPYW, 3> : wa <= 4 ? fsai_ws<EPI_AXPYW, 4> : fsai_ws<EPI_AXPYW, 5>;
+}
+
+typedef void (*SpmvSplitShortFn)(const SpmvArgs, const SplitArgs, int);
+typedef void (*SpmvSplitLongFn)(const SpmvArgs, const SplitArgs);
+
+static SpmvSplitShortFn spmv_split_short_fn(int epi)
+{
+    switch (epi) {
+    case EPI_PLAIN: return spmv_split_short<EPI_PLAIN>;
+    case EPI_RESID: return spmv_split_short<EPI_RESID>;
+    case EPI_AXPYW: return spmv_split_short<EPI_AXPYW>;
+    case EPI_SETW: return spmv_split_short<EPI_SETW>;
+    default: return spmv_split_short<EPI_ADD>;
+    }
+}
+
+static SpmvSplitLongFn spmv_split_long_fn(int epi)
+{
+    switch (epi) {
+    case EPI_PLAIN: return spmv_split_long<EPI_PLAIN>;
+    case EPI_RESID: return spmv_split_long<EPI_RESID>;
+    case EPI_AXPYW: return spmv_split_long<EPI_AXPYW>;
+    case EPI_SETW: return spmv_split_long<EPI_SETW>;
+    default: return spmv_split_long<EPI_ADD>;
+    }
 }
 
 typedef void (*SpmvSellqFn)(const SpmvArgs, const SellArgs, const SellqArgs, int);
@@ -743,6 +774,18 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
             TRY(launch_k(h, spmv_symd_fixed_fn(epi, M.sym_fl, h->symd_minb, M.sym_blocked), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
         else
             TRY(launch_k(h, spmv_symd_fn(epi, h->symd_gminb, M.sym_blocked), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
+    } else if (M.spv && h->split) {
+        SplitArgs qa{M.spv, M.spc, M.splen, M.splong, M.sp_nlong, 0};
+        const bool red = dotw != nullptr || fin != FIN_NONE;
+        const int g = grid_cap ? std::min(grid_cap, M.sp_grid) : M.sp_grid;
+        qa.short_grid = g;
+        if (red && g > h->max_grid) return fail(AMG_E_STATE, "internal: split partials exceed the scratch");
+        TRY(launch_k(h, spmv_split_short_fn(epi), g, VEC_SPMV_THREADS, 0, a, qa, (int)M.nrows));
+        SpmvArgs a2 = a;
+        a2.partials = h->partials;
+        const int gl = grid_cap ? std::min(grid_cap, M.sp_lgrid) : M.sp_lgrid;
+        if (red && g + gl > h->max_grid) return fail(AMG_E_STATE, "internal: split partials exceed the scratch");
+        TRY(launch_k(h, spmv_split_long_fn(epi), gl, VEC_SPMV_THREADS, 0, a2, qa));
     } else if (M.sv_s && h->sells) {
         SellSArgs qa{M.sv_s, M.sc_s, M.sb_s, M.sw_s, M.sp_s, M.sl_s};
         TRY(launch_k(h, spmv_sells_fn(epi, h->sells_plen), grid_cap ? std::min(grid_cap, M.s_grid) : M.s_grid, VEC_SPMV_THREADS, 0, a,
@@ -1363,7 +1406,7 @@ void amg_destroy(amg_t *h)
     auto F = [](void *p) { if (p) cudaFree(p); };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s);
+            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.spv); F(M.spc); F(M.splong); F(M.splen); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s);
             symd_slot_give(h->device, M.sym_slot);
             M.sym_slot = -1;
             symd_tab_give(h->device, M.sym_tab, M.sym_ntab);
@@ -1414,6 +1457,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "small_rows_per_sm") { h->small_rows_per_sm = (int)value; return AMG_OK; }
     if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
     if (k == "symm") { h->symm = value ? 1 : 0; return AMG_OK; }
+    if (k == "split") { h->split = value ? 1 : 0; return AMG_OK; }
     if (k == "sells") { h->sells = (int)value; return AMG_OK; }
     if (k == "sells_max_rows") { h->sells_max_rows = value; return AMG_OK; }
     if (k == "sells_buckets") { h->sells_buckets = (int)value; return AMG_OK; }
@@ -2360,7 +2404,60 @@ int amg_finalize(amg_t *h)
                     h->max_grid = std::max(h->max_grid, M.u_grid);
                 }
             }
-            if (!M.uval && !M.uval_s && h->sells && !longrows && !h->lanes_override && h->sells_sigma >= 32 &&
+            if (!M.uval && !M.uval_s && h->split && !longrows && !h->lanes_override && M.nrows > h->sells_max_rows &&
+                (double)M.nnz >= h->sells_min_avg * (double)M.nrows && M.nrows < INT32_MAX / 32 / 16) {
+                // short / long split: rows of <= 16 entries as width-16 SELL-32 (padding never loaded)
+                int64_t nshort = 0;
+                for (int64_t r = 0; r < M.nrows; ++r) nshort += (off32[r + 1] - off32[r] <= 16);
+                if ((double)nshort >= 0.75 * (double)M.nrows) {
+                    std::vector<int32_t> col_h(M.nnz);
+                    std::vector<double> val_h(M.nnz);
+                    if (M.nnz) {
+                        CK(cudaMemcpy(col_h.data(), M.col, M.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+                        CK(cudaMemcpy(val_h.data(), M.val, M.nnz * sizeof(double), cudaMemcpyDeviceToHost));
+                    }
+                    const int64_t ns = (M.nrows + 31) / 32;
+                    const size_t tot = (size_t)ns * 32 * 16;
+                    std::vector<double> sv(tot, 0.0);
+                    std::vector<int32_t> sc(tot, 0);
+                    std::vector<uint8_t> ln(M.nrows + 16, 0);
+                    std::vector<int32_t> lr;
+                    for (int64_t r = 0; r < M.nrows; ++r) {
+                        const int32_t len = off32[r + 1] - off32[r];
+                        if (len > 16) {
+                            ln[r] = 255;
+                            lr.push_back((int32_t)r);
+                            continue;
+                        }
+                        ln[r] = (uint8_t)len;
+                        const int64_t b0 = (r >> 5) * 32 * 16 + (r & 31);
+                        for (int32_t k = 0; k < len; ++k) {
+                            sv[b0 + 32 * k] = val_h[off32[r] + k];
+                            sc[b0 + 32 * k] = col_h[off32[r] + k];
+                        }
+                    }
+                    TRY(dalloc(&M.spv, tot));
+                    TRY(dalloc(&M.spc, tot));
+                    TRY(dalloc(&M.splen, ln.size()));
+                    TRY(dalloc(&M.splong, lr.size() + 1));
+                    CK(cudaMemcpy(M.spv, sv.data(), tot * sizeof(double), cudaMemcpyHostToDevice));
+                    CK(cudaMemcpy(M.spc, sc.data(), tot * sizeof(int32_t), cudaMemcpyHostToDevice));
+                    CK(cudaMemcpy(M.splen, ln.data(), ln.size(), cudaMemcpyHostToDevice));
+                    if (!lr.empty()) CK(cudaMemcpy(M.splong, lr.data(), lr.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                    M.sp_nlong = (int)lr.size();
+                    int nb1 = 0, nb2 = 0;
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb1, (const void *)spmv_split_short_fn(EPI_RESID),
+                                                                     VEC_SPMV_THREADS, 0));
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, (const void *)spmv_split_long_fn(EPI_RESID),
+                                                                     VEC_SPMV_THREADS, 0));
+                    M.sp_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
+                                                                           (int64_t)h->sm_count * std::max(nb1, 1)));
+                    M.sp_lgrid = (int)std::max<int64_t>(1, std::min<int64_t>((M.sp_nlong + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
+                                                                            (int64_t)h->sm_count * std::max(nb2, 1)));
+                    h->max_grid = std::max(h->max_grid, M.sp_grid + M.sp_lgrid);
+                }
+            }
+            if (!M.uval && !M.uval_s && !M.spv && h->sells && !longrows && !h->lanes_override && h->sells_sigma >= 32 &&
                 M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm &&
                 (M.nrows <= h->sells_max_rows || h->sells_buckets) &&
                 (double)M.nnz >= h->sells_min_avg * (double)M.nrows) {
@@ -2920,6 +3017,7 @@ int amg_matrix_layout(amg_t *h, int level, int which, int *layout)
     // same precedence as launch_spmv
     *layout = M.ntiles == 0           ? AMG_LAYOUT_EMPTY
               : (M.uval && h->symm)   ? AMG_LAYOUT_SYMD
+              : (M.spv && h->split)    ? AMG_LAYOUT_SPLIT
               : (M.sv_s && h->sells)   ? AMG_LAYOUT_SELL_SORTED
               : (M.uval_s && h->sellu) ? AMG_LAYOUT_SELL_UNIFORM
               : M.sbeg                ? (M.scol ? AMG_LAYOUT_SELL : AMG_LAYOUT_SELL_PAT)

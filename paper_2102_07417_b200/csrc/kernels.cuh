@@ -270,6 +270,36 @@ __device__ __forceinline__ void grid_finalize(double v, double *partials, unsign
     }
 }
 
+// As grid_finalize, for the second kernel of a pair: this grid's partials go
+// to partials[base + blockIdx.x] and the last CTA folds partials[0, base + gridDim.x)
+// (the first kernel, complete before this one passed griddepcontrol.wait,
+// wrote partials[0, base)).
+template <int NT>
+__device__ __forceinline__ void grid_finalize_pair(double v, double *partials, int base, unsigned *ticket, int fin,
+                                                   PcgCtl *ctl)
+{
+    __shared__ int s_last;
+    __shared__ double s_red[NT / 32];
+    if (threadIdx.x == 0) {
+        partials[base + blockIdx.x] = v;
+        __threadfence();
+        unsigned t = atomicAdd(ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        double a = 0.0;
+        for (int i = threadIdx.x; i < base + (int)gridDim.x; i += NT) a += __ldcg(partials + i);
+        a = block_sum<NT>(a, s_red);
+        if (threadIdx.x == 0) {
+            apply_fin(fin, a, ctl);
+            *ticket = 0u;
+            __threadfence();
+        }
+    }
+}
+
 // ---------------------------------------------------------------- SpMV
 
 // numpy's pairwise sum over products read through `P` (leaf: n <= 128).
@@ -1993,6 +2023,112 @@ __global__ void __launch_bounds__(256) l2_prefetch(const PrefetchRange *__restri
         const PrefetchRange q = r[k];
         for (long long off = t * 128; off < q.bytes; off += nt * 128)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(q.p + off));
+    }
+}
+
+// ---------------------------------------------------------------- SpMV, short / long row split
+
+// Fine-level ragged matrices (the FSAI transpose G^T_0: 1..46 entries, 90% of
+// rows <= 16): rows of <= 16 entries run as uniform SELL-32 slices of width
+// 16 with their columns and lengths fetched one row ahead and padding slots
+// never loaded (spmv_split_short, rows in their natural order, so lanes stay
+// on neighbouring rows); the remaining long rows (len byte 255) are skipped
+// there and summed by spmv_split_long over a row list.  Both write disjoint
+// rows of y with the same epilogue; a dot / finalize spans both kernels
+// (short: per-CTA partials; long: folds them with its own).
+struct SplitArgs {
+    const double *val;      // short part: SELL-32, width 16
+    const int32_t *col;
+    const uint8_t *len;     // 255: long row
+    const int32_t *lrows;   // long rows (ascending)
+    int nlong;
+    int short_grid;         // partials written by the short kernel
+};
+
+template <int EPI>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, 3) spmv_split_short(const SpmvArgs a, const SplitArgs q, int nrows)
+{
+    __shared__ double red[VEC_SPMV_THREADS / 32];
+    constexpr int FL = 16;
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const int nthreads = gridDim.x * VEC_SPMV_THREADS;
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    const double *__restrict__ x = a.x;
+    double dacc = 0.0;
+    int row = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x;
+    int c[FL];
+    int len = 0;
+    auto fetch = [&](int r) {
+        const int base = (r >> 5) * (32 * FL) + (r & 31);
+        len = __ldg(q.len + r);
+        const int l = len == 255 ? 0 : len;
+#pragma unroll
+        for (int k = 0; k < FL; ++k) c[k] = (k < l) ? __ldg(q.col + base + 32 * k) : r;
+    };
+    if (row < nrows) fetch(row);
+    for (; row < nrows; row += nthreads) {
+        const int base = (row >> 5) * (32 * FL) + (row & 31);
+        const int clen = len;
+        const int l = clen == 255 ? 0 : clen;
+        double p[FL];
+#pragma unroll
+        for (int k = 0; k < FL; ++k) p[k] = (k < l) ? prod(__ldg(q.val + base + 32 * k), __ldg(x + c[k])) : 0.0;
+        if (row + nthreads < nrows) fetch(row + nthreads);
+        if (clen == 255) continue;  // long row: spmv_split_long
+        double bv = 0.0, wv = 0.0;
+        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
+        if (want_dot && !self_dot) wv = a.dotw[row];
+        const double sum = ref_sum_fixed<FL>(p, l);
+        double yv;
+        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+        else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+        else yv = sum;
+        a.y[row] = yv;
+        if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        const double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
+        if (threadIdx.x == 0) a.partials[blockIdx.x] = v;
+    }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_split_long(const SpmvArgs a, const SplitArgs q)
+{
+    __shared__ double red[VEC_SPMV_THREADS / 32];
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    const double *__restrict__ x = a.x;
+    double dacc = 0.0;
+    for (int t = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x; t < q.nlong; t += gridDim.x * VEC_SPMV_THREADS) {
+        const int row = __ldg(q.lrows + t);
+        const int lo = __ldg(a.off + row), hi = __ldg(a.off + row + 1);
+        auto P = [&](int k) -> double { return prod(__ldg(a.val + lo + k), __ldg(x + __ldg(a.col + lo + k))); };
+        const double sum = ref_row_sum<true>(P, hi - lo);
+        double bv = 0.0, wv = 0.0;
+        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
+        if (want_dot && !self_dot) wv = a.dotw[row];
+        double yv;
+        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+        else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+        else yv = sum;
+        a.y[row] = yv;
+        if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        const double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
+        grid_finalize_pair<VEC_SPMV_THREADS>(v, a.partials, (want_dot || a.fin != FIN_NONE) ? q.short_grid : 0,
+                                             a.ticket, a.fin, a.ctl);
     }
 }
 

@@ -178,6 +178,27 @@ def test_spmv_sorted_sell_bit_identical(maxlen):
         dh.close()
 
 
+@pytest.mark.parametrize("maxlen", [16, 46, 200])
+def test_spmv_short_long_split_bit_identical(maxlen):
+    # fine-level ragged rows: <= 16 entries on width-16 SELL-32 slices, the rest from a row list
+    from paper_2102_07417_b200.problems import Csr
+
+    rng = np.random.default_rng(maxlen + 1)
+    n = 60000
+    lens = np.minimum(rng.geometric(1.0 / 8.0, n), maxlen)
+    lens[:4] = [0, 1, maxlen, 17]
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    m = Csr(n, n, off, cols, rng.uniform(-1, 1, off[-1]))
+    x = rng.uniform(-1, 1, n)
+    want = O.spmv(m, x)
+    for split in (1, 0):
+        dh = amg.DeviceHierarchy.from_matrices([m], options={"split": split, "sells_max_rows": 20000, "symm": 0})
+        assert (dh.layout(0, "a") == "split") == bool(split)
+        np.testing.assert_array_equal(dh.matrix(0, "a")(x), want)
+        dh.close()
+
+
 def test_spmv_symmetric_layout_rejects_one_ulp_asymmetry():
     from paper_2102_07417_b200.problems import Csr
 
