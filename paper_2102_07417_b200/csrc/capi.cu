@@ -89,6 +89,7 @@ struct DevMat {
     int uW = 0, u_grid = 0, u_plen = 0;  // u_plen: padding slots skipped (short ragged rows)
     int nudiag = 0, sym_grid = 0, sym_fl = 0, symf_grid = 0, sym_blocked = 0;  // sym_fl: fixed-slot kernel width (0: none)
     int32_t *pstart = nullptr;   // padded-aligned layout (spmv_vec), nullptr if unused
+    int32_t *pperm = nullptr;    // its visiting order (rows grouped by round count), nullptr = natural
     double *pval = nullptr;
     int32_t *pcol = nullptr;
     int pad_grid = 0;
@@ -247,6 +248,8 @@ struct amg_handle {
     int symd_blocked = 1;         // symmetric layout stored slice-blocked (32 rows x nu diagonals contiguous)
     int symd_gminb = 5;           // round-by-round symmetric kernel: min CTAs/SM 5, 6 or 8
     int symd_minb = 4;            // fixed-slot 32-wide kernel: min CTAs/SM (register budget) 3, 4 or 5
+    int vec_groups = 0;           // padded CSR on > 1M rows: visit rows grouped by round count (measured slower:
+                                  // G^T_0 83 -> 109..124 us, lanes lose the contiguity of neighbouring rows)
     int split = 0;                // fine-level ragged matrices: short rows (<= 16) as SELL-32 + long-row list
                                   // (measured slower on config-2 G^T_0: 121 vs 85 us)
     int sells = 1;                // sorted SELL-32 (sigma window below) where natural slices pad > 10%
@@ -817,7 +820,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         TRY(launch_k(h, spmv_leafsum_fn(epi), grid_cap ? std::min(grid_cap, M.leafsum_grid) : M.leafsum_grid,
                      DIRECT_THREADS, 0, a, la, (int)M.nrows));
     } else if (M.pstart) {
-        PadArgs pa{M.pstart, M.pval, M.pcol};
+        PadArgs pa{M.pstart, M.pval, M.pcol, h->vec_pipe ? nullptr : M.pperm};
         TRY(launch_k(h, spmv_vec_fn(epi, h->vec_pipe), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
                      pa, (int)M.nrows));
     } else if (h->kernel == 3 && M.nwtiles > 0) {
@@ -1406,7 +1409,7 @@ void amg_destroy(amg_t *h)
     auto F = [](void *p) { if (p) cudaFree(p); };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.spv); F(M.spc); F(M.splong); F(M.splen); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s);
+            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.pperm); F(M.spv); F(M.spc); F(M.splong); F(M.splen); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s);
             symd_slot_give(h->device, M.sym_slot);
             M.sym_slot = -1;
             symd_tab_give(h->device, M.sym_tab, M.sym_ntab);
@@ -1457,6 +1460,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "small_rows_per_sm") { h->small_rows_per_sm = (int)value; return AMG_OK; }
     if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
     if (k == "symm") { h->symm = value ? 1 : 0; return AMG_OK; }
+    if (k == "vec_groups") { h->vec_groups = (int)value; return AMG_OK; }
     if (k == "split") { h->split = value ? 1 : 0; return AMG_OK; }
     if (k == "sells") { h->sells = (int)value; return AMG_OK; }
     if (k == "sells_max_rows") { h->sells_max_rows = value; return AMG_OK; }
@@ -2211,6 +2215,19 @@ int amg_finalize(amg_t *h)
                 CK(cudaMemcpy(M.pstart, ps.data(), ps.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
                 CK(cudaMemcpy(M.pcol, pc.data(), pc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
                 CK(cudaMemcpy(M.pval, pv.data(), pv.size() * sizeof(double), cudaMemcpyHostToDevice));
+                if (h->vec_groups > 0 && M.nrows > h->sells_max_rows) {
+                    // warps see rows needing the same number of 8-entry rounds (less divergence on ragged
+                    // fine-level rows); natural order inside a group keeps the x gathers local
+                    std::vector<int32_t> ord(M.nrows);
+                    for (int64_t r = 0; r < M.nrows; ++r) ord[r] = (int32_t)r;
+                    auto grp = [&](int32_t r) {
+                        const int n1 = off32[r + 1] - off32[r] - 1;
+                        return n1 < 8 ? 0 : std::min(1 + (n1 - 8) / 8, h->vec_groups);
+                    };
+                    std::stable_sort(ord.begin(), ord.end(), [&](int32_t x1, int32_t x2) { return grp(x1) < grp(x2); });
+                    TRY(dalloc(&M.pperm, ord.size()));
+                    CK(cudaMemcpy(M.pperm, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                }
                 // stencil patterns: every row's (col - row) tuple from a small dictionary
                 if (h->patterns && h->nranks == 1 && M.ncols == M.nrows) {
                     std::vector<int32_t> rel, beg;

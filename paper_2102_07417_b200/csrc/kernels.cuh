@@ -1221,6 +1221,8 @@ struct PadArgs {
     const int32_t *pstart;  // nrows + 1 padded row starts (== 3 mod 4)
     const double *pval;     // padded values (16-byte aligned base)
     const int32_t *pcol;    // padded columns
+    const int32_t *perm;    // visiting order of the rows (nullptr: natural): rows grouped by the number
+                            // of 8-entry rounds they need, natural order inside a group
 };
 
 // PIPE: software pipeline -- row offsets two rows ahead and the first
@@ -1249,10 +1251,13 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, PIPE ? 3 : 4) spmv_vec(const
         nca = len > 1 ? __ldg(c4) : make_int4(0, 0, 0, 0);
         ncb = len > 5 ? __ldg(c4 + 1) : make_int4(0, 0, 0, 0);
     };
+    const int32_t *__restrict__ perm = pa.perm;
+    int prow = 0;  // row visited at position `row` (== row without a permutation)
     if (row < nrows) {
-        nlo = __ldg(a.off + row);
-        nhi = __ldg(a.off + row + 1);
-        nps = __ldg(pa.pstart + row);
+        prow = perm ? __ldg(perm + row) : row;
+        nlo = __ldg(a.off + prow);
+        nhi = __ldg(a.off + prow + 1);
+        nps = __ldg(pa.pstart + prow);
     }
     if constexpr (PIPE) {
         if (row + nthreads < nrows) {
@@ -1261,7 +1266,8 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, PIPE ? 3 : 4) spmv_vec(const
         }
         if (row < nrows) fetch_cols(nps, nhi - nlo);
     }
-    for (; row < nrows; row += nthreads) {
+    for (int pos = row; pos < nrows; pos += nthreads) {
+        const int row = prow;
         const int len = nhi - nlo;
         const int ps = nps;
         int c0 = 0;
@@ -1273,15 +1279,16 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, PIPE ? 3 : 4) spmv_vec(const
             nlo = 0;
             nhi = len2;
             nps = ps2;
-            if (row + nthreads < nrows) fetch_cols(nps, nhi);
-            if (row + 2 * nthreads < nrows) {
-                len2 = __ldg(a.off + row + 2 * nthreads + 1) - __ldg(a.off + row + 2 * nthreads);
-                ps2 = __ldg(pa.pstart + row + 2 * nthreads);
+            if (pos + nthreads < nrows) fetch_cols(nps, nhi);  // PIPE: natural order only (no perm)
+            if (pos + 2 * nthreads < nrows) {
+                len2 = __ldg(a.off + pos + 2 * nthreads + 1) - __ldg(a.off + pos + 2 * nthreads);
+                ps2 = __ldg(pa.pstart + pos + 2 * nthreads);
             }
-        } else if (row + nthreads < nrows) {
-            nlo = __ldg(a.off + row + nthreads);
-            nhi = __ldg(a.off + row + nthreads + 1);
-            nps = __ldg(pa.pstart + row + nthreads);
+        } else if (pos + nthreads < nrows) {
+            prow = perm ? __ldg(perm + pos + nthreads) : pos + nthreads;
+            nlo = __ldg(a.off + prow);
+            nhi = __ldg(a.off + prow + 1);
+            nps = __ldg(pa.pstart + prow);
         }
         double bv = 0.0, wv = 0.0;
         if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
