@@ -136,12 +136,26 @@ struct LevelD {
     } fz;
 };
 
+std::mutex g_alloc_mu;
+std::unordered_map<const void *, size_t> g_alloc_size;  // allocation sizes (L2 access-policy windows)
+
+size_t alloc_bytes(const void *p)
+{
+    std::lock_guard<std::mutex> g(g_alloc_mu);
+    auto it = g_alloc_size.find(p);
+    return it == g_alloc_size.end() ? 0 : it->second;
+}
+
 template <class T>
 int dalloc(T **p, size_t count)
 {
     size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
     cudaError_t e = cudaMalloc((void **)p, bytes);
     if (e != cudaSuccess) return fail(AMG_E_CUDA, std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    {
+        std::lock_guard<std::mutex> g(g_alloc_mu);
+        g_alloc_size[*p] = bytes;
+    }
     e = cudaMemset(*p, 0, bytes);
     if (e != cudaSuccess) return fail(AMG_E_CUDA, cudaGetErrorString(e));
     return AMG_OK;
@@ -206,6 +220,10 @@ struct amg_handle {
     int device = 0, rank = 0, nranks = 1;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;           // side stream: L2 prefetch of the tail levels
+    const void *win_ptr = nullptr;         // L2 persisting window of the next launches (l2_persist)
+    size_t win_bytes = 0;
+    bool persist_now = false;
+    size_t win_max = 0;
     cudaEvent_t pf_fork = nullptr, pf_join = nullptr;
     PrefetchRange *pf_ranges = nullptr;    // device copy of the tail matrices' ranges
     int pf_n = 0;
@@ -289,6 +307,9 @@ struct amg_handle {
                                  // footprint delays the cluster launch; streamed from L2 by default)
     int cluster = 16;
     int coarse_pipe = 1;          // pipelined per-warp Cholesky substitution
+    int l2_persist = 0;           // levels [l2_persist_from, l2_persist] mark their matrix values L2-persisting
+    int l2_persist_from = 1;      // (measured slower: the set-aside starves the level-0 gathers)
+    int l2_persist_mb = 0;        // persisting set-aside (0 = device maximum)
     int side_prefetch = 1;        // side-stream L2 prefetch of the tail matrices during the level above it
     int tail_prefetch = 1;        // tail kernel prefetches its streamed matrices into L2 before griddepcontrol.wait
     int tail_level = 0;  // 0 = disabled
@@ -577,11 +598,24 @@ static int launch_k(amg_t *h, void (*kern)(KArgs...), int grid, int block, size_
     cfg.blockDim = dim3((unsigned)block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = h->stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (h->pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (h->persist_now && h->win_ptr && h->win_bytes) {
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[na].val.accessPolicyWindow.base_ptr = const_cast<void *>(h->win_ptr);
+        attr[na].val.accessPolicyWindow.num_bytes = std::min(h->win_bytes, h->win_max);
+        attr[na].val.accessPolicyWindow.hitRatio = 1.0f;
+        attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = h->pdl ? 1 : 0;
+    cfg.numAttrs = na;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
     if (e != cudaSuccess) return fail(AMG_E_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e));
     ++h->launches;
@@ -718,6 +752,16 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         return AMG_OK;
     }
     TRY(exchange(h, M, const_cast<double *>(x)));
+    if (h->persist_now) {  // the active layout's value array
+        const void *vp = (M.uval && h->symm) ? (const void *)M.uval
+                         : (M.spv && h->split) ? (const void *)M.spv
+                         : (M.sv_s && h->sells) ? (const void *)M.sv_s
+                         : (M.uval_s && h->sellu) ? (const void *)M.uval_s
+                         : M.sbeg ? (const void *)M.sval
+                         : M.pstart ? (const void *)M.pval : (const void *)M.val;
+        h->win_ptr = vp;
+        h->win_bytes = alloc_bytes(vp);
+    }
     if (h->grid_per_sm > 0) {  // global cap on CTAs per SM (tuning)
         const int c = h->grid_per_sm * h->sm_count;
         grid_cap = grid_cap ? std::min(grid_cap, c) : c;
@@ -1052,6 +1096,7 @@ static int enqueue_vcycle(amg_t *h, int k, const double *y, double *x, const int
     if (k == nl - 1) return launch_coarse(h, y, x, g1, fin, dotw);
     LevelD &L = h->lv[k];
     LevelD &C = h->lv[k + 1];
+    h->persist_now = h->l2_persist > 0 && k >= h->l2_persist_from && k <= h->l2_persist && h->win_max > 0;
     if (!h->collect && h->side_prefetch && h->pf_n > 0 && h->tail_level > 0 && k == h->tail_level - 1) {
         CK(cudaEventRecord(h->pf_fork, h->stream));
         CK(cudaStreamWaitEvent(h->side, h->pf_fork, 0));
@@ -1071,6 +1116,7 @@ static int enqueue_vcycle(amg_t *h, int k, const double *y, double *x, const int
     TRY(launch_spmv(h, L.m[AMG_PT], r, yc, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, g1, nullptr));
     if (agglom) TRY(allgather_level(h, k + 1, C.y));
     TRY(enqueue_vcycle(h, k + 1, C.y, C.x, g1, FIN_NONE, nullptr));
+    h->persist_now = h->l2_persist > 0 && k >= h->l2_persist_from && k <= h->l2_persist && h->win_max > 0;
     const bool tail_on_p = (h->nu2 == 0);
     TRY(launch_spmv(h, L.m[AMG_P], C.x, x, h->nu1 > 0 ? EPI_ADD : EPI_PLAIN, x, 0.0, tail_on_p ? dotw : nullptr,
                     tail_on_p ? fin : FIN_NONE, g1, nullptr));
@@ -1106,6 +1152,7 @@ static int enqueue_pcg_body(amg_t *h, cudaGraphConditionalHandle handle, int use
     TRY(launch_spmv(h, A, h->x, h->r, EPI_RESID, h->b, 0.0, h->r, FIN_TRUE, act, &h->ctl->need_true, gcap));
     // z = M r ; rz_new = r.z ; beta                     (:87-90)
     TRY(enqueue_vcycle(h, 0, h->r, h->z, act, FIN_RZ, h->r));
+    h->persist_now = false;
     if (h->lv.size() == 1) {
         // the coarse kernel carried the dot already
     }
@@ -1422,6 +1469,10 @@ void amg_destroy(amg_t *h)
         L.fz.slot = -1;
     }
     F(h->pf_ranges);
+    if (h->win_max > 0) {  // give the persisting L2 set-aside back (process-wide device limit)
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+        cudaCtxResetPersistingL2Cache();
+    }
     if (h->side) cudaStreamDestroy(h->side);
     if (h->pf_fork) cudaEventDestroy(h->pf_fork);
     if (h->pf_join) cudaEventDestroy(h->pf_join);
@@ -1478,6 +1529,9 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "symd_fixed") { h->symd_fixed = (int)value; return AMG_OK; }
     if (k == "symd_chunked") { h->symd_chunked = value ? 1 : 0; return AMG_OK; }
     if (k == "coarse_pipe") { h->coarse_pipe = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
+    if (k == "l2_persist_from") { h->l2_persist_from = (int)value; return AMG_OK; }
+    if (k == "l2_persist_mb") { h->l2_persist_mb = (int)value; return AMG_OK; }
+    if (k == "l2_persist") { h->l2_persist = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "side_prefetch") { h->side_prefetch = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "tail_prefetch") { h->tail_prefetch = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "symd_classes") { h->symd_classes = (int)value; return AMG_OK; }
@@ -2610,6 +2664,16 @@ int amg_finalize(amg_t *h)
     TRY(dalloc(&h->ctl, 1));
     CK(cudaMallocHost((void **)&h->ctl_h, sizeof(PcgCtl)));
     std::memset(h->ctl_h, 0, sizeof(PcgCtl));
+    if (!container && h->l2_persist > 0) {
+        int maxp = 0, maxw = 0;
+        CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device));
+        CK(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, h->device));
+        if (maxp > 0 && maxw > 0) {
+            const size_t want = h->l2_persist_mb > 0 ? std::min((size_t)maxp, (size_t)h->l2_persist_mb << 20) : (size_t)maxp;
+            CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+            h->win_max = (size_t)maxw;
+        }
+    }
     if (!container && h->fused) TRY(build_fused(h));
     if (!container) TRY(build_tail(h));
     h->finalized = true;

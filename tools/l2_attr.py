@@ -1,0 +1,5 @@
+import ctypes
+from cuda.bindings import runtime as rt
+for a in ("cudaDevAttrMaxPersistingL2CacheSize", "cudaDevAttrMaxAccessPolicyWindowSize", "cudaDevAttrL2CacheSize"):
+    e, v = rt.cudaDeviceGetAttribute(getattr(rt.cudaDeviceAttr, a), 0)
+    print(a, v)
