@@ -279,6 +279,7 @@ struct amg_handle {
     double sells_min_avg = 4.0;   // ... for matrices averaging at least this many entries per row
     int64_t sells_max_rows = 1 << 20;  // ... and at most this many rows (sorting costs fine-grid rows their gather
                                        // locality: config-2 G^T_0 85 -> 134 us; coarse A_1 18 -> 13 us)
+    int vec_minb = 4;             // padded-CSR kernel: min CTAs per SM (register budget) 4, 5 or 6
     int vec_pipe = 0;             // padded-CSR kernel with the first round's columns fetched one row ahead
     int sellu_short = 1;          // ... and for rows of <= 8 entries at any padding, padding slots skipped
     int sellu = 1;                // uniform-width SELL-32 for rows of <= 16 entries padding <= 10% (e.g. FSAI G)
@@ -503,9 +504,9 @@ static SpmvPatFn spmv_pat_fn(int epi)
 
 typedef void (*SpmvVecFn)(const SpmvArgs, const PadArgs, int);
 
-static SpmvVecFn spmv_vec_fn(int epi, bool pipe = false)
+static SpmvVecFn spmv_vec_fn(int epi, bool pipe = false, int vminb = 4)
 {
-#define AMG_V(E) return pipe ? spmv_vec<E, true> : spmv_vec<E, false>;
+#define AMG_V(E) return pipe ? spmv_vec<E, true> : (vminb >= 6 ? spmv_vec<E, false, 6> : vminb == 5 ? spmv_vec<E, false, 5> : spmv_vec<E, false, 4>);
     switch (epi) {
     case EPI_PLAIN: AMG_V(EPI_PLAIN)
     case EPI_RESID: AMG_V(EPI_RESID)
@@ -865,7 +866,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
                      DIRECT_THREADS, 0, a, la, (int)M.nrows));
     } else if (M.pstart) {
         PadArgs pa{M.pstart, M.pval, M.pcol, h->vec_pipe ? nullptr : M.pperm};
-        TRY(launch_k(h, spmv_vec_fn(epi, h->vec_pipe), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
+        TRY(launch_k(h, spmv_vec_fn(epi, h->vec_pipe, h->vec_minb), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
                      pa, (int)M.nrows));
     } else if (h->kernel == 3 && M.nwtiles > 0) {
         SpmvArgs w = a;
@@ -1520,6 +1521,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "sells_max_pad") { h->sells_max_pad = (int)value; return AMG_OK; }
     if (k == "sells_sigma") { h->sells_sigma = (int)value; return AMG_OK; }
     if (k == "sells_min_avg10") { h->sells_min_avg = value / 10.0; return AMG_OK; }
+    if (k == "vec_minb") { h->vec_minb = (int)value; return AMG_OK; }
     if (k == "vec_pipe") { h->vec_pipe = value ? 1 : 0; return AMG_OK; }
     if (k == "sellu_short") { h->sellu_short = value ? 1 : 0; return AMG_OK; }
     if (k == "sellu") { h->sellu = value ? 1 : 0; return AMG_OK; }
@@ -2400,7 +2402,7 @@ int amg_finalize(amg_t *h)
                     }
                 }
                 int nb = 0;
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_vec_fn(EPI_RESID, h->vec_pipe), VEC_SPMV_THREADS, 0));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_vec_fn(EPI_RESID, h->vec_pipe, h->vec_minb), VEC_SPMV_THREADS, 0));
                 M.pad_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
                                                                         (int64_t)h->sm_count * std::max(nb, 1)));
                 h->max_grid = std::max(h->max_grid, M.pad_grid);

@@ -1229,8 +1229,8 @@ struct PadArgs {
 // round's columns (entry 0 and the aligned 8 after it) one row ahead, so a
 // row's first-round value loads and x gathers leave together (fewer CTAs:
 // the prefetched columns cost registers).
-template <int EPI, bool PIPE>
-__global__ void __launch_bounds__(VEC_SPMV_THREADS, PIPE ? 3 : 4) spmv_vec(const SpmvArgs a, const PadArgs pa, int nrows)
+template <int EPI, bool PIPE, int MINB = 4>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, PIPE ? 3 : MINB) spmv_vec(const SpmvArgs a, const PadArgs pa, int nrows)
 {
     __shared__ double red[VEC_SPMV_THREADS / 32];
     pdl_launch();
