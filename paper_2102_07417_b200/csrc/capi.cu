@@ -103,6 +103,7 @@ struct DevMat {
     int32_t *sq_cta = nullptr;   // SELL streamed by bulk copies (spmv_sellq), nullptr if unused
     int sq_grid = 0, sq_stage = 0, sq_stages = 0, sq_smem = 0;
     int2 *leaf = nullptr;        // long-row leaves (spmv_leaves + spmv_leafsum), nullptr if unused
+    int lrow_ok = 0;             // rows short enough for the one-warp-per-row kernel (spmv_lrow)
     int32_t *row_leaf = nullptr;
     double *lsum = nullptr;
     int nleaves = 0, leaf_grid = 0, leafsum_grid = 0;
@@ -279,6 +280,8 @@ struct amg_handle {
     double sells_min_avg = 4.0;   // ... for matrices averaging at least this many entries per row
     int64_t sells_max_rows = 1 << 20;  // ... and at most this many rows (sorting costs fine-grid rows their gather
                                        // locality: config-2 G^T_0 85 -> 134 us; coarse A_1 18 -> 13 us)
+    int lrow = 0;                 // long rows: one warp per row (spmv_lrow) instead of the two-pass leaf kernels
+                                  // (bit-identical; measured slower on config 3: A1 425 vs 155 us)
     int vec_minb = 4;             // padded-CSR kernel: min CTAs per SM (register budget) 4, 5 or 6
     int vec_pipe = 0;             // padded-CSR kernel with the first round's columns fetched one row ahead
     int sellu_short = 1;          // ... and for rows of <= 8 entries at any padding, padding slots skipped
@@ -471,6 +474,19 @@ static SpmvSplitLongFn spmv_split_long_fn(int epi)
     case EPI_AXPYW: return spmv_split_long<EPI_AXPYW>;
     case EPI_SETW: return spmv_split_long<EPI_SETW>;
     default: return spmv_split_long<EPI_ADD>;
+    }
+}
+
+typedef void (*SpmvLrowFn)(const SpmvArgs, int);
+
+static SpmvLrowFn spmv_lrow_fn(int epi)
+{
+    switch (epi) {
+    case EPI_PLAIN: return spmv_lrow<EPI_PLAIN>;
+    case EPI_RESID: return spmv_lrow<EPI_RESID>;
+    case EPI_AXPYW: return spmv_lrow<EPI_AXPYW>;
+    case EPI_SETW: return spmv_lrow<EPI_SETW>;
+    default: return spmv_lrow<EPI_ADD>;
     }
 }
 
@@ -856,6 +872,10 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         PatArgs pa{M.pstart, M.pval, M.pid, M.prel, M.pbeg, M.npat, M.nrel};
         TRY(launch_k(h, spmv_pat_fn(epi), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
                      pa, (int)M.nrows));
+    } else if (M.leaf && M.lrow_ok && h->lrow) {
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + LR_WARPS - 1) / LR_WARPS, (int64_t)h->sm_count * 2));
+        TRY(launch_k(h, spmv_lrow_fn(epi), grid_cap ? std::min(grid_cap, g) : g, LR_WARPS * 32,
+                     (size_t)LR_WARPS * LR_BUF * sizeof(double), a, (int)M.nrows));
     } else if (M.leaf) {
         LeafArgs la{M.leaf, M.nleaves, M.lsum, M.row_leaf};
         SpmvArgs a1 = a;  // leaf pass: no reduction
@@ -1521,6 +1541,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "sells_max_pad") { h->sells_max_pad = (int)value; return AMG_OK; }
     if (k == "sells_sigma") { h->sells_sigma = (int)value; return AMG_OK; }
     if (k == "sells_min_avg10") { h->sells_min_avg = value / 10.0; return AMG_OK; }
+    if (k == "lrow") { h->lrow = value ? 1 : 0; return AMG_OK; }
     if (k == "vec_minb") { h->vec_minb = (int)value; return AMG_OK; }
     if (k == "vec_pipe") { h->vec_pipe = value ? 1 : 0; return AMG_OK; }
     if (k == "sellu_short") { h->sellu_short = value ? 1 : 0; return AMG_OK; }
@@ -2202,6 +2223,14 @@ int amg_finalize(amg_t *h)
             const bool longrows = h->long_avg > 0 && !h->lanes_override && M.nrows > 0 &&
                                   (double)M.nnz / (double)M.nrows > (double)h->long_avg;
             if (longrows) {
+                int64_t mx = 0;
+                for (int64_t r = 0; r < M.nrows; ++r) mx = std::max<int64_t>(mx, off32[r + 1] - off32[r]);
+                M.lrow_ok = mx <= 6000 ? 1 : 0;  // <= LR_MAXLEAF leaves per row
+                if (M.lrow_ok) {
+                    for (int e = 0; e < 5; ++e)
+                        CK(cudaFuncSetAttribute((const void *)spmv_lrow_fn(e), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(LR_WARPS * LR_BUF * sizeof(double))));
+                }
                 std::vector<int2> lv;
                 std::vector<int32_t> rl(M.nrows + 1);
                 int sb[32], sm[32];

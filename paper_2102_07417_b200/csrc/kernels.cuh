@@ -1085,6 +1085,127 @@ __global__ void __launch_bounds__(DIRECT_THREADS) spmv_leafsum(const SpmvArgs a,
     }
 }
 
+// ---------------------------------------------------------------- SpMV, long rows: one warp per row
+
+// Rows of hundreds to thousands of entries (the Galerkin coarse operators of
+// the elasticity hierarchy: 293..951 entries per row on average).  One warp
+// per row: the row's products are formed with coalesced 32-wide loads into a
+// per-warp shared buffer (whole pairwise leaves at a time, up to LR_BUF
+// entries), then every (leaf, accumulator) pair is one lane: numpy's 8
+// strided accumulators of a leaf are summed in order by 8 lanes, combined
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) with an xor-shuffle butterfly inside
+// the 8-lane group, the leaf's tail added in order, and the leaf sums folded
+// in numpy's recursive tree (leaf_tree_combine) -- bit-identical to
+// np.add.reduceat, in one kernel without a leaf-sum round trip through HBM.
+constexpr int LR_WARPS = 8;
+constexpr int LR_BUF = 1024;     // products staged per warp (8 KB)
+constexpr int LR_MAXLEAF = 96;   // rows up to ~6000 entries
+
+template <int EPI>
+__global__ void __launch_bounds__(LR_WARPS * 32, 2) spmv_lrow(const SpmvArgs a, int nrows)
+{
+    extern __shared__ __align__(16) double lr_buf[];  // LR_WARPS * LR_BUF
+    __shared__ int2 s_leaf[LR_WARPS][LR_MAXLEAF];
+    __shared__ double s_lsum[LR_WARPS][LR_MAXLEAF];
+    __shared__ double red[LR_WARPS];
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *buf = lr_buf + warp * LR_BUF;
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    const double *__restrict__ x = a.x;
+    double dacc = 0.0;
+    for (int row = blockIdx.x * LR_WARPS + warp; row < nrows; row += gridDim.x * LR_WARPS) {
+        const int lo = __ldg(a.off + row), n = __ldg(a.off + row + 1) - lo;
+        double sum = 0.0;
+        if (n > 0) {
+            const int m = n - 1, s0 = lo + 1;  // products after p0
+            double tree = 0.0;
+            if (m < 8) {
+                if (lane == 0)
+                    for (int i = 0; i < m; ++i) tree = add(tree, prod(__ldg(a.val + s0 + i), __ldg(x + __ldg(a.col + s0 + i))));
+            } else {
+                int nleaf = 0;
+                if (lane == 0) {  // pre-order leaves (left to right), as numpy's recursion visits them
+                    int st_s[24], st_n[24], sp = 0;
+                    st_s[sp] = 0;
+                    st_n[sp++] = m;
+                    while (sp > 0) {
+                        --sp;
+                        int b = st_s[sp], c = st_n[sp];
+                        while (c > 128) {
+                            const int c2 = pairwise_split(c);
+                            st_s[sp] = b + c2;
+                            st_n[sp++] = c - c2;
+                            c = c2;
+                        }
+                        if (nleaf < LR_MAXLEAF) s_leaf[warp][nleaf] = make_int2(b, c);
+                        ++nleaf;
+                    }
+                }
+                nleaf = __shfl_sync(0xffffffffu, nleaf, 0);
+                __syncwarp();
+                if (nleaf > LR_MAXLEAF) __trap();  // host checks the longest row (build: lrow only if it fits)
+                for (int L0 = 0; L0 < nleaf;) {
+                    const int b0 = s_leaf[warp][L0].x;
+                    int L1 = L0 + 1;
+                    while (L1 < nleaf && s_leaf[warp][L1].x + s_leaf[warp][L1].y - b0 <= LR_BUF) ++L1;
+                    const int e_end = s_leaf[warp][L1 - 1].x + s_leaf[warp][L1 - 1].y;
+#pragma unroll 4
+                    for (int e = b0 + lane; e < e_end; e += 32)
+                        buf[e - b0] = prod(__ldg(a.val + s0 + e), __ldg(x + __ldg(a.col + s0 + e)));
+                    __syncwarp();
+                    for (int L = L0 + (lane >> 3); L - (lane >> 3) < L1; L += 4) {
+                        const bool act = L < L1;
+                        const int j = lane & 7;
+                        int st = 0, len = 0;
+                        if (act) {
+                            st = s_leaf[warp][L].x - b0;
+                            len = s_leaf[warp][L].y;
+                        }
+                        const int main = len - len % 8;
+                        double acc = 0.0;
+                        if (act) {
+                            acc = buf[st + j];
+                            for (int k = j + 8; k < main; k += 8) acc = add(acc, buf[st + k]);
+                        }
+                        double t = add(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+                        t = add(t, __shfl_xor_sync(0xffffffffu, t, 2));
+                        t = add(t, __shfl_xor_sync(0xffffffffu, t, 4));
+                        if (act && j == 0) {
+                            for (int k = main; k < len; ++k) t = add(t, buf[st + k]);
+                            s_lsum[warp][L] = t;
+                        }
+                    }
+                    __syncwarp();
+                    L0 = L1;
+                }
+                if (lane == 0) tree = (nleaf == 1) ? s_lsum[warp][0] : leaf_tree_combine(s_lsum[warp], m);
+                __syncwarp();
+            }
+            if (lane == 0) sum = add(prod(__ldg(a.val + lo), __ldg(x + __ldg(a.col + lo))), tree);
+        }
+        if (lane == 0) {
+            double bv = 0.0;
+            if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
+            double yv;
+            if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+            else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+            else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+            else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+            else yv = sum;
+            a.y[row] = yv;
+            if (want_dot) dacc = fma(yv, self_dot ? yv : a.dotw[row], dacc);
+        }
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v = block_sum<LR_WARPS * 32>(dacc, red);
+        grid_finalize<LR_WARPS * 32>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
 // ---------------------------------------------------------------- SpMV, warp tiles
 
 // Warp-tile SpMV: rows are cut into small tiles (<= wt_nnz entries, <= 32

@@ -49,7 +49,7 @@ def test_spmv_ragged_rows_bit_identical(name, lanes):
 
 
 @pytest.mark.parametrize("nrows,mean", [(700, 300), (20000, 200)])
-@pytest.mark.parametrize("lanes", [0, 1, 8])
+@pytest.mark.parametrize("lanes", [0, 1, 8, -1])
 def test_spmv_long_rows_bit_identical(nrows, mean, lanes):
     # rows of 0..~3*mean entries: numpy's recursive pairwise split (n > 128);
     # lanes=0 takes the leaf-list kernels, the overrides the direct kernel's tree walk
@@ -63,7 +63,8 @@ def test_spmv_long_rows_bit_identical(nrows, mean, lanes):
     cols = np.concatenate([np.sort(rng.choice(ncols, l, replace=False)) for l in lens]).astype(np.int32)
     m = Csr(nrows, ncols, off, cols, rng.uniform(-1, 1, off[-1]))
     x = rng.uniform(-1, 1, ncols)
-    dh = amg.DeviceHierarchy.from_matrices([m], options={"lanes": lanes})
+    opts = {"lrow": 1} if lanes < 0 else {"lanes": lanes}  # -1: one warp per row (spmv_lrow)
+    dh = amg.DeviceHierarchy.from_matrices([m], options=opts)
     np.testing.assert_array_equal(dh.matrix(0, "a")(x), O.spmv(m, x))
     dh.close()
 
