@@ -56,3 +56,24 @@ def test_no_gpu_no_fallback():
 
     with pytest.raises(amg.AmgError):
         amg.DeviceHierarchy(device=0)
+
+
+def test_layout_names_follow_the_header_enum():
+    # dh.layout() maps amg_matrix_layout's AMG_LAYOUT_* ids to names by position
+    from paper_2102_07417_b200.device import DeviceHierarchy
+
+    src = open(os.path.join(ROOT, "include", "amgb200.h")).read()
+    ids = {m.group(1).lower(): int(m.group(2)) for m in re.finditer(r"AMG_LAYOUT_([A-Z_]+)\s*=\s*(\d+)", src)}
+    names = list(DeviceHierarchy.LAYOUTS)
+    assert len(ids) == len(names)
+    aliases = {"sell_pat": "sell_pattern"}
+    for name, i in ids.items():
+        assert names[i] == aliases.get(name, name), (name, i, names[i])
+
+
+def test_stats_struct_matches_header():
+    # the ctypes mirror of amg_stats_t must list the header's fields in order
+    src = open(os.path.join(ROOT, "include", "amgb200.h")).read()
+    body = src[src.index("typedef struct amg_stats {"):src.index("} amg_stats_t;")]
+    fields = re.findall(r"^\s*(?:double|int64_t|int)\s+([a-z0-9_]+);", body, re.M)
+    assert fields == [f for f, _ in _capi.Stats._fields_]
