@@ -280,6 +280,7 @@ struct amg_handle {
     double sells_min_avg = 4.0;   // ... for matrices averaging at least this many entries per row
     int64_t sells_max_rows = 1 << 20;  // ... and at most this many rows (sorting costs fine-grid rows their gather
                                        // locality: config-2 G^T_0 85 -> 134 us; coarse A_1 18 -> 13 us)
+    int rz_sep = 0;               // PCG: r.z in a separate dot kernel instead of the V-cycle's last SpMV
     int lrow = 0;                 // long rows: one warp per row (spmv_lrow) instead of the two-pass leaf kernels
                                   // (bit-identical; measured slower on config 3: A1 425 vs 155 us)
     int vec_minb = 4;             // padded-CSR kernel: min CTAs per SM (register budget) 4, 5 or 6
@@ -1172,7 +1173,12 @@ static int enqueue_pcg_body(amg_t *h, cudaGraphConditionalHandle handle, int use
     // relres <= rtol: true residual check              (:81-86)
     TRY(launch_spmv(h, A, h->x, h->r, EPI_RESID, h->b, 0.0, h->r, FIN_TRUE, act, &h->ctl->need_true, gcap));
     // z = M r ; rz_new = r.z ; beta                     (:87-90)
-    TRY(enqueue_vcycle(h, 0, h->r, h->z, act, FIN_RZ, h->r));
+    if (h->rz_sep) {  // r.z as its own fixed-order dot after the V-cycle
+        TRY(enqueue_vcycle(h, 0, h->r, h->z, act, FIN_NONE, nullptr));
+        TRY(launch_dot(h, h->r, h->z, n, FIN_RZ, act, nullptr));
+    } else {
+        TRY(enqueue_vcycle(h, 0, h->r, h->z, act, FIN_RZ, h->r));
+    }
     h->persist_now = false;
     if (h->lv.size() == 1) {
         // the coarse kernel carried the dot already
@@ -1474,7 +1480,12 @@ void amg_destroy(amg_t *h)
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    auto F = [](void *p) { if (p) cudaFree(p); };
+    auto F = [](void *p) {
+        if (!p) return;
+        cudaFree(p);
+        std::lock_guard<std::mutex> g(g_alloc_mu);
+        g_alloc_size.erase(p);
+    };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
             F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.pperm); F(M.spv); F(M.spc); F(M.splong); F(M.splen); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s);
@@ -1541,6 +1552,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "sells_max_pad") { h->sells_max_pad = (int)value; return AMG_OK; }
     if (k == "sells_sigma") { h->sells_sigma = (int)value; return AMG_OK; }
     if (k == "sells_min_avg10") { h->sells_min_avg = value / 10.0; return AMG_OK; }
+    if (k == "rz_sep") { h->rz_sep = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "lrow") { h->lrow = value ? 1 : 0; return AMG_OK; }
     if (k == "vec_minb") { h->vec_minb = (int)value; return AMG_OK; }
     if (k == "vec_pipe") { h->vec_pipe = value ? 1 : 0; return AMG_OK; }
