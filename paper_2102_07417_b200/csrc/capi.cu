@@ -316,10 +316,13 @@ struct amg_handle {
     int l2_persist_from = 1;      // (measured slower: the set-aside starves the level-0 gathers)
     int l2_persist_mb = 0;        // persisting set-aside (0 = device maximum)
     int side_prefetch = 1;        // side-stream L2 prefetch of the tail matrices during the level above it
+    int tail_dsm = 0;             // tail level vectors in distributed shared memory
     int tail_prefetch = 1;        // tail kernel prefetches its streamed matrices into L2 before griddepcontrol.wait
     int tail_level = 0;  // 0 = disabled
     TailOp *tail_ops = nullptr;
     TailMat *tail_mats = nullptr;
+    int2 *tail_vecs = nullptr;    // DSMEM slots of the tail's level vectors (tail_dsm)
+    int tail_nvecs = 0;
     int tail_nmats = 0;
     int32_t *tail_splits = nullptr;
     int tail_prod_off = 0;
@@ -1001,9 +1004,10 @@ static int launch_tail(amg_t *h, const int *g1)
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = h->pdl ? 2 : 1;
+    const TailVecs tv{h->tail_vecs, h->tail_nvecs};
     cudaError_t e = cudaLaunchKernelEx(&cfg, tail_vcycle, (const TailOp *)h->tail_ops, h->tail_nops,
                                        (const TailMat *)h->tail_mats, h->tail_nmats, (const int32_t *)h->tail_splits,
-                                       h->tail_prod_off, coarse_args(h), g1, h->trace);
+                                       h->tail_prod_off, coarse_args(h), g1, h->trace, tv);
     if (e != cudaSuccess) return fail(AMG_E_CUDA, std::string("tail launch failed: ") + cudaGetErrorString(e));
     ++h->launches;
     return AMG_OK;
@@ -1400,6 +1404,46 @@ static int build_tail(amg_t *h)
         if (e != cudaSuccess) { cudaGetLastError(); nclusters = 0; }
     }
     if (nclusters < 1) return AMG_OK;  // cluster shape not resident here: per-op kernels are used
+    for (auto &o : best_ops) o.xs = o.ys = o.bs = -1;
+    if (h->tail_dsm) {
+        // level vectors below the tail's entry / exit (y, x of its first level stay in global memory)
+        struct V { const double *p; int shift; int off; };
+        std::vector<V> vs;
+        size_t off = ((size_t)best_smem + 15) & ~(size_t)15;
+        auto add = [&](const double *p, int64_t n) {
+            int64_t r = (n + h->cluster - 1) / h->cluster, sh = 0;
+            while ((int64_t(1) << sh) < r) ++sh;
+            vs.push_back({p, (int)sh, (int)off});
+            off += ((size_t)8 << sh);
+        };
+        for (int k = best; k < nl; ++k) {
+            LevelD &L = h->lv[k];
+            if (k > best) {
+                add(L.y, L.n);
+                add(L.x, L.n);
+            }
+            add(L.r, L.n);
+            add(L.t, L.n);
+        }
+        if ((int)vs.size() <= TAIL_MAX_VECS && off <= (size_t)(optin - 64 * 1024 / 8)) {
+            auto slot = [&](const double *p) {
+                for (size_t q = 0; q < vs.size(); ++q)
+                    if (vs[q].p == p) return (int)q;
+                return -1;
+            };
+            for (auto &o : best_ops) {
+                o.xs = o.x ? slot(o.x) : -1;
+                o.ys = o.y ? slot(o.y) : -1;
+                o.bs = o.b ? slot(o.b) : -1;
+            }
+            std::vector<int2> tab(vs.size());
+            for (size_t q = 0; q < vs.size(); ++q) tab[q] = make_int2(vs[q].shift, vs[q].off);
+            TRY(dalloc(&h->tail_vecs, tab.size()));
+            CK(cudaMemcpy(h->tail_vecs, tab.data(), tab.size() * sizeof(int2), cudaMemcpyHostToDevice));
+            h->tail_nvecs = (int)tab.size();
+            best_smem = (int)off;
+        }
+    }
     TRY(dalloc(&h->tail_ops, best_ops.size()));
     CK(cudaMemcpy(h->tail_ops, best_ops.data(), best_ops.size() * sizeof(TailOp), cudaMemcpyHostToDevice));
     TRY(dalloc(&h->tail_mats, best_mats.size()));
@@ -1508,7 +1552,7 @@ void amg_destroy(amg_t *h)
     if (h->side) cudaStreamDestroy(h->side);
     if (h->pf_fork) cudaEventDestroy(h->pf_fork);
     if (h->pf_join) cudaEventDestroy(h->pf_join);
-    F(h->Lp); F(h->LU); F(h->dinv); F(h->binv); F(h->tail_ops); F(h->tail_mats); F(h->tail_splits); F(h->piv); F(h->partials); F(h->ticket); F(h->ctl);
+    F(h->Lp); F(h->LU); F(h->dinv); F(h->binv); F(h->tail_ops); F(h->tail_mats); F(h->tail_vecs); F(h->tail_splits); F(h->piv); F(h->partials); F(h->ticket); F(h->ctl);
     F(h->b); F(h->x); F(h->r); F(h->z); F(h->p); F(h->q); F(h->tmp_in); F(h->tmp_out); F(h->hist);
     for (auto *bp : h->bicg) F(bp);
     if (h->ctl_h) cudaFreeHost(h->ctl_h);
@@ -1568,6 +1612,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "l2_persist_mb") { h->l2_persist_mb = (int)value; return AMG_OK; }
     if (k == "l2_persist") { h->l2_persist = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "side_prefetch") { h->side_prefetch = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
+    if (k == "tail_dsm") { h->tail_dsm = value ? 1 : 0; return AMG_OK; }
     if (k == "tail_prefetch") { h->tail_prefetch = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "symd_classes") { h->symd_classes = (int)value; return AMG_OK; }
     if (k == "symd_blocked") { h->symd_blocked = value ? 1 : 0; return AMG_OK; }

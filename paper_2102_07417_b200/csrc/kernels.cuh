@@ -3207,12 +3207,48 @@ struct TailOp {
     int nrows;
     int mode;  // jacobi: 0 set, 1 accumulate
     int mat;   // SpMV: index into the staged-matrix table
+    int xs, ys, bs;  // distributed-shared-memory slots of x / y / b (-1: global memory)
     const double *x;
     double *y;
     const double *b;
     const double *d;
     double omega;
 };
+
+// Level vectors of the tail held in distributed shared memory (option
+// tail_dsm): element i of slot s lives in CTA i >> shift at byte offset
+// off + 8 (i & (2^shift - 1)) of the cluster's shared windows; gathers are
+// ld.shared::cluster (no L2 round trip), ordered by the cluster barriers.
+constexpr int TAIL_MAX_VECS = 48;
+struct TailVecs {
+    const int2 *slot;  // {shift, byte offset} per slot
+    int nslots;
+};
+
+__device__ __forceinline__ double tv_ld(const double *g, int s, int i, const int2 *sv, const char *smem)
+{
+    if (s < 0) return __ldcg(g + i);
+    const int2 d = sv[s];
+    const unsigned la = smem_u32(smem + d.y) + ((unsigned)(i & ((1 << d.x) - 1)) << 3);
+    unsigned ra;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"((unsigned)(i >> d.x)));
+    double v;
+    asm("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra));
+    return v;
+}
+
+__device__ __forceinline__ void tv_st(double *g, int s, int i, double v, const int2 *sv, const char *smem)
+{
+    if (s < 0) {
+        g[i] = v;
+        return;
+    }
+    const int2 d = sv[s];
+    const unsigned la = smem_u32(smem + d.y) + ((unsigned)(i & ((1 << d.x) - 1)) << 3);
+    unsigned ra;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"((unsigned)(i >> d.x)));
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+}
 
 // A distinct matrix of the tail and where each CTA's block of it lives.
 struct TailMat {
@@ -3261,13 +3297,14 @@ __device__ __forceinline__ unsigned long long globaltimer()
 // global memory (L2) in the op itself (matrices that did not fit the smem
 // budget); same phases and order as the staged variant.
 template <int EPI>
-__device__ __forceinline__ void tail_spmv_streamed(const TailOp &o, const TailMat &M, int r0, int r1, double *ps)
+__device__ __forceinline__ void tail_spmv_streamed(const TailOp &o, const TailMat &M, int r0, int r1, double *ps,
+                                                   const int2 *tvs, const char *smem)
 {
     const int k0 = __ldg(M.off + r0);
     const int nk = __ldg(M.off + r1) - k0;
     double bpre = 0.0;
     if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD)
-        if (r0 + (int)threadIdx.x < r1) bpre = __ldcg(o.b + r0 + threadIdx.x);
+        if (r0 + (int)threadIdx.x < r1) bpre = tv_ld(o.b, o.bs, r0 + threadIdx.x, tvs, smem);
     int lo = 0, hi = 0;
     if (r0 + (int)threadIdx.x < r1) {
         lo = __ldg(M.off + r0 + threadIdx.x) - k0;
@@ -3275,7 +3312,7 @@ __device__ __forceinline__ void tail_spmv_streamed(const TailOp &o, const TailMa
     }
 #pragma unroll 8
     for (int k = threadIdx.x; k < nk; k += TAIL_THREADS)
-        ps[k] = prod(__ldg(M.val + k0 + k), __ldcg(o.x + __ldg(M.col + k0 + k)));
+        ps[k] = prod(__ldg(M.val + k0 + k), tv_ld(o.x, o.xs, __ldg(M.col + k0 + k), tvs, smem));
     __syncthreads();
     for (int rr = threadIdx.x; rr < r1 - r0; rr += TAIL_THREADS) {
         if (rr != (int)threadIdx.x) {
@@ -3286,43 +3323,43 @@ __device__ __forceinline__ void tail_spmv_streamed(const TailOp &o, const TailMa
         const int row = r0 + rr;
         double bv = 0.0;
         if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD)
-            bv = (rr == (int)threadIdx.x) ? bpre : __ldcg(o.b + row);
+            bv = (rr == (int)threadIdx.x) ? bpre : tv_ld(o.b, o.bs, row, tvs, smem);
         double yv;
         if constexpr (EPI == EPI_PLAIN) yv = sv;
         else if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sv);
         else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(o.omega, sv));
         else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(o.omega, sv);
         else yv = add(bv, sv);
-        o.y[row] = yv;
+        tv_st(o.y, o.ys, row, yv, tvs, smem);
     }
 }
 
 template <int EPI>
 __device__ __forceinline__ void tail_spmv(const TailOp &o, int r0, int r1, const int32_t *os, const int32_t *cs,
-                                          const double *vs, double *ps)
+                                          const double *vs, double *ps, const int2 *tvs, const char *smem)
 {
     if (r1 <= r0) return;  // no rows on this CTA (CTA 0 runs the coarsest solve; its smem holds the factor)
     const int nk = os[r1 - r0];
     // prefetch the epilogue operand of this thread's first row with the gathers
     double bpre = 0.0;
     if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD)
-        if (r0 + (int)threadIdx.x < r1) bpre = __ldcg(o.b + r0 + threadIdx.x);
+        if (r0 + (int)threadIdx.x < r1) bpre = tv_ld(o.b, o.bs, r0 + threadIdx.x, tvs, smem);
 #pragma unroll 8
-    for (int k = threadIdx.x; k < nk; k += TAIL_THREADS) ps[k] = prod(vs[k], __ldcg(o.x + cs[k]));
+    for (int k = threadIdx.x; k < nk; k += TAIL_THREADS) ps[k] = prod(vs[k], tv_ld(o.x, o.xs, cs[k], tvs, smem));
     __syncthreads();
     for (int rr = threadIdx.x; rr < r1 - r0; rr += TAIL_THREADS) {
         const double s = row_sum_staged<1>(ps, 0, os[rr], os[rr + 1], 0, 0u);
         const int row = r0 + rr;
         double bv = 0.0;
         if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD)
-            bv = (rr == (int)threadIdx.x) ? bpre : __ldcg(o.b + row);
+            bv = (rr == (int)threadIdx.x) ? bpre : tv_ld(o.b, o.bs, row, tvs, smem);
         double yv;
         if constexpr (EPI == EPI_PLAIN) yv = s;
         else if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, s);
         else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(o.omega, s));
         else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(o.omega, s);
         else yv = add(bv, s);
-        o.y[row] = yv;
+        tv_st(o.y, o.ys, row, yv, tvs, smem);
     }
 }
 
@@ -3330,8 +3367,10 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
                                                              const TailMat *__restrict__ mats, int nmats,
                                                              const int32_t *__restrict__ splits, int prod_off,
                                                              const CoarseArgs c, const int *gate1,
-                                                             unsigned long long *trace)
+                                                             unsigned long long *trace, const TailVecs tvv)
 {
+    __shared__ int2 s_vec[TAIL_MAX_VECS];
+    for (int i = threadIdx.x; i < tvv.nslots; i += blockDim.x) s_vec[i] = tvv.slot[i];
     extern __shared__ __align__(16) double sh[];
     __shared__ TailOp s_ops[TAIL_MAX_OPS];
     __shared__ int s_split[TAIL_MAX_MATS][2];
@@ -3418,11 +3457,11 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
             if (moff < 0) {
                 const TailMat M = mats[o.mat];
                 switch (o.epi) {
-                case EPI_PLAIN: tail_spmv_streamed<EPI_PLAIN>(o, M, r0, r1, ps); break;
-                case EPI_RESID: tail_spmv_streamed<EPI_RESID>(o, M, r0, r1, ps); break;
-                case EPI_AXPYW: tail_spmv_streamed<EPI_AXPYW>(o, M, r0, r1, ps); break;
-                case EPI_SETW: tail_spmv_streamed<EPI_SETW>(o, M, r0, r1, ps); break;
-                default: tail_spmv_streamed<EPI_ADD>(o, M, r0, r1, ps); break;
+                case EPI_PLAIN: tail_spmv_streamed<EPI_PLAIN>(o, M, r0, r1, ps, s_vec, smem); break;
+                case EPI_RESID: tail_spmv_streamed<EPI_RESID>(o, M, r0, r1, ps, s_vec, smem); break;
+                case EPI_AXPYW: tail_spmv_streamed<EPI_AXPYW>(o, M, r0, r1, ps, s_vec, smem); break;
+                case EPI_SETW: tail_spmv_streamed<EPI_SETW>(o, M, r0, r1, ps, s_vec, smem); break;
+                default: tail_spmv_streamed<EPI_ADD>(o, M, r0, r1, ps, s_vec, smem); break;
                 }
                 cluster_barrier();
                 if (trace && t0 == 0) trace[i + 1] = globaltimer();
@@ -3432,25 +3471,25 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
             const int32_t *cs = reinterpret_cast<const int32_t *>(smem + moff + (((rcap + 1) * 4 + 15) & ~15));
             const double *vs = reinterpret_cast<const double *>(reinterpret_cast<const char *>(cs) + ((kcap * 4 + 15) & ~15));
             switch (o.epi) {
-            case EPI_PLAIN: tail_spmv<EPI_PLAIN>(o, r0, r1, os, cs, vs, ps); break;
-            case EPI_RESID: tail_spmv<EPI_RESID>(o, r0, r1, os, cs, vs, ps); break;
-            case EPI_AXPYW: tail_spmv<EPI_AXPYW>(o, r0, r1, os, cs, vs, ps); break;
-            case EPI_SETW: tail_spmv<EPI_SETW>(o, r0, r1, os, cs, vs, ps); break;
-            default: tail_spmv<EPI_ADD>(o, r0, r1, os, cs, vs, ps); break;
+            case EPI_PLAIN: tail_spmv<EPI_PLAIN>(o, r0, r1, os, cs, vs, ps, s_vec, smem); break;
+            case EPI_RESID: tail_spmv<EPI_RESID>(o, r0, r1, os, cs, vs, ps, s_vec, smem); break;
+            case EPI_AXPYW: tail_spmv<EPI_AXPYW>(o, r0, r1, os, cs, vs, ps, s_vec, smem); break;
+            case EPI_SETW: tail_spmv<EPI_SETW>(o, r0, r1, os, cs, vs, ps, s_vec, smem); break;
+            default: tail_spmv<EPI_ADD>(o, r0, r1, os, cs, vs, ps, s_vec, smem); break;
             }
         } else if (o.kind == TAIL_JACOBI) {
             for (int r = t0; r < o.nrows; r += nt) {
-                const double z = __dmul_rn(o.omega, __dmul_rn(__ldg(o.d + r), __ldcg(o.x + r)));
-                o.y[r] = o.mode ? add(__ldcg(o.y + r), z) : z;
+                const double z = __dmul_rn(o.omega, __dmul_rn(__ldg(o.d + r), tv_ld(o.x, o.xs, r, s_vec, smem)));
+                tv_st(o.y, o.ys, r, o.mode ? add(tv_ld(o.y, o.ys, r, s_vec, smem), z) : z, s_vec, smem);
             }
         } else if (rank == 0) {  // coarsest solve on CTA 0
             double *v = sh;
-            for (int r = threadIdx.x; r < c.n; r += blockDim.x) v[r] = __ldcg(o.x + r);
+            for (int r = threadIdx.x; r < c.n; r += blockDim.x) v[r] = tv_ld(o.x, o.xs, r, s_vec, smem);
             __syncthreads();
             if (c.kind == 0 && c.pipe && c.n <= 32 * (int)(blockDim.x / 32) && c.n <= 512) chol_solve_pipe(c.n, L, D, v, c.pipe > 1 ? c.pipe : 0);
             else if (c.kind == 0) chol_solve_cta(c.n, L, D, c.staged ? nullptr : MN, v);
             else lu_solve_cta(c.n, c.LU, c.piv, v);
-            for (int r = threadIdx.x; r < c.n; r += blockDim.x) o.y[r] = v[r];
+            for (int r = threadIdx.x; r < c.n; r += blockDim.x) tv_st(o.y, o.ys, r, v[r], s_vec, smem);
         }
         cluster_barrier();
         if (trace && t0 == 0) trace[i + 1] = globaltimer();

@@ -264,6 +264,17 @@ def test_coarse_solve_variants(name, opts, cases):
     assert _relerr(dh.vcycle(v["y"]), v["vcycle_z"]) <= 1e-12
 
 
+@pytest.mark.parametrize("name", HIER_CASES)
+def test_tail_vectors_in_distributed_shared_memory(name, cases):
+    # tail_dsm: the cluster tail keeps its level vectors in DSMEM -- same arithmetic, same bits
+    c, dh = _dh(name, cases)
+    _, dh2 = _dh(name, cases, tail_dsm=1)
+    v = c["vec"]
+    z = dh2.vcycle(v["y"])
+    assert _relerr(z, v["vcycle_z"]) <= 1e-12
+    np.testing.assert_array_equal(z, dh.vcycle(v["y"]))
+
+
 @pytest.mark.parametrize("n", [31, 33, 96, 200, 250])
 @pytest.mark.parametrize("pipe", [0, 1])
 def test_coarse_cholesky_sizes(n, pipe):

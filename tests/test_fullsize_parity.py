@@ -121,3 +121,14 @@ def test_fullsize_fused_fsai_steps_bit_identical(full, mode):
     np.testing.assert_array_equal(dh.vcycle(y), dh2.vcycle(y))
     dh2.close()
     dh.close()
+
+
+def test_fullsize_tail_dsm_bit_identical(full):
+    # the cluster tail with its level vectors in distributed shared memory
+    import paper_2102_07417_b200 as amg
+
+    name, h, dh = full
+    dh2 = amg.DeviceHierarchy.from_reference(h, options={"tail_dsm": 1})
+    y = np.random.default_rng(31).uniform(-1, 1, h.levels[0].a.nrows)
+    np.testing.assert_array_equal(dh2.vcycle(y), dh.vcycle(y))
+    dh2.close()
