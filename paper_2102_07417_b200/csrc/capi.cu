@@ -316,6 +316,8 @@ struct amg_handle {
     int l2_persist_from = 1;      // (measured slower: the set-aside starves the level-0 gathers)
     int l2_persist_mb = 0;        // persisting set-aside (0 = device maximum)
     int side_prefetch = 1;        // side-stream L2 prefetch of the tail matrices during the level above it
+    int tail_pcap = 16384;        // tail product buffer (entries); larger per-CTA blocks are processed in chunks
+    int tail_pcap_used = 0;
     int tail_dsm = 0;             // tail level vectors in distributed shared memory
     int tail_prefetch = 1;        // tail kernel prefetches its streamed matrices into L2 before griddepcontrol.wait
     int tail_level = 0;  // 0 = disabled
@@ -1004,7 +1006,7 @@ static int launch_tail(amg_t *h, const int *g1)
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = h->pdl ? 2 : 1;
-    const TailVecs tv{h->tail_vecs, h->tail_nvecs};
+    const TailVecs tv{h->tail_vecs, h->tail_nvecs, h->tail_pcap_used};
     cudaError_t e = cudaLaunchKernelEx(&cfg, tail_vcycle, (const TailOp *)h->tail_ops, h->tail_nops,
                                        (const TailMat *)h->tail_mats, h->tail_nmats, (const int32_t *)h->tail_splits,
                                        h->tail_prod_off, coarse_args(h), g1, h->trace, tv);
@@ -1360,6 +1362,7 @@ static int build_tail(amg_t *h)
         if ((int)mats.size() > TAIL_MAX_MATS) continue;
         // smem: CTA 0 = coarse area; CTAs >= 1 = [staged regions ...][products] (overlaid)
         const size_t base = (h->cluster > 1) ? 0 : ((coarse_bytes + 15) & ~(size_t)15);
+        if (!h->tail_stage) prod_cap = std::min(prod_cap, h->tail_pcap);  // streamed SpMVs run in chunks
         const size_t prod_bytes = (size_t)prod_cap * 8 + 16;
         if (base + prod_bytes > (size_t)budget || coarse_bytes > (size_t)budget) continue;
         std::vector<int> order(mats.size());
@@ -1384,6 +1387,7 @@ static int build_tail(amg_t *h)
         best_splits = splits;
         best_prod_off = (int)prod_off;
         best_smem = (int)std::max(prod_off + prod_bytes, coarse_bytes);
+        h->tail_pcap_used = prod_cap;
     }
     if (best == 0) return AMG_OK;
     TRY(raise_smem_caps(h->device));
@@ -1612,6 +1616,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "l2_persist_mb") { h->l2_persist_mb = (int)value; return AMG_OK; }
     if (k == "l2_persist") { h->l2_persist = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "side_prefetch") { h->side_prefetch = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
+    if (k == "tail_pcap") { h->tail_pcap = (int)value; return AMG_OK; }
     if (k == "tail_dsm") { h->tail_dsm = value ? 1 : 0; return AMG_OK; }
     if (k == "tail_prefetch") { h->tail_prefetch = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "symd_classes") { h->symd_classes = (int)value; return AMG_OK; }

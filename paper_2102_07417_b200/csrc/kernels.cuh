@@ -3223,6 +3223,7 @@ constexpr int TAIL_MAX_VECS = 48;
 struct TailVecs {
     const int2 *slot;  // {shift, byte offset} per slot
     int nslots;
+    int pcap;          // product-buffer capacity (entries): streamed SpMVs run their rows in chunks
 };
 
 __device__ __forceinline__ double tv_ld(const double *g, int s, int i, const int2 *sv, const char *smem)
@@ -3297,8 +3298,39 @@ __device__ __forceinline__ unsigned long long globaltimer()
 // global memory (L2) in the op itself (matrices that did not fit the smem
 // budget); same phases and order as the staged variant.
 template <int EPI>
+__device__ __forceinline__ void tail_spmv_streamed_chunk(const TailOp &o, const TailMat &M, int r0, int r1, double *ps,
+                                                         const int2 *tvs, const char *smem);
+
+// rows [r0, r1) in chunks whose products fit the buffer (pcap entries)
+template <int EPI>
 __device__ __forceinline__ void tail_spmv_streamed(const TailOp &o, const TailMat &M, int r0, int r1, double *ps,
-                                                   const int2 *tvs, const char *smem)
+                                                   const int2 *tvs, const char *smem, int pcap)
+{
+    __shared__ int s_re;
+    int rs = r0;
+    while (rs < r1) {
+        if (threadIdx.x == 0) {
+            const int base = __ldg(M.off + rs);
+            int lo = rs + 1, hi = r1;  // largest re in [rs + 1, r1] with off[re] - off[rs] <= pcap
+            if (__ldg(M.off + hi) - base <= pcap) lo = hi;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (__ldg(M.off + mid) - base <= pcap) lo = mid;
+                else hi = mid - 1;
+            }
+            s_re = lo;
+        }
+        __syncthreads();
+        const int re = s_re;
+        tail_spmv_streamed_chunk<EPI>(o, M, rs, re, ps, tvs, smem);
+        __syncthreads();
+        rs = re;
+    }
+}
+
+template <int EPI>
+__device__ __forceinline__ void tail_spmv_streamed_chunk(const TailOp &o, const TailMat &M, int r0, int r1, double *ps,
+                                                         const int2 *tvs, const char *smem)
 {
     const int k0 = __ldg(M.off + r0);
     const int nk = __ldg(M.off + r1) - k0;
@@ -3457,11 +3489,11 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
             if (moff < 0) {
                 const TailMat M = mats[o.mat];
                 switch (o.epi) {
-                case EPI_PLAIN: tail_spmv_streamed<EPI_PLAIN>(o, M, r0, r1, ps, s_vec, smem); break;
-                case EPI_RESID: tail_spmv_streamed<EPI_RESID>(o, M, r0, r1, ps, s_vec, smem); break;
-                case EPI_AXPYW: tail_spmv_streamed<EPI_AXPYW>(o, M, r0, r1, ps, s_vec, smem); break;
-                case EPI_SETW: tail_spmv_streamed<EPI_SETW>(o, M, r0, r1, ps, s_vec, smem); break;
-                default: tail_spmv_streamed<EPI_ADD>(o, M, r0, r1, ps, s_vec, smem); break;
+                case EPI_PLAIN: tail_spmv_streamed<EPI_PLAIN>(o, M, r0, r1, ps, s_vec, smem, tvv.pcap); break;
+                case EPI_RESID: tail_spmv_streamed<EPI_RESID>(o, M, r0, r1, ps, s_vec, smem, tvv.pcap); break;
+                case EPI_AXPYW: tail_spmv_streamed<EPI_AXPYW>(o, M, r0, r1, ps, s_vec, smem, tvv.pcap); break;
+                case EPI_SETW: tail_spmv_streamed<EPI_SETW>(o, M, r0, r1, ps, s_vec, smem, tvv.pcap); break;
+                default: tail_spmv_streamed<EPI_ADD>(o, M, r0, r1, ps, s_vec, smem, tvv.pcap); break;
                 }
                 cluster_barrier();
                 if (trace && t0 == 0) trace[i + 1] = globaltimer();

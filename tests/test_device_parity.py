@@ -254,7 +254,7 @@ def test_coarse_solve_and_vcycle(name, tail, cases):
 
 
 @pytest.mark.parametrize("opts", [{"coarse_pipe": 0}, {"coarse_pipe": 1}, {"coarse_pipe": 0, "tail_nnz": 0},
-                                  {"coarse_pipe": 1, "tail_nnz": 0}, {"tail_prefetch": 0}])
+                                  {"coarse_pipe": 1, "tail_nnz": 0}, {"tail_prefetch": 0}, {"tail_pcap": 64}])
 @pytest.mark.parametrize("name", [n for n in HIER_CASES if n != "poisson1d_50_single"])
 def test_coarse_solve_variants(name, opts, cases):
     # blocked and pipelined substitution, standalone and inside the cluster tail

@@ -132,3 +132,14 @@ def test_fullsize_tail_dsm_bit_identical(full):
     y = np.random.default_rng(31).uniform(-1, 1, h.levels[0].a.nrows)
     np.testing.assert_array_equal(dh2.vcycle(y), dh.vcycle(y))
     dh2.close()
+
+
+def test_fullsize_wider_tail_bit_identical(full):
+    # a cluster tail that starts one level higher, its SpMV blocks run in product chunks
+    import paper_2102_07417_b200 as amg
+
+    name, h, dh = full
+    dh2 = amg.DeviceHierarchy.from_reference(h, options={"tail_nnz": 2_000_000, "tail_pcap": 4096})
+    y = np.random.default_rng(37).uniform(-1, 1, h.levels[0].a.nrows)
+    np.testing.assert_array_equal(dh2.vcycle(y), dh.vcycle(y))
+    dh2.close()
