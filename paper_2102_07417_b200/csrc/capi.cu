@@ -263,6 +263,7 @@ struct amg_handle {
     int long_avg = 128;           // rows averaging more entries run leaf by leaf (spmv_leaves); 0 = off
     int small_rows_per_sm = 128;  // below sm_count * this many rows a matrix counts as small
     int patterns = 1;             // stencil-pattern layout for square operators with few row patterns
+    int symd_tsm = 0;             // round-by-round symmetric kernel: pattern table staged in smem instead of __constant__
     int symd_classes = 3;         // symmetric layout: try row classes r % K, K = 1..symd_classes
     int symd_blocked = 1;         // symmetric layout stored slice-blocked (32 rows x nu diagonals contiguous)
     int symd_gminb = 5;           // round-by-round symmetric kernel: min CTAs/SM 5, 6 or 8
@@ -386,10 +387,10 @@ static SpmvSellFn spmv_sell_fn(int epi, bool pat)
 
 typedef void (*SpmvSymFn)(const SpmvArgs, const SymArgs, int);
 
-static SpmvSymFn spmv_symd_fn(int epi, int minb = 5, bool blk = false)
+static SpmvSymFn spmv_symd_fn(int epi, int minb = 5, bool blk = false, bool tsm = false)
 {
 #define AMG_Y(E)                                                                                     \
-    return blk ? spmv_symd<E, 5, true>                                                                \
+    return (blk && tsm) ? spmv_symd<E, 5, true, true> : blk ? spmv_symd<E, 5, true>                   \
                : (minb >= 8 ? spmv_symd<E, 8, false> : minb == 6 ? spmv_symd<E, 6, false> : spmv_symd<E, 5, false>);
     switch (epi) {
     case EPI_PLAIN: AMG_Y(EPI_PLAIN)
@@ -839,11 +840,15 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
                 g = (int)((M.nrows + c - 1) / c);
             }
         }
-        SymArgs sa{M.uval, M.pid, M.sym_slot, chunk, M.sym_blocked ? 32 * M.nudiag : 0, M.sym_npad};
+        SymArgs sa{M.uval, M.pid, M.sym_slot, chunk, M.sym_blocked ? 32 * M.nudiag : 0, M.sym_npad,
+                   M.sym_tab, M.sym_ntab, M.npat};
+        const bool tsm = h->symd_tsm && M.sym_blocked && !fx;
+        const size_t tsm_bytes = tsm ? (size_t)M.sym_ntab * sizeof(int2) + (size_t)(M.npat + 1) * sizeof(int32_t) : 0;
         if (fx)
             TRY(launch_k(h, spmv_symd_fixed_fn(epi, M.sym_fl, h->symd_minb, M.sym_blocked), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
         else
-            TRY(launch_k(h, spmv_symd_fn(epi, h->symd_gminb, M.sym_blocked), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
+            TRY(launch_k(h, spmv_symd_fn(epi, h->symd_gminb, M.sym_blocked, tsm), g, VEC_SPMV_THREADS, tsm_bytes, a, sa,
+                         (int)M.nrows));
     } else if (M.spv && h->split) {
         SplitArgs qa{M.spv, M.spc, M.splen, M.splong, M.sp_nlong, 0};
         const bool red = dotw != nullptr || fin != FIN_NONE;
@@ -1619,6 +1624,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "tail_pcap") { h->tail_pcap = (int)value; return AMG_OK; }
     if (k == "tail_dsm") { h->tail_dsm = value ? 1 : 0; return AMG_OK; }
     if (k == "tail_prefetch") { h->tail_prefetch = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
+    if (k == "symd_tsm") { h->symd_tsm = value ? 1 : 0; return AMG_OK; }
     if (k == "symd_classes") { h->symd_classes = (int)value; return AMG_OK; }
     if (k == "symd_blocked") { h->symd_blocked = value ? 1 : 0; return AMG_OK; }
     if (k == "symd_gminb") { h->symd_gminb = (int)value; return AMG_OK; }

@@ -1785,6 +1785,7 @@ struct SymArgs {
     int w32;    // slice-blocked storage (BLK): the nu diagonals of each 32-row slice contiguous,
                 // uval[(i/32)*w32 + 32 j + i%32], w32 = 32 nu
     int npad;   // diagonal-major storage (!BLK): uval[j * npad + i]
+    int tbase, nent, npat;  // this matrix's entries in c_symd_tab (staged to smem by the TSM variant)
 };
 
 // value index of pattern entry {rel, y} for `row`
@@ -1839,10 +1840,18 @@ __device__ __forceinline__ double ref_row_sum(const PF &P, int len)
     return sum;
 }
 
-template <int EPI, int MINB, bool BLK>
+template <int EPI, int MINB, bool BLK, bool TSM = false>
 __global__ void __launch_bounds__(VEC_SPMV_THREADS, MINB) spmv_symd(const SpmvArgs a, const SymArgs sa, int nrows)
 {
     __shared__ double red[VEC_SPMV_THREADS / 32];
+    extern __shared__ int2 symd_stab[];  // TSM: the pattern table staged in smem (entries, then starts)
+    int32_t *symd_sbeg = reinterpret_cast<int32_t *>(symd_stab + (TSM ? sa.nent : 0));
+    if constexpr (TSM) {
+        for (int i = threadIdx.x; i < sa.nent; i += blockDim.x) symd_stab[i] = c_symd_tab[sa.tbase + i];
+        for (int i = threadIdx.x; i <= sa.npat; i += blockDim.x)
+            symd_sbeg[i] = c_symd_beg[sa.slot * SYMD_BEG_MAX + i] - sa.tbase;
+        __syncthreads();
+    }
     pdl_launch();
     pdl_wait();
     if (!gate_open(a.gate1, a.gate2)) return;
@@ -1861,10 +1870,10 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, MINB) spmv_symd(const SpmvAr
         double bv = 0.0, wv = 0.0;
         if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
         if (want_dot && !self_dot) wv = a.dotw[row];
-        const int rb = c_symd_beg[bbase + pid];
-        const int len = c_symd_beg[bbase + pid + 1] - rb;
+        const int rb = TSM ? symd_sbeg[pid] : c_symd_beg[bbase + pid];
+        const int len = (TSM ? symd_sbeg[pid + 1] : c_symd_beg[bbase + pid + 1]) - rb;
         auto P = [&](int k) -> double {
-            const int2 q = c_symd_tab[rb + k];
+            const int2 q = TSM ? symd_stab[rb + k] : c_symd_tab[rb + k];
             return prod(__ldg(uv + symd_vidx<BLK>(row, q.y, sa.w32)), __ldg(x + (row + q.x)));
         };
         const double sum = ref_row_sum<false>(P, len);  // pattern rows have <= 129 entries
