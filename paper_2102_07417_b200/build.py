@@ -23,6 +23,8 @@ NVCC_FLAGS = [
     "-I" + os.path.join(ROOT, "include"), "-I" + CSRC,
     "-diag-suppress", "550",
 ]
+FSAI_SRC = os.path.join(CSRC, "fsai_host.c")
+FSAI_LIB = os.path.join(PKG, "libamgfsai.so")
 ORACLE_SRC = os.path.join(ROOT, "oracle", "rowsum.c")
 ORACLE_LIB = os.path.join(ROOT, "oracle", "build", "liboracle_rowsum.so")
 
@@ -43,6 +45,16 @@ def build_library(force=False, verbose=False):
     return LIB
 
 
+def build_fsai_host(force=False, verbose=False):
+    """Host C helper that replays FSAI coefficients when a lean hierarchy cache is loaded."""
+    if force or _stale(FSAI_LIB, [FSAI_SRC]):
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-pthread", FSAI_SRC, "-o", FSAI_LIB, "-lm"]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+    return FSAI_LIB
+
+
 def build_oracle(force=False):
     """Compile oracle/rowsum.c (the plain-C checker, test infrastructure only)."""
     os.makedirs(os.path.dirname(ORACLE_LIB), exist_ok=True)
@@ -54,5 +66,6 @@ def build_oracle(force=False):
 
 if __name__ == "__main__":
     build_library(force="--force" in sys.argv, verbose=True)
+    build_fsai_host(force="--force" in sys.argv, verbose=True)
     build_oracle(force="--force" in sys.argv)
     print(LIB)

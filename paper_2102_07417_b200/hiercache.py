@@ -10,7 +10,7 @@ The in-memory form is a duck-typed mirror of ``AmgHierarchy`` / ``Level`` /
 ``Smoother`` (``amgkit/hierarchy.py:95-152``, ``amgkit/smoothers.py:26-43``)
 so that :meth:`DeviceHierarchy.from_reference` accepts either.
 
-Two storage modes:
+Three storage modes:
 
 * ``full``: every level's A, P, Pt, G, Gt is stored.
 * ``compact``: only what setup *chose* is stored -- G and P per level, the
@@ -21,6 +21,14 @@ Two storage modes:
   verified against SHA-256 digests of the reference's arrays recorded at
   export time.  Any mismatch raises: a hierarchy that differs from the
   reference's is never used silently.
+* ``lean``: ``compact`` without the FSAI coefficients.  Only G's final
+  sparsity pattern (and the rows that fell back to Jacobi) is stored; the
+  coefficients are a pure function of (A_k, pattern) -- one dense Cholesky
+  solve per row, ``amgkit/smoothers.py:80-96`` -- and are replayed with the
+  same LAPACK routines scipy calls (``csrc/fsai_host.c``), then checked
+  against the digest of the reference's G.  This is what makes the
+  16.8 M-row config-4 hierarchy shippable (its level-1 G alone holds 33 M
+  distinct fp64 coefficients).
 """
 from __future__ import annotations
 
@@ -45,6 +53,7 @@ __all__ = [
 ]
 
 FORMAT = "amgb200-hier-v1"
+MODES = ("full", "compact", "lean")
 
 
 @dataclass
@@ -153,6 +162,90 @@ def _load_csr(path):
         return Csr(nr, nc, z["row_offsets"], z["col_indices"], z["values"])
 
 
+def _save_csr_packed(path, m):
+    """CSR with row lengths and delta-coded columns (lean mode; deflates ~2x better)."""
+    lens = np.diff(np.asarray(m.row_offsets, dtype=np.int64))
+    d = np.diff(np.asarray(m.col_indices, dtype=np.int64), prepend=0).astype(np.int32)
+    lt = np.uint8 if lens.size == 0 or lens.max() < 256 else np.int32
+    np.savez_compressed(path, shape=np.asarray([m.nrows, m.ncols], dtype=np.int64), lens=lens.astype(lt),
+                        dcols=d, values=np.asarray(m.values, dtype=np.float64))
+
+
+def _load_csr_any(path):
+    with np.load(path) as z:
+        if "dcols" not in z.files:
+            nr, nc = (int(v) for v in z["shape"])
+            return Csr(nr, nc, z["row_offsets"], z["col_indices"], z["values"])
+        nr, nc = (int(v) for v in z["shape"])
+        offs = np.zeros(nr + 1, dtype=np.int64)
+        np.cumsum(z["lens"].astype(np.int64), out=offs[1:])
+        cols = np.cumsum(z["dcols"].astype(np.int64)).astype(np.int32)
+        return Csr(nr, nc, offs, cols, z["values"])
+
+
+def _save_pattern(path, g, fallback_mask=None):
+    """G's sparsity only: row lengths and i - col per entry (small integers; deflates well)."""
+    offs = np.asarray(g.row_offsets, dtype=np.int64)
+    lens = np.diff(offs)
+    rows = np.repeat(np.arange(g.nrows, dtype=np.int64), lens)
+    rel = (rows - np.asarray(g.col_indices, dtype=np.int64)).astype(np.int32)
+    if fallback_mask is None:
+        fb = np.zeros(0, dtype=np.int64)
+    else:
+        fb = np.flatnonzero(np.asarray(fallback_mask, dtype=bool)).astype(np.int64)
+    lt = np.uint8 if lens.size == 0 or lens.max() < 256 else np.int32
+    np.savez_compressed(path, shape=np.asarray([g.nrows, g.ncols], dtype=np.int64), lens=lens.astype(lt),
+                        rel=rel, fallback=fb)
+
+
+def _fallback_mask(a, g):
+    """Rows of G the reference reset to the Jacobi row (smoothers.py:94-97).
+
+    The reference keeps only their count; they are identified by replaying
+    every row and checking where the stored value is 1/sqrt(a_ii) instead of
+    the Cholesky result.  Raises unless the replay then reproduces G exactly
+    (a lean cache must rebuild the reference's G bit for bit).
+    """
+    from . import fsai_host
+
+    ref = np.asarray(g.values, dtype=np.float64)
+    vals = fsai_host.fsai_values(a, g.row_offsets, g.col_indices, None, allow_failed=True)
+    same = vals == ref
+    if same.all():
+        return None
+    lens = np.diff(np.asarray(g.row_offsets, dtype=np.int64))
+    rows = np.unique(np.repeat(np.arange(g.nrows), lens)[~same])
+    diag = _to_scipy(a).diagonal()
+    mask = np.zeros(g.nrows, dtype=np.uint8)
+    ok = (lens[rows] == 1) & (ref[g.row_offsets[rows]] == 1.0 / np.sqrt(diag[rows]))
+    if not ok.all():
+        raise ValueError(f"FSAI replay differs from the reference on row {int(rows[~ok][0])}: lean mode unusable")
+    mask[rows] = 1
+    vals = fsai_host.fsai_values(a, g.row_offsets, g.col_indices, mask)
+    if not np.array_equal(vals, ref):
+        raise ValueError("FSAI replay with the fallback rows does not reproduce the reference's G")
+    return mask
+
+
+def _load_pattern(path, a, threads=None):
+    from . import fsai_host
+
+    with np.load(path) as z:
+        nr, nc = (int(v) for v in z["shape"])
+        lens = z["lens"].astype(np.int64)
+        rel = z["rel"].astype(np.int64)
+        fb = z["fallback"]
+    offs = np.zeros(nr + 1, dtype=np.int64)
+    np.cumsum(lens, out=offs[1:])
+    cols = (np.repeat(np.arange(nr, dtype=np.int64), lens) - rel).astype(np.int32)
+    mask = None
+    if fb.size:
+        mask = np.zeros(nr, dtype=np.uint8)
+        mask[fb] = 1
+    vals = fsai_host.fsai_values(a, offs, cols, mask, threads=threads)
+    return Csr(nr, nc, offs, cols, vals)
+
+
 def save_hierarchy(h, directory, mode="full", generator=None, symmetrize_flags=None, extra=None):
     """Freeze a setup result (``amgkit.AmgHierarchy`` or :class:`HostHierarchy`).
 
@@ -174,11 +267,12 @@ def save_hierarchy(h, directory, mode="full", generator=None, symmetrize_flags=N
         "levels": [],
         "extra": extra or {},
     }
-    if mode == "compact" and generator is None:
-        raise ValueError("compact mode needs the generator name")
+    if mode not in MODES:
+        raise ValueError(f"mode must be one of {MODES}")
     for k, lvl in enumerate(levels):
         ent = {"n": int(lvl.a.nrows), "nnz_a": int(lvl.a.nnz), "digest": {"a": csr_digest(lvl.a)}}
-        if mode == "full":
+        if mode == "full" or (k == 0 and generator is None):
+            # compact / lean rebuild A_0 from the named generator when there is one
             _save_csr(os.path.join(directory, f"L{k}_a.npz"), lvl.a)
         sm = lvl.smoother
         if sm is not None:
@@ -186,12 +280,19 @@ def save_hierarchy(h, directory, mode="full", generator=None, symmetrize_flags=N
             if sm.kind == "jacobi":
                 np.save(os.path.join(directory, f"L{k}_invdiag.npy"), np.asarray(sm.inv_diag, dtype=np.float64))
             else:
-                _save_csr(os.path.join(directory, f"L{k}_g.npz"), sm.gmat)
+                if mode == "lean":
+                    _save_pattern(os.path.join(directory, f"L{k}_gpat.npz"), sm.gmat,
+                                  _fallback_mask(lvl.a, sm.gmat))
+                    ent["g_store"] = "pattern"
+                else:
+                    _save_csr(os.path.join(directory, f"L{k}_g.npz"), sm.gmat)
+                ent["digest"]["g"] = csr_digest(sm.gmat)
                 ent["digest"]["gt"] = csr_digest(sm.gmat_t)
                 if mode == "full":
                     _save_csr(os.path.join(directory, f"L{k}_gt.npz"), sm.gmat_t)
         if lvl.p is not None:
-            _save_csr(os.path.join(directory, f"L{k}_p.npz"), lvl.p)
+            (_save_csr_packed if mode == "lean" else _save_csr)(os.path.join(directory, f"L{k}_p.npz"), lvl.p)
+            ent["digest"]["p"] = csr_digest(lvl.p)
             ent["digest"]["pt"] = csr_digest(lvl.pt)
             if mode == "full":
                 _save_csr(os.path.join(directory, f"L{k}_pt.npz"), lvl.pt)
@@ -213,8 +314,14 @@ def save_hierarchy(h, directory, mode="full", generator=None, symmetrize_flags=N
     return man
 
 
-def load_hierarchy(directory, verify=True):
-    """Load a frozen hierarchy as a :class:`HostHierarchy`."""
+def load_hierarchy(directory, verify=True, threads=None):
+    """Load a frozen hierarchy as a :class:`HostHierarchy`.
+
+    ``lean`` caches replay the FSAI coefficients on ``threads`` host threads
+    (default: all available) and always verify them against the recorded
+    digest of the reference's G (the replay is the one step whose result
+    could depend on the host's LAPACK build).
+    """
     with open(os.path.join(directory, "manifest.json")) as f:
         man = json.load(f)
     if man.get("format") != FORMAT:
@@ -223,7 +330,7 @@ def load_hierarchy(directory, verify=True):
     levels = []
     a = None
     for k, ent in enumerate(man["levels"]):
-        if mode == "full":
+        if mode == "full" or (k == 0 and man.get("generator") is None):
             a = _load_csr(os.path.join(directory, f"L{k}_a.npz"))
         elif k == 0:
             a = build_config(man["generator"])
@@ -239,7 +346,15 @@ def load_hierarchy(directory, verify=True):
                 inv = np.load(os.path.join(directory, f"L{k}_invdiag.npy"))
                 lvl.smoother = HostSmoother("jacobi", sm["omega"], inv_diag=inv)
             else:
-                g = _load_csr(os.path.join(directory, f"L{k}_g.npz"))
+                if ent.get("g_store") == "pattern":
+                    g = _load_pattern(os.path.join(directory, f"L{k}_gpat.npz"), a, threads)
+                    if csr_digest(g) != ent["digest"]["g"]:
+                        raise ValueError(f"{directory}: level {k} replayed FSAI factor does not match the "
+                                         "reference digest (host LAPACK differs from the export host's?)")
+                else:
+                    g = _load_csr(os.path.join(directory, f"L{k}_g.npz"))
+                    if verify and "g" in ent["digest"] and csr_digest(g) != ent["digest"]["g"]:
+                        raise ValueError(f"{directory}: level {k} G does not match the reference digest")
                 gt_path = os.path.join(directory, f"L{k}_gt.npz")
                 gt = _load_csr(gt_path) if os.path.exists(gt_path) else transpose(g)
                 if verify and csr_digest(gt) != ent["digest"]["gt"]:
@@ -247,7 +362,9 @@ def load_hierarchy(directory, verify=True):
                 lvl.smoother = HostSmoother("fsai", sm["omega"], gmat=g, gmat_t=gt)
         p_path = os.path.join(directory, f"L{k}_p.npz")
         if os.path.exists(p_path):
-            lvl.p = _load_csr(p_path)
+            lvl.p = _load_csr_any(p_path)
+            if verify and "p" in ent["digest"] and csr_digest(lvl.p) != ent["digest"]["p"]:
+                raise ValueError(f"{directory}: level {k} P does not match the reference digest")
             pt_path = os.path.join(directory, f"L{k}_pt.npz")
             lvl.pt = _load_csr(pt_path) if os.path.exists(pt_path) else transpose(lvl.p)
             if verify and csr_digest(lvl.pt) != ent["digest"]["pt"]:

@@ -94,3 +94,70 @@ def test_report_emit_matches_reference_schema():
         ref = RefReport(**rep.__dict__)
         for fmt in ("json", "csv", "text"):
             assert report_emit(rep, fmt) == ref_emit(ref, fmt)
+
+
+@pytest.mark.parametrize("case", ["poisson7_12", "hetero27_10", "rtanis7_12", "elasticity_3_bamg",
+                                  "poisson1d_8_twogrid_fsai", "poisson2d_16_jacobi"])
+def test_lean_cache_replays_fsai_bit_for_bit(tmp_path, case):
+    # lean mode stores only G's pattern; the FSAI coefficients are replayed with
+    # scipy's own LAPACK (csrc/fsai_host.c) and must equal the reference's G
+    h = load_case(case)["h"]
+    d = str(tmp_path / "lean")
+    flags = [True] * h.n_levels
+    hiercache.save_hierarchy(h, d, mode="lean", symmetrize_flags=flags)
+    assert not any(f.endswith("_g.npz") for f in os.listdir(d))
+    h2 = hiercache.load_hierarchy(d, verify=True, threads=3)
+    for l1, l2 in zip(h.levels, h2.levels):
+        assert _eq(l1.a, l2.a)
+        if l1.smoother is not None and l1.smoother.kind == "fsai":
+            assert _eq(l1.smoother.gmat, l2.smoother.gmat)
+            assert _eq(l1.smoother.gmat_t, l2.smoother.gmat_t)
+        if l1.p is not None:
+            assert _eq(l1.p, l2.p)
+            assert _eq(l1.pt, l2.pt)
+
+
+def test_lean_replay_is_loud_on_a_wrong_pattern(tmp_path):
+    h = load_case("poisson7_12")["h"]
+    d = str(tmp_path / "lean")
+    hiercache.save_hierarchy(h, d, mode="lean", symmetrize_flags=[True] * h.n_levels)
+    z = dict(np.load(os.path.join(d, "L1_gpat.npz")))
+    rel = z["rel"].copy()
+    k = int(np.flatnonzero(rel > 1)[0])
+    rel[k] -= 1  # move one off-diagonal entry of G_1 to a neighbouring column
+    z["rel"] = rel
+    np.savez_compressed(os.path.join(d, "L1_gpat.npz"), **z)
+    with pytest.raises(ValueError, match="digest|FSAI replay"):
+        hiercache.load_hierarchy(d)
+
+
+def test_fsai_replay_matches_scipy_cho_solve():
+    # the replay against scipy.linalg.cho_factor / cho_solve called as the
+    # reference calls them (smoothers.py:84-91), on random SPD blocks
+    import scipy.linalg as sla
+    import scipy.sparse as sp
+    from paper_2102_07417_b200.fsai_host import fsai_values
+    from paper_2102_07417_b200.problems import Csr
+
+    rng = np.random.default_rng(3)
+    n = 60
+    m = sp.random(n, n, density=0.3, random_state=4) + sp.eye(n) * 0.1
+    a = (m @ m.T + sp.eye(n) * n).tocsr()
+    a.sort_indices()
+    A = Csr(n, n, a.indptr, a.indices, a.data)
+    dense = a.toarray()
+    offs, cols, want = [0], [], []
+    for i in range(n):
+        k = min(i, int(rng.integers(0, 9)))
+        pat = np.sort(rng.choice(i, size=k, replace=False)) if k else np.zeros(0, dtype=np.int64)
+        idx = np.concatenate([pat, [i]]).astype(np.int64)
+        sub = dense[np.ix_(idx, idx)]
+        c, low = sla.cho_factor(sub, lower=True, check_finite=False)
+        e = np.zeros(idx.size)
+        e[-1] = 1.0
+        y = sla.cho_solve((c, low), e, check_finite=False)
+        want.append(y / np.sqrt(y[-1]))
+        cols.extend(idx.tolist())
+        offs.append(len(cols))
+    got = fsai_values(A, np.asarray(offs), np.asarray(cols), threads=4)
+    np.testing.assert_array_equal(got, np.concatenate(want))
