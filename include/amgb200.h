@@ -169,6 +169,11 @@ enum {
     AMG_LAYOUT_SPLIT = 10        /* rows <= 16 entries as width-16 SELL-32, longer rows from a row list */
 };
 int amg_matrix_layout(amg_t *h, int level, int which, int *layout);
+/* Diagnostics (roofline numerator): *stored = bytes the SpMV kernel of the
+ * chosen layout must stream per launch (values, column / pattern ids, row
+ * metadata; padding slots it never loads are not counted), *vectors = 8 B per
+ * column of x (read once) + 8 B per row of y (written once). */
+int amg_matrix_bytes(amg_t *h, int level, int which, int64_t *stored, int64_t *vectors);
 /* Tuning / diagnostics: 0 = auto. */
 int amg_set_option(amg_t *h, const char *key, int64_t value);
 

@@ -26,7 +26,7 @@ EXPORTS = (
     "amg_set_cycle", "amg_finalize", "amg_local_rows", "amg_spmv", "amg_smoother",
     "amg_coarse_solve", "amg_vcycle", "amg_pcg", "amg_get_stats", "amg_set_option", "amg_time_spmv",
     "amg_nccl_unique_id", "amg_set_halo", "amg_set_agglomeration", "amg_bicgstab",
-    "amg_matrix_layout",
+    "amg_matrix_layout", "amg_matrix_bytes",
 )
 
 
@@ -91,6 +91,7 @@ def lib():
         "amg_set_agglomeration": (I32, [P, I32]),
         "amg_bicgstab": (I32, [P, P, P, D, I32, I32, P, P, P, P, P, P, P, I32]),
         "amg_matrix_layout": (I32, [P, I32, I32, ctypes.POINTER(I32)]),
+        "amg_matrix_bytes": (I32, [P, I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

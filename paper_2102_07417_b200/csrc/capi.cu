@@ -108,6 +108,7 @@ struct DevMat {
     double *lsum = nullptr;
     int nleaves = 0, leaf_grid = 0, leafsum_grid = 0;
     HaloPlan halo;  // exchange feeding this matrix's halo columns (nranks > 1)
+    int64_t lbytes[12] = {};  // per layout: bytes its kernel must stream (values, indices, row metadata)
 };
 
 struct LevelD {
@@ -1317,6 +1318,7 @@ static int build_tail(amg_t *h)
         std::vector<int32_t> splits;
         std::vector<int> mat_level;
         int prod_cap = 0;
+        int longest_row = 1;  // a streamed chunk holds at least one whole row
         for (auto &o : ops) {
             if (o.kind != TAIL_SPMV) continue;
             const DevMat *M = mats_raw[o.mode];
@@ -1333,6 +1335,7 @@ static int build_tail(amg_t *h)
                 T.val = M->val;
                 T.split = (int)splits.size();
                 const int64_t nnz = off[M->nrows];
+                for (int64_t q = 0; q < M->nrows; ++q) longest_row = std::max(longest_row, off[q + 1] - off[q]);
                 // CTA 0 runs the coarsest solve and owns no SpMV rows; rows are
                 // balanced by stored entries over CTAs 1..cluster-1
                 const int workers = std::max(1, h->cluster - 1);
@@ -1368,6 +1371,7 @@ static int build_tail(amg_t *h)
         // smem: CTA 0 = coarse area; CTAs >= 1 = [staged regions ...][products] (overlaid)
         const size_t base = (h->cluster > 1) ? 0 : ((coarse_bytes + 15) & ~(size_t)15);
         if (!h->tail_stage) prod_cap = std::min(prod_cap, h->tail_pcap);  // streamed SpMVs run in chunks
+        prod_cap = std::max(prod_cap, longest_row);  // ... of whole rows: the chunk search assumes one row fits
         const size_t prod_bytes = (size_t)prod_cap * 8 + 16;
         if (base + prod_bytes > (size_t)budget || coarse_bytes > (size_t)budget) continue;
         std::vector<int> order(mats.size());
@@ -1621,7 +1625,11 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "l2_persist_mb") { h->l2_persist_mb = (int)value; return AMG_OK; }
     if (k == "l2_persist") { h->l2_persist = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "side_prefetch") { h->side_prefetch = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
-    if (k == "tail_pcap") { h->tail_pcap = (int)value; return AMG_OK; }
+    if (k == "tail_pcap") {
+        if (value < 1 || value > (1 << 24)) return fail(AMG_E_ARG, "tail_pcap must be in [1, 2^24]");
+        h->tail_pcap = (int)value;
+        return AMG_OK;
+    }
     if (k == "tail_dsm") { h->tail_dsm = value ? 1 : 0; return AMG_OK; }
     if (k == "tail_prefetch") { h->tail_prefetch = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "symd_tsm") { h->symd_tsm = value ? 1 : 0; return AMG_OK; }
@@ -1631,7 +1639,10 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "symd_minb") { h->symd_minb = (int)value; return AMG_OK; }
     if (k == "sell") { h->sell = value ? 1 : 0; return AMG_OK; }
     if (k == "grid_per_sm") { h->grid_per_sm = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
-    if (k == "vec_per_sm") { h->vec_per_sm = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
+    if (k == "vec_per_sm") {
+        // the reduction partials scratch holds sm_count * 8 CTAs (max_grid)
+        if (value < 0 || value > 8) return fail(AMG_E_ARG, "vec_per_sm must be in [0, 8]");
+        h->vec_per_sm = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "gated_grid") { h->gated_grid = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "sell_pad") { h->sell_pad = (int)value; return AMG_OK; }
     if (k == "sell_sigma") { h->sell_sigma = (int)value; return AMG_OK; }
@@ -1881,6 +1892,9 @@ int amg_set_cycle(amg_t *h, int nu1, int nu2)
 {
     if (!h) return fail(AMG_E_ARG, "NULL handle");
     if (nu1 < 0 || nu2 < 0) return fail(AMG_E_ARG, "smoothing step counts must be nonnegative");
+    // the cluster tail's op list is fixed at amg_finalize: a later change would
+    // reach the upper levels only
+    if (h->finalized) return fail(AMG_E_STATE, "amg_set_cycle: already finalized");
     h->nu1 = nu1;
     h->nu2 = nu2;
     if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
@@ -2035,6 +2049,7 @@ static int build_symd(amg_t *h, DevMat &M, const std::vector<int32_t> &off32, co
     M.sym_npad = (int)npad;
     TRY(dalloc(&M.uval, uv.size()));
     CK(cudaMemcpy(M.uval, uv.data(), uv.size() * sizeof(double), cudaMemcpyHostToDevice));
+    M.lbytes[AMG_LAYOUT_SYMD] = (int64_t)uv.size() * 8 + n;  // stored diagonals + 1-byte pattern id per row
     M.nudiag = nu;
     int nb = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_symd_fn(EPI_RESID, h->symd_gminb, blk), VEC_SPMV_THREADS, 0));
@@ -2365,6 +2380,7 @@ int amg_finalize(amg_t *h)
                 TRY(dalloc(&M.pstart, ps.size()));
                 TRY(dalloc(&M.pcol, pc.size()));
                 TRY(dalloc(&M.pval, pv.size()));
+                M.lbytes[AMG_LAYOUT_PADDED] = (int64_t)pv.size() * 12 + (int64_t)ps.size() * 4;
                 CK(cudaMemcpy(M.pstart, ps.data(), ps.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
                 CK(cudaMemcpy(M.pcol, pc.data(), pc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
                 CK(cudaMemcpy(M.pval, pv.data(), pv.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -2454,6 +2470,9 @@ int amg_finalize(amg_t *h)
                         TRY(dalloc(&M.sbeg, sb.size()));
                         TRY(dalloc(&M.sval, sv.size()));
                         TRY(dalloc(&M.slen, ln.size()));
+                        M.lbytes[pat ? AMG_LAYOUT_SELL_PAT : AMG_LAYOUT_SELL] =
+                            (int64_t)sv.size() * (pat ? 8 : 12) + (int64_t)ln.size() + (int64_t)sb.size() * 4 +
+                            (sorted ? M.nrows * 4 : 0) + (pat ? M.nrows : 0);
                         CK(cudaMemcpy(M.sbeg, sb.data(), sb.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
                         CK(cudaMemcpy(M.sval, sv.data(), sv.size() * sizeof(double), cudaMemcpyHostToDevice));
                         CK(cudaMemcpy(M.slen, ln.data(), ln.size(), cudaMemcpyHostToDevice));
@@ -2561,6 +2580,8 @@ int amg_finalize(amg_t *h)
                     TRY(dalloc(&M.uval_s, tot));
                     TRY(dalloc(&M.ucol_s, tot));
                     TRY(dalloc(&M.ulen_s, ln.size()));
+                    // padding slots are loaded unless skipped (plen)
+                    M.lbytes[AMG_LAYOUT_SELL_UNIFORM] = (plen ? M.nnz : (int64_t)tot) * 12 + (int64_t)ln.size();
                     CK(cudaMemcpy(M.uval_s, sv.data(), tot * sizeof(double), cudaMemcpyHostToDevice));
                     CK(cudaMemcpy(M.ucol_s, sc.data(), tot * sizeof(int32_t), cudaMemcpyHostToDevice));
                     CK(cudaMemcpy(M.ulen_s, ln.data(), ln.size(), cudaMemcpyHostToDevice));
@@ -2608,6 +2629,7 @@ int amg_finalize(amg_t *h)
                     }
                     TRY(dalloc(&M.spv, tot));
                     TRY(dalloc(&M.spc, tot));
+                    M.lbytes[AMG_LAYOUT_SPLIT] = (int64_t)tot * 12 + (int64_t)ln.size() + (int64_t)lr.size() * 4;
                     TRY(dalloc(&M.splen, ln.size()));
                     TRY(dalloc(&M.splong, lr.size() + 1));
                     CK(cudaMemcpy(M.spv, sv.data(), tot * sizeof(double), cudaMemcpyHostToDevice));
@@ -2702,6 +2724,9 @@ int amg_finalize(amg_t *h)
                     }
                     TRY(dalloc(&M.sv_s, sv.size()));
                     TRY(dalloc(&M.sc_s, sc.size()));
+                    // padding slots are never loaded: entries + slice starts/widths + row permutation + lengths
+                    M.lbytes[AMG_LAYOUT_SELL_SORTED] = M.nnz * 12 + (int64_t)sb.size() * 4 + (int64_t)sw.size() +
+                                                        (int64_t)pm.size() * 4 + (int64_t)ln.size();
                     TRY(dalloc(&M.sb_s, sb.size()));
                     TRY(dalloc(&M.sw_s, sw.size()));
                     TRY(dalloc(&M.sp_s, pm.size()));
@@ -3186,6 +3211,8 @@ int amg_bicgstab(amg_t *h, const double *b, const double *x0, double rtol, int m
     return finish(max_iters, relres, 0);
 }
 
+static int layout_of(const amg_t *h, const DevMat &M);
+
 int amg_matrix_layout(amg_t *h, int level, int which, int *layout)
 {
     if (!h || !layout) return fail(AMG_E_ARG, "amg_matrix_layout: NULL argument");
@@ -3194,8 +3221,30 @@ int amg_matrix_layout(amg_t *h, int level, int which, int *layout)
         return fail(AMG_E_ARG, "amg_matrix_layout: level/which out of range");
     const DevMat &M = h->lv[level].m[which];
     if (!M.present) return fail(AMG_E_ARG, "amg_matrix_layout: matrix not uploaded");
+    *layout = layout_of(h, M);
+    return AMG_OK;
+}
+
+int amg_matrix_bytes(amg_t *h, int level, int which, int64_t *stored, int64_t *vectors)
+{
+    if (!h || !stored || !vectors) return fail(AMG_E_ARG, "amg_matrix_bytes: NULL argument");
+    if (!h->finalized) return fail(AMG_E_STATE, "amg_matrix_bytes: handle not finalized");
+    if (level < 0 || level >= (int)h->lv.size() || which < 0 || which > 4)
+        return fail(AMG_E_ARG, "amg_matrix_bytes: level/which out of range");
+    const DevMat &M = h->lv[level].m[which];
+    if (!M.present) return fail(AMG_E_ARG, "amg_matrix_bytes: matrix not uploaded");
+    const int lay = layout_of(h, M);
+    *stored = (lay == AMG_LAYOUT_CSR || lay == AMG_LAYOUT_LEAVES || M.lbytes[lay] == 0)
+                  ? M.nnz * 12 + (M.nrows + 1) * 4
+                  : M.lbytes[lay];
+    *vectors = 8 * (M.ncols + M.nrows);  // x read once, y written once
+    return AMG_OK;
+}
+
+static int layout_of(const amg_t *h, const DevMat &M)
+{
     // same precedence as launch_spmv
-    *layout = M.ntiles == 0           ? AMG_LAYOUT_EMPTY
+    return M.ntiles == 0           ? AMG_LAYOUT_EMPTY
               : (M.uval && h->symm)   ? AMG_LAYOUT_SYMD
               : (M.spv && h->split)    ? AMG_LAYOUT_SPLIT
               : (M.sv_s && h->sells)   ? AMG_LAYOUT_SELL_SORTED
@@ -3205,7 +3254,6 @@ int amg_matrix_layout(amg_t *h, int level, int which, int *layout)
               : M.leaf                ? AMG_LAYOUT_LEAVES
               : M.pstart              ? AMG_LAYOUT_PADDED
                                       : AMG_LAYOUT_CSR;
-    return AMG_OK;
 }
 
 int amg_get_stats(amg_t *h, amg_stats_t *out)

@@ -24,7 +24,8 @@ import numpy as np
 from . import _capi as C
 from .errors import AmgError, DimensionMismatchError
 
-__all__ = ["DeviceHierarchy", "DeviceMatrix", "DeviceVcycle", "model_bytes_flops", "nccl_unique_id"]
+__all__ = ["DeviceHierarchy", "DeviceMatrix", "DeviceVcycle", "model_bytes_flops", "layout_bytes_per_iter",
+           "nccl_unique_id"]
 
 
 def nccl_unique_id():
@@ -239,13 +240,17 @@ class DeviceHierarchy:
     # ------------------------------------------------------------------ ops
     def _vec_in(self, x, n, op, shape):
         if _is_cuda_tensor(x):
-            if x.dtype.itemsize != 8 or not x.is_contiguous() or x.dim() != 1:
+            import torch
+
+            if x.dtype != torch.float64 or not x.is_contiguous() or x.dim() != 1:
                 raise AmgError(f"{op}: device vectors must be contiguous 1-D float64 tensors")
             if x.shape[0] != n:
                 raise DimensionMismatchError(op, shape, tuple(x.shape))
             return x, 1
         if hasattr(x, "is_pinned") and x.is_pinned():  # pinned host tensor: async H2D / D2H
-            if x.dtype.itemsize != 8 or not x.is_contiguous() or x.dim() != 1 or not x.is_floating_point():
+            import torch
+
+            if x.dtype != torch.float64 or not x.is_contiguous() or x.dim() != 1:
                 raise AmgError(f"{op}: pinned host vectors must be contiguous 1-D float64 tensors")
             if x.shape[0] != n:
                 raise DimensionMismatchError(op, shape, tuple(x.shape))
@@ -256,6 +261,21 @@ class DeviceHierarchy:
         if a.shape[0] != n:
             raise DimensionMismatchError(op, shape, a.shape)
         return a, 0
+
+    def _vec_in_like(self, x, n, op, shape, dev, like):
+        """A second input vector (x0) staged to the residency of the first (b): the C
+        side copies every vector of one call with one memcpy kind."""
+        v, d = self._vec_in(x, n, op, shape)
+        if d == dev:
+            if dev == 1 and v.device != like.device:
+                v = v.to(like.device)
+            return v
+        if dev == 1:
+            import torch
+
+            return torch.as_tensor(np.asarray(v.numpy() if hasattr(v, "numpy") else v, dtype=np.float64),
+                                   device=like.device).contiguous()
+        return np.ascontiguousarray(v.detach().cpu().numpy(), dtype=np.float64)
 
     def _vec_out(self, like, n):
         if _is_cuda_tensor(like):
@@ -283,7 +303,7 @@ class DeviceHierarchy:
         bin_, dev = self._vec_in(b, n, "apply_smoother", (n, n))
         x0in = None
         if x0 is not None:
-            x0in, _ = self._vec_in(x0, n, "apply_smoother", (n, n))
+            x0in = self._vec_in_like(x0, n, "apply_smoother", (n, n), dev, bin_)
         x = self._vec_out(bin_, n)
         C.check(C.lib().amg_smoother(self._h, level, C.ptr(bin_), C.ptr(x0in), C.ptr(x), int(steps), dev),
                 "apply_smoother")
@@ -323,6 +343,14 @@ class DeviceHierarchy:
         C.check(C.lib().amg_matrix_layout(self._h, int(level), self._SLOTS[slot], ctypes.byref(v)), "amg_matrix_layout")
         return self.LAYOUTS[v.value]
 
+    def matrix_bytes(self, level, slot):
+        """(stored, vectors): bytes one SpMV launch of this matrix's layout must move
+        (``amg_matrix_bytes``; the roofline numerator of the chosen layout)."""
+        st, ve = ctypes.c_int64(0), ctypes.c_int64(0)
+        C.check(C.lib().amg_matrix_bytes(self._h, int(level), self._SLOTS[slot], ctypes.byref(st), ctypes.byref(ve)),
+                "amg_matrix_bytes")
+        return int(st.value), int(ve.value)
+
     def stats(self):
         s = C.Stats()
         C.check(C.lib().amg_get_stats(self._h, ctypes.byref(s)), "amg_get_stats")
@@ -338,6 +366,42 @@ class DeviceHierarchy:
             self.close()
         except Exception:
             pass
+
+
+def layout_bytes_per_iter(dh, h):
+    """Bytes per PCG iteration on the layouts the device actually runs.
+
+    Same application counts and vector terms as :func:`model_bytes_flops`,
+    but each matrix application costs the bytes its chosen layout must stream
+    (``DeviceHierarchy.matrix_bytes``: e.g. the symmetric stencil layout
+    stores only the diagonals d >= 0, uniform SELL skips no slots) instead of
+    the 12 B/entry CSR model.  The roofline fraction on these bytes cannot
+    exceed 1 unless the hardware moved fewer bytes than the data structure
+    holds (L2 reuse across kernels).
+    """
+    levels = h.levels
+    nu1, nu2 = int(h.config.nu1), int(h.config.nu2)
+
+    def M(k, slot):
+        return dh.matrix_bytes(k, slot)[0]
+
+    nbytes = 0
+    for k in range(len(levels) - 1):
+        lv = levels[k]
+        n_k, n_c = lv.a.nrows, levels[k + 1].a.nrows
+        n_a = (max(nu1 - 1, 0) + 1 + nu2) if nu1 else nu2
+        steps = nu1 + nu2
+        nbytes += n_a * M(k, "a") + M(k, "p") + M(k, "pt")
+        if lv.smoother.kind == "fsai":
+            nbytes += steps * (M(k, "g") + M(k, "gt"))
+        else:
+            nbytes += steps * 8 * 3 * n_k
+        nbytes += 8 * (18 * n_k + 2 * n_c)
+    nL = levels[-1].a.nrows
+    nbytes += 8 * nL * (nL + 1) + 16 * nL
+    n0 = levels[0].a.nrows
+    nbytes += M(0, "a") + 8 * 13 * n0
+    return int(nbytes)
 
 
 def model_bytes_flops(h):

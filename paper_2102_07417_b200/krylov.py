@@ -60,7 +60,7 @@ def pcg(apply_a, b, apply_m=None, x0=None, config=None):
     bin_, dev = dh._vec_in(b, n, "pcg", (n, n))
     x0in = None
     if x0 is not None:
-        x0in, _ = dh._vec_in(x0, n, "pcg", (n, n))
+        x0in = dh._vec_in_like(x0, n, "pcg", (n, n), dev, bin_)
     x = dh._vec_out(bin_, n)
     n_iter = C.I32(0)
     relres = C.D(0.0)
@@ -110,7 +110,7 @@ def bicgstab(apply_a, b, apply_m=None, x0=None, config=None):
     bin_, dev = dh._vec_in(b, n, "bicgstab", (n, n))
     x0in = None
     if x0 is not None:
-        x0in, _ = dh._vec_in(x0, n, "bicgstab", (n, n))
+        x0in = dh._vec_in_like(x0, n, "bicgstab", (n, n), dev, bin_)
     x = dh._vec_out(bin_, n)
     n_iter, conv, rst, hist_len = C.I32(0), C.I32(0), C.I32(0), C.I32(0)
     relres = C.D(0.0)

@@ -410,6 +410,49 @@ def test_torch_device_vectors(cases):
     assert r.converged and r.x.is_cuda
 
 
+def test_mixed_residency_x0_and_dtype_checks(cases):
+    # x0 on the other side of b is staged to b's residency; non-float64 device
+    # tensors are rejected instead of being read as doubles
+    torch = pytest.importorskip("torch")
+    c, dh = _dh("poisson7_12", cases)
+    b = c["b"]
+    x0 = np.random.default_rng(2).uniform(-1, 1, b.size)
+    want = amg.pcg(dh.A0, b, apply_m=dh.vcycle, x0=x0)
+    r1 = amg.pcg(dh.A0, b, apply_m=dh.vcycle, x0=torch.tensor(x0, device="cuda"))
+    np.testing.assert_array_equal(r1.x, want.x)
+    r2 = amg.pcg(dh.A0, torch.tensor(b, device="cuda"), apply_m=dh.vcycle, x0=x0)
+    np.testing.assert_array_equal(r2.x.cpu().numpy(), want.x)
+    n = b.size
+    np.testing.assert_array_equal(dh.apply_smoother(0, torch.tensor(b, device="cuda"), x0, 1).cpu().numpy(),
+                                  dh.apply_smoother(0, b, x0, 1))
+    for bad in (torch.zeros(n, dtype=torch.int64, device="cuda"), torch.zeros(n, dtype=torch.complex64, device="cuda")):
+        with pytest.raises(amg.AmgError):
+            dh.vcycle(bad)
+
+
+def test_option_guards(cases):
+    # tail_pcap < 1 and vec_per_sm beyond the partials scratch are rejected;
+    # amg_set_cycle after finalize is rejected (the tail's op list is fixed then)
+    from paper_2102_07417_b200 import _capi as C
+
+    c, dh = _dh("poisson7_12", cases)
+    L = C.lib()
+    assert L.amg_set_cycle(dh._h, 2, 2) != 0
+    for key, val in (("tail_pcap", 0), ("tail_pcap", -5), ("vec_per_sm", 9)):
+        with pytest.raises(amg.AmgError):
+            amg.DeviceHierarchy.from_reference(c["h"], options={key: val})
+
+
+@pytest.mark.parametrize("pcap", [1, 8])
+def test_tail_rows_longer_than_product_buffer(pcap, cases):
+    # tail_pcap below the longest tail row: chunks still hold whole rows
+    c, dh = _dh("hetero27_10", cases)
+    dh2 = amg.DeviceHierarchy.from_reference(c["h"], options={"tail_pcap": pcap})
+    y = c["y"]
+    np.testing.assert_array_equal(dh2.vcycle(y), dh.vcycle(y))
+    dh2.close()
+
+
 def _dense(m):
     d = np.zeros((m.nrows, m.ncols))
     rows = np.repeat(np.arange(m.nrows), np.diff(m.row_offsets))
