@@ -109,6 +109,10 @@ struct DevMat {
     int nleaves = 0, leaf_grid = 0, leafsum_grid = 0;
     HaloPlan halo;  // exchange feeding this matrix's halo columns (nranks > 1)
     int64_t lbytes[12] = {};  // per layout: bytes its kernel must stream (values, indices, row metadata)
+    void *dcls = nullptr;     // row-class dictionary (spmv_dict): class id per row, nullptr if unused
+    int32_t *dbeg = nullptr, *drel = nullptr;
+    double *dval = nullptr;
+    int dncls = 0, dnent = 0, dwide = 0, dfl = 0, dgrid = 0;
 };
 
 struct LevelD {
@@ -298,6 +302,7 @@ struct amg_handle {
     int symd_fixed = 1;           // fixed-slot symmetric kernel: 1 rows <= 8 entries (7-point), 2 also <= 32 (27-point:
                                   // measured slower than the round-by-round kernel on config 2), 0 off
     int symm = 1;                 // symmetric stencil layout (upper diagonals) for bitwise-symmetric pattern operators
+    int dict = 1;                 // row-class dictionary layout for operators with few distinct rows
     int sell = 1;                 // SELL-32 slices where padding <= sell_pad %
     int gated_grid = 1;           // CTAs per SM for the rarely active gated residual SpMVs (0 = full grid)
     int grid_per_sm = 0;          // cap on SpMV CTAs per SM (0 = occupancy)
@@ -435,6 +440,23 @@ static SpmvSellUFn spmv_sellu_fn(int epi, int W, bool plen = false)
     default: AMG_U(EPI_ADD)
     }
 #undef AMG_U
+}
+
+typedef void (*SpmvDictFn)(const SpmvArgs, const DictArgs, int);
+
+static SpmvDictFn spmv_dict_fn(int epi, int fl, bool wide)
+{
+#define AMG_D(E)                                                                                         \
+    return wide ? (fl <= 8 ? spmv_dict<E, 8, true> : fl <= 16 ? spmv_dict<E, 16, true> : spmv_dict<E, 32, true>) \
+                : (fl <= 8 ? spmv_dict<E, 8, false> : fl <= 16 ? spmv_dict<E, 16, false> : spmv_dict<E, 32, false>);
+    switch (epi) {
+    case EPI_PLAIN: AMG_D(EPI_PLAIN)
+    case EPI_RESID: AMG_D(EPI_RESID)
+    case EPI_AXPYW: AMG_D(EPI_AXPYW)
+    case EPI_SETW: AMG_D(EPI_SETW)
+    default: AMG_D(EPI_ADD)
+    }
+#undef AMG_D
 }
 
 typedef void (*SpmvSellSFn)(const SpmvArgs, const SellSArgs, int);
@@ -828,7 +850,12 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     a.ctl = h->ctl;
     a.gate1 = g1;
     a.gate2 = g2;
-    if (M.uval && h->symm) {
+    if (M.dcls) {
+        DictArgs da{M.dcls, M.dbeg, M.drel, M.dval, M.dncls, M.dnent};
+        const size_t sm = (size_t)M.dnent * 12 + (size_t)(M.dncls + 1) * 4;
+        TRY(launch_k(h, spmv_dict_fn(epi, M.dfl, M.dwide), grid_cap ? std::min(grid_cap, M.dgrid) : M.dgrid,
+                     VEC_SPMV_THREADS, sm, a, da, (int)M.nrows));
+    } else if (M.uval && h->symm) {
         const bool fx = M.sym_fl && (h->symd_fixed >= 2 || (h->symd_fixed == 1 && M.sym_fl <= 8));
         int g = fx ? M.symf_grid : M.sym_grid;
         if (grid_cap) g = std::min(g, grid_cap);
@@ -1545,7 +1572,7 @@ void amg_destroy(amg_t *h)
     };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.pperm); F(M.spv); F(M.spc); F(M.splong); F(M.splen); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s);
+            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.pperm); F(M.spv); F(M.spc); F(M.splong); F(M.splen); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s); F(M.dcls); F(M.dbeg); F(M.drel); F(M.dval);
             symd_slot_give(h->device, M.sym_slot);
             M.sym_slot = -1;
             symd_tab_give(h->device, M.sym_tab, M.sym_ntab);
@@ -1600,6 +1627,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "small_rows_per_sm") { h->small_rows_per_sm = (int)value; return AMG_OK; }
     if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
     if (k == "symm") { h->symm = value ? 1 : 0; return AMG_OK; }
+    if (k == "dict") { h->dict = value ? 1 : 0; return AMG_OK; }
     if (k == "vec_groups") { h->vec_groups = (int)value; return AMG_OK; }
     if (k == "split") { h->split = value ? 1 : 0; return AMG_OK; }
     if (k == "sells") { h->sells = (int)value; return AMG_OK; }
@@ -1898,6 +1926,92 @@ int amg_set_cycle(amg_t *h, int nu1, int nu2)
     h->nu1 = nu1;
     h->nu2 = nu2;
     if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+    return AMG_OK;
+}
+
+// Row-class dictionary (spmv_dict): rows grouped by their exact (length, col - row
+// offsets, value bits) tuple; used when at most DICT_MAX_CLS classes with at most
+// DICT_MAX_ENT table entries in total cover every row of <= 32 entries.  Hash
+// buckets hold candidate classes that are compared entry by entry, so equal
+// hashes never merge different rows.  Gives up as soon as a limit is exceeded
+// (irregular matrices cost a few thousand rows of hashing).
+static constexpr int DICT_MAX_CLS = 1024;
+static constexpr int DICT_MAX_ENT = 3072;
+
+static int build_dict(amg_t *h, DevMat &M, const std::vector<int32_t> &off32)
+{
+    if (M.nrows <= 0 || M.nnz <= 0 || M.nrows >= INT32_MAX - 1) return AMG_OK;
+    int maxlen = 0;
+    for (int64_t r = 0; r < M.nrows; ++r) maxlen = std::max(maxlen, off32[r + 1] - off32[r]);
+    if (maxlen > 32) return AMG_OK;
+    std::vector<int32_t> col_h(M.nnz);
+    std::vector<double> val_h(M.nnz);
+    CK(cudaMemcpy(col_h.data(), M.col, M.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(val_h.data(), M.val, M.nnz * sizeof(double), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> beg(1, 0), rel;
+    std::vector<double> val;
+    std::unordered_map<uint64_t, std::vector<int>> buckets;
+    std::vector<uint16_t> cls(M.nrows);
+    for (int64_t r = 0; r < M.nrows; ++r) {
+        const int32_t s = off32[r], e = off32[r + 1];
+        uint64_t hsh = 1469598103934665603ull ^ (uint64_t)(e - s);
+        for (int32_t k = s; k < e; ++k) {
+            uint64_t vb;
+            memcpy(&vb, &val_h[k], 8);
+            hsh = (hsh ^ (uint64_t)(uint32_t)(col_h[k] - (int32_t)r)) * 1099511628211ull;
+            hsh = (hsh ^ vb) * 1099511628211ull;
+        }
+        auto &bk = buckets[hsh];
+        int found = -1;
+        for (int c : bk) {
+            if (beg[c + 1] - beg[c] != e - s) continue;
+            bool same = true;
+            for (int32_t k = s; k < e && same; ++k) {
+                const int q = beg[c] + (k - s);
+                same = rel[q] == col_h[k] - (int32_t)r && memcmp(&val[q], &val_h[k], 8) == 0;
+            }
+            if (same) { found = c; break; }
+        }
+        if (found < 0) {
+            found = (int)beg.size() - 1;
+            if (found >= DICT_MAX_CLS || (int)rel.size() + (e - s) > DICT_MAX_ENT) return AMG_OK;
+            for (int32_t k = s; k < e; ++k) {
+                rel.push_back(col_h[k] - (int32_t)r);
+                val.push_back(val_h[k]);
+            }
+            beg.push_back((int32_t)rel.size());
+            bk.push_back(found);
+        }
+        cls[r] = (uint16_t)found;
+    }
+    M.dncls = (int)beg.size() - 1;
+    M.dnent = (int)rel.size();
+    M.dwide = M.dncls > 256 ? 1 : 0;
+    M.dfl = maxlen <= 8 ? 8 : maxlen <= 16 ? 16 : 32;
+    if (M.dwide) {
+        TRY(dalloc((uint16_t **)&M.dcls, (size_t)M.nrows));
+        CK(cudaMemcpy(M.dcls, cls.data(), (size_t)M.nrows * 2, cudaMemcpyHostToDevice));
+    } else {
+        std::vector<uint8_t> c8(cls.begin(), cls.end());
+        TRY(dalloc((uint8_t **)&M.dcls, (size_t)M.nrows));
+        CK(cudaMemcpy(M.dcls, c8.data(), (size_t)M.nrows, cudaMemcpyHostToDevice));
+    }
+    TRY(dalloc(&M.dbeg, beg.size()));
+    TRY(dalloc(&M.drel, std::max<size_t>(rel.size(), 1)));
+    TRY(dalloc(&M.dval, std::max<size_t>(val.size(), 1)));
+    CK(cudaMemcpy(M.dbeg, beg.data(), beg.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    if (!rel.empty()) {
+        CK(cudaMemcpy(M.drel, rel.data(), rel.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(M.dval, val.data(), val.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    const size_t sm = (size_t)M.dnent * 12 + (size_t)(M.dncls + 1) * 4;
+    int nb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_dict_fn(EPI_RESID, M.dfl, M.dwide),
+                                                     VEC_SPMV_THREADS, sm));
+    M.dgrid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
+                                                          (int64_t)h->sm_count * std::max(nb, 1)));
+    h->max_grid = std::max(h->max_grid, M.dgrid);
+    M.lbytes[AMG_LAYOUT_DICT] = M.nrows * (M.dwide ? 2 : 1) + (int64_t)sm;  // class ids + the table
     return AMG_OK;
 }
 
@@ -2302,8 +2416,11 @@ int amg_finalize(amg_t *h)
                 M.wt_grid = std::max(1, std::min((warps_needed + WT_WARPS - 1) / WT_WARPS, h->sm_count * nb));
                 h->max_grid = std::max(h->max_grid, M.wt_grid);
             }
+            // row-class dictionary first: where it applies no value / column stream is needed
+            if (h->dict && h->nranks == 1 && !h->lanes_override && M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm)
+                TRY(build_dict(h, M, off32));
             // rows averaging > long_avg entries: leaf list for spmv_leaves / spmv_leafsum
-            const bool longrows = h->long_avg > 0 && !h->lanes_override && M.nrows > 0 &&
+            const bool longrows = !M.dcls && h->long_avg > 0 && !h->lanes_override && M.nrows > 0 &&
                                   (double)M.nnz / (double)M.nrows > (double)h->long_avg;
             if (longrows) {
                 int64_t mx = 0;
@@ -2350,7 +2467,7 @@ int amg_finalize(amg_t *h)
                                                                             (int64_t)h->sm_count * 4));
                 h->max_grid = std::max(h->max_grid, std::max(M.leaf_grid, M.leafsum_grid));
             }
-            if (!longrows && h->pad_min > 0 && M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm && !h->lanes_override &&
+            if (!M.dcls && !longrows && h->pad_min > 0 && M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm && !h->lanes_override &&
                 (double)M.nnz / (double)M.nrows >= (double)h->pad_min) {
                 // padded-aligned copy: row starts == 3 (mod 4) so entry 1 is 16-byte aligned
                 std::vector<int32_t> col_h(M.nnz);
@@ -2522,7 +2639,7 @@ int amg_finalize(amg_t *h)
                 M.pad_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
                                                                         (int64_t)h->sm_count * std::max(nb, 1)));
                 h->max_grid = std::max(h->max_grid, M.pad_grid);
-            } else if (!longrows && h->symm && h->patterns && h->nranks == 1 && M.ncols == M.nrows && !h->lanes_override &&
+            } else if (!M.dcls && !longrows && h->symm && h->patterns && h->nranks == 1 && M.ncols == M.nrows && !h->lanes_override &&
                        M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm) {
                 // short-row stencil operators (7-point): the symmetric layout alone, pattern ids kept only with it
                 std::vector<int32_t> col_h(M.nnz);
@@ -2546,7 +2663,7 @@ int amg_finalize(amg_t *h)
                     }
                 }
             }
-            if (!M.uval && !longrows && !h->lanes_override && M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm) {
+            if (!M.dcls && !M.uval && !longrows && !h->lanes_override && M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm) {
                 // uniform-width SELL-32: rows of <= 16 entries, every slice as wide as the widest row
                 int W = 0;
                 for (int64_t r = 0; r < M.nrows; ++r) W = std::max(W, off32[r + 1] - off32[r]);
@@ -2595,7 +2712,7 @@ int amg_finalize(amg_t *h)
                     h->max_grid = std::max(h->max_grid, M.u_grid);
                 }
             }
-            if (!M.uval && !M.uval_s && h->split && !longrows && !h->lanes_override && M.nrows > h->sells_max_rows &&
+            if (!M.dcls && !M.uval && !M.uval_s && h->split && !longrows && !h->lanes_override && M.nrows > h->sells_max_rows &&
                 (double)M.nnz >= h->sells_min_avg * (double)M.nrows && M.nrows < INT32_MAX / 32 / 16) {
                 // short / long split: rows of <= 16 entries as width-16 SELL-32 (padding never loaded)
                 int64_t nshort = 0;
@@ -2649,7 +2766,7 @@ int amg_finalize(amg_t *h)
                     h->max_grid = std::max(h->max_grid, M.sp_grid + M.sp_lgrid);
                 }
             }
-            if (!M.uval && !M.uval_s && !M.spv && h->sells && !longrows && !h->lanes_override && h->sells_sigma >= 32 &&
+            if (!M.dcls && !M.uval && !M.uval_s && !M.spv && h->sells && !longrows && !h->lanes_override && h->sells_sigma >= 32 &&
                 M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm &&
                 (M.nrows <= h->sells_max_rows || h->sells_buckets) &&
                 (double)M.nnz >= h->sells_min_avg * (double)M.nrows) {
@@ -3245,6 +3362,7 @@ static int layout_of(const amg_t *h, const DevMat &M)
 {
     // same precedence as launch_spmv
     return M.ntiles == 0           ? AMG_LAYOUT_EMPTY
+              : M.dcls                ? AMG_LAYOUT_DICT
               : (M.uval && h->symm)   ? AMG_LAYOUT_SYMD
               : (M.spv && h->split)    ? AMG_LAYOUT_SPLIT
               : (M.sv_s && h->sells)   ? AMG_LAYOUT_SELL_SORTED

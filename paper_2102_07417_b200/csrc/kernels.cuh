@@ -1990,6 +1990,83 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, MINB) spmv_symd_fixed(const 
     }
 }
 
+// ---------------------------------------------------------------- SpMV, row-class dictionary
+
+// Operators whose rows fall into few distinct (column-offset tuple, value
+// tuple) classes -- constant-coefficient stencils and the FSAI factors built
+// from them (config 1 / config 4 level 0: A 27 classes, G 7, G^T 14 of
+// 262 k rows) -- are stored as ONE class id per row (1 or 2 bytes) plus a
+// class table {start, offsets, values} held in shared memory.  A row then
+// costs its class id, its x gathers and its y store: the value and column
+// streams disappear from HBM.  Entry k of a row is val[k] * x[row + rel[k]]
+// with exactly the stored value, summed in the reference order (p0 + numpy
+// pairwise, ref_sum_fixed), so every row is bit-identical to the CSR SpMV.
+struct DictArgs {
+    const void *cls;      // uint8_t or uint16_t per row (WIDE)
+    const int32_t *beg;   // class starts [ncls + 1]
+    const int32_t *rel;   // column offset col - row per entry
+    const double *val;    // value per entry
+    int ncls, nent;
+};
+
+template <int EPI, int FL, bool WIDE>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_dict(const SpmvArgs a, const DictArgs d, int nrows)
+{
+    __shared__ double red[VEC_SPMV_THREADS / 32];
+    extern __shared__ double dict_sm[];  // val[nent] | rel[nent] | beg[ncls + 1]
+    double *sval = dict_sm;
+    int32_t *srel = reinterpret_cast<int32_t *>(dict_sm + d.nent);
+    int32_t *sbeg = srel + d.nent;
+    for (int i = threadIdx.x; i < d.nent; i += blockDim.x) {  // static data: staged before the PDL wait
+        sval[i] = d.val[i];
+        srel[i] = d.rel[i];
+    }
+    for (int i = threadIdx.x; i <= d.ncls; i += blockDim.x) sbeg[i] = d.beg[i];
+    __syncthreads();
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const int nthreads = gridDim.x * VEC_SPMV_THREADS;
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    const double *__restrict__ x = a.x;
+    auto cls_of = [&](int r) -> int {
+        if constexpr (WIDE) return __ldg(reinterpret_cast<const uint16_t *>(d.cls) + r);
+        else return __ldg(reinterpret_cast<const uint8_t *>(d.cls) + r);
+    };
+    double dacc = 0.0;
+    int row = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x;
+    int ncl = row < nrows ? cls_of(row) : 0;
+    for (; row < nrows; row += nthreads) {
+        const int c = ncl;
+        if (row + nthreads < nrows) ncl = cls_of(row + nthreads);  // next row's class one step ahead
+        double bv = 0.0, wv = 0.0;
+        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
+        if (want_dot && !self_dot) wv = a.dotw[row];
+        const int rb = sbeg[c];
+        const int len = sbeg[c + 1] - rb;
+        double p[FL];
+#pragma unroll
+        for (int k = 0; k < FL; ++k) {
+            p[k] = 0.0;
+            if (k < len) p[k] = prod(sval[rb + k], __ldg(x + (row + srel[rb + k])));
+        }
+        const double sum = ref_sum_fixed<FL>(p, len);
+        double yv;
+        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+        else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+        else yv = sum;
+        a.y[row] = yv;
+        if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
+        grid_finalize<VEC_SPMV_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
 // ---------------------------------------------------------------- SpMV, uniform-width SELL-32
 
 // Every 32-row slice padded to the same width W (taken where that costs

@@ -123,10 +123,60 @@ def test_spmv_symmetric_diagonals_bit_identical(kind):
     variants = [{"symm": 0}, {"symm": 1, "symd_tsm": 1}] + [
         {"symm": 1, "symd_fixed": f, "symd_chunked": c, "symd_blocked": b} for f in (0, 1, 2) for c in (0, 1) for b in (0, 1)]
     for opts in variants:
+        opts["dict"] = 0  # constant-coefficient stencils would take the row-class dictionary
         dh = amg.DeviceHierarchy.from_matrices([m], options=opts)
         assert (dh.layout(0, "a") == "symd") == bool(opts["symm"])
         np.testing.assert_array_equal(dh.matrix(0, "a")(x), want, err_msg=str(opts))
         dh.close()
+
+
+def _class_matrix(ncls, nrows, maxlen, seed):
+    # rows drawn from `ncls` distinct (offsets, values) classes, columns clipped at the
+    # borders (clipped rows form classes of their own)
+    from paper_2102_07417_b200.problems import Csr
+
+    rng = np.random.default_rng(seed)
+    proto = []
+    for _ in range(ncls):
+        ln = int(rng.integers(1, maxlen + 1))
+        rel = np.sort(rng.choice(np.arange(-40, 41), size=ln, replace=False))
+        proto.append((rel, rng.uniform(-1, 1, ln)))
+    pick = rng.integers(0, ncls, nrows)
+    offs, cols, vals = [0], [], []
+    for r in range(nrows):
+        rel, v = proto[pick[r]]
+        c = r + rel
+        ok = (c >= 0) & (c < nrows)
+        cols.extend(c[ok].tolist())
+        vals.extend(v[ok].tolist())
+        offs.append(len(cols))
+    return Csr(nrows, nrows, np.asarray(offs), np.asarray(cols), np.asarray(vals))
+
+
+@pytest.mark.parametrize("kind", ["poisson7", "rtanis7", "hetero27", "cls200", "cls700", "len20"])
+def test_spmv_row_class_dictionary_bit_identical(kind):
+    # operators with few distinct rows run on the row-class dictionary (class id per
+    # row + (offsets, values) table in smem); rows bit-identical to the reference
+    if kind in ("poisson7", "rtanis7", "hetero27"):
+        m = _stencil(kind)
+        expect = kind != "hetero27"  # lognormal coefficients: every row distinct
+    else:
+        ncls, ln = {"cls200": (200, 9), "cls700": (700, 4), "len20": (60, 20)}[kind]
+        m = _class_matrix(ncls, 40000, ln, seed=ncls)
+        expect = True
+    x = np.random.default_rng(3).uniform(-1, 1, m.ncols)
+    want = O.spmv(m, x)
+    dh = amg.DeviceHierarchy.from_matrices([m])
+    assert (dh.layout(0, "a") == "dict") == expect
+    np.testing.assert_array_equal(dh.matrix(0, "a")(x), want)
+    if expect:
+        stored, vec = dh.matrix_bytes(0, "a")
+        assert stored < m.nrows * 2 + 3072 * 12 + 1025 * 4 and vec == 8 * (m.ncols + m.nrows)
+    dh.close()
+    dh = amg.DeviceHierarchy.from_matrices([m], options={"dict": 0})
+    assert dh.layout(0, "a") != "dict"
+    np.testing.assert_array_equal(dh.matrix(0, "a")(x), want)
+    dh.close()
 
 
 @pytest.mark.parametrize("width", [3, 9, 16, -4, -8])
@@ -227,9 +277,11 @@ def test_spmv_tile_geometry_does_not_change_bits(opts):
     dh.close()
 
 
+@pytest.mark.parametrize("small", [False, True])
 @pytest.mark.parametrize("name", [n for n in HIER_CASES if n != "poisson1d_50_single"])
-def test_smoother_sweeps_bit_identical(name, cases):
-    c, dh = _dh(name, cases)
+def test_smoother_sweeps_bit_identical(name, small, cases):
+    # small: every matrix counts as large (dict / symmetric / SELL layouts, all epilogues)
+    c, dh = _dh(name, cases, **({"small_rows_per_sm": 1} if small else {}))
     v = c["vec"]
     for k in range(c["h"].n_levels - 1):
         b, x0 = v[f"smooth_L{k}_b"], v[f"smooth_L{k}_x0"]
@@ -297,7 +349,8 @@ def test_coarse_cholesky_sizes(n, pipe):
     dh.close()
 
 
-@pytest.mark.parametrize("opts", [{}, {"tail_nnz": 0}, {"pdl": 0}, {"graph": 1}])
+@pytest.mark.parametrize("opts", [{}, {"tail_nnz": 0}, {"pdl": 0}, {"graph": 1},
+                                  {"small_rows_per_sm": 1}])  # layouts of large matrices (dict, symd, SELL)
 @pytest.mark.parametrize("name", cases_with("pcg"))
 def test_pcg_matches_reference(name, opts, cases):
     c, dh = _dh(name, cases, **{k: v for k, v in opts.items() if k != "graph"})

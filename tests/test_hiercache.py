@@ -161,3 +161,31 @@ def test_fsai_replay_matches_scipy_cho_solve():
         offs.append(len(cols))
     got = fsai_values(A, np.asarray(offs), np.asarray(cols), threads=4)
     np.testing.assert_array_equal(got, np.concatenate(want))
+
+
+@pytest.mark.skipif(not have_reference(), reason="reference package only in the build container")
+@pytest.mark.parametrize("n", [3, 6])
+def test_elasticity3d_matches_reference_generator_at_sigma0(n):
+    # config 3's generator (per-element lognormal E, unit cube h = 1/n) pinned to
+    # the reference's gen_elasticity3d (problems.py:142-199): with sigma = 0 every
+    # E is 1 and the Q1 stiffness scales with h in 3-D, so ours == h * reference
+    # up to assembly-order rounding; same clamped-dof numbering, coords * h
+    from amgkit.problems import gen_elasticity3d
+
+    a, coords = problems.elasticity3d(n, n, n, sigma=0.0, nu=0.3, seed=7)
+    r, rc = gen_elasticity3d(n, n, n, e=1.0, nu=0.3, bc="clamped")
+    assert a.shape == r.shape == (3 * n * (n + 1) ** 2,) * 2
+    np.testing.assert_array_equal(coords, np.asarray(rc) * (1.0 / n))
+
+    def dense(m):
+        d = np.zeros(m.shape)
+        rows = np.repeat(np.arange(m.nrows), np.diff(m.row_offsets))
+        np.add.at(d, (rows, m.col_indices), m.values)
+        return d
+
+    da, dr = dense(a), dense(r) / n
+    scale = np.abs(dr).max()
+    assert np.abs(da - dr).max() <= 1e-13 * scale
+    # stored patterns agree except where exact cancellation leaves a rounding-level entry
+    diff = (da != 0) ^ (dr != 0)
+    assert np.all(np.abs(da[diff]) <= 1e-13 * scale) and np.all(np.abs(dr[diff]) <= 1e-13 * scale)
