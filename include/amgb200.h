@@ -81,7 +81,6 @@ typedef struct amg_stats {
     int n_levels;
     int tail_level;           /* first level run by the cluster tail kernel (0 = none) */
     int cluster;              /* CTAs in the tail cluster */
-    int fused_levels;         /* bit k: level k's FSAI steps run as one G/G^T kernel */
 } amg_stats_t;
 
 /* Handle for one GPU.  nccl_unique_id: 128 bytes (NULL when nranks == 1). */

@@ -42,7 +42,6 @@ class Stats(ctypes.Structure):
         ("n_levels", ctypes.c_int),
         ("tail_level", ctypes.c_int),
         ("cluster", ctypes.c_int),
-        ("fused_levels", ctypes.c_int),
     ]
 
 

@@ -60,8 +60,6 @@ struct DevMat {
     int64_t n_own = 0;                       // owned columns (== gncols without a halo plan)
     int32_t *off = nullptr, *col = nullptr;
     double *val = nullptr;
-    TileDesc *tiles = nullptr;
-    int ntiles = 0;
     int32_t *sbeg = nullptr;     // SELL-32 layout (spmv_sell), nullptr if unused
     double *sval = nullptr;
     int32_t *scol = nullptr;
@@ -76,10 +74,6 @@ struct DevMat {
     int sym_slot = -1;           // its __constant__ pattern-start slot
     int sym_tab = -1, sym_ntab = 0, sym_classes = 1, sym_npad = 0;  // entry range in c_symd_tab; row classes
     double *uval_s = nullptr;    // uniform-width SELL-32 (spmv_sellu), nullptr if unused
-    double *spv = nullptr;       // short/long split (spmv_split_short + spmv_split_long), nullptr if unused
-    int32_t *spc = nullptr, *splong = nullptr;
-    uint8_t *splen = nullptr;
-    int sp_nlong = 0, sp_grid = 0, sp_lgrid = 0;
     double *sv_s = nullptr;      // sorted SELL-32 (spmv_sells), nullptr if unused
     int32_t *sc_s = nullptr, *sb_s = nullptr, *sp_s = nullptr;
     uint8_t *sw_s = nullptr, *sl_s = nullptr;
@@ -93,17 +87,9 @@ struct DevMat {
     double *pval = nullptr;
     int32_t *pcol = nullptr;
     int pad_grid = 0;
-    TileDesc *wtiles = nullptr;  // warp tiles (<= wt_nnz entries, <= 32 rows)
-    int nwtiles = 0;
-    int wt_nnz = 256;
-    int wt_lanes = 1;
-    int wt_grid = 0;
     int lanes = 1;
     int grid = 0;
-    int32_t *sq_cta = nullptr;   // SELL streamed by bulk copies (spmv_sellq), nullptr if unused
-    int sq_grid = 0, sq_stage = 0, sq_stages = 0, sq_smem = 0;
     int2 *leaf = nullptr;        // long-row leaves (spmv_leaves + spmv_leafsum), nullptr if unused
-    int lrow_ok = 0;             // rows short enough for the one-warp-per-row kernel (spmv_lrow)
     int32_t *row_leaf = nullptr;
     double *lsum = nullptr;
     int nleaves = 0, leaf_grid = 0, leafsum_grid = 0;
@@ -127,30 +113,10 @@ struct LevelD {
     double omega = 1.0;
     double *inv_diag = nullptr;
     double *y = nullptr, *x = nullptr, *r = nullptr, *t = nullptr;
-    struct Fused {  // FSAI step with G and G^T in one kernel (fsai_fused), nullptrs if unused
-        bool on = false;
-        double *gval = nullptr;
-        int32_t *gcol = nullptr;
-        uint8_t *glen = nullptr;
-        int32_t *tstart = nullptr, *tq = nullptr;
-        unsigned *bcnt = nullptr;
-        unsigned *ctr = nullptr;
-        double *upart = nullptr;
-        uint16_t *gt16 = nullptr;  // warp-specialised kernel (fsai_ws): G^T as (k << 8 | offset id)
-        int slot = -1, ws_grid = 0;
-        int W = 0, nunits = 0, nblk = 0, lag = 0, reach = 0, grid = 0;
-    } fz;
 };
 
 std::mutex g_alloc_mu;
-std::unordered_map<const void *, size_t> g_alloc_size;  // allocation sizes (L2 access-policy windows)
-
-size_t alloc_bytes(const void *p)
-{
-    std::lock_guard<std::mutex> g(g_alloc_mu);
-    auto it = g_alloc_size.find(p);
-    return it == g_alloc_size.end() ? 0 : it->second;
-}
+std::unordered_map<const void *, size_t> g_alloc_size;  // allocation sizes (device memory accounting)
 
 template <class T>
 int dalloc(T **p, size_t count)
@@ -226,10 +192,6 @@ struct amg_handle {
     int device = 0, rank = 0, nranks = 1;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;           // side stream: L2 prefetch of the tail levels
-    const void *win_ptr = nullptr;         // L2 persisting window of the next launches (l2_persist)
-    size_t win_bytes = 0;
-    bool persist_now = false;
-    size_t win_max = 0;
     cudaEvent_t pf_fork = nullptr, pf_join = nullptr;
     PrefetchRange *pf_ranges = nullptr;    // device copy of the tail matrices' ranges
     int pf_n = 0;
@@ -257,14 +219,8 @@ struct amg_handle {
     double *hist = nullptr;
     int hist_cap = 0;
     // options
-    int tile_nnz = 2048, tile_rows = 256, stages = 2, ctas_per_sm = 0, force_graph = -1, batch = 8;
-    int persistent = 1;  // 1: grid = resident capacity, tiles round-robin; 0: one tile per CTA
-    int ws = 0;          // warp-specialized tile kernel (producer warp + consumer warps)
-    int kernel = 2;      // 0: staged CTA tiles (spmv_tiles / spmv_ws), 2: direct register kernel, 3: warp tiles
-    int wt_nnz = 256;    // warp-tile capacity (entries)
+    int force_graph = -1, batch = 8;
     int pad_min = 8;     // matrices averaging >= pad_min entries/row get the padded-aligned layout (0 = off)
-    int sellq = 0;                // (measured slower than spmv_sell on B200: the ring leaves L1 too small for x)
-    int sell_pf = 0;              // spmv_sell: L2 bulk prefetch distance in grid strides (0 = off)                // SELL matrices with rows <= 33 entries streamed by bulk copies (spmv_sellq)
     int long_avg = 128;           // rows averaging more entries run leaf by leaf (spmv_leaves); 0 = off
     int small_rows_per_sm = 128;  // below sm_count * this many rows a matrix counts as small
     int patterns = 1;             // stencil-pattern layout for square operators with few row patterns
@@ -275,8 +231,6 @@ struct amg_handle {
     int symd_minb = 4;            // fixed-slot 32-wide kernel: min CTAs/SM (register budget) 3, 4 or 5
     int vec_groups = 0;           // padded CSR on > 1M rows: visit rows grouped by round count (measured slower:
                                   // G^T_0 83 -> 109..124 us, lanes lose the contiguity of neighbouring rows)
-    int split = 0;                // fine-level ragged matrices: short rows (<= 16) as SELL-32 + long-row list
-                                  // (measured slower on config-2 G^T_0: 121 vs 85 us)
     int sells = 1;                // sorted SELL-32 (sigma window below) where natural slices pad > 10%
     int sells_sigma = 128;
     int sells_buckets = 0;        // > 0: matrices above sells_max_rows get rows partitioned by round count into
@@ -287,17 +241,10 @@ struct amg_handle {
     int64_t sells_max_rows = 1 << 20;  // ... and at most this many rows (sorting costs fine-grid rows their gather
                                        // locality: config-2 G^T_0 85 -> 134 us; coarse A_1 18 -> 13 us)
     int rz_sep = 0;               // PCG: r.z in a separate dot kernel instead of the V-cycle's last SpMV
-    int lrow = 0;                 // long rows: one warp per row (spmv_lrow) instead of the two-pass leaf kernels
-                                  // (bit-identical; measured slower on config 3: A1 425 vs 155 us)
     int vec_minb = 4;             // padded-CSR kernel: min CTAs per SM (register budget) 4, 5 or 6
     int vec_pipe = 0;             // padded-CSR kernel with the first round's columns fetched one row ahead
     int sellu_short = 1;          // ... and for rows of <= 8 entries at any padding, padding slots skipped
     int sellu = 1;                // uniform-width SELL-32 for rows of <= 16 entries padding <= 10% (e.g. FSAI G)
-    int fused = 0;                // FSAI steps of large levels as one G/G^T kernel (fsai_fused): bit-identical but
-                                  // measured slower on config 2 (294 vs 144 us per level-0 step: the kernels are latency-
-                                  // bound, fusing serialises G's and G^T's dependent loads per warp)
-    int fused_wa = 4;             // fsai_ws: G warps per CTA of 8 (the rest compute G^T)
-    int fused_lag_extra = 0;      // extra ticket lag (0 = one grid)
     int symd_chunked = 0;         // symmetric kernels: contiguous row chunk per CTA (measured slower than grid-stride)
     int symd_fixed = 1;           // fixed-slot symmetric kernel: 1 rows <= 8 entries (7-point), 2 also <= 32 (27-point:
                                   // measured slower than the round-by-round kernel on config 2), 0 off
@@ -319,9 +266,6 @@ struct amg_handle {
                                  // footprint delays the cluster launch; streamed from L2 by default)
     int cluster = 16;
     int coarse_pipe = 1;          // pipelined per-warp Cholesky substitution
-    int l2_persist = 0;           // levels [l2_persist_from, l2_persist] mark their matrix values L2-persisting
-    int l2_persist_from = 1;      // (measured slower: the set-aside starves the level-0 gathers)
-    int l2_persist_mb = 0;        // persisting set-aside (0 = device maximum)
     int side_prefetch = 1;        // side-stream L2 prefetch of the tail matrices during the level above it
     int tail_pcap = 16384;        // tail product buffer (entries); larger per-CTA blocks are processed in chunks
     int tail_pcap_used = 0;
@@ -356,25 +300,6 @@ struct amg_handle {
 // ------------------------------------------------------------------ kernels dispatch
 
 typedef void (*SpmvFn)(const SpmvArgs);
-
-static SpmvFn spmv_wt_fn(int epi, int lanes)
-{
-#define AMG_L(E)                                               \
-    switch (lanes) {                                           \
-    case 1: return spmv_wt<E, 1>;                              \
-    case 2: return spmv_wt<E, 2>;                              \
-    case 4: return spmv_wt<E, 4>;                              \
-    default: return spmv_wt<E, 8>;                             \
-    }
-    switch (epi) {
-    case EPI_PLAIN: AMG_L(EPI_PLAIN)
-    case EPI_RESID: AMG_L(EPI_RESID)
-    case EPI_AXPYW: AMG_L(EPI_AXPYW)
-    case EPI_SETW: AMG_L(EPI_SETW)
-    default: AMG_L(EPI_ADD)
-    }
-#undef AMG_L
-}
 
 typedef void (*SpmvSellFn)(const SpmvArgs, const SellArgs, int);
 
@@ -474,67 +399,6 @@ static SpmvSellSFn spmv_sells_fn(int epi, bool plen = false)
 #undef AMG_S2
 }
 
-typedef void (*FusedWsFn)(const FusedWsArgs);
-
-static FusedWsFn fsai_ws_fn(bool set, int wa)
-{
-    if (set) return wa <= 2 ? fsai_ws<EPI_SETW, 2> : wa <= 3 ? fsai_ws<EPI_SETW, 3> : wa <= 4 ? fsai_ws<EPI_SETW, 4> : fsai_ws<EPI_SETW, 5>;
-    return wa <= 2 ? fsai_ws<EPI_AXPYW, 2> : wa <= 3 ? fsai_ws<EPI_AXPYW, 3> : wa <= 4 ? fsai_ws<EPI_AXPYW, 4> : fsai_ws<EPI_AXPYW, 5>;
-}
-
-typedef void (*SpmvSplitShortFn)(const SpmvArgs, const SplitArgs, int);
-typedef void (*SpmvSplitLongFn)(const SpmvArgs, const SplitArgs);
-
-static SpmvSplitShortFn spmv_split_short_fn(int epi)
-{
-    switch (epi) {
-    case EPI_PLAIN: return spmv_split_short<EPI_PLAIN>;
-    case EPI_RESID: return spmv_split_short<EPI_RESID>;
-    case EPI_AXPYW: return spmv_split_short<EPI_AXPYW>;
-    case EPI_SETW: return spmv_split_short<EPI_SETW>;
-    default: return spmv_split_short<EPI_ADD>;
-    }
-}
-
-static SpmvSplitLongFn spmv_split_long_fn(int epi)
-{
-    switch (epi) {
-    case EPI_PLAIN: return spmv_split_long<EPI_PLAIN>;
-    case EPI_RESID: return spmv_split_long<EPI_RESID>;
-    case EPI_AXPYW: return spmv_split_long<EPI_AXPYW>;
-    case EPI_SETW: return spmv_split_long<EPI_SETW>;
-    default: return spmv_split_long<EPI_ADD>;
-    }
-}
-
-typedef void (*SpmvLrowFn)(const SpmvArgs, int);
-
-static SpmvLrowFn spmv_lrow_fn(int epi)
-{
-    switch (epi) {
-    case EPI_PLAIN: return spmv_lrow<EPI_PLAIN>;
-    case EPI_RESID: return spmv_lrow<EPI_RESID>;
-    case EPI_AXPYW: return spmv_lrow<EPI_AXPYW>;
-    case EPI_SETW: return spmv_lrow<EPI_SETW>;
-    default: return spmv_lrow<EPI_ADD>;
-    }
-}
-
-typedef void (*SpmvSellqFn)(const SpmvArgs, const SellArgs, const SellqArgs, int);
-
-static SpmvSellqFn spmv_sellq_fn(int epi, bool pat)
-{
-#define AMG_S(E) return pat ? spmv_sellq<E, true> : spmv_sellq<E, false>;
-    switch (epi) {
-    case EPI_PLAIN: AMG_S(EPI_PLAIN)
-    case EPI_RESID: AMG_S(EPI_RESID)
-    case EPI_AXPYW: AMG_S(EPI_AXPYW)
-    case EPI_SETW: AMG_S(EPI_SETW)
-    default: AMG_S(EPI_ADD)
-    }
-#undef AMG_S
-}
-
 typedef void (*SpmvPatFn)(const SpmvArgs, const PatArgs, int);
 
 static SpmvPatFn spmv_pat_fn(int epi)
@@ -597,44 +461,6 @@ static SpmvLeafsumFn spmv_leafsum_fn(int epi)
     }
 }
 
-static SpmvFn spmv_ws_fn(int epi, int lanes)
-{
-#define AMG_L(E)                                               \
-    switch (lanes) {                                           \
-    case 1: return spmv_ws<E, 1>;                              \
-    case 2: return spmv_ws<E, 2>;                              \
-    case 4: return spmv_ws<E, 4>;                              \
-    default: return spmv_ws<E, 8>;                             \
-    }
-    switch (epi) {
-    case EPI_PLAIN: AMG_L(EPI_PLAIN)
-    case EPI_RESID: AMG_L(EPI_RESID)
-    case EPI_AXPYW: AMG_L(EPI_AXPYW)
-    case EPI_SETW: AMG_L(EPI_SETW)
-    default: AMG_L(EPI_ADD)
-    }
-#undef AMG_L
-}
-
-static SpmvFn spmv_fn(int epi, int lanes)
-{
-#define AMG_L(E)                                               \
-    switch (lanes) {                                           \
-    case 1: return spmv_tiles<E, 1>;                           \
-    case 2: return spmv_tiles<E, 2>;                           \
-    case 4: return spmv_tiles<E, 4>;                           \
-    default: return spmv_tiles<E, 8>;                          \
-    }
-    switch (epi) {
-    case EPI_PLAIN: AMG_L(EPI_PLAIN)
-    case EPI_RESID: AMG_L(EPI_RESID)
-    case EPI_AXPYW: AMG_L(EPI_AXPYW)
-    case EPI_SETW: AMG_L(EPI_SETW)
-    default: AMG_L(EPI_ADD)
-    }
-#undef AMG_L
-}
-
 // Every kernel goes through here: programmatic dependent launch lets a kernel
 // start (stage static matrix tiles) while its predecessor drains.
 template <typename... KArgs, typename... Args>
@@ -650,15 +476,6 @@ static int launch_k(amg_t *h, void (*kern)(KArgs...), int grid, int block, size_
     if (h->pdl) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na].val.programmaticStreamSerializationAllowed = 1;
-        ++na;
-    }
-    if (h->persist_now && h->win_ptr && h->win_bytes) {
-        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[na].val.accessPolicyWindow.base_ptr = const_cast<void *>(h->win_ptr);
-        attr[na].val.accessPolicyWindow.num_bytes = std::min(h->win_bytes, h->win_max);
-        attr[na].val.accessPolicyWindow.hitRatio = 1.0f;
-        attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         ++na;
     }
     cfg.attrs = attr;
@@ -683,24 +500,12 @@ static int raise_smem_caps(int device)
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
         return AMG_OK;
     };
-    for (int e = 0; e <= 4; ++e)
-        for (int l : {1, 2, 4, 8}) {
-            TRY(cap((const void *)spmv_fn(e, l)));
-            TRY(cap((const void *)spmv_ws_fn(e, l)));
-            TRY(cap((const void *)spmv_wt_fn(e, l)));
-        }
-    for (int e = 0; e <= 4; ++e) {
-        TRY(cap((const void *)spmv_sellq_fn(e, true)));
-        TRY(cap((const void *)spmv_sellq_fn(e, false)));
-    }
     TRY(cap((const void *)coarse_solve_k));
     TRY(cap((const void *)tail_vcycle));
     CK(cudaFuncSetAttribute((const void *)tail_vcycle, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     done_for = device;
     return AMG_OK;
 }
-
-static int stage_smem(const amg_t *h) { return h->stages * stage_layout(h->tile_nnz, h->tile_rows).stage_bytes; }
 
 static int exchange(amg_t *h, const DevMat &M, double *x)
 {
@@ -758,23 +563,6 @@ static int allgather_level(amg_t *h, int k, double *y)
     return AMG_OK;
 }
 
-static int configure_kernels(amg_t *h, int *blocks_per_sm)
-{
-    const int smem = stage_smem(h);
-    int best = 1 << 30;
-    TRY(raise_smem_caps(h->device));
-    for (int e = 0; e <= 4; ++e)
-        for (int l : {1, 2, 4, 8}) {
-            SpmvFn f = h->ws ? spmv_ws_fn(e, l) : spmv_fn(e, l);
-            int nb = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, h->ws ? WS_THREADS : TILE_THREADS, smem));
-            best = std::min(best, nb);
-        }
-    if (best < 1) return fail(AMG_E_CUDA, "SpMV tile kernel does not fit on an SM with the chosen staging");
-    *blocks_per_sm = best;
-    return AMG_OK;
-}
-
 // Halo exchange (nranks > 1): pack the owned entries each peer needs, then
 // one grouped ncclSend/ncclRecv per peer into x[n_own ...] (plan order).
 static int exchange(amg_t *h, const DevMat &M, double *x);
@@ -799,23 +587,13 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         return AMG_OK;
     }
     TRY(exchange(h, M, const_cast<double *>(x)));
-    if (h->persist_now) {  // the active layout's value array
-        const void *vp = (M.uval && h->symm) ? (const void *)M.uval
-                         : (M.spv && h->split) ? (const void *)M.spv
-                         : (M.sv_s && h->sells) ? (const void *)M.sv_s
-                         : (M.uval_s && h->sellu) ? (const void *)M.uval_s
-                         : M.sbeg ? (const void *)M.sval
-                         : M.pstart ? (const void *)M.pval : (const void *)M.val;
-        h->win_ptr = vp;
-        h->win_bytes = alloc_bytes(vp);
-    }
     if (h->grid_per_sm > 0) {  // global cap on CTAs per SM (tuning)
         const int c = h->grid_per_sm * h->sm_count;
         grid_cap = grid_cap ? std::min(grid_cap, c) : c;
     }
     const int ufin = fin;
     fin = kfin(h, fin);
-    if (M.ntiles == 0) {
+    if (M.nrows == 0) {
         if (fin != FIN_NONE) {
             VecArgs v{};
             v.n = 0;
@@ -834,11 +612,6 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     a.off = M.off;
     a.col = M.col;
     a.val = M.val;
-    a.tiles = M.tiles;
-    a.ntiles = M.ntiles;
-    a.tile_nnz = h->tile_nnz;
-    a.tile_rows = h->tile_rows;
-    a.stages = h->stages;
     a.x = x;
     a.y = y;
     a.b = b;
@@ -877,18 +650,6 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         else
             TRY(launch_k(h, spmv_symd_fn(epi, h->symd_gminb, M.sym_blocked, tsm), g, VEC_SPMV_THREADS, tsm_bytes, a, sa,
                          (int)M.nrows));
-    } else if (M.spv && h->split) {
-        SplitArgs qa{M.spv, M.spc, M.splen, M.splong, M.sp_nlong, 0};
-        const bool red = dotw != nullptr || fin != FIN_NONE;
-        const int g = grid_cap ? std::min(grid_cap, M.sp_grid) : M.sp_grid;
-        qa.short_grid = g;
-        if (red && g > h->max_grid) return fail(AMG_E_STATE, "internal: split partials exceed the scratch");
-        TRY(launch_k(h, spmv_split_short_fn(epi), g, VEC_SPMV_THREADS, 0, a, qa, (int)M.nrows));
-        SpmvArgs a2 = a;
-        a2.partials = h->partials;
-        const int gl = grid_cap ? std::min(grid_cap, M.sp_lgrid) : M.sp_lgrid;
-        if (red && g + gl > h->max_grid) return fail(AMG_E_STATE, "internal: split partials exceed the scratch");
-        TRY(launch_k(h, spmv_split_long_fn(epi), gl, VEC_SPMV_THREADS, 0, a2, qa));
     } else if (M.sv_s && h->sells) {
         SellSArgs qa{M.sv_s, M.sc_s, M.sb_s, M.sw_s, M.sp_s, M.sl_s};
         TRY(launch_k(h, spmv_sells_fn(epi, h->sells_plen), grid_cap ? std::min(grid_cap, M.s_grid) : M.s_grid, VEC_SPMV_THREADS, 0, a,
@@ -897,12 +658,6 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW};
         TRY(launch_k(h, spmv_sellu_fn(epi, M.uW, M.u_plen), grid_cap ? std::min(grid_cap, M.u_grid) : M.u_grid, VEC_SPMV_THREADS, 0,
                      a, ua, (int)M.nrows));
-    } else if (M.sbeg && M.sq_cta && h->sellq) {
-        SellArgs sa{M.sbeg, M.sval, M.scol, M.slen, M.pid, M.prel, M.pbeg, M.npat, M.nrel, M.sperm};
-        SellqArgs q{M.sq_cta, M.sq_stage, M.sq_stages};
-        // grid fixed by the upload-time CTA ranges (one CTA per SM, never above a gated grid cap)
-        TRY(launch_k(h, spmv_sellq_fn(epi, M.scol == nullptr), M.sq_grid, SQ_THREADS, (size_t)M.sq_smem, a, sa, q,
-                     (int)M.nrows));
     } else if (M.sbeg) {
         SellArgs sa{M.sbeg, M.sval, M.scol, M.slen, M.pid, M.prel, M.pbeg, M.npat, M.nrel, M.sperm};
         TRY(launch_k(h, spmv_sell_fn(epi, M.scol == nullptr), grid_cap ? std::min(grid_cap, M.sell_grid) : M.sell_grid,
@@ -911,10 +666,6 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         PatArgs pa{M.pstart, M.pval, M.pid, M.prel, M.pbeg, M.npat, M.nrel};
         TRY(launch_k(h, spmv_pat_fn(epi), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
                      pa, (int)M.nrows));
-    } else if (M.leaf && M.lrow_ok && h->lrow) {
-        const int g = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + LR_WARPS - 1) / LR_WARPS, (int64_t)h->sm_count * 2));
-        TRY(launch_k(h, spmv_lrow_fn(epi), grid_cap ? std::min(grid_cap, g) : g, LR_WARPS * 32,
-                     (size_t)LR_WARPS * LR_BUF * sizeof(double), a, (int)M.nrows));
     } else if (M.leaf) {
         LeafArgs la{M.leaf, M.nleaves, M.lsum, M.row_leaf};
         SpmvArgs a1 = a;  // leaf pass: no reduction
@@ -927,20 +678,12 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         PadArgs pa{M.pstart, M.pval, M.pcol, h->vec_pipe ? nullptr : M.pperm};
         TRY(launch_k(h, spmv_vec_fn(epi, h->vec_pipe, h->vec_minb), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
                      pa, (int)M.nrows));
-    } else if (h->kernel == 3 && M.nwtiles > 0) {
-        SpmvArgs w = a;
-        w.tiles = M.wtiles;
-        w.ntiles = M.nwtiles;
-        w.tile_nnz = M.wt_nnz;
-        const size_t smem = (size_t)WT_WARPS * 2 * stage_layout(M.wt_nnz, WT_ROWS).stage_bytes;
-        TRY(launch_k(h, spmv_wt_fn(epi, M.wt_lanes), M.wt_grid, WT_THREADS, smem, w));
-    } else if (h->kernel == 2) {
+    } else {
         const int gpr = DIRECT_THREADS / M.lanes;  // row groups per CTA
         int g = (int)std::min<int64_t>((M.nrows + gpr - 1) / gpr, (int64_t)h->sm_count * h->direct_per_sm);
         if (grid_cap) g = std::min(g, grid_cap);
         TRY(launch_k(h, spmv_direct_fn(epi, M.lanes), std::max(g, 1), DIRECT_THREADS, 0, a, (int)M.nrows));
-    } else if (h->ws) TRY(launch_k(h, spmv_ws_fn(epi, std::min(M.lanes, 8)), M.grid, WS_THREADS, (size_t)stage_smem(h), a));
-    else TRY(launch_k(h, spmv_fn(epi, std::min(M.lanes, 8)), M.grid, TILE_THREADS, (size_t)stage_smem(h), a));
+    }
     TRY(post_fin(h, ufin, g1));
     return AMG_OK;
 }
@@ -1064,61 +807,7 @@ static int enqueue_smooth(amg_t *h, int k, const double *b, double *x, int steps
             src = L.r;
         }
         const bool set = from_zero && s == 0;
-        if (L.sm_kind == AMG_SMOOTHER_FSAI && L.fz.on && h->fused && !h->collect) {
-            FusedArgs fa{};
-            fa.gval = L.fz.gval;
-            fa.gcol = L.fz.gcol;
-            fa.glen = L.fz.glen;
-            fa.tstart = L.fz.tstart;
-            fa.tq = L.fz.tq;
-            fa.y = src;
-            fa.t = L.t;
-            fa.x = x;
-            fa.omega = L.omega;
-            fa.nrows = (int)L.n;
-            fa.W = L.fz.W;
-            fa.nunits = L.fz.nunits;
-            fa.nblk = L.fz.nblk;
-            fa.lag = L.fz.lag;
-            fa.reach = L.fz.reach;
-            fa.bcnt = L.fz.bcnt;
-            fa.ctr = L.fz.ctr;
-            fa.upart = L.fz.upart;
-            fa.dotw = dw;
-            fa.fin = kfin(h, f);
-            fa.ctl = h->ctl;
-            fa.gate1 = g1;
-            fa.gate2 = nullptr;
-            if (h->fused >= 2 && L.fz.gt16) {
-                FusedWsArgs wa{};
-                wa.gval = L.fz.gval;
-                wa.gcol = L.fz.gcol;
-                wa.glen = L.fz.glen;
-                wa.tstart = L.fz.tstart;
-                wa.gt16 = L.fz.gt16;
-                wa.y = src;
-                wa.t = L.t;
-                wa.x = x;
-                wa.omega = L.omega;
-                wa.nrows = (int)L.n;
-                wa.W = L.fz.W;
-                wa.nunits = L.fz.nunits;
-                wa.nblk = L.fz.nblk;
-                wa.reach = L.fz.reach;
-                wa.slot = L.fz.slot;
-                wa.bcnt = L.fz.bcnt;
-                wa.ctr = L.fz.ctr;
-                wa.upart = L.fz.upart;
-                wa.dotw = dw;
-                wa.fin = kfin(h, f);
-                wa.ctl = h->ctl;
-                wa.gate1 = g1;
-                TRY(launch_k(h, fsai_ws_fn(set, h->fused_wa), L.fz.ws_grid, FUSED_THREADS, 0, wa));
-            } else {
-                TRY(launch_k(h, set ? fsai_fused<EPI_SETW> : fsai_fused<EPI_AXPYW>, L.fz.grid, FUSED_THREADS, 0, fa));
-            }
-            TRY(post_fin(h, f, g1));
-        } else if (L.sm_kind == AMG_SMOOTHER_FSAI) {
+        if (L.sm_kind == AMG_SMOOTHER_FSAI) {
             TRY(launch_spmv(h, L.m[AMG_G], src, L.t, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, g1, nullptr));
             TRY(launch_spmv(h, L.m[AMG_GT], L.t, x, set ? EPI_SETW : EPI_AXPYW, x, L.omega, dw, f, g1, nullptr));
         } else if (h->collect) {
@@ -1157,7 +846,6 @@ static int enqueue_vcycle(amg_t *h, int k, const double *y, double *x, const int
     if (k == nl - 1) return launch_coarse(h, y, x, g1, fin, dotw);
     LevelD &L = h->lv[k];
     LevelD &C = h->lv[k + 1];
-    h->persist_now = h->l2_persist > 0 && k >= h->l2_persist_from && k <= h->l2_persist && h->win_max > 0;
     if (!h->collect && h->side_prefetch && h->pf_n > 0 && h->tail_level > 0 && k == h->tail_level - 1) {
         CK(cudaEventRecord(h->pf_fork, h->stream));
         CK(cudaStreamWaitEvent(h->side, h->pf_fork, 0));
@@ -1177,7 +865,6 @@ static int enqueue_vcycle(amg_t *h, int k, const double *y, double *x, const int
     TRY(launch_spmv(h, L.m[AMG_PT], r, yc, EPI_PLAIN, nullptr, 0.0, nullptr, FIN_NONE, g1, nullptr));
     if (agglom) TRY(allgather_level(h, k + 1, C.y));
     TRY(enqueue_vcycle(h, k + 1, C.y, C.x, g1, FIN_NONE, nullptr));
-    h->persist_now = h->l2_persist > 0 && k >= h->l2_persist_from && k <= h->l2_persist && h->win_max > 0;
     const bool tail_on_p = (h->nu2 == 0);
     TRY(launch_spmv(h, L.m[AMG_P], C.x, x, h->nu1 > 0 ? EPI_ADD : EPI_PLAIN, x, 0.0, tail_on_p ? dotw : nullptr,
                     tail_on_p ? fin : FIN_NONE, g1, nullptr));
@@ -1218,7 +905,6 @@ static int enqueue_pcg_body(amg_t *h, cudaGraphConditionalHandle handle, int use
     } else {
         TRY(enqueue_vcycle(h, 0, h->r, h->z, act, FIN_RZ, h->r));
     }
-    h->persist_now = false;
     if (h->lv.size() == 1) {
         // the coarse kernel carried the dot already
     }
@@ -1572,7 +1258,7 @@ void amg_destroy(amg_t *h)
     };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.tiles); F(M.wtiles); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.sq_cta); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.pperm); F(M.spv); F(M.spc); F(M.splong); F(M.splen); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s); F(M.dcls); F(M.dbeg); F(M.drel); F(M.dval);
+            F(M.off); F(M.col); F(M.val); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.pperm); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s); F(M.dcls); F(M.dbeg); F(M.drel); F(M.dval);
             symd_slot_give(h->device, M.sym_slot);
             M.sym_slot = -1;
             symd_tab_give(h->device, M.sym_tab, M.sym_ntab);
@@ -1580,15 +1266,8 @@ void amg_destroy(amg_t *h)
             halo_free(M.halo);
         }
         F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
-        F(L.fz.gval); F(L.fz.gcol); F(L.fz.glen); F(L.fz.tstart); F(L.fz.tq); F(L.fz.bcnt); F(L.fz.ctr); F(L.fz.upart); F(L.fz.gt16);
-        symd_slot_give(h->device, L.fz.slot);
-        L.fz.slot = -1;
     }
     F(h->pf_ranges);
-    if (h->win_max > 0) {  // give the persisting L2 set-aside back (process-wide device limit)
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
-        cudaCtxResetPersistingL2Cache();
-    }
     if (h->side) cudaStreamDestroy(h->side);
     if (h->pf_fork) cudaEventDestroy(h->pf_fork);
     if (h->pf_join) cudaEventDestroy(h->pf_join);
@@ -1612,24 +1291,16 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "batch") { h->batch = std::max<int>(1, (int)value); return AMG_OK; }
     if (k == "pdl") { h->pdl = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (h->finalized) return fail(AMG_E_STATE, "amg_set_option: '" + k + "' must be set before amg_finalize");
-    if (k == "tile_nnz") { if (value < 64 || value > 8192) return fail(AMG_E_ARG, "tile_nnz out of range"); h->tile_nnz = (int)value; return AMG_OK; }
-    if (k == "tile_rows") { if (value < 32 || value > 1024) return fail(AMG_E_ARG, "tile_rows out of range"); h->tile_rows = (int)value; return AMG_OK; }
-    if (k == "stages") { if (value < 1 || value > 8) return fail(AMG_E_ARG, "stages out of range"); h->stages = (int)value; return AMG_OK; }
     if (k == "tail_nnz") { h->tail_nnz = value; return AMG_OK; }
     if (k == "tail_stage") { h->tail_stage = value ? 1 : 0; return AMG_OK; }
     if (k == "cluster") { if (value != 8 && value != 16 && value != 4 && value != 2 && value != 1) return fail(AMG_E_ARG, "cluster must be 1,2,4,8,16"); h->cluster = (int)value; return AMG_OK; }
-    if (k == "persistent") { h->persistent = value ? 1 : 0; return AMG_OK; }
-    if (k == "ws") { h->ws = value ? 1 : 0; return AMG_OK; }
-    if (k == "kernel") { h->kernel = (int)value; return AMG_OK; }
     if (k == "pad_min") { h->pad_min = (int)value; return AMG_OK; }
-    if (k == "sellq") { h->sellq = (int)value; return AMG_OK; }
     if (k == "long_avg") { h->long_avg = (int)value; return AMG_OK; }
     if (k == "small_rows_per_sm") { h->small_rows_per_sm = (int)value; return AMG_OK; }
     if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
     if (k == "symm") { h->symm = value ? 1 : 0; return AMG_OK; }
     if (k == "dict") { h->dict = value ? 1 : 0; return AMG_OK; }
     if (k == "vec_groups") { h->vec_groups = (int)value; return AMG_OK; }
-    if (k == "split") { h->split = value ? 1 : 0; return AMG_OK; }
     if (k == "sells") { h->sells = (int)value; return AMG_OK; }
     if (k == "sells_max_rows") { h->sells_max_rows = value; return AMG_OK; }
     if (k == "sells_buckets") { h->sells_buckets = (int)value; return AMG_OK; }
@@ -1638,20 +1309,13 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "sells_sigma") { h->sells_sigma = (int)value; return AMG_OK; }
     if (k == "sells_min_avg10") { h->sells_min_avg = value / 10.0; return AMG_OK; }
     if (k == "rz_sep") { h->rz_sep = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
-    if (k == "lrow") { h->lrow = value ? 1 : 0; return AMG_OK; }
     if (k == "vec_minb") { h->vec_minb = (int)value; return AMG_OK; }
     if (k == "vec_pipe") { h->vec_pipe = value ? 1 : 0; return AMG_OK; }
     if (k == "sellu_short") { h->sellu_short = value ? 1 : 0; return AMG_OK; }
     if (k == "sellu") { h->sellu = value ? 1 : 0; return AMG_OK; }
-    if (k == "fused") { h->fused = (int)value; return AMG_OK; }
-    if (k == "fused_wa") { h->fused_wa = (int)value; return AMG_OK; }
-    if (k == "fused_lag_extra") { h->fused_lag_extra = (int)value; return AMG_OK; }
     if (k == "symd_fixed") { h->symd_fixed = (int)value; return AMG_OK; }
     if (k == "symd_chunked") { h->symd_chunked = value ? 1 : 0; return AMG_OK; }
     if (k == "coarse_pipe") { h->coarse_pipe = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
-    if (k == "l2_persist_from") { h->l2_persist_from = (int)value; return AMG_OK; }
-    if (k == "l2_persist_mb") { h->l2_persist_mb = (int)value; return AMG_OK; }
-    if (k == "l2_persist") { h->l2_persist = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "side_prefetch") { h->side_prefetch = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "tail_pcap") {
         if (value < 1 || value > (1 << 24)) return fail(AMG_E_ARG, "tail_pcap must be in [1, 2^24]");
@@ -1674,9 +1338,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "gated_grid") { h->gated_grid = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "sell_pad") { h->sell_pad = (int)value; return AMG_OK; }
     if (k == "sell_sigma") { h->sell_sigma = (int)value; return AMG_OK; }
-    if (k == "wt_nnz") { if (value < 64 || value > 1024) return fail(AMG_E_ARG, "wt_nnz out of range"); h->wt_nnz = (int)value; return AMG_OK; }
     if (k == "direct_ctas") { h->direct_ctas = (int)value; return AMG_OK; }
-    if (k == "ctas_per_sm") { h->ctas_per_sm = (int)value; return AMG_OK; }
     if (k == "lanes") { if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8) return fail(AMG_E_ARG, "lanes must be 0,1,2,4,8"); h->lanes_override = (int)value; return AMG_OK; }
     return fail(AMG_E_ARG, "amg_set_option: unknown key '" + k + "'");
 }
@@ -1770,24 +1432,6 @@ int64_t amg_local_rows(amg_t *h, int level)
 {
     if (!h || level < 0 || level >= (int)h->lv.size()) return -1;
     return h->lv[level].n;
-}
-
-static void build_tiles(const std::vector<int32_t> &off, int64_t nrows, int tile_nnz, int tile_rows,
-                        std::vector<TileDesc> &tiles)
-{
-    tiles.clear();
-    int64_t r = 0;
-    while (r < nrows) {
-        const int64_t r0 = r;
-        const int32_t k0 = off[r];
-        if (off[r + 1] - off[r] > tile_nnz) {
-            tiles.push_back({(int32_t)r, (int32_t)(r + 1), off[r], off[r + 1]});
-            ++r;
-            continue;
-        }
-        while (r < nrows && r - r0 < tile_rows && off[r + 1] - k0 <= tile_nnz) ++r;
-        tiles.push_back({(int32_t)r0, (int32_t)r, k0, off[r]});
-    }
 }
 
 int amg_upload_matrix(amg_t *h, int level, int which, int64_t local_nrows, int64_t global_ncols,
@@ -2181,131 +1825,6 @@ static int build_symd(amg_t *h, DevMat &M, const std::vector<int32_t> &off32, co
     return AMG_OK;
 }
 
-// FSAI step kernel data (fsai_fused) for the large levels of a single-GPU
-// hierarchy: G as uniform-width SELL-32 (padding <= 10%), G^T as positions
-// into it.  Taken only if the uploaded G^T is exactly the transpose of G
-// (same entries, same order, bitwise values); otherwise the two-kernel path stays.
-static int build_fused(amg_t *h)
-{
-    if (h->nranks != 1) return AMG_OK;
-    const int nl = (int)h->lv.size();
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)fsai_fused<EPI_AXPYW>, FUSED_THREADS, 0));
-    if (occ < 1) return AMG_OK;
-    for (int k = 0; k < nl - 1; ++k) {
-        LevelD &L = h->lv[k];
-        if (L.sm_kind != AMG_SMOOTHER_FSAI || L.n < (int64_t)h->sm_count * h->small_rows_per_sm) continue;
-        const DevMat &G = L.m[AMG_G], &GT = L.m[AMG_GT];
-        if (!G.present || !GT.present || G.nrows != L.n || G.ncols != L.n || GT.nrows != L.n || GT.nnz != G.nnz) continue;
-        const int64_t n = L.n, nnz = G.nnz;
-        std::vector<int32_t> go(n + 1), gc(nnz), to(n + 1), tc(nnz);
-        std::vector<double> gv(nnz), tv(nnz);
-        CK(cudaMemcpy(go.data(), G.off, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(to.data(), GT.off, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
-        if (nnz) {
-            CK(cudaMemcpy(gc.data(), G.col, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(gv.data(), G.val, nnz * sizeof(double), cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(tc.data(), GT.col, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(tv.data(), GT.val, nnz * sizeof(double), cudaMemcpyDeviceToHost));
-        }
-        int W = 0;
-        for (int64_t r = 0; r < n; ++r) W = std::max(W, go[r + 1] - go[r]);
-        const int64_t ns = (n + 31) / 32;
-        if (W == 0 || W > 129 || (double)ns * 32 * W > 1.10 * (double)nnz || ns * 32 * W >= INT32_MAX - 64) continue;
-        for (int64_t r = 0; r < n; ++r)
-            if (to[r + 1] - to[r] > 129) W = -1;
-        if (W < 0) continue;
-        std::vector<double> sv((size_t)ns * 32 * W, 0.0);
-        std::vector<int32_t> sc((size_t)ns * 32 * W, 0);
-        std::vector<uint8_t> ln(n + 16, 0);
-        std::vector<int32_t> cnt(n + 1, 0);
-        for (int64_t r = 0; r < n; ++r) {
-            ln[r] = (uint8_t)(go[r + 1] - go[r]);
-            for (int32_t e = go[r]; e < go[r + 1]; ++e) {
-                const int64_t q = (r >> 5) * 32 * W + 32 * (int64_t)(e - go[r]) + (r & 31);
-                sv[q] = gv[e];
-                sc[q] = gc[e];
-                ++cnt[gc[e] + 1];
-            }
-            for (int32_t e = go[r + 1] - go[r]; e < W; ++e) sc[(r >> 5) * 32 * W + 32 * e + (r & 31)] = (int32_t)r;
-        }
-        for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
-        bool ok = true;
-        for (int64_t i = 0; i < n && ok; ++i) ok = (cnt[i + 1] - cnt[i]) == (to[i + 1] - to[i]) && to[i] == cnt[i];
-        if (!ok) continue;
-        std::vector<int32_t> tq(nnz > 0 ? nnz : 1), fill(cnt.begin(), cnt.end() - 1);
-        int64_t reach = 0;
-        for (int64_t r = 0; r < n; ++r)  // rows of G in ascending order: G^T rows fill in ascending column order
-            for (int32_t e = go[r]; e < go[r + 1]; ++e) {
-                const int32_t i = gc[e];
-                const int64_t q = (r >> 5) * 32 * W + 32 * (int64_t)(e - go[r]) + (r & 31);
-                const int32_t m = fill[i]++;
-                if (tc[m] != (int32_t)r || memcmp(&tv[m], &gv[e], sizeof(double)) != 0) ok = false;
-                tq[m] = (int32_t)q;
-                reach = std::max<int64_t>(reach, r - i);
-            }
-        if (!ok) continue;
-        // 2-byte G^T entries for fsai_ws: G offset ids (<= 256 distinct) and positions k < 256
-        std::vector<uint16_t> g16;
-        std::vector<int32_t> rels;
-        if (h->fused >= 2 && W <= 16) {
-            std::vector<int32_t> all(nnz);
-            for (int64_t r = 0; r < n; ++r)
-                for (int32_t e = go[r]; e < go[r + 1]; ++e) all[e] = r - gc[e];  // j - i >= 0
-            rels = all;
-            std::sort(rels.begin(), rels.end());
-            rels.erase(std::unique(rels.begin(), rels.end()), rels.end());
-            if (rels.size() <= 256) {
-                g16.resize(nnz > 0 ? nnz : 1);
-                std::vector<int32_t> fill2(cnt.begin(), cnt.end() - 1);
-                for (int64_t r = 0; r < n; ++r)
-                    for (int32_t e = go[r]; e < go[r + 1]; ++e) {
-                        const int32_t i = gc[e];
-                        const int id = (int)(std::lower_bound(rels.begin(), rels.end(), (int32_t)(r - i)) - rels.begin());
-                        g16[fill2[i]++] = (uint16_t)(((e - go[r]) << 8) | id);
-                    }
-            }
-        }
-        auto &F = L.fz;
-        F.W = W;
-        F.nunits = (int)((n + 31) / 32);
-        F.nblk = (F.nunits + 7) / 8;
-        F.reach = (int)reach;
-        F.grid = std::max(1, std::min((F.nunits + 7) / 8, occ * h->sm_count));  // one resident wave
-        F.lag = (int)((reach + 63) / 32) + 8 + (h->fused_lag_extra > 0 ? h->fused_lag_extra : F.grid * (FUSED_THREADS / 32));
-        TRY(dalloc(&F.gval, sv.size()));
-        TRY(dalloc(&F.gcol, sc.size()));
-        TRY(dalloc(&F.glen, ln.size()));
-        TRY(dalloc(&F.tstart, (size_t)n + 1));
-        TRY(dalloc(&F.tq, tq.size()));
-        TRY(dalloc(&F.bcnt, (size_t)F.nblk));
-        TRY(dalloc(&F.ctr, 4));
-        TRY(dalloc(&F.upart, (size_t)F.nunits));
-        CK(cudaMemcpy(F.gval, sv.data(), sv.size() * sizeof(double), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(F.gcol, sc.data(), sc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(F.glen, ln.data(), ln.size(), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(F.tstart, cnt.data(), ((size_t)n + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(F.tq, tq.data(), tq.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-        if (!g16.empty()) {
-            const int slot = symd_slot_take(h->device);
-            if (slot >= 0) {
-                std::vector<int32_t> tab(256, 0);
-                for (size_t q = 0; q < rels.size(); ++q) tab[q] = -rels[q];  // j = i - c_gt_rel[id]
-                CK(cudaMemcpyToSymbol(c_gt_rel, tab.data(), 256 * sizeof(int32_t), (size_t)slot * 256 * sizeof(int32_t)));
-                TRY(dalloc(&F.gt16, g16.size()));
-                CK(cudaMemcpy(F.gt16, g16.data(), g16.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
-                F.slot = slot;
-                int occw = 0;
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occw, (const void *)fsai_ws_fn(false, h->fused_wa),
-                                                                 FUSED_THREADS, 0));
-                F.ws_grid = std::max(1, std::min((F.nunits + 7) / 8, std::max(occw, 1) * h->sm_count));  // one resident wave
-            }
-        }
-        F.on = true;
-    }
-    return AMG_OK;
-}
-
 int amg_finalize(amg_t *h)
 {
     if (!h) return fail(AMG_E_ARG, "NULL handle");
@@ -2365,9 +1884,7 @@ int amg_finalize(amg_t *h)
     }
     h->container = container;
     if (!container && h->nc != h->lv[nl - 1].gn) return fail(AMG_E_DIM, "coarsest factor size does not match the last level");
-    int bps = 1;
-    TRY(configure_kernels(h, &bps));
-    const int per_sm = h->ctas_per_sm > 0 ? std::min(h->ctas_per_sm, bps) : bps;
+    TRY(raise_smem_caps(h->device));
     {
         int best = 1 << 30;
         for (int e = 0; e <= 4; ++e)
@@ -2380,8 +1897,7 @@ int amg_finalize(amg_t *h)
         h->max_grid = std::max(h->max_grid, h->sm_count * h->direct_per_sm);
     }
     h->max_grid = h->sm_count * 8;
-    if (!h->persistent) h->stages = 1;  // one tile per CTA: a single staging buffer
-    // halos (nranks > 1) + tile schedules
+    // device layouts per matrix
     for (int k = 0; k < nl; ++k) {
         LevelD &L = h->lv[k];
         for (int w = 0; w < 5; ++w) {
@@ -2389,33 +1905,6 @@ int amg_finalize(amg_t *h)
             if (!M.present) continue;
             std::vector<int32_t> off32(M.nrows + 1);
             CK(cudaMemcpy(off32.data(), M.off, (M.nrows + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
-            std::vector<TileDesc> tiles;
-            build_tiles(off32, M.nrows, h->tile_nnz, h->tile_rows, tiles);
-            M.ntiles = (int)tiles.size();
-            TRY(dalloc(&M.tiles, tiles.size()));
-            if (!tiles.empty()) CK(cudaMemcpy(M.tiles, tiles.data(), tiles.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
-            {   // warp tiles: capacity covers the typical row so long rows stay rare
-                int maxlen = 0;
-                for (int64_t r = 0; r < M.nrows; ++r) maxlen = std::max(maxlen, off32[r + 1] - off32[r]);
-                int cap = h->wt_nnz;
-                while (cap < maxlen && cap < 1024) cap *= 2;
-                M.wt_nnz = cap;
-                std::vector<TileDesc> wt;
-                build_tiles(off32, M.nrows, cap, WT_ROWS, wt);
-                M.nwtiles = (int)wt.size();
-                TRY(dalloc(&M.wtiles, wt.size()));
-                if (!wt.empty()) CK(cudaMemcpy(M.wtiles, wt.data(), wt.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
-                const double rows_per_tile = wt.empty() ? 1.0 : (double)M.nrows / (double)wt.size();
-                M.wt_lanes = h->lanes_override ? std::min(h->lanes_override, 8)
-                             : rows_per_tile >= 24.0 ? 1 : rows_per_tile >= 12.0 ? 2 : rows_per_tile >= 6.0 ? 4 : 8;
-                const size_t smem = (size_t)WT_WARPS * 2 * stage_layout(cap, WT_ROWS).stage_bytes;
-                int nb = 0;
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_wt_fn(EPI_RESID, M.wt_lanes), WT_THREADS, smem));
-                nb = std::max(nb, 1);
-                const int warps_needed = (M.nwtiles + 1) / 2;  // >= 2 tiles per warp keeps the ring busy
-                M.wt_grid = std::max(1, std::min((warps_needed + WT_WARPS - 1) / WT_WARPS, h->sm_count * nb));
-                h->max_grid = std::max(h->max_grid, M.wt_grid);
-            }
             // row-class dictionary first: where it applies no value / column stream is needed
             if (h->dict && h->nranks == 1 && !h->lanes_override && M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm)
                 TRY(build_dict(h, M, off32));
@@ -2423,14 +1912,6 @@ int amg_finalize(amg_t *h)
             const bool longrows = !M.dcls && h->long_avg > 0 && !h->lanes_override && M.nrows > 0 &&
                                   (double)M.nnz / (double)M.nrows > (double)h->long_avg;
             if (longrows) {
-                int64_t mx = 0;
-                for (int64_t r = 0; r < M.nrows; ++r) mx = std::max<int64_t>(mx, off32[r + 1] - off32[r]);
-                M.lrow_ok = mx <= 6000 ? 1 : 0;  // <= LR_MAXLEAF leaves per row
-                if (M.lrow_ok) {
-                    for (int e = 0; e < 5; ++e)
-                        CK(cudaFuncSetAttribute((const void *)spmv_lrow_fn(e), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)(LR_WARPS * LR_BUF * sizeof(double))));
-                }
                 std::vector<int2> lv;
                 std::vector<int32_t> rl(M.nrows + 1);
                 int sb[32], sm[32];
@@ -2597,37 +2078,6 @@ int amg_finalize(amg_t *h)
                             TRY(dalloc(&M.scol, sc.size()));
                             CK(cudaMemcpy(M.scol, sc.data(), sc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
                         }
-                        if (h->sellq && maxlen <= SQ_MAXLEN && !sorted) {
-                            // bulk-copy streamed variant: chunk c = slices [8c, 8c + 8); ring stages sized for
-                            // the largest chunk, as many as fit (2..4); chunk ranges per CTA balanced by entries
-                            const int bpe = pat ? 8 : 12;
-                            const int rel_bytes = pat ? (((M.nrel + 3) & ~3) + M.npat + 1) * 4 : 0;
-                            cudaFuncAttributes fa;
-                            CK(cudaFuncGetAttributes(&fa, (const void *)spmv_sellq_fn(EPI_RESID, pat)));
-                            int optin = 0;
-                            CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
-                            const int avail = optin - (int)fa.sharedSizeBytes - rel_bytes - 256;
-                            const int64_t nch = (ns + SQ_WARPS - 1) / SQ_WARPS;
-                            int64_t se = 0;
-                            for (int64_t c = 0; c < nch; ++c)
-                                se = std::max<int64_t>(se, sb[std::min<int64_t>(ns, (c + 1) * SQ_WARPS)] - sb[c * SQ_WARPS]);
-                            const int S = (int)std::min<int64_t>(SQ_MAXSTAGES, avail / std::max<int64_t>(1, se * bpe));
-                            if (S >= 2 && nch > 0) {
-                                const int G = (int)std::max<int64_t>(1, std::min<int64_t>(h->sm_count, nch));
-                                std::vector<int32_t> ct(G + 1, (int32_t)nch);
-                                ct[0] = 0;
-                                int b = 1;
-                                for (int64_t c = 0; c < nch && b < G; ++c)  // CTA b starts past b/G of the entries
-                                    while (b < G && (int64_t)sb[std::min<int64_t>(ns, (c + 1) * SQ_WARPS)] * G >= (int64_t)tot * b)
-                                        ct[b++] = (int32_t)(c + 1);
-                                TRY(dalloc(&M.sq_cta, ct.size()));
-                                CK(cudaMemcpy(M.sq_cta, ct.data(), ct.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-                                M.sq_grid = G;
-                                M.sq_stage = (int)se;
-                                M.sq_stages = S;
-                                M.sq_smem = S * (int)se * bpe + rel_bytes;
-                            }
-                        }
                         int nbs = 0;
                         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbs, (const void *)spmv_sell_fn(EPI_RESID, pat), VEC_SPMV_THREADS, 0));
                         M.sell_grid = (int)std::max<int64_t>(1, std::min<int64_t>((ns + 7) / 8, (int64_t)h->sm_count * std::max(nbs, 1)));
@@ -2712,61 +2162,7 @@ int amg_finalize(amg_t *h)
                     h->max_grid = std::max(h->max_grid, M.u_grid);
                 }
             }
-            if (!M.dcls && !M.uval && !M.uval_s && h->split && !longrows && !h->lanes_override && M.nrows > h->sells_max_rows &&
-                (double)M.nnz >= h->sells_min_avg * (double)M.nrows && M.nrows < INT32_MAX / 32 / 16) {
-                // short / long split: rows of <= 16 entries as width-16 SELL-32 (padding never loaded)
-                int64_t nshort = 0;
-                for (int64_t r = 0; r < M.nrows; ++r) nshort += (off32[r + 1] - off32[r] <= 16);
-                if ((double)nshort >= 0.75 * (double)M.nrows) {
-                    std::vector<int32_t> col_h(M.nnz);
-                    std::vector<double> val_h(M.nnz);
-                    if (M.nnz) {
-                        CK(cudaMemcpy(col_h.data(), M.col, M.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
-                        CK(cudaMemcpy(val_h.data(), M.val, M.nnz * sizeof(double), cudaMemcpyDeviceToHost));
-                    }
-                    const int64_t ns = (M.nrows + 31) / 32;
-                    const size_t tot = (size_t)ns * 32 * 16;
-                    std::vector<double> sv(tot, 0.0);
-                    std::vector<int32_t> sc(tot, 0);
-                    std::vector<uint8_t> ln(M.nrows + 16, 0);
-                    std::vector<int32_t> lr;
-                    for (int64_t r = 0; r < M.nrows; ++r) {
-                        const int32_t len = off32[r + 1] - off32[r];
-                        if (len > 16) {
-                            ln[r] = 255;
-                            lr.push_back((int32_t)r);
-                            continue;
-                        }
-                        ln[r] = (uint8_t)len;
-                        const int64_t b0 = (r >> 5) * 32 * 16 + (r & 31);
-                        for (int32_t k = 0; k < len; ++k) {
-                            sv[b0 + 32 * k] = val_h[off32[r] + k];
-                            sc[b0 + 32 * k] = col_h[off32[r] + k];
-                        }
-                    }
-                    TRY(dalloc(&M.spv, tot));
-                    TRY(dalloc(&M.spc, tot));
-                    M.lbytes[AMG_LAYOUT_SPLIT] = (int64_t)tot * 12 + (int64_t)ln.size() + (int64_t)lr.size() * 4;
-                    TRY(dalloc(&M.splen, ln.size()));
-                    TRY(dalloc(&M.splong, lr.size() + 1));
-                    CK(cudaMemcpy(M.spv, sv.data(), tot * sizeof(double), cudaMemcpyHostToDevice));
-                    CK(cudaMemcpy(M.spc, sc.data(), tot * sizeof(int32_t), cudaMemcpyHostToDevice));
-                    CK(cudaMemcpy(M.splen, ln.data(), ln.size(), cudaMemcpyHostToDevice));
-                    if (!lr.empty()) CK(cudaMemcpy(M.splong, lr.data(), lr.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-                    M.sp_nlong = (int)lr.size();
-                    int nb1 = 0, nb2 = 0;
-                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb1, (const void *)spmv_split_short_fn(EPI_RESID),
-                                                                     VEC_SPMV_THREADS, 0));
-                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, (const void *)spmv_split_long_fn(EPI_RESID),
-                                                                     VEC_SPMV_THREADS, 0));
-                    M.sp_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
-                                                                           (int64_t)h->sm_count * std::max(nb1, 1)));
-                    M.sp_lgrid = (int)std::max<int64_t>(1, std::min<int64_t>((M.sp_nlong + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
-                                                                            (int64_t)h->sm_count * std::max(nb2, 1)));
-                    h->max_grid = std::max(h->max_grid, M.sp_grid + M.sp_lgrid);
-                }
-            }
-            if (!M.dcls && !M.uval && !M.uval_s && !M.spv && h->sells && !longrows && !h->lanes_override && h->sells_sigma >= 32 &&
+            if (!M.dcls && !M.uval && !M.uval_s && h->sells && !longrows && !h->lanes_override && h->sells_sigma >= 32 &&
                 M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm &&
                 (M.nrows <= h->sells_max_rows || h->sells_buckets) &&
                 (double)M.nnz >= h->sells_min_avg * (double)M.nrows) {
@@ -2868,11 +2264,7 @@ int amg_finalize(amg_t *h)
             // more lanes: the dependent load chain per lane shrinks and more SMs take part
             const bool small = M.nrows < (int64_t)h->sm_count * h->small_rows_per_sm;
             M.lanes = h->lanes_override ? h->lanes_override
-                      : h->kernel == 2   ? (small ? (avg >= 16.0 ? 8 : avg >= 6.0 ? 4 : 2)
-                                                  : (avg < 48.0 ? 1 : avg < 96.0 ? 4 : 8))
-                                         : (avg < 9.0 ? 1 : avg < 17.0 ? 2 : avg < 33.0 ? 4 : 8);
-            M.grid = h->persistent ? std::max(1, std::min(M.ntiles, h->sm_count * per_sm)) : std::max(1, M.ntiles);
-            h->max_grid = std::max(h->max_grid, M.grid);
+                      : small ? (avg >= 16.0 ? 8 : avg >= 6.0 ? 4 : 2) : (avg < 48.0 ? 1 : avg < 96.0 ? 4 : 8);
         }
     }
     // vectors: capacity = local rows + the largest halo feeding a matrix on that level's column space
@@ -2905,17 +2297,6 @@ int amg_finalize(amg_t *h)
     TRY(dalloc(&h->ctl, 1));
     CK(cudaMallocHost((void **)&h->ctl_h, sizeof(PcgCtl)));
     std::memset(h->ctl_h, 0, sizeof(PcgCtl));
-    if (!container && h->l2_persist > 0) {
-        int maxp = 0, maxw = 0;
-        CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device));
-        CK(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, h->device));
-        if (maxp > 0 && maxw > 0) {
-            const size_t want = h->l2_persist_mb > 0 ? std::min((size_t)maxp, (size_t)h->l2_persist_mb << 20) : (size_t)maxp;
-            CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
-            h->win_max = (size_t)maxw;
-        }
-    }
-    if (!container && h->fused) TRY(build_fused(h));
     if (!container) TRY(build_tail(h));
     h->finalized = true;
     CK(cudaDeviceSynchronize());
@@ -3361,10 +2742,9 @@ int amg_matrix_bytes(amg_t *h, int level, int which, int64_t *stored, int64_t *v
 static int layout_of(const amg_t *h, const DevMat &M)
 {
     // same precedence as launch_spmv
-    return M.ntiles == 0           ? AMG_LAYOUT_EMPTY
+    return M.nrows == 0            ? AMG_LAYOUT_EMPTY
               : M.dcls                ? AMG_LAYOUT_DICT
               : (M.uval && h->symm)   ? AMG_LAYOUT_SYMD
-              : (M.spv && h->split)    ? AMG_LAYOUT_SPLIT
               : (M.sv_s && h->sells)   ? AMG_LAYOUT_SELL_SORTED
               : (M.uval_s && h->sellu) ? AMG_LAYOUT_SELL_UNIFORM
               : M.sbeg                ? (M.scol ? AMG_LAYOUT_SELL : AMG_LAYOUT_SELL_PAT)
@@ -3386,8 +2766,6 @@ int amg_get_stats(amg_t *h, amg_stats_t *out)
     out->n_levels = (int)h->lv.size();
     out->tail_level = h->tail_level;
     out->cluster = h->cluster;
-    for (size_t k = 0; k < h->lv.size() && k < 31; ++k)
-        if (h->lv[k].fz.on && h->fused) out->fused_levels |= 1 << k;
     return AMG_OK;
 }
 

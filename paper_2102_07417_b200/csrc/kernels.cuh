@@ -66,20 +66,10 @@ struct PcgCtl {
     double part_all[MAX_RANKS];
 };
 
-struct TileDesc {
-    int32_t r0, r1;  // rows [r0, r1)
-    int32_t k0, k1;  // stored entries [k0, k1)
-};
-
 struct SpmvArgs {
     const int32_t *off;
     const int32_t *col;
     const double *val;
-    const TileDesc *tiles;
-    int ntiles;
-    int tile_nnz;   // staging capacity (entries)
-    int tile_rows;  // staging capacity (rows)
-    int stages;
     const double *x;  // gathered vector
     double *y;        // output
     const double *b;  // epilogue operand (may alias y)
@@ -448,301 +438,6 @@ __device__ __forceinline__ double epilogue(double s, const double *b, int64_t ro
     return s;
 }
 
-struct StageLayout {
-    int vals_bytes, cols_bytes, offs_bytes, stage_bytes;
-};
-
-__host__ __device__ inline StageLayout stage_layout(int tile_nnz, int tile_rows)
-{
-    StageLayout L;
-    L.vals_bytes = ((tile_nnz + 2) * 8 + 15) & ~15;
-    L.cols_bytes = ((tile_nnz + 4) * 4 + 15) & ~15;
-    L.offs_bytes = ((tile_rows + 1 + 4) * 4 + 15) & ~15;
-    L.stage_bytes = L.vals_bytes + L.cols_bytes + L.offs_bytes;
-    return L;
-}
-
-__device__ __forceinline__ void issue_tile(const SpmvArgs &a, const StageLayout &L, char *stage, uint64_t *bar,
-                                           int t)
-{
-    const TileDesc d = a.tiles[t];
-    const int nk = d.k1 - d.k0;
-    if (nk > a.tile_nnz) {  // long row: consumers read it from global memory
-        mbar_arrive_tx(bar, 0);
-        return;
-    }
-    const int va = d.k0 & ~1, ca = d.k0 & ~3, oa = d.r0 & ~3;
-    const unsigned vb = nk ? (unsigned)(((d.k1 - va) * 8 + 15) & ~15) : 0u;
-    const unsigned cb = nk ? (unsigned)(((d.k1 - ca) * 4 + 15) & ~15) : 0u;
-    const unsigned ob = (unsigned)(((d.r1 + 1 - oa) * 4 + 15) & ~15);
-    mbar_arrive_tx(bar, vb + cb + ob);
-    if (vb) bulk_g2s(stage, a.val + va, vb, bar);
-    if (cb) bulk_g2s(stage + L.vals_bytes, a.col + ca, cb, bar);
-    bulk_g2s(stage + L.vals_bytes + L.cols_bytes, a.off + oa, ob, bar);
-}
-
-template <int EPI, int LANES>
-__global__ void __launch_bounds__(TILE_THREADS) spmv_tiles(const SpmvArgs a)
-{
-    extern __shared__ __align__(128) char smem[];
-    __shared__ __align__(8) uint64_t bars[8];
-    __shared__ double red[TILE_THREADS / 32];
-
-    const StageLayout L = stage_layout(a.tile_nnz, a.tile_rows);
-    const int S = a.stages;
-    // Stage the first S tiles: matrix data is static, so this may run before
-    // the predecessor kernel has finished (programmatic dependent launch).
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int s = 0; s < S; ++s) {
-            int t = blockIdx.x + s * gridDim.x;
-            if (t < a.ntiles) issue_tile(a, L, smem + s * L.stage_bytes, &bars[s], t);
-        }
-    }
-    __syncthreads();
-    pdl_launch();
-    pdl_wait();
-    if (!gate_open(a.gate1, a.gate2)) {
-        if (threadIdx.x == 0)  // drain the staged copies before the CTA releases its smem
-            for (int s = 0; s < S; ++s)
-                if ((int)blockIdx.x + s * (int)gridDim.x < a.ntiles) mbar_wait(&bars[s], 0u);
-        return;
-    }
-
-    constexpr int G = TILE_THREADS / LANES;
-    const int grp = threadIdx.x / LANES;
-    const int lane = threadIdx.x % LANES;
-    const unsigned gmask = (LANES == 32) ? 0xffffffffu
-                                         : (((1u << LANES) - 1u) << ((threadIdx.x & 31) / LANES * LANES));
-    double dacc = 0.0;
-    const bool want_dot = a.dotw != nullptr;
-    const bool self_dot = a.dotw == a.y;  // r.r: the partner is the value being written
-
-    int i = 0;
-    for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++i) {
-        const int s = i % S;
-        char *stage = smem + s * L.stage_bytes;
-        mbar_wait(&bars[s], (unsigned)((i / S) & 1));
-        const TileDesc d = a.tiles[t];
-        const int nrows = d.r1 - d.r0;
-        if (d.k1 - d.k0 > a.tile_nnz) {
-            // a single row longer than the staging tile: lane 0 of the CTA
-            // reduces it straight from global memory (same order).
-            if (threadIdx.x == 0) {
-                const int lo = a.off[d.r0], hi = a.off[d.r0 + 1];
-                auto P = [&](int k) -> double { return prod(a.val[k], __ldg(a.x + a.col[k])); };
-                double sum = add(P(lo), pairwise_sum(P, lo + 1, hi - lo - 1));
-                double yv = epilogue<EPI>(sum, a.b, d.r0, a.omega);
-                a.y[d.r0] = yv;
-                if (want_dot) dacc = fma(yv, a.dotw[d.r0], dacc);
-            }
-        } else {
-            double *vs = reinterpret_cast<double *>(stage);
-            const int32_t *cs = reinterpret_cast<const int32_t *>(stage + L.vals_bytes);
-            const int32_t *os = reinterpret_cast<const int32_t *>(stage + L.vals_bytes + L.cols_bytes);
-            const int vdelta = d.k0 & ~1, cdelta = d.k0 & ~3, odelta = d.r0 & ~3;
-            // epilogue operands of this group's first row, fetched with the gathers
-            double bpre = 0.0, wpre = 0.0;
-            if (lane == 0 && grp < nrows) {
-                if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bpre = a.b[d.r0 + grp];
-                if (want_dot && !self_dot) wpre = a.dotw[d.r0 + grp];
-            }
-            // phase 1: every product of the tile, flat over the threads so all
-            // x gathers of the tile are in flight together; p_k = a_k * x[c_k]
-            // overwrites a_k in place (rounded product, no FMA contraction).
-            {
-                const int nk = d.k1 - d.k0;
-                double *pv = vs + (d.k0 - vdelta);
-                const int32_t *pc = cs + (d.k0 - cdelta);
-#pragma unroll 8
-                for (int k = threadIdx.x; k < nk; k += TILE_THREADS) pv[k] = prod(pv[k], __ldg(a.x + pc[k]));
-            }
-            __syncthreads();
-            // phase 2: row sums in the reference order from shared memory
-            for (int rr = grp; rr < nrows; rr += G) {
-                const int row = d.r0 + rr;
-                const int lo = os[row - odelta], hi = os[row + 1 - odelta];
-                double sum = row_sum_staged<LANES>(vs, vdelta, lo, hi, lane, gmask);
-                if (lane == 0) {
-                    const bool first = (rr == grp);
-                    double yv;
-                    if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) {
-                        const double bv = first ? bpre : a.b[row];
-                        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
-                        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
-                        else yv = add(bv, sum);
-                    } else {
-                        yv = epilogue<EPI>(sum, a.b, row, a.omega);
-                    }
-                    a.y[row] = yv;
-                    if (want_dot) dacc = fma(yv, self_dot ? yv : (first ? wpre : a.dotw[row]), dacc);
-                }
-            }
-        }
-        __syncthreads();  // every thread is done with stage s
-        if (threadIdx.x == 0) {
-            int tn = t + S * gridDim.x;
-            if (tn < a.ntiles) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue_tile(a, L, stage, &bars[s], tn);
-            }
-        }
-    }
-    if (want_dot || a.fin != FIN_NONE) {
-        double v = block_sum<TILE_THREADS>(dacc, red);
-        grid_finalize<TILE_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
-    }
-}
-
-// ---------------------------------------------------------------- SpMV, warp-specialized
-
-// Warp-specialized tile SpMV: warp WS_CONSUMERS (the producer) streams tiles
-// into a STAGES-deep smem ring with cp.async.bulk (evict-first L2 policy) and
-// never touches dynamic data, so it runs ahead of griddepcontrol.wait; each
-// consumer warp owns a contiguous slice of every tile's rows: it computes the
-// products of its slice (all x gathers of the slice in flight), then sums its
-// rows in the reference order -- warp-local work, no CTA barriers in the
-// loop; stages are recycled through full/empty mbarriers.
-constexpr int WS_CONSUMERS = 8;
-constexpr int WS_THREADS = 32 * (WS_CONSUMERS + 1);
-
-__device__ __forceinline__ void ws_issue(const SpmvArgs &a, const StageLayout &L, char *stage, uint64_t *bar, int t,
-                                         uint64_t pol)
-{
-    const TileDesc d = a.tiles[t];
-    const int nk = d.k1 - d.k0;
-    if (nk > a.tile_nnz) {
-        mbar_arrive_tx(bar, 0);
-        return;
-    }
-    const int va = d.k0 & ~1, ca = d.k0 & ~3, oa = d.r0 & ~3;
-    const unsigned vb = nk ? (unsigned)(((d.k1 - va) * 8 + 15) & ~15) : 0u;
-    const unsigned cb = nk ? (unsigned)(((d.k1 - ca) * 4 + 15) & ~15) : 0u;
-    const unsigned ob = (unsigned)(((d.r1 + 1 - oa) * 4 + 15) & ~15);
-    mbar_arrive_tx(bar, vb + cb + ob);
-    if (vb) bulk_g2s_hint(stage, a.val + va, vb, bar, pol);
-    if (cb) bulk_g2s_hint(stage + L.vals_bytes, a.col + ca, cb, bar, pol);
-    bulk_g2s_hint(stage + L.vals_bytes + L.cols_bytes, a.off + oa, ob, bar, pol);
-}
-
-template <int EPI, int LANES>
-__global__ void __launch_bounds__(WS_THREADS) spmv_ws(const SpmvArgs a)
-{
-    extern __shared__ __align__(128) char smem[];
-    __shared__ __align__(8) uint64_t full[8];
-    __shared__ __align__(8) uint64_t empty[8];
-    __shared__ double red[WS_THREADS / 32];
-
-    const StageLayout L = stage_layout(a.tile_nnz, a.tile_rows);
-    const int S = a.stages;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool producer = (warp == WS_CONSUMERS);
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], WS_CONSUMERS);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const int my_tiles = (a.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-    const uint64_t pol = policy_evict_first();
-    int issued = 0;
-    if (producer && lane == 0) {  // static data: stage the first S tiles before the dependency wait
-        for (; issued < S && issued < my_tiles; ++issued)
-            ws_issue(a, L, smem + issued * L.stage_bytes, &full[issued], blockIdx.x + issued * gridDim.x, pol);
-    }
-    pdl_launch();
-    pdl_wait();
-    const bool open = gate_open(a.gate1, a.gate2);
-    double dacc = 0.0;
-    const bool want_dot = a.dotw != nullptr;
-    const bool self_dot = a.dotw == a.y;
-    if (producer) {
-        if (lane == 0) {
-            if (!open) {  // drain what is in flight before the CTA releases its smem
-                for (int i = 0; i < issued; ++i) mbar_wait(&full[i], 0u);
-            } else {
-                for (int i = issued; i < my_tiles; ++i) {
-                    const int s = i % S;
-                    mbar_wait(&empty[s], (unsigned)(((i / S) - 1) & 1));
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    ws_issue(a, L, smem + s * L.stage_bytes, &full[s], blockIdx.x + i * gridDim.x, pol);
-                }
-            }
-        }
-    } else if (open) {
-        constexpr int G = 32 / LANES;
-        const int grp = lane / LANES;
-        const int gl = lane % LANES;
-        const unsigned gmask = (LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << (grp * LANES));
-        for (int i = 0; i < my_tiles; ++i) {
-            const int t = blockIdx.x + i * gridDim.x;
-            const int s = i % S;
-            char *stage = smem + s * L.stage_bytes;
-            const TileDesc d = a.tiles[t];
-            const int nrows = d.r1 - d.r0;
-            // this warp's row slice of the tile
-            const int w0 = d.r0 + (int)(((long long)nrows * warp) / WS_CONSUMERS);
-            const int w1 = d.r0 + (int)(((long long)nrows * (warp + 1)) / WS_CONSUMERS);
-            double bpre = 0.0, wpre = 0.0;
-            if (gl == 0 && w0 + grp < w1) {
-                if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bpre = a.b[w0 + grp];
-                if (want_dot && !self_dot) wpre = a.dotw[w0 + grp];
-            }
-            mbar_wait(&full[s], (unsigned)((i / S) & 1));
-            if (d.k1 - d.k0 > a.tile_nnz) {
-                if (warp == 0 && lane == 0) {
-                    const int lo = a.off[d.r0], hi = a.off[d.r0 + 1];
-                    auto P = [&](int k) -> double { return prod(a.val[k], __ldg(a.x + a.col[k])); };
-                    double sum = add(P(lo), pairwise_sum(P, lo + 1, hi - lo - 1));
-                    double yv = epilogue<EPI>(sum, a.b, d.r0, a.omega);
-                    a.y[d.r0] = yv;
-                    if (want_dot) dacc = fma(yv, a.dotw[d.r0], dacc);
-                }
-            } else if (w0 < w1) {
-                double *vs = reinterpret_cast<double *>(stage);
-                const int32_t *cs = reinterpret_cast<const int32_t *>(stage + L.vals_bytes);
-                const int32_t *os = reinterpret_cast<const int32_t *>(stage + L.vals_bytes + L.cols_bytes);
-                const int vdelta = d.k0 & ~1, cdelta = d.k0 & ~3, odelta = d.r0 & ~3;
-                const int klo = os[w0 - odelta], khi = os[w1 - odelta];
-                {
-                    double *pv = vs - vdelta;
-                    const int32_t *pc = cs - cdelta;
-#pragma unroll 8
-                    for (int k = klo + lane; k < khi; k += 32) pv[k] = prod(pv[k], __ldg(a.x + pc[k]));
-                }
-                __syncwarp();
-                for (int row = w0 + grp; row < w1; row += G) {
-                    const int lo = os[row - odelta], hi = os[row + 1 - odelta];
-                    double sum = row_sum_staged<LANES>(vs, vdelta, lo, hi, gl, gmask);
-                    if (gl == 0) {
-                        const bool first = (row == w0 + grp);
-                        double yv;
-                        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) {
-                            const double bv = first ? bpre : a.b[row];
-                            if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
-                            else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
-                            else yv = add(bv, sum);
-                        } else {
-                            yv = epilogue<EPI>(sum, a.b, row, a.omega);
-                        }
-                        a.y[row] = yv;
-                        if (want_dot) dacc = fma(yv, self_dot ? yv : (first ? wpre : a.dotw[row]), dacc);
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-        }
-    }
-    if ((want_dot || a.fin != FIN_NONE) && open) {
-        double v = block_sum<WS_THREADS>(dacc, red);
-        grid_finalize<WS_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
-    }
-}
-
 // ---------------------------------------------------------------- SpMV, direct
 
 // Register-only CSR SpMV: a group of LANES lanes owns a row; every load of
@@ -1082,249 +777,6 @@ __global__ void __launch_bounds__(DIRECT_THREADS) spmv_leafsum(const SpmvArgs a,
     if (want_dot || a.fin != FIN_NONE) {
         double v = block_sum<DIRECT_THREADS>(dacc, red);
         grid_finalize<DIRECT_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
-    }
-}
-
-// ---------------------------------------------------------------- SpMV, long rows: one warp per row
-
-// Rows of hundreds to thousands of entries (the Galerkin coarse operators of
-// the elasticity hierarchy: 293..951 entries per row on average).  One warp
-// per row: the row's products are formed with coalesced 32-wide loads into a
-// per-warp shared buffer (whole pairwise leaves at a time, up to LR_BUF
-// entries), then every (leaf, accumulator) pair is one lane: numpy's 8
-// strided accumulators of a leaf are summed in order by 8 lanes, combined
-// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) with an xor-shuffle butterfly inside
-// the 8-lane group, the leaf's tail added in order, and the leaf sums folded
-// in numpy's recursive tree (leaf_tree_combine) -- bit-identical to
-// np.add.reduceat, in one kernel without a leaf-sum round trip through HBM.
-constexpr int LR_WARPS = 8;
-constexpr int LR_BUF = 1024;     // products staged per warp (8 KB)
-constexpr int LR_MAXLEAF = 96;   // rows up to ~6000 entries
-
-template <int EPI>
-__global__ void __launch_bounds__(LR_WARPS * 32, 2) spmv_lrow(const SpmvArgs a, int nrows)
-{
-    extern __shared__ __align__(16) double lr_buf[];  // LR_WARPS * LR_BUF
-    __shared__ int2 s_leaf[LR_WARPS][LR_MAXLEAF];
-    __shared__ double s_lsum[LR_WARPS][LR_MAXLEAF];
-    __shared__ double red[LR_WARPS];
-    pdl_launch();
-    pdl_wait();
-    if (!gate_open(a.gate1, a.gate2)) return;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double *buf = lr_buf + warp * LR_BUF;
-    const bool want_dot = a.dotw != nullptr;
-    const bool self_dot = a.dotw == a.y;
-    const double *__restrict__ x = a.x;
-    double dacc = 0.0;
-    for (int row = blockIdx.x * LR_WARPS + warp; row < nrows; row += gridDim.x * LR_WARPS) {
-        const int lo = __ldg(a.off + row), n = __ldg(a.off + row + 1) - lo;
-        double sum = 0.0;
-        if (n > 0) {
-            const int m = n - 1, s0 = lo + 1;  // products after p0
-            double tree = 0.0;
-            if (m < 8) {
-                if (lane == 0)
-                    for (int i = 0; i < m; ++i) tree = add(tree, prod(__ldg(a.val + s0 + i), __ldg(x + __ldg(a.col + s0 + i))));
-            } else {
-                int nleaf = 0;
-                if (lane == 0) {  // pre-order leaves (left to right), as numpy's recursion visits them
-                    int st_s[24], st_n[24], sp = 0;
-                    st_s[sp] = 0;
-                    st_n[sp++] = m;
-                    while (sp > 0) {
-                        --sp;
-                        int b = st_s[sp], c = st_n[sp];
-                        while (c > 128) {
-                            const int c2 = pairwise_split(c);
-                            st_s[sp] = b + c2;
-                            st_n[sp++] = c - c2;
-                            c = c2;
-                        }
-                        if (nleaf < LR_MAXLEAF) s_leaf[warp][nleaf] = make_int2(b, c);
-                        ++nleaf;
-                    }
-                }
-                nleaf = __shfl_sync(0xffffffffu, nleaf, 0);
-                __syncwarp();
-                if (nleaf > LR_MAXLEAF) __trap();  // host checks the longest row (build: lrow only if it fits)
-                for (int L0 = 0; L0 < nleaf;) {
-                    const int b0 = s_leaf[warp][L0].x;
-                    int L1 = L0 + 1;
-                    while (L1 < nleaf && s_leaf[warp][L1].x + s_leaf[warp][L1].y - b0 <= LR_BUF) ++L1;
-                    const int e_end = s_leaf[warp][L1 - 1].x + s_leaf[warp][L1 - 1].y;
-#pragma unroll 4
-                    for (int e = b0 + lane; e < e_end; e += 32)
-                        buf[e - b0] = prod(__ldg(a.val + s0 + e), __ldg(x + __ldg(a.col + s0 + e)));
-                    __syncwarp();
-                    for (int L = L0 + (lane >> 3); L - (lane >> 3) < L1; L += 4) {
-                        const bool act = L < L1;
-                        const int j = lane & 7;
-                        int st = 0, len = 0;
-                        if (act) {
-                            st = s_leaf[warp][L].x - b0;
-                            len = s_leaf[warp][L].y;
-                        }
-                        const int main = len - len % 8;
-                        double acc = 0.0;
-                        if (act) {
-                            acc = buf[st + j];
-                            for (int k = j + 8; k < main; k += 8) acc = add(acc, buf[st + k]);
-                        }
-                        double t = add(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
-                        t = add(t, __shfl_xor_sync(0xffffffffu, t, 2));
-                        t = add(t, __shfl_xor_sync(0xffffffffu, t, 4));
-                        if (act && j == 0) {
-                            for (int k = main; k < len; ++k) t = add(t, buf[st + k]);
-                            s_lsum[warp][L] = t;
-                        }
-                    }
-                    __syncwarp();
-                    L0 = L1;
-                }
-                if (lane == 0) tree = (nleaf == 1) ? s_lsum[warp][0] : leaf_tree_combine(s_lsum[warp], m);
-                __syncwarp();
-            }
-            if (lane == 0) sum = add(prod(__ldg(a.val + lo), __ldg(x + __ldg(a.col + lo))), tree);
-        }
-        if (lane == 0) {
-            double bv = 0.0;
-            if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
-            double yv;
-            if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
-            else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
-            else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
-            else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
-            else yv = sum;
-            a.y[row] = yv;
-            if (want_dot) dacc = fma(yv, self_dot ? yv : a.dotw[row], dacc);
-        }
-    }
-    if (want_dot || a.fin != FIN_NONE) {
-        double v = block_sum<LR_WARPS * 32>(dacc, red);
-        grid_finalize<LR_WARPS * 32>(v, a.partials, a.ticket, a.fin, a.ctl);
-    }
-}
-
-// ---------------------------------------------------------------- SpMV, warp tiles
-
-// Warp-tile SpMV: rows are cut into small tiles (<= wt_nnz entries, <= 32
-// rows); every warp streams its own tiles into a private 2-slot smem ring
-// with cp.async.bulk issued by its lane 0 (per-warp mbarriers), so the matrix
-// never passes through L1 and a warp never waits on another warp.  Per tile:
-// all products of the tile are formed flat over the 32 lanes (every x gather
-// of the tile in flight at once), then rows are summed in the reference
-// order by LANES-wide groups.  The first two tiles of each warp are static
-// data and are staged before griddepcontrol.wait.
-constexpr int WT_WARPS = 8;
-constexpr int WT_THREADS = 32 * WT_WARPS;
-constexpr int WT_ROWS = 32;
-
-template <int EPI, int LANES>
-__global__ void __launch_bounds__(WT_THREADS, 4) spmv_wt(const SpmvArgs a)
-{
-    extern __shared__ __align__(128) char smem[];
-    __shared__ __align__(8) uint64_t full[WT_WARPS][2];
-    __shared__ TileDesc sdesc[WT_WARPS][2];  // descriptor of the tile in each slot (written at issue)
-    __shared__ double red[WT_THREADS / 32];
-    const StageLayout L = stage_layout(a.tile_nnz, WT_ROWS);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    char *wbuf = smem + (size_t)warp * 2 * L.stage_bytes;
-    const int wg = blockIdx.x * WT_WARPS + warp;
-    const int nw = gridDim.x * WT_WARPS;
-    const int my_tiles = (a.ntiles > wg) ? (a.ntiles - wg + nw - 1) / nw : 0;
-    const uint64_t pol = policy_evict_first();
-    if (lane == 0) {
-        mbar_init(&full[warp][0], 1);
-        mbar_init(&full[warp][1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int i = 0; i < 2 && i < my_tiles; ++i) {
-            sdesc[warp][i] = a.tiles[wg + i * nw];
-            ws_issue(a, L, wbuf + i * L.stage_bytes, &full[warp][i], wg + i * nw, pol);
-        }
-    }
-    __syncwarp();
-    pdl_launch();
-    pdl_wait();
-    const bool open = gate_open(a.gate1, a.gate2);
-    if (!open) {
-        if (lane == 0)
-            for (int i = 0; i < 2 && i < my_tiles; ++i) mbar_wait(&full[warp][i], 0u);
-        return;  // uniform over the grid: no reduction follows
-    }
-    constexpr int G = 32 / LANES;
-    const int grp = lane / LANES;
-    const int gl = lane % LANES;
-    const unsigned gmask = (LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << (grp * LANES));
-    const bool want_dot = a.dotw != nullptr;
-    const bool self_dot = a.dotw == a.y;
-    double dacc = 0.0;
-    for (int i = 0; i < my_tiles; ++i) {
-        const int s = i & 1;
-        char *stage = wbuf + s * L.stage_bytes;
-        const TileDesc d = sdesc[warp][s];
-        const int nrows = d.r1 - d.r0;
-        // epilogue operands of this group's first row, in flight with the tile
-        double bpre = 0.0, wpre = 0.0;
-        if (gl == 0 && grp < nrows) {
-            if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bpre = a.b[d.r0 + grp];
-            if (want_dot && !self_dot) wpre = a.dotw[d.r0 + grp];
-        }
-        mbar_wait(&full[warp][s], (unsigned)((i >> 1) & 1));
-        if (d.k1 - d.k0 > a.tile_nnz) {  // one row longer than the tile capacity: straight from global
-            double sum = 0.0;
-            if (lane == 0) {
-                const int lo = a.off[d.r0], hi = a.off[d.r0 + 1];
-                auto P = [&](int k) -> double { return prod(a.val[k], __ldg(a.x + a.col[k])); };
-                sum = add(P(lo), pairwise_sum(P, lo + 1, hi - lo - 1));
-                double yv = epilogue<EPI>(sum, a.b, d.r0, a.omega);
-                a.y[d.r0] = yv;
-                if (want_dot) dacc = fma(yv, a.dotw[d.r0], dacc);
-            }
-        } else {
-            double *vs = reinterpret_cast<double *>(stage);
-            const int32_t *cs = reinterpret_cast<const int32_t *>(stage + L.vals_bytes);
-            const int32_t *os = reinterpret_cast<const int32_t *>(stage + L.vals_bytes + L.cols_bytes);
-            const int vdelta = d.k0 & ~1, cdelta = d.k0 & ~3, odelta = d.r0 & ~3;
-            {
-                const int nk = d.k1 - d.k0;
-                double *pv = vs + (d.k0 - vdelta);
-                const int32_t *pc = cs + (d.k0 - cdelta);
-#pragma unroll 8
-                for (int k = lane; k < nk; k += 32) pv[k] = prod(pv[k], __ldg(a.x + pc[k]));
-            }
-            __syncwarp();
-            for (int rr = grp; rr < nrows; rr += G) {
-                const int row = d.r0 + rr;
-                const int lo = os[row - odelta], hi = os[row + 1 - odelta];
-                double sum = row_sum_staged<LANES>(vs, vdelta, lo, hi, gl, gmask);
-                if (gl == 0) {
-                    const bool first = (rr == grp);
-                    double yv;
-                    if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) {
-                        const double bv = first ? bpre : a.b[row];
-                        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
-                        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
-                        else yv = add(bv, sum);
-                    } else {
-                        yv = epilogue<EPI>(sum, a.b, row, a.omega);
-                    }
-                    a.y[row] = yv;
-                    if (want_dot) dacc = fma(yv, self_dot ? yv : (first ? wpre : a.dotw[row]), dacc);
-                }
-            }
-        }
-        __syncwarp();
-        if (lane == 0 && i + 2 < my_tiles) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            sdesc[warp][s] = a.tiles[wg + (i + 2) * nw];
-            ws_issue(a, L, stage, &full[warp][s], wg + (i + 2) * nw, pol);
-        }
-        __syncwarp();
-    }
-    if (want_dot || a.fin != FIN_NONE) {
-        double v = block_sum<WT_THREADS>(dacc, red);
-        grid_finalize<WT_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
     }
 }
 
@@ -2237,597 +1689,6 @@ __global__ void __launch_bounds__(256) l2_prefetch(const PrefetchRange *__restri
         const PrefetchRange q = r[k];
         for (long long off = t * 128; off < q.bytes; off += nt * 128)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(q.p + off));
-    }
-}
-
-// ---------------------------------------------------------------- SpMV, short / long row split
-
-// Fine-level ragged matrices (the FSAI transpose G^T_0: 1..46 entries, 90% of
-// rows <= 16): rows of <= 16 entries run as uniform SELL-32 slices of width
-// 16 with their columns and lengths fetched one row ahead and padding slots
-// never loaded (spmv_split_short, rows in their natural order, so lanes stay
-// on neighbouring rows); the remaining long rows (len byte 255) are skipped
-// there and summed by spmv_split_long over a row list.  Both write disjoint
-// rows of y with the same epilogue; a dot / finalize spans both kernels
-// (short: per-CTA partials; long: folds them with its own).
-struct SplitArgs {
-    const double *val;      // short part: SELL-32, width 16
-    const int32_t *col;
-    const uint8_t *len;     // 255: long row
-    const int32_t *lrows;   // long rows (ascending)
-    int nlong;
-    int short_grid;         // partials written by the short kernel
-};
-
-template <int EPI>
-__global__ void __launch_bounds__(VEC_SPMV_THREADS, 3) spmv_split_short(const SpmvArgs a, const SplitArgs q, int nrows)
-{
-    __shared__ double red[VEC_SPMV_THREADS / 32];
-    constexpr int FL = 16;
-    pdl_launch();
-    pdl_wait();
-    if (!gate_open(a.gate1, a.gate2)) return;
-    const int nthreads = gridDim.x * VEC_SPMV_THREADS;
-    const bool want_dot = a.dotw != nullptr;
-    const bool self_dot = a.dotw == a.y;
-    const double *__restrict__ x = a.x;
-    double dacc = 0.0;
-    int row = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x;
-    int c[FL];
-    int len = 0;
-    auto fetch = [&](int r) {
-        const int base = (r >> 5) * (32 * FL) + (r & 31);
-        len = __ldg(q.len + r);
-        const int l = len == 255 ? 0 : len;
-#pragma unroll
-        for (int k = 0; k < FL; ++k) c[k] = (k < l) ? __ldg(q.col + base + 32 * k) : r;
-    };
-    if (row < nrows) fetch(row);
-    for (; row < nrows; row += nthreads) {
-        const int base = (row >> 5) * (32 * FL) + (row & 31);
-        const int clen = len;
-        const int l = clen == 255 ? 0 : clen;
-        double p[FL];
-#pragma unroll
-        for (int k = 0; k < FL; ++k) p[k] = (k < l) ? prod(__ldg(q.val + base + 32 * k), __ldg(x + c[k])) : 0.0;
-        if (row + nthreads < nrows) fetch(row + nthreads);
-        if (clen == 255) continue;  // long row: spmv_split_long
-        double bv = 0.0, wv = 0.0;
-        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
-        if (want_dot && !self_dot) wv = a.dotw[row];
-        const double sum = ref_sum_fixed<FL>(p, l);
-        double yv;
-        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
-        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
-        else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
-        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
-        else yv = sum;
-        a.y[row] = yv;
-        if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
-    }
-    if (want_dot || a.fin != FIN_NONE) {
-        const double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
-        if (threadIdx.x == 0) a.partials[blockIdx.x] = v;
-    }
-}
-
-template <int EPI>
-__global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_split_long(const SpmvArgs a, const SplitArgs q)
-{
-    __shared__ double red[VEC_SPMV_THREADS / 32];
-    pdl_launch();
-    pdl_wait();
-    if (!gate_open(a.gate1, a.gate2)) return;
-    const bool want_dot = a.dotw != nullptr;
-    const bool self_dot = a.dotw == a.y;
-    const double *__restrict__ x = a.x;
-    double dacc = 0.0;
-    for (int t = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x; t < q.nlong; t += gridDim.x * VEC_SPMV_THREADS) {
-        const int row = __ldg(q.lrows + t);
-        const int lo = __ldg(a.off + row), hi = __ldg(a.off + row + 1);
-        auto P = [&](int k) -> double { return prod(__ldg(a.val + lo + k), __ldg(x + __ldg(a.col + lo + k))); };
-        const double sum = ref_row_sum<true>(P, hi - lo);
-        double bv = 0.0, wv = 0.0;
-        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
-        if (want_dot && !self_dot) wv = a.dotw[row];
-        double yv;
-        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
-        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
-        else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
-        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
-        else yv = sum;
-        a.y[row] = yv;
-        if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
-    }
-    if (want_dot || a.fin != FIN_NONE) {
-        const double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
-        grid_finalize_pair<VEC_SPMV_THREADS>(v, a.partials, (want_dot || a.fin != FIN_NONE) ? q.short_grid : 0,
-                                             a.ticket, a.fin, a.ctl);
-    }
-}
-
-// ---------------------------------------------------------------- FSAI smoother step, G and G^T fused
-
-// x = w * G^T (G y)  (EPI_SETW)  or  x = x + w * G^T (G y)  (EPI_AXPYW)
-// (amgkit/smoothers.py:45-50, 170-172) in ONE persistent kernel.  Work unit =
-// 32 rows = one warp, no CTA barriers: warp w of the grid takes tickets
-// w, w + NW, w + 2 NW, ...  Ticket u: phase A computes t = G y for unit u (G
-// in uniform-width SELL-32, lane = row) and counts the unit into its 256-row
-// block's completion counter (release); phase B computes the G^T rows of
-// unit u - lag once every block holding a G row they read (up to `reach`
-// rows ahead) is complete (acquire; a per-warp watermark skips blocks
-// already seen complete).  G^T is not stored as values: entry m of G^T row i
-// is the position q of G(j, i) in G's SELL array -> value gval[q], column
-// j = (q / (32 W)) * 32 + q % 32, both read from L2 where phase A left them,
-// as it left t.  HBM traffic per step: G once (12 B/entry) + 4 B/entry of
-// G^T positions + the y / x vectors (vs. G and G^T as two 12 B/entry
-// matrices plus t written and re-read).  Row sums are the reference's
-// (p0 + numpy pairwise; G^T rows in ascending column order), so x is
-// bit-identical to the two-kernel sequence.  Progress: a ticket only waits
-// on smaller tickets; the grid is at most one resident wave (occupancy), so
-// every ticket's warp is running.  Dot partials are per unit (fixed),
-// folded in unit order by the last CTA: deterministic.
-struct FusedArgs {
-    const double *gval;     // G, SELL-32 uniform width W: entry k of row j at (j/32)*32W + 32k + j%32
-    const int32_t *gcol;
-    const uint8_t *glen;    // G row lengths (<= W)
-    const int32_t *tstart;  // G^T rows: CSR starts into tq
-    const int32_t *tq;      // positions of the G^T entries in gval
-    const double *y;
-    double *t;
-    double *x;
-    double omega;
-    int nrows, W, nunits, nblk, lag, reach;
-    unsigned *bcnt;         // per 256-row block: completed units, cumulative over launches
-    unsigned *ctr;          // [1] CTAs done, [2] generation
-    double *upart;          // per-unit dot partials
-    const double *dotw;
-    int fin;
-    PcgCtl *ctl;
-    const int *gate1;
-    const int *gate2;
-};
-
-constexpr int FUSED_THREADS = 256;
-
-__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned *p)
-{
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void red_release_gpu_add(unsigned *p, unsigned v)
-{
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-template <int EPI>
-__global__ void __launch_bounds__(FUSED_THREADS, 4) fsai_fused(const FusedArgs a)
-{
-    __shared__ int s_last;
-    __shared__ double red[FUSED_THREADS / 32];
-    pdl_launch();
-    pdl_wait();
-    if (!gate_open(a.gate1, a.gate2)) return;
-    const unsigned gen = *(volatile unsigned *)(a.ctr + 2) + 1u;
-    const bool want_dot = a.dotw != nullptr;
-    const bool self_dot = a.dotw == a.x;
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int nw = gridDim.x * (FUSED_THREADS / 32);
-    const int W32 = 32 * a.W;
-    const int total = a.nunits + a.lag;
-    int ready = -1;  // blocks [0, ready] seen complete by this warp
-    for (int u = blockIdx.x * (FUSED_THREADS / 32) + (tid >> 5); u < total; u += nw) {
-        if (u < a.nunits) {  // phase A: t = G y, rows of unit u
-            const int row = u * 32 + lane;
-            if (row < a.nrows) {
-                const int len = __ldg(a.glen + row);
-                const int sb = u * W32 + lane;
-                const double *__restrict__ y = a.y;
-                auto P = [&](int k) -> double {
-                    return prod(__ldg(a.gval + sb + 32 * k), __ldg(y + __ldg(a.gcol + sb + 32 * k)));
-                };
-                a.t[row] = ref_row_sum<false>(P, len);
-            }
-            __syncwarp();
-            if (lane == 0) red_release_gpu_add(a.bcnt + (u >> 3), 1u);
-        }
-        const int ub = u - a.lag;
-        if (ub >= 0) {  // phase B: x = EPI(w * G^T t), rows of unit ub
-            const int need = min(a.nblk - 1, (ub * 32 + 31 + a.reach) >> 8);
-            while (ready < need) {
-                const int b = ready + 1 + lane;
-                if (b <= need) {
-                    const unsigned full = (b == a.nblk - 1) ? (unsigned)(a.nunits - 8 * b) : 8u;
-                    while (ld_acquire_gpu_u32(a.bcnt + b) < full * gen) __nanosleep(32);
-                }
-                __syncwarp();
-                ready = min(need, ready + 32);
-            }
-            const int row = ub * 32 + lane;
-            double dv = 0.0;
-            if (row < a.nrows) {
-                const int ts = __ldg(a.tstart + row);
-                const int len = __ldg(a.tstart + row + 1) - ts;
-                const double *tt = a.t;
-                auto P = [&](int m) -> double {
-                    const int q = __ldg(a.tq + ts + m);
-                    const int j = (q / W32) * 32 + (q & 31);
-                    return prod(__ldg(a.gval + q), __ldcg(tt + j));
-                };
-                const double sum = ref_row_sum<false>(P, len);
-                double yv;
-                if constexpr (EPI == EPI_AXPYW) yv = add(a.x[row], __dmul_rn(a.omega, sum));
-                else yv = __dmul_rn(a.omega, sum);
-                a.x[row] = yv;
-                if (want_dot) dv = yv * (self_dot ? yv : a.dotw[row]);
-            }
-            if (want_dot || a.fin != FIN_NONE) {
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) dv += __shfl_xor_sync(0xffffffffu, dv, o);
-                if (lane == 0) a.upart[ub] = dv;
-            }
-        }
-    }
-    __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        s_last = atomicAdd(a.ctr + 1, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-        __threadfence();
-        if (want_dot || a.fin != FIN_NONE) {
-            double acc = 0.0;
-            for (int i = tid; i < a.nunits; i += FUSED_THREADS) acc += __ldcg(a.upart + i);
-            acc = block_sum<FUSED_THREADS>(acc, red);
-            if (tid == 0) apply_fin(a.fin, acc, a.ctl);
-        }
-        if (tid == 0) {
-            a.ctr[1] = 0u;
-            a.ctr[2] = gen;
-            __threadfence();
-        }
-    }
-}
-
-// ---------------------------------------------------------------- FSAI step, warp-specialised G / G^T
-
-// The same step as fsai_fused with the two halves on DIFFERENT warps, so
-// their dependent load chains overlap instead of adding up: in every CTA,
-// warps [0, WA) stream t = G y over 32-row units (uniform SELL-32 G, next
-// row's columns fetched one unit ahead) and count each unit into its 256-row
-// block's completion counter (release); warps [WA, 8) compute the G^T rows of
-// their units once every block holding a G row they read is complete
-// (acquire).  G^T is stored as 2 bytes per entry: the G offset id (column
-// j = i - rel[id], rel in __constant__) and the position k of G(j, i) in G
-// row j, so its value gval[(j/32)*32W + 32k + j%32] and t_j come from L2,
-// where the G warps left them.  HBM per step: G (12 B/entry) + 2 B/entry +
-// y, x.  Reference order throughout (bit-identical to G then G^T).  Only the
-// G^T warps wait, only on G warps, which never wait; the grid is one
-// resident wave, so every unit's producer is running.  Dot partials per unit.
-__constant__ int32_t c_gt_rel[SYMD_SLOTS][256];
-
-struct FusedWsArgs {
-    const double *gval;
-    const int32_t *gcol;
-    const uint8_t *glen;
-    const int32_t *tstart;   // G^T rows: CSR starts into gt16
-    const uint16_t *gt16;    // (k << 8) | offset id
-    const double *y;
-    double *t;
-    double *x;
-    double omega;
-    int nrows, W, nunits, nblk, reach, slot;
-    unsigned *bcnt;
-    unsigned *ctr;           // [1] CTAs done, [2] generation
-    double *upart;
-    const double *dotw;
-    int fin;
-    PcgCtl *ctl;
-    const int *gate1;
-    const int *gate2;
-};
-
-template <int EPI, int WA>
-__global__ void __launch_bounds__(FUSED_THREADS, 4) fsai_ws(const FusedWsArgs a)
-{
-    __shared__ int s_last;
-    __shared__ double red[FUSED_THREADS / 32];
-    pdl_launch();
-    pdl_wait();
-    if (!gate_open(a.gate1, a.gate2)) return;
-    const unsigned gen = *(volatile unsigned *)(a.ctr + 2) + 1u;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int W32 = 32 * a.W;
-    if (warp < WA) {  // ---- G warps: t = G y
-        const int na = gridDim.x * WA;
-        int u = blockIdx.x * WA + warp;
-        constexpr int FL = 16;
-        int c[FL];
-        int len = 0;
-        auto fetch = [&](int uu) {
-            const int r = uu * 32 + lane;
-            const int base = uu * W32 + lane;
-            len = r < a.nrows ? __ldg(a.glen + r) : 0;
-#pragma unroll
-            for (int k = 0; k < FL; ++k) c[k] = (k < a.W) ? __ldg(a.gcol + base + 32 * k) : 0;
-        };
-        if (u < a.nunits) fetch(u);
-        for (; u < a.nunits; u += na) {
-            const int row = u * 32 + lane;
-            const int base = u * W32 + lane;
-            double p[FL];
-#pragma unroll
-            for (int k = 0; k < FL; ++k) p[k] = (k < a.W) ? prod(__ldg(a.gval + base + 32 * k), __ldg(a.y + c[k])) : 0.0;
-            const int clen = len;
-            if (u + na < a.nunits) fetch(u + na);
-            if (row < a.nrows) a.t[row] = ref_sum_fixed<FL>(p, clen);
-            __syncwarp();
-            if (lane == 0) red_release_gpu_add(a.bcnt + (u >> 3), 1u);
-        }
-    } else {  // ---- G^T warps: x = EPI(w * G^T t)
-        const int nb = gridDim.x * (8 - WA);
-        const bool want_dot = a.dotw != nullptr;
-        const bool self_dot = a.dotw == a.x;
-        const int slot = a.slot;
-        int ready = -1;
-        for (int u = blockIdx.x * (8 - WA) + (warp - WA); u < a.nunits; u += nb) {
-            const int need = min(a.nblk - 1, (u * 32 + 31 + a.reach) >> 8);
-            while (ready < need) {
-                const int b = ready + 1 + lane;
-                if (b <= need) {
-                    const unsigned full = (b == a.nblk - 1) ? (unsigned)(a.nunits - 8 * b) : 8u;
-                    while (ld_acquire_gpu_u32(a.bcnt + b) < full * gen) __nanosleep(32);
-                }
-                __syncwarp();
-                ready = min(need, ready + 32);
-            }
-            const int row = u * 32 + lane;
-            double dv = 0.0;
-            if (row < a.nrows) {
-                const int ts = __ldg(a.tstart + row);
-                const int len = __ldg(a.tstart + row + 1) - ts;
-                const double *tt = a.t;
-                auto P = [&](int m) -> double {
-                    const unsigned e = __ldg(a.gt16 + ts + m);
-                    const int j = row - c_gt_rel[slot][e & 255u];
-                    const int q = (j >> 5) * W32 + 32 * (int)(e >> 8) + (j & 31);
-                    return prod(__ldg(a.gval + q), __ldcg(tt + j));
-                };
-                const double sum = ref_row_sum<false>(P, len);
-                double yv;
-                if constexpr (EPI == EPI_AXPYW) yv = add(a.x[row], __dmul_rn(a.omega, sum));
-                else yv = __dmul_rn(a.omega, sum);
-                a.x[row] = yv;
-                if (want_dot) dv = yv * (self_dot ? yv : a.dotw[row]);
-            }
-            if (want_dot || a.fin != FIN_NONE) {
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) dv += __shfl_xor_sync(0xffffffffu, dv, o);
-                if (lane == 0) a.upart[u] = dv;
-            }
-        }
-    }
-    __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        s_last = atomicAdd(a.ctr + 1, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-        __threadfence();
-        if (a.dotw != nullptr || a.fin != FIN_NONE) {
-            double acc = 0.0;
-            for (int i = tid; i < a.nunits; i += FUSED_THREADS) acc += __ldcg(a.upart + i);
-            acc = block_sum<FUSED_THREADS>(acc, red);
-            if (tid == 0) apply_fin(a.fin, acc, a.ctl);
-        }
-        if (tid == 0) {
-            a.ctr[1] = 0u;
-            a.ctr[2] = gen;
-            __threadfence();
-        }
-    }
-}
-
-// ---------------------------------------------------------------- SpMV, SELL-32 streamed by the bulk-copy engine
-
-// The SELL-32 layout's value (and column) arrays are one contiguous stream, so
-// a persistent CTA (one per SM) can move its share with cp.async.bulk instead
-// of per-lane loads: a producer thread copies chunks of SQ_WARPS consecutive
-// slices (chunk c = slices [c*SQ_WARPS, (c+1)*SQ_WARPS)) into a q.stages-deep
-// shared-memory ring (full / empty mbarriers); consumer warp w sums the rows
-// of slice c*SQ_WARPS + w from shared memory in exactly the spmv_sell order.
-// The matrix stream needs no registers in flight, so each lane issues every x
-// gather of its row (<= SQ_MAXLEN entries) at once; the per-slice metadata
-// (slice offsets, row lengths, pattern ids, b) is fetched one chunk ahead.
-// Chunks are static data: the first stages are copied before
-// griddepcontrol.wait, overlapping the previous kernel.  CTA b owns chunks
-// [q.cta[b], q.cta[b+1]) (entries balanced at upload).
-constexpr int SQ_WARPS = 8;
-constexpr int SQ_THREADS = (SQ_WARPS + 1) * 32;  // + one producer warp
-constexpr int SQ_MAXSTAGES = 4;
-constexpr int SQ_MAXLEN = 33;                     // rows of <= 33 entries: p0 + 4 full rounds
-
-struct SellqArgs {
-    const int32_t *cta;       // CTA b = chunks [cta[b], cta[b+1])
-    int stage_entries;        // ring stage capacity (entries) >= the largest chunk
-    int stages;               // ring depth (<= SQ_MAXSTAGES)
-};
-
-template <int EPI, bool PAT>
-__global__ void __launch_bounds__(SQ_THREADS, 1) spmv_sellq(const SpmvArgs a, const SellArgs sa, const SellqArgs q,
-                                                             int nrows)
-{
-    extern __shared__ __align__(128) unsigned char sq_smem[];
-    __shared__ double red[SQ_THREADS / 32];
-    __shared__ __align__(8) uint64_t full[SQ_MAXSTAGES], empty[SQ_MAXSTAGES];
-    // dynamic smem: [stages: values (8 B/entry) | columns (4 B/entry, !PAT)] [pattern table]
-    constexpr int bpe = PAT ? 8 : 12;
-    const int S = q.stages;
-    auto stage = [&](int st) { return sq_smem + (size_t)st * q.stage_entries * bpe; };
-    int32_t *s_rel = reinterpret_cast<int32_t *>(sq_smem + (size_t)S * q.stage_entries * bpe);
-    int32_t *s_beg = s_rel + (PAT ? ((sa.nrel + 3) & ~3) : 0);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c0 = __ldg(q.cta + blockIdx.x), c1 = __ldg(q.cta + blockIdx.x + 1);
-    const int nch = c1 - c0;
-    const int nslices = (nrows + 31) >> 5;
-    if (threadIdx.x == 0) {
-        for (int st = 0; st < S; ++st) {
-            mbar_init(&full[st], 1);
-            mbar_init(&empty[st], SQ_WARPS);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if constexpr (PAT) {
-        for (int i = threadIdx.x; i < sa.nrel; i += SQ_THREADS) s_rel[i] = sa.rel[i];
-        for (int i = threadIdx.x; i <= sa.npat; i += SQ_THREADS) s_beg[i] = sa.pbeg[i];
-    }
-    __syncthreads();
-    const bool producer = warp == SQ_WARPS && lane == 0;
-    auto chunk_range = [&](int c, int &e0, int &nb) {
-        const int f = c * SQ_WARPS, e = min(f + SQ_WARPS, nslices);
-        e0 = __ldg(sa.sbeg + f);
-        nb = __ldg(sa.sbeg + e) - e0;
-    };
-    auto issue = [&](int i, int e0, int nb) {  // chunk c0 + i -> stage i % S
-        const int st = i % S;
-        unsigned char *sp = stage(st);
-        mbar_arrive_tx(&full[st], (unsigned)nb * (unsigned)bpe);
-        bulk_g2s(sp, sa.sval + e0, (unsigned)nb * 8u, &full[st]);
-        if constexpr (!PAT) bulk_g2s(sp + (size_t)nb * 8, sa.scol + e0, (unsigned)nb * 4u, &full[st]);
-    };
-    const int pre = nch < S ? nch : S;
-    if (producer)  // the matrix is static: stage ahead of the dependency wait
-        for (int i = 0; i < pre; ++i) {
-            int e0, nb;
-            chunk_range(c0 + i, e0, nb);
-            issue(i, e0, nb);
-        }
-    pdl_launch();
-    pdl_wait();
-    if (!gate_open(a.gate1, a.gate2)) {
-        if (producer)
-            for (int i = 0; i < pre; ++i) mbar_wait(&full[i], 0u);  // no copy may outlive the CTA
-        return;
-    }
-    const bool want_dot = a.dotw != nullptr;
-    const bool self_dot = a.dotw == a.y;
-    const double *__restrict__ x = a.x;
-    double dacc = 0.0;
-    if (warp == SQ_WARPS) {
-        if (producer && nch > S) {
-            int e0, nb;
-            chunk_range(c0 + S, e0, nb);
-            for (int i = S; i < nch; ++i) {
-                int ne0 = 0, nnb = 0;
-                if (i + 1 < nch) chunk_range(c0 + i + 1, ne0, nnb);  // next descriptor in flight
-                mbar_wait(&empty[i % S], (unsigned)(((i / S) - 1) & 1));
-                issue(i, e0, nb);
-                e0 = ne0;
-                nb = nnb;
-            }
-        }
-    } else {
-        // per-slice metadata of chunk i, fetched one chunk ahead
-        int m_eoff = 0, m_nent = 0, m_len = 0, m_rb = 0;
-        double m_bv = 0.0, m_wv = 0.0;
-        auto meta = [&](int c, int &eoff, int &nent, int &len, int &pidv, double &bv, double &wv) {
-            const int f = c * SQ_WARPS, e = min(f + SQ_WARPS, nslices);
-            const int sl = f + warp;
-            const int pos = sl * 32 + lane;
-            const int fb = __ldg(sa.sbeg + f);
-            nent = __ldg(sa.sbeg + e) - fb;
-            eoff = (sl < e) ? __ldg(sa.sbeg + sl) - fb : 0;
-            len = 0;
-            pidv = 0;
-            bv = 0.0;
-            wv = 0.0;
-            if (sl < e && pos < nrows) {
-                len = __ldg(sa.len + pos);
-                if constexpr (PAT) pidv = __ldg(sa.pid + pos);
-                if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[pos];
-                if (want_dot && !self_dot) wv = a.dotw[pos];
-            }
-        };
-        if (nch > 0) meta(c0, m_eoff, m_nent, m_len, m_rb, m_bv, m_wv);
-        for (int i = 0; i < nch; ++i) {
-            const int st = i % S;
-            const int sl = (c0 + i) * SQ_WARPS + warp;
-            const int pos = sl * 32 + lane;
-            const int eoff = m_eoff, nent = m_nent, len = m_len;
-            const double bv = m_bv, wv = m_wv;
-            const int rb = PAT ? s_beg[m_rb] : 0;
-            if (i + 1 < nch) meta(c0 + i + 1, m_eoff, m_nent, m_len, m_rb, m_bv, m_wv);
-            mbar_wait(&full[st], (unsigned)((i / S) & 1));
-            if (sl < nslices) {
-                const bool live = pos < nrows;
-                const int row = pos;
-                const double *vb = reinterpret_cast<const double *>(stage(st)) + eoff + lane;
-                const int32_t *cb = PAT ? nullptr
-                                        : reinterpret_cast<const int32_t *>(stage(st) + (size_t)nent * 8) + eoff + lane;
-                // every gather of the row in flight at once
-                double pk[SQ_MAXLEN];
-#pragma unroll
-                for (int k = 0; k < SQ_MAXLEN; ++k) {
-                    if (k < len) {
-                        const int c = PAT ? row + s_rel[rb + k] : cb[32 * k];
-                        pk[k] = __ldg(x + c);
-                    } else {
-                        pk[k] = 0.0;
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < SQ_MAXLEN; ++k)
-                    if (k < len) pk[k] = prod(vb[32 * k], pk[k]);
-                const int n = len - 1;
-                double sum = 0.0;
-                if (n >= 0) {
-                    double res;
-                    if (n < 8) {
-                        res = 0.0;
-#pragma unroll
-                        for (int t = 1; t < 8; ++t)
-                            if (t <= n) res = add(res, pk[t]);
-                    } else {
-                        const int main = n - (n % 8);
-                        double acc[8];
-#pragma unroll
-                        for (int t = 0; t < 8; ++t) acc[t] = pk[1 + t];
-#pragma unroll
-                        for (int i8 = 8; i8 < 32; i8 += 8)
-                            if (i8 < main) {
-#pragma unroll
-                                for (int t = 0; t < 8; ++t) acc[t] = add(acc[t], pk[1 + i8 + t]);
-                            }
-                        res = add(add(add(acc[0], acc[1]), add(acc[2], acc[3])),
-                                  add(add(acc[4], acc[5]), add(acc[6], acc[7])));
-#pragma unroll
-                        for (int k = 9; k < SQ_MAXLEN; ++k)  // tail: entries main+1 .. n
-                            if (k > main && k <= n) res = add(res, pk[k]);
-                    }
-                    sum = add(pk[0], res);
-                }
-                if (live) {
-                    double yv;
-                    if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
-                    else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
-                    else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
-                    else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
-                    else yv = sum;
-                    a.y[row] = yv;
-                    if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
-        }
-    }
-    if (want_dot || a.fin != FIN_NONE) {
-        double v = block_sum<SQ_THREADS>(dacc, red);
-        grid_finalize<SQ_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
     }
 }
 

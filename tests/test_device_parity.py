@@ -49,7 +49,7 @@ def test_spmv_ragged_rows_bit_identical(name, lanes):
 
 
 @pytest.mark.parametrize("nrows,mean", [(700, 300), (20000, 200)])
-@pytest.mark.parametrize("lanes", [0, 1, 8, -1])
+@pytest.mark.parametrize("lanes", [0, 1, 8])
 def test_spmv_long_rows_bit_identical(nrows, mean, lanes):
     # rows of 0..~3*mean entries: numpy's recursive pairwise split (n > 128);
     # lanes=0 takes the leaf-list kernels, the overrides the direct kernel's tree walk
@@ -63,17 +63,14 @@ def test_spmv_long_rows_bit_identical(nrows, mean, lanes):
     cols = np.concatenate([np.sort(rng.choice(ncols, l, replace=False)) for l in lens]).astype(np.int32)
     m = Csr(nrows, ncols, off, cols, rng.uniform(-1, 1, off[-1]))
     x = rng.uniform(-1, 1, ncols)
-    opts = {"lrow": 1} if lanes < 0 else {"lanes": lanes}  # -1: one warp per row (spmv_lrow)
-    dh = amg.DeviceHierarchy.from_matrices([m], options=opts)
+    dh = amg.DeviceHierarchy.from_matrices([m], options={"lanes": lanes})
     np.testing.assert_array_equal(dh.matrix(0, "a")(x), O.spmv(m, x))
     dh.close()
 
 
-@pytest.mark.parametrize("sellq", [0, 1])
 @pytest.mark.parametrize("kind", ["stencil", "uniform", "uniform_wide"])
-def test_spmv_sell_layouts_bit_identical(kind, sellq):
-    # SELL-32 (stencil-pattern columns or stored columns), per-lane loads or
-    # bulk-copy streamed (spmv_sellq), on matrices large enough for the layout
+def test_spmv_sell_layouts_bit_identical(kind):
+    # SELL-32 (stencil-pattern columns or stored columns) on matrices large enough for the layout
     from paper_2102_07417_b200.problems import Csr, poisson7
 
     rng = np.random.default_rng(3)
@@ -87,7 +84,7 @@ def test_spmv_sell_layouts_bit_identical(kind, sellq):
         cols = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
         m = Csr(n, n, off, cols, rng.uniform(-1, 1, off[-1]))
     x = rng.uniform(-1, 1, m.ncols)
-    dh = amg.DeviceHierarchy.from_matrices([m], options={"sellq": sellq})
+    dh = amg.DeviceHierarchy.from_matrices([m], options={"dict": 0, "symm": 0})
     np.testing.assert_array_equal(dh.matrix(0, "a")(x), O.spmv(m, x))
     dh.close()
 
@@ -229,27 +226,6 @@ def test_spmv_sorted_sell_bit_identical(maxlen):
         dh.close()
 
 
-@pytest.mark.parametrize("maxlen", [16, 46, 200])
-def test_spmv_short_long_split_bit_identical(maxlen):
-    # fine-level ragged rows: <= 16 entries on width-16 SELL-32 slices, the rest from a row list
-    from paper_2102_07417_b200.problems import Csr
-
-    rng = np.random.default_rng(maxlen + 1)
-    n = 60000
-    lens = np.minimum(rng.geometric(1.0 / 8.0, n), maxlen)
-    lens[:4] = [0, 1, maxlen, 17]
-    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
-    cols = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
-    m = Csr(n, n, off, cols, rng.uniform(-1, 1, off[-1]))
-    x = rng.uniform(-1, 1, n)
-    want = O.spmv(m, x)
-    for split in (1, 0):
-        dh = amg.DeviceHierarchy.from_matrices([m], options={"split": split, "sells_max_rows": 20000, "symm": 0})
-        assert (dh.layout(0, "a") == "split") == bool(split)
-        np.testing.assert_array_equal(dh.matrix(0, "a")(x), want)
-        dh.close()
-
-
 def test_spmv_symmetric_layout_rejects_one_ulp_asymmetry():
     from paper_2102_07417_b200.problems import Csr
 
@@ -264,16 +240,6 @@ def test_spmv_symmetric_layout_rejects_one_ulp_asymmetry():
     dh = amg.DeviceHierarchy.from_matrices([m2])
     assert dh.layout(0, "a") != "symd"
     np.testing.assert_array_equal(dh.matrix(0, "a")(x), O.spmv(m2, x))
-    dh.close()
-
-
-@pytest.mark.parametrize("opts", [{"tile_nnz": 64, "tile_rows": 32, "stages": 1},
-                                  {"tile_nnz": 300, "tile_rows": 64, "stages": 2},
-                                  {"tile_nnz": 4096, "tile_rows": 512, "stages": 2}])
-def test_spmv_tile_geometry_does_not_change_bits(opts):
-    m, x, y = load_spmv_case("spmv_ragged")
-    dh = amg.DeviceHierarchy.from_matrices([m], options=opts)
-    np.testing.assert_array_equal(dh.matrix(0, "a")(x), y)
     dh.close()
 
 

@@ -92,38 +92,6 @@ def test_fullsize_pcg_matches_reference_solve(full):
     np.testing.assert_array_equal(res.x, res2.x)
 
 
-@pytest.mark.parametrize("mode", [1, 2])
-def test_fullsize_fused_fsai_steps_bit_identical(full, mode):
-    # the one-kernel G/G^T step (fsai_fused) on the large levels: smoother
-    # sweeps bit-identical to the oracle, V-cycle bit-identical to the
-    # two-kernel path
-    import paper_2102_07417_b200 as amg
-    from oracle import solve as O
-
-    name, h, dh0 = full
-    if h.levels[0].smoother is None or h.levels[0].smoother.kind != "fsai":
-        pytest.skip("no FSAI smoother")
-    dh = amg.DeviceHierarchy.from_reference(h, options={"fused": mode})
-    fused = dh.stats()["fused_levels"]
-    assert fused & 1, "level 0 should run the fused FSAI step"
-    rng = np.random.default_rng(23)
-    for k, lv in enumerate(h.levels[:-1]):
-        if not (fused >> k) & 1:
-            continue
-        b, x0 = rng.uniform(-1, 1, lv.a.nrows), rng.uniform(-1, 1, lv.a.nrows)
-        for steps in (1, 2):
-            np.testing.assert_array_equal(dh.apply_smoother(k, b, None, steps),
-                                          O.apply_smoother(lv.smoother, lv.a, b, np.zeros_like(b), steps))
-            np.testing.assert_array_equal(dh.apply_smoother(k, b, x0, steps),
-                                          O.apply_smoother(lv.smoother, lv.a, b, x0, steps))
-    y = rng.uniform(-1, 1, h.levels[0].a.nrows)
-    dh2 = amg.DeviceHierarchy.from_reference(h, options={"fused": 0})
-    assert dh2.stats()["fused_levels"] == 0
-    np.testing.assert_array_equal(dh.vcycle(y), dh2.vcycle(y))
-    dh2.close()
-    dh.close()
-
-
 def test_fullsize_tail_dsm_bit_identical(full):
     # the cluster tail with its level vectors in distributed shared memory
     import paper_2102_07417_b200 as amg
