@@ -189,3 +189,51 @@ def test_elasticity3d_matches_reference_generator_at_sigma0(n):
     # stored patterns agree except where exact cancellation leaves a rounding-level entry
     diff = (da != 0) ^ (dr != 0)
     assert np.all(np.abs(da[diff]) <= 1e-13 * scale) and np.all(np.abs(dr[diff]) <= 1e-13 * scale)
+
+
+@pytest.mark.skipif(not have_reference(), reason="reference package only in the build container")
+@pytest.mark.parametrize("name", ["t_poisson7_8", "t_elasticity_4", "t_filtered"])
+def test_resumable_setup_matches_reference_setup(tmp_path, name):
+    # tools/setup_resumable.py replays amgkit.setup's loop body level by level,
+    # pickling each finished level; a run interrupted after level 1 and resumed
+    # must give the reference's hierarchy bit for bit
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    from setup_resumable import setup_resumable
+    from amgkit import AmgConfig, SparseMatrix, setup
+
+    if name == "t_poisson7_8":
+        a0 = problems.poisson7(8, 8, 8)
+        cfg = dict(smoother="fsai")
+    elif name == "t_elasticity_4":
+        a0, coords = problems.elasticity3d(4, 4, 4, sigma=1.0, nu=0.3, seed=1)
+        cfg = dict(smoother="fsai", interp="bamg", testspace="rigid_body", n_test_vectors=6, coords=coords)
+    else:  # operator filtering: nonsymmetric coarse levels, LU coarsest factor
+        a0 = problems.poisson7(6, 6, 6)
+        cfg = dict(smoother="jacobi", filter_target="operator", filter_rho=0.5, max_coarse=20)
+    A = SparseMatrix(a0.nrows, a0.ncols, a0.row_offsets, a0.col_indices, a0.values, check=True)
+    want = setup(A, AmgConfig(**cfg))
+    st = str(tmp_path / "state")
+    full = setup_resumable(A, AmgConfig(**cfg), st)
+    # interrupted run: keep only the first finished level, resume
+    st2 = str(tmp_path / "state2")
+    os.makedirs(st2)
+    import shutil
+
+    shutil.copy(os.path.join(st, "level_0.pkl"), st2)
+    resumed = setup_resumable(A, AmgConfig(**cfg), st2)
+    for h in (full, resumed):
+        assert h.n_levels == want.n_levels and h.factor_kind == want.factor_kind and h.symmetric == want.symmetric
+        for l1, l2 in zip(h.levels, want.levels):
+            assert hiercache.csr_digest(l1.a) == hiercache.csr_digest(l2.a)
+            for f in ("p", "pt"):
+                m1, m2 = getattr(l1, f), getattr(l2, f)
+                assert (m1 is None) == (m2 is None)
+                if m1 is not None:
+                    assert hiercache.csr_digest(m1) == hiercache.csr_digest(m2)
+            if l2.smoother is not None:
+                assert l1.smoother.omega == l2.smoother.omega
+                if l2.smoother.kind == "fsai":
+                    assert hiercache.csr_digest(l1.smoother.gmat) == hiercache.csr_digest(l2.smoother.gmat)
+        np.testing.assert_array_equal(np.asarray(h.factor[0]), np.asarray(want.factor[0]))

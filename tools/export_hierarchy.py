@@ -1,12 +1,16 @@
 """Run the REFERENCE hierarchy setup once and freeze it (build container only).
 
-Usage: python tools/export_hierarchy.py <config> [--out hier_cache] [--mode compact|full]
-                                        [--solve]
+Usage: python tools/export_hierarchy.py <config> [--out hier_cache] [--mode lean|compact|full]
+                                        [--solve] [--state DIR] [--oneshot]
 
 Imports ``amgkit`` from /root/reference/pkg/src (it is not available on the
-GPU box), builds A_0 with the config's generator, runs
-``amgkit.setup(A, AmgConfig(**recipe))`` (``amgkit/hierarchy.py:155-223``),
-and writes the result with :func:`paper_2102_07417_b200.hiercache.save_hierarchy`.
+GPU box), builds A_0 with the config's generator, runs the reference setup
+(``amgkit/hierarchy.py:155-223``) level by level through
+``tools/setup_resumable.py`` (every finished level is pickled under --state,
+so an interrupted multi-hour setup resumes where it stopped; ``--oneshot``
+calls ``amgkit.setup`` directly instead), and writes the result with
+:func:`paper_2102_07417_b200.hiercache.save_hierarchy` (lean by default:
+G's pattern only, see hiercache.py).
 With ``--solve`` it also runs the reference solve
 ``pcg(spmv(A0,.), b, vcycle(h,.), KrylovConfig(rtol=1e-8, record_history=True))``
 on ``b = default_rng(42).uniform(-1, 1, n)`` and records iterations, final
@@ -24,6 +28,7 @@ import time
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
+sys.path.insert(0, HERE)
 sys.path.insert(0, "/root/reference/pkg/src")
 
 import numpy as np  # noqa: E402
@@ -38,8 +43,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("config")
     ap.add_argument("--out", default=os.path.join(os.path.dirname(HERE), "hier_cache"))
-    ap.add_argument("--mode", default="compact", choices=("compact", "full"))
+    ap.add_argument("--mode", default="lean", choices=("lean", "compact", "full"))
     ap.add_argument("--solve", action="store_true")
+    ap.add_argument("--state", default=None, help="per-level setup state (default <out>/.setup_<config>)")
+    ap.add_argument("--oneshot", action="store_true", help="amgkit.setup in one call (no per-level state)")
     args = ap.parse_args()
 
     fn, gargs, gkw, recipe = problems.CONFIGS[args.config]
@@ -49,7 +56,13 @@ def main():
     if coords is not None:
         cfg["coords"] = coords
     t0 = time.perf_counter()
-    h = setup(A, AmgConfig(**cfg))
+    if args.oneshot:
+        h = setup(A, AmgConfig(**cfg))
+    else:
+        from setup_resumable import setup_resumable
+
+        state = args.state or os.path.join(args.out, f".setup_{args.config}")
+        h = setup_resumable(A, AmgConfig(**cfg), state, log=lambda m: print(m, flush=True))
     t_setup = time.perf_counter() - t0
     flags = []
     for lvl in h.levels[:-1]:
