@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <memory>
 #include <mutex>
 #include <unordered_map>
@@ -83,7 +84,6 @@ struct DevMat {
     int uW = 0, u_grid = 0, u_plen = 0;  // u_plen: padding slots skipped (short ragged rows)
     int nudiag = 0, sym_grid = 0, sym_fl = 0, symf_grid = 0, sym_blocked = 0;  // sym_fl: fixed-slot kernel width (0: none)
     int32_t *pstart = nullptr;   // padded-aligned layout (spmv_vec), nullptr if unused
-    int32_t *pperm = nullptr;    // its visiting order (rows grouped by round count), nullptr = natural
     double *pval = nullptr;
     int32_t *pcol = nullptr;
     int pad_grid = 0;
@@ -95,6 +95,7 @@ struct DevMat {
     int nleaves = 0, leaf_grid = 0, leafsum_grid = 0;
     HaloPlan halo;  // exchange feeding this matrix's halo columns (nranks > 1)
     int64_t lbytes[12] = {};  // per layout: bytes its kernel must stream (values, indices, row metadata)
+    int64_t int_lo = 0, int_hi = 0;  // interior rows [int_lo, int_hi): no halo column (overlap split), 128-aligned
     void *dcls = nullptr;     // row-class dictionary (spmv_dict): class id per row, nullptr if unused
     int32_t *dbeg = nullptr, *drel = nullptr;
     double *dval = nullptr;
@@ -192,6 +193,9 @@ struct amg_handle {
     int device = 0, rank = 0, nranks = 1;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;           // side stream: L2 prefetch of the tail levels
+    cudaStream_t comm_stream = nullptr;    // nranks > 1: halo send / recv, overlapped with interior rows
+    cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
+    int overlap_test = 0;                  // nranks == 1 diagnostics: run the interior / boundary split anyway
     cudaEvent_t pf_fork = nullptr, pf_join = nullptr;
     PrefetchRange *pf_ranges = nullptr;    // device copy of the tail matrices' ranges
     int pf_n = 0;
@@ -229,8 +233,6 @@ struct amg_handle {
     int symd_blocked = 1;         // symmetric layout stored slice-blocked (32 rows x nu diagonals contiguous)
     int symd_gminb = 5;           // round-by-round symmetric kernel: min CTAs/SM 5, 6 or 8
     int symd_minb = 4;            // fixed-slot 32-wide kernel: min CTAs/SM (register budget) 3, 4 or 5
-    int vec_groups = 0;           // padded CSR on > 1M rows: visit rows grouped by round count (measured slower:
-                                  // G^T_0 83 -> 109..124 us, lanes lose the contiguity of neighbouring rows)
     int sells = 1;                // sorted SELL-32 (sigma window below) where natural slices pad > 10%
     int sells_sigma = 128;
     int sells_buckets = 0;        // > 0: matrices above sells_max_rows get rows partitioned by round count into
@@ -242,7 +244,6 @@ struct amg_handle {
                                        // locality: config-2 G^T_0 85 -> 134 us; coarse A_1 18 -> 13 us)
     int rz_sep = 0;               // PCG: r.z in a separate dot kernel instead of the V-cycle's last SpMV
     int vec_minb = 4;             // padded-CSR kernel: min CTAs per SM (register budget) 4, 5 or 6
-    int vec_pipe = 0;             // padded-CSR kernel with the first round's columns fetched one row ahead
     int sellu_short = 1;          // ... and for rows of <= 8 entries at any padding, padding slots skipped
     int sellu = 1;                // uniform-width SELL-32 for rows of <= 16 entries padding <= 10% (e.g. FSAI G)
     int symd_chunked = 0;         // symmetric kernels: contiguous row chunk per CTA (measured slower than grid-stride)
@@ -414,9 +415,9 @@ static SpmvPatFn spmv_pat_fn(int epi)
 
 typedef void (*SpmvVecFn)(const SpmvArgs, const PadArgs, int);
 
-static SpmvVecFn spmv_vec_fn(int epi, bool pipe = false, int vminb = 4)
+static SpmvVecFn spmv_vec_fn(int epi, int vminb = 4)
 {
-#define AMG_V(E) return pipe ? spmv_vec<E, true> : (vminb >= 6 ? spmv_vec<E, false, 6> : vminb == 5 ? spmv_vec<E, false, 5> : spmv_vec<E, false, 4>);
+#define AMG_V(E) return vminb >= 6 ? spmv_vec<E, 6> : vminb == 5 ? spmv_vec<E, 5> : spmv_vec<E, 4>;
     switch (epi) {
     case EPI_PLAIN: AMG_V(EPI_PLAIN)
     case EPI_RESID: AMG_V(EPI_RESID)
@@ -534,6 +535,48 @@ static int exchange(amg_t *h, const DevMat &M, double *x)
     return AMG_OK;
 }
 
+// Overlapped exchange: the pack kernel on the main stream, the grouped
+// send / recv on the comm stream (after the pack), ev_halo marks arrival;
+// exchange_end makes the main stream wait for it.  Captured into the
+// iteration graph as a fork / join.
+static int exchange_begin(amg_t *h, const DevMat &M, double *x)
+{
+    if (h->nranks == 1 || M.halo.empty()) return AMG_OK;
+    const HaloPlan &P = M.halo;
+    NcclApi &api = nccl();
+    if (P.n_send > 0) {
+        int g = (int)std::min<int64_t>((P.n_send + VEC_THREADS - 1) / VEC_THREADS, (int64_t)h->sm_count * 4);
+        TRY(launch_k(h, halo_pack, std::max(g, 1), VEC_THREADS, 0, (const double *)x, (const int32_t *)P.send_idx,
+                     P.send_buf, P.n_send));
+    }
+    CK(cudaEventRecord(h->ev_pack, h->stream));
+    CK(cudaStreamWaitEvent(h->comm_stream, h->ev_pack, 0));
+    auto chk = [&](ncclResult_t r, const char *w) -> int {
+        if (r != ncclSuccess) return fail(AMG_E_NCCL, std::string(w) + ": " + api.GetErrorString(r));
+        return AMG_OK;
+    };
+    TRY(chk(api.GroupStart(), "ncclGroupStart"));
+    int64_t roff = P.n_own;
+    for (size_t i = 0; i < P.recv_peers.size(); ++i) {
+        TRY(chk(api.Recv(x + roff, (size_t)P.recv_counts[i], ncclDouble, P.recv_peers[i], h->comm.comm, h->comm_stream),
+                "ncclRecv"));
+        roff += P.recv_counts[i];
+    }
+    for (size_t i = 0; i < P.send_peers.size(); ++i)
+        TRY(chk(api.Send(P.send_buf + P.send_displ[i], (size_t)P.send_counts[i], ncclDouble, P.send_peers[i],
+                         h->comm.comm, h->comm_stream), "ncclSend"));
+    TRY(chk(api.GroupEnd(), "ncclGroupEnd"));
+    CK(cudaEventRecord(h->ev_halo, h->comm_stream));
+    return AMG_OK;
+}
+
+static int exchange_end(amg_t *h, const DevMat &M)
+{
+    if (h->nranks == 1 || M.halo.empty()) return AMG_OK;
+    CK(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+    return AMG_OK;
+}
+
 // Reductions: with distributed level-0 vectors a kernel's finalize stores the
 // rank's partial; the partials are all-gathered and summed in rank order.
 static int kfin(const amg_t *h, int fin) { return (h->dist_dots && fin != FIN_NONE) ? (int)FIN_LOCAL : fin; }
@@ -567,6 +610,61 @@ static int allgather_level(amg_t *h, int k, double *y)
 // one grouped ncclSend/ncclRecv per peer into x[n_own ...] (plan order).
 static int exchange(amg_t *h, const DevMat &M, double *x);
 
+static int layout_of(const amg_t *h, const DevMat &M)
+{
+    // same precedence as launch_spmv
+    return M.nrows == 0            ? AMG_LAYOUT_EMPTY
+              : M.dcls                ? AMG_LAYOUT_DICT
+              : (M.uval && h->symm)   ? AMG_LAYOUT_SYMD
+              : (M.sv_s && h->sells)   ? AMG_LAYOUT_SELL_SORTED
+              : (M.uval_s && h->sellu) ? AMG_LAYOUT_SELL_UNIFORM
+              : M.sbeg                ? (M.scol ? AMG_LAYOUT_SELL : AMG_LAYOUT_SELL_PAT)
+              : (M.pid && M.pstart)   ? AMG_LAYOUT_PATTERN
+              : M.leaf                ? AMG_LAYOUT_LEAVES
+              : M.pstart              ? AMG_LAYOUT_PADDED
+                                      : AMG_LAYOUT_CSR;
+}
+
+// Layouts whose kernels take row ranges (SpmvArgs rlo / rsplit / rgap).
+static bool range_layout(int lay)
+{
+    return lay == AMG_LAYOUT_SELL_SORTED || lay == AMG_LAYOUT_SELL_UNIFORM || lay == AMG_LAYOUT_PADDED ||
+           lay == AMG_LAYOUT_CSR;
+}
+
+// One launch over `count` virtual rows (a.rlo / a.rsplit / a.rgap map them);
+// *grid_used receives the grid (the partial slots this launch fills).
+static int spmv_range(amg_t *h, const DevMat &M, int lay, const SpmvArgs &a, int epi, int count, int grid_cap,
+                      int *grid_used)
+{
+    auto cap = [&](int g, int64_t need) {
+        g = (int)std::max<int64_t>(1, std::min<int64_t>(g, need));
+        return grid_cap ? std::min(g, grid_cap) : g;
+    };
+    int g = 1;
+    if (lay == AMG_LAYOUT_SELL_SORTED) {
+        SellSArgs qa{M.sv_s, M.sc_s, M.sb_s, M.sw_s, M.sp_s, M.sl_s, (int)M.nrows};
+        g = cap(M.s_grid, ((count + 31) / 32 + 7) / 8);
+        TRY(launch_k(h, spmv_sells_fn(epi, h->sells_plen), g, VEC_SPMV_THREADS, 0, a, qa, count));
+    } else if (lay == AMG_LAYOUT_SELL_UNIFORM) {
+        SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW};
+        g = cap(M.u_grid, (count + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS);
+        TRY(launch_k(h, spmv_sellu_fn(epi, M.uW, M.u_plen), g, VEC_SPMV_THREADS, 0, a, ua, count));
+    } else if (lay == AMG_LAYOUT_PADDED) {
+        PadArgs pa{M.pstart, M.pval, M.pcol};
+        g = cap(M.pad_grid, (count + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS);
+        TRY(launch_k(h, spmv_vec_fn(epi, h->vec_minb), g, VEC_SPMV_THREADS, 0, a, pa, count));
+    } else if (lay == AMG_LAYOUT_CSR) {
+        const int gpr = DIRECT_THREADS / M.lanes;
+        g = cap(h->sm_count * h->direct_per_sm, (count + gpr - 1) / gpr);
+        TRY(launch_k(h, spmv_direct_fn(epi, M.lanes), g, DIRECT_THREADS, 0, a, count));
+    } else {
+        return fail(AMG_E_STATE, "internal: row-range launch on a layout without range support");
+    }
+    if (grid_used) *grid_used = g;
+    return AMG_OK;
+}
+
 static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, int epi, const double *b, double omega,
                        const double *dotw, int fin, const int *g1, const int *g2, int grid_cap = 0)
 {
@@ -586,7 +684,6 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         h->collect->push_back(o);
         return AMG_OK;
     }
-    TRY(exchange(h, M, const_cast<double *>(x)));
     if (h->grid_per_sm > 0) {  // global cap on CTAs per SM (tuning)
         const int c = h->grid_per_sm * h->sm_count;
         grid_cap = grid_cap ? std::min(grid_cap, c) : c;
@@ -623,6 +720,32 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     a.ctl = h->ctl;
     a.gate1 = g1;
     a.gate2 = g2;
+    a.rsplit = INT_MAX;
+    const int lay = layout_of(h, M);
+    if (M.int_hi > M.int_lo && (h->nranks > 1 || h->overlap_test) && range_layout(lay)) {
+        // interior / boundary split: the interior rows need no halo column, so they run
+        // while the halo travels on the comm stream; the boundary rows (both ends of the
+        // block) follow once it has arrived.  Every row is computed whole by one launch:
+        // rows stay bit-identical; a fused dot folds both launches' partials in order.
+        const bool red = dotw != nullptr || fin != FIN_NONE;
+        TRY(exchange_begin(h, M, const_cast<double *>(x)));
+        SpmvArgs ai = a;
+        ai.rlo = (int)M.int_lo;
+        ai.pmode = red ? 1 : 0;
+        int gi = 0;
+        TRY(spmv_range(h, M, lay, ai, epi, (int)(M.int_hi - M.int_lo), grid_cap, &gi));
+        TRY(exchange_end(h, M));
+        SpmvArgs ab = a;
+        ab.rlo = 0;
+        ab.rsplit = (int)M.int_lo;
+        ab.rgap = (int)(M.int_hi - M.int_lo);
+        ab.pmode = red ? 2 : 0;
+        ab.pbase = gi;
+        TRY(spmv_range(h, M, lay, ab, epi, (int)(M.nrows - (M.int_hi - M.int_lo)), grid_cap, nullptr));
+        TRY(post_fin(h, ufin, g1));
+        return AMG_OK;
+    }
+    TRY(exchange(h, M, const_cast<double *>(x)));
     if (M.dcls) {
         DictArgs da{M.dcls, M.dbeg, M.drel, M.dval, M.dncls, M.dnent};
         const size_t sm = (size_t)M.dnent * 12 + (size_t)(M.dncls + 1) * 4;
@@ -651,7 +774,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
             TRY(launch_k(h, spmv_symd_fn(epi, h->symd_gminb, M.sym_blocked, tsm), g, VEC_SPMV_THREADS, tsm_bytes, a, sa,
                          (int)M.nrows));
     } else if (M.sv_s && h->sells) {
-        SellSArgs qa{M.sv_s, M.sc_s, M.sb_s, M.sw_s, M.sp_s, M.sl_s};
+        SellSArgs qa{M.sv_s, M.sc_s, M.sb_s, M.sw_s, M.sp_s, M.sl_s, (int)M.nrows};
         TRY(launch_k(h, spmv_sells_fn(epi, h->sells_plen), grid_cap ? std::min(grid_cap, M.s_grid) : M.s_grid, VEC_SPMV_THREADS, 0, a,
                      qa, (int)M.nrows));
     } else if (M.uval_s && h->sellu) {
@@ -675,8 +798,8 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         TRY(launch_k(h, spmv_leafsum_fn(epi), grid_cap ? std::min(grid_cap, M.leafsum_grid) : M.leafsum_grid,
                      DIRECT_THREADS, 0, a, la, (int)M.nrows));
     } else if (M.pstart) {
-        PadArgs pa{M.pstart, M.pval, M.pcol, h->vec_pipe ? nullptr : M.pperm};
-        TRY(launch_k(h, spmv_vec_fn(epi, h->vec_pipe, h->vec_minb), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
+        PadArgs pa{M.pstart, M.pval, M.pcol};
+        TRY(launch_k(h, spmv_vec_fn(epi, h->vec_minb), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
                      pa, (int)M.nrows));
     } else {
         const int gpr = DIRECT_THREADS / M.lanes;  // row groups per CTA
@@ -1229,6 +1352,9 @@ int amg_create(int device, int rank, int nranks, const void *nccl_unique_id, amg
     h->sm_count = prop.multiProcessorCount;
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->ev_pack, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->pf_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->pf_join, cudaEventDisableTiming));
     CK(cudaEventCreate(&h->ev0));
@@ -1258,7 +1384,7 @@ void amg_destroy(amg_t *h)
     };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.pperm); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s); F(M.dcls); F(M.dbeg); F(M.drel); F(M.dval);
+            F(M.off); F(M.col); F(M.val); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s); F(M.dcls); F(M.dbeg); F(M.drel); F(M.dval);
             symd_slot_give(h->device, M.sym_slot);
             M.sym_slot = -1;
             symd_tab_give(h->device, M.sym_tab, M.sym_ntab);
@@ -1269,6 +1395,9 @@ void amg_destroy(amg_t *h)
     }
     F(h->pf_ranges);
     if (h->side) cudaStreamDestroy(h->side);
+    if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+    if (h->ev_pack) cudaEventDestroy(h->ev_pack);
+    if (h->ev_halo) cudaEventDestroy(h->ev_halo);
     if (h->pf_fork) cudaEventDestroy(h->pf_fork);
     if (h->pf_join) cudaEventDestroy(h->pf_join);
     F(h->Lp); F(h->LU); F(h->dinv); F(h->binv); F(h->tail_ops); F(h->tail_mats); F(h->tail_vecs); F(h->tail_splits); F(h->piv); F(h->partials); F(h->ticket); F(h->ctl);
@@ -1300,7 +1429,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
     if (k == "symm") { h->symm = value ? 1 : 0; return AMG_OK; }
     if (k == "dict") { h->dict = value ? 1 : 0; return AMG_OK; }
-    if (k == "vec_groups") { h->vec_groups = (int)value; return AMG_OK; }
+    if (k == "overlap_test") { h->overlap_test = value ? 1 : 0; return AMG_OK; }
     if (k == "sells") { h->sells = (int)value; return AMG_OK; }
     if (k == "sells_max_rows") { h->sells_max_rows = value; return AMG_OK; }
     if (k == "sells_buckets") { h->sells_buckets = (int)value; return AMG_OK; }
@@ -1310,7 +1439,6 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "sells_min_avg10") { h->sells_min_avg = value / 10.0; return AMG_OK; }
     if (k == "rz_sep") { h->rz_sep = value ? 1 : 0; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
     if (k == "vec_minb") { h->vec_minb = (int)value; return AMG_OK; }
-    if (k == "vec_pipe") { h->vec_pipe = value ? 1 : 0; return AMG_OK; }
     if (k == "sellu_short") { h->sellu_short = value ? 1 : 0; return AMG_OK; }
     if (k == "sellu") { h->sellu = value ? 1 : 0; return AMG_OK; }
     if (k == "symd_fixed") { h->symd_fixed = (int)value; return AMG_OK; }
@@ -1825,6 +1953,42 @@ static int build_symd(amg_t *h, DevMat &M, const std::vector<int32_t> &off32, co
     return AMG_OK;
 }
 
+// Interior rows of a distributed matrix (no column in the halo segment): the
+// rows below the last halo-touching row of the first half and above the first
+// halo-touching row of the second half -- for a z-slab block, everything but
+// its first and last planes.  Aligned inwards to 128 rows (slices / sorted
+// windows map whole).  overlap_test (one rank): the middle half of every
+// matrix, to exercise the split launches on one GPU.
+static int interior_range(amg_t *h, DevMat &M, const std::vector<int32_t> &off32)
+{
+    M.int_lo = M.int_hi = 0;
+    const int64_t n = M.nrows;
+    int64_t lo_end = 0, hi_start = n;
+    if (h->nranks > 1) {
+        if (M.halo.empty() || M.nnz == 0) return AMG_OK;
+        std::vector<int32_t> col_h(M.nnz);
+        CK(cudaMemcpy(col_h.data(), M.col, M.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        for (int64_t r = 0; r < n; ++r) {
+            bool halo = false;
+            for (int32_t k = off32[r]; k < off32[r + 1] && !halo; ++k) halo = col_h[k] >= M.n_own;
+            if (!halo) continue;
+            if (r < n / 2) lo_end = r + 1;
+            else if (hi_start == n) hi_start = r;
+        }
+    } else if (h->overlap_test) {
+        lo_end = n / 4;
+        hi_start = 3 * n / 4;
+    } else {
+        return AMG_OK;
+    }
+    const int64_t a = (lo_end + 127) / 128 * 128, b = hi_start / 128 * 128;
+    if (b - a >= 128 && b - a >= n / 8) {
+        M.int_lo = a;
+        M.int_hi = b;
+    }
+    return AMG_OK;
+}
+
 int amg_finalize(amg_t *h)
 {
     if (!h) return fail(AMG_E_ARG, "NULL handle");
@@ -1905,6 +2069,7 @@ int amg_finalize(amg_t *h)
             if (!M.present) continue;
             std::vector<int32_t> off32(M.nrows + 1);
             CK(cudaMemcpy(off32.data(), M.off, (M.nrows + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+            TRY(interior_range(h, M, off32));
             // row-class dictionary first: where it applies no value / column stream is needed
             if (h->dict && h->nranks == 1 && !h->lanes_override && M.nrows >= (int64_t)h->sm_count * h->small_rows_per_sm)
                 TRY(build_dict(h, M, off32));
@@ -1982,19 +2147,6 @@ int amg_finalize(amg_t *h)
                 CK(cudaMemcpy(M.pstart, ps.data(), ps.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
                 CK(cudaMemcpy(M.pcol, pc.data(), pc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
                 CK(cudaMemcpy(M.pval, pv.data(), pv.size() * sizeof(double), cudaMemcpyHostToDevice));
-                if (h->vec_groups > 0 && M.nrows > h->sells_max_rows) {
-                    // warps see rows needing the same number of 8-entry rounds (less divergence on ragged
-                    // fine-level rows); natural order inside a group keeps the x gathers local
-                    std::vector<int32_t> ord(M.nrows);
-                    for (int64_t r = 0; r < M.nrows; ++r) ord[r] = (int32_t)r;
-                    auto grp = [&](int32_t r) {
-                        const int n1 = off32[r + 1] - off32[r] - 1;
-                        return n1 < 8 ? 0 : std::min(1 + (n1 - 8) / 8, h->vec_groups);
-                    };
-                    std::stable_sort(ord.begin(), ord.end(), [&](int32_t x1, int32_t x2) { return grp(x1) < grp(x2); });
-                    TRY(dalloc(&M.pperm, ord.size()));
-                    CK(cudaMemcpy(M.pperm, ord.data(), ord.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-                }
                 // stencil patterns: every row's (col - row) tuple from a small dictionary
                 if (h->patterns && h->nranks == 1 && M.ncols == M.nrows) {
                     std::vector<int32_t> rel, beg;
@@ -2085,7 +2237,7 @@ int amg_finalize(amg_t *h)
                     }
                 }
                 int nb = 0;
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_vec_fn(EPI_RESID, h->vec_pipe, h->vec_minb), VEC_SPMV_THREADS, 0));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_vec_fn(EPI_RESID, h->vec_minb), VEC_SPMV_THREADS, 0));
                 M.pad_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
                                                                         (int64_t)h->sm_count * std::max(nb, 1)));
                 h->max_grid = std::max(h->max_grid, M.pad_grid);
@@ -2292,7 +2444,7 @@ int amg_finalize(amg_t *h)
     TRY(dalloc(&h->q, c0));
     TRY(dalloc(&h->tmp_in, nmax));
     TRY(dalloc(&h->tmp_out, nmax));
-    TRY(dalloc(&h->partials, h->max_grid));
+    TRY(dalloc(&h->partials, 2 * (size_t)h->max_grid));  // two-launch (interior / boundary) reductions
     TRY(dalloc(&h->ticket, 4));
     TRY(dalloc(&h->ctl, 1));
     CK(cudaMallocHost((void **)&h->ctl_h, sizeof(PcgCtl)));
@@ -2709,8 +2861,6 @@ int amg_bicgstab(amg_t *h, const double *b, const double *x0, double rtol, int m
     return finish(max_iters, relres, 0);
 }
 
-static int layout_of(const amg_t *h, const DevMat &M);
-
 int amg_matrix_layout(amg_t *h, int level, int which, int *layout)
 {
     if (!h || !layout) return fail(AMG_E_ARG, "amg_matrix_layout: NULL argument");
@@ -2739,20 +2889,6 @@ int amg_matrix_bytes(amg_t *h, int level, int which, int64_t *stored, int64_t *v
     return AMG_OK;
 }
 
-static int layout_of(const amg_t *h, const DevMat &M)
-{
-    // same precedence as launch_spmv
-    return M.nrows == 0            ? AMG_LAYOUT_EMPTY
-              : M.dcls                ? AMG_LAYOUT_DICT
-              : (M.uval && h->symm)   ? AMG_LAYOUT_SYMD
-              : (M.sv_s && h->sells)   ? AMG_LAYOUT_SELL_SORTED
-              : (M.uval_s && h->sellu) ? AMG_LAYOUT_SELL_UNIFORM
-              : M.sbeg                ? (M.scol ? AMG_LAYOUT_SELL : AMG_LAYOUT_SELL_PAT)
-              : (M.pid && M.pstart)   ? AMG_LAYOUT_PATTERN
-              : M.leaf                ? AMG_LAYOUT_LEAVES
-              : M.pstart              ? AMG_LAYOUT_PADDED
-                                      : AMG_LAYOUT_CSR;
-}
 
 int amg_get_stats(amg_t *h, amg_stats_t *out)
 {

@@ -81,7 +81,18 @@ struct SpmvArgs {
     PcgCtl *ctl;
     const int *gate1;
     const int *gate2;
+    // row-range launches (multi-GPU interior / boundary split): a kernel's
+    // virtual row v is row rlo + v + (v >= rsplit ? rgap : 0); identity
+    // (0, INT_MAX, 0) by default.  rlo, rsplit, rgap are multiples of 128, so
+    // 32-row slices and 128-row SELL-sigma windows map whole.
+    int rlo, rsplit, rgap;
+    // reductions over two launches: pmode 0 = this launch finalizes alone;
+    // 1 = store partials[pbase + cta] only; 2 = store, then the last CTA folds
+    // partials[0, pbase + grid) (the first launch wrote [0, pbase))
+    int pmode, pbase;
 };
+
+__device__ __forceinline__ int vrow(const SpmvArgs &a, int v) { return a.rlo + v + (v >= a.rsplit ? a.rgap : 0); }
 
 // ---------------------------------------------------------------- helpers
 
@@ -288,6 +299,15 @@ __device__ __forceinline__ void grid_finalize_pair(double v, double *partials, i
             __threadfence();
         }
     }
+}
+
+// SpMV reductions (pmode, see SpmvArgs)
+template <int NT>
+__device__ __forceinline__ void spmv_finalize(double v, const SpmvArgs &a)
+{
+    if (a.pmode == 0) grid_finalize<NT>(v, a.partials, a.ticket, a.fin, a.ctl);
+    else if (a.pmode == 1) { if (threadIdx.x == 0) a.partials[a.pbase + blockIdx.x] = v; }
+    else grid_finalize_pair<NT>(v, a.partials, a.pbase, a.ticket, a.fin, a.ctl);
 }
 
 // ---------------------------------------------------------------- SpMV
@@ -601,14 +621,17 @@ __global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_direct(const SpmvArgs 
     // row offsets of the next row are fetched one iteration ahead
     int nlo = 0, nhi = 0;
     if (g0 < nrows) {
-        nlo = __ldg(off + g0);
-        nhi = __ldg(off + g0 + 1);
+        const int r = vrow(a, g0);
+        nlo = __ldg(off + r);
+        nhi = __ldg(off + r + 1);
     }
-    for (int row = g0; row < nrows; row += ngroups) {
+    for (int v = g0; v < nrows; v += ngroups) {
+        const int row = vrow(a, v);
         const int lo = nlo, hi = nhi;
-        if (row + ngroups < nrows) {
-            nlo = __ldg(off + row + ngroups);
-            nhi = __ldg(off + row + ngroups + 1);
+        if (v + ngroups < nrows) {
+            const int r = vrow(a, v + ngroups);
+            nlo = __ldg(off + r);
+            nhi = __ldg(off + r + 1);
         }
         const int n = hi - lo - 1;
         double bv = 0.0, wv = 0.0;
@@ -627,8 +650,8 @@ __global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_direct(const SpmvArgs 
                 double res = 0.0;
 #pragma unroll
                 for (int t = 1; t < 8; ++t) {
-                    const double v = __shfl_sync(gmask, pk, t, LANES);
-                    if (t <= n) res = add(res, v);
+                    const double pt = __shfl_sync(gmask, pk, t, LANES);
+                    if (t <= n) res = add(res, pt);
                 }
                 sum = add(__shfl_sync(gmask, pk, 0, LANES), res);
             } else {
@@ -642,8 +665,8 @@ __global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_direct(const SpmvArgs 
                 double res = 0.0;
 #pragma unroll
                 for (int t = 1; t < 8; ++t) {
-                    const double v = (LANES == 1) ? pe[t] : __shfl_sync(gmask, pe[t], t % LANES, LANES);
-                    if (t <= n) res = add(res, v);
+                    const double pt = (LANES == 1) ? pe[t] : __shfl_sync(gmask, pe[t], t % LANES, LANES);
+                    if (t <= n) res = add(res, pt);
                 }
                 const double p0 = (LANES == 1) ? pe[0] : __shfl_sync(gmask, pe[0], 0, LANES);
                 sum = add(p0, res);
@@ -669,7 +692,7 @@ __global__ void __launch_bounds__(DIRECT_THREADS, 4) spmv_direct(const SpmvArgs 
     }
     if (want_dot || a.fin != FIN_NONE) {
         double v = block_sum<DIRECT_THREADS>(dacc, red);
-        grid_finalize<DIRECT_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+        spmv_finalize<DIRECT_THREADS>(v, a);
     }
 }
 
@@ -794,16 +817,10 @@ struct PadArgs {
     const int32_t *pstart;  // nrows + 1 padded row starts (== 3 mod 4)
     const double *pval;     // padded values (16-byte aligned base)
     const int32_t *pcol;    // padded columns
-    const int32_t *perm;    // visiting order of the rows (nullptr: natural): rows grouped by the number
-                            // of 8-entry rounds they need, natural order inside a group
 };
 
-// PIPE: software pipeline -- row offsets two rows ahead and the first
-// round's columns (entry 0 and the aligned 8 after it) one row ahead, so a
-// row's first-round value loads and x gathers leave together (fewer CTAs:
-// the prefetched columns cost registers).
-template <int EPI, bool PIPE, int MINB = 4>
-__global__ void __launch_bounds__(VEC_SPMV_THREADS, PIPE ? 3 : MINB) spmv_vec(const SpmvArgs a, const PadArgs pa, int nrows)
+template <int EPI, int MINB = 4>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, MINB) spmv_vec(const SpmvArgs a, const PadArgs pa, int nrows)
 {
     __shared__ double red[VEC_SPMV_THREADS / 32];
     pdl_launch();
@@ -814,51 +831,21 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, PIPE ? 3 : MINB) spmv_vec(co
     const bool self_dot = a.dotw == a.y;
     const double *__restrict__ x = a.x;
     double dacc = 0.0;
-    int row = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x;
+    const int v0 = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x;
     int nlo = 0, nhi = 0, nps = 0;
-    int len2 = 0, ps2 = 0, nc0 = 0;
-    int4 nca = make_int4(0, 0, 0, 0), ncb = make_int4(0, 0, 0, 0);
-    auto fetch_cols = [&](int ps, int len) {
-        if (len > 0) nc0 = __ldg(pa.pcol + ps);
-        const int4 *c4 = reinterpret_cast<const int4 *>(pa.pcol + ps + 1);
-        nca = len > 1 ? __ldg(c4) : make_int4(0, 0, 0, 0);
-        ncb = len > 5 ? __ldg(c4 + 1) : make_int4(0, 0, 0, 0);
-    };
-    const int32_t *__restrict__ perm = pa.perm;
-    int prow = 0;  // row visited at position `row` (== row without a permutation)
-    if (row < nrows) {
-        prow = perm ? __ldg(perm + row) : row;
+    int prow = 0;  // row of the next virtual position (row-range launches)
+    if (v0 < nrows) {
+        prow = vrow(a, v0);
         nlo = __ldg(a.off + prow);
         nhi = __ldg(a.off + prow + 1);
         nps = __ldg(pa.pstart + prow);
     }
-    if constexpr (PIPE) {
-        if (row + nthreads < nrows) {
-            len2 = __ldg(a.off + row + nthreads + 1) - __ldg(a.off + row + nthreads);
-            ps2 = __ldg(pa.pstart + row + nthreads);
-        }
-        if (row < nrows) fetch_cols(nps, nhi - nlo);
-    }
-    for (int pos = row; pos < nrows; pos += nthreads) {
+    for (int pos = v0; pos < nrows; pos += nthreads) {
         const int row = prow;
         const int len = nhi - nlo;
         const int ps = nps;
-        int c0 = 0;
-        int4 fca = make_int4(0, 0, 0, 0), fcb = make_int4(0, 0, 0, 0);
-        if constexpr (PIPE) {
-            c0 = nc0;
-            fca = nca;
-            fcb = ncb;
-            nlo = 0;
-            nhi = len2;
-            nps = ps2;
-            if (pos + nthreads < nrows) fetch_cols(nps, nhi);  // PIPE: natural order only (no perm)
-            if (pos + 2 * nthreads < nrows) {
-                len2 = __ldg(a.off + pos + 2 * nthreads + 1) - __ldg(a.off + pos + 2 * nthreads);
-                ps2 = __ldg(pa.pstart + pos + 2 * nthreads);
-            }
-        } else if (pos + nthreads < nrows) {
-            prow = perm ? __ldg(perm + pos + nthreads) : pos + nthreads;
+        if (pos + nthreads < nrows) {  // next row's offsets one step ahead
+            prow = vrow(a, pos + nthreads);
             nlo = __ldg(a.off + prow);
             nhi = __ldg(a.off + prow + 1);
             nps = __ldg(pa.pstart + prow);
@@ -869,7 +856,7 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, PIPE ? 3 : MINB) spmv_vec(co
         const int n = len - 1;
         double sum = 0.0;
         if (n >= 0 && n <= 128) {
-            const double p0 = prod(__ldg(pa.pval + ps), __ldg(x + (PIPE ? c0 : __ldg(pa.pcol + ps))));
+            const double p0 = prod(__ldg(pa.pval + ps), __ldg(x + __ldg(pa.pcol + ps)));
             const int b1 = ps + 1;  // 16-byte aligned
             const double2 *v2 = reinterpret_cast<const double2 *>(pa.pval + b1);
             const int4 *c4 = reinterpret_cast<const int4 *>(pa.pcol + b1);
@@ -888,8 +875,8 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, PIPE ? 3 : MINB) spmv_vec(co
             };
             // masked round (entries beyond `cnt` belong to padding / the next row: not used)
             auto round8m = [&](int r, int cnt, double p[8]) {
-                const int4 ca = (PIPE && r == 0) ? fca : __ldg(c4 + 2 * r);
-                const int4 cb = (PIPE && r == 0) ? fcb : (cnt > 4 ? __ldg(c4 + 2 * r + 1) : make_int4(0, 0, 0, 0));
+                const int4 ca = __ldg(c4 + 2 * r);
+                const int4 cb = cnt > 4 ? __ldg(c4 + 2 * r + 1) : make_int4(0, 0, 0, 0);
                 const double2 va = __ldg(v2 + 4 * r);
                 const double2 vb = cnt > 2 ? __ldg(v2 + 4 * r + 1) : make_double2(0.0, 0.0);
                 const double2 vc = cnt > 4 ? __ldg(v2 + 4 * r + 2) : make_double2(0.0, 0.0);
@@ -944,7 +931,7 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, PIPE ? 3 : MINB) spmv_vec(co
     }
     if (want_dot || a.fin != FIN_NONE) {
         double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
-        grid_finalize<VEC_SPMV_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+        spmv_finalize<VEC_SPMV_THREADS>(v, a);
     }
 }
 
@@ -1555,7 +1542,7 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, FL <= 4 ? 6 : FL <= 9 ? 4 : 
     const double *__restrict__ x = a.x;
     const int W32 = 32 * u.W;
     double dacc = 0.0;
-    int row = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x;
+    int v = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x;
     int c[FL];
     int len = 0;
     auto fetch = [&](int r) {
@@ -1564,15 +1551,16 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, FL <= 4 ? 6 : FL <= 9 ? 4 : 
 #pragma unroll
         for (int k = 0; k < FL; ++k) c[k] = (k < (PLEN ? len : u.W)) ? __ldg(u.col + base + 32 * k) : r;
     };
-    if (row < nrows) fetch(row);
-    for (; row < nrows; row += nthreads) {
+    if (v < nrows) fetch(vrow(a, v));
+    for (; v < nrows; v += nthreads) {
+        const int row = vrow(a, v);
         const int base = (row >> 5) * W32 + (row & 31);
         double p[FL];
 #pragma unroll
         for (int k = 0; k < FL; ++k)
             p[k] = (k < (PLEN ? len : u.W)) ? prod(__ldg(u.val + base + 32 * k), __ldg(x + c[k])) : 0.0;
         const int clen = len;
-        if (row + nthreads < nrows) fetch(row + nthreads);
+        if (v + nthreads < nrows) fetch(vrow(a, v + nthreads));
         double bv = 0.0, wv = 0.0;
         if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
         if (want_dot && !self_dot) wv = a.dotw[row];
@@ -1588,7 +1576,7 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, FL <= 4 ? 6 : FL <= 9 ? 4 : 
     }
     if (want_dot || a.fin != FIN_NONE) {
         double v2 = block_sum<VEC_SPMV_THREADS>(dacc, red);
-        grid_finalize<VEC_SPMV_THREADS>(v2, a.partials, a.ticket, a.fin, a.ctl);
+        spmv_finalize<VEC_SPMV_THREADS>(v2, a);
     }
 }
 
@@ -1610,6 +1598,7 @@ struct SellSArgs {
     const uint8_t *swid;   // per slice width
     const int32_t *perm;   // slot -> row
     const uint8_t *slen;   // per slot row length
+    int nslots;            // rows of the matrix (slots beyond are empty)
 };
 
 template <int EPI, bool PLEN>
@@ -1620,7 +1609,7 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_sells(const SpmvArgs
     pdl_wait();
     if (!gate_open(a.gate1, a.gate2)) return;
     const int lane = threadIdx.x & 31;
-    const int nslices = (nrows + 31) >> 5;
+    const int nslices = (nrows + 31) >> 5;  // virtual slices (row-range launches: whole windows)
     const int wstride = gridDim.x * (VEC_SPMV_THREADS / 32);
     const bool want_dot = a.dotw != nullptr;
     const bool self_dot = a.dotw == a.y;
@@ -1628,12 +1617,13 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_sells(const SpmvArgs
     double dacc = 0.0;
     int sl = blockIdx.x * (VEC_SPMV_THREADS / 32) + (threadIdx.x >> 5);
     int nsb = 0, nw = 0, nrow = -1, nlen = 0;
-    auto meta = [&](int s) {
+    auto meta = [&](int vs) {
+        const int s = vrow(a, vs * 32) >> 5;
         nsb = __ldg(q.sbeg + s);
         nw = __ldg(q.swid + s);
         const int pos = s * 32 + lane;
-        nrow = pos < nrows ? __ldg(q.perm + pos) : -1;
-        nlen = pos < nrows ? __ldg(q.slen + pos) : 0;
+        nrow = pos < q.nslots ? __ldg(q.perm + pos) : -1;
+        nlen = pos < q.nslots ? __ldg(q.slen + pos) : 0;
     };
     if (sl < nslices) meta(sl);
     for (; sl < nslices; sl += wstride) {
@@ -1667,7 +1657,7 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_sells(const SpmvArgs
     }
     if (want_dot || a.fin != FIN_NONE) {
         double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
-        grid_finalize<VEC_SPMV_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+        spmv_finalize<VEC_SPMV_THREADS>(v, a);
     }
 }
 

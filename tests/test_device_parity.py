@@ -541,3 +541,54 @@ def test_run_solve_report_and_cli(tmp_path):
     assert main(["solve", "--cache", d, "--format", "json", "--history", str(tmp_path / "hist.csv")]) == 0
     assert main(["solve", "--cache", d, "--max-iters", "2"]) == 2
     assert main(["solve", "--cache", str(tmp_path / "missing")]) == 1
+
+
+@pytest.mark.parametrize("kind", ["uniform", "ragged", "padded", "small"])
+def test_interior_boundary_split_spmv_bit_identical(kind):
+    # the multi-GPU overlap schedule on one GPU (overlap_test): interior rows
+    # [n/4, 3n/4) in one launch, the two boundary ranges in a second, reductions
+    # folded over both launches' partials; every row must stay bit-identical
+    from paper_2102_07417_b200.problems import Csr
+
+    rng = np.random.default_rng({"uniform": 1, "ragged": 2, "padded": 3, "small": 4}[kind])
+    n = {"uniform": 60000, "ragged": 50000, "padded": 1_100_000, "small": 9000}[kind]
+    if kind == "uniform":
+        lens = np.full(n, 9)
+    elif kind == "ragged":
+        lens = rng.integers(3, 16, n)
+    elif kind == "padded":
+        lens = rng.integers(8, 30, n)
+    else:
+        lens = rng.integers(1, 60, n)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(np.arange(max(0, r - 200), min(n, r + 200)), l, replace=False))
+                           for r, l in enumerate(lens)]).astype(np.int32)
+    m = Csr(n, n, off, cols, rng.uniform(-1, 1, off[-1]))
+    x = rng.uniform(-1, 1, n)
+    want = O.spmv(m, x)
+    dh = amg.DeviceHierarchy.from_matrices([m], options={"overlap_test": 1, "dict": 0, "symm": 0})
+    lay = dh.layout(0, "a")
+    assert lay == {"uniform": "sell_uniform", "ragged": "sell_sorted", "padded": "padded", "small": "csr"}[kind]
+    np.testing.assert_array_equal(dh.matrix(0, "a")(x), want)
+    dh.close()
+
+
+@pytest.mark.parametrize("name", ["poisson7_12", "hetero27_10", "elasticity_3_bamg"])
+def test_interior_boundary_split_solve(name):
+    # whole solve with every range-capable matrix split into two launches
+    c = load_case(name)
+    h = c["h"]
+    dh = amg.DeviceHierarchy.from_reference(h, options={"overlap_test": 1, "small_rows_per_sm": 1, "dict": 0})
+    ref = amg.DeviceHierarchy.from_reference(h, options={"small_rows_per_sm": 1, "dict": 0})
+    v = c["vec"]
+    for k in range(h.n_levels - 1):
+        b, x0 = v[f"smooth_L{k}_b"], v[f"smooth_L{k}_x0"]
+        np.testing.assert_array_equal(dh.apply_smoother(k, b, x0, 2), v[f"smooth_L{k}_x0_2"])
+    y = c["y"]
+    np.testing.assert_array_equal(dh.vcycle(y), ref.vcycle(y))
+    if "pcg" in c["expect"]:
+        exp = c["expect"]["pcg"]
+        res = amg.pcg(dh.A0, c["b"], apply_m=dh.vcycle, config=amg.KrylovConfig(rtol=exp["rtol"], max_iters=exp["max_iters"]))
+        assert res.converged and abs(res.n_iterations - exp["n_iterations"]) <= 1 and res.relres <= exp["rtol"]
+    dh.close()
+    ref.close()
