@@ -16,19 +16,27 @@ import numpy as np
 from . import solve as O
 
 
+def _rows(m, lo, hi):
+    """Rows [lo, hi) of a CSR matrix (same column space)."""
+    from paper_2102_07417_b200.problems import Csr
+
+    o = np.asarray(m.row_offsets, dtype=np.int64)
+    return Csr(hi - lo, m.ncols, o[lo:hi + 1] - o[lo], m.col_indices[o[lo]:o[hi]], m.values[o[lo]:o[hi]])
+
+
 class DistOracle:
     def __init__(self, plan, dist):
         self.plan = plan
         self.dist = dist
         self.nl = len(plan.starts)
+        self.split_spmvs = 0  # SpMVs that ran the interior / boundary split
 
     # ---------------------------------------------------------------- comm
-    def exchange(self, lm, x_own):
+    def exchange_begin(self, lm, x_own):
+        """Post the halo receives / sends (non-blocking, as the device's comm stream)."""
         import torch
 
         halo = lm.halo
-        x_ext = np.empty(halo.n_own + halo.n_halo)
-        x_ext[: halo.n_own] = x_own
         reqs, recv_bufs = [], []
         for q, cnt in zip(halo.recv_peers, halo.recv_counts):
             buf = torch.empty(cnt, dtype=torch.float64)
@@ -39,13 +47,23 @@ class DistOracle:
             t = torch.from_numpy(np.ascontiguousarray(x_own[idx]))
             sends.append(t)
             reqs.append(self.dist.isend(t, dst=q))
+        return reqs, recv_bufs, sends
+
+    def exchange_end(self, lm, x_ext, pending):
+        reqs, recv_bufs, _ = pending
         for r in reqs:
             r.wait()
-        pos = halo.n_own
+        pos = lm.halo.n_own
         for buf in recv_bufs:
             x_ext[pos:pos + buf.numel()] = buf.numpy()
             pos += buf.numel()
         return x_ext
+
+    def exchange(self, lm, x_own):
+        halo = lm.halo
+        x_ext = np.empty(halo.n_own + halo.n_halo)
+        x_ext[: halo.n_own] = x_own
+        return self.exchange_end(lm, x_ext, self.exchange_begin(lm, x_own))
 
     def allgather_level(self, k, piece):
         import torch
@@ -71,9 +89,31 @@ class DistOracle:
 
     # ---------------------------------------------------------------- ops
     def spmv(self, k, slot, x_local):
+        """The device's overlap schedule (csrc/capi.cu launch_spmv): interior rows
+        from owned columns while the halo is in flight -- the halo segment holds
+        NaN until it arrives, so an interior row reading it would show -- then
+        the boundary rows [0, lo) + [hi, n)."""
+        from paper_2102_07417_b200.partition import interior_range
+
         lm = self.plan.mats[(k, slot)]
-        x = self.exchange(lm, x_local) if lm.halo is not None else x_local
-        return O.spmv(lm.csr, x)
+        if lm.halo is None:
+            return O.spmv(lm.csr, x_local)
+        halo = lm.halo
+        x_ext = np.full(halo.n_own + halo.n_halo, np.nan)
+        x_ext[: halo.n_own] = x_local
+        pending = self.exchange_begin(lm, x_local)
+        lo, hi = interior_range(lm.csr, halo.n_own)
+        y = np.empty(lm.csr.nrows)
+        if hi > lo:
+            y[lo:hi] = O.spmv(_rows(lm.csr, lo, hi), x_ext)
+            self.split_spmvs += 1
+        self.exchange_end(lm, x_ext, pending)
+        if hi > lo:
+            y[:lo] = O.spmv(_rows(lm.csr, 0, lo), x_ext)
+            y[hi:] = O.spmv(_rows(lm.csr, hi, lm.csr.nrows), x_ext)
+        else:
+            y[:] = O.spmv(lm.csr, x_ext)
+        return y
 
     def smooth(self, k, b, x0, steps):
         kind, omega, inv = self.plan.smoothers[k]

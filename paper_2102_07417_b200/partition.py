@@ -158,6 +158,31 @@ def _localize(m, row_starts, col_starts, rank, replicated_cols):
     return LocalMatrix(Csr(r1 - r0, (c1 - c0) + halo.size, loff, local.astype(np.int32), vals), plan, r0, m.shape)
 
 
+def interior_range(csr, n_own, align=128):
+    """Rows [lo, hi) of a local matrix that touch no halo column (column >= n_own).
+
+    Mirrors ``interior_range`` in csrc/capi.cu: lo = 1 + the last halo-touching
+    row in the first half, hi = the first halo-touching row in the second half,
+    aligned inwards to ``align`` rows; (0, 0) when that leaves fewer than
+    max(align, n / 8) rows.  The device runs the interior rows while the halo
+    is in flight, the boundary rows [0, lo) + [hi, n) after it arrived.
+    """
+    n = csr.nrows
+    offs = np.asarray(csr.row_offsets, dtype=np.int64)
+    rows = np.repeat(np.arange(n), np.diff(offs))
+    touch = np.zeros(n, dtype=bool)
+    touch[rows[np.asarray(csr.col_indices) >= n_own]] = True
+    lo_rows = np.flatnonzero(touch[: n // 2])
+    hi_rows = np.flatnonzero(touch[n // 2:])
+    lo_end = int(lo_rows[-1]) + 1 if lo_rows.size else 0
+    hi_start = int(hi_rows[0]) + n // 2 if hi_rows.size else n
+    a = (lo_end + align - 1) // align * align
+    b = hi_start // align * align
+    if b - a >= align and b - a >= n // 8:
+        return a, b
+    return 0, 0
+
+
 def plan_hierarchy(h, nranks, rank, agglom_rows=4096):
     """Partition plan of ``rank`` for hierarchy ``h`` (identical inputs on every rank).
 

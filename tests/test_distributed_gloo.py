@@ -71,6 +71,7 @@ def _worker(rank, world, port, case, agglom, out_q):
             x, its, relres, conv = D.pcg(b[s0[rank]:s0[rank + 1]])
             res["pcg"] = (its, relres, conv, x)
         res["agglom"] = plan.agglom_level
+        res["split_spmvs"] = D.split_spmvs
         out_q.put(res)
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover - surfaced by the parent
@@ -108,6 +109,8 @@ def test_distributed_plan_matches_single_process(case, world, agglom):
     outs = _run(case, world, agglom)
     for o in outs:
         assert o["ok"], o["msgs"]
+    if case == "poisson7_12" and agglom == 0:  # level 0 blocks large enough for the overlap split
+        assert all(o["split_spmvs"] > 0 for o in outs)
     c = load_case(case)
     if "pcg" in c["expect"]:
         exp = c["expect"]["pcg"]
@@ -122,6 +125,29 @@ def test_distributed_plan_matches_single_process(case, world, agglom):
 
         rel = np.linalg.norm(b - O.spmv(c["h"].levels[0].a, x)) / np.linalg.norm(b)
         assert rel <= exp["rtol"] * 1.0001
+
+
+def test_interior_range_matches_brute_force():
+    # the overlap split (partition.interior_range == csrc interior_range): rows
+    # inside [lo, hi) never touch a halo column, lo / hi are 128-aligned
+    from golden_io import load_case
+    from paper_2102_07417_b200.partition import interior_range, plan_hierarchy
+
+    h = load_case("hetero27_10")["h"]
+    seen = 0
+    for world in (2, 3):
+        for r in range(world):
+            plan = plan_hierarchy(h, world, r, agglom_rows=0)
+            for key, lm in plan.mats.items():
+                if lm.halo is None:
+                    continue
+                lo, hi = interior_range(lm.csr, lm.halo.n_own)
+                assert lo % 128 == 0 and hi % 128 == 0 and lo <= hi
+                o = np.asarray(lm.csr.row_offsets)
+                for row in range(lo, hi):
+                    assert np.all(lm.csr.col_indices[o[row]:o[row + 1]] < lm.halo.n_own)
+                seen += hi > lo
+    assert seen > 0
 
 
 def test_partition_inherits_contiguous_ownership():
