@@ -63,6 +63,20 @@ def lib():
             f"{LIB_PATH} not found: build the CUDA library first "
             "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback"
         )
+    if "AMGB200_NCCL" not in os.environ:
+        # multi-GPU: share torch's NCCL build (the one torch.distributed uses) rather than
+        # whatever libnccl.so.2 the loader would find first (csrc/halo.h)
+        try:
+            import importlib.util
+
+            spec = importlib.util.find_spec("nvidia.nccl")
+            for root in (spec.submodule_search_locations or []) if spec else []:
+                cand = os.path.join(root, "lib", "libnccl.so.2")
+                if os.path.exists(cand):
+                    os.environ["AMGB200_NCCL"] = cand
+                    break
+        except Exception:
+            pass
     L = ctypes.CDLL(LIB_PATH)
     sig = {
         "amg_create": (I32, [I32, I32, I32, P, ctypes.POINTER(P)]),

@@ -196,6 +196,9 @@ struct amg_handle {
     cudaStream_t comm_stream = nullptr;    // nranks > 1: halo send / recv, overlapped with interior rows
     cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
     int overlap_test = 0;                  // nranks == 1 diagnostics: run the interior / boundary split anyway
+    int nccl_selftest = 0;                 // nranks == 1 diagnostics: a one-rank NCCL communicator carries the dot
+                                           // all-gathers and a self send / recv per split SpMV on the comm stream
+    double *selftest_buf = nullptr;
     cudaEvent_t pf_fork = nullptr, pf_join = nullptr;
     PrefetchRange *pf_ranges = nullptr;    // device copy of the tail matrices' ranges
     int pf_n = 0;
@@ -541,6 +544,28 @@ static int exchange(amg_t *h, const DevMat &M, double *x)
 // iteration graph as a fork / join.
 static int exchange_begin(amg_t *h, const DevMat &M, double *x)
 {
+    if (h->nranks == 1 && h->nccl_selftest && h->nccl_selftest != 2 && h->comm.comm) {  // one element to self
+        NcclApi &api = nccl();
+        // 4: p2p on the main stream (no fork / join); 5: fork / join with an empty side kernel, no NCCL
+        cudaStream_t cs = h->nccl_selftest == 4 ? h->stream : h->comm_stream;
+        if (h->nccl_selftest != 4) {
+            CK(cudaEventRecord(h->ev_pack, h->stream));
+            CK(cudaStreamWaitEvent(h->comm_stream, h->ev_pack, 0));
+        }
+        if (h->nccl_selftest == 5) {
+            vec_copy<<<1, 32, 0, h->comm_stream>>>(VecArgs{});
+            CK(cudaGetLastError());
+        } else {
+            ncclResult_t r = api.GroupStart();
+            if (r == ncclSuccess) r = api.Recv(h->selftest_buf, 1, ncclDouble, 0, h->comm.comm, cs);
+            if (r == ncclSuccess) r = api.Send(x, 1, ncclDouble, 0, h->comm.comm, cs);
+            ncclResult_t r2 = api.GroupEnd();
+            if (r != ncclSuccess || r2 != ncclSuccess)
+                return fail(AMG_E_NCCL, std::string("self send/recv: ") + api.GetErrorString(r != ncclSuccess ? r : r2));
+        }
+        if (h->nccl_selftest != 4) CK(cudaEventRecord(h->ev_halo, h->comm_stream));
+        return AMG_OK;
+    }
     if (h->nranks == 1 || M.halo.empty()) return AMG_OK;
     const HaloPlan &P = M.halo;
     NcclApi &api = nccl();
@@ -572,6 +597,10 @@ static int exchange_begin(amg_t *h, const DevMat &M, double *x)
 
 static int exchange_end(amg_t *h, const DevMat &M)
 {
+    if (h->nranks == 1 && h->nccl_selftest && h->nccl_selftest != 2 && h->nccl_selftest != 4 && h->comm.comm) {
+        CK(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+        return AMG_OK;
+    }
     if (h->nranks == 1 || M.halo.empty()) return AMG_OK;
     CK(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
     return AMG_OK;
@@ -1069,9 +1098,17 @@ static int build_graph(amg_t *h)
                 cudaGraph_t out = nullptr;
                 cudaError_t e = cudaStreamEndCapture(h->stream, &out);
                 ok = (s == AMG_OK) && e == cudaSuccess;
+                if (!ok && getenv("AMGB200_DEBUG"))
+                    fprintf(stderr, "amgb200: while-body capture failed: %s / %s\n", cudaGetErrorString(e),
+                            s == AMG_OK ? "" : g_err.c_str());
             }
         }
-        if (ok) ok = cudaGraphInstantiate(&h->gexec, g, 0) == cudaSuccess;
+        if (ok) {
+            cudaError_t e = cudaGraphInstantiate(&h->gexec, g, 0);
+            ok = e == cudaSuccess;
+            if (!ok && getenv("AMGB200_DEBUG"))
+                fprintf(stderr, "amgb200: while-graph instantiate failed: %s\n", cudaGetErrorString(e));
+        }
         if (g) cudaGraphDestroy(g);
         cudaGetLastError();
         if (ok) {
@@ -1118,7 +1155,7 @@ static int build_tail(amg_t *h)
 {
     const int nl = (int)h->lv.size();
     h->tail_level = 0;
-    if (h->tail_nnz <= 0 || nl < 2 || h->nranks > 1) return AMG_OK;
+    if (h->tail_nnz <= 0 || nl < 2) return AMG_OK;
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
     // CTA 0 of the tail stages v, tmp, 1/L_ii and the packed factor (not the pre-scaled blocks)
@@ -1138,6 +1175,13 @@ static int build_tail(amg_t *h)
     for (int kt = nl - 1; kt >= 1; --kt) {
         if (h->lv[kt].m[AMG_A].nnz > h->tail_nnz) break;
         kstart = kt;
+    }
+    // multi-GPU: the tail holds replicated levels only (every rank runs the same
+    // tail on its own full copy; no halo or collective inside the cluster kernel)
+    if (h->nranks > 1) {
+        if (h->agglom_level < 1 || kstart == 0) return AMG_OK;
+        kstart = std::max(kstart, h->agglom_level);
+        if (kstart >= nl) return AMG_OK;
     }
     for (int kt = kstart; kt >= 1 && kt < nl && best == 0; ++kt) {
         std::vector<TailOp> ops;
@@ -1394,6 +1438,7 @@ void amg_destroy(amg_t *h)
         F(L.inv_diag); F(L.y); F(L.x); F(L.r); F(L.t);
     }
     F(h->pf_ranges);
+    F(h->selftest_buf);
     if (h->side) cudaStreamDestroy(h->side);
     if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
     if (h->ev_pack) cudaEventDestroy(h->ev_pack);
@@ -1430,6 +1475,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "symm") { h->symm = value ? 1 : 0; return AMG_OK; }
     if (k == "dict") { h->dict = value ? 1 : 0; return AMG_OK; }
     if (k == "overlap_test") { h->overlap_test = value ? 1 : 0; return AMG_OK; }
+    if (k == "nccl_selftest") { h->nccl_selftest = (int)value; return AMG_OK; }
     if (k == "sells") { h->sells = (int)value; return AMG_OK; }
     if (k == "sells_max_rows") { h->sells_max_rows = value; return AMG_OK; }
     if (k == "sells_buckets") { h->sells_buckets = (int)value; return AMG_OK; }
@@ -2002,6 +2048,22 @@ int amg_finalize(amg_t *h)
         if (h->agglom_level < 0 || h->agglom_level > nl - 1)
             return fail(AMG_E_STATE, "multi-GPU: amg_set_agglomeration must name a level <= the coarsest (replicated) level");
         h->dist_dots = h->agglom_level > 0;
+    }
+    if (h->nranks == 1 && h->nccl_selftest && !container) {
+        // one-rank communicator: proves the NCCL calls of the multi-GPU path (dot
+        // all-gathers, p2p on the comm stream with its fork / join) are captured
+        // into the conditional WHILE body on this NCCL build
+        NcclApi &api = nccl();
+        if (!api.loaded) return fail(AMG_E_NCCL, "libnccl.so.2 could not be loaded");
+        ncclUniqueId id;
+        ncclResult_t r = api.GetUniqueId(&id);
+        if (r != ncclSuccess) return fail(AMG_E_NCCL, std::string("ncclGetUniqueId: ") + api.GetErrorString(r));
+        if (comm_init(h->comm, &id, 0, 1) != 0 || !h->comm.comm) {
+            r = api.CommInitRank(&h->comm.comm, 1, id, 0);
+            if (r != ncclSuccess) return fail(AMG_E_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r));
+        }
+        h->dist_dots = h->nccl_selftest != 3;  // 3: p2p only, 2: dots only, 1: both
+        TRY(dalloc(&h->selftest_buf, 2));
     }
     // structural checks mirroring the Level / AmgHierarchy contract
     for (int k = 0; k < nl && !container; ++k) {

@@ -11,6 +11,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <string>
 #include <vector>
@@ -43,10 +44,14 @@ inline NcclApi &nccl()
 {
     static NcclApi api;
     if (api.loaded) return api;
+    // AMGB200_NCCL: an explicit library (the Python shim points it at the NCCL
+    // that torch ships, so both share one NCCL build); else the loader's choice
+    const char *env = getenv("AMGB200_NCCL");
+    if (env && *env) api.lib = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
     const char *names[] = {"libnccl.so.2", "libnccl.so"};
     for (const char *n : names) {
-        api.lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
         if (api.lib) break;
+        api.lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
     }
     if (!api.lib) return api;
 #define AMG_SYM(F) api.F = reinterpret_cast<decltype(api.F)>(dlsym(api.lib, "nccl" #F))

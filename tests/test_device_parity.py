@@ -592,3 +592,29 @@ def test_interior_boundary_split_solve(name):
         assert res.converged and abs(res.n_iterations - exp["n_iterations"]) <= 1 and res.relres <= exp["rtol"]
     dh.close()
     ref.close()
+
+
+@pytest.mark.parametrize("mode,while_graph", [(2, True), (5, True), (3, False), (4, False), (1, False)])
+def test_nccl_calls_in_the_pcg_graph(mode, while_graph):
+    # multi-GPU readiness on one GPU: a one-rank NCCL communicator carries
+    #   2: the dot all-gathers (FIN_LOCAL + ncclAllGather + fin_ranks),
+    #   3: a self send / recv on the comm stream (fork / join events) per split SpMV,
+    #   4: the same p2p on the main stream, 1: both, 5: the fork / join alone.
+    # Measured on NCCL 2.28.9: collectives and stream forks capture into the
+    # conditional WHILE body (graph_mode 2); point-to-point does not instantiate
+    # there, and the solve falls back to one graph launch per iteration
+    # (graph_mode 1) -- with the same bits either way.
+    c = load_case("poisson7_12")
+    h = c["h"]
+    base = {"overlap_test": 1, "small_rows_per_sm": 1, "dict": 0}
+    d0 = amg.DeviceHierarchy.from_reference(h, options=base)
+    d1 = amg.DeviceHierarchy.from_reference(h, options={**base, "nccl_selftest": mode})
+    cfg = amg.KrylovConfig(rtol=1e-10, record_history=True)
+    r0 = amg.pcg(d0.A0, c["b"], apply_m=d0.vcycle, config=cfg)
+    r1 = amg.pcg(d1.A0, c["b"], apply_m=d1.vcycle, config=cfg)
+    assert d1.stats()["graph_mode"] == (2 if while_graph else 1)
+    assert r1.converged and r1.n_iterations == r0.n_iterations
+    np.testing.assert_array_equal(r1.x, r0.x)
+    assert r1.history == r0.history
+    d0.close()
+    d1.close()
