@@ -11,6 +11,9 @@ the reference; its output is uploaded once::
     res = amgb200.pcg(dh.A0, b, apply_m=dh.vcycle,
                       config=amgb200.KrylovConfig(rtol=1e-8))  # whole solve on the GPU
 
+Several GPUs from one process: ``cl = amgb200.DeviceClique(h, devices=[0, 1])``
+then ``amgb200.pcg(cl.A0, b, apply_m=cl.vcycle)``.
+
 Reference names mirrored: ``pcg``, ``KrylovConfig``, ``KrylovResult``,
 ``vcycle``, ``spmv``, ``apply_smoother``, ``AmgError``,
 ``DimensionMismatchError``, ``NotSpdError``.
@@ -18,6 +21,7 @@ Reference names mirrored: ``pcg``, ``KrylovConfig``, ``KrylovResult``,
 from .errors import AmgError, BreakdownError, DimensionMismatchError, NotSpdError  # noqa: F401
 from .device import DeviceHierarchy, DeviceMatrix, DeviceVcycle, model_bytes_flops  # noqa: F401
 from .krylov import KrylovConfig, KrylovResult, bicgstab, pcg  # noqa: F401
+from .clique import DeviceClique  # noqa: F401
 from .ops import apply_smoother, coarse_solve, spmv, vcycle  # noqa: F401
 
 __version__ = "0.1.0"

@@ -2207,7 +2207,10 @@ __host__ __device__ inline int tail_region_bytes(int rows_cap, int nnz_cap)
     return ob + cb + nnz_cap * 8;
 }
 
-constexpr int TAIL_THREADS = 512;
+#ifndef AMG_TAIL_THREADS
+#define AMG_TAIL_THREADS 512
+#endif
+constexpr int TAIL_THREADS = AMG_TAIL_THREADS;
 constexpr int TAIL_MAX_OPS = 96;    // ops per tail (8 per level + coarse): up to 11 levels
 constexpr int TAIL_MAX_MATS = 64;
 constexpr int TAIL_MAX_DINV = 512;

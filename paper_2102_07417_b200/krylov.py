@@ -50,6 +50,13 @@ def pcg(apply_a, b, apply_m=None, x0=None, config=None):
     Raises :class:`NotSpdError` (message contains "curvature") on a
     non-positive curvature, exactly as the reference.
     """
+    from .clique import _CliqueOp
+
+    if isinstance(apply_a, _CliqueOp):
+        if apply_a.kind != "A0" or not isinstance(apply_m, _CliqueOp) or apply_m.kind != "vcycle" or \
+                apply_m.clique is not apply_a.clique:
+            raise TypeError("pcg: a DeviceClique solve takes cl.A0 and cl.vcycle of the same clique")
+        return apply_a.clique.pcg(b, x0=x0, config=config)
     if not isinstance(apply_a, DeviceMatrix) or apply_a.level != 0 or apply_a.slot != "a":
         raise TypeError("pcg: apply_a must be DeviceHierarchy.A0 (no CPU fallback)")
     if not isinstance(apply_m, DeviceVcycle) or apply_m.dh is not apply_a.dh:

@@ -78,8 +78,12 @@ def level_table(h):
     return rows
 
 
-def run_solve(a, b, cfg=None, coords=None, hierarchy=None, device=0, options=None):
-    """Set up (reference) and solve (device); returns ``(result, report, hierarchy)``."""
+def run_solve(a, b, cfg=None, coords=None, hierarchy=None, device=0, options=None, devices=None):
+    """Set up (reference) and solve (device); returns ``(result, report, hierarchy)``.
+
+    ``devices`` (a list of GPU ids, PCG only): the rows are partitioned over
+    those GPUs in this one process (:class:`clique.DeviceClique`).
+    """
     from . import krylov
     from .device import DeviceHierarchy
 
@@ -105,7 +109,14 @@ def run_solve(a, b, cfg=None, coords=None, hierarchy=None, device=0, options=Non
         full.update({k: v for k, v in c.items() if k in full})
         h = setup(a, _amg_config(full, coords=coords))
     t1 = time.perf_counter()
-    dh = DeviceHierarchy.from_reference(h, device=device, options=options)
+    if devices is not None and len(devices) > 1:
+        if method != "pcg":
+            raise AmgError("run_solve: multi-GPU solves are PCG only")
+        from .clique import DeviceClique
+
+        dh = DeviceClique(h, devices, options=options)
+    else:
+        dh = DeviceHierarchy.from_reference(h, device=device if not devices else devices[0], options=options)
     kcfg = krylov.KrylovConfig(rtol=float(c["solver.rtol"]), max_iters=int(c["solver.max_iters"]),
                                record_history=True)
     solver = krylov.pcg if method == "pcg" else krylov.bicgstab
@@ -164,6 +175,7 @@ def main(argv=None):
     sp.add_argument("--format", default="text", choices=("text", "json", "csv"))
     sp.add_argument("--history", help="write the residual history CSV here")
     sp.add_argument("--device", type=int, default=0)
+    sp.add_argument("--devices", help="comma-separated GPU ids: partition the solve over them (one process)")
     args = ap.parse_args(argv)
     try:
         h = hiercache.load_hierarchy(args.cache)
@@ -172,7 +184,8 @@ def main(argv=None):
             h.levels[0].a.nrows)
         _, report, _ = run_solve(h.levels[0].a, b, {"solver.method": args.method, "solver.rtol": args.rtol,
                                                      "solver.max_iters": args.max_iters},
-                                 hierarchy=h, device=args.device)
+                                 hierarchy=h, device=args.device,
+                                 devices=[int(d) for d in args.devices.split(",")] if args.devices else None)
     except (AmgError, OSError, ValueError) as exc:
         print(f"error: {exc}", file=sys.stderr)
         return 1

@@ -618,3 +618,21 @@ def test_nccl_calls_in_the_pcg_graph(mode, while_graph):
     assert r1.history == r0.history
     d0.close()
     d1.close()
+
+
+def test_single_process_clique_one_device(cases):
+    # DeviceClique (N GPUs from one process, one thread per GPU inside amg_pcg):
+    # with one device the plan path must give the direct upload's bits
+    c, dh = _dh("poisson7_12", cases)
+    cl = amg.DeviceClique(c["h"], devices=[0])
+    cfg = amg.KrylovConfig(rtol=1e-10, record_history=True)
+    r1 = amg.pcg(dh.A0, c["b"], apply_m=dh.vcycle, config=cfg)
+    r2 = amg.pcg(cl.A0, c["b"], apply_m=cl.vcycle, config=cfg)
+    np.testing.assert_array_equal(r1.x, r2.x)
+    assert r1.history == r2.history
+    y = c["y"]
+    np.testing.assert_array_equal(cl.vcycle(y), dh.vcycle(y))
+    np.testing.assert_array_equal(cl.A0(y), dh.A0(y))
+    with pytest.raises(TypeError):
+        amg.pcg(cl.A0, c["b"], apply_m=dh.vcycle)
+    cl.close()
