@@ -268,7 +268,9 @@ struct amg_handle {
     int64_t tail_nnz = 300000;   // levels whose A_k has at most this many entries run in the cluster tail
     int tail_stage = 0;          // stage tail matrices in smem (measured slower on B200: the big smem
                                  // footprint delays the cluster launch; streamed from L2 by default)
-    int cluster = 16;
+    int cluster = 16;             // CTAs of the tail: one cluster, or (tail_grid) the cooperative grid
+    int tail_grid = 0;            // tail on a cooperative grid of every SM (grid barriers) instead of one cluster
+    unsigned *tail_gbar = nullptr;
     int coarse_pipe = 1;          // pipelined per-warp Cholesky substitution
     int side_prefetch = 1;        // side-stream L2 prefetch of the tail matrices during the level above it
     int tail_pcap = 16384;        // tail product buffer (entries); larger per-CTA blocks are processed in chunks
@@ -926,10 +928,15 @@ static int launch_tail(amg_t *h, const int *g1)
     cfg.dynamicSmemBytes = h->tail_smem;
     cfg.stream = h->stream;
     cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)h->cluster;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    if (h->tail_grid) {  // every CTA co-resident: grid barriers inside
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+    } else {
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)h->cluster;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+    }
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
@@ -937,7 +944,8 @@ static int launch_tail(amg_t *h, const int *g1)
     const TailVecs tv{h->tail_vecs, h->tail_nvecs, h->tail_pcap_used};
     cudaError_t e = cudaLaunchKernelEx(&cfg, tail_vcycle, (const TailOp *)h->tail_ops, h->tail_nops,
                                        (const TailMat *)h->tail_mats, h->tail_nmats, (const int32_t *)h->tail_splits,
-                                       h->tail_prod_off, coarse_args(h), g1, h->trace, tv);
+                                       h->tail_prod_off, coarse_args(h), g1, h->trace, tv,
+                                       h->tail_grid ? h->tail_gbar : (unsigned *)nullptr);
     if (e != cudaSuccess) return fail(AMG_E_CUDA, std::string("tail launch failed: ") + cudaGetErrorString(e));
     ++h->launches;
     return AMG_OK;
@@ -1281,7 +1289,13 @@ static int build_tail(amg_t *h)
     if (best == 0) return AMG_OK;
     TRY(raise_smem_caps(h->device));
     int nclusters = 0;
-    {
+    if (h->tail_grid) {
+        int nb = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)tail_vcycle, TAIL_THREADS, best_smem));
+        nclusters = (int64_t)nb * h->sm_count >= h->cluster ? 1 : 0;  // the whole grid co-resident
+        if (nclusters) TRY(dalloc(&h->tail_gbar, 2));
+        if (nclusters) CK(cudaMemset(h->tail_gbar, 0, 2 * sizeof(unsigned)));
+    } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)h->cluster);
         cfg.blockDim = dim3(TAIL_THREADS);
@@ -1298,7 +1312,7 @@ static int build_tail(amg_t *h)
     }
     if (nclusters < 1) return AMG_OK;  // cluster shape not resident here: per-op kernels are used
     for (auto &o : best_ops) o.xs = o.ys = o.bs = -1;
-    if (h->tail_dsm) {
+    if (h->tail_dsm && !h->tail_grid) {
         // level vectors below the tail's entry / exit (y, x of its first level stay in global memory)
         struct V { const double *p; int shift; int off; };
         std::vector<V> vs;
@@ -1439,6 +1453,7 @@ void amg_destroy(amg_t *h)
     }
     F(h->pf_ranges);
     F(h->selftest_buf);
+    F(h->tail_gbar);
     if (h->side) cudaStreamDestroy(h->side);
     if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
     if (h->ev_pack) cudaEventDestroy(h->ev_pack);
@@ -1467,6 +1482,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (h->finalized) return fail(AMG_E_STATE, "amg_set_option: '" + k + "' must be set before amg_finalize");
     if (k == "tail_nnz") { h->tail_nnz = value; return AMG_OK; }
     if (k == "tail_stage") { h->tail_stage = value ? 1 : 0; return AMG_OK; }
+    if (k == "tail_grid") { h->tail_grid = value ? 1 : 0; return AMG_OK; }
     if (k == "cluster") { if (value != 8 && value != 16 && value != 4 && value != 2 && value != 1) return fail(AMG_E_ARG, "cluster must be 1,2,4,8,16"); h->cluster = (int)value; return AMG_OK; }
     if (k == "pad_min") { h->pad_min = (int)value; return AMG_OK; }
     if (k == "long_avg") { h->long_avg = (int)value; return AMG_OK; }
@@ -2511,6 +2527,7 @@ int amg_finalize(amg_t *h)
     TRY(dalloc(&h->ctl, 1));
     CK(cudaMallocHost((void **)&h->ctl_h, sizeof(PcgCtl)));
     std::memset(h->ctl_h, 0, sizeof(PcgCtl));
+    if (h->tail_grid) h->cluster = h->sm_count;  // one CTA per SM (512 threads x 128 registers fill an SM)
     if (!container) TRY(build_tail(h));
     h->finalized = true;
     CK(cudaDeviceSynchronize());

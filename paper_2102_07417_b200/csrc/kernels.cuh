@@ -2220,6 +2220,38 @@ __device__ __forceinline__ void cluster_barrier()
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// Grid-wide barrier of a cooperative (co-resident) tail grid: arrival count +
+// generation word, release by the last CTA, acquire spin by the others.
+__device__ __forceinline__ void grid_sync(unsigned *bar)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned g;
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+        __threadfence();
+        const unsigned a = atomicAdd(bar, 1u);
+        if (a == gridDim.x - 1) {
+            bar[0] = 0u;  // nobody arrives again before the generation flips
+            __threadfence();
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
+        } else {
+            unsigned c;
+            do {
+                asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(c) : "l"(bar + 1) : "memory");
+            } while (c == g);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// tail synchronisation: one cluster (barrier.cluster) or a cooperative grid (gbar)
+__device__ __forceinline__ void tail_sync(unsigned *gbar)
+{
+    if (gbar) grid_sync(gbar);
+    else cluster_barrier();
+}
+
 __device__ __forceinline__ unsigned cluster_rank()
 {
     unsigned r;
@@ -2339,7 +2371,8 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
                                                              const TailMat *__restrict__ mats, int nmats,
                                                              const int32_t *__restrict__ splits, int prod_off,
                                                              const CoarseArgs c, const int *gate1,
-                                                             unsigned long long *trace, const TailVecs tvv)
+                                                             unsigned long long *trace, const TailVecs tvv,
+                                                             unsigned *gbar)
 {
     __shared__ int2 s_vec[TAIL_MAX_VECS];
     for (int i = threadIdx.x; i < tvv.nslots; i += blockDim.x) s_vec[i] = tvv.slot[i];
@@ -2349,7 +2382,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
     __shared__ int s_geo[TAIL_MAX_MATS][3];
     char *smem = reinterpret_cast<char *>(sh);
     double *ps = reinterpret_cast<double *>(smem + prod_off);  // product buffer
-    const unsigned rank = cluster_rank();
+    const unsigned rank = gbar ? blockIdx.x : cluster_rank();
     // ---- stage static data (before waiting on the predecessor)
     const double *L = c.Lp, *D = c.dinv, *MN = c.mn;
     double *ctmp = sh + ((c.n + 1) & ~1);
@@ -2435,7 +2468,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
                 case EPI_SETW: tail_spmv_streamed<EPI_SETW>(o, M, r0, r1, ps, s_vec, smem, tvv.pcap); break;
                 default: tail_spmv_streamed<EPI_ADD>(o, M, r0, r1, ps, s_vec, smem, tvv.pcap); break;
                 }
-                cluster_barrier();
+                tail_sync(gbar);
                 if (trace && t0 == 0) trace[i + 1] = globaltimer();
                 continue;
             }
@@ -2463,7 +2496,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) tail_vcycle(const TailOp *__rest
             else lu_solve_cta(c.n, c.LU, c.piv, v);
             for (int r = threadIdx.x; r < c.n; r += blockDim.x) tv_st(o.y, o.ys, r, v[r], s_vec, smem);
         }
-        cluster_barrier();
+        tail_sync(gbar);
         if (trace && t0 == 0) trace[i + 1] = globaltimer();
     }
 }
