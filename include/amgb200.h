@@ -166,7 +166,8 @@ enum {
     AMG_LAYOUT_SELL_UNIFORM = 8, /* SELL-32, every slice the same width (short rows) */
     AMG_LAYOUT_SELL_SORTED = 9,  /* SELL-32 over rows sorted by length in windows (SELL-C-sigma) */
     AMG_LAYOUT_SPLIT = 10,       /* rows <= 16 entries as width-16 SELL-32, longer rows from a row list */
-    AMG_LAYOUT_DICT = 11         /* row-class dictionary: class id per row + (offsets, values) table */
+    AMG_LAYOUT_DICT = 11,        /* row-class dictionary: class id per row + (offsets, values) table */
+    AMG_LAYOUT_WCSR = 12         /* CSR, one warp per 32 consecutive rows (coalesced entries, products in smem) */
 };
 int amg_matrix_layout(amg_t *h, int level, int which, int *layout);
 /* Diagnostics (roofline numerator): *stored = bytes the SpMV kernel of the

@@ -94,12 +94,13 @@ struct DevMat {
     double *lsum = nullptr;
     int nleaves = 0, leaf_grid = 0, leafsum_grid = 0;
     HaloPlan halo;  // exchange feeding this matrix's halo columns (nranks > 1)
-    int64_t lbytes[12] = {};  // per layout: bytes its kernel must stream (values, indices, row metadata)
+    int64_t lbytes[16] = {};  // per layout: bytes its kernel must stream (values, indices, row metadata)
     int64_t int_lo = 0, int_hi = 0;  // interior rows [int_lo, int_hi): no halo column (overlap split), 128-aligned
     void *dcls = nullptr;     // row-class dictionary (spmv_dict): class id per row, nullptr if unused
     int32_t *dbeg = nullptr, *drel = nullptr;
     double *dval = nullptr;
     int dncls = 0, dnent = 0, dwide = 0, dfl = 0, dgrid = 0;
+    int wcsr = 0, wcsr_grid = 0;  // warp-cooperative CSR (spmv_wcsr) on the uploaded arrays
 };
 
 struct LevelD {
@@ -254,6 +255,7 @@ struct amg_handle {
                                   // measured slower than the round-by-round kernel on config 2), 0 off
     int symm = 1;                 // symmetric stencil layout (upper diagonals) for bitwise-symmetric pattern operators
     int dict = 1;                 // row-class dictionary layout for operators with few distinct rows
+    int wcsr = 1;                 // large matrices averaging >= pad_min entries: warp-cooperative CSR instead of the padded copy
     int sell = 1;                 // SELL-32 slices where padding <= sell_pad %
     int gated_grid = 1;           // CTAs per SM for the rarely active gated residual SpMVs (0 = full grid)
     int grid_per_sm = 0;          // cap on SpMV CTAs per SM (0 = occupancy)
@@ -371,6 +373,19 @@ static SpmvSellUFn spmv_sellu_fn(int epi, int W, bool plen = false)
     default: AMG_U(EPI_ADD)
     }
 #undef AMG_U
+}
+
+typedef void (*SpmvWcsrFn)(const SpmvArgs, int);
+
+static SpmvWcsrFn spmv_wcsr_fn(int epi)
+{
+    switch (epi) {
+    case EPI_PLAIN: return spmv_wcsr<EPI_PLAIN>;
+    case EPI_RESID: return spmv_wcsr<EPI_RESID>;
+    case EPI_AXPYW: return spmv_wcsr<EPI_AXPYW>;
+    case EPI_SETW: return spmv_wcsr<EPI_SETW>;
+    default: return spmv_wcsr<EPI_ADD>;
+    }
 }
 
 typedef void (*SpmvDictFn)(const SpmvArgs, const DictArgs, int);
@@ -652,6 +667,7 @@ static int layout_of(const amg_t *h, const DevMat &M)
               : M.sbeg                ? (M.scol ? AMG_LAYOUT_SELL : AMG_LAYOUT_SELL_PAT)
               : (M.pid && M.pstart)   ? AMG_LAYOUT_PATTERN
               : M.leaf                ? AMG_LAYOUT_LEAVES
+              : M.wcsr                ? AMG_LAYOUT_WCSR
               : M.pstart              ? AMG_LAYOUT_PADDED
                                       : AMG_LAYOUT_CSR;
 }
@@ -660,7 +676,7 @@ static int layout_of(const amg_t *h, const DevMat &M)
 static bool range_layout(int lay)
 {
     return lay == AMG_LAYOUT_SELL_SORTED || lay == AMG_LAYOUT_SELL_UNIFORM || lay == AMG_LAYOUT_PADDED ||
-           lay == AMG_LAYOUT_CSR;
+           lay == AMG_LAYOUT_WCSR || lay == AMG_LAYOUT_CSR;
 }
 
 // One launch over `count` virtual rows (a.rlo / a.rsplit / a.rgap map them);
@@ -681,6 +697,9 @@ static int spmv_range(amg_t *h, const DevMat &M, int lay, const SpmvArgs &a, int
         SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW};
         g = cap(M.u_grid, (count + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS);
         TRY(launch_k(h, spmv_sellu_fn(epi, M.uW, M.u_plen), g, VEC_SPMV_THREADS, 0, a, ua, count));
+    } else if (lay == AMG_LAYOUT_WCSR) {
+        g = cap(M.wcsr_grid, ((count + 31) / 32 + WCSR_THREADS / 32 - 1) / (WCSR_THREADS / 32));
+        TRY(launch_k(h, spmv_wcsr_fn(epi), g, WCSR_THREADS, 0, a, count));
     } else if (lay == AMG_LAYOUT_PADDED) {
         PadArgs pa{M.pstart, M.pval, M.pcol};
         g = cap(M.pad_grid, (count + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS);
@@ -828,6 +847,9 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         TRY(launch_k(h, spmv_leaves, grid_cap ? std::min(grid_cap, M.leaf_grid) : M.leaf_grid, DIRECT_THREADS, 0, a1, la));
         TRY(launch_k(h, spmv_leafsum_fn(epi), grid_cap ? std::min(grid_cap, M.leafsum_grid) : M.leafsum_grid,
                      DIRECT_THREADS, 0, a, la, (int)M.nrows));
+    } else if (M.wcsr) {
+        TRY(launch_k(h, spmv_wcsr_fn(epi), grid_cap ? std::min(grid_cap, M.wcsr_grid) : M.wcsr_grid, WCSR_THREADS, 0, a,
+                     (int)M.nrows));
     } else if (M.pstart) {
         PadArgs pa{M.pstart, M.pval, M.pcol};
         TRY(launch_k(h, spmv_vec_fn(epi, h->vec_minb), grid_cap ? std::min(grid_cap, M.pad_grid) : M.pad_grid, VEC_SPMV_THREADS, 0, a,
@@ -1490,6 +1512,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
     if (k == "symm") { h->symm = value ? 1 : 0; return AMG_OK; }
     if (k == "dict") { h->dict = value ? 1 : 0; return AMG_OK; }
+    if (k == "wcsr") { h->wcsr = value ? 1 : 0; return AMG_OK; }
     if (k == "overlap_test") { h->overlap_test = value ? 1 : 0; return AMG_OK; }
     if (k == "nccl_selftest") { h->nccl_selftest = (int)value; return AMG_OK; }
     if (k == "sells") { h->sells = (int)value; return AMG_OK; }
@@ -2200,6 +2223,16 @@ int amg_finalize(amg_t *h)
                     CK(cudaMemcpy(col_h.data(), M.col, M.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
                     CK(cudaMemcpy(val_h.data(), M.val, M.nnz * sizeof(double), cudaMemcpyDeviceToHost));
                 }
+                if (h->wcsr) {
+                    // warp-cooperative CSR on the uploaded arrays (no padded copy)
+                    M.wcsr = 1;
+                    int nbw = 0;
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbw, (const void *)spmv_wcsr<EPI_RESID>, WCSR_THREADS, 0));
+                    M.wcsr_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + WCSR_THREADS - 1) / WCSR_THREADS,
+                                                                             (int64_t)h->sm_count * std::max(nbw, 1)));
+                    h->max_grid = std::max(h->max_grid, M.wcsr_grid);
+                    M.lbytes[AMG_LAYOUT_WCSR] = M.nnz * 12 + (M.nrows + 1) * 4;
+                } else {
                 std::vector<int32_t> ps(M.nrows + 1);
                 int64_t pos = 3;
                 for (int64_t r = 0; r < M.nrows; ++r) {
@@ -2225,6 +2258,7 @@ int amg_finalize(amg_t *h)
                 CK(cudaMemcpy(M.pstart, ps.data(), ps.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
                 CK(cudaMemcpy(M.pcol, pc.data(), pc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
                 CK(cudaMemcpy(M.pval, pv.data(), pv.size() * sizeof(double), cudaMemcpyHostToDevice));
+                }
                 // stencil patterns: every row's (col - row) tuple from a small dictionary
                 if (h->patterns && h->nranks == 1 && M.ncols == M.nrows) {
                     std::vector<int32_t> rel, beg;

@@ -1429,6 +1429,145 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, MINB) spmv_symd_fixed(const 
     }
 }
 
+// ---------------------------------------------------------------- SpMV, warp-cooperative CSR
+
+// Plain CSR (no extra copy), one warp per group of 32 consecutive rows: the
+// group's entries [off[r0], off[r0 + 32]) are contiguous, so the warp streams
+// values and columns with fully coalesced loads (lane-strided entries, all of
+// a lane's loads issued before the first gather), gathers x, and parks the
+// products in a per-warp shared-memory buffer; then lane l sums row r0 + l
+// from the buffer in the reference order (row_sum_staged: p0 + numpy
+// pairwise).  Versus one lane per row walking its own row, every warp-level
+// load touches 1-2 lines instead of ~32, and no padding is moved.  Groups
+// with more than WCSR_BUF entries go through the buffer in row chunks.
+constexpr int WCSR_THREADS = 256;
+constexpr int WCSR_BUF = 640;   // products per warp (5.3 KB with the skew; 8 warps = 42 KB per CTA)
+// buffer slot of product k: one pad slot every 16 (rows starting 16 products
+// apart -- the same bank -- land on different banks when lanes sum their rows)
+__device__ __forceinline__ int wslot(int k) { return k + (k >> 4); }
+constexpr int WCSR_UNROLL = 10; // entries per lane issued together (one pass of a <= 320-entry group)
+
+// reference row sum (p0 + numpy pairwise) of the products in skewed slots [lo, hi)
+__device__ __forceinline__ double wcsr_row_sum(const double *ps, int lo, int hi)
+{
+    auto P = [&](int k) -> double { return ps[wslot(k)]; };
+    const int n = hi - lo - 1;
+    if (n < 0) return 0.0;
+    return add(P(lo), n <= 128 ? pairwise_leaf(P, lo + 1, n) : pairwise_sum(P, lo + 1, n));
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(WCSR_THREADS, 3) spmv_wcsr(const SpmvArgs a, int nrows)
+{
+    __shared__ double red[WCSR_THREADS / 32];
+    __shared__ double buf[WCSR_THREADS / 32][WCSR_BUF + WCSR_BUF / 16];
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *ps = buf[warp];
+    const int ngroups = (nrows + 31) >> 5;
+    const int gstride = gridDim.x * (WCSR_THREADS / 32);
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    const int32_t *__restrict__ off = a.off;
+    const int32_t *__restrict__ col = a.col;
+    const double *__restrict__ val = a.val;
+    const double *__restrict__ x = a.x;
+    double dacc = 0.0;
+    int g = blockIdx.x * (WCSR_THREADS / 32) + warp;
+    // offsets of this lane's row, one group ahead
+    int nlo = 0, nhi = 0, nrow = -1;
+    auto fetch = [&](int gg) {
+        const int v = gg * 32 + lane;
+        nrow = v < nrows ? vrow(a, v) : -1;
+        if (nrow >= 0) {
+            nlo = __ldg(off + nrow);
+            nhi = __ldg(off + nrow + 1);
+        } else {
+            nlo = nhi = -1;
+        }
+    };
+    if (g < ngroups) fetch(g);
+    for (; g < ngroups; g += gstride) {
+        const int row = nrow;
+        const int lo = nlo, hi = nhi;
+        if (g + gstride < ngroups) fetch(g + gstride);
+        double bv = 0.0, wv = 0.0;
+        if (row >= 0) {
+            if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
+            if (want_dot && !self_dot) wv = a.dotw[row];
+        }
+        // group entry range: rows of a group are consecutive (range starts are 128-aligned)
+        const int k0 = __shfl_sync(0xffffffffu, lo, 0);
+        int last = 31;
+        {
+            const unsigned live = __ballot_sync(0xffffffffu, row >= 0);
+            last = 31 - __clz(live);
+        }
+        const int k1 = __shfl_sync(0xffffffffu, hi, last);
+        double sum = 0.0;
+        if (k1 - k0 <= WCSR_BUF) {
+            const int nk = k1 - k0;
+            for (int kb = 0; kb < nk; kb += 32 * WCSR_UNROLL) {
+                double pv[WCSR_UNROLL];
+                int pc[WCSR_UNROLL];
+                // clamped (not predicated) loads keep pv / pc in registers
+#pragma unroll
+                for (int u = 0; u < WCSR_UNROLL; ++u) {
+                    const int k = min(kb + u * 32 + lane, nk - 1);
+                    pv[u] = __ldg(val + k0 + k);
+                    pc[u] = __ldg(col + k0 + k);
+                }
+#pragma unroll
+                for (int u = 0; u < WCSR_UNROLL; ++u) {
+                    const double xv = __ldg(x + pc[u]);
+                    const int k = kb + u * 32 + lane;
+                    if (k < nk) ps[wslot(k)] = prod(pv[u], xv);
+                }
+            }
+            __syncwarp();
+            if (row >= 0) sum = wcsr_row_sum(ps, lo - k0, hi - k0);
+            __syncwarp();
+        } else {
+            // a heavy group: its rows through the buffer in chunks of whole rows
+            // (a single row longer than the buffer sums straight from global memory)
+            int rs = 0;  // first lane of the chunk
+            while (rs <= last) {
+                const int ks = __shfl_sync(0xffffffffu, lo, rs);
+                int re = rs;  // chunk = lanes [rs, re]
+                while (re < last && __shfl_sync(0xffffffffu, hi, re + 1) - ks <= WCSR_BUF) ++re;
+                const int ke = __shfl_sync(0xffffffffu, hi, re);
+                if (ke - ks <= WCSR_BUF) {
+                    for (int k = lane; k < ke - ks; k += 32) ps[wslot(k)] = prod(__ldg(val + ks + k), __ldg(x + __ldg(col + ks + k)));
+                    __syncwarp();
+                    if (lane >= rs && lane <= re && row >= 0) sum = wcsr_row_sum(ps, lo - ks, hi - ks);
+                    __syncwarp();
+                } else if (lane == rs && row >= 0) {
+                    auto P = [&](int k) -> double { return prod(__ldg(val + k), __ldg(x + __ldg(col + k))); };
+                    const int n = hi - lo - 1;
+                    sum = n < 0 ? 0.0 : add(P(lo), pairwise_sum(P, lo + 1, n));
+                }
+                rs = re + 1;
+            }
+        }
+        if (row >= 0) {
+            double yv;
+            if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+            else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+            else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+            else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+            else yv = sum;
+            a.y[row] = yv;
+            if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
+        }
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v = block_sum<WCSR_THREADS>(dacc, red);
+        spmv_finalize<WCSR_THREADS>(v, a);
+    }
+}
+
 // ---------------------------------------------------------------- SpMV, row-class dictionary
 
 // Operators whose rows fall into few distinct (column-offset tuple, value

@@ -334,7 +334,7 @@ class DeviceHierarchy:
     def set_option(self, key, value):
         C.check(C.lib().amg_set_option(self._h, key.encode(), int(value)), f"option {key}")
 
-    LAYOUTS = ("csr", "padded", "pattern", "sell", "sell_pattern", "symd", "leaves", "empty", "sell_uniform", "sell_sorted", "split", "dict")
+    LAYOUTS = ("csr", "padded", "pattern", "sell", "sell_pattern", "symd", "leaves", "empty", "sell_uniform", "sell_sorted", "split", "dict", "wcsr")
     _SLOTS = {"a": 0, "p": 1, "pt": 2, "g": 3, "gt": 4}
 
     def layout(self, level, slot):

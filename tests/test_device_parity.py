@@ -127,6 +127,37 @@ def test_spmv_symmetric_diagonals_bit_identical(kind):
         dh.close()
 
 
+@pytest.mark.parametrize("lens", ["ragged9", "long", "heavy"])
+def test_spmv_warp_cooperative_csr_bit_identical(lens):
+    # wcsr: one warp per 32 consecutive rows, coalesced entry loads, products in a
+    # per-warp smem buffer, rows summed from it in the reference order; groups
+    # heavier than the buffer go through it in row chunks, rows longer than it
+    # straight from global memory
+    from paper_2102_07417_b200.problems import Csr
+
+    rng = np.random.default_rng(7)
+    n = 60000
+    if lens == "ragged9":
+        ln = np.minimum(rng.geometric(1.0 / 9.0, n), 46)
+    elif lens == "long":
+        ln = rng.integers(8, 40, n)
+        ln[::97] = 700  # single rows longer than the 640-entry warp buffer (recursive pairwise)
+    else:
+        ln = rng.integers(15, 30, n)  # ~700 entries per 32-row group: chunked groups
+    ln[:3] = [0, 1, 129]
+    off = np.concatenate([[0], np.cumsum(ln)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(np.arange(max(0, r - 800), min(n, r + 800)), l, replace=False))
+                           for r, l in enumerate(ln)]).astype(np.int32)
+    m = Csr(n, n, off, cols, rng.uniform(-1, 1, off[-1]))
+    x = rng.uniform(-1, 1, n)
+    want = O.spmv(m, x)
+    dh = amg.DeviceHierarchy.from_matrices([m], options={"dict": 0, "symm": 0, "sells": 0, "sell": 0,
+                                                         "small_rows_per_sm": 1})
+    assert dh.layout(0, "a") == "wcsr"
+    np.testing.assert_array_equal(dh.matrix(0, "a")(x), want)
+    dh.close()
+
+
 def _class_matrix(ncls, nrows, maxlen, seed):
     # rows drawn from `ncls` distinct (offsets, values) classes, columns clipped at the
     # borders (clipped rows form classes of their own)
@@ -543,20 +574,20 @@ def test_run_solve_report_and_cli(tmp_path):
     assert main(["solve", "--cache", str(tmp_path / "missing")]) == 1
 
 
-@pytest.mark.parametrize("kind", ["uniform", "ragged", "padded", "small"])
+@pytest.mark.parametrize("kind", ["uniform", "ragged", "padded", "wcsr", "small"])
 def test_interior_boundary_split_spmv_bit_identical(kind):
     # the multi-GPU overlap schedule on one GPU (overlap_test): interior rows
     # [n/4, 3n/4) in one launch, the two boundary ranges in a second, reductions
     # folded over both launches' partials; every row must stay bit-identical
     from paper_2102_07417_b200.problems import Csr
 
-    rng = np.random.default_rng({"uniform": 1, "ragged": 2, "padded": 3, "small": 4}[kind])
-    n = {"uniform": 60000, "ragged": 50000, "padded": 1_100_000, "small": 9000}[kind]
+    rng = np.random.default_rng({"uniform": 1, "ragged": 2, "padded": 3, "wcsr": 3, "small": 4}[kind])
+    n = {"uniform": 60000, "ragged": 50000, "padded": 1_100_000, "wcsr": 1_100_000, "small": 9000}[kind]
     if kind == "uniform":
         lens = np.full(n, 9)
     elif kind == "ragged":
         lens = rng.integers(3, 16, n)
-    elif kind == "padded":
+    elif kind in ("padded", "wcsr"):
         lens = rng.integers(8, 30, n)
     else:
         lens = rng.integers(1, 60, n)
@@ -566,9 +597,11 @@ def test_interior_boundary_split_spmv_bit_identical(kind):
     m = Csr(n, n, off, cols, rng.uniform(-1, 1, off[-1]))
     x = rng.uniform(-1, 1, n)
     want = O.spmv(m, x)
-    dh = amg.DeviceHierarchy.from_matrices([m], options={"overlap_test": 1, "dict": 0, "symm": 0})
+    dh = amg.DeviceHierarchy.from_matrices([m], options={"overlap_test": 1, "dict": 0, "symm": 0,
+                                                         "wcsr": int(kind != "padded")})
     lay = dh.layout(0, "a")
-    assert lay == {"uniform": "sell_uniform", "ragged": "sell_sorted", "padded": "padded", "small": "csr"}[kind]
+    assert lay == {"uniform": "sell_uniform", "ragged": "sell_sorted", "padded": "padded", "wcsr": "wcsr",
+                   "small": "csr"}[kind]
     np.testing.assert_array_equal(dh.matrix(0, "a")(x), want)
     dh.close()
 
