@@ -11,7 +11,7 @@ import os
 
 from .errors import AmgError, BreakdownError, DimensionMismatchError, NotSpdError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libamgb200.so")
+LIB_PATH = os.environ.get("AMGB200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libamgb200.so")
 
 AMG_OK, AMG_E_ARG, AMG_E_DIM, AMG_E_NOT_SPD, AMG_E_CUDA, AMG_E_NCCL, AMG_E_STATE, AMG_E_BREAKDOWN = range(8)
 AMG_A, AMG_P, AMG_PT, AMG_G, AMG_GT = range(5)
