@@ -45,6 +45,20 @@ def build_library(force=False, verbose=False):
     return LIB
 
 
+CHECKED_LIB = os.path.join(PKG, "libamgb200_checks.so")
+
+
+def build_checked_library(force=False, verbose=False):
+    """libamgb200_checks.so: the same library with device-side invariant checks
+    (AMG_CHECK in csrc/kernels.cuh; load it with AMGB200_LIB=... for a test run)."""
+    if force or _stale(CHECKED_LIB, SOURCES + HEADERS):
+        cmd = [NVCC] + NVCC_FLAGS + ["-DAMG_CHECKS"] + SOURCES + ["-o", CHECKED_LIB]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+    return CHECKED_LIB
+
+
 def build_fsai_host(force=False, verbose=False):
     """Host C helper that replays FSAI coefficients when a lean hierarchy cache is loaded."""
     if force or _stale(FSAI_LIB, [FSAI_SRC]):

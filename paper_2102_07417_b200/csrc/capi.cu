@@ -771,6 +771,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     a.gate1 = g1;
     a.gate2 = g2;
     a.rsplit = INT_MAX;
+    a.pcap = 2 * h->max_grid;
     const int lay = layout_of(h, M);
     if (M.int_hi > M.int_lo && (h->nranks > 1 || h->overlap_test) && range_layout(lay)) {
         // interior / boundary split: the interior rows need no halo column, so they run

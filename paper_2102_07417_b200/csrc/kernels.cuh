@@ -24,6 +24,26 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
+
+// AMG_CHECKS builds (paper_2102_07417_b200.build.build_checked_library; the
+// stand-in for compute-sanitizer, which this GPU pool does not allow): index
+// and protocol invariants of the kernels checked on the device, a violation
+// prints its site and traps (the launch fails with an error).
+#ifdef AMG_CHECKS
+#define AMG_CHECK(cond)                                                                                   \
+    do {                                                                                                  \
+        if (!(cond)) {                                                                                    \
+            printf("amgb200 check failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,    \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                   \
+            __trap();                                                                                     \
+        }                                                                                                 \
+    } while (0)
+#else
+#define AMG_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
 
 namespace amg {
 
@@ -90,9 +110,11 @@ struct SpmvArgs {
     // 1 = store partials[pbase + cta] only; 2 = store, then the last CTA folds
     // partials[0, pbase + grid) (the first launch wrote [0, pbase))
     int pmode, pbase;
+    int pcap;  // partial slots available (2 x max grid): AMG_CHECKS bound for pbase + grid
 };
 
 __device__ __forceinline__ int vrow(const SpmvArgs &a, int v) { return a.rlo + v + (v >= a.rsplit ? a.rgap : 0); }
+// (AMG_CHECKS: spmv_finalize checks the two-launch partial slots against the scratch size)
 
 // ---------------------------------------------------------------- helpers
 
@@ -255,6 +277,7 @@ __device__ __forceinline__ void grid_finalize(double v, double *partials, unsign
         partials[blockIdx.x] = v;
         __threadfence();
         unsigned t = atomicAdd(ticket, 1u);
+        AMG_CHECK(t < gridDim.x);  // the ticket was left at 0 by the previous reduction
         s_last = (t == gridDim.x - 1);
     }
     __syncthreads();
@@ -285,6 +308,7 @@ __device__ __forceinline__ void grid_finalize_pair(double v, double *partials, i
         partials[base + blockIdx.x] = v;
         __threadfence();
         unsigned t = atomicAdd(ticket, 1u);
+        AMG_CHECK(t < gridDim.x);
         s_last = (t == gridDim.x - 1);
     }
     __syncthreads();
@@ -305,6 +329,7 @@ __device__ __forceinline__ void grid_finalize_pair(double v, double *partials, i
 template <int NT>
 __device__ __forceinline__ void spmv_finalize(double v, const SpmvArgs &a)
 {
+    AMG_CHECK(a.pmode == 0 || a.pbase + (int)gridDim.x <= a.pcap);
     if (a.pmode == 0) grid_finalize<NT>(v, a.partials, a.ticket, a.fin, a.ctl);
     else if (a.pmode == 1) { if (threadIdx.x == 0) a.partials[a.pbase + blockIdx.x] = v; }
     else grid_finalize_pair<NT>(v, a.partials, a.pbase, a.ticket, a.fin, a.ctl);
@@ -1523,6 +1548,7 @@ __global__ void __launch_bounds__(WCSR_THREADS, 3) spmv_wcsr(const SpmvArgs a, i
                 for (int u = 0; u < WCSR_UNROLL; ++u) {
                     const double xv = __ldg(x + pc[u]);
                     const int k = kb + u * 32 + lane;
+                    AMG_CHECK(k >= nk || wslot(k) < WCSR_BUF + WCSR_BUF / 16);
                     if (k < nk) ps[wslot(k)] = prod(pv[u], xv);
                 }
             }
@@ -1621,8 +1647,10 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_dict(const SpmvArgs 
         double bv = 0.0, wv = 0.0;
         if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
         if (want_dot && !self_dot) wv = a.dotw[row];
+        AMG_CHECK(c >= 0 && c < d.ncls);
         const int rb = sbeg[c];
         const int len = sbeg[c + 1] - rb;
+        AMG_CHECK(len >= 0 && len <= FL && rb + len <= d.nent);
         double p[FL];
 #pragma unroll
         for (int k = 0; k < FL; ++k) {
@@ -1761,6 +1789,7 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_sells(const SpmvArgs
         nsb = __ldg(q.sbeg + s);
         nw = __ldg(q.swid + s);
         const int pos = s * 32 + lane;
+        AMG_CHECK(s >= 0 && s * 32 < q.nslots);
         nrow = pos < q.nslots ? __ldg(q.perm + pos) : -1;
         nlen = pos < q.nslots ? __ldg(q.slen + pos) : 0;
     };
@@ -2306,6 +2335,7 @@ __device__ __forceinline__ double tv_ld(const double *g, int s, int i, const int
 {
     if (s < 0) return __ldcg(g + i);
     const int2 d = sv[s];
+    AMG_CHECK((unsigned)(i >> d.x) < 16u);
     const unsigned la = smem_u32(smem + d.y) + ((unsigned)(i & ((1 << d.x) - 1)) << 3);
     unsigned ra;
     asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"((unsigned)(i >> d.x)));
@@ -2433,6 +2463,7 @@ __device__ __forceinline__ void tail_spmv_streamed(const TailOp &o, const TailMa
         }
         __syncthreads();
         const int re = s_re;
+        AMG_CHECK(re > rs && __ldg(M.off + re) - __ldg(M.off + rs) <= pcap);  // whole rows within the buffer
         tail_spmv_streamed_chunk<EPI>(o, M, rs, re, ps, tvs, smem);
         __syncthreads();
         rs = re;
@@ -2445,6 +2476,7 @@ __device__ __forceinline__ void tail_spmv_streamed_chunk(const TailOp &o, const 
 {
     const int k0 = __ldg(M.off + r0);
     const int nk = __ldg(M.off + r1) - k0;
+    AMG_CHECK(r0 <= r1);
     double bpre = 0.0;
     if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD)
         if (r0 + (int)threadIdx.x < r1) bpre = tv_ld(o.b, o.bs, r0 + threadIdx.x, tvs, smem);
