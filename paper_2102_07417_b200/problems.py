@@ -279,6 +279,8 @@ CONFIGS = {
     "t_poisson7_16": (poisson7, (16, 16, 16), {}, {"smoother": "fsai"}),
     "t_hetero27_24": (hetero27, (24, 24, 24), {"sigma": 2.0, "seed": 42}, {"smoother": "fsai"}),
     "t_rtanis7_32": (rtanis7, (32, 32, 32), {"kx": 1.0, "ky": 1.0, "kz": 1e-3}, {"smoother": "fsai"}),
+    # config 4's x-y planes with a quarter of its z extent (tuning stand-in: same per-plane coarsening)
+    "t_rtanis7_256x64": (rtanis7, (256, 256, 64), {"kx": 1.0, "ky": 1.0, "kz": 1e-3}, {"smoother": "fsai"}),
     "t_elasticity_12": (elasticity3d, (12, 12, 12), {"sigma": 1.0, "nu": 0.3, "seed": 42},
                         {"smoother": "fsai", "interp": "bamg", "testspace": "rigid_body", "n_test_vectors": 6}),
 }
