@@ -100,6 +100,9 @@ struct DevMat {
     int32_t *dbeg = nullptr, *drel = nullptr;
     double *dval = nullptr;
     int dncls = 0, dnent = 0, dwide = 0, dfl = 0, dgrid = 0;
+    int dmcls = -1, dmlen = 0;   // most frequent class (its entries travel as kernel parameters), -1: none
+    int32_t dmrel[8] = {};
+    double dmval[8] = {};
     int wcsr = 0, wcsr_grid = 0;  // warp-cooperative CSR (spmv_wcsr) on the uploaded arrays
 };
 
@@ -254,6 +257,8 @@ struct amg_handle {
     int symd_fixed = 1;           // fixed-slot symmetric kernel: 1 rows <= 8 entries (7-point), 2 also <= 32 (27-point:
                                   // measured slower than the round-by-round kernel on config 2), 0 off
     int symm = 1;                 // symmetric stencil layout (upper diagonals) for bitwise-symmetric pattern operators
+    int dict_rows = 2;            // spmv_dict: rows per thread and step for rows of <= 4 entries (measured: no gain on 7-entry rows)
+    int dict_main = 1;            // spmv_dict: warps whose rows all have the most frequent class take its entries from kernel parameters
     int dict = 1;                 // row-class dictionary layout for operators with few distinct rows
     int wcsr = 1;                 // large matrices averaging >= pad_min entries: warp-cooperative CSR instead of the padded copy
     int sell = 1;                 // SELL-32 slices where padding <= sell_pad %
@@ -390,11 +395,12 @@ static SpmvWcsrFn spmv_wcsr_fn(int epi)
 
 typedef void (*SpmvDictFn)(const SpmvArgs, const DictArgs, int);
 
-static SpmvDictFn spmv_dict_fn(int epi, int fl, bool wide)
+static SpmvDictFn spmv_dict_fn(int epi, int fl, bool wide, int rows)
 {
-#define AMG_D(E)                                                                                         \
-    return wide ? (fl <= 8 ? spmv_dict<E, 8, true> : fl <= 16 ? spmv_dict<E, 16, true> : spmv_dict<E, 32, true>) \
-                : (fl <= 8 ? spmv_dict<E, 8, false> : fl <= 16 ? spmv_dict<E, 16, false> : spmv_dict<E, 32, false>);
+#define AMG_D(E)                                                                                                   \
+    if (fl <= 4 && rows >= 2) return wide ? spmv_dict<E, 4, true, 2> : spmv_dict<E, 4, false, 2>;                   \
+    return wide ? (fl <= 8 ? spmv_dict<E, 8, true, 1> : fl <= 16 ? spmv_dict<E, 16, true, 1> : spmv_dict<E, 32, true, 1>) \
+                : (fl <= 8 ? spmv_dict<E, 8, false, 1> : fl <= 16 ? spmv_dict<E, 16, false, 1> : spmv_dict<E, 32, false, 1>);
     switch (epi) {
     case EPI_PLAIN: AMG_D(EPI_PLAIN)
     case EPI_RESID: AMG_D(EPI_RESID)
@@ -798,10 +804,14 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
     }
     TRY(exchange(h, M, const_cast<double *>(x)));
     if (M.dcls) {
-        DictArgs da{M.dcls, M.dbeg, M.drel, M.dval, M.dncls, M.dnent};
+        DictArgs da{M.dcls, M.dbeg, M.drel, M.dval, M.dncls, M.dnent, h->dict_main ? M.dmcls : -1, M.dmlen};
+        for (int k = 0; k < 8; ++k) {
+            da.mrel[k] = M.dmrel[k];
+            da.mval[k] = M.dmval[k];
+        }
+        const int dg = grid_cap ? std::min(grid_cap, M.dgrid) : M.dgrid;
         const size_t sm = (size_t)M.dnent * 12 + (size_t)(M.dncls + 1) * 4;
-        TRY(launch_k(h, spmv_dict_fn(epi, M.dfl, M.dwide), grid_cap ? std::min(grid_cap, M.dgrid) : M.dgrid,
-                     VEC_SPMV_THREADS, sm, a, da, (int)M.nrows));
+        TRY(launch_k(h, spmv_dict_fn(epi, M.dfl, M.dwide, h->dict_rows), dg, VEC_SPMV_THREADS, sm, a, da, (int)M.nrows));
     } else if (M.uval && h->symm) {
         const bool fx = M.sym_fl && (h->symd_fixed >= 2 || (h->symd_fixed == 1 && M.sym_fl <= 8));
         int g = fx ? M.symf_grid : M.sym_grid;
@@ -1513,6 +1523,12 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
     if (k == "symm") { h->symm = value ? 1 : 0; return AMG_OK; }
     if (k == "dict") { h->dict = value ? 1 : 0; return AMG_OK; }
+    if (k == "dict_main") { h->dict_main = value ? 1 : 0; return AMG_OK; }
+    if (k == "dict_rows") {
+        if (value < 1 || value > 2) return fail(AMG_E_ARG, "dict_rows must be 1 or 2");
+        h->dict_rows = (int)value;
+        return AMG_OK;
+    }
     if (k == "wcsr") { h->wcsr = value ? 1 : 0; return AMG_OK; }
     if (k == "overlap_test") { h->overlap_test = value ? 1 : 0; return AMG_OK; }
     if (k == "nccl_selftest") { h->nccl_selftest = (int)value; return AMG_OK; }
@@ -1844,8 +1860,25 @@ static int build_dict(amg_t *h, DevMat &M, const std::vector<int32_t> &off32)
     }
     M.dncls = (int)beg.size() - 1;
     M.dnent = (int)rel.size();
+    {
+        // the class most rows share (the interior stencil): rows of <= 8 entries only
+        std::vector<int64_t> cnt(M.dncls, 0);
+        for (int64_t r = 0; r < M.nrows; ++r) ++cnt[cls[r]];
+        int best = -1;
+        for (int c = 0; c < M.dncls; ++c)
+            if (beg[c + 1] - beg[c] <= 8 && (best < 0 || cnt[c] > cnt[best])) best = c;
+        M.dmcls = -1;
+        if (best >= 0 && maxlen <= 8) {
+            M.dmcls = best;
+            M.dmlen = beg[best + 1] - beg[best];
+            for (int k = 0; k < 8; ++k) {
+                M.dmrel[k] = k < M.dmlen ? rel[beg[best] + k] : 0;
+                M.dmval[k] = k < M.dmlen ? val[beg[best] + k] : 0.0;
+            }
+        }
+    }
     M.dwide = M.dncls > 256 ? 1 : 0;
-    M.dfl = maxlen <= 8 ? 8 : maxlen <= 16 ? 16 : 32;
+    M.dfl = maxlen <= 4 ? 4 : maxlen <= 8 ? 8 : maxlen <= 16 ? 16 : 32;
     if (M.dwide) {
         TRY(dalloc((uint16_t **)&M.dcls, (size_t)M.nrows));
         CK(cudaMemcpy(M.dcls, cls.data(), (size_t)M.nrows * 2, cudaMemcpyHostToDevice));
@@ -1864,7 +1897,7 @@ static int build_dict(amg_t *h, DevMat &M, const std::vector<int32_t> &off32)
     }
     const size_t sm = (size_t)M.dnent * 12 + (size_t)(M.dncls + 1) * 4;
     int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_dict_fn(EPI_RESID, M.dfl, M.dwide),
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_dict_fn(EPI_RESID, M.dfl, M.dwide, h->dict_rows),
                                                      VEC_SPMV_THREADS, sm));
     M.dgrid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
                                                           (int64_t)h->sm_count * std::max(nb, 1)));

@@ -1611,10 +1611,21 @@ struct DictArgs {
     const int32_t *rel;   // column offset col - row per entry
     const double *val;    // value per entry
     int ncls, nent;
+    // the most frequent class (rows of <= 8 entries; -1: none): its offsets and values travel as
+    // kernel parameters, i.e. constant-bank operands -- a warp whose 32 rows all have it (the
+    // interior of a stencil operator) reads no table at all
+    int mcls, mlen;
+    int32_t mrel[8];
+    double mval[8];
 };
 
-template <int EPI, int FL, bool WIDE>
-__global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_dict(const SpmvArgs a, const DictArgs d, int nrows)
+// ROWS rows per thread and step (rows row, row + nthreads, ...): all their gathers are issued
+// before the first sum, so a thread keeps ROWS x len loads in flight -- on the 4 M-row
+// constant-coefficient operators the one-row kernel waited on one row's gathers at a time
+// (ncu: long-scoreboard stalls, 49% of the warp slots occupied, 2.0 TB/s).
+template <int EPI, int FL, bool WIDE, int ROWS>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, (ROWS > 1 || FL > 8) ? 4 : 5) spmv_dict(const SpmvArgs a, const DictArgs d,
+                                                                                          int nrows)
 {
     __shared__ double red[VEC_SPMV_THREADS / 32];
     extern __shared__ double dict_sm[];  // val[nent] | rel[nent] | beg[ncls + 1]
@@ -1634,38 +1645,69 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, 4) spmv_dict(const SpmvArgs 
     const bool want_dot = a.dotw != nullptr;
     const bool self_dot = a.dotw == a.y;
     const double *__restrict__ x = a.x;
-    auto cls_of = [&](int r) -> int {
+    auto cls_at = [&](int r) -> int {
         if constexpr (WIDE) return __ldg(reinterpret_cast<const uint16_t *>(d.cls) + r);
         else return __ldg(reinterpret_cast<const uint8_t *>(d.cls) + r);
     };
     double dacc = 0.0;
-    int row = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x;
-    int ncl = row < nrows ? cls_of(row) : 0;
-    for (; row < nrows; row += nthreads) {
-        const int c = ncl;
-        if (row + nthreads < nrows) ncl = cls_of(row + nthreads);  // next row's class one step ahead
-        double bv = 0.0, wv = 0.0;
-        if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
-        if (want_dot && !self_dot) wv = a.dotw[row];
-        AMG_CHECK(c >= 0 && c < d.ncls);
-        const int rb = sbeg[c];
-        const int len = sbeg[c + 1] - rb;
-        AMG_CHECK(len >= 0 && len <= FL && rb + len <= d.nent);
-        double p[FL];
+    const int rstep = nthreads;  // distance of a thread's consecutive rows
+    const int rend = nrows;
+    int row0 = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x;
+    auto cls_of = [&](int r) -> int { return r < rend ? cls_at(r) : 0; };
+    int ncl[ROWS];
 #pragma unroll
-        for (int k = 0; k < FL; ++k) {
-            p[k] = 0.0;
-            if (k < len) p[k] = prod(sval[rb + k], __ldg(x + (row + srel[rb + k])));
+    for (int q = 0; q < ROWS; ++q) ncl[q] = cls_of(row0 + q * rstep);
+    // warp-uniform trip count (the vote below needs every lane): lanes beyond the last row idle
+    for (; row0 - (int)(threadIdx.x & 31) < rend; row0 += ROWS * rstep) {
+        int len[ROWS];
+        double p[ROWS][FL], bv[ROWS], wv[ROWS];
+#pragma unroll
+        for (int q = 0; q < ROWS; ++q) {
+            const int row = row0 + q * rstep;
+            const int c = ncl[q];
+            ncl[q] = cls_of(row + ROWS * rstep);  // the class one step ahead
+            AMG_CHECK(c >= 0 && c < d.ncls);
+            const int rb = sbeg[c];
+            len[q] = row < rend ? sbeg[c + 1] - rb : 0;
+            AMG_CHECK(len[q] >= 0 && len[q] <= FL && rb + len[q] <= d.nent);
+            bv[q] = wv[q] = 0.0;
+            if (row < rend) {
+                if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv[q] = a.b[row];
+                if (want_dot && !self_dot) wv[q] = a.dotw[row];
+            }
+            bool fast = false;
+            if constexpr (FL <= 8) fast = __all_sync(0xffffffffu, c == d.mcls && row < rend);
+            if (fast) {
+                if constexpr (FL <= 8) {
+#pragma unroll
+                    for (int k = 0; k < FL; ++k) {
+                        p[q][k] = 0.0;
+                        if (k < d.mlen) p[q][k] = prod(d.mval[k], __ldg(x + (row + d.mrel[k])));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < FL; ++k) {
+                    p[q][k] = 0.0;
+                    if (k < len[q]) p[q][k] = prod(sval[rb + k], __ldg(x + (row + srel[rb + k])));
+                }
+            }
         }
-        const double sum = ref_sum_fixed<FL>(p, len);
-        double yv;
-        if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
-        else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
-        else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
-        else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
-        else yv = sum;
-        a.y[row] = yv;
-        if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
+#pragma unroll
+        for (int q = 0; q < ROWS; ++q) {
+            const int row = row0 + q * rstep;
+            if (row < rend) {
+                const double sum = ref_sum_fixed<FL>(p[q], len[q]);
+                double yv;
+                if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv[q], sum);
+                else if constexpr (EPI == EPI_AXPYW) yv = add(bv[q], __dmul_rn(a.omega, sum));
+                else if constexpr (EPI == EPI_ADD) yv = add(bv[q], sum);
+                else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+                else yv = sum;
+                a.y[row] = yv;
+                if (want_dot) dacc = fma(yv, self_dot ? yv : wv[q], dacc);
+            }
+        }
     }
     if (want_dot || a.fin != FIN_NONE) {
         double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
