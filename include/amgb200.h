@@ -178,6 +178,27 @@ int amg_matrix_bytes(amg_t *h, int level, int which, int64_t *stored, int64_t *v
 /* Tuning / diagnostics: 0 = auto. */
 int amg_set_option(amg_t *h, const char *key, int64_t value);
 
+/* ---- Device setup operators -------------------------------
+ * The two operators a lean hierarchy cache replays on load, on the GPU and
+ * bit-identical to the reference's scipy calls (same terms, same order, products
+ * rounded before the add, exact zeros dropped):
+ *   amg_device_galerkin : amgkit/sparse.py:256-282 galerkin_product(A, P, symmetrize)
+ *                         = P^T A P [(R + R^T)/2], called at hierarchy.py:210
+ *   amg_device_transpose: amgkit/sparse.py:220-224 transpose(A) (hierarchy.py:216,
+ *                         smoothers.py:145)
+ * Host CSR in (int64 offsets, int32 columns, f64 values: the reference dtypes,
+ * sparse.py:67-69), result held on the device until fetched into caller buffers
+ * sized from amg_csr_result_shape; canonical CSR out (sorted unique columns). */
+typedef struct amg_csr_result amg_csr_result_t;
+int amg_device_galerkin(int device, int64_t n, int64_t m, const int64_t *a_offsets, const int32_t *a_cols,
+                        const double *a_vals, const int64_t *p_offsets, const int32_t *p_cols, const double *p_vals,
+                        int symmetrize, amg_csr_result_t **out);
+int amg_device_transpose(int device, int64_t nrows, int64_t ncols, const int64_t *offsets, const int32_t *cols,
+                         const double *vals, amg_csr_result_t **out);
+int amg_csr_result_shape(const amg_csr_result_t *r, int64_t *nrows, int64_t *ncols, int64_t *nnz);
+int amg_csr_result_fetch(const amg_csr_result_t *r, int64_t *offsets, int32_t *cols, double *vals);
+void amg_csr_result_free(amg_csr_result_t *r);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,6 +27,8 @@ EXPORTS = (
     "amg_coarse_solve", "amg_vcycle", "amg_pcg", "amg_get_stats", "amg_set_option", "amg_time_spmv",
     "amg_nccl_unique_id", "amg_set_halo", "amg_set_agglomeration", "amg_bicgstab",
     "amg_matrix_layout", "amg_matrix_bytes",
+    "amg_device_galerkin", "amg_device_transpose", "amg_csr_result_shape", "amg_csr_result_fetch",
+    "amg_csr_result_free",
 )
 
 
@@ -105,6 +107,11 @@ def lib():
         "amg_bicgstab": (I32, [P, P, P, D, I32, I32, P, P, P, P, P, P, P, I32]),
         "amg_matrix_layout": (I32, [P, I32, I32, ctypes.POINTER(I32)]),
         "amg_matrix_bytes": (I32, [P, I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+        "amg_device_galerkin": (I32, [I32, I64, I64, P, P, P, P, P, P, I32, ctypes.POINTER(P)]),
+        "amg_device_transpose": (I32, [I32, I64, I64, P, P, P, ctypes.POINTER(P)]),
+        "amg_csr_result_shape": (I32, [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+        "amg_csr_result_fetch": (I32, [P, P, P, P]),
+        "amg_csr_result_free": (None, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

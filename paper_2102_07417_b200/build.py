@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libamgb200.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("capi.cu",)]
-HEADERS = [os.path.join(CSRC, f) for f in ("kernels.cuh", "halo.h")] + [os.path.join(ROOT, "include", "amgb200.h")]
+HEADERS = [os.path.join(CSRC, f) for f in ("kernels.cuh", "halo.h", "setup.cuh")] + [os.path.join(ROOT, "include", "amgb200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -52,6 +52,8 @@ static int fail(int code, const std::string &msg)
         if (s_ != AMG_OK) return s_; \
     } while (0)
 
+#include "setup.cuh"
+
 namespace {
 
 struct DevMat {
@@ -3050,6 +3052,83 @@ int amg_get_stats(amg_t *h, amg_stats_t *out)
     out->tail_level = h->tail_level;
     out->cluster = h->cluster;
     return AMG_OK;
+}
+
+
+// ---------------------------------------------------------------- device setup operators (setup.cuh)
+
+static int setup_device(int device)
+{
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count <= 0)
+        return fail(AMG_E_CUDA, "no CUDA device (there is no CPU fallback)");
+    if (device < 0 || device >= count) return fail(AMG_E_ARG, "device index out of range");
+    CK(cudaSetDevice(device));
+    return AMG_OK;
+}
+
+int amg_device_galerkin(int device, int64_t n, int64_t m, const int64_t *a_offsets, const int32_t *a_cols,
+                        const double *a_vals, const int64_t *p_offsets, const int32_t *p_cols, const double *p_vals,
+                        int symmetrize, amg_csr_result_t **out)
+{
+    if (!out) return fail(AMG_E_ARG, "amg_device_galerkin: NULL output");
+    *out = nullptr;
+    TRY(setup_device(device));
+    amg_csr_result *r = new amg_csr_result();
+    r->device = device;
+    const int st = amg_setup::galerkin(r, n, m, a_offsets, a_cols, a_vals, p_offsets, p_cols, p_vals, symmetrize);
+    if (st != AMG_OK) {
+        delete r;
+        return st;
+    }
+    *out = r;
+    return AMG_OK;
+}
+
+int amg_device_transpose(int device, int64_t nrows, int64_t ncols, const int64_t *offsets, const int32_t *cols,
+                         const double *vals, amg_csr_result_t **out)
+{
+    if (!out) return fail(AMG_E_ARG, "amg_device_transpose: NULL output");
+    *out = nullptr;
+    TRY(setup_device(device));
+    amg_csr_result *r = new amg_csr_result();
+    r->device = device;
+    const int st = amg_setup::transpose(r, nrows, ncols, offsets, cols, vals);
+    if (st != AMG_OK) {
+        delete r;
+        return st;
+    }
+    *out = r;
+    return AMG_OK;
+}
+
+int amg_csr_result_shape(const amg_csr_result_t *r, int64_t *nrows, int64_t *ncols, int64_t *nnz)
+{
+    if (!r || !nrows || !ncols || !nnz) return fail(AMG_E_ARG, "amg_csr_result_shape: NULL argument");
+    *nrows = r->nrows;
+    *ncols = r->ncols;
+    *nnz = r->nnz;
+    return AMG_OK;
+}
+
+int amg_csr_result_fetch(const amg_csr_result_t *r, int64_t *offsets, int32_t *cols, double *vals)
+{
+    if (!r || !offsets) return fail(AMG_E_ARG, "amg_csr_result_fetch: NULL argument");
+    if (r->nnz > 0 && (!cols || !vals)) return fail(AMG_E_ARG, "amg_csr_result_fetch: NULL entry buffers");
+    CK(cudaSetDevice(r->device));
+    CK(cudaMemcpy(offsets, r->off.p, (r->nrows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (r->nnz) {
+        CK(cudaMemcpy(cols, r->col.p, r->nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(vals, r->val.p, r->nnz * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    return AMG_OK;
+}
+
+void amg_csr_result_free(amg_csr_result_t *r)
+{
+    if (!r) return;
+    cudaSetDevice(r->device);
+    delete r;
 }
 
 }  // extern "C"

@@ -61,6 +61,10 @@ class Csr:
     def shape(self):
         return (self.nrows, self.ncols)
 
+    def as_tuple(self):
+        """(nrows, ncols, row_offsets, col_indices, values): ``amgkit.SparseMatrix``'s positional arguments."""
+        return (self.nrows, self.ncols, self.row_offsets, self.col_indices, self.values)
+
     def __repr__(self):
         return f"Csr({self.nrows}x{self.ncols}, nnz={self.nnz})"
 
