@@ -259,7 +259,6 @@ struct amg_handle {
     int symd_fixed = 1;           // fixed-slot symmetric kernel: 1 rows <= 8 entries (7-point), 2 also <= 32 (27-point:
                                   // measured slower than the round-by-round kernel on config 2), 0 off
     int symm = 1;                 // symmetric stencil layout (upper diagonals) for bitwise-symmetric pattern operators
-    int dict_rows = 2;            // spmv_dict: rows per thread and step for rows of <= 4 entries (measured: no gain on 7-entry rows)
     int dict_main = 1;            // spmv_dict: warps whose rows all have the most frequent class take its entries from kernel parameters
     int dict = 1;                 // row-class dictionary layout for operators with few distinct rows
     int wcsr = 1;                 // large matrices averaging >= pad_min entries: warp-cooperative CSR instead of the padded copy
@@ -397,10 +396,15 @@ static SpmvWcsrFn spmv_wcsr_fn(int epi)
 
 typedef void (*SpmvDictFn)(const SpmvArgs, const DictArgs, int);
 
-static SpmvDictFn spmv_dict_fn(int epi, int fl, bool wide, int rows)
+static SpmvDictFn spmv_dict_fn(int epi, int fl, bool wide, int ml)
 {
+    // ml: entries of the most frequent class when it gets a compile-time interior path (3, 5, 7), else 0.
+    // Two rows per thread and step were measured slower once the interior path was lean (stand-in A0
+    // 31.7 vs 25.3 us, G0 19.7 vs 16.5 us): one row per thread, 5 CTAs / SM.
 #define AMG_D(E)                                                                                                   \
-    if (fl <= 4 && rows >= 2) return wide ? spmv_dict<E, 4, true, 2> : spmv_dict<E, 4, false, 2>;                   \
+    if (!wide && fl <= 4 && ml == 3) return spmv_dict<E, 4, false, 1, 3>;                                          \
+    if (!wide && fl == 8 && ml == 5) return spmv_dict<E, 8, false, 1, 5>;                                          \
+    if (!wide && fl == 8 && ml == 7) return spmv_dict<E, 8, false, 1, 7>;                                          \
     return wide ? (fl <= 8 ? spmv_dict<E, 8, true, 1> : fl <= 16 ? spmv_dict<E, 16, true, 1> : spmv_dict<E, 32, true, 1>) \
                 : (fl <= 8 ? spmv_dict<E, 8, false, 1> : fl <= 16 ? spmv_dict<E, 16, false, 1> : spmv_dict<E, 32, false, 1>);
     switch (epi) {
@@ -809,11 +813,12 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         DictArgs da{M.dcls, M.dbeg, M.drel, M.dval, M.dncls, M.dnent, h->dict_main ? M.dmcls : -1, M.dmlen};
         for (int k = 0; k < 8; ++k) {
             da.mrel[k] = M.dmrel[k];
+            da.moff[k] = (long long)M.dmrel[k] * 8;
             da.mval[k] = M.dmval[k];
         }
         const int dg = grid_cap ? std::min(grid_cap, M.dgrid) : M.dgrid;
         const size_t sm = (size_t)M.dnent * 12 + (size_t)(M.dncls + 1) * 4;
-        TRY(launch_k(h, spmv_dict_fn(epi, M.dfl, M.dwide, h->dict_rows), dg, VEC_SPMV_THREADS, sm, a, da, (int)M.nrows));
+        TRY(launch_k(h, spmv_dict_fn(epi, M.dfl, M.dwide, (h->dict_main && M.dmcls >= 0) ? M.dmlen : 0), dg, VEC_SPMV_THREADS, sm, a, da, (int)M.nrows));
     } else if (M.uval && h->symm) {
         const bool fx = M.sym_fl && (h->symd_fixed >= 2 || (h->symd_fixed == 1 && M.sym_fl <= 8));
         int g = fx ? M.symf_grid : M.sym_grid;
@@ -1526,11 +1531,6 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "symm") { h->symm = value ? 1 : 0; return AMG_OK; }
     if (k == "dict") { h->dict = value ? 1 : 0; return AMG_OK; }
     if (k == "dict_main") { h->dict_main = value ? 1 : 0; return AMG_OK; }
-    if (k == "dict_rows") {
-        if (value < 1 || value > 2) return fail(AMG_E_ARG, "dict_rows must be 1 or 2");
-        h->dict_rows = (int)value;
-        return AMG_OK;
-    }
     if (k == "wcsr") { h->wcsr = value ? 1 : 0; return AMG_OK; }
     if (k == "overlap_test") { h->overlap_test = value ? 1 : 0; return AMG_OK; }
     if (k == "nccl_selftest") { h->nccl_selftest = (int)value; return AMG_OK; }
@@ -1899,7 +1899,7 @@ static int build_dict(amg_t *h, DevMat &M, const std::vector<int32_t> &off32)
     }
     const size_t sm = (size_t)M.dnent * 12 + (size_t)(M.dncls + 1) * 4;
     int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_dict_fn(EPI_RESID, M.dfl, M.dwide, h->dict_rows),
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_dict_fn(EPI_RESID, M.dfl, M.dwide, (h->dict_main && M.dmcls >= 0) ? M.dmlen : 0),
                                                      VEC_SPMV_THREADS, sm));
     M.dgrid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
                                                           (int64_t)h->sm_count * std::max(nb, 1)));

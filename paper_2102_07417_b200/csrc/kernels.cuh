@@ -1381,7 +1381,7 @@ __device__ __forceinline__ double ref_sum_fixed(const double (&p)[FL], int len)
 {
     const int n = len - 1;
     double res = 0.0;
-    if (n < 8) {
+    if (FL <= 8 || n < 8) {  // len <= FL: arrays of <= 8 products never reach the 8-accumulator part
 #pragma unroll
         for (int k = 1; k < (FL < 8 ? FL : 8); ++k)
             if (k <= n) res = add(res, p[k]);
@@ -1616,14 +1616,19 @@ struct DictArgs {
     // interior of a stencil operator) reads no table at all
     int mcls, mlen;
     int32_t mrel[8];
+    long long moff[8];  // mrel in bytes (64-bit: the interior path adds it to the row's x pointer)
     double mval[8];
 };
 
-// ROWS rows per thread and step (rows row, row + nthreads, ...): all their gathers are issued
-// before the first sum, so a thread keeps ROWS x len loads in flight -- on the 4 M-row
-// constant-coefficient operators the one-row kernel waited on one row's gathers at a time
-// (ncu: long-scoreboard stalls, 49% of the warp slots occupied, 2.0 TB/s).
-template <int EPI, int FL, bool WIDE, int ROWS>
+// ROWS rows per thread and step (rows row, row + nthreads, ...), all gathers issued before the
+// first sum.  Only ROWS = 1 is instantiated: two rows helped the table-driven path (G0 27.6 ->
+// 20.2 us) but lose to one row once the interior path is lean (16.5 us); a contiguous row chunk
+// per CTA (x lines reused from L1: hit rate 27 -> 50%, 37% fewer L2 sectors, ncu) was never faster.
+// ML > 0: the most frequent class has ML entries (compile time): the interior path is ML
+// independent gathers at constant-bank offsets, ML products with constant-bank values and
+// the reference-order sum of exactly ML terms -- no predicates, no table (ncu on the general
+// path: 61% of the issue slots busy with 145 instructions per 32 rows).
+template <int EPI, int FL, bool WIDE, int ROWS, int ML = 0>
 __global__ void __launch_bounds__(VEC_SPMV_THREADS, (ROWS > 1 || FL > 8) ? 4 : 5) spmv_dict(const SpmvArgs a, const DictArgs d,
                                                                                           int nrows)
 {
@@ -1660,6 +1665,7 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, (ROWS > 1 || FL > 8) ? 4 : 5
     // warp-uniform trip count (the vote below needs every lane): lanes beyond the last row idle
     for (; row0 - (int)(threadIdx.x & 31) < rend; row0 += ROWS * rstep) {
         int len[ROWS];
+        bool fast[ROWS];
         double p[ROWS][FL], bv[ROWS], wv[ROWS];
 #pragma unroll
         for (int q = 0; q < ROWS; ++q) {
@@ -1667,25 +1673,25 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, (ROWS > 1 || FL > 8) ? 4 : 5
             const int c = ncl[q];
             ncl[q] = cls_of(row + ROWS * rstep);  // the class one step ahead
             AMG_CHECK(c >= 0 && c < d.ncls);
-            const int rb = sbeg[c];
-            len[q] = row < rend ? sbeg[c + 1] - rb : 0;
-            AMG_CHECK(len[q] >= 0 && len[q] <= FL && rb + len[q] <= d.nent);
             bv[q] = wv[q] = 0.0;
             if (row < rend) {
                 if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv[q] = a.b[row];
                 if (want_dot && !self_dot) wv[q] = a.dotw[row];
             }
-            bool fast = false;
-            if constexpr (FL <= 8) fast = __all_sync(0xffffffffu, c == d.mcls && row < rend);
-            if (fast) {
-                if constexpr (FL <= 8) {
+            fast[q] = false;
+            len[q] = 0;
+            if constexpr (ML > 0) fast[q] = __all_sync(0xffffffffu, c == d.mcls && row < rend);
+            if (fast[q]) {
+                if constexpr (ML > 0) {
+                    const char *xr = reinterpret_cast<const char *>(x + row);
 #pragma unroll
-                    for (int k = 0; k < FL; ++k) {
-                        p[q][k] = 0.0;
-                        if (k < d.mlen) p[q][k] = prod(d.mval[k], __ldg(x + (row + d.mrel[k])));
-                    }
+                    for (int k = 0; k < ML; ++k)
+                        p[q][k] = prod(d.mval[k], __ldg(reinterpret_cast<const double *>(xr + d.moff[k])));
                 }
             } else {
+                const int rb = sbeg[c];
+                len[q] = row < rend ? sbeg[c + 1] - rb : 0;
+                AMG_CHECK(len[q] >= 0 && len[q] <= FL && rb + len[q] <= d.nent);
 #pragma unroll
                 for (int k = 0; k < FL; ++k) {
                     p[q][k] = 0.0;
@@ -1697,7 +1703,15 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, (ROWS > 1 || FL > 8) ? 4 : 5
         for (int q = 0; q < ROWS; ++q) {
             const int row = row0 + q * rstep;
             if (row < rend) {
-                const double sum = ref_sum_fixed<FL>(p[q], len[q]);
+                double sum;
+                if (ML > 0 && fast[q]) {
+                    double t[ML > 0 ? ML : 1];
+#pragma unroll
+                    for (int k = 0; k < ML; ++k) t[k] = p[q][k];
+                    sum = ref_sum_fixed<(ML > 0 ? ML : 1)>(t, ML);
+                } else {
+                    sum = ref_sum_fixed<FL>(p[q], len[q]);
+                }
                 double yv;
                 if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv[q], sum);
                 else if constexpr (EPI == EPI_AXPYW) yv = add(bv[q], __dmul_rn(a.omega, sum));
