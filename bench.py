@@ -4,11 +4,12 @@ GFLOP/s and HBM-roofline fraction on B200).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl amgb200|reference]
 
-Workload (``config.workload``): BASELINE configs[1] -- 3-D heterogeneous
-diffusion, 27-point stencil on 128^3 (2,097,152 unknowns, 55,742,968 nnz),
-lognormal sigma=2 conductivity, rhs uniform(-1,1) seed 42, classical AMG +
-FSAI from the reference's setup (frozen in hier_cache/),
-PCG to rtol 1e-8.  A step = one complete PCG solve from x0 = 0 (initial
+Workload (``config.workload``): the largest single-GPU BASELINE configuration
+whose reference setup could be run -- configs[3], anisotropic 3-D Poisson,
+7-point stencil on 256^3 (16,777,216 unknowns, 117,047,296 nnz), eps = 1e-3 in
+z, rhs uniform(-1,1) seed 42, classical AMG + FSAI from the reference's setup
+(frozen in hier_cache/), PCG to rtol 1e-8.  ``--config`` runs
+configs 1-3 (c1_poisson7_64, c2_hetero27_128, c3_elasticity_64) the same way.  A step = one complete PCG solve from x0 = 0 (initial
 residual, every iteration, final true residual) with b already resident in
 HBM; ``value`` = device time of the K solves / total iterations (ms per PCG
 iteration; lower is better).  ``e2e`` = the same through the public API with
@@ -34,13 +35,17 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-DEFAULT_CONFIG = "c2_hetero27_128"
+DEFAULT_CONFIG = "c4_rtanis7_256"
 METRIC = "PCG+AMG solve ms/iter (GFLOP/s, HBM-roofline fraction alongside)"
 WORKLOADS = {
     "c1_poisson7_64": "config 1: 3-D Poisson 7-pt 64^3 (262,144 unknowns), FSAI + classical AMG, PCG 1e-8",
     "c2_hetero27_128": ("config 2: 3-D heterogeneous diffusion 27-pt 128^3 (2,097,152 unknowns, 55.7 M nnz), "
                         "lognormal sigma=2, FSAI + classical AMG, PCG 1e-8"),
-    "c4_rtanis7_256": "config 4: anisotropic Poisson 7-pt 256^3 eps=1e-3 (16.8 M unknowns), PCG 1e-8",
+    "c3_elasticity_64": ("config 3: 3-D linear elasticity Q1 hexahedra 64^3 elements (811,200 dofs, 63.7 M nnz), "
+                         "lognormal E sigma=1, FSAI + BAMG + rigid-body modes, PCG 1e-8"),
+    "c4_rtanis7_256": ("config 4: anisotropic 3-D Poisson 7-pt 256^3 eps=1e-3 in z (16,777,216 unknowns, 117.0 M nnz), "
+                       "FSAI + classical AMG, PCG 1e-8"),
+    "t_rtanis7_256x64": "stand-in: config 4's x-y planes, 64 of its 256 planes (4,194,304 unknowns)",
 }
 
 
@@ -132,9 +137,9 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(config, layout=None):
+def ncu_traffic(config, layout=None, matrix=None):
     """dram bytes per launch of the dominant kernel from the committed ncu summary, if any
-    (only when the summary was captured on the same device layout)."""
+    (only when the summary was captured on the same matrix and device layout)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
@@ -142,6 +147,8 @@ def ncu_traffic(config, layout=None):
         with open(p) as f:
             d = json.load(f).get(config, {})
         if layout is not None and d.get("layout") not in (None, layout):
+            return None
+        if matrix is not None and d.get("matrix", "L0.a") != matrix:
             return None
         return d.get("dram_bytes_per_launch")
     except Exception:
@@ -321,18 +328,46 @@ def run_amgb200(args):
     e2e_ms_iter = float(np.median(e_per_iter))
     e2e_mean = float(np.mean(e_per_iter))
 
-    # dominant kernel: SpMV on A0, timed alone with CUDA events on the library stream.
-    # Roofline numerator = the bytes the chosen layout must stream per launch
-    # (amg_matrix_bytes: stored values + indices + x read once + y written once).
-    a0 = plan.mats[(0, "a")].csr if plan is not None else h.levels[0].a
-    k_ms = dh.time_spmv(0, "a", reps=50)
-    k_stored, k_vec = dh.matrix_bytes(0, "a")
+    # dominant kernel: the SpMV with the largest share of a PCG iteration -- every matrix of the
+    # levels above the cluster tail timed alone with CUDA events on the library stream
+    # (amg_time_spmv), weighted by its applications per iteration (A: 2 per V-cycle + 1 outside
+    # at level 0, G / G^T: 2, P / P^T: 1).  Roofline numerator = the bytes the chosen layout
+    # must stream per launch (amg_matrix_bytes: stored values + indices + x once + y once).
+    apps = {"a": 2, "g": 2, "gt": 2, "p": 1, "pt": 1}
+    shares = []
+    if plan is None:
+        tail_level = dh.stats()["tail_level"]
+        top = tail_level if tail_level > 0 else len(h.levels) - 1
+        for k, lv in enumerate(h.levels[:max(top, 1)]):
+            slots = ["a"]
+            if lv.p is not None:
+                slots += ["p", "pt"]
+                if lv.smoother is not None and getattr(lv.smoother, "gmat", None) is not None:
+                    slots += ["g", "gt"]
+            for slot in slots:
+                try:
+                    t_ms = dh.time_spmv(k, slot, reps=10)
+                except Exception:
+                    continue
+                n_app = apps[slot] + (1 if (k == 0 and slot == "a") else 0)
+                shares.append((n_app * t_ms, k, slot, t_ms, n_app))
+    if shares:
+        shares.sort(reverse=True)
+        _, dk, dslot, _, dn = shares[0]
+    else:
+        dk, dslot, dn = 0, "a", 3
+    dm = (plan.mats[(dk, dslot)].csr if plan is not None else
+          {"a": h.levels[dk].a, "p": h.levels[dk].p, "pt": h.levels[dk].pt,
+           "g": getattr(h.levels[dk].smoother, "gmat", None), "gt": getattr(h.levels[dk].smoother, "gmat_t", None)}[dslot])
+    k_ms = dh.time_spmv(dk, dslot, reps=50)
+    k_stored, k_vec = dh.matrix_bytes(dk, dslot)
     k_bytes = k_stored + k_vec
-    csr_bytes = 12 * a0.nnz + 4 * (a0.nrows + 1) + 8 * a0.ncols + 8 * a0.nrows
+    csr_bytes = 12 * dm.nnz + 4 * (dm.nrows + 1) + 8 * dm.ncols + 8 * dm.nrows
     peak, peak_src = peaks()
     achieved = k_bytes / (k_ms * 1e-3) / 1e9
-    k_layout = dh.layout(0, "a") if plan is None else "partitioned"
-    traffic = ncu_traffic(args.config, k_layout)
+    k_layout = dh.layout(dk, dslot) if plan is None else "partitioned"
+    k_name = f"L{dk}.{dslot}"
+    traffic = ncu_traffic(args.config, k_layout, k_name)
     lay_iter = layout_bytes_per_iter(dh, h) if plan is None else None
     line = {
         "metric": METRIC,
@@ -374,8 +409,12 @@ def run_amgb200(args):
         },
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": f"A0 SpMV (plain epilogue), device layout '{k_layout}'",
+            "traffic": traffic,
+            "kernel": (f"SpMV of {k_name} ({dm.nrows} rows, {dm.nnz} nnz; plain epilogue), device layout '{k_layout}': "
+                       f"the largest share of an iteration ({dn} applications)"),
             "bytes_per_launch": k_bytes, "ms_per_launch": k_ms, "peak_source": peak_src,
+            "iteration_share": [{"matrix": f"L{k}.{sl}", "ms_per_launch": t, "applications": n, "ms_per_iter": w}
+                                for w, k, sl, t, n in shares[:8]],
             "note": ("achieved = bytes the layout must stream per launch (stored values + indices + x once + y "
                      "once, amg_matrix_bytes) / CUDA-event time of the launch; traffic = ncu dram bytes of one "
                      "launch from profiles/ncu_summary.json (null when not captured on this layout)"),

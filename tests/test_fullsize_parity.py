@@ -22,7 +22,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CACHE = os.path.join(ROOT, "hier_cache")
 CONFIGS = ["c1_poisson7_64", "c2_hetero27_128", "c3_elasticity_64", "c4_rtanis7_256"]
 # caches that may legitimately be absent from a snapshot (everything else must ship)
-OPTIONAL = {"c4_rtanis7_256": "its reference setup takes ~2.5 h; tools/export_hierarchy.py c4_rtanis7_256 --solve"}
+OPTIONAL = {}
+# the opt-in tail variants re-upload the hierarchy: skipped above this many rows (config 4: 16.8 M)
+VARIANT_MAX_ROWS = 4_000_000
 
 
 def _load(name):
@@ -101,6 +103,8 @@ def test_fullsize_tail_dsm_bit_identical(full):
     import paper_2102_07417_b200 as amg
 
     name, h, dh = full
+    if h.levels[0].a.nrows > VARIANT_MAX_ROWS:
+        pytest.skip("opt-in variant: checked on configs 1-3")
     dh2 = amg.DeviceHierarchy.from_reference(h, options={"tail_dsm": 1})
     y = np.random.default_rng(31).uniform(-1, 1, h.levels[0].a.nrows)
     np.testing.assert_array_equal(dh2.vcycle(y), dh.vcycle(y))
@@ -112,6 +116,8 @@ def test_fullsize_wider_tail_bit_identical(full):
     import paper_2102_07417_b200 as amg
 
     name, h, dh = full
+    if h.levels[0].a.nrows > VARIANT_MAX_ROWS:
+        pytest.skip("opt-in variant: checked on configs 1-3")
     dh2 = amg.DeviceHierarchy.from_reference(h, options={"tail_nnz": 2_000_000, "tail_pcap": 4096})
     y = np.random.default_rng(37).uniform(-1, 1, h.levels[0].a.nrows)
     np.testing.assert_array_equal(dh2.vcycle(y), dh.vcycle(y))
