@@ -83,6 +83,7 @@ struct DevMat {
     int s_grid = 0;
     int32_t *ucol_s = nullptr;
     uint8_t *ulen_s = nullptr;
+    uint8_t *uperm_s = nullptr;  // PLEN layouts sorted inside each slice: slot -> row within the slice
     int uW = 0, u_grid = 0, u_plen = 0;  // u_plen: padding slots skipped (short ragged rows)
     int nudiag = 0, sym_grid = 0, sym_fl = 0, symf_grid = 0, sym_blocked = 0;  // sym_fl: fixed-slot kernel width (0: none)
     int32_t *pstart = nullptr;   // padded-aligned layout (spmv_vec), nullptr if unused
@@ -249,11 +250,12 @@ struct amg_handle {
     int sells_plen = 1;           // sorted SELL: predicate slot loads on the row length (padding moves no bytes)
     int sells_max_pad = 60;       // % padding allowed for the sorted layout (padding slots are skipped with sells_plen)
     double sells_min_avg = 4.0;   // ... for matrices averaging at least this many entries per row
-    int64_t sells_max_rows = 1 << 20;  // ... and at most this many rows (sorting costs fine-grid rows their gather
+    int64_t sells_max_rows = 2000000;  // ... and at most this many rows (sorting costs fine-grid rows their gather
                                        // locality: config-2 G^T_0 85 -> 134 us; coarse A_1 18 -> 13 us)
     int rz_sep = 0;               // PCG: r.z in a separate dot kernel instead of the V-cycle's last SpMV
     int vec_minb = 4;             // padded-CSR kernel: min CTAs per SM (register budget) 4, 5 or 6
     int sellu_short = 1;          // ... and for rows of <= 8 entries at any padding, padding slots skipped
+    int sellu_sort = 1;           // skipped-padding uniform SELL: rows sorted by length inside each slice
     int sellu = 1;                // uniform-width SELL-32 for rows of <= 16 entries padding <= 10% (e.g. FSAI G)
     int symd_chunked = 0;         // symmetric kernels: contiguous row chunk per CTA (measured slower than grid-stride)
     int symd_fixed = 1;           // fixed-slot symmetric kernel: 1 rows <= 8 entries (7-point), 2 also <= 32 (27-point:
@@ -706,7 +708,7 @@ static int spmv_range(amg_t *h, const DevMat &M, int lay, const SpmvArgs &a, int
         g = cap(M.s_grid, ((count + 31) / 32 + 7) / 8);
         TRY(launch_k(h, spmv_sells_fn(epi, h->sells_plen), g, VEC_SPMV_THREADS, 0, a, qa, count));
     } else if (lay == AMG_LAYOUT_SELL_UNIFORM) {
-        SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW};
+        SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW, M.uperm_s};
         g = cap(M.u_grid, (count + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS);
         TRY(launch_k(h, spmv_sellu_fn(epi, M.uW, M.u_plen), g, VEC_SPMV_THREADS, 0, a, ua, count));
     } else if (lay == AMG_LAYOUT_WCSR) {
@@ -846,7 +848,7 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         TRY(launch_k(h, spmv_sells_fn(epi, h->sells_plen), grid_cap ? std::min(grid_cap, M.s_grid) : M.s_grid, VEC_SPMV_THREADS, 0, a,
                      qa, (int)M.nrows));
     } else if (M.uval_s && h->sellu) {
-        SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW};
+        SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW, M.uperm_s};
         TRY(launch_k(h, spmv_sellu_fn(epi, M.uW, M.u_plen), grid_cap ? std::min(grid_cap, M.u_grid) : M.u_grid, VEC_SPMV_THREADS, 0,
                      a, ua, (int)M.nrows));
     } else if (M.sbeg) {
@@ -1482,7 +1484,7 @@ void amg_destroy(amg_t *h)
     };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s); F(M.dcls); F(M.dbeg); F(M.drel); F(M.dval);
+            F(M.off); F(M.col); F(M.val); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.uperm_s); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s); F(M.dcls); F(M.dbeg); F(M.drel); F(M.dval);
             symd_slot_give(h->device, M.sym_slot);
             M.sym_slot = -1;
             symd_tab_give(h->device, M.sym_tab, M.sym_ntab);
@@ -1545,6 +1547,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "vec_minb") { h->vec_minb = (int)value; return AMG_OK; }
     if (k == "sellu_short") { h->sellu_short = value ? 1 : 0; return AMG_OK; }
     if (k == "sellu") { h->sellu = value ? 1 : 0; return AMG_OK; }
+    if (k == "sellu_sort") { h->sellu_sort = value ? 1 : 0; return AMG_OK; }
     if (k == "symd_fixed") { h->symd_fixed = (int)value; return AMG_OK; }
     if (k == "symd_chunked") { h->symd_chunked = value ? 1 : 0; return AMG_OK; }
     if (k == "coarse_pipe") { h->coarse_pipe = (int)value; if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; } return AMG_OK; }
@@ -2429,11 +2432,23 @@ int amg_finalize(amg_t *h)
                     const size_t tot = (size_t)ns * 32 * W;
                     std::vector<double> sv(tot, 0.0);
                     std::vector<int32_t> sc(tot, 0);
-                    std::vector<uint8_t> ln(M.nrows + 16, 0);
-                    for (int64_t r = 0; r < M.nrows; ++r) {
+                    std::vector<uint8_t> ln(ns * 32 + 16, 0);
+                    // skipped padding (plen): rows sorted by length inside each slice, so the live
+                    // lanes of a slot are a prefix and dead lanes cost no sectors
+                    const bool sorted = plen && h->sellu_sort;
+                    std::vector<uint8_t> pm(sorted ? ns * 32 + 16 : 0, 0);
+                    for (int64_t sl = 0; sl < ns; ++sl) {
+                      int ord[32];
+                      for (int l = 0; l < 32; ++l) ord[l] = l;
+                      auto rl = [&](int l) { return sl * 32 + l < M.nrows ? off32[sl * 32 + l + 1] - off32[sl * 32 + l] : -1; };
+                      if (sorted) std::stable_sort(ord, ord + 32, [&](int x1, int x2) { return rl(x1) > rl(x2); });
+                      for (int l = 0; l < 32; ++l) {
+                        const int64_t r = sl * 32 + ord[l];   // row held by slot sl * 32 + l
+                        if (sorted) pm[sl * 32 + l] = (uint8_t)ord[l];
+                        if (r >= M.nrows) continue;
                         const int32_t len = off32[r + 1] - off32[r];
-                        ln[r] = (uint8_t)len;
-                        const int64_t b0 = (r >> 5) * 32 * W + (r & 31);
+                        ln[sl * 32 + l] = (uint8_t)len;
+                        const int64_t b0 = sl * 32 * W + l;
                         for (int32_t k = 0; k < W; ++k) {
                             const int64_t q = b0 + 32 * (int64_t)k;
                             if (k < len) {
@@ -2443,12 +2458,17 @@ int amg_finalize(amg_t *h)
                                 sc[q] = (int32_t)std::min<int64_t>(r, M.ncols - 1);  // padding: any valid column
                             }
                         }
+                      }
+                    }
+                    if (sorted) {
+                        TRY(dalloc(&M.uperm_s, pm.size()));
+                        CK(cudaMemcpy(M.uperm_s, pm.data(), pm.size(), cudaMemcpyHostToDevice));
                     }
                     TRY(dalloc(&M.uval_s, tot));
                     TRY(dalloc(&M.ucol_s, tot));
                     TRY(dalloc(&M.ulen_s, ln.size()));
                     // padding slots are loaded unless skipped (plen)
-                    M.lbytes[AMG_LAYOUT_SELL_UNIFORM] = (plen ? M.nnz : (int64_t)tot) * 12 + (int64_t)ln.size();
+                    M.lbytes[AMG_LAYOUT_SELL_UNIFORM] = (plen ? M.nnz : (int64_t)tot) * 12 + (int64_t)M.nrows * (sorted ? 2 : 1);
                     CK(cudaMemcpy(M.uval_s, sv.data(), tot * sizeof(double), cudaMemcpyHostToDevice));
                     CK(cudaMemcpy(M.ucol_s, sc.data(), tot * sizeof(int32_t), cudaMemcpyHostToDevice));
                     CK(cudaMemcpy(M.ulen_s, ln.data(), ln.size(), cudaMemcpyHostToDevice));

@@ -1743,6 +1743,12 @@ struct SellUArgs {
     const int32_t *col;
     const uint8_t *len;
     int W;
+    // PLEN layouts: the rows of each 32-row slice sit in its lanes sorted by length (descending,
+    // stable), perm[slot] = the row's position inside the slice.  The live lanes of a slot are then
+    // a prefix, so skipping the padding skips whole sectors (unsorted, slot 2 of an interpolation
+    // operator has ~40% of its lanes live but touches ~87% of its sectors); the warp still works
+    // on the same 32 neighbouring rows and the y store stays one 256-byte segment.  nullptr: slot = row.
+    const uint8_t *perm;
 };
 
 // Software-pipelined: the next row's columns and length are loaded one
@@ -1767,17 +1773,19 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, FL <= 4 ? 6 : FL <= 9 ? 4 : 
     double dacc = 0.0;
     int v = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x;
     int c[FL];
-    int len = 0;
-    auto fetch = [&](int r) {
+    int len = 0, nrowid = 0;
+    auto fetch = [&](int r) {  // r: slot
         const int base = (r >> 5) * W32 + (r & 31);
         len = __ldg(u.len + r);
+        nrowid = (PLEN && u.perm) ? ((r & ~31) | (int)__ldg(u.perm + r)) : r;
 #pragma unroll
-        for (int k = 0; k < FL; ++k) c[k] = (k < (PLEN ? len : u.W)) ? __ldg(u.col + base + 32 * k) : r;
+        for (int k = 0; k < FL; ++k) c[k] = (k < (PLEN ? len : u.W)) ? __ldg(u.col + base + 32 * k) : 0;
     };
     if (v < nrows) fetch(vrow(a, v));
     for (; v < nrows; v += nthreads) {
-        const int row = vrow(a, v);
-        const int base = (row >> 5) * W32 + (row & 31);
+        const int slot = vrow(a, v);
+        const int row = nrowid;
+        const int base = (slot >> 5) * W32 + (slot & 31);
         double p[FL];
 #pragma unroll
         for (int k = 0; k < FL; ++k)
