@@ -131,6 +131,10 @@ int amg_smoother(amg_t *h, int level, const double *b, const double *x0, double 
 int amg_coarse_solve(amg_t *h, const double *y, double *z, int on_device);
 /* z = vcycle(h, y) from level 0. */
 int amg_vcycle(amg_t *h, const double *y, double *z, int on_device);
+/* z = vcycle(h, y, level) (hierarchy.py:294: the cycle restarted at `level`, vectors of that level's
+ * size).  Levels below the first level of the cluster-tail kernel cannot be entered separately
+ * (AMG_E_STATE) unless the tail is switched off (option "tail_nnz" = 0). */
+int amg_vcycle_level(amg_t *h, int level, const double *y, double *z, int on_device);
 
 /* PCG with the V-cycle preconditioner (krylov.py:40-92).  x0 may be NULL.
  * history: max_iters+1 doubles or NULL; *hist_len = entries written.

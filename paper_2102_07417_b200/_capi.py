@@ -24,7 +24,7 @@ EXPORTS = (
     "amg_create", "amg_destroy", "amg_last_error", "amg_get_version", "amg_set_levels",
     "amg_set_partition", "amg_upload_matrix", "amg_set_smoother", "amg_upload_coarse",
     "amg_set_cycle", "amg_finalize", "amg_local_rows", "amg_spmv", "amg_smoother",
-    "amg_coarse_solve", "amg_vcycle", "amg_pcg", "amg_get_stats", "amg_set_option", "amg_time_spmv",
+    "amg_coarse_solve", "amg_vcycle", "amg_vcycle_level", "amg_pcg", "amg_get_stats", "amg_set_option", "amg_time_spmv",
     "amg_nccl_unique_id", "amg_set_halo", "amg_set_agglomeration", "amg_bicgstab",
     "amg_matrix_layout", "amg_matrix_bytes",
     "amg_device_galerkin", "amg_device_transpose", "amg_csr_result_shape", "amg_csr_result_fetch",
@@ -97,6 +97,7 @@ def lib():
         "amg_smoother": (I32, [P, I32, P, P, P, I32, I32]),
         "amg_coarse_solve": (I32, [P, P, P, I32]),
         "amg_vcycle": (I32, [P, P, P, I32]),
+        "amg_vcycle_level": (I32, [P, I32, P, P, I32]),
         "amg_pcg": (I32, [P, P, P, D, I32, I32, P, P, P, P, P, P, P, I32]),
         "amg_get_stats": (I32, [P, ctypes.POINTER(Stats)]),
         "amg_set_option": (I32, [P, ctypes.c_char_p, I64]),

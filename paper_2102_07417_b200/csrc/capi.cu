@@ -2717,6 +2717,32 @@ int amg_vcycle(amg_t *h, const double *y, double *z, int on_device)
     return AMG_OK;
 }
 
+int amg_vcycle_level(amg_t *h, int level, const double *y, double *z, int on_device)
+{
+    TRY(check_final(h));
+    if (h->container) return fail(AMG_E_STATE, "matrix container handle: no hierarchy uploaded");
+    if (!y || !z) return fail(AMG_E_ARG, "amg_vcycle_level: NULL vector");
+    const int nl = (int)h->lv.size();
+    if (level < 0 || level >= nl) return fail(AMG_E_ARG, "amg_vcycle_level: level out of range");
+    if (h->nranks > 1 && level > 0) return fail(AMG_E_STATE, "amg_vcycle_level: level > 0 needs a single-GPU handle");
+    if (h->tail_level > 0 && level > h->tail_level)
+        return fail(AMG_E_STATE, "amg_vcycle_level: levels below the first cluster-tail level run inside the tail kernel "
+                                 "(start at or above it, or set option tail_nnz = 0)");
+    const int64_t n = h->lv[level].n;
+    if (h->tail_level > 0 && level == h->tail_level) {
+        // the tail kernel works on the level's own vectors
+        TRY(to_dev(h, h->lv[level].y, y, n, on_device));
+        TRY(enqueue_vcycle(h, level, h->lv[level].y, h->lv[level].x, nullptr, FIN_NONE, nullptr));
+        TRY(from_dev(h, z, h->lv[level].x, n, on_device));
+    } else {
+        TRY(to_dev(h, h->tmp_in, y, n, on_device));
+        TRY(enqueue_vcycle(h, level, h->tmp_in, h->tmp_out, nullptr, FIN_NONE, nullptr));
+        TRY(from_dev(h, z, h->tmp_out, n, on_device));
+    }
+    TRY(sync_stream(h));
+    return AMG_OK;
+}
+
 int amg_pcg(amg_t *h, const double *b, const double *x0, double rtol, int max_iters, int recompute_every,
             double *x_out, int *n_iter, double *relres, int *converged, double *history, int *hist_len,
             double *curvature_at_fail, int on_device)

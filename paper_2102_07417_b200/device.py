@@ -43,6 +43,14 @@ def _is_cuda_tensor(x):
     return hasattr(x, "is_cuda") and bool(x.is_cuda)
 
 
+class DeviceSmoother:
+    """Level smoother handle: what ``Level.smoother`` is to the reference's ``apply_smoother``."""
+
+    def __init__(self, dh, level):
+        self.dh = dh
+        self.level = level
+
+
 class DeviceMatrix:
     """A matrix slot of the device hierarchy; calling it is ``spmv``."""
 
@@ -316,12 +324,20 @@ class DeviceHierarchy:
         C.check(C.lib().amg_coarse_solve(self._h, C.ptr(yin), C.ptr(z), dev), "coarse_solve")
         return z
 
-    def apply_vcycle(self, y):
-        """``vcycle(h, y)`` (``amgkit/hierarchy.py:294-312``)."""
-        n = self.levels[0]["n"]
+    def smoother(self, level):
+        """The level's smoother as an object (``amgkit.smoothers.Smoother``'s role in
+        ``apply_smoother(sm, A, b, x0, steps)``); the device owns the factors."""
+        return DeviceSmoother(self, int(level))
+
+    def apply_vcycle(self, y, level=0):
+        """``vcycle(h, y, level)`` (``amgkit/hierarchy.py:294-312``)."""
+        n = self.levels[level]["n"]
         yin, dev = self._vec_in(y, n, "vcycle", (n, n))
         z = self._vec_out(yin, n)
-        C.check(C.lib().amg_vcycle(self._h, C.ptr(yin), C.ptr(z), dev), "vcycle")
+        if level == 0:
+            C.check(C.lib().amg_vcycle(self._h, C.ptr(yin), C.ptr(z), dev), "vcycle")
+        else:
+            C.check(C.lib().amg_vcycle_level(self._h, int(level), C.ptr(yin), C.ptr(z), dev), "vcycle")
         return z
 
     def time_spmv(self, level, slot, reps=20):

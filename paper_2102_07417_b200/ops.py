@@ -11,8 +11,7 @@ float64 tensors are used in place.
 """
 from __future__ import annotations
 
-from .device import DeviceHierarchy, DeviceMatrix
-from .errors import AmgError
+from .device import DeviceHierarchy, DeviceMatrix, DeviceSmoother
 
 __all__ = ["spmv", "vcycle", "apply_smoother", "coarse_solve"]
 
@@ -26,16 +25,19 @@ def spmv(A, x):
 def vcycle(h, y, level=0):
     if not isinstance(h, DeviceHierarchy):
         raise TypeError("vcycle: h must be a DeviceHierarchy (no CPU fallback)")
-    if level != 0:
-        raise AmgError("vcycle: the device path starts V-cycles at level 0")
-    return h.apply_vcycle(y)
+    return h.apply_vcycle(y, level)
 
 
 def apply_smoother(sm, A, b, x0, steps):
-    """``sm`` is the level index of the smoother (the device owns the factors)."""
+    """``sm``: ``dh.smoother(k)`` (or the level index, or None for A's level); ``A``: ``dh.matrix(k, "a")``."""
     if not isinstance(A, DeviceMatrix) or A.slot != "a":
         raise TypeError("apply_smoother: A must be the level operator DeviceMatrix")
-    level = A.level if sm is None else int(sm)
+    if isinstance(sm, DeviceSmoother):
+        if sm.dh is not A.dh or sm.level != A.level:
+            raise TypeError("apply_smoother: smoother and operator belong to different levels")
+        level = sm.level
+    else:
+        level = A.level if sm is None else int(sm)
     return A.dh.apply_smoother(level, b, x0, steps)
 
 

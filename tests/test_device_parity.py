@@ -574,6 +574,33 @@ def test_run_solve_report_and_cli(tmp_path):
     assert main(["solve", "--cache", str(tmp_path / "missing")]) == 1
 
 
+@pytest.mark.parametrize("name", ["poisson7_12", "hetero27_10", "elasticity_3_bamg", "poisson2d_16_jacobi"])
+@pytest.mark.parametrize("tail", [0, 1])
+def test_vcycle_from_any_level_and_smoother_objects(name, tail):
+    # vcycle(h, y, level=k) (hierarchy.py:294) and apply_smoother(sm, A, b, x0, steps) with the
+    # level's smoother object, as the reference signatures have them
+    c = load_case(name)
+    h = c["h"]
+    dh = amg.DeviceHierarchy.from_reference(h, options=({} if tail else {"tail_nnz": 0}))
+    tl = dh.stats()["tail_level"]
+    rng = np.random.default_rng(9)
+    for k in range(h.n_levels):
+        y = rng.uniform(-1, 1, h.levels[k].a.nrows)
+        if tl > 0 and k > tl:
+            with pytest.raises(amg.AmgError):
+                amg.vcycle(dh, y, level=k)
+            continue
+        assert _relerr(amg.vcycle(dh, y, level=k), O.vcycle(h, y, k)) <= 1e-12
+    for k in range(h.n_levels - 1):
+        b = rng.uniform(-1, 1, h.levels[k].a.nrows)
+        got = amg.apply_smoother(dh.smoother(k), dh.matrix(k, "a"), b, None, 2)
+        want = O.apply_smoother(h.levels[k].smoother, h.levels[k].a, b, np.zeros_like(b), 2)
+        np.testing.assert_array_equal(got, want)
+    with pytest.raises(TypeError):
+        amg.apply_smoother(dh.smoother(0), dh.matrix(1, "a"), np.zeros(h.levels[1].a.nrows), None, 1)
+    dh.close()
+
+
 @pytest.mark.parametrize("kind", ["uniform", "ragged", "padded", "wcsr", "small"])
 def test_interior_boundary_split_spmv_bit_identical(kind):
     # the multi-GPU overlap schedule on one GPU (overlap_test): interior rows
@@ -598,7 +625,9 @@ def test_interior_boundary_split_spmv_bit_identical(kind):
     x = rng.uniform(-1, 1, n)
     want = O.spmv(m, x)
     dh = amg.DeviceHierarchy.from_matrices([m], options={"overlap_test": 1, "dict": 0, "symm": 0,
-                                                         "wcsr": int(kind != "padded")})
+                                                         "wcsr": int(kind != "padded"),
+                                                         # 1.1 M rows: inside the sorted-SELL row limit (2 M)
+                                                         "sells": int(kind not in ("padded", "wcsr"))})
     lay = dh.layout(0, "a")
     assert lay == {"uniform": "sell_uniform", "ragged": "sell_sorted", "padded": "padded", "wcsr": "wcsr",
                    "small": "csr"}[kind]
