@@ -85,7 +85,10 @@ struct DevMat {
     uint8_t *ulen_s = nullptr;
     uint8_t *uperm_s = nullptr;  // PLEN layouts sorted inside each slice: slot -> row within the slice
     int uW = 0, u_grid = 0, u_plen = 0;  // u_plen: padding slots skipped (short ragged rows)
-    int nudiag = 0, sym_grid = 0, sym_fl = 0, symf_grid = 0, sym_blocked = 0;  // sym_fl: fixed-slot kernel width (0: none)
+    int nudiag = 0, sym_grid = 0, sym_fl = 0, symf_grid = 0, sym_blocked = 0;
+    bool sym_fast_on = false;    // interior 27-entry pattern with parameter-bank offsets (spmv_symd27)
+    SymFast sym_fast = {};
+    int sym27_grid = 0;  // sym_fl: fixed-slot kernel width (0: none)
     int32_t *pstart = nullptr;   // padded-aligned layout (spmv_vec), nullptr if unused
     double *pval = nullptr;
     int32_t *pcol = nullptr;
@@ -261,6 +264,7 @@ struct amg_handle {
     int symd_fixed = 1;           // fixed-slot symmetric kernel: 1 rows <= 8 entries (7-point), 2 also <= 32 (27-point:
                                   // measured slower than the round-by-round kernel on config 2), 0 off
     int symm = 1;                 // symmetric stencil layout (upper diagonals) for bitwise-symmetric pattern operators
+    int symd_fast = 1;            // symmetric layout: interior 27-entry rows through spmv_symd27 (offsets as kernel parameters)
     int dict_main = 1;            // spmv_dict: warps whose rows all have the most frequent class take its entries from kernel parameters
     int dict = 1;                 // row-class dictionary layout for operators with few distinct rows
     int wcsr = 1;                 // large matrices averaging >= pad_min entries: warp-cooperative CSR instead of the padded copy
@@ -347,6 +351,19 @@ static SpmvSymFn spmv_symd_fn(int epi, int minb = 5, bool blk = false, bool tsm 
     default: AMG_Y(EPI_ADD)
     }
 #undef AMG_Y
+}
+
+typedef void (*SpmvSym27Fn)(const SpmvArgs, const SymArgs, const SymFast, int);
+
+static SpmvSym27Fn spmv_symd27_fn(int epi)
+{
+    switch (epi) {
+    case EPI_PLAIN: return spmv_symd27<EPI_PLAIN>;
+    case EPI_RESID: return spmv_symd27<EPI_RESID>;
+    case EPI_AXPYW: return spmv_symd27<EPI_AXPYW>;
+    case EPI_SETW: return spmv_symd27<EPI_SETW>;
+    default: return spmv_symd27<EPI_ADD>;
+    }
 }
 
 static SpmvSymFn spmv_symd_fixed_fn(int epi, int fl, int minb = 0, bool blk = false)
@@ -838,7 +855,13 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
                    M.sym_tab, M.sym_ntab, M.npat};
         const bool tsm = h->symd_tsm && M.sym_blocked && !fx;
         const size_t tsm_bytes = tsm ? (size_t)M.sym_ntab * sizeof(int2) + (size_t)(M.npat + 1) * sizeof(int32_t) : 0;
-        if (fx)
+        if (!fx && M.sym_fast_on && h->symd_fast && !tsm) {
+            int g27 = M.sym27_grid;
+            if (grid_cap) g27 = std::min(g27, grid_cap);
+            SymArgs sb = sa;
+            sb.chunk = 0;
+            TRY(launch_k(h, spmv_symd27_fn(epi), g27, VEC_SPMV_THREADS, 0, a, sb, M.sym_fast, (int)M.nrows));
+        } else if (fx)
             TRY(launch_k(h, spmv_symd_fixed_fn(epi, M.sym_fl, h->symd_minb, M.sym_blocked), g, VEC_SPMV_THREADS, 0, a, sa, (int)M.nrows));
         else
             TRY(launch_k(h, spmv_symd_fn(epi, h->symd_gminb, M.sym_blocked, tsm), g, VEC_SPMV_THREADS, tsm_bytes, a, sa,
@@ -1532,6 +1555,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "patterns") { h->patterns = value ? 1 : 0; return AMG_OK; }
     if (k == "symm") { h->symm = value ? 1 : 0; return AMG_OK; }
     if (k == "dict") { h->dict = value ? 1 : 0; return AMG_OK; }
+    if (k == "symd_fast") { h->symd_fast = value ? 1 : 0; return AMG_OK; }
     if (k == "dict_main") { h->dict_main = value ? 1 : 0; return AMG_OK; }
     if (k == "wcsr") { h->wcsr = value ? 1 : 0; return AMG_OK; }
     if (k == "overlap_test") { h->overlap_test = value ? 1 : 0; return AMG_OK; }
@@ -2062,6 +2086,46 @@ static int build_symd(amg_t *h, DevMat &M, const std::vector<int32_t> &off32, co
     M.lbytes[AMG_LAYOUT_SYMD] = (int64_t)uv.size() * 8 + n;  // stored diagonals + 1-byte pattern id per row
     M.nudiag = nu;
     int nb = 0;
+    M.sym_fast_on = false;
+    if (blk && K == 1 && n < INT32_MAX - 64) {
+        // the pattern most rows have; 27 entries -> interior fast path with parameter-bank offsets
+        std::vector<int64_t> cnt(npat, 0);
+        for (int64_t r = 0; r < n; ++r) ++cnt[ids[r]];
+        int mp = 0;
+        for (int p2 = 1; p2 < npat; ++p2)
+            if (cnt[p2] > cnt[mp]) mp = p2;
+        if (beg[mp + 1] - beg[mp] == 27) {
+            SymFast &F = M.sym_fast;
+            F.pat = mp;
+            const long long w32 = 32LL * nu;
+            for (int k = 0; k < 27; ++k) {
+                const int e = beg[mp] + k;
+                const long long d = rel[e];
+                const int j = ent[e].y & 63;
+                F.xoff[k] = d * 8;
+                if (d >= 0) {
+                    F.thr[k] = 0;
+                    F.voffA[k] = F.voffB[k] = 32LL * j * 8;
+                } else {
+                    const long long dd = -d, qA = -(dd / 32) - ((dd % 32) ? 0 : 0);
+                    // row i = 32 s + l reads the copy in row i - dd: lane l - dd (mod 32) of slice s + floor((l - dd) / 32)
+                    const long long t = dd % 32;
+                    const long long qa = -(dd / 32);          // lanes l >= t
+                    const long long qb = qa - 1;              // lanes l < t (t > 0)
+                    (void)qA;
+                    F.thr[k] = (int)t;
+                    F.voffA[k] = (qa * (w32 - 32) + 32LL * j - dd) * 8;
+                    F.voffB[k] = (qb * (w32 - 32) + 32LL * j - dd) * 8;
+                }
+            }
+            M.sym_fast_on = true;
+            int nb27 = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb27, (const void *)spmv_symd27_fn(EPI_RESID), VEC_SPMV_THREADS, 0));
+            M.sym27_grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
+                                                                       (int64_t)h->sm_count * std::max(nb27, 1)));
+            h->max_grid = std::max(h->max_grid, M.sym27_grid);
+        }
+    }
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)spmv_symd_fn(EPI_RESID, h->symd_gminb, blk), VEC_SPMV_THREADS, 0));
     M.sym_grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
                                                              (int64_t)h->sm_count * std::max(nb, 1)));

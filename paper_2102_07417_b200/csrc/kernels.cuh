@@ -1356,6 +1356,100 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, MINB) spmv_symd(const SpmvAr
     }
 }
 
+// Interior fast path for 27-entry rows (the 27-point operator of configs 2 / 5): when all 32
+// rows of a warp have the most frequent pattern, the pattern is not decoded from the
+// constant-memory table -- every column offset and every value offset (own diagonal, or the
+// mirror's slice-blocked position) is a kernel parameter, i.e. a constant-bank operand of the
+// address arithmetic, and the 27 products are folded by straight-line code in the reference
+// order (p0 + pairwise over p1..p26: 8 accumulators x 3 rounds, tree, 2-entry tail).  The
+// table-driven loop spends ~24 instructions per entry (ncu: 45% of the issue slots at 660
+// instructions per 32 rows); this path ~9.  A mirror entry a(i, i - d) sits in row i - d's
+// slice: with i = 32 s + l the offset from the row's own slot takes two values, split at
+// lane l = d mod 32 (voffA for lanes >= thr, voffB below).
+struct SymFast {
+    int pat;                 // pattern id of the interior rows (-1: no fast path)
+    int thr[27];
+    long long xoff[27];      // column offset in bytes
+    long long voffA[27], voffB[27];
+};
+
+#ifndef SYMD27_MINB
+#define SYMD27_MINB 4
+#endif
+template <int EPI>
+__global__ void __launch_bounds__(VEC_SPMV_THREADS, SYMD27_MINB) spmv_symd27(const SpmvArgs a, const SymArgs sa, const SymFast fa,
+                                                                    int nrows)
+{
+    __shared__ double red[VEC_SPMV_THREADS / 32];
+    pdl_launch();
+    pdl_wait();
+    if (!gate_open(a.gate1, a.gate2)) return;
+    const int nthreads = gridDim.x * VEC_SPMV_THREADS;
+    const int lane = threadIdx.x & 31;
+    const bool want_dot = a.dotw != nullptr;
+    const bool self_dot = a.dotw == a.y;
+    const double *__restrict__ x = a.x;
+    const double *__restrict__ uv = sa.uval;
+    const int bbase = sa.slot * SYMD_BEG_MAX;
+    double dacc = 0.0;
+    const int r0 = sa.chunk ? blockIdx.x * sa.chunk : blockIdx.x * VEC_SPMV_THREADS;
+    const int rend = sa.chunk ? min(nrows, r0 + sa.chunk) : nrows;
+    const int step = sa.chunk ? VEC_SPMV_THREADS : nthreads;
+    // warp-uniform trip count (the vote needs every lane); lanes beyond the last row idle
+    for (int row = r0 + threadIdx.x; row - lane < rend; row += step) {
+        const bool inr = row < rend;
+        const int pid = inr ? __ldg(sa.pid + row) : -1;
+        double bv = 0.0, wv = 0.0, sum = 0.0;
+        if (inr) {
+            if constexpr (EPI == EPI_RESID || EPI == EPI_AXPYW || EPI == EPI_ADD) bv = a.b[row];
+            if (want_dot && !self_dot) wv = a.dotw[row];
+        }
+        if (__all_sync(0xffffffffu, pid == fa.pat)) {
+            const char *xr = reinterpret_cast<const char *>(x + row);
+            const char *vr = reinterpret_cast<const char *>(uv + ((row >> 5) * sa.w32 + (row & 31)));
+            auto PV = [&](int k) -> double {
+                const long long vo = (lane >= fa.thr[k]) ? fa.voffA[k] : fa.voffB[k];
+                return prod(__ldg(reinterpret_cast<const double *>(vr + vo)),
+                            __ldg(reinterpret_cast<const double *>(xr + fa.xoff[k])));
+            };
+            const double p0 = PV(0);
+            double acc[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) acc[t] = PV(1 + t);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) acc[t] = add(acc[t], PV(9 + t));
+#pragma unroll
+            for (int t = 0; t < 8; ++t) acc[t] = add(acc[t], PV(17 + t));
+            double res = add(add(add(acc[0], acc[1]), add(acc[2], acc[3])), add(add(acc[4], acc[5]), add(acc[6], acc[7])));
+            res = add(res, PV(25));
+            res = add(res, PV(26));
+            sum = add(p0, res);
+        } else if (inr) {
+            const int rb = c_symd_beg[bbase + pid];
+            const int len = c_symd_beg[bbase + pid + 1] - rb;
+            auto P = [&](int k) -> double {
+                const int2 q = c_symd_tab[rb + k];
+                return prod(__ldg(uv + symd_vidx<true>(row, q.y, sa.w32)), __ldg(x + (row + q.x)));
+            };
+            sum = ref_row_sum<false>(P, len);
+        }
+        if (inr) {
+            double yv;
+            if constexpr (EPI == EPI_RESID) yv = __dsub_rn(bv, sum);
+            else if constexpr (EPI == EPI_AXPYW) yv = add(bv, __dmul_rn(a.omega, sum));
+            else if constexpr (EPI == EPI_ADD) yv = add(bv, sum);
+            else if constexpr (EPI == EPI_SETW) yv = __dmul_rn(a.omega, sum);
+            else yv = sum;
+            a.y[row] = yv;
+            if (want_dot) dacc = fma(yv, self_dot ? yv : wv, dacc);
+        }
+    }
+    if (want_dot || a.fin != FIN_NONE) {
+        double v = block_sum<VEC_SPMV_THREADS>(dacc, red);
+        grid_finalize<VEC_SPMV_THREADS>(v, a.partials, a.ticket, a.fin, a.ctl);
+    }
+}
+
 // Fixed-slot variant for matrices whose rows have at most FL entries (the
 // stencil operators: FL = 8 covers 7-point, FL = 32 the 27-point rows).  Every
 // lane walks the same FL statically unrolled slots, slot k live iff k < len:

@@ -117,7 +117,7 @@ def test_spmv_symmetric_diagonals_bit_identical(kind):
     m = _stencil(kind)
     x = np.random.default_rng(11).uniform(-1, 1, m.ncols)
     want = O.spmv(m, x)
-    variants = [{"symm": 0}, {"symm": 1, "symd_tsm": 1}] + [
+    variants = [{"symm": 0}, {"symm": 1, "symd_tsm": 1}, {"symm": 1, "symd_fast": 0}] + [
         {"symm": 1, "symd_fixed": f, "symd_chunked": c, "symd_blocked": b} for f in (0, 1, 2) for c in (0, 1) for b in (0, 1)]
     for opts in variants:
         opts["dict"] = 0  # constant-coefficient stencils would take the row-class dictionary
