@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "halo.h"
@@ -84,6 +85,10 @@ struct DevMat {
     int32_t *ucol_s = nullptr;
     uint8_t *ulen_s = nullptr;
     uint8_t *uperm_s = nullptr;  // PLEN layouts sorted inside each slice: slot -> row within the slice
+    uint8_t *ucls_s = nullptr;   // value-tuple class per slot (VD kernels), nullptr if unused
+    double *uvtab = nullptr;
+    int32_t *uvlen = nullptr;
+    int uncls = 0;
     int uW = 0, u_grid = 0, u_plen = 0;  // u_plen: padding slots skipped (short ragged rows)
     int nudiag = 0, sym_grid = 0, sym_fl = 0, symf_grid = 0, sym_blocked = 0;
     bool sym_fast_on = false;    // interior 27-entry pattern with parameter-bank offsets (spmv_symd27)
@@ -258,6 +263,7 @@ struct amg_handle {
     int rz_sep = 0;               // PCG: r.z in a separate dot kernel instead of the V-cycle's last SpMV
     int vec_minb = 4;             // padded-CSR kernel: min CTAs per SM (register budget) 4, 5 or 6
     int sellu_short = 1;          // ... and for rows of <= 8 entries at any padding, padding slots skipped
+    int sellu_vdict = 1;          // skipped-padding uniform SELL: value-tuple classes (<= 255) instead of stored values
     int sellu_sort = 1;           // skipped-padding uniform SELL: rows sorted by length inside each slice
     int sellu = 1;                // uniform-width SELL-32 for rows of <= 16 entries padding <= 10% (e.g. FSAI G)
     int symd_chunked = 0;         // symmetric kernels: contiguous row chunk per CTA (measured slower than grid-stride)
@@ -385,9 +391,11 @@ static SpmvSymFn spmv_symd_fixed_fn(int epi, int fl, int minb = 0, bool blk = fa
 
 typedef void (*SpmvSellUFn)(const SpmvArgs, const SellUArgs, int);
 
-static SpmvSellUFn spmv_sellu_fn(int epi, int W, bool plen = false)
+static SpmvSellUFn spmv_sellu_fn(int epi, int W, bool plen = false, bool vd = false)
 {
 #define AMG_U(E)                                                                                        \
+    if (plen && vd) return W <= 4 ? spmv_sellu<E, 4, true, true> : spmv_sellu<E, 8, true, true>;          \
+    if (!plen && vd && W <= 9) return W <= 4 ? spmv_sellu<E, 4, false, true> : spmv_sellu<E, 9, false, true>; \
     return plen ? (W <= 4 ? spmv_sellu<E, 4, true> : spmv_sellu<E, 8, true>)                             \
                 : (W <= 4 ? spmv_sellu<E, 4, false> : W <= 9 ? spmv_sellu<E, 9, false> : spmv_sellu<E, 16, false>);
     switch (epi) {
@@ -398,6 +406,17 @@ static SpmvSellUFn spmv_sellu_fn(int epi, int W, bool plen = false)
     default: AMG_U(EPI_ADD)
     }
 #undef AMG_U
+}
+
+// dynamic shared memory of the value-class uniform SELL kernels: table [ncls][FL] + lengths
+// slots per row of the spmv_sellu instantiation serving width W
+static int sellu_fl(int W, bool plen) { return plen ? (W <= 4 ? 4 : 8) : (W <= 4 ? 4 : W <= 9 ? 9 : 16); }
+
+static size_t sellu_vd_bytes(const DevMat &M)
+{
+    if (!M.ucls_s) return 0;
+    const int fl = sellu_fl(M.uW, M.u_plen != 0);
+    return (size_t)M.uncls * fl * sizeof(double) + (size_t)M.uncls * sizeof(int32_t);
 }
 
 typedef void (*SpmvWcsrFn)(const SpmvArgs, int);
@@ -725,9 +744,9 @@ static int spmv_range(amg_t *h, const DevMat &M, int lay, const SpmvArgs &a, int
         g = cap(M.s_grid, ((count + 31) / 32 + 7) / 8);
         TRY(launch_k(h, spmv_sells_fn(epi, h->sells_plen), g, VEC_SPMV_THREADS, 0, a, qa, count));
     } else if (lay == AMG_LAYOUT_SELL_UNIFORM) {
-        SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW, M.uperm_s};
+        SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW, M.uperm_s, M.ucls_s, M.uvtab, M.uvlen, M.uncls};
         g = cap(M.u_grid, (count + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS);
-        TRY(launch_k(h, spmv_sellu_fn(epi, M.uW, M.u_plen), g, VEC_SPMV_THREADS, 0, a, ua, count));
+        TRY(launch_k(h, spmv_sellu_fn(epi, M.uW, M.u_plen, M.ucls_s != nullptr), g, VEC_SPMV_THREADS, sellu_vd_bytes(M), a, ua, count));
     } else if (lay == AMG_LAYOUT_WCSR) {
         g = cap(M.wcsr_grid, ((count + 31) / 32 + WCSR_THREADS / 32 - 1) / (WCSR_THREADS / 32));
         TRY(launch_k(h, spmv_wcsr_fn(epi), g, WCSR_THREADS, 0, a, count));
@@ -871,8 +890,8 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         TRY(launch_k(h, spmv_sells_fn(epi, h->sells_plen), grid_cap ? std::min(grid_cap, M.s_grid) : M.s_grid, VEC_SPMV_THREADS, 0, a,
                      qa, (int)M.nrows));
     } else if (M.uval_s && h->sellu) {
-        SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW, M.uperm_s};
-        TRY(launch_k(h, spmv_sellu_fn(epi, M.uW, M.u_plen), grid_cap ? std::min(grid_cap, M.u_grid) : M.u_grid, VEC_SPMV_THREADS, 0,
+        SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW, M.uperm_s, M.ucls_s, M.uvtab, M.uvlen, M.uncls};
+        TRY(launch_k(h, spmv_sellu_fn(epi, M.uW, M.u_plen, M.ucls_s != nullptr), grid_cap ? std::min(grid_cap, M.u_grid) : M.u_grid, VEC_SPMV_THREADS, sellu_vd_bytes(M),
                      a, ua, (int)M.nrows));
     } else if (M.sbeg) {
         SellArgs sa{M.sbeg, M.sval, M.scol, M.slen, M.pid, M.prel, M.pbeg, M.npat, M.nrel, M.sperm};
@@ -1507,7 +1526,7 @@ void amg_destroy(amg_t *h)
     };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.uperm_s); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s); F(M.dcls); F(M.dbeg); F(M.drel); F(M.dval);
+            F(M.off); F(M.col); F(M.val); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.uperm_s); F(M.ucls_s); F(M.uvtab); F(M.uvlen); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s); F(M.dcls); F(M.dbeg); F(M.drel); F(M.dval);
             symd_slot_give(h->device, M.sym_slot);
             M.sym_slot = -1;
             symd_tab_give(h->device, M.sym_tab, M.sym_ntab);
@@ -1571,6 +1590,7 @@ int amg_set_option(amg_t *h, const char *key, int64_t value)
     if (k == "vec_minb") { h->vec_minb = (int)value; return AMG_OK; }
     if (k == "sellu_short") { h->sellu_short = value ? 1 : 0; return AMG_OK; }
     if (k == "sellu") { h->sellu = value ? 1 : 0; return AMG_OK; }
+    if (k == "sellu_vdict") { h->sellu_vdict = value ? 1 : 0; return AMG_OK; }
     if (k == "sellu_sort") { h->sellu_sort = value ? 1 : 0; return AMG_OK; }
     if (k == "symd_fixed") { h->symd_fixed = (int)value; return AMG_OK; }
     if (k == "symd_chunked") { h->symd_chunked = value ? 1 : 0; return AMG_OK; }
@@ -2528,19 +2548,55 @@ int amg_finalize(amg_t *h)
                         TRY(dalloc(&M.uperm_s, pm.size()));
                         CK(cudaMemcpy(M.uperm_s, pm.data(), pm.size(), cudaMemcpyHostToDevice));
                     }
+                    bool vd = false;
+                    if ((plen || W <= 9) && h->sellu_vdict) {
+                        // value-tuple classes: rows whose values (bit patterns, in order) coincide share a class
+                        const int fl = sellu_fl(W, plen);
+                        std::map<std::vector<uint64_t>, int> cmap;
+                        std::vector<uint8_t> cl(ns * 32 + 16, 0);
+                        std::vector<double> vt;
+                        std::vector<int32_t> vl;
+                        vd = true;
+                        std::vector<uint64_t> key;
+                        for (int64_t sl = 0; sl < ns && vd; ++sl)
+                            for (int l = 0; l < 32; ++l) {
+                                const int64_t r = sl * 32 + (sorted ? pm[sl * 32 + l] : l);
+                                const int32_t len = r < M.nrows ? off32[r + 1] - off32[r] : 0;
+                                key.assign((size_t)len, 0);
+                                for (int32_t k2 = 0; k2 < len; ++k2) memcpy(&key[k2], &val_h[off32[r] + k2], 8);
+                                auto it = cmap.find(key);
+                                if (it == cmap.end()) {
+                                    if (cmap.size() >= 255) { vd = false; break; }
+                                    it = cmap.emplace(key, (int)cmap.size()).first;
+                                    vl.push_back(len);
+                                    for (int k2 = 0; k2 < fl; ++k2) vt.push_back(k2 < len ? val_h[off32[r] + k2] : 0.0);
+                                }
+                                cl[sl * 32 + l] = (uint8_t)it->second;
+                            }
+                        if (vd) {
+                            M.uncls = (int)cmap.size();
+                            TRY(dalloc(&M.ucls_s, cl.size()));
+                            TRY(dalloc(&M.uvtab, vt.size()));
+                            TRY(dalloc(&M.uvlen, vl.size()));
+                            CK(cudaMemcpy(M.ucls_s, cl.data(), cl.size(), cudaMemcpyHostToDevice));
+                            CK(cudaMemcpy(M.uvtab, vt.data(), vt.size() * sizeof(double), cudaMemcpyHostToDevice));
+                            CK(cudaMemcpy(M.uvlen, vl.data(), vl.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                        }
+                    }
                     TRY(dalloc(&M.uval_s, tot));
                     TRY(dalloc(&M.ucol_s, tot));
                     TRY(dalloc(&M.ulen_s, ln.size()));
                     // padding slots are loaded unless skipped (plen)
-                    M.lbytes[AMG_LAYOUT_SELL_UNIFORM] = (plen ? M.nnz : (int64_t)tot) * 12 + (int64_t)M.nrows * (sorted ? 2 : 1);
+                    M.lbytes[AMG_LAYOUT_SELL_UNIFORM] = vd ? (plen ? M.nnz : (int64_t)tot) * 4 + (int64_t)M.nrows * (sorted ? 2 : 1)  // columns + class (+ perm)
+                                                          : (plen ? M.nnz : (int64_t)tot) * 12 + (int64_t)M.nrows * (sorted ? 2 : 1);
                     CK(cudaMemcpy(M.uval_s, sv.data(), tot * sizeof(double), cudaMemcpyHostToDevice));
                     CK(cudaMemcpy(M.ucol_s, sc.data(), tot * sizeof(int32_t), cudaMemcpyHostToDevice));
                     CK(cudaMemcpy(M.ulen_s, ln.data(), ln.size(), cudaMemcpyHostToDevice));
                     M.uW = W;
                     M.u_plen = plen ? 1 : 0;
                     int nbu = 0;
-                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbu, (const void *)spmv_sellu_fn(EPI_RESID, W, plen),
-                                                                     VEC_SPMV_THREADS, 0));
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbu, (const void *)spmv_sellu_fn(EPI_RESID, W, plen, vd),
+                                                                     VEC_SPMV_THREADS, sellu_vd_bytes(M)));
                     M.u_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
                                                                           (int64_t)h->sm_count * std::max(nbu, 1)));
                     h->max_grid = std::max(h->max_grid, M.u_grid);

@@ -1843,6 +1843,14 @@ struct SellUArgs {
     // operator has ~40% of its lanes live but touches ~87% of its sectors); the warp still works
     // on the same 32 neighbouring rows and the y store stays one 256-byte segment.  nullptr: slot = row.
     const uint8_t *perm;
+    // VD kernels: rows whose VALUE tuples fall into <= 255 classes (the interpolation of a
+    // constant-coefficient problem: config 4's P_0 holds 8 distinct weights in 30 M entries) store one
+    // class id per slot; the table {length, values} sits in shared memory, so a row streams its
+    // columns (4 B per entry) and one byte -- no values, no length.
+    const uint8_t *cls;
+    const double *vtab;   // [ncls][FL]
+    const int32_t *vlen;  // [ncls]
+    int ncls;
 };
 
 // Software-pipelined: the next row's columns and length are loaded one
@@ -1851,11 +1859,21 @@ struct SellUArgs {
 // gathers).
 // PLEN: slots at or beyond the row's length are not loaded (no bytes for padding): short ragged
 // rows (interpolation P, 1..8 entries) pad their slices freely.
-template <int EPI, int FL, bool PLEN>
+template <int EPI, int FL, bool PLEN, bool VD = false>
 __global__ void __launch_bounds__(VEC_SPMV_THREADS, FL <= 4 ? 6 : FL <= 9 ? 4 : 3) spmv_sellu(const SpmvArgs a,
                                                                                            const SellUArgs u, int nrows)
 {
     __shared__ double red[VEC_SPMV_THREADS / 32];
+    extern __shared__ double sellu_vd[];  // VD: value table [ncls][FL], then lengths [ncls]
+    const double *svt = sellu_vd;
+    const int32_t *svl = reinterpret_cast<const int32_t *>(sellu_vd + (VD ? u.ncls * FL : 0));
+    if constexpr (VD) {  // static data: staged before the PDL wait
+        double *wv_ = sellu_vd;
+        int32_t *wl_ = reinterpret_cast<int32_t *>(sellu_vd + u.ncls * FL);
+        for (int i = threadIdx.x; i < u.ncls * FL; i += blockDim.x) wv_[i] = u.vtab[i];
+        for (int i = threadIdx.x; i < u.ncls; i += blockDim.x) wl_[i] = u.vlen[i];
+        __syncthreads();
+    }
     pdl_launch();
     pdl_wait();
     if (!gate_open(a.gate1, a.gate2)) return;
@@ -1867,10 +1885,15 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, FL <= 4 ? 6 : FL <= 9 ? 4 : 
     double dacc = 0.0;
     int v = blockIdx.x * VEC_SPMV_THREADS + threadIdx.x;
     int c[FL];
-    int len = 0, nrowid = 0;
+    int len = 0, nrowid = 0, ncls_ = 0;
     auto fetch = [&](int r) {  // r: slot
         const int base = (r >> 5) * W32 + (r & 31);
-        len = __ldg(u.len + r);
+        if constexpr (VD) {
+            ncls_ = __ldg(u.cls + r);
+            len = svl[ncls_];
+        } else {
+            len = __ldg(u.len + r);
+        }
         nrowid = (PLEN && u.perm) ? ((r & ~31) | (int)__ldg(u.perm + r)) : r;
 #pragma unroll
         for (int k = 0; k < FL; ++k) c[k] = (k < (PLEN ? len : u.W)) ? __ldg(u.col + base + 32 * k) : 0;
@@ -1881,9 +1904,15 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, FL <= 4 ? 6 : FL <= 9 ? 4 : 
         const int row = nrowid;
         const int base = (slot >> 5) * W32 + (slot & 31);
         double p[FL];
+        if constexpr (VD) {
+            const double *tv = svt + ncls_ * FL;
 #pragma unroll
-        for (int k = 0; k < FL; ++k)
-            p[k] = (k < (PLEN ? len : u.W)) ? prod(__ldg(u.val + base + 32 * k), __ldg(x + c[k])) : 0.0;
+            for (int k = 0; k < FL; ++k) p[k] = (k < len) ? prod(tv[k], __ldg(x + c[k])) : 0.0;
+        } else {
+#pragma unroll
+            for (int k = 0; k < FL; ++k)
+                p[k] = (k < (PLEN ? len : u.W)) ? prod(__ldg(u.val + base + 32 * k), __ldg(x + c[k])) : 0.0;
+        }
         const int clen = len;
         if (v + nthreads < nrows) fetch(vrow(a, v + nthreads));
         double bv = 0.0, wv = 0.0;

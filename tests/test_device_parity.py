@@ -235,6 +235,33 @@ def test_spmv_uniform_sell_bit_identical(width):
         dh.close()
 
 
+@pytest.mark.parametrize("width", [4, 8])
+@pytest.mark.parametrize("vdict", [0, 1])
+def test_spmv_uniform_sell_value_classes_bit_identical(width, vdict):
+    # interpolation-like rows (0..width entries) whose VALUE tuples fall into few classes
+    # (config 4's P_0: 8 distinct weights): one class id per row + a table in shared memory
+    # instead of the value stream; must equal the stored-value kernel and the oracle bit for bit
+    from paper_2102_07417_b200.problems import Csr
+
+    rng = np.random.default_rng(width)
+    n = 50021
+    lens = rng.integers(0, width + 1, n)
+    lens[:3] = [0, 1, width]
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    weights = {1: [1.0], 2: [0.5, 0.5], 3: [0.25, 0.5, 0.25], 4: [0.25, 0.25, 0.25, 0.25]}
+    vals = np.concatenate([np.asarray(weights.get(int(l), [1.0 / l] * int(l)))[: int(l)] * (1 + (r % 3 == 0))
+                           if l else np.zeros(0) for r, l in enumerate(lens)])
+    m = Csr(n, n, off, cols, vals)
+    x = rng.uniform(-1, 1, n)
+    dh = amg.DeviceHierarchy.from_matrices([m], options={"symm": 0, "dict": 0, "sellu_vdict": vdict})
+    assert dh.layout(0, "a") == "sell_uniform"
+    st, _ = dh.matrix_bytes(0, "a")
+    assert (st < 6 * m.nnz + 4 * n) == bool(vdict)  # columns + class ids vs 12 B per entry
+    np.testing.assert_array_equal(dh.matrix(0, "a")(x), O.spmv(m, x))
+    dh.close()
+
+
 @pytest.mark.parametrize("maxlen", [12, 46, 129])
 def test_spmv_sorted_sell_bit_identical(maxlen):
     # ragged rows (FSAI-transpose-like length spread) on SELL-32 slices sorted
