@@ -85,6 +85,7 @@ struct DevMat {
     int32_t *ucol_s = nullptr;
     uint8_t *ulen_s = nullptr;
     uint8_t *uperm_s = nullptr;  // PLEN layouts sorted inside each slice: slot -> row within the slice
+    uint8_t *uvid_s = nullptr;   // value id per stored entry (VD == 2 kernels), nullptr if unused
     uint8_t *ucls_s = nullptr;   // value-tuple class per slot (VD kernels), nullptr if unused
     double *uvtab = nullptr;
     int32_t *uvlen = nullptr;
@@ -391,11 +392,13 @@ static SpmvSymFn spmv_symd_fixed_fn(int epi, int fl, int minb = 0, bool blk = fa
 
 typedef void (*SpmvSellUFn)(const SpmvArgs, const SellUArgs, int);
 
-static SpmvSellUFn spmv_sellu_fn(int epi, int W, bool plen = false, bool vd = false)
+static SpmvSellUFn spmv_sellu_fn(int epi, int W, bool plen = false, int vd = 0)
 {
 #define AMG_U(E)                                                                                        \
-    if (plen && vd) return W <= 4 ? spmv_sellu<E, 4, true, true> : spmv_sellu<E, 8, true, true>;          \
-    if (!plen && vd && W <= 9) return W <= 4 ? spmv_sellu<E, 4, false, true> : spmv_sellu<E, 9, false, true>; \
+    if (plen && vd == 1) return W <= 4 ? spmv_sellu<E, 4, true, 1> : spmv_sellu<E, 8, true, 1>;           \
+    if (!plen && vd == 1 && W <= 9) return W <= 4 ? spmv_sellu<E, 4, false, 1> : spmv_sellu<E, 9, false, 1>; \
+    if (plen && vd == 2) return W <= 4 ? spmv_sellu<E, 4, true, 2> : spmv_sellu<E, 8, true, 2>;           \
+    if (!plen && vd == 2 && W <= 9) return W <= 4 ? spmv_sellu<E, 4, false, 2> : spmv_sellu<E, 9, false, 2>; \
     return plen ? (W <= 4 ? spmv_sellu<E, 4, true> : spmv_sellu<E, 8, true>)                             \
                 : (W <= 4 ? spmv_sellu<E, 4, false> : W <= 9 ? spmv_sellu<E, 9, false> : spmv_sellu<E, 16, false>);
     switch (epi) {
@@ -412,8 +415,11 @@ static SpmvSellUFn spmv_sellu_fn(int epi, int W, bool plen = false, bool vd = fa
 // slots per row of the spmv_sellu instantiation serving width W
 static int sellu_fl(int W, bool plen) { return plen ? (W <= 4 ? 4 : 8) : (W <= 4 ? 4 : W <= 9 ? 9 : 16); }
 
+static int sellu_vd_mode(const DevMat &M) { return M.ucls_s ? 1 : M.uvid_s ? 2 : 0; }
+
 static size_t sellu_vd_bytes(const DevMat &M)
 {
+    if (M.uvid_s) return (size_t)M.uncls * sizeof(double);
     if (!M.ucls_s) return 0;
     const int fl = sellu_fl(M.uW, M.u_plen != 0);
     return (size_t)M.uncls * fl * sizeof(double) + (size_t)M.uncls * sizeof(int32_t);
@@ -744,9 +750,9 @@ static int spmv_range(amg_t *h, const DevMat &M, int lay, const SpmvArgs &a, int
         g = cap(M.s_grid, ((count + 31) / 32 + 7) / 8);
         TRY(launch_k(h, spmv_sells_fn(epi, h->sells_plen), g, VEC_SPMV_THREADS, 0, a, qa, count));
     } else if (lay == AMG_LAYOUT_SELL_UNIFORM) {
-        SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW, M.uperm_s, M.ucls_s, M.uvtab, M.uvlen, M.uncls};
+        SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW, M.uperm_s, M.ucls_s, M.uvtab, M.uvlen, M.uncls, M.uvid_s};
         g = cap(M.u_grid, (count + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS);
-        TRY(launch_k(h, spmv_sellu_fn(epi, M.uW, M.u_plen, M.ucls_s != nullptr), g, VEC_SPMV_THREADS, sellu_vd_bytes(M), a, ua, count));
+        TRY(launch_k(h, spmv_sellu_fn(epi, M.uW, M.u_plen, sellu_vd_mode(M)), g, VEC_SPMV_THREADS, sellu_vd_bytes(M), a, ua, count));
     } else if (lay == AMG_LAYOUT_WCSR) {
         g = cap(M.wcsr_grid, ((count + 31) / 32 + WCSR_THREADS / 32 - 1) / (WCSR_THREADS / 32));
         TRY(launch_k(h, spmv_wcsr_fn(epi), g, WCSR_THREADS, 0, a, count));
@@ -890,8 +896,8 @@ static int launch_spmv(amg_t *h, const DevMat &M, const double *x, double *y, in
         TRY(launch_k(h, spmv_sells_fn(epi, h->sells_plen), grid_cap ? std::min(grid_cap, M.s_grid) : M.s_grid, VEC_SPMV_THREADS, 0, a,
                      qa, (int)M.nrows));
     } else if (M.uval_s && h->sellu) {
-        SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW, M.uperm_s, M.ucls_s, M.uvtab, M.uvlen, M.uncls};
-        TRY(launch_k(h, spmv_sellu_fn(epi, M.uW, M.u_plen, M.ucls_s != nullptr), grid_cap ? std::min(grid_cap, M.u_grid) : M.u_grid, VEC_SPMV_THREADS, sellu_vd_bytes(M),
+        SellUArgs ua{M.uval_s, M.ucol_s, M.ulen_s, M.uW, M.uperm_s, M.ucls_s, M.uvtab, M.uvlen, M.uncls, M.uvid_s};
+        TRY(launch_k(h, spmv_sellu_fn(epi, M.uW, M.u_plen, sellu_vd_mode(M)), grid_cap ? std::min(grid_cap, M.u_grid) : M.u_grid, VEC_SPMV_THREADS, sellu_vd_bytes(M),
                      a, ua, (int)M.nrows));
     } else if (M.sbeg) {
         SellArgs sa{M.sbeg, M.sval, M.scol, M.slen, M.pid, M.prel, M.pbeg, M.npat, M.nrel, M.sperm};
@@ -1526,7 +1532,7 @@ void amg_destroy(amg_t *h)
     };
     for (auto &L : h->lv) {
         for (auto &M : L.m) {
-            F(M.off); F(M.col); F(M.val); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.uperm_s); F(M.ucls_s); F(M.uvtab); F(M.uvlen); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s); F(M.dcls); F(M.dbeg); F(M.drel); F(M.dval);
+            F(M.off); F(M.col); F(M.val); F(M.pstart); F(M.pval); F(M.pcol); F(M.pid); F(M.prel); F(M.pbeg); F(M.sbeg); F(M.sval); F(M.scol); F(M.slen); F(M.sperm); F(M.leaf); F(M.row_leaf); F(M.lsum); F(M.uval); F(M.uval_s); F(M.ucol_s); F(M.ulen_s); F(M.uperm_s); F(M.ucls_s); F(M.uvtab); F(M.uvlen); F(M.uvid_s); F(M.sv_s); F(M.sc_s); F(M.sb_s); F(M.sp_s); F(M.sw_s); F(M.sl_s); F(M.dcls); F(M.dbeg); F(M.drel); F(M.dval);
             symd_slot_give(h->device, M.sym_slot);
             M.sym_slot = -1;
             symd_tab_give(h->device, M.sym_tab, M.sym_ntab);
@@ -2548,7 +2554,7 @@ int amg_finalize(amg_t *h)
                         TRY(dalloc(&M.uperm_s, pm.size()));
                         CK(cudaMemcpy(M.uperm_s, pm.data(), pm.size(), cudaMemcpyHostToDevice));
                     }
-                    bool vd = false;
+                    bool vd = false, vd2 = false;
                     if ((plen || W <= 9) && h->sellu_vdict) {
                         // value-tuple classes: rows whose values (bit patterns, in order) coincide share a class
                         const int fl = sellu_fl(W, plen);
@@ -2573,6 +2579,32 @@ int amg_finalize(amg_t *h)
                                 }
                                 cl[sl * 32 + l] = (uint8_t)it->second;
                             }
+                        if (!vd) {
+                            // too many tuples: <= 256 distinct values -> one value id per stored entry
+                            std::map<uint64_t, int> vmap;
+                            std::vector<double> tab;
+                            std::vector<uint8_t> vi(tot + 16, 0);
+                            bool ok = true;
+                            for (size_t q2 = 0; q2 < tot && ok; ++q2) {
+                                uint64_t bits;
+                                memcpy(&bits, &sv[q2], 8);
+                                auto it = vmap.find(bits);
+                                if (it == vmap.end()) {
+                                    if (vmap.size() >= 256) { ok = false; break; }
+                                    it = vmap.emplace(bits, (int)vmap.size()).first;
+                                    tab.push_back(sv[q2]);
+                                }
+                                vi[q2] = (uint8_t)it->second;
+                            }
+                            if (ok) {
+                                vd2 = true;
+                                M.uncls = (int)tab.size();
+                                TRY(dalloc(&M.uvid_s, vi.size()));
+                                TRY(dalloc(&M.uvtab, tab.size()));
+                                CK(cudaMemcpy(M.uvid_s, vi.data(), vi.size(), cudaMemcpyHostToDevice));
+                                CK(cudaMemcpy(M.uvtab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+                            }
+                        }
                         if (vd) {
                             M.uncls = (int)cmap.size();
                             TRY(dalloc(&M.ucls_s, cl.size()));
@@ -2587,7 +2619,8 @@ int amg_finalize(amg_t *h)
                     TRY(dalloc(&M.ucol_s, tot));
                     TRY(dalloc(&M.ulen_s, ln.size()));
                     // padding slots are loaded unless skipped (plen)
-                    M.lbytes[AMG_LAYOUT_SELL_UNIFORM] = vd ? (plen ? M.nnz : (int64_t)tot) * 4 + (int64_t)M.nrows * (sorted ? 2 : 1)  // columns + class (+ perm)
+                    M.lbytes[AMG_LAYOUT_SELL_UNIFORM] = vd2 ? (plen ? M.nnz : (int64_t)tot) * 5 + (int64_t)M.nrows * (sorted ? 2 : 1)  // columns + value ids + length (+ perm)
+                                                          : vd ? (plen ? M.nnz : (int64_t)tot) * 4 + (int64_t)M.nrows * (sorted ? 2 : 1)  // columns + class (+ perm)
                                                           : (plen ? M.nnz : (int64_t)tot) * 12 + (int64_t)M.nrows * (sorted ? 2 : 1);
                     CK(cudaMemcpy(M.uval_s, sv.data(), tot * sizeof(double), cudaMemcpyHostToDevice));
                     CK(cudaMemcpy(M.ucol_s, sc.data(), tot * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -2595,7 +2628,7 @@ int amg_finalize(amg_t *h)
                     M.uW = W;
                     M.u_plen = plen ? 1 : 0;
                     int nbu = 0;
-                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbu, (const void *)spmv_sellu_fn(EPI_RESID, W, plen, vd),
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbu, (const void *)spmv_sellu_fn(EPI_RESID, W, plen, vd ? 1 : vd2 ? 2 : 0),
                                                                      VEC_SPMV_THREADS, sellu_vd_bytes(M)));
                     M.u_grid = (int)std::max<int64_t>(1, std::min<int64_t>((M.nrows + VEC_SPMV_THREADS - 1) / VEC_SPMV_THREADS,
                                                                           (int64_t)h->sm_count * std::max(nbu, 1)));

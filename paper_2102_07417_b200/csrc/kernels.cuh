@@ -1851,6 +1851,10 @@ struct SellUArgs {
     const double *vtab;   // [ncls][FL]
     const int32_t *vlen;  // [ncls]
     int ncls;
+    // VD == 2: too many value TUPLES but <= 256 distinct VALUES (config 4's P^T_0: 5-entry rows of
+    // the same 8 weights): one value id per stored entry (1 B instead of 8, same slot layout as col),
+    // the value table (vtab[0 .. ncls)) in shared memory; lengths come from `len` as usual.
+    const uint8_t *vid;
 };
 
 // Software-pipelined: the next row's columns and length are loaded one
@@ -1859,19 +1863,24 @@ struct SellUArgs {
 // gathers).
 // PLEN: slots at or beyond the row's length are not loaded (no bytes for padding): short ragged
 // rows (interpolation P, 1..8 entries) pad their slices freely.
-template <int EPI, int FL, bool PLEN, bool VD = false>
+template <int EPI, int FL, bool PLEN, int VD = 0>
 __global__ void __launch_bounds__(VEC_SPMV_THREADS, FL <= 4 ? 6 : FL <= 9 ? 4 : 3) spmv_sellu(const SpmvArgs a,
                                                                                            const SellUArgs u, int nrows)
 {
     __shared__ double red[VEC_SPMV_THREADS / 32];
     extern __shared__ double sellu_vd[];  // VD: value table [ncls][FL], then lengths [ncls]
     const double *svt = sellu_vd;
-    const int32_t *svl = reinterpret_cast<const int32_t *>(sellu_vd + (VD ? u.ncls * FL : 0));
-    if constexpr (VD) {  // static data: staged before the PDL wait
+    const int32_t *svl = reinterpret_cast<const int32_t *>(sellu_vd + (VD == 1 ? u.ncls * FL : 0));
+    if constexpr (VD == 1) {  // static data: staged before the PDL wait
         double *wv_ = sellu_vd;
         int32_t *wl_ = reinterpret_cast<int32_t *>(sellu_vd + u.ncls * FL);
         for (int i = threadIdx.x; i < u.ncls * FL; i += blockDim.x) wv_[i] = u.vtab[i];
         for (int i = threadIdx.x; i < u.ncls; i += blockDim.x) wl_[i] = u.vlen[i];
+        __syncthreads();
+    }
+    if constexpr (VD == 2) {
+        double *wv_ = sellu_vd;
+        for (int i = threadIdx.x; i < u.ncls; i += blockDim.x) wv_[i] = u.vtab[i];
         __syncthreads();
     }
     pdl_launch();
@@ -1888,7 +1897,7 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, FL <= 4 ? 6 : FL <= 9 ? 4 : 
     int len = 0, nrowid = 0, ncls_ = 0;
     auto fetch = [&](int r) {  // r: slot
         const int base = (r >> 5) * W32 + (r & 31);
-        if constexpr (VD) {
+        if constexpr (VD == 1) {
             ncls_ = __ldg(u.cls + r);
             len = svl[ncls_];
         } else {
@@ -1904,10 +1913,16 @@ __global__ void __launch_bounds__(VEC_SPMV_THREADS, FL <= 4 ? 6 : FL <= 9 ? 4 : 
         const int row = nrowid;
         const int base = (slot >> 5) * W32 + (slot & 31);
         double p[FL];
-        if constexpr (VD) {
+        if constexpr (VD == 1) {
             const double *tv = svt + ncls_ * FL;
 #pragma unroll
             for (int k = 0; k < FL; ++k) p[k] = (k < len) ? prod(tv[k], __ldg(x + c[k])) : 0.0;
+        } else if constexpr (VD == 2) {
+            int vi[FL];
+#pragma unroll
+            for (int k = 0; k < FL; ++k) vi[k] = (k < (PLEN ? len : u.W)) ? (int)__ldg(u.vid + base + 32 * k) : 0;
+#pragma unroll
+            for (int k = 0; k < FL; ++k) p[k] = (k < (PLEN ? len : u.W)) ? prod(svt[vi[k]], __ldg(x + c[k])) : 0.0;
         } else {
 #pragma unroll
             for (int k = 0; k < FL; ++k)

@@ -237,6 +237,30 @@ def test_spmv_uniform_sell_bit_identical(width):
 
 @pytest.mark.parametrize("width", [4, 8])
 @pytest.mark.parametrize("vdict", [0, 1])
+@pytest.mark.parametrize("ragged", [0, 1])
+def test_spmv_uniform_sell_value_ids_bit_identical(width, vdict, ragged):
+    # thousands of value TUPLES but six distinct VALUES: one value id per stored entry (1 B for
+    # 8) and the value table in shared memory; ragged = 0: every row full (no skipped padding)
+    from paper_2102_07417_b200.problems import Csr
+
+    rng = np.random.default_rng(100 + width)
+    n = 50021
+    lens = rng.integers(0, width + 1, n) if ragged else np.full(n, width)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    vals = rng.choice(np.array([0.125, 0.25, 0.5, 1.0, 2.0, -0.5]), int(off[-1]))
+    m = Csr(n, n, off, cols, vals)
+    x = rng.uniform(-1, 1, n)
+    dh = amg.DeviceHierarchy.from_matrices([m], options={"symm": 0, "dict": 0, "sellu_vdict": vdict})
+    assert dh.layout(0, "a") == "sell_uniform"
+    st, _ = dh.matrix_bytes(0, "a")
+    assert (st < 7 * m.nnz + 4 * n) == bool(vdict)  # columns + value ids vs 12 B per entry
+    np.testing.assert_array_equal(dh.matrix(0, "a")(x), O.spmv(m, x))
+    dh.close()
+
+
+@pytest.mark.parametrize("width", [4, 8])
+@pytest.mark.parametrize("vdict", [0, 1])
 def test_spmv_uniform_sell_value_classes_bit_identical(width, vdict):
     # interpolation-like rows (0..width entries) whose VALUE tuples fall into few classes
     # (config 4's P_0: 8 distinct weights): one class id per row + a table in shared memory
